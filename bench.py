@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — FCFS hot-path throughput on B200 (BASELINE.json metric: Fourier coeff.vertex
+terms/sec, Gterm/s, and % of tensor peak, 1/2/4/8 B200).
+
+One STEP = one pass of the whole hot path over one batch:
+  a1 fcfs_vertices_from_rects (rects -> signed corners + area)  then
+  a2-a5 fcfs_coeffs_batched   (twiddles + contraction + axes/DC + pupil epilogue).
+Default workload = BASELINE.json configs[2] ("c3"): 4096 clips per GPU, T = 2048, ~1200
+lines/clip, ~4.8k corners/clip, pupil radius 27.22 (2337 coefficients/clip), split-TF32.
+Multi-GPU (torchrun): clips are sharded — every rank runs its own 4096 clips (weak
+scaling, no data-path collective); time = max over ranks (all_reduce MAX).
+
+terms = sum over clips of W_out x K_clip.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1010_5562_b200 import inputs  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3"])
+    ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
+            "fallback"
+
+
+def workload(cfg, seed, rank, clips):
+    if cfg == "c3":
+        # weak scaling: each rank its own clip range (seed streams (seed, clip) with clip offset by rank)
+        T = 2048
+        rects = np.concatenate([inputs.c3_clip(seed, rank * clips + b, T) for b in range(clips)])
+        cp = np.arange(0, clips + 1, dtype=np.int64) * 1200
+        r2 = inputs.pupil_r2(T)
+        M = int(math.floor(math.sqrt(r2)))
+        return inputs.Workload("c3", T, M, M, r2, rects, None, cp, ("tf32x3",))
+    return inputs.make(cfg, seed=seed + rank)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_baseline(wl, target_s, prec):
+    """The oracle as it stands (extraction + direct sums), timed on a bounded sample of clips."""
+    import oracle
+    cores = oracle.max_threads()
+    ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    terms = 0
+    t0 = time.perf_counter()
+    b = 0
+    nclips = 0
+    while True:
+        r0, r1 = wl.clip_rect_range(b % wl.B)
+        sub = wl.rects[r0:r1]
+        gp = None
+        if wl.group_ptr is not None:
+            g0, g1 = (wl.clip_ptr[b], wl.clip_ptr[b + 1]) if wl.clip_ptr is not None else (0, len(wl.group_ptr) - 1)
+            gp = wl.group_ptr[g0:g1 + 1] - wl.group_ptr[g0]
+        e = oracle.extract(sub, wl.T, gp)
+        if wl.B == 1 and wl.R > 20000:
+            # one huge clip: sample the output set instead of the clips
+            rng = np.random.default_rng(0)
+            pick = rng.choice(len(ms), size=min(len(ms), 64), replace=False)
+            oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms[pick], ns[pick])
+            terms += len(pick) * e["K"]
+            nclips += 1
+            sample = f"1 clip, extraction + {len(pick)} of {len(ms)} coefficients (K={e['K']})"
+            break
+        oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
+        terms += len(ms) * e["K"]
+        nclips += 1
+        b += 1
+        sample = f"{nclips} clips (extraction + all {len(ms)} coefficients each)"
+        if time.perf_counter() - t0 > target_s or nclips >= wl.B:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": terms / dt / 1e9, "unit": "Gterm/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the same workload."""
+    if rank != 0:
+        return
+    wl = workload(args.config, args.seed, 0, args.clips)
+    prec = args.prec or ("tf32x3" if args.config == "c3" else "fp64")
+    per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(wl, per_step / 4, prec)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(wl, per_step, prec)
+        vals.append(last["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": "fourier_coeff_vertex_terms_per_sec", "value": v, "unit": "Gterm/s",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f80 (x87 long double)", "data": "synthetic",
+            "config": config_dict(args, wl, prec, world),
+            "cpu_baseline": {"value": v, "unit": "Gterm/s", "cores": last["cores"], "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": v, "unit": "Gterm/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, wl, prec, world):
+    W = inputs.window_count(wl.M, wl.N, wl.r2)
+    d = {"workload": f"{wl.name}: T={wl.T}, {wl.B} clip(s)/GPU, R={wl.R} rects/GPU, window |m|,|n|<={wl.M}"
+                     + (f" pupil r2={wl.r2:.2f}" if wl.r2 >= 0 else "") + f", W_out={W}/clip",
+         "T": wl.T, "clips_per_gpu": wl.B, "rects_per_gpu": wl.R, "M": wl.M, "N": wl.N, "W_out": W,
+         "precision": prec, "parallelism": f"clip-sharded x{world}" if wl.B > 1 else f"replicas x{world}",
+         "l2": "flushed between steps (512 MiB write, outside the timed events)"}
+    return d
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1010_5562_b200 import fcfs
+
+    fcfs.device_check()
+    prec = args.prec or ("tf32x3" if args.config == "c3" else "fp64")
+    wl = workload(args.config, args.seed, rank, args.clips)
+    layout = "pupil" if wl.r2 >= 0 else "dense"
+    W = inputs.window_count(wl.M, wl.N, wl.r2)
+
+    # inputs resident in HBM (value) and pinned host copies (e2e)
+    rects_h = torch.from_numpy(wl.rects).pin_memory()
+    rects = rects_h.to(dev)
+    gp = None if wl.group_ptr is None else torch.from_numpy(wl.group_ptr).to(dev)
+    cp = None if wl.clip_ptr is None else torch.from_numpy(wl.clip_ptr).to(dev)
+    mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
+    G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
+    vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=gp is not None, device=dev)
+    K = vp.run(rects, gp, cp)
+    cptr_h = vp.corner_ptr.cpu().numpy()
+    kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
+    if wl.B > 1:
+        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
+
+        def coeffs():
+            return plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area)
+        out_bytes = plan.out.numel() * plan.out.element_size()
+    else:
+        plan = fcfs.CoeffsPlan(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
+        area_h = int(vp.area[0].item())
+
+        def coeffs():
+            return plan.run(vp.x[:K], vp.y[:K], vp.w[:K], area_h)
+        out_bytes = plan.out.numel() * plan.out.element_size()
+    terms = float(W) * float(K)                     # per rank per step
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        vp.run(rects, gp, cp)
+        return coeffs()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-timed: events per step, L2 flushed between steps)
+    fcfs.profile_enable(True)
+    fcfs.profile_read()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = fcfs.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+            flush.fill_(i & 0xff)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = fcfs.kernel_launches() - launches0
+    stages = fcfs.profile_read()
+    fcfs.profile_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = terms * world * args.steps / (total_ms / 1e3) / 1e9
+
+    # ---------------- roofline of the dominant kernel (the a3 contraction)
+    peaks, src = load_peaks()
+    c_ms, c_n = stages["contract"]
+    c_ms_launch = c_ms / max(c_n, 1)
+    Kc = np.diff(cptr_h).astype(np.float64)
+    alg_flops = float(np.sum(8.0 * wl.M * wl.N * Kc))      # real quadrant GEMM 2M x 2N x K, 2 flop/MAC
+    achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
+    clocks = clk.summary()
+    if prec == "tf32x3":
+        tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+        peak = tf32 / 3.0
+        peak_note = (f"TF32 dense = {src} bf16 {peaks['bf16_tflops']} x (1.1/2.25 nominal ratio) = {tf32:.1f} "
+                     f"TF/s, / 3 (split-TF32: 3 TF32 MMAs per FP32-accurate product)")
+        bound = "tensor"
+    else:
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
+        peak_note = f"FP64 DFMA: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived, B200 FP64 = 1/2 FP32 rate)"
+        bound = "alu"
+    roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "kernel": "k_gemm_" + prec,
+            "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
+            "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()}}
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        out_h = torch.empty(plan.out.numel(), dtype=plan.out.dtype).pin_memory()
+        e2e_steps = max(2, min(args.steps, 5))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(e2e_steps):
+            rects.copy_(rects_h, non_blocking=True)
+            vp.run(rects, gp, cp)
+            o = coeffs()
+            out_h.copy_(o.reshape(-1), non_blocking=True)
+        eb.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([ea.elapsed_time(eb)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": terms * world * e2e_steps / (float(te.item()) / 1e3) / 1e9, "unit": "Gterm/s",
+               "h2d_bytes_per_step": int(rects_h.numel() * 4), "d2h_bytes_per_step": int(out_bytes)}
+
+    if rank == 0:
+        line = {"metric": "fourier_coeff_vertex_terms_per_sec", "value": round(value, 3), "unit": "Gterm/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "tf32x3 (split-TF32, FP32-accurate; FP64 flush)" if prec == "tf32x3" else "f64",
+                "data": "synthetic", "config": config_dict(args, wl, prec, world),
+                "K_per_gpu": int(K), "terms_per_step_per_gpu": terms,
+                "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
+                "e2e": e2e}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds, prec)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

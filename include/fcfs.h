@@ -1,0 +1,164 @@
+/*
+ * fcfs.h — C-ABI of libfcfs.so: the B200 (sm_100a) hot path of the fast continuous
+ * Fourier series (FCFS) of rectilinear polygons, arXiv 1010.5562.
+ *
+ * Citations are PAPER.md line numbers ("P:n") with the section / equation they fall in.
+ *
+ * Problem (readings A1-A7).  A clip of period T holds the mask
+ *     f(x,y) = sum over polygon groups g of 1[ union of the rects of g ]      (P:589-595 Eq. signal_model)
+ * and the library returns its continuous-Fourier-series coefficients
+ *     F[m,n] = (1/T^2) * integral_[0,T)^2 f(x,y) e^{-2 pi i (m x + n y)/T} dx dy
+ * (the paper's orthonormal F^_{k,l} equals T*F[k,l]), from the signed corner list of f:
+ *     F[0,0] = area/T^2                                  Eq. Fdc P:831-834 (Step 1)
+ *     F[m,0] = i/(2 pi m T) sum_k w_k y_k E_x[m,k]        Eq. Fk0 P:835-838 (Step 2)
+ *     F[0,n] = i/(2 pi n T) sum_k w_k x_k E_y[n,k]        Eq. F0l P:839-842 (Step 3)
+ *     F[m,n] = -1/(4 pi^2 m n) sum_k w_k E_x[m,k] E_y[n,k] Eq. Fkl P:843-846 (Step 4)
+ * with E_x[m,k] = e^{-2 pi i ((m x_k) mod T)/T}; phases are reduced exactly in integers
+ * because the vertices lie on the integer lattice.  The contraction is the
+ * paper's "Goertzel-like" direct evaluation restricted to a low-pass window
+ * or pupil disk (future work P:1247-1255), run in parallel (future work P:1257-1259).
+ *
+ * Conventions for every entry point:
+ *  - All array pointers are DEVICE pointers owned by the caller unless the name ends in
+ *    _host or the argument is a struct pointer (fcfs_window, fcfs_shard: host structs).
+ *    The library never allocates or frees device memory; scratch comes from `ws`,
+ *    sized by the matching *_workspace_bytes query.  `ws` must be 256-byte aligned.
+ *  - `stream` is a cudaStream_t (0 = legacy default stream).  All device work is
+ *    enqueued on it; outputs are valid once that stream's work completes.
+ *  - Return value: FCFS_OK or an error code; no exception crosses the ABI.  A
+ *    human-readable detail for the last error of the calling thread is available from
+ *    fcfs_last_error().  On error nothing useful has been written to the outputs.
+ *  - Coordinates: rects are half-open [x0,x1) x [y0,y1) with
+ *    0 <= x0 < x1 <= T, 0 <= y0 < y1 <= T, T in [1, 2^20].  Corners with x = T or
+ *    y = T are kept with their raw coordinate (reading A7): only phases wrap mod T.
+ */
+#ifndef FCFS_H_
+#define FCFS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t fcfs_status;
+#define FCFS_OK 0
+#define FCFS_E_INVALID 1     /* null pointer, T out of range, M or N < 0, bad enum, bad CSR   */
+#define FCFS_E_RANGE 2       /* a rect outside [0,T]^2 or with x0 >= x1 / y0 >= y1 (device-checked) */
+#define FCFS_E_CAPACITY 3    /* more corners than `cap`; *K_total_host still holds the count   */
+#define FCFS_E_WORKSPACE 4   /* ws too small (or unaligned) for this call                       */
+#define FCFS_E_UNSUPPORTED 5 /* device is not sm_100, or a size limit of this build is exceeded */
+#define FCFS_E_CUDA 6        /* a CUDA runtime error (detail in fcfs_last_error())              */
+
+/* Arithmetic of the contraction (BASELINE.json north_star (3)). */
+typedef int32_t fcfs_precision;
+#define FCFS_FP64 0    /* FP64 throughout; output complex128 (double re, double im); |err| <= 1e-12 B */
+#define FCFS_TF32X3 1  /* split-TF32 tcgen05 tensor-core contraction, FP64 flush of FP32 TMEM partials;
+                          output complex64 (float re, float im); |err| <= 1e-5 B                      */
+
+/* Output layout. */
+#define FCFS_LAYOUT_DENSE 0  /* (2M+1) x (2N+1) row-major, entry (m,n) at (m+M)*(2N+1) + (n+N);
+                                if pupil_r2 >= 0, entries with m^2+n^2 > pupil_r2 are written as 0 */
+#define FCFS_LAYOUT_PUPIL 1  /* packed: only |m|<=M, |n|<=N, m^2+n^2 <= pupil_r2, m-major then n
+                                (fcfs_pupil_indices gives the order); requires pupil_r2 >= 0    */
+
+/* Frequency window (reading A3: signed window, alpha at the signed index) and pupil disk
+ * (BASELINE.json cut-off NA(1+sigma)/lambda, inclusive, reading A11). */
+typedef struct {
+    int32_t M;          /* |m| <= M */
+    int32_t N;          /* |n| <= N */
+    double pupil_r2;    /* < 0: rectangular window; else keep m^2+n^2 <= pupil_r2 */
+    int32_t layout;     /* FCFS_LAYOUT_DENSE or FCFS_LAYOUT_PUPIL */
+} fcfs_window;
+
+/* Work partition of one clip (BASELINE.json north_star (6); linearity Prop. 2). */
+#define FCFS_SHARD_NONE 0
+#define FCFS_SHARD_ROWS 1          /* rows m in [m_lo, m_hi] (signed, inside [-M, M]) of the DENSE
+                                      layout; F holds (m_hi-m_lo+1)*(2N+1) entries                    */
+#define FCFS_SHARD_VERTEX_BLOCK 2  /* corners [k_lo, k_hi) only: F = that block's partial window
+                                      (full DENSE/PUPIL layout).  Its DC is (sum w x y over the block)/T^2,
+                                      so the sum of the P blocks' F equals the unsharded F (`area` unused) */
+typedef struct {
+    int32_t kind;
+    int32_t m_lo, m_hi;
+    int64_t k_lo, k_hi;
+} fcfs_shard;
+
+/* ------------------------------------------------------------------------------------------
+ * a1 — vertex extraction (Alg. 2 lines 1-14; Prop. 1; Step 1 P:866-868).
+ *
+ * rects      int32 [R][4] (x0, y0, x1, y1), device.
+ * group_ptr  int64 [G+1] CSR over rects, device; NULL => every rect is its own group (G == R).
+ *            Within a group the rects are UNIONED; groups are SUMMED (reading A5).
+ * clip_ptr   int64 [B+1] CSR over groups, device; NULL => one clip (B == 1).
+ * x, y, w    int32 [cap] out: canonical signed corners w(x,y) = f(x,y)-f(x-1,y)-f(x,y-1)+f(x-1,y-1)
+ *            of every clip, zero weights dropped, sorted by (clip, y, x).  Bit-exact.
+ * corner_ptr int64 [B+1] out: CSR of corners per clip.
+ * area       int64 [B] out: sum_k w_k x_k y_k = area of f per clip (exact).
+ * K_total_host  out (host): total corner count.  This call synchronises `stream` once.
+ * max_group  the largest number of rects in one group (host-known; sizes the workspace).
+ * Limits: T <= 2^20, B < 2^22, groups of at most 100 rects (else FCFS_E_UNSUPPORTED).
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_vertices_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_group);
+fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int64_t *group_ptr,
+                                     int64_t G, const int64_t *clip_ptr, int64_t B, int32_t T,
+                                     int64_t max_group, int32_t *x, int32_t *y, int32_t *w,
+                                     int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                     int64_t *K_total_host, void *ws, size_t ws_bytes,
+                                     void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * a2-a5 — coefficients of ONE clip: phase reduction + twiddles (a2), the separable
+ * contraction P = A diag(w) B^T over cos/sin quadrant rows (a3), axes + DC (a4) and the
+ * window / pupil epilogue with exact conj mirroring F[-m,-n] = conj F[m,n] (a5).
+ *
+ * x, y, w  int32 [K] corners (device) as produced by fcfs_vertices_from_rects (any order
+ *          is accepted; results are order-independent up to rounding).
+ * area     sum_k w_k x_k y_k (host value), used for F[0,0] = area/T^2.
+ * win      host struct, see fcfs_window.   prec  FCFS_FP64 or FCFS_TF32X3.
+ * shard    host struct or NULL (= FCFS_SHARD_NONE).
+ * F        out (device): complex128 (FP64) or complex64 (TF32X3) in the window layout.
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
+                                   fcfs_precision prec, const fcfs_shard *shard);
+fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K,
+                        int64_t area, int32_t T, const fcfs_window *win, fcfs_precision prec,
+                        const fcfs_shard *shard, void *F, void *ws, size_t ws_bytes,
+                        void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * a3-a5 batched — B independent clips (the paper's tiles) in one launch sequence.
+ * corner_ptr int64 [B+1] (device) CSR into x, y, w; area int64 [B] (device).
+ * K_total = corner_ptr[B] and K_max = max_b (corner_ptr[b+1]-corner_ptr[b]) are passed from
+ * the host (fcfs_vertices_from_rects returns K_total; K_max sizes the per-clip plan).
+ * F out: B consecutive output blocks of fcfs_window_size(win) entries each.
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T,
+                                    const fcfs_window *win, fcfs_precision prec);
+fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total,
+                                int64_t K_max, const int32_t *x, const int32_t *y,
+                                const int32_t *w, const int64_t *area, int32_t T,
+                                const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
+                                size_t ws_bytes, void *stream);
+
+/* Host helpers. */
+int64_t fcfs_window_size(const fcfs_window *win);        /* outputs per clip; -1 if invalid */
+int64_t fcfs_pupil_indices(int32_t M, int32_t N, double r2, int32_t *m_out_host,
+                           int32_t *n_out_host, int64_t cap); /* packed order; returns count */
+const char *fcfs_status_string(fcfs_status s);
+const char *fcfs_last_error(void);                        /* thread-local detail string */
+fcfs_status fcfs_device_check(void);                      /* FCFS_OK iff current device is sm_100 */
+int32_t fcfs_kernel_launches(void);                       /* kernels launched by this thread so far */
+
+/* Stage timing for the bench (CUDA events recorded on the caller's stream around each stage
+ * while enabled).  Stages: 0 = a1 extraction, 1 = a2+a3 contraction, 2 = a4+a5 epilogue.
+ * fcfs_profile_read synchronises the recorded events, writes the summed milliseconds and the
+ * number of recorded launches per stage (n_stages <= 3), and clears the record. */
+fcfs_status fcfs_profile_enable(int32_t on);
+fcfs_status fcfs_profile_read(double *ms_host, int64_t *count_host, int32_t n_stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCFS_H_ */

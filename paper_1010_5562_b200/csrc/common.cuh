@@ -1,0 +1,132 @@
+// common.cuh — internal helpers of libfcfs.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fcfs.h"
+
+namespace fcfs {
+
+// ---- error plumbing -------------------------------------------------------------------
+void set_error(const char *fmt, ...);
+fcfs_status cuda_status(cudaError_t e, const char *where);
+void count_launch(int n = 1);
+
+// stage timing (fcfs_profile_*): RAII pair of events around a stage on stream s
+enum Stage { kStageExtract = 0, kStageContract = 1, kStageEpilogue = 2, kNumStages = 3 };
+void profile_mark(int stage, int begin, cudaStream_t s);
+struct StageScope {
+    int stage;
+    cudaStream_t s;
+    StageScope(int st, cudaStream_t ss) : stage(st), s(ss) { profile_mark(stage, 1, s); }
+    ~StageScope() { profile_mark(stage, 0, s); }
+};
+
+#define FCFS_TRY_CUDA(expr)                                      \
+    do {                                                         \
+        cudaError_t _e = (expr);                                 \
+        if (_e != cudaSuccess) return fcfs::cuda_status(_e, #expr); \
+    } while (0)
+
+#define FCFS_CHECK_LAUNCH(name)                                  \
+    do {                                                         \
+        fcfs::count_launch();                                    \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return fcfs::cuda_status(_e, name); \
+    } while (0)
+
+// ---- workspace carving (256-byte aligned bump allocator) ---------------------------------
+struct Carver {
+    char *base;
+    size_t off, cap;
+    explicit Carver(void *b, size_t c) : base((char *)b), off(0), cap(c) {}
+    template <typename T>
+    T *take(size_t n) {
+        size_t a = (off + 255) & ~size_t(255);
+        off = a + n * sizeof(T);
+        return base ? (T *)(base + a) : nullptr;
+    }
+    size_t used() const { return (off + 255) & ~size_t(255); }
+    bool fits() const { return used() <= cap; }
+};
+
+// ---- plan of the real quadrant GEMM P = A diag(w) B^T -------------------
+// Side X rows: row 2j = w*cos(2 pi (m0+j) x / T), row 2j+1 = w*sin(...), j < nm;
+//              row 2*nm = w*x (axis row) if has_axis.
+// Side Y rows: row 2j = cos(2 pi (n0+j) y / T), row 2j+1 = sin(...), j < nn; row 2*nn = y.
+// P[ix][iy] = sum_k A[ix,k] B[iy,k].  The epilogue combines quadrant entries into F.
+struct SidePlan {
+    int32_t f0;      // first positive frequency (>= 1)
+    int32_t nf;      // number of positive frequencies
+    int32_t axis;    // 1 if the axis row (coordinate weight) is present
+    int32_t rows;    // 2*nf + axis
+};
+
+// Tiling of P over (clips x tiles_x x tiles_y x splits) work items; P_ws holds one
+// kTile x kTile FP64 block per item, row-major [ix][iy].
+static constexpr int kTile = 64;
+
+struct GemmPlan {
+    SidePlan X, Y;
+    int32_t tiles_x, tiles_y, splits;
+    int64_t B;                // clips
+    int64_t items;            // B * tiles_x * tiles_y * splits
+};
+
+// Corner source of one contraction: either one clip [k_lo, k_hi) or B clips by CSR.
+struct CornerSrc {
+    const int32_t *x, *y, *w;
+    const int64_t *corner_ptr;   // device CSR [B+1] or nullptr
+    int64_t k_lo, k_hi;          // used when corner_ptr == nullptr
+};
+
+struct EpiArgs {
+    int32_t M, N, layout;
+    double r2;
+    int32_t m_lo, m_hi;          // output rows (signed)
+    int64_t out_per_clip;
+    int32_t T;
+    const int64_t *area_dev;     // per-clip area (device) or nullptr
+    int64_t area_host;
+    int32_t out_f32;             // 1: complex64, 0: complex128
+};
+
+__host__ __device__ inline int32_t ilog2_ceil(int64_t v) {
+    int32_t b = 0;
+    while ((int64_t(1) << b) < v) ++b;
+    return b;
+}
+
+// Two-level twiddle table: r = hi*L + lo, e^{-i th(r)} = E_hi[hi] * E_lo[lo], th(r) = 2 pi r / T.
+// Tables hold (cos, sin) of +th; the sign of the imaginary part is applied by the caller.
+struct TwiddleGeom {
+    int32_t T;
+    int32_t lbits;   // L = 2^lbits
+    int32_t nhi;     // ceil(T / L)
+    int32_t pow2;    // T is a power of two
+};
+
+inline TwiddleGeom make_twiddle_geom(int32_t T) {
+    TwiddleGeom g;
+    g.T = T;
+    int32_t tb = ilog2_ceil(T);
+    g.lbits = (tb + 1) / 2;
+    g.nhi = (int32_t)((T + (1 << g.lbits) - 1) >> g.lbits);
+    g.pow2 = ((T & (T - 1)) == 0) ? 1 : 0;
+    return g;
+}
+
+// exact (m * v) mod T for m >= 0, 0 <= v <= T
+__device__ __forceinline__ uint32_t phase_mod(uint32_t m, uint32_t v, const TwiddleGeom &g) {
+    if (g.pow2) return (m * v) & (uint32_t)(g.T - 1);   // T | 2^32: wrap-around is harmless
+    return (uint32_t)(((uint64_t)m * v) % (uint64_t)g.T);
+}
+
+// launchers (contract_fp64.cu, epilogue.cu)
+fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
+                             cudaStream_t s);
+fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F,
+                            cudaStream_t s);
+fcfs_status launch_block_area(const CornerSrc &src, int64_t *area_dev, cudaStream_t s);
+
+}  // namespace fcfs

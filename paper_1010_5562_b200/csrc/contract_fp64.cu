@@ -1,0 +1,203 @@
+// contract_fp64.cu — a2 + a3 (FP64): generated-operand real GEMM P = A diag(w) B^T.
+//
+// The interior coefficients of Eq. Fkl are the 2-D DFT of the
+// sparse +-1 image f~_xy (Step 4), evaluated directly ("Goertzel-like",
+// P:917-920) on a low-pass window.  Writing E = c - i s, the complex sum
+// sum_k w_k E_x[m,k] E_y[n,k] for (m, +-n) is recombined from the four real quadrant
+// products P_cc, P_cs, P_sc, P_ss of
+//     A[2j  ,k] = w_k cos(2 pi m_j x_k / T),   A[2j+1,k] = w_k sin(...),   A[2nf,k] = w_k x_k
+//     B[2j  ,k] =     cos(2 pi n_j y_k / T),   B[2j+1,k] =     sin(...),   B[2nf,k] = y_k
+// (the last rows carry the axis sums of Eqs. Fk0/F0l, Steps 2-3 P:870-888).
+//
+// a2 (twiddles) is fused: each CTA generates its K-slab of A and B in shared memory
+// from the integer phase r = (m x) mod T (exact, lattice vertices P:860-862) through a
+// two-level table E(r) = E_hi(r >> L) * E_lo(r & (2^L - 1)) built in SMEM with sincospi,
+// so the twiddle matrices never touch HBM ("no full-length arrays").
+//
+// a3 (FP64): CUDA-core DFMA, 64x64 P tile per CTA, 4x4 register tile per thread,
+// double-buffered slabs of 16 corners.  Accumulation is hierarchical: a fresh register
+// accumulator per chunk of <= kChunk corners is added into a running total, bounding
+// the rounding error by about (kChunk + K/kChunk) u B instead of K u B.
+#include "common.cuh"
+
+namespace fcfs {
+
+static constexpr int kBK = 16;        // corners per slab
+static constexpr int kChunk = 2048;   // corners per register accumulator
+static constexpr int kThreads = 256;  // 16 x 16 threads, 4x4 outputs each
+
+struct TabPtrs {
+    double2 *hi, *lo;
+};
+
+__device__ __forceinline__ void build_tables(const TwiddleGeom &g, double2 *thi, double2 *tlo) {
+    const int L = 1 << g.lbits;
+    for (int i = threadIdx.x; i < g.nhi + L; i += blockDim.x) {
+        double s, c;
+        if (i < g.nhi) {
+            sincospi(2.0 * (double)((int64_t)i << g.lbits) / (double)g.T, &s, &c);
+            thi[i] = make_double2(c, s);
+        } else {
+            int b = i - g.nhi;
+            sincospi(2.0 * (double)b / (double)g.T, &s, &c);
+            tlo[b] = make_double2(c, s);
+        }
+    }
+}
+
+// (cos, sin) of 2 pi r / T via the two-level table
+__device__ __forceinline__ double2 twiddle(uint32_t r, const TwiddleGeom &g, const double2 *thi,
+                                           const double2 *tlo) {
+    double2 a = thi[r >> g.lbits];
+    double2 b = tlo[r & ((1u << g.lbits) - 1)];
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.y, b.x, a.x * b.y));
+}
+
+// (row 2p, row 2p+1) values of one side for corner coordinate v and weight wt
+__device__ __forceinline__ double2 side_pair(int p_global, const SidePlan &sp, int32_t v, double wt,
+                                             const TwiddleGeom &g, const double2 *thi, const double2 *tlo) {
+    if (p_global < sp.nf) {
+        uint32_t r = phase_mod((uint32_t)(sp.f0 + p_global), (uint32_t)v, g);
+        double2 cs = twiddle(r, g, thi, tlo);
+        return make_double2(wt * cs.x, wt * cs.y);
+    }
+    if (p_global == sp.nf && sp.axis) return make_double2(wt * (double)v, 0.0);
+    return make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_ws) {
+    extern __shared__ __align__(16) double smem_d[];
+    double2 *thi = (double2 *)smem_d;
+    double2 *tlo = thi + g.nhi;
+    double *As = (double *)(tlo + (1 << g.lbits));   // [2][kBK][64]
+    double *Bs = As + 2 * kBK * kTile;               // [2][kBK][64]
+
+    build_tables(g, thi, tlo);
+
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;          // output rows 4tx.., cols 4ty..
+    const int gp = tid & 31, gk = tid >> 5;          // generation: pair gp, corner gk (+8)
+    const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
+
+    for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
+        const int64_t clip = item / per_clip;
+        int64_t rem = item - clip * per_clip;
+        const int tix = (int)(rem / ((int64_t)plan.tiles_y * plan.splits));
+        rem -= (int64_t)tix * plan.tiles_y * plan.splits;
+        const int tiy = (int)(rem / plan.splits);
+        const int split = (int)(rem - (int64_t)tiy * plan.splits);
+        int64_t kb, ke;
+        if (src.corner_ptr) { kb = src.corner_ptr[clip]; ke = src.corner_ptr[clip + 1]; }
+        else { kb = src.k_lo; ke = src.k_hi; }
+        const int64_t span = ke - kb;
+        const int64_t k0 = kb + span * split / plan.splits;
+        const int64_t k1 = kb + span * (split + 1) / plan.splits;
+
+        double tot[4][4], acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tot[i][j] = 0.0;
+
+        __syncthreads();   // tables ready / previous item's smem reads done
+        auto generate = [&](int buf, int64_t ks, int64_t kend) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kk = gk + 8 * h;
+                const int64_t k = ks + kk;
+                int32_t xv = 0, yv = 0;
+                double wv = 0.0;
+                if (k < kend) { xv = __ldg(src.x + k); yv = __ldg(src.y + k); wv = (double)__ldg(src.w + k); }
+                double2 a = side_pair(tix * (kTile / 2) + gp, plan.X, xv, wv, g, thi, tlo);
+                double2 b = side_pair(tiy * (kTile / 2) + gp, plan.Y, yv, 1.0, g, thi, tlo);
+                if (k >= kend) b = make_double2(0.0, 0.0);
+                *(double2 *)&As[(buf * kBK + kk) * kTile + 2 * gp] = a;
+                *(double2 *)&Bs[(buf * kBK + kk) * kTile + 2 * gp] = b;
+            }
+        };
+
+        for (int64_t c0 = k0; c0 < k1; c0 += kChunk) {
+            const int64_t c1 = c0 + kChunk < k1 ? c0 + kChunk : k1;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+            int buf = 0;
+            generate(0, c0, c1);
+            __syncthreads();
+            for (int64_t ks = c0; ks < c1; ks += kBK) {
+                if (ks + kBK < c1) generate(buf ^ 1, ks + kBK, c1);
+                const double *Ab = As + buf * kBK * kTile + 4 * tx;
+                const double *Bb = Bs + buf * kBK * kTile + 4 * ty;
+#pragma unroll
+                for (int kk = 0; kk < kBK; ++kk) {
+                    double2 a01 = *(const double2 *)(Ab + kk * kTile);
+                    double2 a23 = *(const double2 *)(Ab + kk * kTile + 2);
+                    double2 b01 = *(const double2 *)(Bb + kk * kTile);
+                    double2 b23 = *(const double2 *)(Bb + kk * kTile + 2);
+                    double a[4] = {a01.x, a01.y, a23.x, a23.y};
+                    double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                }
+                __syncthreads();
+                buf ^= 1;
+            }
+            // corners k >= c1 of the last slab were generated as zeros (A = B = 0)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) tot[i][j] += acc[i][j];
+        }
+        double *out = P_ws + item * (int64_t)(kTile * kTile);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double *row = out + (4 * tx + i) * kTile + 4 * ty;
+            *(double2 *)row = make_double2(tot[i][0], tot[i][1]);
+            *(double2 *)(row + 2) = make_double2(tot[i][2], tot[i][3]);
+        }
+    }
+}
+
+fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
+                             cudaStream_t s) {
+    if (plan.items <= 0) return FCFS_OK;
+    TwiddleGeom g = make_twiddle_geom(T);
+    size_t smem = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kTile;
+    static bool attr = false;
+    if (!attr) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+    }
+    int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
+    k_gemm_fp64<<<(unsigned)grid, kThreads, smem, s>>>(src, plan, g, P_ws);
+    FCFS_CHECK_LAUNCH("k_gemm_fp64");
+    return FCFS_OK;
+}
+
+// sum_k w_k x_k y_k over [k_lo, k_hi) (vertex-block DC), exact int64
+__global__ void k_block_area(const int32_t *x, const int32_t *y, const int32_t *w, int64_t k_lo, int64_t k_hi,
+                             int64_t *area) {
+    long long s = 0;
+    for (int64_t k = k_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k_hi;
+         k += (int64_t)gridDim.x * blockDim.x)
+        s += (long long)w[k] * (long long)x[k] * (long long)y[k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s != 0) atomicAdd((unsigned long long *)area, (unsigned long long)s);
+}
+
+fcfs_status launch_block_area(const CornerSrc &src, int64_t *area_dev, cudaStream_t s) {
+    FCFS_TRY_CUDA(cudaMemsetAsync(area_dev, 0, sizeof(int64_t), s));
+    int64_t n = src.k_hi - src.k_lo;
+    if (n <= 0) return FCFS_OK;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    k_block_area<<<(unsigned)blocks, 256, 0, s>>>(src.x, src.y, src.w, src.k_lo, src.k_hi, area_dev);
+    FCFS_CHECK_LAUNCH("k_block_area");
+    return FCFS_OK;
+}
+
+}  // namespace fcfs

@@ -1,0 +1,117 @@
+// epilogue.cu — a4 + a5: axes, DC, quadrant recombination, scaling, mirror, window/pupil.
+//
+// From the real quadrant products P (contract_fp64.cu / contract_tf32.cu) of one clip:
+//   interior (Eq. Fkl, alpha case 4):  S(m,+n) = (Pcc - Pss) - i (Psc + Pcs)
+//                                                S(m,-n) = (Pcc + Pss) - i (Psc - Pcs)
+//                                                F[m,n]  = -S / (4 pi^2 m n)
+//   axes (Eqs. Fk0/F0l P:835-842, alpha cases 2-3): S(m,0) = P[c_m, y] - i P[s_m, y]
+//                                                F[m,0]  = i S / (2 pi m T)   (and F[0,n] likewise)
+//   DC (Eq. Fdc, Step 1): F[0,0] = area / T^2 from the exact int64 area.
+//   mirror: F[-m,-n] = conj F[m,n], written as a bitwise conjugate of the computed value.
+// The window is the signed low-pass box |m|<=M, |n|<=N (reading A3), optionally masked or
+// packed to the pupil disk m^2+n^2 <= r2 (reading A11).  P of a clip is the
+// fixed-order sum of its split-K partial tiles (deterministic).
+#include "common.cuh"
+
+namespace fcfs {
+
+__device__ __forceinline__ double getP(const double *P_ws, const GemmPlan &pl, int64_t clip, int ix, int iy) {
+    const int tix = ix / kTile, tiy = iy / kTile;
+    const int64_t base = ((clip * pl.tiles_x + tix) * pl.tiles_y + tiy) * pl.splits;
+    const int64_t off = (int64_t)(ix - tix * kTile) * kTile + (iy - tiy * kTile);
+    double s = 0.0;
+    for (int sp = 0; sp < pl.splits; ++sp) s += P_ws[(base + sp) * (kTile * kTile) + off];
+    return s;
+}
+
+// largest n >= 0 with m^2 + n^2 <= r2 (the same double comparison as the definition), -1 if none
+__device__ __forceinline__ int pupil_nmax(int m, double r2, int N) {
+    double mm = (double)m * (double)m;
+    if (mm > r2) return -1;
+    int n = (int)floor(sqrt(r2 - mm));
+    while (n + 1 <= N && mm + (double)(n + 1) * (double)(n + 1) <= r2) ++n;
+    while (n >= 0 && mm + (double)n * (double)n > r2) --n;
+    return n < N ? n : N;
+}
+
+__device__ double2 coeff(const double *P_ws, const GemmPlan &pl, const EpiArgs &ea, int64_t clip, int m, int n,
+                         double dc) {
+    const double pi = 3.141592653589793238462643383279502884;
+    if (m == 0 && n == 0) return make_double2(dc, 0.0);
+    const bool neg = (m < 0) || (m == 0 && n < 0);
+    if (neg) { m = -m; n = -n; }
+    double re, im;
+    if (n == 0) {
+        const int ic = 2 * (m - pl.X.f0), ia = 2 * pl.Y.nf;
+        double sre = getP(P_ws, pl, clip, ic, ia), sim = -getP(P_ws, pl, clip, ic + 1, ia);
+        double d = 2.0 * pi * (double)m * (double)ea.T;
+        re = -sim / d; im = sre / d;
+    } else if (m == 0) {
+        const int ia = 2 * pl.X.nf, jc = 2 * (n - pl.Y.f0);
+        double sre = getP(P_ws, pl, clip, ia, jc), sim = -getP(P_ws, pl, clip, ia, jc + 1);
+        double d = 2.0 * pi * (double)n * (double)ea.T;
+        re = -sim / d; im = sre / d;
+    } else {
+        const int an = n < 0 ? -n : n;
+        const int ic = 2 * (m - pl.X.f0), jc = 2 * (an - pl.Y.f0);
+        double pcc = getP(P_ws, pl, clip, ic, jc), pcs = getP(P_ws, pl, clip, ic, jc + 1);
+        double psc = getP(P_ws, pl, clip, ic + 1, jc), pss = getP(P_ws, pl, clip, ic + 1, jc + 1);
+        double sre, sim;
+        if (n > 0) { sre = pcc - pss; sim = -(psc + pcs); }
+        else { sre = pcc + pss; sim = -(psc - pcs); }
+        double d = -4.0 * pi * pi * (double)m * (double)n;
+        re = sre / d; im = sim / d;
+    }
+    if (neg) im = -im;
+    return make_double2(re, im);
+}
+
+// grid: (output rows, clips); block loops over n
+__global__ void k_epilogue(const double *__restrict__ P_ws, GemmPlan pl, EpiArgs ea, void *F) {
+    const int64_t clip = blockIdx.y;
+    const int m = ea.m_lo + (int)blockIdx.x;
+    if (m > ea.m_hi) return;
+    const int64_t area = ea.area_dev ? ea.area_dev[clip] : ea.area_host;
+    const double dc = (double)area / ((double)ea.T * (double)ea.T);
+    int64_t off;
+    int nlo, nhi;
+    if (ea.layout == FCFS_LAYOUT_PUPIL) {
+        off = 0;
+        for (int mm = -ea.M; mm < m; ++mm) {
+            int c = pupil_nmax(mm, ea.r2, ea.N);
+            off += c < 0 ? 0 : 2 * c + 1;
+        }
+        int c = pupil_nmax(m, ea.r2, ea.N);
+        if (c < 0) return;
+        nlo = -c; nhi = c;
+    } else {
+        off = (int64_t)(m - ea.m_lo) * (2 * ea.N + 1);
+        nlo = -ea.N; nhi = ea.N;
+    }
+    off += clip * ea.out_per_clip;
+    for (int n = nlo + (int)threadIdx.x; n <= nhi; n += blockDim.x) {
+        double2 v;
+        bool keep = true;
+        if (ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0)
+            keep = (double)m * (double)m + (double)n * (double)n <= ea.r2;
+        v = keep ? coeff(P_ws, pl, ea, clip, m, n, dc) : make_double2(0.0, 0.0);
+        const int64_t o = off + (n - nlo);
+        if (ea.out_f32) ((float2 *)F)[o] = make_float2((float)v.x, (float)v.y);
+        else ((double2 *)F)[o] = v;
+    }
+}
+
+fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F, cudaStream_t s) {
+    const int rows = ea.m_hi - ea.m_lo + 1;
+    if (rows <= 0 || plan.B <= 0) return FCFS_OK;
+    if (plan.B > 65535) {
+        set_error("epilogue: %lld clips exceed the grid limit", (long long)plan.B);
+        return FCFS_E_UNSUPPORTED;
+    }
+    dim3 grid((unsigned)rows, (unsigned)plan.B);
+    k_epilogue<<<grid, 128, 0, s>>>(P_ws, plan, ea, F);
+    FCFS_CHECK_LAUNCH("k_epilogue");
+    return FCFS_OK;
+}
+
+}  // namespace fcfs

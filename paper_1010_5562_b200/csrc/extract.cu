@@ -1,0 +1,396 @@
+// extract.cu — a1: vertex extraction, rects -> canonical signed corners + exact area.
+//
+// Follows Alg. 2 lines 1-14 re-expressed on signed corners:
+// the +1/-1 entries of V^KL/S^KL at the ends of horizontal edges are the
+// mixed difference w = f(x,y) - f(x-1,y) - f(x,y-1) + f(x-1,y-1) of the cell mask f
+// (Prop. 1, half-open convention P:398-402).  Step 1's area is
+// sum_k w_k x_k y_k, accumulated exactly in int64.
+//
+// Pipeline (all on the caller's stream, one host sync at the end for K):
+//   1. raw corners:  singleton groups -> 4 corners per rect (thread per rect);
+//                    unions -> one CTA per group: coordinate compression, 2-D difference
+//                    array of the coverage count on the compressed grid in SMEM, prefix
+//                    sums, union indicator, mixed difference, append non-zeros.
+//   2. CUB radix sort of 64-bit keys (clip<<42 | y<<21 | x) with int32 weights.
+//   3. CUB reduce-by-key (sum weights of equal keys; groups are SUMMED, reading A5).
+//   4. drop zero weights: flag + exclusive scan + scatter into x, y, w; int64 area atomics.
+//   5. corner_ptr by lower_bound of b<<42 in the compacted keys.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fcfs {
+
+static constexpr int kCoordBits = 21;
+static constexpr unsigned long long kSentinel = ~0ull;
+static constexpr int kMaxGroup = 100;
+
+struct ExtractWs {
+    unsigned long long *keys_a, *keys_b;
+    int32_t *w_a, *w_b;
+    int32_t *flags, *pos;
+    int64_t *num_runs, *K;
+    int32_t *err;
+    void *cub_tmp;
+    size_t cub_bytes;
+    int64_t cap_raw;
+};
+
+__device__ __forceinline__ unsigned long long make_key(int64_t clip, int32_t y, int32_t x) {
+    return ((unsigned long long)clip << (2 * kCoordBits)) | ((unsigned long long)y << kCoordBits) |
+           (unsigned long long)x;
+}
+
+__device__ __forceinline__ int64_t find_clip(const int64_t *clip_ptr, int64_t B, int64_t g) {
+    if (clip_ptr == nullptr) return 0;
+    // last b with clip_ptr[b] <= g
+    int64_t lo = 0, hi = B - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (clip_ptr[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ bool rect_ok(int4 q, int32_t T) {
+    return q.x >= 0 && q.y >= 0 && q.z <= T && q.w <= T && q.x < q.z && q.y < q.w;
+}
+
+// one thread per rect, every rect its own group (group_ptr == NULL)
+__global__ void k_singleton_corners(const int4 *__restrict__ rects, int64_t R,
+                                    const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
+                                    unsigned long long *keys, int32_t *wts, int32_t *err) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int4 q = rects[r];
+        int64_t b = find_clip(clip_ptr, B, r);
+        if (!rect_ok(q, T)) {
+            atomicOr(err, 1);
+            q = make_int4(0, 0, 0, 0);
+        }
+        keys[4 * r + 0] = make_key(b, q.y, q.x); wts[4 * r + 0] = 1;
+        keys[4 * r + 1] = make_key(b, q.y, q.z); wts[4 * r + 1] = -1;
+        keys[4 * r + 2] = make_key(b, q.w, q.x); wts[4 * r + 2] = -1;
+        keys[4 * r + 3] = make_key(b, q.w, q.z); wts[4 * r + 3] = 1;
+        if (q.x == q.z) { wts[4 * r + 0] = wts[4 * r + 1] = wts[4 * r + 2] = wts[4 * r + 3] = 0; }
+    }
+}
+
+// sort v[0..n) (stable rank sort, O(n) per thread) and unique it into uniq[0..*nu)
+__device__ __forceinline__ void compress(const int32_t *v, int n, int32_t *tmp, int32_t *uniq, int32_t *nu) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int32_t vi = v[i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            int32_t vj = v[j];
+            rank += (vj < vi) || (vj == vi && j < i);
+        }
+        tmp[rank] = vi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int i = 0; i < n; ++i)
+            if (i == 0 || tmp[i] != tmp[i - 1]) uniq[c++] = tmp[i];
+        *nu = c;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ int find_sorted(const int32_t *u, int n, int32_t key) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (u[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// one CTA per group: union of the group's rects on its compressed grid
+__global__ void k_group_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ group_ptr,
+                                int64_t G, const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
+                                unsigned long long *keys, int32_t *wts, int64_t cap_raw,
+                                unsigned long long *raw_count, int32_t *err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int4 *sr = (int4 *)smem;                                  // [kMaxGroup]
+    int32_t *vx = (int32_t *)(sr + kMaxGroup);                // [2*kMaxGroup]
+    int32_t *vy = vx + 2 * kMaxGroup;                         // [2*kMaxGroup]
+    int32_t *ux = vy + 2 * kMaxGroup;                         // [2*kMaxGroup]
+    int32_t *uy = ux + 2 * kMaxGroup;                         // [2*kMaxGroup]
+    int32_t *tmp = uy + 2 * kMaxGroup;                        // [2*kMaxGroup]
+    int32_t *nxy = tmp + 2 * kMaxGroup;                       // [2]
+    int32_t *grid = nxy + 2;                                  // [nx*ny] (dynamic extent)
+
+    for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+        int64_t r0 = group_ptr[g], r1 = group_ptr[g + 1];
+        int n = (int)(r1 - r0);
+        if (n <= 0) continue;
+        if (n > kMaxGroup) {
+            if (threadIdx.x == 0) atomicOr(err, 2);
+            continue;
+        }
+        int64_t b = find_clip(clip_ptr, B, g);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            int4 q = rects[r0 + i];
+            if (!rect_ok(q, T)) { atomicOr(err, 1); q = make_int4(0, 0, 0, 0); }
+            sr[i] = q;
+            vx[2 * i] = q.x; vx[2 * i + 1] = q.z;
+            vy[2 * i] = q.y; vy[2 * i + 1] = q.w;
+        }
+        __syncthreads();
+        compress(vx, 2 * n, tmp, ux, &nxy[0]);
+        compress(vy, 2 * n, tmp, uy, &nxy[1]);
+        const int nx = nxy[0], ny = nxy[1];
+        // difference array of the coverage count at grid points (i, j), i < nx, j < ny
+        for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) grid[t] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            int4 q = sr[i];
+            if (q.x == q.z) continue;   // invalid rect, already flagged
+            int i0 = find_sorted(ux, nx, q.x), i1 = find_sorted(ux, nx, q.z);
+            int j0 = find_sorted(uy, ny, q.y), j1 = find_sorted(uy, ny, q.w);
+            atomicAdd(&grid[i0 * ny + j0], 1);
+            atomicAdd(&grid[i1 * ny + j0], -1);
+            atomicAdd(&grid[i0 * ny + j1], -1);
+            atomicAdd(&grid[i1 * ny + j1], 1);
+        }
+        __syncthreads();
+        // prefix sums: along j for each i, then along i for each j -> coverage count of cell (i, j)
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            int s = 0;
+            for (int j = 0; j < ny; ++j) { s += grid[i * ny + j]; grid[i * ny + j] = s; }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < ny; j += blockDim.x) {
+            int s = 0;
+            for (int i = 0; i < nx; ++i) { s += grid[i * ny + j]; grid[i * ny + j] = (s > 0 ? 1 : 0); }
+        }
+        __syncthreads();
+        // mixed difference of the union indicator at every grid point
+        for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) {
+            int i = t / ny, j = t - i * ny;
+            int c00 = grid[t];
+            int cm0 = i > 0 ? grid[t - ny] : 0;
+            int c0m = j > 0 ? grid[t - 1] : 0;
+            int cmm = (i > 0 && j > 0) ? grid[t - ny - 1] : 0;
+            int wv = c00 - cm0 - c0m + cmm;
+            if (wv != 0) {
+                unsigned long long slot = atomicAdd(raw_count, 1ull);
+                if ((int64_t)slot < cap_raw) {
+                    keys[slot] = make_key(b, uy[j], ux[i]);
+                    wts[slot] = wv;
+                } else {
+                    atomicOr(err, 4);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fill_sentinel(unsigned long long *keys, int32_t *wts, int64_t n,
+                                const unsigned long long *raw_count) {
+    int64_t start = raw_count ? (int64_t)*raw_count : 0;
+    for (int64_t i = start + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = kSentinel;
+        wts[i] = 0;
+    }
+}
+
+__global__ void k_flags(const int32_t *wts, const int64_t *num_runs, int64_t n, int32_t *flags) {
+    int64_t nr = *num_runs;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flags[i] = (i < nr && wts[i] != 0) ? 1 : 0;
+}
+
+__global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, const int32_t *flags,
+                          const int32_t *pos, int64_t n, int64_t cap, int32_t *x, int32_t *y, int32_t *w,
+                          unsigned long long *ckeys, int64_t *area, int64_t *K) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == n - 1) *K = (int64_t)pos[i] + flags[i];
+        if (!flags[i]) continue;
+        unsigned long long key = ukeys[i];
+        int32_t xx = (int32_t)(key & ((1ull << kCoordBits) - 1));
+        int32_t yy = (int32_t)((key >> kCoordBits) & ((1ull << kCoordBits) - 1));
+        int64_t b = (int64_t)(key >> (2 * kCoordBits));
+        int64_t p = pos[i];
+        ckeys[p] = key;
+        if (p < cap) { x[p] = xx; y[p] = yy; w[p] = agg[i]; }
+        long long a = (long long)agg[i] * (long long)xx * (long long)yy;
+        atomicAdd((unsigned long long *)&area[b], (unsigned long long)a);
+    }
+}
+
+__global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, int64_t B, int64_t *corner_ptr) {
+    int64_t n = *K;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= B;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        if (b == B) { corner_ptr[b] = n; continue; }
+        unsigned long long target = (unsigned long long)b << (2 * kCoordBits);
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (ckeys[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        corner_ptr[b] = lo;
+    }
+}
+
+static int64_t raw_capacity(int64_t R, int64_t max_group, bool singleton) {
+    if (singleton) return 4 * R;
+    int64_t g = max_group < 1 ? 1 : max_group;
+    return 4 * R * g;   // a union of g rects has at most (2g)^2 grid points: sum_g 4 g^2 <= 4 R gmax
+}
+
+static size_t cub_bytes_for(int64_t n, int end_bit) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, end_bit);
+    cub::DeviceReduce::ReduceByKey(nullptr, b, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                   (int32_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr,
+                                   cub::Sum(), (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+    size_t m = a > b ? a : b;
+    return m > c ? m : c;
+}
+
+static int clip_bits(int64_t B) {
+    int bits = 1;
+    while ((int64_t(1) << bits) <= B) ++bits;
+    return bits;
+}
+
+static void carve(Carver &cv, int64_t cap_raw, size_t cub_bytes, ExtractWs &w) {
+    w.cap_raw = cap_raw;
+    w.keys_a = cv.take<unsigned long long>(cap_raw);
+    w.keys_b = cv.take<unsigned long long>(cap_raw);
+    w.w_a = cv.take<int32_t>(cap_raw);
+    w.w_b = cv.take<int32_t>(cap_raw);
+    w.flags = cv.take<int32_t>(cap_raw);
+    w.pos = cv.take<int32_t>(cap_raw);
+    w.num_runs = cv.take<int64_t>(1);
+    w.K = cv.take<int64_t>(1);
+    w.err = cv.take<int32_t>(4);
+    w.cub_tmp = cv.take<char>(cub_bytes);
+    w.cub_bytes = cub_bytes;
+}
+
+size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_group, bool singleton) {
+    int64_t cap = raw_capacity(R, max_group, singleton);
+    if (cap < 1) cap = 1;
+    Carver cv(nullptr, 0);
+    ExtractWs w;
+    carve(cv, cap, cub_bytes_for(cap, 2 * kCoordBits + clip_bits(B)), w);
+    return cv.used();
+}
+
+fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                    const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
+                    int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {
+    const bool singleton = (group_ptr == nullptr);
+    if (!singleton && max_group > kMaxGroup) {
+        set_error("fcfs_vertices_from_rects: max_group=%lld exceeds this build's limit %d",
+                  (long long)max_group, kMaxGroup);
+        return FCFS_E_UNSUPPORTED;
+    }
+    int64_t cap_raw = raw_capacity(R, max_group, singleton);
+    if (cap_raw < 1) cap_raw = 1;
+    if (cap_raw >= (int64_t(1) << 31)) {
+        set_error("fcfs_vertices_from_rects: %lld raw corners exceed 2^31", (long long)cap_raw);
+        return FCFS_E_UNSUPPORTED;
+    }
+    const int end_bit = 2 * kCoordBits + clip_bits(B);
+    Carver cv(ws, ws_bytes);
+    ExtractWs W;
+    carve(cv, cap_raw, cub_bytes_for(cap_raw, end_bit), W);
+    if (!cv.fits()) {
+        set_error("fcfs_vertices_from_rects: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.num_runs, 0, 2 * sizeof(int64_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(area, 0, B * sizeof(int64_t), s));
+    unsigned long long *raw_count = (unsigned long long *)W.num_runs;   // reused before reduce
+    const int threads = 256;
+    if (singleton) {
+        if (R > 0) {
+            int64_t blocks = (R + threads - 1) / threads;
+            if (blocks > 148 * 32) blocks = 148 * 32;
+            k_singleton_corners<<<(unsigned)blocks, threads, 0, s>>>((const int4 *)rects, R, clip_ptr, B, T,
+                                                                      W.keys_a, W.w_a, W.err);
+            FCFS_CHECK_LAUNCH("k_singleton_corners");
+        }
+        if (cap_raw > 4 * R) {
+            k_fill_sentinel<<<1, 32, 0, s>>>(W.keys_a + 4 * R, W.w_a + 4 * R, cap_raw - 4 * R, nullptr);
+            FCFS_CHECK_LAUNCH("k_fill_sentinel");
+        }
+    } else {
+        int mg = (int)(max_group < 1 ? 1 : max_group);
+        size_t smem = sizeof(int4) * kMaxGroup + sizeof(int32_t) * (10 * kMaxGroup + 2) +
+                      sizeof(int32_t) * (size_t)(2 * mg) * (2 * mg) + 16;
+        static bool attr_set = false;
+        if (!attr_set) {
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_group_corners, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               210 * 1024));
+            attr_set = true;
+        }
+        if (G > 0) {
+            int64_t blocks = G < 148 * 8 ? G : 148 * 8;
+            k_group_corners<<<(unsigned)blocks, 256, smem, s>>>((const int4 *)rects, group_ptr, G, clip_ptr, B, T,
+                                                                 W.keys_a, W.w_a, cap_raw, raw_count, W.err);
+            FCFS_CHECK_LAUNCH("k_group_corners");
+        }
+        k_fill_sentinel<<<148 * 4, 256, 0, s>>>(W.keys_a, W.w_a, cap_raw, raw_count);
+        FCFS_CHECK_LAUNCH("k_fill_sentinel");
+    }
+    size_t tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, W.keys_a, W.keys_b, W.w_a, W.w_b, (int)cap_raw,
+                                                  0, end_bit, s));
+    count_launch(4);
+    tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceReduce::ReduceByKey(W.cub_tmp, tb, W.keys_b, W.keys_a, W.w_b, W.w_a, W.num_runs,
+                                                 cub::Sum(), (int)cap_raw, s));
+    count_launch(2);
+    int64_t blocks = (cap_raw + threads - 1) / threads;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_flags<<<(unsigned)blocks, threads, 0, s>>>(W.w_a, W.num_runs, cap_raw, W.flags);
+    FCFS_CHECK_LAUNCH("k_flags");
+    tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.flags, W.pos, (int)cap_raw, s));
+    count_launch(2);
+    k_scatter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, W.flags, W.pos, cap_raw, cap, x, y, w,
+                                                   W.keys_b, area, W.K);
+    FCFS_CHECK_LAUNCH("k_scatter");
+    int64_t pb = (B + 1 + threads - 1) / threads;
+    k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr);
+    FCFS_CHECK_LAUNCH("k_corner_ptr");
+    int64_t Kh = 0;
+    int32_t errh = 0;
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, W.K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (K_host) *K_host = Kh;
+    if (errh & 1) {
+        set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");
+        return FCFS_E_RANGE;
+    }
+    if (errh & 2) {
+        set_error("fcfs_vertices_from_rects: a group has more than %d rects", kMaxGroup);
+        return FCFS_E_UNSUPPORTED;
+    }
+    if (errh & 4) {
+        set_error("fcfs_vertices_from_rects: raw corner capacity exceeded (max_group too small?)");
+        return FCFS_E_WORKSPACE;
+    }
+    if (Kh > cap) {
+        set_error("fcfs_vertices_from_rects: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
+        return FCFS_E_CAPACITY;
+    }
+    return FCFS_OK;
+}
+
+}  // namespace fcfs

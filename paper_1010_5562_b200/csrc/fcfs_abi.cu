@@ -1,0 +1,393 @@
+// fcfs_abi.cu — the extern "C" boundary of libfcfs.so (include/fcfs.h): argument
+// validation, planning, workspace carving and kernel launches on the caller's stream.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace fcfs {
+
+static thread_local char g_err[1024] = "";
+static thread_local int g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+fcfs_status cuda_status(cudaError_t e, const char *where) {
+    set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+    return FCFS_E_CUDA;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+struct ProfRec {
+    cudaEvent_t a, b;
+    int stage;
+};
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfRec> g_prof;        // recorded pairs
+static thread_local std::vector<cudaEvent_t> g_pool;    // free events
+static thread_local cudaEvent_t g_open[kNumStages] = {};
+
+static cudaEvent_t pool_get() {
+    if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void profile_mark(int stage, int begin, cudaStream_t s) {
+    if (!g_prof_on) return;
+    cudaEvent_t e = pool_get();
+    cudaEventRecord(e, s);
+    if (begin) { g_open[stage] = e; return; }
+    g_prof.push_back(ProfRec{g_open[stage], e, stage});
+    g_open[stage] = nullptr;
+}
+
+// extract.cu
+size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_group, bool singleton);
+fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                    const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
+                    int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s);
+// contract_tf32.cu
+fcfs_status tf32_supported(const GemmPlan &plan, int32_t T);
+fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
+                             cudaStream_t s);
+
+static fcfs_status device_ok() {
+    static int cached = -1;
+    if (cached < 0) {
+        int dev = 0, major = 0, minor = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        if (e != cudaSuccess) return cuda_status(e, "device query");
+        cached = (major == 10 && minor == 0) ? 1 : 0;
+        if (!cached) set_error("device is sm_%d%d; libfcfs.so is built for sm_100a only", major, minor);
+    }
+    if (!cached) {
+        set_error("device is not sm_100; libfcfs.so is built for sm_100a only");
+        return FCFS_E_UNSUPPORTED;
+    }
+    return FCFS_OK;
+}
+
+static bool valid_T(int32_t T) { return T >= 1 && T <= (1 << 20); }
+
+static fcfs_status check_window(const fcfs_window *win) {
+    if (!win) { set_error("win is NULL"); return FCFS_E_INVALID; }
+    if (win->M < 0 || win->N < 0 || win->M > 65535 || win->N > 65535) {
+        set_error("window M=%d N=%d out of range", win->M, win->N);
+        return FCFS_E_INVALID;
+    }
+    if (win->layout != FCFS_LAYOUT_DENSE && win->layout != FCFS_LAYOUT_PUPIL) {
+        set_error("bad layout %d", win->layout);
+        return FCFS_E_INVALID;
+    }
+    if (win->layout == FCFS_LAYOUT_PUPIL && !(win->pupil_r2 >= 0.0)) {
+        set_error("PUPIL layout needs pupil_r2 >= 0");
+        return FCFS_E_INVALID;
+    }
+    return FCFS_OK;
+}
+
+static int64_t pupil_count(int32_t M, int32_t N, double r2, int32_t *mo, int32_t *no, int64_t cap) {
+    int64_t c = 0;
+    for (int64_t m = -M; m <= M; ++m)
+        for (int64_t n = -N; n <= N; ++n) {
+            if ((double)m * (double)m + (double)n * (double)n > r2) continue;
+            if (mo && no && c < cap) { mo[c] = (int32_t)m; no[c] = (int32_t)n; }
+            ++c;
+        }
+    return c;
+}
+
+static SidePlan side_for_rows(int32_t m_lo, int32_t m_hi) {
+    SidePlan sp;
+    sp.axis = (m_lo <= 0 && 0 <= m_hi) ? 1 : 0;
+    int32_t a, b;
+    if (m_lo >= 1) { a = m_lo; b = m_hi; }
+    else if (m_hi <= -1) { a = -m_hi; b = -m_lo; }
+    else { a = 1; b = (-m_lo > m_hi) ? -m_lo : m_hi; }
+    sp.f0 = a;
+    sp.nf = b >= a ? b - a + 1 : 0;
+    if (sp.nf == 0) sp.f0 = 1;
+    sp.rows = 2 * sp.nf + sp.axis;
+    return sp;
+}
+
+static GemmPlan make_plan(int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t B, int64_t K, bool batched) {
+    GemmPlan p;
+    p.X = side_for_rows(m_lo, m_hi);
+    p.Y = side_for_rows(-N, N);
+    p.tiles_x = (p.X.rows + kTile - 1) / kTile;
+    p.tiles_y = (p.Y.rows + kTile - 1) / kTile;
+    if (p.tiles_x < 1) p.tiles_x = 1;
+    if (p.tiles_y < 1) p.tiles_y = 1;
+    int64_t tiles = (int64_t)p.tiles_x * p.tiles_y;
+    int64_t splits = 1;
+    if (!batched) {
+        const int64_t target = 2 * 2 * 148;   // two waves of 2 CTAs/SM
+        splits = (target + tiles - 1) / tiles;
+        int64_t kcap = (K + 511) / 512;
+        if (splits > kcap) splits = kcap;
+        if (splits < 1) splits = 1;
+        if (splits > 4096) splits = 4096;
+    }
+    p.splits = (int32_t)splits;
+    p.B = B;
+    p.items = B * tiles * splits;
+    return p;
+}
+
+struct CoeffWs {
+    double *P;
+    int64_t *area;
+};
+
+static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w) {
+    w.P = cv.take<double>((size_t)p.items * kTile * kTile);
+    w.area = cv.take<int64_t>(1);
+}
+
+static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard, int32_t &m_lo, int32_t &m_hi) {
+    m_lo = -win->M;
+    m_hi = win->M;
+    if (shard && shard->kind == FCFS_SHARD_ROWS) {
+        if (win->layout != FCFS_LAYOUT_DENSE) { set_error("ROWS shard needs the DENSE layout"); return FCFS_E_INVALID; }
+        if (shard->m_lo < -win->M || shard->m_hi > win->M || shard->m_lo > shard->m_hi) {
+            set_error("ROWS shard [%d, %d] outside [-M, M]", shard->m_lo, shard->m_hi);
+            return FCFS_E_INVALID;
+        }
+        m_lo = shard->m_lo;
+        m_hi = shard->m_hi;
+    } else if (shard && shard->kind != FCFS_SHARD_NONE && shard->kind != FCFS_SHARD_VERTEX_BLOCK) {
+        set_error("bad shard kind %d", shard->kind);
+        return FCFS_E_INVALID;
+    }
+    return FCFS_OK;
+}
+
+static fcfs_status run_gemm(const CornerSrc &src, const GemmPlan &plan, int32_t T, fcfs_precision prec,
+                            double *P, cudaStream_t s) {
+    if (prec == FCFS_FP64) return launch_gemm_fp64(src, plan, T, P, s);
+    if (prec == FCFS_TF32X3) {
+        fcfs_status st = tf32_supported(plan, T);
+        if (st != FCFS_OK) return st;
+        return launch_gemm_tf32(src, plan, T, P, s);
+    }
+    set_error("bad precision %d", prec);
+    return FCFS_E_INVALID;
+}
+
+}  // namespace fcfs
+
+using namespace fcfs;
+
+extern "C" {
+
+const char *fcfs_status_string(fcfs_status s) {
+    switch (s) {
+        case FCFS_OK: return "FCFS_OK";
+        case FCFS_E_INVALID: return "FCFS_E_INVALID";
+        case FCFS_E_RANGE: return "FCFS_E_RANGE";
+        case FCFS_E_CAPACITY: return "FCFS_E_CAPACITY";
+        case FCFS_E_WORKSPACE: return "FCFS_E_WORKSPACE";
+        case FCFS_E_UNSUPPORTED: return "FCFS_E_UNSUPPORTED";
+        case FCFS_E_CUDA: return "FCFS_E_CUDA";
+        default: return "FCFS_E_UNKNOWN";
+    }
+}
+
+const char *fcfs_last_error(void) { return g_err; }
+
+int32_t fcfs_kernel_launches(void) { return g_launches; }
+
+fcfs_status fcfs_device_check(void) { return device_ok(); }
+
+fcfs_status fcfs_profile_enable(int32_t on) {
+    g_prof_on = on != 0;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_profile_read(double *ms_host, int64_t *count_host, int32_t n_stages) {
+    if (n_stages < 0 || n_stages > kNumStages || (n_stages > 0 && (!ms_host || !count_host))) {
+        set_error("fcfs_profile_read: bad arguments");
+        return FCFS_E_INVALID;
+    }
+    for (int i = 0; i < n_stages; ++i) { ms_host[i] = 0.0; count_host[i] = 0; }
+    fcfs_status st = FCFS_OK;
+    for (auto &r : g_prof) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) st = cuda_status(e, "fcfs_profile_read");
+        if (r.stage < n_stages) { ms_host[r.stage] += ms; count_host[r.stage] += 1; }
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    return st;
+}
+
+int64_t fcfs_window_size(const fcfs_window *win) {
+    if (check_window(win) != FCFS_OK) return -1;
+    if (win->layout == FCFS_LAYOUT_PUPIL) return pupil_count(win->M, win->N, win->pupil_r2, nullptr, nullptr, 0);
+    return (int64_t)(2 * win->M + 1) * (2 * win->N + 1);
+}
+
+int64_t fcfs_pupil_indices(int32_t M, int32_t N, double r2, int32_t *m_out_host, int32_t *n_out_host, int64_t cap) {
+    if (M < 0 || N < 0) return -1;
+    return pupil_count(M, N, r2, m_out_host, n_out_host, cap);
+}
+
+size_t fcfs_vertices_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_group) {
+    // the singleton path is chosen by group_ptr == NULL at call time; size for the larger
+    size_t a = extract_workspace_bytes(R, G, B, max_group, true);
+    size_t b = extract_workspace_bytes(R, G, B, max_group, false);
+    return a > b ? a : b;
+}
+
+fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group,
+                                     int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr,
+                                     int64_t *area, int64_t *K_total_host, void *ws, size_t ws_bytes,
+                                     void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && !rects) || !corner_ptr || !area || !K_total_host) {
+        set_error("fcfs_vertices_from_rects: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (cap > 0 && (!x || !y || !w)) { set_error("null corner output with cap > 0"); return FCFS_E_INVALID; }
+    if (group_ptr == nullptr && G != R) { set_error("group_ptr NULL requires G == R"); return FCFS_E_INVALID; }
+    if (clip_ptr == nullptr && B != 1) { set_error("clip_ptr NULL requires B == 1"); return FCFS_E_INVALID; }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageExtract, (cudaStream_t)stream);
+    return extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
+                   K_total_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
+                                   const fcfs_shard *shard) {
+    (void)T; (void)prec;
+    if (check_window(win) != FCFS_OK) return 0;
+    int32_t m_lo, m_hi;
+    if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
+    int64_t k = K;
+    if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
+    GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
+    Carver cv(nullptr, 0);
+    CoeffWs w;
+    carve_coeff(cv, p, w);
+    return cv.used();
+}
+
+fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
+                        const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard, void *F, void *ws,
+                        size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    fcfs_status st = check_window(win);
+    if (st != FCFS_OK) return st;
+    if (K < 0 || (K > 0 && (!x || !y || !w)) || !F) { set_error("fcfs_coeffs: null pointer or K < 0"); return FCFS_E_INVALID; }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    int32_t m_lo, m_hi;
+    st = resolve_rows(win, shard, m_lo, m_hi);
+    if (st != FCFS_OK) return st;
+    CornerSrc src;
+    src.x = x; src.y = y; src.w = w; src.corner_ptr = nullptr; src.k_lo = 0; src.k_hi = K;
+    bool vblock = shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK;
+    if (vblock) {
+        if (shard->k_lo < 0 || shard->k_hi > K || shard->k_lo > shard->k_hi) {
+            set_error("VERTEX_BLOCK [%lld, %lld) outside [0, K)", (long long)shard->k_lo, (long long)shard->k_hi);
+            return FCFS_E_INVALID;
+        }
+        src.k_lo = shard->k_lo; src.k_hi = shard->k_hi;
+    }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    st = device_ok();
+    if (st != FCFS_OK) return st;
+    GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
+    Carver cv(ws, ws_bytes);
+    CoeffWs W;
+    carve_coeff(cv, plan, W);
+    if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    EpiArgs ea;
+    ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
+    ea.m_lo = m_lo; ea.m_hi = m_hi; ea.T = T; ea.area_dev = nullptr; ea.area_host = area;
+    ea.out_f32 = prec == FCFS_TF32X3 ? 1 : 0;
+    ea.out_per_clip = 0;
+    if (vblock) {
+        st = launch_block_area(src, W.area, s);
+        if (st != FCFS_OK) return st;
+        ea.area_dev = W.area;
+    }
+    {
+        StageScope scope(kStageContract, s);
+        st = run_gemm(src, plan, T, prec, W.P, s);
+    }
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageEpilogue, s);
+    return launch_epilogue(plan, W.P, ea, F, s);
+}
+
+size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,
+                                    fcfs_precision prec) {
+    (void)K_total; (void)T; (void)prec;
+    if (check_window(win) != FCFS_OK || B < 1) return 0;
+    GemmPlan p = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
+    Carver cv(nullptr, 0);
+    CoeffWs w;
+    carve_coeff(cv, p, w);
+    return cv.used();
+}
+
+fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
+                                const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
+                                int32_t T, const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
+                                size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    fcfs_status st = check_window(win);
+    if (st != FCFS_OK) return st;
+    if (B < 1 || !corner_ptr || !area || !F || K_total < 0 || K_max < 0 || (K_total > 0 && (!x || !y || !w))) {
+        set_error("fcfs_coeffs_batched: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    st = device_ok();
+    if (st != FCFS_OK) return st;
+    GemmPlan plan = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
+    Carver cv(ws, ws_bytes);
+    CoeffWs W;
+    carve_coeff(cv, plan, W);
+    if (!cv.fits()) { set_error("fcfs_coeffs_batched: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    CornerSrc src;
+    src.x = x; src.y = y; src.w = w; src.corner_ptr = corner_ptr; src.k_lo = 0; src.k_hi = 0;
+    EpiArgs ea;
+    ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
+    ea.m_lo = -win->M; ea.m_hi = win->M; ea.T = T; ea.area_dev = area; ea.area_host = 0;
+    ea.out_f32 = prec == FCFS_TF32X3 ? 1 : 0;
+    ea.out_per_clip = fcfs_window_size(win);
+    {
+        StageScope scope(kStageContract, s);
+        st = run_gemm(src, plan, T, prec, W.P, s);
+    }
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageEpilogue, s);
+    return launch_epilogue(plan, W.P, ea, F, s);
+}
+
+}  // extern "C"

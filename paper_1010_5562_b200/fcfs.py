@@ -1,0 +1,280 @@
+"""ctypes binding of libfcfs.so (include/fcfs.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+allocates torch tensors (device memory, workspaces), passes raw pointers and the
+current CUDA stream, and raises ``FcfsError`` on a non-OK status.  There is no CPU
+fallback: importing this module fails loudly if ``libfcfs.so`` is missing.
+
+Names follow the C-ABI: ``vertices_from_rects`` (a1), ``coeffs`` (a2-a5, one clip,
+optional shard), ``coeffs_batched`` (many clips), ``pupil_indices``, ``window_size``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfcfs.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libfcfs.so not found at {LIB_PATH}: build it with "
+                      "`python -m paper_1010_5562_b200.build` (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+FCFS_OK, E_INVALID, E_RANGE, E_CAPACITY, E_WORKSPACE, E_UNSUPPORTED, E_CUDA = range(7)
+FP64, TF32X3 = 0, 1
+LAYOUT_DENSE, LAYOUT_PUPIL = 0, 1
+SHARD_NONE, SHARD_ROWS, SHARD_VERTEX_BLOCK = 0, 1, 2
+_PREC = {"fp64": FP64, "tf32x3": TF32X3, FP64: FP64, TF32X3: TF32X3}
+_LAYOUT = {"dense": LAYOUT_DENSE, "pupil": LAYOUT_PUPIL, LAYOUT_DENSE: LAYOUT_DENSE, LAYOUT_PUPIL: LAYOUT_PUPIL}
+
+
+class Window(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("pupil_r2", ctypes.c_double),
+                ("layout", ctypes.c_int32)]
+
+
+class Shard(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("m_lo", ctypes.c_int32), ("m_hi", ctypes.c_int32),
+                ("k_lo", ctypes.c_int64), ("k_hi", ctypes.c_int64)]
+
+
+_P, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+_WP, _SP = ctypes.POINTER(Window), ctypes.POINTER(Shard)
+
+_lib.fcfs_status_string.argtypes = [_i32]
+_lib.fcfs_status_string.restype = ctypes.c_char_p
+_lib.fcfs_last_error.argtypes = []
+_lib.fcfs_last_error.restype = ctypes.c_char_p
+_lib.fcfs_device_check.argtypes = []
+_lib.fcfs_device_check.restype = _i32
+_lib.fcfs_kernel_launches.argtypes = []
+_lib.fcfs_kernel_launches.restype = _i32
+_lib.fcfs_window_size.argtypes = [_WP]
+_lib.fcfs_window_size.restype = _i64
+_lib.fcfs_pupil_indices.argtypes = [_i32, _i32, ctypes.c_double, _P, _P, _i64]
+_lib.fcfs_pupil_indices.restype = _i64
+_lib.fcfs_vertices_workspace_bytes.argtypes = [_i64, _i64, _i64, _i64]
+_lib.fcfs_vertices_workspace_bytes.restype = _sz
+_lib.fcfs_vertices_from_rects.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P,
+                                          ctypes.POINTER(_i64), _P, _sz, _P]
+_lib.fcfs_vertices_from_rects.restype = _i32
+_lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
+_lib.fcfs_coeffs_workspace_bytes.restype = _sz
+_lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _P, _P, _sz, _P]
+_lib.fcfs_coeffs.restype = _i32
+_lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32]
+_lib.fcfs_batched_workspace_bytes.restype = _sz
+_lib.fcfs_coeffs_batched.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _i32, _WP, _i32, _P, _P, _sz, _P]
+_lib.fcfs_coeffs_batched.restype = _i32
+
+_lib.fcfs_profile_enable.argtypes = [_i32]
+_lib.fcfs_profile_enable.restype = _i32
+_lib.fcfs_profile_read.argtypes = [_P, _P, _i32]
+_lib.fcfs_profile_read.restype = _i32
+
+EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_coeffs_workspace_bytes",
+            "fcfs_coeffs", "fcfs_batched_workspace_bytes", "fcfs_coeffs_batched", "fcfs_window_size",
+            "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
+            "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read"]
+STAGES = ("extract", "contract", "epilogue")
+
+
+class FcfsError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        name = _lib.fcfs_status_string(status).decode()
+        detail = _lib.fcfs_last_error().decode()
+        super().__init__(f"{where}: {name}: {detail}")
+
+
+def _check(st, where):
+    if st != FCFS_OK:
+        raise FcfsError(st, where)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ws(nbytes, device):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def make_window(M, N, r2=-1.0, layout="dense"):
+    return Window(int(M), int(N), float(r2), _LAYOUT[layout])
+
+
+def window_size(M, N, r2=-1.0, layout="dense"):
+    w = make_window(M, N, r2, layout)
+    n = _lib.fcfs_window_size(ctypes.byref(w))
+    if n < 0:
+        raise FcfsError(E_INVALID, "window_size")
+    return int(n)
+
+
+def pupil_indices(M, N, r2):
+    """(ms, ns) int32 host tensors of the packed pupil order (m-major, then n)."""
+    cnt = _lib.fcfs_pupil_indices(int(M), int(N), float(r2), None, None, 0)
+    ms = torch.zeros(cnt, dtype=torch.int32)
+    ns = torch.zeros(cnt, dtype=torch.int32)
+    _lib.fcfs_pupil_indices(int(M), int(N), float(r2), _ptr(ms), _ptr(ns), cnt)
+    return ms, ns
+
+
+def device_check():
+    _check(_lib.fcfs_device_check(), "device_check")
+
+
+def kernel_launches() -> int:
+    return int(_lib.fcfs_kernel_launches())
+
+
+def profile_enable(on=True):
+    _check(_lib.fcfs_profile_enable(1 if on else 0), "fcfs_profile_enable")
+
+
+def profile_read():
+    """{stage: (ms_total, launches)} of the CUDA-event-timed stages since the last read."""
+    ms = (ctypes.c_double * 3)()
+    cnt = (ctypes.c_int64 * 3)()
+    _check(_lib.fcfs_profile_read(ms, cnt, 3), "fcfs_profile_read")
+    return {STAGES[i]: (float(ms[i]), int(cnt[i])) for i in range(3)}
+
+
+def _max_group_host(group_ptr):
+    if group_ptr is None:
+        return 1
+    d = group_ptr[1:] - group_ptr[:-1]
+    return int(d.max().item()) if d.numel() else 1
+
+
+def vertices_from_rects(rects, T, group_ptr=None, clip_ptr=None, max_group=None, stream=None):
+    """a1: canonical signed corners.  rects int32 [R,4] cuda; group_ptr/clip_ptr int64 cuda or None.
+
+    Returns dict(x, y, w (int32 cuda [K]), corner_ptr (int64 cuda [B+1]), area (int64 cuda [B]), K).
+    """
+    dev = rects.device
+    rects = rects.contiguous()
+    R = rects.shape[0]
+    G = R if group_ptr is None else group_ptr.shape[0] - 1
+    B = 1 if clip_ptr is None else clip_ptr.shape[0] - 1
+    mg = _max_group_host(group_ptr) if max_group is None else int(max_group)
+    cap = 4 * R if group_ptr is None else 4 * R * max(mg, 1)
+    x = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    y = torch.empty_like(x)
+    w = torch.empty_like(x)
+    cptr = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    area = torch.empty(B, dtype=torch.int64, device=dev)
+    ws = _ws(_lib.fcfs_vertices_workspace_bytes(R, G, B, mg), dev)
+    K = ctypes.c_int64(0)
+    st = _lib.fcfs_vertices_from_rects(_ptr(rects), R, _ptr(group_ptr), G, _ptr(clip_ptr), B, int(T), mg,
+                                       _ptr(x), _ptr(y), _ptr(w), cap, _ptr(cptr), _ptr(area), ctypes.byref(K),
+                                       _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "fcfs_vertices_from_rects")
+    k = K.value
+    return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
+
+
+class VerticesPlan:
+    """Pre-allocated outputs + workspace for repeated ``fcfs_vertices_from_rects`` calls."""
+
+    def __init__(self, R, T, G=None, B=1, max_group=1, grouped=False, device="cuda"):
+        self.R, self.T, self.B = int(R), int(T), int(B)
+        self.G = self.R if G is None else int(G)
+        self.mg = max(int(max_group), 1)
+        self.cap = 4 * self.R * (self.mg if grouped else 1)
+        self.x = torch.empty(max(self.cap, 1), dtype=torch.int32, device=device)
+        self.y = torch.empty_like(self.x)
+        self.w = torch.empty_like(self.x)
+        self.corner_ptr = torch.empty(self.B + 1, dtype=torch.int64, device=device)
+        self.area = torch.empty(self.B, dtype=torch.int64, device=device)
+        self.ws = _ws(_lib.fcfs_vertices_workspace_bytes(self.R, self.G, self.B, self.mg), device)
+        self.K = 0
+
+    def run(self, rects, group_ptr=None, clip_ptr=None, stream=None):
+        K = ctypes.c_int64(0)
+        st = _lib.fcfs_vertices_from_rects(_ptr(rects), self.R, _ptr(group_ptr), self.G, _ptr(clip_ptr), self.B,
+                                           self.T, self.mg, _ptr(self.x), _ptr(self.y), _ptr(self.w), self.cap,
+                                           _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K), _ptr(self.ws),
+                                           self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_vertices_from_rects")
+        self.K = K.value
+        return self.K
+
+
+def _out_dtype(prec):
+    return torch.complex128 if _PREC[prec] == FP64 else torch.complex64
+
+
+class CoeffsPlan:
+    """Pre-allocated workspace + output for repeated ``fcfs_coeffs`` calls on one clip."""
+
+    def __init__(self, K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, device="cuda"):
+        self.K, self.T, self.prec = int(K), int(T), _PREC[prec]
+        self.win = make_window(M, N, r2, layout)
+        self.shard = shard
+        sp = ctypes.byref(shard) if shard is not None else None
+        nbytes = _lib.fcfs_coeffs_workspace_bytes(self.K, self.T, ctypes.byref(self.win), self.prec, sp)
+        if nbytes == 0:
+            raise FcfsError(E_INVALID, "fcfs_coeffs_workspace_bytes")
+        self.ws = _ws(nbytes, device)
+        if shard is not None and shard.kind == SHARD_ROWS:
+            n_out = (shard.m_hi - shard.m_lo + 1) * (2 * int(N) + 1)
+        else:
+            n_out = window_size(M, N, r2, layout)
+        self.out = torch.empty(n_out, dtype=_out_dtype(prec), device=device)
+
+    def run(self, x, y, w, area, stream=None, out=None):
+        out = self.out if out is None else out
+        sp = ctypes.byref(self.shard) if self.shard is not None else None
+        st = _lib.fcfs_coeffs(_ptr(x), _ptr(y), _ptr(w), self.K, int(area), self.T, ctypes.byref(self.win),
+                              self.prec, sp, _ptr(out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_coeffs")
+        return out
+
+
+def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, stream=None):
+    """a2-a5 for one clip.  Returns complex128 (fp64) or complex64 (tf32x3) cuda tensor."""
+    plan = CoeffsPlan(x.shape[0], T, M, N, r2, layout, prec, shard, device=x.device)
+    return plan.run(x, y, w, area, stream=stream)
+
+
+class BatchedPlan:
+    """Pre-allocated workspace + output for repeated ``fcfs_coeffs_batched`` calls."""
+
+    def __init__(self, B, K_total, K_max, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", device="cuda"):
+        self.B, self.K_total, self.K_max, self.T, self.prec = int(B), int(K_total), int(K_max), int(T), _PREC[prec]
+        self.win = make_window(M, N, r2, layout)
+        nbytes = _lib.fcfs_batched_workspace_bytes(self.B, self.K_total, self.K_max, self.T,
+                                                   ctypes.byref(self.win), self.prec)
+        if nbytes == 0:
+            raise FcfsError(E_INVALID, "fcfs_batched_workspace_bytes")
+        self.ws = _ws(nbytes, device)
+        self.per_clip = window_size(M, N, r2, layout)
+        self.out = torch.empty(self.B * self.per_clip, dtype=_out_dtype(prec), device=device)
+
+    def run(self, corner_ptr, x, y, w, area, stream=None, out=None):
+        out = self.out if out is None else out
+        st = _lib.fcfs_coeffs_batched(_ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y),
+                                      _ptr(w), _ptr(area), self.T, ctypes.byref(self.win), self.prec, _ptr(out),
+                                      _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_coeffs_batched")
+        return out.view(self.B, self.per_clip)
+
+
+def coeffs_batched(corner_ptr, x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", K_max=None,
+                   stream=None):
+    B = corner_ptr.shape[0] - 1
+    if K_max is None:
+        K_max = int((corner_ptr[1:] - corner_ptr[:-1]).max().item()) if B > 0 else 0
+    plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device)
+    return plan.run(corner_ptr, x, y, w, area, stream=stream)

@@ -1,0 +1,82 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the header
+declares, struct layouts match, and the host helpers agree with the oracle's window
+enumeration.  No compute entry point is called here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1010_5562_b200 import inputs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fcfs.h")
+
+
+@pytest.fixture(scope="module")
+def fcfs():
+    from paper_1010_5562_b200 import build
+    build.build()
+    from paper_1010_5562_b200 import fcfs as f
+    return f
+
+
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fcfs_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(fcfs):
+    declared = _declared_functions()
+    assert len(declared) >= 12
+    lib = ctypes.CDLL(fcfs.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/fcfs.h but not exported"
+    assert sorted(fcfs.EXPORTED) == declared
+
+
+def test_library_is_sm100a_only(fcfs):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", fcfs.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_struct_layouts(fcfs):
+    assert ctypes.sizeof(fcfs.Window) == 24 and fcfs.Window.pupil_r2.offset == 8 and fcfs.Window.layout.offset == 16
+    assert ctypes.sizeof(fcfs.Shard) == 32 and fcfs.Shard.k_lo.offset == 16 and fcfs.Shard.k_hi.offset == 24
+
+
+def test_window_helpers_match_oracle(fcfs):
+    r2 = inputs.pupil_r2(2048)
+    assert fcfs.window_size(27, 27, r2, "pupil") == 2337
+    assert fcfs.window_size(32, 32) == 65 * 65
+    assert fcfs.window_size(3, 5, 10.0, "dense") == 7 * 11
+    ms, ns = fcfs.pupil_indices(27, 27, r2)
+    oms, ons = oracle.window(27, 27, r2)
+    assert np.array_equal(ms.numpy(), oms) and np.array_equal(ns.numpy(), ons)
+    ms, ns = fcfs.pupil_indices(5, 3, 9.0)
+    oms, ons = oracle.window(5, 3, 9.0)
+    assert np.array_equal(ms.numpy(), oms) and np.array_equal(ns.numpy(), ons)
+    with pytest.raises(fcfs.FcfsError):
+        fcfs.window_size(3, 3, -1.0, "pupil")
+
+
+def test_status_strings_and_no_gpu_behaviour(fcfs):
+    assert fcfs._lib.fcfs_status_string(0) == b"FCFS_OK"
+    assert fcfs._lib.fcfs_status_string(5) == b"FCFS_E_UNSUPPORTED"
+    import torch
+    if not torch.cuda.is_available():
+        st = fcfs._lib.fcfs_device_check()
+        assert st != 0                      # fails loudly without an sm_100 device
+
+
+def test_workspace_queries_are_positive(fcfs):
+    w = fcfs.make_window(512, 512)
+    assert fcfs._lib.fcfs_coeffs_workspace_bytes(1_000_000, 65536, ctypes.byref(w), 0, None) > 0
+    assert fcfs._lib.fcfs_vertices_workspace_bytes(250_000, 250_000, 1, 1) > 250_000 * 4 * 8
+    wp = fcfs.make_window(27, 27, inputs.pupil_r2(2048), "pupil")
+    assert fcfs._lib.fcfs_batched_workspace_bytes(4096, 4096 * 4800, 5000, 2048, ctypes.byref(wp), 1) > 0

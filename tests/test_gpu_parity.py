@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, on the same
+seeded inputs.  Tolerances (BASELINE.json north_star):
+  extraction (x, y, w, corner_ptr, area): bit-exact
+  F[0,0]: exact
+  FP64:   |F_gpu - F_ref| <= 1e-12 * B[m,n]
+  TF32X3: |F_gpu - F_ref| <= 1e-5  * B[m,n]
+where B[m,n] = sum_k |term_k| is the oracle's per-coefficient L1 bound."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1010_5562_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp64": 1e-12, "tf32x3": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def fcfs():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1010_5562_b200 import fcfs as f
+    f.device_check()
+    return f
+
+
+def _dev(a, dtype):
+    return None if a is None else torch.as_tensor(np.asarray(a), dtype=dtype).cuda()
+
+
+def _gpu_extract(fcfs, wl):
+    return fcfs.vertices_from_rects(_dev(wl.rects, torch.int32), wl.T, _dev(wl.group_ptr, torch.int64),
+                                    _dev(wl.clip_ptr, torch.int64))
+
+
+def _assert_extract_equal(g, e):
+    assert g["K"] == e["K"]
+    assert np.array_equal(g["x"].cpu().numpy(), e["x"])
+    assert np.array_equal(g["y"].cpu().numpy(), e["y"])
+    assert np.array_equal(g["w"].cpu().numpy(), e["w"])
+    assert np.array_equal(g["corner_ptr"].cpu().numpy(), e["corner_ptr"])
+    assert np.array_equal(g["area"].cpu().numpy(), e["area"])
+
+
+def _assert_parity(F, Fref, B, prec, what, ms=None, ns=None):
+    F = np.asarray(F, np.complex128)
+    err = np.abs(F - Fref)
+    tol = TOL[prec]
+    bad = err > tol * B
+    if ms is not None:
+        dc = (ms == 0) & (ns == 0)
+        if prec == "fp64":
+            assert np.array_equal(F[dc], Fref[dc]), f"{what}: DC not exact"
+        else:
+            assert np.all(np.abs(F[dc] - Fref[dc]) <= 1e-7 * np.abs(Fref[dc]) + 1e-30), f"{what}: DC"
+        bad &= ~dc
+    if bad.any():
+        i = int(np.argmax(np.where(B > 0, err / np.maximum(B, 1e-300), 0)))
+        raise AssertionError(f"{what}: {bad.sum()} of {len(F)} outside {tol}*B; worst err/B = "
+                             f"{err[i] / B[i]:.3e} at index {i}")
+
+
+# ------------------------------------------------------------------ a1: extraction, bit-exact
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3x64", "c4", "c5"])
+def test_extraction_bit_exact(fcfs, cfg):
+    wl = inputs.c3(clips=64) if cfg == "c3x64" else inputs.make(cfg)
+    e = oracle.extract(wl.rects, wl.T, wl.group_ptr, wl.clip_ptr)
+    g = _gpu_extract(fcfs, wl)
+    _assert_extract_equal(g, e)
+
+
+def test_extraction_edge_cases(fcfs):
+    # empty clip among non-empty ones; touching T; pinch (|w| = 2); duplicate rects summed across groups
+    rects = np.array([[0, 0, 8, 8], [5, 5, 8, 8], [1, 1, 2, 2], [2, 2, 3, 3], [3, 3, 5, 5], [3, 3, 5, 5]], np.int32)
+    gp = np.array([0, 2, 4, 5, 6], np.int64)       # groups: {0,1} union, {2,3} pinch, {4}, {5}
+    cp = np.array([0, 1, 1, 4], np.int64)          # clip 1 is empty
+    e = oracle.extract(rects, 8, gp, cp)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), 8, _dev(gp, torch.int64), _dev(cp, torch.int64))
+    _assert_extract_equal(g, e)
+    assert 2 in np.abs(g["w"].cpu().numpy())
+    # no rects at all
+    g = fcfs.vertices_from_rects(torch.zeros((0, 4), dtype=torch.int32, device="cuda"), 16)
+    assert g["K"] == 0 and g["area"].item() == 0
+    # invalid rect -> E_RANGE
+    with pytest.raises(fcfs.FcfsError) as ei:
+        fcfs.vertices_from_rects(_dev(np.array([[2, 0, 2, 5]]), torch.int32), 8)
+    assert ei.value.status == fcfs.E_RANGE
+    with pytest.raises(fcfs.FcfsError) as ei:
+        fcfs.vertices_from_rects(_dev(np.array([[2, 0, 9, 5]]), torch.int32), 8)
+    assert ei.value.status == fcfs.E_RANGE
+
+
+# ------------------------------------------------------------------ a2-a5: one clip, full window
+
+def _clip_coeffs(fcfs, wl, prec, M=None, N=None, r2=None, layout="dense", shard=None):
+    g = _gpu_extract(fcfs, wl)
+    M = wl.M if M is None else M
+    N = wl.N if N is None else N
+    r2 = wl.r2 if r2 is None else r2
+    F = fcfs.coeffs(g["x"], g["y"], g["w"], int(g["area"][0].item()), wl.T, M, N, r2, layout, prec, shard)
+    torch.cuda.synchronize()
+    return g, F.cpu().numpy()
+
+
+def _oracle_window(g, T, M, N, r2=-1.0, layout="dense"):
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = int(g["area"][0].item())
+    ms, ns = oracle.window(M, N, r2 if layout == "pupil" else -1.0)
+    F, B = oracle.coeffs(x, y, w, area, T, ms, ns)
+    if layout == "dense" and r2 >= 0:
+        out = (ms.astype(np.float64) ** 2 + ns.astype(np.float64) ** 2) > r2
+        F[out] = 0
+        B[out] = 0
+    return ms, ns, F, B
+
+
+@pytest.mark.parametrize("cfg,prec", [("c1", "fp64"), ("c2", "fp64")])
+def test_full_window_parity(fcfs, cfg, prec):
+    wl = inputs.make(cfg)
+    g, F = _clip_coeffs(fcfs, wl, prec)
+    ms, ns, Fr, B = _oracle_window(g, wl.T, wl.M, wl.N)
+    _assert_parity(F, Fr, B, prec, f"{cfg}/{prec}", ms, ns)
+    # exact mirror: F[-m,-n] == conj F[m,n] bitwise
+    Fm = F[::-1]
+    assert np.array_equal(Fm.real, F.real) and np.array_equal(Fm.imag, -F.imag)
+
+
+@pytest.mark.parametrize("prec", ["fp64"])
+def test_ragged_sizes_and_tiny_windows(fcfs, prec):
+    # several tiles along both sides with ragged tails, non-power-of-two T, M != N, M = 0 / N = 0
+    wl = inputs.c2(seed=7, n_poly=150, T=3000)
+    for (M, N) in [(40, 23), (0, 5), (7, 0), (0, 0), (33, 31)]:
+        g, F = _clip_coeffs(fcfs, wl, prec, M=M, N=N, r2=-1.0)
+        ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
+        _assert_parity(F, Fr, B, prec, f"M={M} N={N}", ms, ns)
+
+
+def test_pupil_layouts_single_clip(fcfs):
+    wl = inputs.c1(seed=1)
+    r2 = 300.5
+    for layout in ("pupil", "dense"):
+        g, F = _clip_coeffs(fcfs, wl, "fp64", M=20, N=18, r2=r2, layout=layout)
+        ms, ns, Fr, B = _oracle_window(g, wl.T, 20, 18, r2, layout)
+        _assert_parity(F, Fr, B, "fp64", f"pupil/{layout}", ms, ns)
+
+
+def test_empty_corner_list(fcfs):
+    x = torch.zeros(0, dtype=torch.int32, device="cuda")
+    F = fcfs.coeffs(x, x, x, 0, 64, 3, 3)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(F).item() == 0
+
+
+# ------------------------------------------------------------------ a6 building blocks: shards on one GPU
+
+def test_row_shards_concatenate_to_full(fcfs):
+    wl = inputs.c2(seed=3, n_poly=400)
+    g = _gpu_extract(fcfs, wl)
+    area = int(g["area"][0].item())
+    M = N = 40
+    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N).cpu().numpy()
+    parts = []
+    for lo, hi in [(-40, -14), (-13, -1), (0, 0), (1, 9), (10, 40)]:
+        sh = fcfs.Shard(fcfs.SHARD_ROWS, lo, hi, 0, 0)
+        parts.append(fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N, shard=sh).cpu().numpy())
+    cat = np.concatenate(parts)
+    ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
+    _assert_parity(cat, Fr, B, "fp64", "row shards", ms, ns)
+    _assert_parity(full, Fr, B, "fp64", "full", ms, ns)
+
+
+def test_vertex_blocks_sum_to_full(fcfs):
+    wl = inputs.c2(seed=4, n_poly=600)
+    g = _gpu_extract(fcfs, wl)
+    K = g["K"]
+    M = N = 24
+    cuts = [0, K // 3, K // 2, K - 5, K]
+    acc = None
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sh = fcfs.Shard(fcfs.SHARD_VERTEX_BLOCK, 0, 0, a, b)
+        Fb = fcfs.coeffs(g["x"], g["y"], g["w"], 0, wl.T, M, N, shard=sh).cpu().numpy()
+        acc = Fb if acc is None else acc + Fb
+    ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
+    _assert_parity(acc, Fr, B, "fp64", "vertex blocks", None, None)
+    dc = (ms == 0) & (ns == 0)
+    assert acc[dc][0] == Fr[dc][0]
+
+
+# ------------------------------------------------------------------ batched clips (a5)
+
+@pytest.mark.parametrize("prec", ["fp64"])
+def test_batched_pupil_clips(fcfs, prec):
+    wl = inputs.c3(clips=24)
+    g = _gpu_extract(fcfs, wl)
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], wl.T, wl.M, wl.N, wl.r2,
+                            "pupil", prec).cpu().numpy()
+    ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    cp = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for b in (0, 7, 23):
+        sl = slice(cp[b], cp[b + 1])
+        Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], wl.T, ms, ns)
+        _assert_parity(F[b], Fr, B, prec, f"clip {b}", ms, ns)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled outputs
+
+def _sample_indices(M, N, n_rand=384, seed=0):
+    """all axis + DC entries, the lowest |f| block, and seeded random (m, n)."""
+    rng = np.random.default_rng(seed)
+    pts = set()
+    for m in range(-M, M + 1):
+        pts.add((m, 0))
+    for n in range(-N, N + 1):
+        pts.add((0, n))
+    for m in range(-4, 5):
+        for n in range(-4, 5):
+            pts.add((m, n))
+    for _ in range(n_rand):
+        pts.add((int(rng.integers(-M, M + 1)), int(rng.integers(-N, N + 1))))
+    pts = sorted(pts)
+    return np.array([p[0] for p in pts], np.int32), np.array([p[1] for p in pts], np.int32)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_sampled_fp64(fcfs, cfg):
+    wl = inputs.make(cfg)
+    g, F = _clip_coeffs(fcfs, wl, "fp64")
+    ms, ns = _sample_indices(wl.M, wl.N, n_rand=128 if cfg == "c5" else 256)
+    idx = (ms + wl.M) * (2 * wl.N + 1) + (ns + wl.N)
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    Fr, B = oracle.coeffs(x, y, w, int(g["area"][0].item()), wl.T, ms, ns)
+    _assert_parity(F[idx], Fr, B, "fp64", f"{cfg} sampled", ms, ns)
+    # properties that hold at any size: exact mirror
+    assert np.array_equal(F[::-1].real, F.real) and np.array_equal(F[::-1].imag, -F.imag)
