@@ -71,7 +71,15 @@ struct GemmPlan {
     int32_t tiles_x, tiles_y, splits;
     int64_t B;                // clips
     int64_t items;            // B * tiles_x * tiles_y * splits
+    int32_t phys;             // P_ws row order inside a 64-row tile: 0 = (c0,s0,c1,s1,...) [FP64 kernel],
+                              // 1 = (c0..c31, s0..s31) [tcgen05 kernel]
 };
+
+// physical row of logical quadrant row (pair p, t = 0 cos / 1 sin) inside P_ws
+__host__ __device__ inline int phys_row(int p, int t, int phys) {
+    const int tile = p / (kTile / 2), pp = p - tile * (kTile / 2);
+    return tile * kTile + (phys ? pp + (kTile / 2) * t : 2 * pp + t);
+}
 
 // Corner source of one contraction: either one clip [k_lo, k_hi) or B clips by CSR.
 struct CornerSrc {

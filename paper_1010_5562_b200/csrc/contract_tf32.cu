@@ -1,17 +1,451 @@
-// contract_tf32.cu — a3 (split-TF32 tcgen05 path).  Placeholder until the tensor-core
-// kernel lands: reports FCFS_E_UNSUPPORTED rather than silently computing elsewhere.
+// contract_tf32.cu — a2 + a3 (split-TF32): the quadrant GEMM P = A diag(w) B^T on the
+// 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators in TMEM).
+//
+// Same product as contract_fp64.cu (Eq. Fkl P:843-846 / Steps 2-4 P:870-904, evaluated
+// directly as in P:917-920), FP32-accurate:
+//   * every generated operand value v (w*cos, w*sin, axis weight) is split v = hi + lo with
+//     hi = tf32(v), lo = tf32(v - hi); the operand tile stacks [hi rows; lo rows] (128 rows),
+//     so ONE M=128 x N=128 x K=8 MMA yields hi*hi, hi*lo, lo*hi (and lo*lo) for a 64x64 tile;
+//   * FP32 TMEM partials are flushed into FP64 registers every kChunk corners (hierarchical
+//     accumulation), double-buffered in TMEM so the flush overlaps the MMAs.
+//
+// a2 is fused: producer warps reduce the phase (f * v) mod T exactly in integers (lattice
+// vertices), look up e^{i 2 pi r/T} in an SMEM table and write the split operand
+// tiles straight into the canonical no-swizzle K-major UMMA layout; the twiddle matrices
+// never exist in HBM ("no full-length arrays").
+//
+// Warp roles (416 threads, 1 CTA per SM, persistent over work items):
+//   warps 0-3   epilogue: tcgen05.ld TMEM -> registers, combine 4 quadrant blocks, FP64 flush,
+//               write the item's 64x64 FP64 P tile (phys layout 1: c0..c31, s0..s31)
+//   warps 4-11  producers: twiddle generation into a 4-stage SMEM ring (mbarrier full/empty)
+//   warp 12     TMEM allocator + single-thread MMA issuer (tcgen05.mma / tcgen05.commit)
 #include "common.cuh"
 
 namespace fcfs {
+namespace tc {
 
-fcfs_status tf32_supported(const GemmPlan &, int32_t) {
-    set_error("FCFS_TF32X3 is not built yet");
-    return FCFS_E_UNSUPPORTED;
+constexpr int kBK = 32;                         // corners per stage (K of 4 MMAs)
+constexpr int kStages = 4;
+constexpr int kRows = 128;                      // operand rows: 64 hi + 64 lo
+constexpr int kRowBytes = kBK * 4;              // one operand row of a stage = one SW128 atom row
+constexpr int kOpBytes = kRows * kBK * 4;       // 16 KB per operand per stage
+constexpr int kStageBytes = 2 * kOpBytes;       // A + B
+constexpr int kChunk = 1024;                    // corners per TMEM accumulation (FP64 flush)
+constexpr int kEpiWarps = 4, kProdWarps = 8;
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kThreads = (kEpiWarps + kProdWarps + 1) * 32;
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+constexpr int kTmemCols = 256;                  // 2 accumulators x 128 fp32 columns
+constexpr int kXStride = 33;                    // exchange buffer row stride (floats)
+constexpr int kSingleTableMax = 8192;           // T <= this: one-level table of T entries
+// instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                            ((uint32_t)(128 >> 4) << 24);
+
+struct Smem {
+    // offsets from the 1024-aligned dynamic smem base
+    uint32_t stage0, table, xbuf, bars;
+    uint32_t total;
+};
+
+__host__ __device__ inline Smem smem_layout(int table_entries) {
+    Smem s;
+    s.stage0 = 0;
+    s.table = kStages * kStageBytes;
+    s.xbuf = s.table + ((table_entries * 8 + 1023) & ~1023);
+    s.bars = s.xbuf + 2 * 2 * 64 * kXStride * 4;
+    s.total = s.bars + 256;
+    return s;
 }
 
-fcfs_status launch_gemm_tf32(const CornerSrc &, const GemmPlan &, int32_t, double *, cudaStream_t) {
-    set_error("FCFS_TF32X3 is not built yet");
-    return FCFS_E_UNSUPPORTED;
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// bounded spin: a protocol bug traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try(bar, parity)) {
+        if (++n > (1u << 26)) __trap();
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ uint32_t tf32_rna(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return r;
+}
+
+// canonical K-major SWIZZLE_128B UMMA smem descriptor: rows of 128 B (32 tf32 corners), 8-row
+// atoms of 1024 B (SBO); inside an atom the 16-byte chunk c of row r sits at chunk c ^ (r % 8).
+// byte offset of (row r, corner k) = (r/8) 1024 + (r%8) 128 + (((k/4) ^ (r%8)) 16) + (k%4) 4.
+// The K step of one MMA (8 tf32 = 32 B) advances the start address by 32 B inside the atom.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;                          // LBO: unused for swizzled K-major
+    d |= (uint64_t)((1024 >> 4) & 0x3FFFu) << 32;    // SBO: 8-row atom stride
+    d |= (uint64_t)1 << 46;                          // descriptor version for sm_100
+    d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                  \
+    asm volatile(                                                                                            \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),             \
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),           \
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),           \
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                                \
+        : "r"(taddr))
+#define TMEM_LD16(taddr, r)                                                                                  \
+    asm volatile(                                                                                            \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),             \
+          "=r"(r[15])                                                                                          \
+        : "r"(taddr))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct ItemInfo {
+    int64_t k0, k1;
+    int tix, tiy;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const CornerSrc &src, const GemmPlan &plan, int64_t item) {
+    const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
+    const int64_t clip = item / per_clip;
+    int64_t rem = item - clip * per_clip;
+    ItemInfo it;
+    it.tix = (int)(rem / ((int64_t)plan.tiles_y * plan.splits));
+    rem -= (int64_t)it.tix * plan.tiles_y * plan.splits;
+    it.tiy = (int)(rem / plan.splits);
+    const int split = (int)(rem - (int64_t)it.tiy * plan.splits);
+    int64_t kb, ke;
+    if (src.corner_ptr) { kb = src.corner_ptr[clip]; ke = src.corner_ptr[clip + 1]; }
+    else { kb = src.k_lo; ke = src.k_hi; }
+    const int64_t span = ke - kb;
+    it.k0 = kb + span * split / plan.splits;
+    it.k1 = kb + span * (split + 1) / plan.splits;
+    return it;
+}
+
+struct TabGeom {
+    int32_t T, single, lbits, nhi, pow2;
+};
+
+// (cos, sin)(2 pi r / T) in fp32
+__device__ __forceinline__ float2 twiddle(uint32_t r, const TabGeom &g, const float2 *tab) {
+    if (g.single) return tab[r];
+    float2 a = tab[r >> g.lbits];
+    float2 b = tab[g.nhi + (r & ((1u << g.lbits) - 1))];
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.y, b.x, a.x * b.y));
+}
+
+__device__ __forceinline__ uint32_t phase(uint32_t f, uint32_t v, const TabGeom &g) {
+    if (g.pow2) return (f * v) & (uint32_t)(g.T - 1);
+    return (uint32_t)(((uint64_t)f * v) % (uint64_t)g.T);
+}
+
+// hi/lo split for the tensor core: hi keeps the top 10 mantissa bits (exact bit mask), lo = v - hi
+// is exact in fp32 and is read by the MMA as tf32 (|lo| <= 2^-10 |v|: relative error <= 2^-20).
+__device__ __forceinline__ void split(float v, float &hi, float &lo) {
+    hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    lo = v - hi;
+}
+
+// One producer task: 4 consecutive corners (chunk `quad` of the stage) x 8 consecutive pair
+// slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup for
+// the first frequency, pre-multiplied by the corner weight, and the angle-addition recurrence
+// E(f+1) = E(f) E(1) for the other 7; the split hi/lo values go straight into the SW128
+// K-major operand tile: rows j0+i (cos hi), 32+j0+i (sin hi), 64+j0+i (cos lo), 96+j0+i (sin lo).
+__device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
+                                        const int32_t v[4], const float wt[4], const TabGeom &g,
+                                        const float2 *tab) {
+    const uint32_t f0 = (uint32_t)(sp.f0 + p0);
+    float2 e[4], e1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float2 a = twiddle(phase(f0, (uint32_t)v[q], g), g, tab);
+        e[q] = make_float2(wt[q] * a.x, wt[q] * a.y);
+        e1[q] = twiddle(phase(1u, (uint32_t)v[q], g), g, tab);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int p = p0 + i;
+        float c[4], s[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c[q] = e[q].x;
+            s[q] = e[q].y;
+            if (p >= sp.nf) {
+                c[q] = (p == sp.nf && sp.axis) ? wt[q] * (float)v[q] : 0.f;
+                s[q] = 0.f;
+            }
+            const float nx = fmaf(e[q].x, e1[q].x, -e[q].y * e1[q].y);
+            const float ny = fmaf(e[q].y, e1[q].x, e[q].x * e1[q].y);
+            e[q] = make_float2(nx, ny);
+        }
+        float ch[4], cl[4], sh[4], sl[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { split(c[q], ch[q], cl[q]); split(s[q], sh[q], sl[q]); }
+        const int r = j0 + i;                                   // r % 8 == i
+        uint8_t *base = op + (r >> 3) * 1024 + i * kRowBytes + ((quad ^ i) << 4);
+        *(float4 *)(base) = make_float4(ch[0], ch[1], ch[2], ch[3]);              // row r
+        *(float4 *)(base + 4 * 1024) = make_float4(sh[0], sh[1], sh[2], sh[3]);   // row 32 + r
+        *(float4 *)(base + 8 * 1024) = make_float4(cl[0], cl[1], cl[2], cl[3]);   // row 64 + r
+        *(float4 *)(base + 12 * 1024) = make_float4(sl[0], sl[1], sl[2], sl[3]);  // row 96 + r
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
+    const Smem L = smem_layout(tab_entries);
+    float2 *tab = (float2 *)(smem + L.table);
+    float *xbuf = (float *)(smem + L.xbuf);
+    uint64_t *bars = (uint64_t *)(smem + L.bars);
+    // barrier indices: full[0..S), empty[S..2S), tfull[2S..2S+2), tempty[2S+2..2S+4)
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
+    const uint32_t bar0 = su32(bars);
+    auto FULL = [&](int s) { return bar0 + 8u * s; };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
+    auto TFULL = [&](int b) { return bar0 + 8u * (2 * kStages + b); };
+    auto TEMPTY = [&](int b) { return bar0 + 8u * (2 * kStages + 2 + b); };
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+
+    // twiddle table (all threads), barriers (thread 0), TMEM (MMA warp)
+    for (int i = tid; i < tab_entries; i += kThreads) {
+        double sn, cs;
+        if (g.single) sincospi(2.0 * (double)i / (double)g.T, &sn, &cs);
+        else if (i < g.nhi) sincospi(2.0 * (double)((int64_t)i << g.lbits) / (double)g.T, &sn, &cs);
+        else sincospi(2.0 * (double)(i - g.nhi) / (double)g.T, &sn, &cs);
+        tab[i] = make_float2((float)cs, (float)sn);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) { mbar_init(FULL(s), kProdThreads / kStages); mbar_init(EMPTY(s), 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(TFULL(b), 1); mbar_init(TEMPTY(b), kEpiWarps * 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp >= kEpiWarps && warp < kMmaWarp) {
+        // ============================== producers ==============================
+        // 4 groups of 64 threads; group gq produces every 4th stage, always into ring slot gq.
+        // In a group: side = A (threads 0-31) or B (32-63); lane -> (corner quad, slot block).
+        const int pt = tid - kEpiWarps * 32;
+        const int gq = pt >> 6;
+        const int sideB = (pt >> 5) & 1;
+        const int l = pt & 31;
+        const int quad = l & 7, j0 = (l >> 3) << 3;
+        const SidePlan sp = sideB ? plan.Y : plan.X;
+        const int32_t *vsrc = sideB ? src.y : src.x;
+        uint32_t sc = 0;                                  // global stage counter
+        for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
+            const ItemInfo it = item_info(src, plan, item);
+            const int p0 = (sideB ? it.tiy : it.tix) * 32 + j0;
+            for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
+                const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
+                for (int64_t ks = c0; ks < c1; ks += kBK, ++sc) {
+                    if ((int)(sc & 3) != gq) continue;
+                    int32_t v[4];
+                    float wt[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int64_t k = ks + 4 * quad + q;
+                        const bool ok = k < c1;
+                        v[q] = ok ? __ldg(vsrc + k) : 0;
+                        wt[q] = ok ? (sideB ? 1.f : (float)__ldg(src.w + k)) : 0.f;
+                    }
+                    mbar_wait(EMPTY(gq), ((sc >> 2) & 1) ^ 1);
+                    uint8_t *op = smem + L.stage0 + gq * kStageBytes + sideB * kOpBytes;
+                    produce(op, quad, j0, p0, sp, v, wt, g, tab);
+                    fence_proxy_async();
+                    mbar_arrive(FULL(gq));
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ============================== MMA issuer ==============================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase_bit = 0;
+            uint32_t chunk_ctr = 0;
+            const uint32_t smem_base = su32(smem + L.stage0);
+            for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
+                const ItemInfo it = item_info(src, plan, item);
+                for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
+                    const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
+                    const uint32_t b = chunk_ctr & 1;
+                    mbar_wait(TEMPTY(b), ((chunk_ctr >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + b * 128;
+                    uint32_t acc = 0;
+                    for (int64_t ks = c0; ks < c1; ks += kBK) {
+                        mbar_wait(FULL(stage), phase_bit);
+                        tc_fence_after();
+                        const uint32_t a_addr = smem_base + stage * kStageBytes;
+                        const uint32_t b_addr = a_addr + kOpBytes;
+#pragma unroll
+                        for (int u = 0; u < kBK / 8; ++u) {
+                            umma_tf32(d_tmem, umma_desc(a_addr + u * 32), umma_desc(b_addr + u * 32), acc);
+                            acc = 1;
+                        }
+                        umma_commit(EMPTY(stage));
+                        if (++stage == kStages) { stage = 0; phase_bit ^= 1; }
+                    }
+                    umma_commit(TFULL(b));
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ============================== epilogue ==============================
+        const int L_ = tid;                          // TMEM lane = D row
+        const int hi_row = L_ < 64;
+        const int r = hi_row ? L_ : L_ - 64;         // physical P row in the 64-row tile
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        uint32_t chunk_ctr = 0;
+        for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
+            const ItemInfo it = item_info(src, plan, item);
+            double acc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+            for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
+                const uint32_t b = chunk_ctr & 1;
+                mbar_wait(TFULL(b), (chunk_ctr >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tb = tmem_base + lane_base + b * 128;
+                // D[L][c] + D[L][64+c] for the 32 columns this row keeps and the 32 it sends
+                float *xb = xbuf + (chunk_ctr & 1) * (2 * 64 * kXStride);
+                float *XH = xb, *XL = xb + 64 * kXStride;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = 16 * q;          // columns col..col+15 (send half for q >= 2 if hi row)
+                    uint32_t ra[16], rb[16];
+                    TMEM_LD16(tb + col, ra);
+                    TMEM_LD16(tb + 64 + col, rb);
+                    tmem_wait_ld();
+                    const bool keep = hi_row ? (q < 2) : (q >= 2);
+                    float *xdst = hi_row ? XH : XL;
+                    const int o = (q & 1) * 16;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float v = __uint_as_float(ra[i]) + __uint_as_float(rb[i]);
+                        if (keep) acc[o + i] += (double)v;
+                        else xdst[r * kXStride + o + i] = v;
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(TEMPTY(b));
+                named_bar(1, kEpiWarps * 32);
+                {
+                    const float *xsrc = hi_row ? XL : XH;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] += (double)xsrc[r * kXStride + i];
+                }
+            }
+            double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+}  // namespace tc
+
+static tc::TabGeom make_tab(int32_t T) {
+    tc::TabGeom g;
+    g.T = T;
+    g.pow2 = (T & (T - 1)) == 0;
+    g.single = T <= tc::kSingleTableMax ? 1 : 0;
+    int tb = ilog2_ceil(T);
+    g.lbits = (tb + 1) / 2;
+    g.nhi = (int32_t)((T + (1 << g.lbits) - 1) >> g.lbits);
+    return g;
+}
+
+fcfs_status tf32_supported(const GemmPlan &plan, int32_t T) {
+    (void)plan;
+    if (T > (1 << 20)) {
+        set_error("TF32X3: T=%d too large", T);
+        return FCFS_E_UNSUPPORTED;
+    }
+    return FCFS_OK;
+}
+
+fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
+                             cudaStream_t s) {
+    if (plan.items <= 0) return FCFS_OK;
+    tc::TabGeom g = make_tab(T);
+    const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
+    const tc::Smem L = tc::smem_layout(entries);
+    const size_t smem = L.total + 1024;
+    static size_t attr = 0;
+    if (smem > attr) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = plan.items < sms ? plan.items : sms;
+    tc::k_gemm_tf32<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws);
+    FCFS_CHECK_LAUNCH("k_gemm_tf32");
+    return FCFS_OK;
 }
 
 }  // namespace fcfs

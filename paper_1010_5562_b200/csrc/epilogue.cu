@@ -15,7 +15,10 @@
 
 namespace fcfs {
 
-__device__ __forceinline__ double getP(const double *P_ws, const GemmPlan &pl, int64_t clip, int ix, int iy) {
+// P at logical quadrant rows (px, tx) x (py, ty): pair index p, t = 0 cos / 1 sin (axis: p = nf, t = 0)
+__device__ __forceinline__ double getP(const double *P_ws, const GemmPlan &pl, int64_t clip, int px, int tx, int py,
+                                       int ty) {
+    const int ix = phys_row(px, tx, pl.phys), iy = phys_row(py, ty, pl.phys);
     const int tix = ix / kTile, tiy = iy / kTile;
     const int64_t base = ((clip * pl.tiles_x + tix) * pl.tiles_y + tiy) * pl.splits;
     const int64_t off = (int64_t)(ix - tix * kTile) * kTile + (iy - tiy * kTile);
@@ -42,20 +45,20 @@ __device__ double2 coeff(const double *P_ws, const GemmPlan &pl, const EpiArgs &
     if (neg) { m = -m; n = -n; }
     double re, im;
     if (n == 0) {
-        const int ic = 2 * (m - pl.X.f0), ia = 2 * pl.Y.nf;
-        double sre = getP(P_ws, pl, clip, ic, ia), sim = -getP(P_ws, pl, clip, ic + 1, ia);
+        const int pm = m - pl.X.f0, pa = pl.Y.nf;
+        double sre = getP(P_ws, pl, clip, pm, 0, pa, 0), sim = -getP(P_ws, pl, clip, pm, 1, pa, 0);
         double d = 2.0 * pi * (double)m * (double)ea.T;
         re = -sim / d; im = sre / d;
     } else if (m == 0) {
-        const int ia = 2 * pl.X.nf, jc = 2 * (n - pl.Y.f0);
-        double sre = getP(P_ws, pl, clip, ia, jc), sim = -getP(P_ws, pl, clip, ia, jc + 1);
+        const int pa = pl.X.nf, pn = n - pl.Y.f0;
+        double sre = getP(P_ws, pl, clip, pa, 0, pn, 0), sim = -getP(P_ws, pl, clip, pa, 0, pn, 1);
         double d = 2.0 * pi * (double)n * (double)ea.T;
         re = -sim / d; im = sre / d;
     } else {
         const int an = n < 0 ? -n : n;
-        const int ic = 2 * (m - pl.X.f0), jc = 2 * (an - pl.Y.f0);
-        double pcc = getP(P_ws, pl, clip, ic, jc), pcs = getP(P_ws, pl, clip, ic, jc + 1);
-        double psc = getP(P_ws, pl, clip, ic + 1, jc), pss = getP(P_ws, pl, clip, ic + 1, jc + 1);
+        const int pm = m - pl.X.f0, pn = an - pl.Y.f0;
+        double pcc = getP(P_ws, pl, clip, pm, 0, pn, 0), pcs = getP(P_ws, pl, clip, pm, 0, pn, 1);
+        double psc = getP(P_ws, pl, clip, pm, 1, pn, 0), pss = getP(P_ws, pl, clip, pm, 1, pn, 1);
         double sre, sim;
         if (n > 0) { sre = pcc - pss; sim = -(psc + pcs); }
         else { sre = pcc + pss; sim = -(psc - pcs); }

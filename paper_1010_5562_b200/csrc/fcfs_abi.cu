@@ -146,6 +146,7 @@ static GemmPlan make_plan(int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int6
     p.splits = (int32_t)splits;
     p.B = B;
     p.items = B * tiles * splits;
+    p.phys = 0;
     return p;
 }
 
@@ -183,7 +184,7 @@ static fcfs_status run_gemm(const CornerSrc &src, const GemmPlan &plan, int32_t 
     if (prec == FCFS_TF32X3) {
         fcfs_status st = tf32_supported(plan, T);
         if (st != FCFS_OK) return st;
-        return launch_gemm_tf32(src, plan, T, P, s);
+        return launch_gemm_tf32(src, plan, T, P, s);   // writes P in phys layout 1
     }
     set_error("bad precision %d", prec);
     return FCFS_E_INVALID;
@@ -318,6 +319,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     st = device_ok();
     if (st != FCFS_OK) return st;
     GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
+    plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W);
@@ -369,6 +371,7 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     st = device_ok();
     if (st != FCFS_OK) return st;
     GemmPlan plan = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
+    plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W);

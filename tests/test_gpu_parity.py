@@ -117,7 +117,7 @@ def _oracle_window(g, T, M, N, r2=-1.0, layout="dense"):
     return ms, ns, F, B
 
 
-@pytest.mark.parametrize("cfg,prec", [("c1", "fp64"), ("c2", "fp64")])
+@pytest.mark.parametrize("cfg,prec", [("c1", "fp64"), ("c2", "fp64"), ("c1", "tf32x3"), ("c2", "tf32x3")])
 def test_full_window_parity(fcfs, cfg, prec):
     wl = inputs.make(cfg)
     g, F = _clip_coeffs(fcfs, wl, prec)
@@ -128,7 +128,7 @@ def test_full_window_parity(fcfs, cfg, prec):
     assert np.array_equal(Fm.real, F.real) and np.array_equal(Fm.imag, -F.imag)
 
 
-@pytest.mark.parametrize("prec", ["fp64"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
 def test_ragged_sizes_and_tiny_windows(fcfs, prec):
     # several tiles along both sides with ragged tails, non-power-of-two T, M != N, M = 0 / N = 0
     wl = inputs.c2(seed=7, n_poly=150, T=3000)
@@ -138,60 +138,70 @@ def test_ragged_sizes_and_tiny_windows(fcfs, prec):
         _assert_parity(F, Fr, B, prec, f"M={M} N={N}", ms, ns)
 
 
-def test_pupil_layouts_single_clip(fcfs):
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_pupil_layouts_single_clip(fcfs, prec):
     wl = inputs.c1(seed=1)
     r2 = 300.5
     for layout in ("pupil", "dense"):
-        g, F = _clip_coeffs(fcfs, wl, "fp64", M=20, N=18, r2=r2, layout=layout)
+        g, F = _clip_coeffs(fcfs, wl, prec, M=20, N=18, r2=r2, layout=layout)
         ms, ns, Fr, B = _oracle_window(g, wl.T, 20, 18, r2, layout)
-        _assert_parity(F, Fr, B, "fp64", f"pupil/{layout}", ms, ns)
+        _assert_parity(F, Fr, B, prec, f"pupil/{layout}", ms, ns)
 
 
-def test_empty_corner_list(fcfs):
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_empty_corner_list(fcfs, prec):
     x = torch.zeros(0, dtype=torch.int32, device="cuda")
-    F = fcfs.coeffs(x, x, x, 0, 64, 3, 3)
+    F = fcfs.coeffs(x, x, x, 0, 64, 3, 3, prec=prec)
     torch.cuda.synchronize()
     assert torch.count_nonzero(F).item() == 0
 
 
 # ------------------------------------------------------------------ a6 building blocks: shards on one GPU
 
-def test_row_shards_concatenate_to_full(fcfs):
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_row_shards_concatenate_to_full(fcfs, prec):
     wl = inputs.c2(seed=3, n_poly=400)
     g = _gpu_extract(fcfs, wl)
     area = int(g["area"][0].item())
     M = N = 40
-    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N).cpu().numpy()
+    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N, prec=prec).cpu().numpy()
     parts = []
     for lo, hi in [(-40, -14), (-13, -1), (0, 0), (1, 9), (10, 40)]:
         sh = fcfs.Shard(fcfs.SHARD_ROWS, lo, hi, 0, 0)
-        parts.append(fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N, shard=sh).cpu().numpy())
+        parts.append(fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N, prec=prec, shard=sh).cpu().numpy())
     cat = np.concatenate(parts)
     ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
-    _assert_parity(cat, Fr, B, "fp64", "row shards", ms, ns)
-    _assert_parity(full, Fr, B, "fp64", "full", ms, ns)
+    _assert_parity(cat, Fr, B, prec, "row shards", ms, ns)
+    _assert_parity(full, Fr, B, prec, "full", ms, ns)
 
 
-def test_vertex_blocks_sum_to_full(fcfs):
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_vertex_blocks_sum_to_full(fcfs, prec):
     wl = inputs.c2(seed=4, n_poly=600)
     g = _gpu_extract(fcfs, wl)
     K = g["K"]
     M = N = 24
     cuts = [0, K // 3, K // 2, K - 5, K]
     acc = None
+    dc_abs = 0.0
+    ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
+    dc = (ms == 0) & (ns == 0)
     for a, b in zip(cuts[:-1], cuts[1:]):
         sh = fcfs.Shard(fcfs.SHARD_VERTEX_BLOCK, 0, 0, a, b)
-        Fb = fcfs.coeffs(g["x"], g["y"], g["w"], 0, wl.T, M, N, shard=sh).cpu().numpy()
+        Fb = fcfs.coeffs(g["x"], g["y"], g["w"], 0, wl.T, M, N, prec=prec, shard=sh).cpu().numpy()
+        Fb = Fb.astype(np.complex128)
+        dc_abs += abs(Fb[dc][0])
         acc = Fb if acc is None else acc + Fb
-    ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
-    _assert_parity(acc, Fr, B, "fp64", "vertex blocks", None, None)
-    dc = (ms == 0) & (ns == 0)
-    assert acc[dc][0] == Fr[dc][0]
+    _assert_parity(acc[~dc], Fr[~dc], B[~dc], prec, "vertex blocks")
+    if prec == "fp64":
+        assert acc[dc][0] == Fr[dc][0]          # block DCs are exact integers / T^2: the sum is exact
+    else:
+        assert abs(acc[dc][0] - Fr[dc][0]) <= 2 ** -23 * 4 * dc_abs   # complex64 rounding of each block DC
 
 
 # ------------------------------------------------------------------ batched clips (a5)
 
-@pytest.mark.parametrize("prec", ["fp64"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
 def test_batched_pupil_clips(fcfs, prec):
     wl = inputs.c3(clips=24)
     g = _gpu_extract(fcfs, wl)
@@ -226,14 +236,33 @@ def _sample_indices(M, N, n_rand=384, seed=0):
     return np.array([p[0] for p in pts], np.int32), np.array([p[1] for p in pts], np.int32)
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
-def test_full_size_sampled_fp64(fcfs, cfg):
+@pytest.mark.parametrize("cfg,prec", [("c4", "fp64"), ("c5", "fp64"), ("c4", "tf32x3"), ("c5", "tf32x3")])
+def test_full_size_sampled(fcfs, cfg, prec):
     wl = inputs.make(cfg)
-    g, F = _clip_coeffs(fcfs, wl, "fp64")
+    g, F = _clip_coeffs(fcfs, wl, prec)
     ms, ns = _sample_indices(wl.M, wl.N, n_rand=128 if cfg == "c5" else 256)
     idx = (ms + wl.M) * (2 * wl.N + 1) + (ns + wl.N)
     x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
     Fr, B = oracle.coeffs(x, y, w, int(g["area"][0].item()), wl.T, ms, ns)
-    _assert_parity(F[idx], Fr, B, "fp64", f"{cfg} sampled", ms, ns)
+    _assert_parity(F[idx], Fr, B, prec, f"{cfg} sampled", ms, ns)
     # properties that hold at any size: exact mirror
     assert np.array_equal(F[::-1].real, F.real) and np.array_equal(F[::-1].imag, -F.imag)
+
+
+def test_batched_full_c3_sampled_clips(fcfs):
+    """BASELINE configs[2] at full size (4096 clips) in the launch configuration bench.py
+    times (batched, pupil, TF32X3); the oracle checks a seeded sample of clips."""
+    wl = inputs.c3(clips=4096)
+    g = _gpu_extract(fcfs, wl)
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], wl.T, wl.M, wl.N, wl.r2,
+                            "pupil", "tf32x3").cpu().numpy()
+    ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    cp = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    rng = np.random.default_rng(1)
+    for b in sorted(set([0, 4095] + rng.integers(0, 4096, 6).tolist())):
+        sl = slice(cp[b], cp[b + 1])
+        Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], wl.T, ms, ns)
+        _assert_parity(F[b], Fr, B, "tf32x3", f"c3 clip {b}", ms, ns)
+    assert np.all(np.isfinite(F))
