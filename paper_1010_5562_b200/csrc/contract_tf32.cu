@@ -82,6 +82,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (++n > (1u << 26)) __trap();
     }
 }
+// the same for waits that are long by construction (epilogue per chunk): back off with nanosleep
+// so idle warps do not take issue slots from the producers
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(128);
+        if (++n > (1u << 24)) __trap();
+    }
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -165,16 +174,18 @@ struct TabGeom {
     int32_t T, single, lbits, nhi, pow2;
 };
 
-// (cos, sin)(2 pi r / T) in fp32
+// (cos, sin)(2 pi r / T) in fp32.  kFast: one-level table and power-of-two T (compile time).
+template <bool kFast>
 __device__ __forceinline__ float2 twiddle(uint32_t r, const TabGeom &g, const float2 *tab) {
-    if (g.single) return tab[r];
+    if (kFast || g.single) return tab[r];
     float2 a = tab[r >> g.lbits];
     float2 b = tab[g.nhi + (r & ((1u << g.lbits) - 1))];
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.y, b.x, a.x * b.y));
 }
 
+template <bool kFast>
 __device__ __forceinline__ uint32_t phase(uint32_t f, uint32_t v, const TabGeom &g) {
-    if (g.pow2) return (f * v) & (uint32_t)(g.T - 1);
+    if (kFast || g.pow2) return (f * v) & (uint32_t)(g.T - 1);
     return (uint32_t)(((uint64_t)f * v) % (uint64_t)g.T);
 }
 
@@ -185,54 +196,82 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
     lo = v - hi;
 }
 
+__device__ __forceinline__ float2 lo2(float2 v) {   // v - tf32_truncate(v), exact
+    const float2 h = make_float2(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                                 __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+    return __fadd2_rn(v, make_float2(-h.x, -h.y));
+}
+
 // One producer task: 4 consecutive corners (chunk `quad` of the stage) x 8 consecutive pair
 // slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup for
 // the first frequency, pre-multiplied by the corner weight, and the angle-addition recurrence
-// E(f+1) = E(f) E(1) for the other 7; the split hi/lo values go straight into the SW128
-// K-major operand tile: rows j0+i (cos hi), 32+j0+i (sin hi), 64+j0+i (cos lo), 96+j0+i (sin lo).
+// E(f+1) = E(f) E(1) for the other 7, computed on corner pairs with the sm_100 packed FP32x2
+// FMA.  The split values go straight into the SW128 K-major operand tile: rows j0+i (cos hi),
+// 32+j0+i (sin hi), 64+j0+i (cos lo), 96+j0+i (sin lo).  The hi rows store v itself (the tf32
+// MMA reads only its top 19 bits, hi = v & 0xFFFFE000); the lo rows store the exact v - hi.
+// Padding slots (p > nf) keep recurrence values: they only feed P entries nobody reads.  The
+// axis slot (p == nf) is overwritten with the coordinate weight.
+template <bool kFast>
 __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
                                         const int32_t v[4], const float wt[4], const TabGeom &g,
                                         const float2 *tab) {
     const uint32_t f0 = (uint32_t)(sp.f0 + p0);
-    float2 e[4], e1[4];
+    float2 re[2], im[2], c1[2], s1[2], ns1[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const float2 a = twiddle(phase(f0, (uint32_t)v[q], g), g, tab);
-        e[q] = make_float2(wt[q] * a.x, wt[q] * a.y);
-        e1[q] = twiddle(phase(1u, (uint32_t)v[q], g), g, tab);
+    for (int h = 0; h < 2; ++h) {
+        const float2 a0 = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[2 * h], g), g, tab);
+        const float2 a1 = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[2 * h + 1], g), g, tab);
+        const float2 b0 = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[2 * h], g), g, tab);
+        const float2 b1 = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[2 * h + 1], g), g, tab);
+        re[h] = make_float2(wt[2 * h] * a0.x, wt[2 * h + 1] * a1.x);
+        im[h] = make_float2(wt[2 * h] * a0.y, wt[2 * h + 1] * a1.y);
+        c1[h] = make_float2(b0.x, b1.x);
+        s1[h] = make_float2(b0.y, b1.y);
+        ns1[h] = make_float2(-b0.y, -b1.y);
     }
+    uint8_t *opq = op + (j0 >> 3) * 1024;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int p = p0 + i;
-        float c[4], s[4];
+        const float2 rl0 = lo2(re[0]), rl1 = lo2(re[1]), il0 = lo2(im[0]), il1 = lo2(im[1]);
+        uint8_t *base = opq + i * kRowBytes + ((quad ^ i) << 4);   // row j0 + i (r % 8 == i)
+        *(float4 *)(base) = make_float4(re[0].x, re[0].y, re[1].x, re[1].y);
+        *(float4 *)(base + 4 * 1024) = make_float4(im[0].x, im[0].y, im[1].x, im[1].y);
+        *(float4 *)(base + 8 * 1024) = make_float4(rl0.x, rl0.y, rl1.x, rl1.y);
+        *(float4 *)(base + 12 * 1024) = make_float4(il0.x, il0.y, il1.x, il1.y);
+        if (i < 7) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float2 t = __fmul2_rn(im[h], ns1[h]);
+                const float2 u = __fmul2_rn(re[h], s1[h]);
+                re[h] = __ffma2_rn(re[h], c1[h], t);
+                im[h] = __ffma2_rn(im[h], c1[h], u);
+            }
+        }
+    }
+    const int ia = sp.nf - p0;
+    if (sp.axis && ia >= 0 && ia < 8) {
+        float c[4], cl[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            c[q] = e[q].x;
-            s[q] = e[q].y;
-            if (p >= sp.nf) {
-                c[q] = (p == sp.nf && sp.axis) ? wt[q] * (float)v[q] : 0.f;
-                s[q] = 0.f;
-            }
-            const float nx = fmaf(e[q].x, e1[q].x, -e[q].y * e1[q].y);
-            const float ny = fmaf(e[q].y, e1[q].x, e[q].x * e1[q].y);
-            e[q] = make_float2(nx, ny);
+            c[q] = wt[q] * (float)v[q];
+            cl[q] = c[q] - __uint_as_float(__float_as_uint(c[q]) & 0xFFFFE000u);
         }
-        float ch[4], cl[4], sh[4], sl[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { split(c[q], ch[q], cl[q]); split(s[q], sh[q], sl[q]); }
-        const int r = j0 + i;                                   // r % 8 == i
-        uint8_t *base = op + (r >> 3) * 1024 + i * kRowBytes + ((quad ^ i) << 4);
-        *(float4 *)(base) = make_float4(ch[0], ch[1], ch[2], ch[3]);              // row r
-        *(float4 *)(base + 4 * 1024) = make_float4(sh[0], sh[1], sh[2], sh[3]);   // row 32 + r
-        *(float4 *)(base + 8 * 1024) = make_float4(cl[0], cl[1], cl[2], cl[3]);   // row 64 + r
-        *(float4 *)(base + 12 * 1024) = make_float4(sl[0], sl[1], sl[2], sl[3]);  // row 96 + r
+        uint8_t *base = opq + ia * kRowBytes + ((quad ^ ia) << 4);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        *(float4 *)(base) = make_float4(c[0], c[1], c[2], c[3]);
+        *(float4 *)(base + 4 * 1024) = z;
+        *(float4 *)(base + 8 * 1024) = make_float4(cl[0], cl[1], cl[2], cl[3]);
+        *(float4 *)(base + 12 * 1024) = z;
     }
 }
 
+template <bool kFast>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-align by offset arithmetic on the __shared__ array (keeps the shared address space, so
+    // loads / stores compile to LDS / STS rather than generic LD / ST)
+    uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
     const Smem L = smem_layout(tab_entries);
     float2 *tab = (float2 *)(smem + L.table);
@@ -291,20 +330,35 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) 
             const int p0 = (sideB ? it.tiy : it.tix) * 32 + j0;
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
                 const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
+                // this group's first slab in the chunk, and a one-slab-ahead register prefetch;
+                // 32-bit corner offsets relative to the chunk base keep the address math short
+                const int n = (int)(c1 - c0);
+                const int32_t *vp = vsrc + c0;
+                const int32_t *wp = src.w + c0;
+                const int first = (gq - (int)(sc & 3)) & 3;
+                int32_t vn[4], wn[4];
+                auto fetch = [&](int kr0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int kr = kr0 + q;
+                        const bool ok = kr < n;
+                        vn[q] = ok ? __ldg(vp + kr) : 0;
+                        wn[q] = ok ? (sideB ? 1 : __ldg(wp + kr)) : 0;
+                    }
+                };
+                int kr0 = first * kBK + 4 * quad;
+                fetch(kr0);
                 for (int64_t ks = c0; ks < c1; ks += kBK, ++sc) {
                     if ((int)(sc & 3) != gq) continue;
                     int32_t v[4];
                     float wt[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int64_t k = ks + 4 * quad + q;
-                        const bool ok = k < c1;
-                        v[q] = ok ? __ldg(vsrc + k) : 0;
-                        wt[q] = ok ? (sideB ? 1.f : (float)__ldg(src.w + k)) : 0.f;
-                    }
+                    for (int q = 0; q < 4; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
+                    kr0 += 4 * kBK;
+                    fetch(kr0);
                     mbar_wait(EMPTY(gq), ((sc >> 2) & 1) ^ 1);
                     uint8_t *op = smem + L.stage0 + gq * kStageBytes + sideB * kOpBytes;
-                    produce(op, quad, j0, p0, sp, v, wt, g, tab);
+                    produce<kFast>(op, quad, j0, p0, sp, v, wt, g, tab);
                     fence_proxy_async();
                     mbar_arrive(FULL(gq));
                 }
@@ -358,7 +412,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) 
             for (int i = 0; i < 32; ++i) acc[i] = 0.0;
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
                 const uint32_t b = chunk_ctr & 1;
-                mbar_wait(TFULL(b), (chunk_ctr >> 1) & 1);
+                mbar_wait_sleep(TFULL(b), (chunk_ctr >> 1) & 1);
                 tc_fence_after();
                 const uint32_t tb = tmem_base + lane_base + b * 128;
                 // D[L][c] + D[L][64+c] for the 32 columns this row keeps and the 32 it sends
@@ -434,16 +488,18 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
     const tc::Smem L = tc::smem_layout(entries);
     const size_t smem = L.total + 1024;
-    static size_t attr = 0;
-    if (smem > attr) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+    const bool fast = g.single && g.pow2;
+    auto kern = fast ? tc::k_gemm_tf32<true> : tc::k_gemm_tf32<false>;
+    static size_t attr[2] = {0, 0};
+    if (smem > attr[fast]) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[fast] = smem;
     }
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = plan.items < sms ? plan.items : sms;
-    tc::k_gemm_tf32<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws);
+    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws);
     FCFS_CHECK_LAUNCH("k_gemm_tf32");
     return FCFS_OK;
 }
