@@ -19,7 +19,7 @@
 //               write the item's 64x64 FP64 P tile (phys layout 1: c0..c31, s0..s31)
 //   warps 4-11  producers: twiddle generation into a 4-stage SMEM ring (mbarrier full/empty)
 //   warp 12     TMEM allocator + single-thread MMA issuer (tcgen05.mma / tcgen05.commit)
-#include "common.cuh"
+#include "coeff.cuh"
 
 namespace fcfs {
 namespace tc {
@@ -37,7 +37,8 @@ constexpr int kThreads = (kEpiWarps + kProdWarps + 1) * 32;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kTmemCols = 256;                  // 2 accumulators x 128 fp32 columns
 constexpr int kXStride = 33;                    // exchange buffer row stride (floats)
-constexpr int kSingleTableMax = 8192;           // T <= this: one-level table of T entries
+constexpr int kSingleTableMax = 4096;           // T <= this: one-level table of T entries
+constexpr int kMaxFuseRows = 64;                // fused epilogue: at most 63 output rows (M <= 31)
 // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
                             ((uint32_t)(128 >> 4) << 24);
@@ -53,8 +54,8 @@ __host__ __device__ inline Smem smem_layout(int table_entries) {
     s.stage0 = 0;
     s.table = kStages * kStageBytes;
     s.xbuf = s.table + ((table_entries * 8 + 1023) & ~1023);
-    s.bars = s.xbuf + 2 * 2 * 64 * kXStride * 4;
-    s.total = s.bars + 256;
+    s.bars = s.xbuf + 2 * 2 * 64 * kXStride * 4;   // xbuf also holds the fused epilogue's P tile (64 x 65 doubles)
+    s.total = s.bars + 256 + 4 * (kMaxFuseRows + 2);
     return s;
 }
 
@@ -265,9 +266,11 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
     }
 }
 
+// fuse != 0: one work item = one whole clip (single 64x64 tile, no split); the epilogue warps
+// turn P into the clip's output window directly (a4 + a5 fused; P never touches HBM).
 template <bool kFast>
 __global__ void __launch_bounds__(kThreads, 1)
-k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) {
+k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-align by offset arithmetic on the __shared__ array (keeps the shared address space, so
     // loads / stores compile to LDS / STS rather than generic LD / ST)
@@ -279,6 +282,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) 
     uint64_t *bars = (uint64_t *)(smem + L.bars);
     // barrier indices: full[0..S), empty[S..2S), tfull[2S..2S+2), tempty[2S+2..2S+4)
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
+    int32_t *rowoff = (int32_t *)(smem + L.bars + 256);   // fused pupil layout: output offset per row
     const uint32_t bar0 = su32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
     auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
@@ -295,6 +299,16 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) 
         else if (i < g.nhi) sincospi(2.0 * (double)((int64_t)i << g.lbits) / (double)g.T, &sn, &cs);
         else sincospi(2.0 * (double)(i - g.nhi) / (double)g.T, &sn, &cs);
         tab[i] = make_float2((float)cs, (float)sn);
+    }
+    if (tid == 0 && fuse) {
+        // output offset of each row m = -M..M (pupil: 2 nmax(m) + 1 entries, dense: 2N + 1)
+        int32_t off = 0;
+        for (int i = 0; i <= 2 * ea.M; ++i) {
+            rowoff[i] = off;
+            const int c = ea.layout == FCFS_LAYOUT_PUPIL ? pupil_nmax(i - ea.M, ea.r2, ea.N) : ea.N;
+            off += c < 0 ? 0 : 2 * c + 1;
+        }
+        rowoff[2 * ea.M + 1] = off;
     }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) { mbar_init(FULL(s), kProdThreads / kStages); mbar_init(EMPTY(s), 1); }
@@ -444,9 +458,44 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws) 
                     for (int i = 0; i < 32; ++i) acc[i] += (double)xsrc[r * kXStride + i];
                 }
             }
-            double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
+            if (!fuse) {
+                double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
+                for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
+                continue;
+            }
+            // ---- fused a4 + a5: P tile -> SMEM (aliases the exchange buffer) -> this clip's outputs
+            double *Ps = (double *)xbuf;   // [64][65]
+            named_bar(1, kEpiWarps * 32);  // every thread is done with the exchange buffer
+#pragma unroll
+            for (int i = 0; i < 32; ++i) Ps[r * 65 + (hi_row ? 0 : 32) + i] = acc[i];
+            named_bar(1, kEpiWarps * 32);
+            {
+                const int64_t clip = item;
+                const double dc = (double)(ea.area_dev ? ea.area_dev[clip] : ea.area_host) / ((double)ea.T * (double)ea.T);
+                auto get = [&](int px, int tx, int py, int ty) {
+                    return Ps[phys_row(px, tx, 1) * 65 + phys_row(py, ty, 1)];
+                };
+                const int W = rowoff[2 * ea.M + 1];
+                void *Fc = ea.out_f32 ? (void *)((float2 *)F + clip * ea.out_per_clip)
+                                      : (void *)((double2 *)F + clip * ea.out_per_clip);
+                for (int o = tid; o < W; o += kEpiWarps * 32) {
+                    int lo = 0, hi = 2 * ea.M;          // row i with rowoff[i] <= o < rowoff[i+1]
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (rowoff[mid] <= o) lo = mid; else hi = mid - 1;
+                    }
+                    const int m = lo - ea.M;
+                    const int cnt = rowoff[lo + 1] - rowoff[lo];
+                    const int n = o - rowoff[lo] - (cnt - 1) / 2;
+                    double2 v = make_double2(0.0, 0.0);
+                    if (!(ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0 &&
+                          (double)m * (double)m + (double)n * (double)n > ea.r2))
+                        v = coeff_from_P(get, plan.X, plan.Y, ea.T, m, n, dc);
+                    store_out(Fc, o, v, ea.out_f32);
+                }
+            }
+            named_bar(1, kEpiWarps * 32);  // P tile consumed before the next item's chunk flush
         }
     }
 
@@ -481,9 +530,17 @@ fcfs_status tf32_supported(const GemmPlan &plan, int32_t T) {
     return FCFS_OK;
 }
 
-fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
-                             cudaStream_t s) {
+bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea) {
+    return plan.tiles_x == 1 && plan.tiles_y == 1 && plan.splits == 1 && ea.m_lo == -ea.M && ea.m_hi == ea.M &&
+           2 * ea.M + 1 < tc::kMaxFuseRows;
+}
+
+fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws, const EpiArgs *ea,
+                             void *F, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
+    const int fuse = (ea && F && tf32_can_fuse(plan, *ea)) ? 1 : 0;
+    EpiArgs e{};
+    if (ea) e = *ea;
     tc::TabGeom g = make_tab(T);
     const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
     const tc::Smem L = tc::smem_layout(entries);
@@ -499,7 +556,7 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = plan.items < sms ? plan.items : sms;
-    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws);
+    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse);
     FCFS_CHECK_LAUNCH("k_gemm_tf32");
     return FCFS_OK;
 }

@@ -11,7 +11,7 @@
 // The window is the signed low-pass box |m|<=M, |n|<=N (reading A3), optionally masked or
 // packed to the pupil disk m^2+n^2 <= r2 (reading A11).  P of a clip is the
 // fixed-order sum of its split-K partial tiles (deterministic).
-#include "common.cuh"
+#include "coeff.cuh"
 
 namespace fcfs {
 
@@ -27,46 +27,10 @@ __device__ __forceinline__ double getP(const double *P_ws, const GemmPlan &pl, i
     return s;
 }
 
-// largest n >= 0 with m^2 + n^2 <= r2 (the same double comparison as the definition), -1 if none
-__device__ __forceinline__ int pupil_nmax(int m, double r2, int N) {
-    double mm = (double)m * (double)m;
-    if (mm > r2) return -1;
-    int n = (int)floor(sqrt(r2 - mm));
-    while (n + 1 <= N && mm + (double)(n + 1) * (double)(n + 1) <= r2) ++n;
-    while (n >= 0 && mm + (double)n * (double)n > r2) --n;
-    return n < N ? n : N;
-}
-
 __device__ double2 coeff(const double *P_ws, const GemmPlan &pl, const EpiArgs &ea, int64_t clip, int m, int n,
                          double dc) {
-    const double pi = 3.141592653589793238462643383279502884;
-    if (m == 0 && n == 0) return make_double2(dc, 0.0);
-    const bool neg = (m < 0) || (m == 0 && n < 0);
-    if (neg) { m = -m; n = -n; }
-    double re, im;
-    if (n == 0) {
-        const int pm = m - pl.X.f0, pa = pl.Y.nf;
-        double sre = getP(P_ws, pl, clip, pm, 0, pa, 0), sim = -getP(P_ws, pl, clip, pm, 1, pa, 0);
-        double d = 2.0 * pi * (double)m * (double)ea.T;
-        re = -sim / d; im = sre / d;
-    } else if (m == 0) {
-        const int pa = pl.X.nf, pn = n - pl.Y.f0;
-        double sre = getP(P_ws, pl, clip, pa, 0, pn, 0), sim = -getP(P_ws, pl, clip, pa, 0, pn, 1);
-        double d = 2.0 * pi * (double)n * (double)ea.T;
-        re = -sim / d; im = sre / d;
-    } else {
-        const int an = n < 0 ? -n : n;
-        const int pm = m - pl.X.f0, pn = an - pl.Y.f0;
-        double pcc = getP(P_ws, pl, clip, pm, 0, pn, 0), pcs = getP(P_ws, pl, clip, pm, 0, pn, 1);
-        double psc = getP(P_ws, pl, clip, pm, 1, pn, 0), pss = getP(P_ws, pl, clip, pm, 1, pn, 1);
-        double sre, sim;
-        if (n > 0) { sre = pcc - pss; sim = -(psc + pcs); }
-        else { sre = pcc + pss; sim = -(psc - pcs); }
-        double d = -4.0 * pi * pi * (double)m * (double)n;
-        re = sre / d; im = sim / d;
-    }
-    if (neg) im = -im;
-    return make_double2(re, im);
+    auto get = [&](int px, int tx, int py, int ty) { return getP(P_ws, pl, clip, px, tx, py, ty); };
+    return coeff_from_P(get, pl.X, pl.Y, ea.T, m, n, dc);
 }
 
 // grid: (output rows, clips); block loops over n
@@ -99,8 +63,7 @@ __global__ void k_epilogue(const double *__restrict__ P_ws, GemmPlan pl, EpiArgs
             keep = (double)m * (double)m + (double)n * (double)n <= ea.r2;
         v = keep ? coeff(P_ws, pl, ea, clip, m, n, dc) : make_double2(0.0, 0.0);
         const int64_t o = off + (n - nlo);
-        if (ea.out_f32) ((float2 *)F)[o] = make_float2((float)v.x, (float)v.y);
-        else ((double2 *)F)[o] = v;
+        store_out(F, o, v, ea.out_f32);
     }
 }
 

@@ -239,6 +239,206 @@ __global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, 
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Per-clip fast path (every rect its own group, clips of <= kClipRects rects, T < 2^16): one
+// CTA per clip builds the clip's 4n raw corners with 32-bit keys (y << 16 | x), sorts them in
+// shared memory (CUB BlockRadixSort), merges equal keys with a segmented block scan, drops zero
+// weights, and writes the compacted clip to a staging area at its raw offset 4*r0 together with
+// its exact int64 area.  A device scan of the per-clip counts gives corner_ptr; a copy kernel
+// packs the clips into x, y, w.  Same canonical (clip, y, x) order as the global path.
+// ------------------------------------------------------------------------------------------
+static constexpr int kClipThreads = 512;
+static constexpr int kClipItems = 16;
+static constexpr int kClipRects = kClipThreads * kClipItems / 4;   // 2048 rects -> 8192 corners
+
+struct SegSum {
+    int head;   // a segment starts at or before this element
+    int val;
+};
+struct SegSumOp {
+    __device__ __forceinline__ SegSum operator()(const SegSum &a, const SegSum &b) const {
+        SegSum r;
+        r.head = a.head | b.head;
+        r.val = b.head ? b.val : a.val + b.val;
+        return r;
+    }
+};
+
+__global__ void __launch_bounds__(kClipThreads, 1)
+k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
+               int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t *counts, int64_t *area, int32_t *err) {
+    typedef cub::BlockRadixSort<uint32_t, kClipThreads, kClipItems, int32_t> Sort;
+    typedef cub::BlockScan<SegSum, kClipThreads> SegScan;
+    typedef cub::BlockScan<int, kClipThreads> IntScan;
+    typedef cub::BlockReduce<long long, kClipThreads> Red;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        typename SegScan::TempStorage seg;
+        typename IntScan::TempStorage scan;
+        typename Red::TempStorage red;
+    } tmp;
+    __shared__ uint32_t edge_first[kClipThreads], edge_last[kClipThreads];
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
+        const int n = (int)(r1 - r0);
+        if (n > kClipRects) {
+            if (threadIdx.x == 0) atomicOr(err, 8);
+            continue;
+        }
+        uint32_t key[kClipItems];
+        int32_t val[kClipItems];
+#pragma unroll
+        for (int j = 0; j < kClipItems / 4; ++j) {
+            const int r = threadIdx.x * (kClipItems / 4) + j;
+            int4 q = make_int4(0, 0, 0, 0);
+            bool ok = r < n;
+            if (ok) {
+                q = rects[r0 + r];
+                if (!rect_ok(q, T)) { atomicOr(err, 1); ok = false; }
+            }
+            const uint32_t kx0 = (uint32_t)q.x, kx1 = (uint32_t)q.z, ky0 = (uint32_t)q.y, ky1 = (uint32_t)q.w;
+            key[4 * j + 0] = ok ? (ky0 << 16) | kx0 : 0xFFFFFFFFu; val[4 * j + 0] = ok ? 1 : 0;
+            key[4 * j + 1] = ok ? (ky0 << 16) | kx1 : 0xFFFFFFFFu; val[4 * j + 1] = ok ? -1 : 0;
+            key[4 * j + 2] = ok ? (ky1 << 16) | kx0 : 0xFFFFFFFFu; val[4 * j + 2] = ok ? -1 : 0;
+            key[4 * j + 3] = ok ? (ky1 << 16) | kx1 : 0xFFFFFFFFu; val[4 * j + 3] = ok ? 1 : 0;
+        }
+        __syncthreads();
+        Sort(tmp.sort).Sort(key, val);   // blocked: thread t holds sorted items 16 t .. 16 t + 15
+        __syncthreads();
+        // heads: key differs from the previous item (previous thread's last key via SMEM)
+        edge_first[threadIdx.x] = key[0];
+        edge_last[threadIdx.x] = key[kClipItems - 1];
+        __syncthreads();
+        SegSum seg[kClipItems];
+#pragma unroll
+        for (int j = 0; j < kClipItems; ++j) {
+            const uint32_t prev = j ? key[j - 1] : (threadIdx.x ? edge_last[threadIdx.x - 1] : 0xFFFFFFFEu);
+            seg[j].head = key[j] != prev;
+            seg[j].val = val[j];
+        }
+        SegScan(tmp.seg).InclusiveScan(seg, seg, SegSumOp());
+        __syncthreads();
+        // tails: key differs from the next item; keep a tail whose run sum is non-zero
+        int keep[kClipItems], pos[kClipItems];
+        long long a = 0;
+#pragma unroll
+        for (int j = 0; j < kClipItems; ++j) {
+            const bool last = (j + 1 == kClipItems) && (threadIdx.x + 1 == kClipThreads);
+            const uint32_t nxt = j + 1 < kClipItems ? key[j + 1] : (last ? 0u : edge_first[threadIdx.x + 1]);
+            const bool tail = last || key[j] != nxt;
+            keep[j] = (tail && key[j] != 0xFFFFFFFFu && seg[j].val != 0) ? 1 : 0;
+            if (keep[j]) a += (long long)seg[j].val * (long long)(key[j] & 0xFFFFu) * (long long)(key[j] >> 16);
+        }
+        __syncthreads();   // edge_key reads above complete before it is reused next clip
+        int total = 0;
+        IntScan(tmp.scan).ExclusiveSum(keep, pos, total);
+        __syncthreads();
+        const int64_t base = 4 * r0;
+#pragma unroll
+        for (int j = 0; j < kClipItems; ++j) {
+            if (keep[j]) {
+                xs[base + pos[j]] = (int32_t)(key[j] & 0xFFFFu);
+                ys[base + pos[j]] = (int32_t)(key[j] >> 16);
+                ws[base + pos[j]] = seg[j].val;
+            }
+        }
+        const long long asum = Red(tmp.red).Sum(a);
+        if (threadIdx.x == 0) {
+            counts[b] = total;
+            area[b] = asum;
+        }
+        __syncthreads();
+    }
+}
+
+// pack each clip's staged corners (at 4 r0) to its CSR position corner_ptr[b]
+__global__ void k_clip_pack(const int64_t *__restrict__ clip_ptr, int64_t B, const int64_t *__restrict__ corner_ptr,
+                            const int32_t *xs, const int32_t *ys, const int32_t *ws, int64_t cap, int32_t *x, int32_t *y,
+                            int32_t *w) {
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        const int64_t src = 4 * (clip_ptr ? clip_ptr[b] : 0);
+        const int64_t dst = corner_ptr[b], n = corner_ptr[b + 1] - dst;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            if (dst + i < cap) {
+                x[dst + i] = xs[src + i];
+                y[dst + i] = ys[src + i];
+                w[dst + i] = ws[src + i];
+            }
+        }
+    }
+}
+
+struct ClipWs {
+    int32_t *xs, *ys, *ws;
+    int64_t *counts, *K;
+    int32_t *err;
+    void *cub_tmp;
+    size_t cub_bytes;
+};
+
+static void carve_clip(Carver &cv, int64_t R, int64_t B, ClipWs &w) {
+    w.xs = cv.take<int32_t>(4 * R + 1);
+    w.ys = cv.take<int32_t>(4 * R + 1);
+    w.ws = cv.take<int32_t>(4 * R + 1);
+    w.counts = cv.take<int64_t>(B + 1);
+    w.K = cv.take<int64_t>(1);
+    w.err = cv.take<int32_t>(4);
+    size_t c = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (int64_t *)nullptr, (int64_t *)nullptr, (int)(B + 1));
+    w.cub_tmp = cv.take<char>(c);
+    w.cub_bytes = c;
+}
+
+size_t extract_clip_workspace_bytes(int64_t R, int64_t B) {
+    Carver cv(nullptr, 0);
+    ClipWs w;
+    carve_clip(cv, R, B, w);
+    return cv.used();
+}
+
+// returns FCFS_E_UNSUPPORTED (after a sync) if a clip exceeds kClipRects: the caller falls back
+fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B, int32_t T,
+                          int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                          int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    ClipWs W;
+    carve_clip(cv, R, B, W);
+    if (!cv.fits()) {
+        set_error("fcfs_vertices_from_rects: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+    int64_t grid = B < 148 * 2 * 16 ? B : 148 * 2 * 16;
+    k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, W.xs, W.ys, W.ws,
+                                                           W.counts, area, W.err);
+    FCFS_CHECK_LAUNCH("k_clip_corners");
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.counts + B, 0, sizeof(int64_t), s));
+    size_t tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.counts, corner_ptr, (int)(B + 1), s));
+    count_launch(2);
+    k_clip_pack<<<(unsigned)grid, 256, 0, s>>>(clip_ptr, B, corner_ptr, W.xs, W.ys, W.ws, cap, x, y, w);
+    FCFS_CHECK_LAUNCH("k_clip_pack");
+    int64_t Kh = 0;
+    int32_t errh = 0;
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, corner_ptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (errh & 8) {
+        set_error("a clip has more than %d rects", kClipRects);
+        return FCFS_E_UNSUPPORTED;
+    }
+    if (K_host) *K_host = Kh;
+    if (errh & 1) {
+        set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");
+        return FCFS_E_RANGE;
+    }
+    if (Kh > cap) {
+        set_error("fcfs_vertices_from_rects: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
+        return FCFS_E_CAPACITY;
+    }
+    return FCFS_OK;
+}
+
 static int64_t raw_capacity(int64_t R, int64_t max_group, bool singleton) {
     if (singleton) return 4 * R;
     int64_t g = max_group < 1 ? 1 : max_group;
@@ -284,7 +484,9 @@ size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_grou
     Carver cv(nullptr, 0);
     ExtractWs w;
     carve(cv, cap, cub_bytes_for(cap, 2 * kCoordBits + clip_bits(B)), w);
-    return cv.used();
+    size_t a = cv.used();
+    size_t b = singleton ? extract_clip_workspace_bytes(R, B) : 0;
+    return a > b ? a : b;
 }
 
 fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
@@ -292,6 +494,11 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                     int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {
     const bool singleton = (group_ptr == nullptr);
+    if (singleton && T <= 65534 && (clip_ptr != nullptr || R <= kClipRects)) {
+        fcfs_status st = extract_clips(rects, R, clip_ptr, B, T, x, y, w, cap, corner_ptr, area, K_host, ws,
+                                       ws_bytes, s);
+        if (st != FCFS_E_UNSUPPORTED) return st;   // else: a clip is too large for the per-clip path
+    }
     if (!singleton && max_group > kMaxGroup) {
         set_error("fcfs_vertices_from_rects: max_group=%lld exceeds this build's limit %d",
                   (long long)max_group, kMaxGroup);

@@ -61,7 +61,8 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
 // contract_tf32.cu
 fcfs_status tf32_supported(const GemmPlan &plan, int32_t T);
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
-                             cudaStream_t s);
+                             const EpiArgs *ea, void *F, cudaStream_t s);
+bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 
 static fcfs_status device_ok() {
     static int cached = -1;
@@ -155,8 +156,15 @@ struct CoeffWs {
     int64_t *area;
 };
 
-static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w) {
-    w.P = cv.take<double>((size_t)p.items * kTile * kTile);
+// P_ws is not needed when the tcgen05 kernel fuses the epilogue (whole clip = one 64x64 tile)
+static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m_lo, int32_t m_hi) {
+    EpiArgs ea{};
+    ea.M = M; ea.m_lo = m_lo; ea.m_hi = m_hi;
+    return prec == FCFS_TF32X3 && tf32_can_fuse(p, ea);
+}
+
+static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P = true) {
+    w.P = cv.take<double>(need_P ? (size_t)p.items * kTile * kTile : 1);
     w.area = cv.take<int64_t>(1);
 }
 
@@ -178,13 +186,17 @@ static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard,
     return FCFS_OK;
 }
 
+// a2 + a3 (+ a4/a5 when the tcgen05 kernel can fuse its epilogue); *fused tells the caller
+// whether the stand-alone epilogue kernel is still needed.
 static fcfs_status run_gemm(const CornerSrc &src, const GemmPlan &plan, int32_t T, fcfs_precision prec,
-                            double *P, cudaStream_t s) {
+                            double *P, const EpiArgs &ea, void *F, cudaStream_t s, bool *fused) {
+    *fused = false;
     if (prec == FCFS_FP64) return launch_gemm_fp64(src, plan, T, P, s);
     if (prec == FCFS_TF32X3) {
         fcfs_status st = tf32_supported(plan, T);
         if (st != FCFS_OK) return st;
-        return launch_gemm_tf32(src, plan, T, P, s);   // writes P in phys layout 1
+        *fused = tf32_can_fuse(plan, ea);
+        return launch_gemm_tf32(src, plan, T, P, &ea, F, s);   // P in phys layout 1 when not fused
     }
     set_error("bad precision %d", prec);
     return FCFS_E_INVALID;
@@ -290,7 +302,7 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w);
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi));
     return cv.used();
 }
 
@@ -322,7 +334,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W);
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi));
     if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     EpiArgs ea;
@@ -335,11 +347,12 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
         if (st != FCFS_OK) return st;
         ea.area_dev = W.area;
     }
+    bool fused = false;
     {
         StageScope scope(kStageContract, s);
-        st = run_gemm(src, plan, T, prec, W.P, s);
+        st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
-    if (st != FCFS_OK) return st;
+    if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
     return launch_epilogue(plan, W.P, ea, F, s);
 }
@@ -351,7 +364,7 @@ size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, i
     GemmPlan p = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w);
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, -win->M, win->M));
     return cv.used();
 }
 
@@ -374,7 +387,7 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W);
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M));
     if (!cv.fits()) { set_error("fcfs_coeffs_batched: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     CornerSrc src;
@@ -384,11 +397,12 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     ea.m_lo = -win->M; ea.m_hi = win->M; ea.T = T; ea.area_dev = area; ea.area_host = 0;
     ea.out_f32 = prec == FCFS_TF32X3 ? 1 : 0;
     ea.out_per_clip = fcfs_window_size(win);
+    bool fused = false;
     {
         StageScope scope(kStageContract, s);
-        st = run_gemm(src, plan, T, prec, W.P, s);
+        st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
-    if (st != FCFS_OK) return st;
+    if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
     return launch_epilogue(plan, W.P, ea, F, s);
 }

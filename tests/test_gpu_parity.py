@@ -64,9 +64,15 @@ def _assert_parity(F, Fref, B, prec, what, ms=None, ns=None):
 
 # ------------------------------------------------------------------ a1: extraction, bit-exact
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "c3x64", "c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3x64", "c3one", "c4", "c5"])
 def test_extraction_bit_exact(fcfs, cfg):
-    wl = inputs.c3(clips=64) if cfg == "c3x64" else inputs.make(cfg)
+    if cfg == "c3x64":
+        wl = inputs.c3(clips=64)                     # per-clip SMEM sort path
+    elif cfg == "c3one":
+        wl = inputs.c3(clips=1)
+        wl.clip_ptr = None                           # single clip, singleton groups, no clip CSR
+    else:
+        wl = inputs.make(cfg)
     e = oracle.extract(wl.rects, wl.T, wl.group_ptr, wl.clip_ptr)
     g = _gpu_extract(fcfs, wl)
     _assert_extract_equal(g, e)
