@@ -250,6 +250,7 @@ __global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, 
 static constexpr int kClipThreads = 512;
 static constexpr int kClipItems = 16;
 static constexpr int kClipRects = kClipThreads * kClipItems / 4;   // 2048 rects -> 8192 corners
+static_assert(kClipRects == 512 * 4, "bucket path: 4 rects per thread");
 
 struct SegSum {
     int head;   // a segment starts at or before this element
@@ -351,6 +352,143 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
     }
 }
 
+// Per-clip bucket path (every rect its own group, T <= kBucketMaxT, clips <= kClipRects rects):
+// one CTA per clip counting-sorts the clip's 4n corners by y into T+1 SMEM buckets (atomics);
+// then every corner finds its rank inside its (short) bucket by x, the first of equal (y, x)
+// carries the summed weight (groups are summed, reading A5), a block scan over the sorted
+// positions drops zero weights, and the clip is written in canonical (y, x) order to the
+// staging area at 4*r0 (coalesced), with its exact int64 area.  O(n * bucket) with all threads
+// busy, instead of a radix sort of 4n keys.
+static constexpr int kBucketThreads = 512;
+static constexpr int kBucketRectsPerThread = 4;   // kClipRects / kBucketThreads
+static constexpr int kBucketMaxT = 8191;
+static constexpr int kBucketCap = 4 * kClipRects;
+
+__global__ void __launch_bounds__(kBucketThreads)
+k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
+                      int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t *counts, int64_t *area,
+                      int32_t *err) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    uint16_t *bx = (uint16_t *)bsm;                     // [cap] bucketed (unsorted) x
+    uint16_t *by = bx + kBucketCap;                     // [cap] bucket y
+    int16_t *bw = (int16_t *)(by + kBucketCap);         // [cap] bucketed weight
+    uint32_t *syx = (uint32_t *)(bw + kBucketCap);      // [cap] sorted (y << 16 | x)
+    int16_t *sw = (int16_t *)(syx + kBucketCap);        // [cap] sorted merged weight (0 = dropped)
+    int32_t *hist = (int32_t *)(sw + kBucketCap);       // [T + 2]: bucket start, then bucket end
+    __shared__ int32_t wsum[kBucketThreads / 32];
+    __shared__ long long asum[kBucketThreads / 32];
+    __shared__ int tot_s;
+    const int nb = T + 1;                               // buckets y = 0..T
+    const int per = (nb + kBucketThreads - 1) / kBucketThreads;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
+        const int n = (int)(r1 - r0);
+        if (n > kClipRects) {
+            if (threadIdx.x == 0) atomicOr(err, 8);
+            continue;
+        }
+        // all of this thread's rects are loaded up front (independent loads in flight)
+        int4 rq[kBucketRectsPerThread];
+        bool rok[kBucketRectsPerThread];
+#pragma unroll
+        for (int j = 0; j < kBucketRectsPerThread; ++j) {
+            const int r = threadIdx.x + j * kBucketThreads;
+            rok[j] = r < n;
+            rq[j] = rok[j] ? rects[r0 + r] : make_int4(0, 0, 0, 0);
+        }
+        for (int i = threadIdx.x; i < nb + 1; i += kBucketThreads) hist[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kBucketRectsPerThread; ++j) {
+            if (!rok[j]) continue;
+            if (!rect_ok(rq[j], T)) { atomicOr(err, 1); rok[j] = false; continue; }
+            atomicAdd(&hist[rq[j].y], 2);
+            atomicAdd(&hist[rq[j].w], 2);
+        }
+        __syncthreads();
+        {   // exclusive scan of bucket sizes: thread t owns buckets [t*per, (t+1)*per)
+            const int lo = threadIdx.x * per, hi = min(lo + per, nb);
+            int sown = 0;
+            for (int i = lo; i < hi; ++i) sown += hist[i];
+            int incl = sown;
+            for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+            if (lane == 31) wsum[wid] = incl;
+            __syncthreads();
+            int run = incl - sown;
+            for (int i = 0; i < wid; ++i) run += wsum[i];
+            for (int i = lo; i < hi; ++i) { const int c = hist[i]; hist[i] = run; run += c; }
+        }
+        __syncthreads();
+        // scatter into buckets: afterwards hist[y] = end of bucket y (= start of bucket y + 1)
+#pragma unroll
+        for (int j = 0; j < kBucketRectsPerThread; ++j) {
+            if (!rok[j]) continue;
+            const int4 q = rq[j];
+            int p = atomicAdd(&hist[q.y], 2);
+            bx[p] = (uint16_t)q.x; by[p] = (uint16_t)q.y; bw[p] = 1;
+            bx[p + 1] = (uint16_t)q.z; by[p + 1] = (uint16_t)q.y; bw[p + 1] = -1;
+            p = atomicAdd(&hist[q.w], 2);
+            bx[p] = (uint16_t)q.x; by[p] = (uint16_t)q.w; bw[p] = -1;
+            bx[p + 1] = (uint16_t)q.z; by[p + 1] = (uint16_t)q.w; bw[p + 1] = 1;
+        }
+        __syncthreads();
+        const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
+        // rank inside the bucket by x (ties by index); the first of equal x carries the run sum
+        for (int i = threadIdx.x; i < nv; i += kBucketThreads) {
+            const int y = by[i];
+            const int st = y ? hist[y - 1] : 0, en = hist[y];
+            const uint16_t xi = bx[i];
+            int rank = 0, wv = 0;
+            bool first = true;
+            for (int j = st; j < en; ++j) {
+                const uint16_t xj = bx[j];
+                rank += (xj < xi) || (xj == xi && j < i);
+                if (xj == xi) { wv += bw[j]; first &= !(j < i); }
+            }
+            syx[st + rank] = ((uint32_t)y << 16) | xi;
+            sw[st + rank] = first ? (int16_t)wv : (int16_t)0;
+        }
+        __syncthreads();
+        // compact the non-zero sorted entries: thread t owns sorted positions [t*pp, (t+1)*pp)
+        const int pp = (nv + kBucketThreads - 1) / kBucketThreads;
+        const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
+        int cnt = 0;
+        long long a = 0;
+        for (int i = lo; i < hi; ++i)
+            if (sw[i] != 0) {
+                ++cnt;
+                a += (long long)sw[i] * (long long)(syx[i] & 0xFFFFu) * (long long)(syx[i] >> 16);
+            }
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        __syncthreads();                                // wsum reuse
+        if (lane == 31) wsum[wid] = incl;
+        if (lane == 0) asum[wid] = a;
+        __syncthreads();
+        int outp = incl - cnt;
+        for (int i = 0; i < wid; ++i) outp += wsum[i];
+        const int64_t base = 4 * r0;
+        for (int i = lo; i < hi; ++i)
+            if (sw[i] != 0) {
+                xs[base + outp] = (int32_t)(syx[i] & 0xFFFFu);
+                ys[base + outp] = (int32_t)(syx[i] >> 16);
+                ws[base + outp] = sw[i];
+                ++outp;
+            }
+        if (threadIdx.x == kBucketThreads - 1) tot_s = outp;     // the last thread ends at the clip total
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            counts[b] = tot_s;
+            long long t = 0;
+            for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
+            area[b] = t;
+        }
+        __syncthreads();
+    }
+}
+
 // pack each clip's staged corners (at 4 r0) to its CSR position corner_ptr[b]
 __global__ void k_clip_pack(const int64_t *__restrict__ clip_ptr, int64_t B, const int64_t *__restrict__ corner_ptr,
                             const int32_t *xs, const int32_t *ys, const int32_t *ws, int64_t cap, int32_t *x, int32_t *y,
@@ -409,9 +547,23 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
     }
     FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
     int64_t grid = B < 148 * 2 * 16 ? B : 148 * 2 * 16;
-    k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, W.xs, W.ys, W.ws,
-                                                           W.counts, area, W.err);
-    FCFS_CHECK_LAUNCH("k_clip_corners");
+    if (T <= kBucketMaxT) {
+        const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
+        static bool battr = false;
+        if (!battr) {
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kBucketCap * 12 + (kBucketMaxT + 2) * 4));
+            battr = true;
+        }
+        k_clip_corners_bucket<<<(unsigned)grid, kBucketThreads, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T,
+                                                                            W.xs, W.ys, W.ws, W.counts, area,
+                                                                            W.err);
+        FCFS_CHECK_LAUNCH("k_clip_corners_bucket");
+    } else {
+        k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, W.xs, W.ys,
+                                                               W.ws, W.counts, area, W.err);
+        FCFS_CHECK_LAUNCH("k_clip_corners");
+    }
     FCFS_TRY_CUDA(cudaMemsetAsync(W.counts + B, 0, sizeof(int64_t), s));
     size_t tb = W.cub_bytes;
     FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.counts, corner_ptr, (int)(B + 1), s));
