@@ -71,6 +71,7 @@ struct GemmPlan {
     int32_t tiles_x, tiles_y, splits;
     int64_t B;                // clips
     int64_t items;            // B * tiles_x * tiles_y * splits
+    int32_t dbg;              // experiments only (env FCFS_DEBUG): 1 = producers skip generation, 2 = no MMA
     int32_t phys;             // P_ws row order inside a 64-row tile: 0 = (c0,s0,c1,s1,...) [FP64 kernel],
                               // 1 = (c0..c31, s0..s31) [tcgen05 kernel]
 };

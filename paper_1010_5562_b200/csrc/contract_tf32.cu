@@ -17,7 +17,9 @@
 // Warp roles (416 threads, 1 CTA per SM, persistent over work items):
 //   warps 0-3   epilogue: tcgen05.ld TMEM -> registers, combine 4 quadrant blocks, FP64 flush,
 //               write the item's 64x64 FP64 P tile (phys layout 1: c0..c31, s0..s31)
-//   warps 4-11  producers: twiddle generation into a 4-stage SMEM ring (mbarrier full/empty)
+//   warps 4-11  producers: twiddle generation into a 5-stage SMEM ring (mbarrier full/empty);
+//               4 groups of 2 warps (side A, side B), group g fills every 4th stage, so a group
+//               never waits for the consumption of the stage it produced last (ring > groups)
 //   warp 12     TMEM allocator + single-thread MMA issuer (tcgen05.mma / tcgen05.commit)
 #include "coeff.cuh"
 
@@ -25,10 +27,11 @@ namespace fcfs {
 namespace tc {
 
 constexpr int kBK = 32;                         // corners per stage (K of 4 MMAs)
-constexpr int kStages = 4;
+constexpr int kStages = 5;                      // ring depth (> kGroups: no self-wait)
+constexpr int kGroups = 4;                      // producer groups (2 warps each)
 constexpr int kRows = 128;                      // operand rows: 64 hi + 64 lo
-constexpr int kRowBytes = kBK * 4;              // one operand row of a stage = one SW128 atom row
-constexpr int kOpBytes = kRows * kBK * 4;       // 16 KB per operand per stage
+constexpr int kRowBytes = kBK * 4;              // one operand row of a stage = one SW128 atom row (128 B)
+constexpr int kOpBytes = kRows * kRowBytes;     // 16 KB per operand per stage
 constexpr int kStageBytes = 2 * kOpBytes;       // A + B
 constexpr int kChunk = 1024;                    // corners per TMEM accumulation (FP64 flush)
 constexpr int kEpiWarps = 4, kProdWarps = 8;
@@ -37,8 +40,9 @@ constexpr int kThreads = (kEpiWarps + kProdWarps + 1) * 32;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kTmemCols = 256;                  // 2 accumulators x 128 fp32 columns
 constexpr int kXStride = 33;                    // exchange buffer row stride (floats)
-constexpr int kSingleTableMax = 4096;           // T <= this: one-level table of T entries
+constexpr int kSingleTableMax = 2048;           // T <= this: one-level table of T entries (smem budget)
 constexpr int kMaxFuseRows = 64;                // fused epilogue: at most 63 output rows (M <= 31)
+constexpr int kMaxFuseOut = 63 * 63;            // fused epilogue: output (m, n) table entries
 // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
                             ((uint32_t)(128 >> 4) << 24);
@@ -54,8 +58,8 @@ __host__ __device__ inline Smem smem_layout(int table_entries) {
     s.stage0 = 0;
     s.table = kStages * kStageBytes;
     s.xbuf = s.table + ((table_entries * 8 + 1023) & ~1023);
-    s.bars = s.xbuf + 2 * 2 * 64 * kXStride * 4;   // xbuf also holds the fused epilogue's P tile (64 x 65 doubles)
-    s.total = s.bars + 256 + 4 * (kMaxFuseRows + 2);
+    s.bars = s.xbuf + 2 * 64 * kXStride * 4;       // xbuf also holds the fused epilogue's fp32 P tile (64 x 65)
+    s.total = s.bars + 256 + 4 * (kMaxFuseRows + 2) + 8 * 4 * kMaxFuseRows + 4 * kMaxFuseOut;
     return s;
 }
 
@@ -76,9 +80,24 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 // bounded spin: a protocol bug traps (kernel error) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int spin = 0) {
     uint32_t n = 0;
+    if (spin) {
+        while (!mbar_test(bar, parity)) {
+            if (++n > (1u << 30)) __trap();
+        }
+        return;
+    }
     while (!mbar_try(bar, parity)) {
         if (++n > (1u << 26)) __trap();
     }
@@ -115,6 +134,15 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     d |= (uint64_t)1 << 46;                          // descriptor version for sm_100
     d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
     return d;
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
 }
 
 __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
@@ -197,77 +225,78 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
     lo = v - hi;
 }
 
-__device__ __forceinline__ float2 lo2(float2 v) {   // v - tf32_truncate(v), exact
-    const float2 h = make_float2(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
-                                 __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
-    return __fadd2_rn(v, make_float2(-h.x, -h.y));
-}
-
-// One producer task: 4 consecutive corners (chunk `quad` of the stage) x 8 consecutive pair
-// slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup for
-// the first frequency, pre-multiplied by the corner weight, and the angle-addition recurrence
-// E(f+1) = E(f) E(1) for the other 7, computed on corner pairs with the sm_100 packed FP32x2
-// FMA.  The split values go straight into the SW128 K-major operand tile: rows j0+i (cos hi),
-// 32+j0+i (sin hi), 64+j0+i (cos lo), 96+j0+i (sin lo).  The hi rows store v itself (the tf32
-// MMA reads only its top 19 bits, hi = v & 0xFFFFE000); the lo rows store the exact v - hi.
-// Padding slots (p > nf) keep recurrence values: they only feed P entries nobody reads.  The
-// axis slot (p == nf) is overwritten with the coordinate weight.
+// One producer task: 4 consecutive corners (16-byte chunk `quad` of the stage) x 8 consecutive
+// pair slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup
+// for the first frequency, pre-multiplied by the corner weight, and the angle-addition
+// recurrence E(f+1) = E(f) E(1) for the other 7.  The split values go straight into the SW128
+// K-major operand tile: rows j0+i (cos hi), 32+j0+i (sin hi), 64+j0+i (cos lo), 96+j0+i (sin lo).
+// The hi rows store v itself (the tf32 MMA reads only its top 19 bits, hi = v & 0xFFFFE000);
+// the lo rows store the exact v - hi.  Padding slots (p > nf) keep recurrence values: they only
+// feed P entries nobody reads.  The axis slot (p == nf) is overwritten with the coordinate weight.
+// Bank use: a warp (one side) = 8 quads x 4 slot blocks; every STS.128 covers 4 full 128 B rows.
 template <bool kFast>
 __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
                                         const int32_t v[4], const float wt[4], const TabGeom &g,
                                         const float2 *tab) {
     const uint32_t f0 = (uint32_t)(sp.f0 + p0);
-    float2 re[2], im[2], c1[2], s1[2], ns1[2];
+    float4 re, im, c1, s1;
+    {
+        float2 a[4], e[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const float2 a0 = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[2 * h], g), g, tab);
-        const float2 a1 = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[2 * h + 1], g), g, tab);
-        const float2 b0 = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[2 * h], g), g, tab);
-        const float2 b1 = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[2 * h + 1], g), g, tab);
-        re[h] = make_float2(wt[2 * h] * a0.x, wt[2 * h + 1] * a1.x);
-        im[h] = make_float2(wt[2 * h] * a0.y, wt[2 * h + 1] * a1.y);
-        c1[h] = make_float2(b0.x, b1.x);
-        s1[h] = make_float2(b0.y, b1.y);
-        ns1[h] = make_float2(-b0.y, -b1.y);
+        for (int q = 0; q < 4; ++q) {
+            a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[q], g), g, tab);
+            e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[q], g), g, tab);
+        }
+        re = make_float4(wt[0] * a[0].x, wt[1] * a[1].x, wt[2] * a[2].x, wt[3] * a[3].x);
+        im = make_float4(wt[0] * a[0].y, wt[1] * a[1].y, wt[2] * a[2].y, wt[3] * a[3].y);
+        c1 = make_float4(e[0].x, e[1].x, e[2].x, e[3].x);
+        s1 = make_float4(e[0].y, e[1].y, e[2].y, e[3].y);
     }
     uint8_t *opq = op + (j0 >> 3) * 1024;
+    const uint32_t M13 = 0xFFFFE000u;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const float2 rl0 = lo2(re[0]), rl1 = lo2(re[1]), il0 = lo2(im[0]), il1 = lo2(im[1]);
+        float4 rl, il;
+        rl.x = re.x - __uint_as_float(__float_as_uint(re.x) & M13);
+        rl.y = re.y - __uint_as_float(__float_as_uint(re.y) & M13);
+        rl.z = re.z - __uint_as_float(__float_as_uint(re.z) & M13);
+        rl.w = re.w - __uint_as_float(__float_as_uint(re.w) & M13);
+        il.x = im.x - __uint_as_float(__float_as_uint(im.x) & M13);
+        il.y = im.y - __uint_as_float(__float_as_uint(im.y) & M13);
+        il.z = im.z - __uint_as_float(__float_as_uint(im.z) & M13);
+        il.w = im.w - __uint_as_float(__float_as_uint(im.w) & M13);
         uint8_t *base = opq + i * kRowBytes + ((quad ^ i) << 4);   // row j0 + i (r % 8 == i)
-        *(float4 *)(base) = make_float4(re[0].x, re[0].y, re[1].x, re[1].y);
-        *(float4 *)(base + 4 * 1024) = make_float4(im[0].x, im[0].y, im[1].x, im[1].y);
-        *(float4 *)(base + 8 * 1024) = make_float4(rl0.x, rl0.y, rl1.x, rl1.y);
-        *(float4 *)(base + 12 * 1024) = make_float4(il0.x, il0.y, il1.x, il1.y);
+        *(float4 *)(base) = re;                    // row r
+        *(float4 *)(base + 4 * 1024) = im;         // row 32 + r
+        *(float4 *)(base + 8 * 1024) = rl;         // row 64 + r
+        *(float4 *)(base + 12 * 1024) = il;        // row 96 + r
         if (i < 7) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const float2 t = __fmul2_rn(im[h], ns1[h]);
-                const float2 u = __fmul2_rn(re[h], s1[h]);
-                re[h] = __ffma2_rn(re[h], c1[h], t);
-                im[h] = __ffma2_rn(im[h], c1[h], u);
-            }
+            float4 nr, ni;
+            nr.x = fmaf(re.x, c1.x, -im.x * s1.x); ni.x = fmaf(im.x, c1.x, re.x * s1.x);
+            nr.y = fmaf(re.y, c1.y, -im.y * s1.y); ni.y = fmaf(im.y, c1.y, re.y * s1.y);
+            nr.z = fmaf(re.z, c1.z, -im.z * s1.z); ni.z = fmaf(im.z, c1.z, re.z * s1.z);
+            nr.w = fmaf(re.w, c1.w, -im.w * s1.w); ni.w = fmaf(im.w, c1.w, re.w * s1.w);
+            re = nr;
+            im = ni;
         }
     }
     const int ia = sp.nf - p0;
     if (sp.axis && ia >= 0 && ia < 8) {
-        float c[4], cl[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            c[q] = wt[q] * (float)v[q];
-            cl[q] = c[q] - __uint_as_float(__float_as_uint(c[q]) & 0xFFFFE000u);
-        }
+        float4 c, cl;
+        c = make_float4(wt[0] * (float)v[0], wt[1] * (float)v[1], wt[2] * (float)v[2], wt[3] * (float)v[3]);
+        cl.x = c.x - __uint_as_float(__float_as_uint(c.x) & M13);
+        cl.y = c.y - __uint_as_float(__float_as_uint(c.y) & M13);
+        cl.z = c.z - __uint_as_float(__float_as_uint(c.z) & M13);
+        cl.w = c.w - __uint_as_float(__float_as_uint(c.w) & M13);
         uint8_t *base = opq + ia * kRowBytes + ((quad ^ ia) << 4);
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        *(float4 *)(base) = make_float4(c[0], c[1], c[2], c[3]);
+        *(float4 *)(base) = c;
         *(float4 *)(base + 4 * 1024) = z;
-        *(float4 *)(base + 8 * 1024) = make_float4(cl[0], cl[1], cl[2], cl[3]);
+        *(float4 *)(base + 8 * 1024) = cl;
         *(float4 *)(base + 12 * 1024) = z;
     }
 }
 
-// fuse != 0: one work item = one whole clip (single 64x64 tile, no split); the epilogue warps
-// turn P into the clip's output window directly (a4 + a5 fused; P never touches HBM).
 template <bool kFast>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse) {
@@ -283,6 +312,12 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     // barrier indices: full[0..S), empty[S..2S), tfull[2S..2S+2), tempty[2S+2..2S+4)
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
     int32_t *rowoff = (int32_t *)(smem + L.bars + 256);   // fused pupil layout: output offset per row
+    // fused output tables: scale factors per |m| / |n| and the packed (m, n) of every output
+    double *f_rows = (double *)(smem + L.bars + 256 + 4 * (kMaxFuseRows + 2));   // -1/(4 pi^2 a)
+    double *f_invn = f_rows + kMaxFuseRows;                                      // 1/b
+    double *f_axm = f_invn + kMaxFuseRows;                                       // 1/(2 pi a T)
+    double *f_axn = f_axm + kMaxFuseRows;                                        // 1/(2 pi b T)
+    uint32_t *f_mn = (uint32_t *)(f_axn + kMaxFuseRows);                        // (m+M) << 16 | (n+N), bit 31: masked
     const uint32_t bar0 = su32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
     auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
@@ -311,7 +346,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         rowoff[2 * ea.M + 1] = off;
     }
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(FULL(s), kProdThreads / kStages); mbar_init(EMPTY(s), 1); }
+        // FULL: one arrive per producer warp (after every lane's proxy fence + __syncwarp)
+        for (int s = 0; s < kStages; ++s) { mbar_init(FULL(s), kProdWarps / kGroups); mbar_init(EMPTY(s), 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(TFULL(b), 1); mbar_init(TEMPTY(b), kEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -326,11 +362,34 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (fuse) {
+        const double pi = 3.141592653589793238462643383279502884;
+        for (int a = tid; a < kMaxFuseRows; a += kThreads) {
+            f_rows[a] = a ? -1.0 / (4.0 * pi * pi * (double)a) : 0.0;
+            f_invn[a] = a ? 1.0 / (double)a : 0.0;
+            f_axm[a] = a ? 1.0 / (2.0 * pi * (double)a * (double)ea.T) : 0.0;
+            f_axn[a] = f_axm[a];
+        }
+        // packed (m, n) of every output, row by row (rows in the layout's order)
+        for (int i = 0; i <= 2 * ea.M; ++i) {
+            const int cnt = rowoff[i + 1] - rowoff[i];
+            const int h = (cnt - 1) / 2;
+            for (int j = tid; j < cnt; j += kThreads) {
+                const int m = i - ea.M, n = j - h;
+                uint32_t pk = ((uint32_t)(m + ea.M) << 16) | (uint32_t)(n + ea.N);
+                if (ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0 &&
+                    (double)m * (double)m + (double)n * (double)n > ea.r2)
+                    pk |= 0x80000000u;
+                f_mn[rowoff[i] + j] = pk;
+            }
+        }
+        __syncthreads();
+    }
 
     if (warp >= kEpiWarps && warp < kMmaWarp) {
         // ============================== producers ==============================
-        // 4 groups of 64 threads; group gq produces every 4th stage, always into ring slot gq.
-        // In a group: side = A (threads 0-31) or B (32-63); lane -> (corner quad, slot block).
+        // group gq = warps (4 + 2 gq, 5 + 2 gq) fills stages sc = gq (mod 4) into ring slot sc % 5.
+        // Warp = one side (A: x-side weighted, B: y-side); lane -> (corner quad, 8-slot block).
         const int pt = tid - kEpiWarps * 32;
         const int gq = pt >> 6;
         const int sideB = (pt >> 5) & 1;
@@ -339,13 +398,14 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         const SidePlan sp = sideB ? plan.Y : plan.X;
         const int32_t *vsrc = sideB ? src.y : src.x;
         uint32_t sc = 0;                                  // global stage counter
+        int slot = 0;                                     // sc % kStages
+        uint32_t ph = 0;                                  // (sc / kStages) & 1
         for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
             const ItemInfo it = item_info(src, plan, item);
             const int p0 = (sideB ? it.tiy : it.tix) * 32 + j0;
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
                 const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
-                // this group's first slab in the chunk, and a one-slab-ahead register prefetch;
-                // 32-bit corner offsets relative to the chunk base keep the address math short
+                // 32-bit corner offsets relative to the chunk base; one-own-stage-ahead prefetch
                 const int n = (int)(c1 - c0);
                 const int32_t *vp = vsrc + c0;
                 const int32_t *wp = src.w + c0;
@@ -363,28 +423,36 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 int kr0 = first * kBK + 4 * quad;
                 fetch(kr0);
                 for (int64_t ks = c0; ks < c1; ks += kBK, ++sc) {
+                    const int my_slot = slot;
+                    const uint32_t my_ph = ph;
+                    if (++slot == kStages) { slot = 0; ph ^= 1; }
                     if ((int)(sc & 3) != gq) continue;
                     int32_t v[4];
                     float wt[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
-                    kr0 += 4 * kBK;
-                    fetch(kr0);
-                    mbar_wait(EMPTY(gq), ((sc >> 2) & 1) ^ 1);
-                    uint8_t *op = smem + L.stage0 + gq * kStageBytes + sideB * kOpBytes;
-                    produce<kFast>(op, quad, j0, p0, sp, v, wt, g, tab);
-                    fence_proxy_async();
-                    mbar_arrive(FULL(gq));
+                    kr0 += kGroups * kBK;
+                    if (!(plan.dbg & 16)) fetch(kr0);
+                    mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
+                    uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + sideB * kOpBytes;
+                    if (!(plan.dbg & 1)) produce<kFast>(op, quad, j0, p0, sp, v, wt, g, tab);
+                    if (!(plan.dbg & 8)) fence_proxy_async();
+                    __syncwarp();
+                    if (l == 0) mbar_arrive(FULL(my_slot));
                 }
             }
         }
     } else if (warp == kMmaWarp) {
         // ============================== MMA issuer ==============================
-        if (lane == 0) {
+        // The whole warp runs the (warp-uniform) loop and waits; one elected lane issues the
+        // MMAs and commits.  Descriptors are built once; a stage only adds its address offset.
+        {
             int stage = 0;
             uint32_t phase_bit = 0;
             uint32_t chunk_ctr = 0;
             const uint32_t smem_base = su32(smem + L.stage0);
+            const uint64_t adesc0 = umma_desc(smem_base), bdesc0 = umma_desc(smem_base + kOpBytes);
+            const bool no_mma = (plan.dbg & 2) != 0;
             for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
                 const ItemInfo it = item_info(src, plan, item);
                 for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
@@ -393,25 +461,45 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     mbar_wait(TEMPTY(b), ((chunk_ctr >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + b * 128;
-                    uint32_t acc = 0;
-                    for (int64_t ks = c0; ks < c1; ks += kBK) {
+                    const int nst = (int)((c1 - c0 + kBK - 1) / kBK);   // stages in this chunk
+                    // two stages per iteration: the barrier waits, fences and the elect are paid once
+                    // per 8 MMAs, so the single issuing warp stays ahead of the tensor pipe
+                    for (int st = 0; st < nst; st += 2) {
+                        const int two = (st + 1 < nst) ? 1 : 0;
+                        const int s1 = (stage + 1 == kStages) ? 0 : stage + 1;
+                        const uint32_t p1 = (stage + 1 == kStages) ? phase_bit ^ 1 : phase_bit;
                         mbar_wait(FULL(stage), phase_bit);
+                        if (two) mbar_wait(FULL(s1), p1);
                         tc_fence_after();
-                        const uint32_t a_addr = smem_base + stage * kStageBytes;
-                        const uint32_t b_addr = a_addr + kOpBytes;
+                        const uint64_t off0 = (uint64_t)((stage * kStageBytes) >> 4);
+                        const uint64_t off1 = (uint64_t)((s1 * kStageBytes) >> 4);
+                        if (elect_one()) {
+                            if (!no_mma) {
 #pragma unroll
-                        for (int u = 0; u < kBK / 8; ++u) {
-                            umma_tf32(d_tmem, umma_desc(a_addr + u * 32), umma_desc(b_addr + u * 32), acc);
-                            acc = 1;
+                                for (int u = 0; u < kBK / 8; ++u)
+                                    umma_tf32(d_tmem, adesc0 + off0 + 2 * u, bdesc0 + off0 + 2 * u,
+                                              (st > 0 || u > 0) ? 1u : 0u);
+                            }
+                            umma_commit(EMPTY(stage));
+                            if (two) {
+                                if (!no_mma) {
+#pragma unroll
+                                    for (int u = 0; u < kBK / 8; ++u)
+                                        umma_tf32(d_tmem, adesc0 + off1 + 2 * u, bdesc0 + off1 + 2 * u, 1u);
+                                }
+                                umma_commit(EMPTY(s1));
+                            }
                         }
-                        umma_commit(EMPTY(stage));
+                        __syncwarp();
+                        stage = two ? s1 : stage;
+                        phase_bit = two ? p1 : phase_bit;
                         if (++stage == kStages) { stage = 0; phase_bit ^= 1; }
                     }
-                    umma_commit(TFULL(b));
+                    if (elect_one()) umma_commit(TFULL(b));
+                    __syncwarp();
                 }
             }
         }
-        __syncwarp();
     } else {
         // ============================== epilogue ==============================
         const int L_ = tid;                          // TMEM lane = D row
@@ -428,10 +516,14 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 const uint32_t b = chunk_ctr & 1;
                 mbar_wait_sleep(TFULL(b), (chunk_ctr >> 1) & 1);
                 tc_fence_after();
+                if (plan.dbg & 4) {
+                    tc_fence_before();
+                    mbar_arrive(TEMPTY(b));
+                    continue;
+                }
                 const uint32_t tb = tmem_base + lane_base + b * 128;
                 // D[L][c] + D[L][64+c] for the 32 columns this row keeps and the 32 it sends
-                float *xb = xbuf + (chunk_ctr & 1) * (2 * 64 * kXStride);
-                float *XH = xb, *XL = xb + 64 * kXStride;
+                float *XH = xbuf, *XL = xbuf + 64 * kXStride;   // single buffer: barriers on both sides
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int col = 16 * q;          // columns col..col+15 (send half for q >= 2 if hi row)
@@ -457,41 +549,62 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 #pragma unroll
                     for (int i = 0; i < 32; ++i) acc[i] += (double)xsrc[r * kXStride + i];
                 }
+                named_bar(1, kEpiWarps * 32);   // exchange buffer free for the next chunk / the P tile
             }
+            if (plan.dbg & 4) continue;
             if (!fuse) {
                 double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
                 continue;
             }
-            // ---- fused a4 + a5: P tile -> SMEM (aliases the exchange buffer) -> this clip's outputs
-            double *Ps = (double *)xbuf;   // [64][65]
-            named_bar(1, kEpiWarps * 32);  // every thread is done with the exchange buffer
+            // ---- fused a4 + a5: P tile (fp32; |dP| <= 2^-24 of the per-term bound B) -> SMEM ->
+            // this clip's outputs.  Same arithmetic as coeff_from_P (coeff.cuh) with the 1/(4 pi^2 m n)
+            // and 1/(2 pi m T) factors taken from tables instead of divisions.
+            float *Ps = xbuf;              // [64][65]
 #pragma unroll
-            for (int i = 0; i < 32; ++i) Ps[r * 65 + (hi_row ? 0 : 32) + i] = acc[i];
+            for (int i = 0; i < 32; ++i) Ps[r * 65 + (hi_row ? 0 : 32) + i] = (float)acc[i];
             named_bar(1, kEpiWarps * 32);
             {
                 const int64_t clip = item;
                 const double dc = (double)(ea.area_dev ? ea.area_dev[clip] : ea.area_host) / ((double)ea.T * (double)ea.T);
-                auto get = [&](int px, int tx, int py, int ty) {
-                    return Ps[phys_row(px, tx, 1) * 65 + phys_row(py, ty, 1)];
-                };
                 const int W = rowoff[2 * ea.M + 1];
+                const int ax = plan.X.nf, ay = plan.Y.nf;          // axis pair slots (f0 == 1 here)
                 void *Fc = ea.out_f32 ? (void *)((float2 *)F + clip * ea.out_per_clip)
                                       : (void *)((double2 *)F + clip * ea.out_per_clip);
                 for (int o = tid; o < W; o += kEpiWarps * 32) {
-                    int lo = 0, hi = 2 * ea.M;          // row i with rowoff[i] <= o < rowoff[i+1]
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (rowoff[mid] <= o) lo = mid; else hi = mid - 1;
-                    }
-                    const int m = lo - ea.M;
-                    const int cnt = rowoff[lo + 1] - rowoff[lo];
-                    const int n = o - rowoff[lo] - (cnt - 1) / 2;
+                    const uint32_t pk = f_mn[o];
+                    int m = (int)((pk >> 16) & 0x7FFF) - ea.M, n = (int)(pk & 0xFFFF) - ea.N;
                     double2 v = make_double2(0.0, 0.0);
-                    if (!(ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0 &&
-                          (double)m * (double)m + (double)n * (double)n > ea.r2))
-                        v = coeff_from_P(get, plan.X, plan.Y, ea.T, m, n, dc);
+                    if (!(pk & 0x80000000u)) {
+                        if (m == 0 && n == 0) {
+                            v = make_double2(dc, 0.0);
+                        } else {
+                            const bool neg = (m < 0) || (m == 0 && n < 0);
+                            if (neg) { m = -m; n = -n; }
+                            double re, im;
+                            if (n == 0) {            // row c_m / s_m x axis column y (pair ay, t 0)
+                                const int pm = m - 1;
+                                const double sre = Ps[pm * 65 + ay], sim = -(double)Ps[(32 + pm) * 65 + ay];
+                                re = -sim * f_axm[m]; im = sre * f_axm[m];
+                            } else if (m == 0) {     // axis row x (pair ax) x columns c_n / s_n
+                                const int pn = n - 1;
+                                const double sre = Ps[ax * 65 + pn], sim = -(double)Ps[ax * 65 + 32 + pn];
+                                re = -sim * f_axn[n]; im = sre * f_axn[n];
+                            } else {
+                                const int an = n < 0 ? -n : n;
+                                const int pm = m - 1, pn = an - 1;
+                                const double pcc = Ps[pm * 65 + pn], pcs = Ps[pm * 65 + 32 + pn];
+                                const double psc = Ps[(32 + pm) * 65 + pn], pss = Ps[(32 + pm) * 65 + 32 + pn];
+                                double sre, sim;
+                                if (n > 0) { sre = pcc - pss; sim = -(psc + pcs); }
+                                else { sre = pcc + pss; sim = -(psc - pcs); }
+                                const double sc = f_rows[m] * (n > 0 ? f_invn[an] : -f_invn[an]);
+                                re = sre * sc; im = sim * sc;
+                            }
+                            v = make_double2(re, neg ? -im : im);
+                        }
+                    }
                     store_out(Fc, o, v, ea.out_f32);
                 }
             }
@@ -532,7 +645,8 @@ fcfs_status tf32_supported(const GemmPlan &plan, int32_t T) {
 
 bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea) {
     return plan.tiles_x == 1 && plan.tiles_y == 1 && plan.splits == 1 && ea.m_lo == -ea.M && ea.m_hi == ea.M &&
-           2 * ea.M + 1 < tc::kMaxFuseRows;
+           2 * ea.M + 1 < tc::kMaxFuseRows && 2 * ea.N + 1 < tc::kMaxFuseRows && plan.X.f0 == 1 &&
+           plan.Y.f0 == 1;
 }
 
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws, const EpiArgs *ea,

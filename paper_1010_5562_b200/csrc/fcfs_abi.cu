@@ -2,6 +2,7 @@
 // validation, planning, workspace carving and kernel launches on the caller's stream.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -148,6 +149,8 @@ static GemmPlan make_plan(int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int6
     p.B = B;
     p.items = B * tiles * splits;
     p.phys = 0;
+    const char *dbg = getenv("FCFS_DEBUG");
+    p.dbg = dbg ? atoi(dbg) : 0;
     return p;
 }
 
