@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3"])
+    ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3", "f16x3"])
     ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -56,6 +56,9 @@ typedef int32_t fcfs_precision;
 #define FCFS_FP64 0    /* FP64 throughout; output complex128 (double re, double im); |err| <= 1e-12 B */
 #define FCFS_TF32X3 1  /* split-TF32 tcgen05 tensor-core contraction, FP64 flush of FP32 TMEM partials;
                           output complex64 (float re, float im); |err| <= 1e-5 B                      */
+#define FCFS_F16X3 2   /* split-FP16 tcgen05 contraction (hi/lo fp16 operands, kind::f16, FP32 TMEM
+                          accumulation, FP64 flush): the same FP32-accurate contract as FCFS_TF32X3
+                          at half the operand bytes; output complex64; |err| <= 1e-5 B              */
 
 /* Output layout. */
 #define FCFS_LAYOUT_DENSE 0  /* (2M+1) x (2N+1) row-major, entry (m,n) at (m+M)*(2N+1) + (n+N);

@@ -1,5 +1,8 @@
-// contract_tf32.cu — a2 + a3 (split-TF32): the quadrant GEMM P = A diag(w) B^T on the
-// 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators in TMEM).
+// contract_tf32.cu — a2 + a3 (split-TF32 / split-FP16): the quadrant GEMM P = A diag(w) B^T on
+// the 5th-generation tensor cores (tcgen05.mma kind::tf32 or kind::f16, accumulators in TMEM).
+// kF16 = 0: operands tf32 hi/lo (4 B per value, 32 corners per stage);
+// kF16 = 1: operands fp16 hi/lo (2 B per value, 64 corners per stage, twice the MMA rate and half
+//           the shared-memory bytes per corner; same FP32-accurate tolerance 1e-5 B).
 //
 // Same product as contract_fp64.cu (Eq. Fkl P:843-846 / Steps 2-4 P:870-904, evaluated
 // directly as in P:917-920), FP32-accurate:
@@ -21,6 +24,8 @@
 //               4 groups of 2 warps (side A, side B), group g fills every 4th stage, so a group
 //               never waits for the consumption of the stage it produced last (ring > groups)
 //   warp 12     TMEM allocator + single-thread MMA issuer (tcgen05.mma / tcgen05.commit)
+#include <cuda_fp16.h>
+
 #include "coeff.cuh"
 
 namespace fcfs {
@@ -152,6 +157,22 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
         : "memory");
 }
+// instruction descriptor for kind::f16 with fp16 A/B (format 0), D=F32, K-major, N=128, M=128
+constexpr uint32_t kIdescF16 = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdescF16), "r"(accumulate)
+        : "memory");
+}
+template <int kF16>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    if (kF16) umma_f16(d_tmem, adesc, bdesc, accumulate);
+    else umma_tf32(d_tmem, adesc, bdesc, accumulate);
+}
+
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -297,9 +318,86 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
     }
 }
 
+__device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
+    __half2 h = __floats2half2_rn(lo_elem, hi_elem);   // .x (low 16 bits) = the lower K index
+    return *(uint32_t *)&h;
+}
+
+// FP16 producer task: 8 consecutive corners (16-byte chunk `oct` of the 64-corner stage) x 8
+// consecutive pair slots of one side.  hi = v with the mantissa cut to 10 bits (exact in fp16 for
+// normal values), lo = fp16(v - hi): |v - (hi + lo)| <= 2^-22 |v| + 2^-25 (fp16 subnormal step).
+// The axis slot carries the coordinate weight scaled by axs = 2^-s (exact) to stay in fp16
+// range; the epilogue multiplies the axis row / column of P back by 2^s.
 template <bool kFast>
+__device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0, const SidePlan &sp,
+                                            const int32_t v[8], const float wt[8], float axs, const TabGeom &g,
+                                            const float2 *tab) {
+    const uint32_t f0 = (uint32_t)(sp.f0 + p0);
+    float re[8], im[8], c1[8], s1[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float2 a = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[q], g), g, tab);
+        const float2 e = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[q], g), g, tab);
+        re[q] = wt[q] * a.x;
+        im[q] = wt[q] * a.y;
+        c1[q] = e.x;
+        s1[q] = e.y;
+    }
+    uint8_t *opq = op + (j0 >> 3) * 1024;
+    const uint32_t M13 = 0xFFFFE000u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t hc[4], hs[4], lc[4], ls[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const float r0 = re[2 * h], r1 = re[2 * h + 1], i0 = im[2 * h], i1 = im[2 * h + 1];
+            const float mr0 = __uint_as_float(__float_as_uint(r0) & M13), mr1 = __uint_as_float(__float_as_uint(r1) & M13);
+            const float mi0 = __uint_as_float(__float_as_uint(i0) & M13), mi1 = __uint_as_float(__float_as_uint(i1) & M13);
+            hc[h] = pack_h2(mr0, mr1);
+            hs[h] = pack_h2(mi0, mi1);
+            lc[h] = pack_h2(r0 - mr0, r1 - mr1);
+            ls[h] = pack_h2(i0 - mi0, i1 - mi1);
+        }
+        uint8_t *base = opq + i * kRowBytes + ((oct ^ i) << 4);   // row j0 + i (r % 8 == i)
+        *(uint4 *)(base) = make_uint4(hc[0], hc[1], hc[2], hc[3]);
+        *(uint4 *)(base + 4 * 1024) = make_uint4(hs[0], hs[1], hs[2], hs[3]);
+        *(uint4 *)(base + 8 * 1024) = make_uint4(lc[0], lc[1], lc[2], lc[3]);
+        *(uint4 *)(base + 12 * 1024) = make_uint4(ls[0], ls[1], ls[2], ls[3]);
+        if (i < 7) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float nr = fmaf(re[q], c1[q], -im[q] * s1[q]);
+                const float ni = fmaf(im[q], c1[q], re[q] * s1[q]);
+                re[q] = nr;
+                im[q] = ni;
+            }
+        }
+    }
+    const int ia = sp.nf - p0;
+    if (sp.axis && ia >= 0 && ia < 8) {
+        uint32_t hc[4], lc[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const float c0 = wt[2 * h] * (float)v[2 * h] * axs, cc1 = wt[2 * h + 1] * (float)v[2 * h + 1] * axs;
+            const float m0 = __uint_as_float(__float_as_uint(c0) & M13), m1 = __uint_as_float(__float_as_uint(cc1) & M13);
+            hc[h] = pack_h2(m0, m1);
+            lc[h] = pack_h2(c0 - m0, cc1 - m1);
+        }
+        uint8_t *base = opq + ia * kRowBytes + ((oct ^ ia) << 4);
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        *(uint4 *)(base) = make_uint4(hc[0], hc[1], hc[2], hc[3]);
+        *(uint4 *)(base + 4 * 1024) = z;
+        *(uint4 *)(base + 8 * 1024) = make_uint4(lc[0], lc[1], lc[2], lc[3]);
+        *(uint4 *)(base + 12 * 1024) = z;
+    }
+}
+
+template <bool kFast, int kF16>
 __global__ void __launch_bounds__(kThreads, 1)
-k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse) {
+k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse,
+            int axis_shift) {
+    constexpr int kBKp = kF16 ? 2 * kBK : kBK;          // corners per stage (one 128 B row of K)
+    constexpr int kCq = kF16 ? 8 : 4;                    // corners per 16-byte chunk (per producer task)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-align by offset arithmetic on the __shared__ array (keeps the shared address space, so
     // loads / stores compile to LDS / STS rather than generic LD / ST)
@@ -394,7 +492,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         const int gq = pt >> 6;
         const int sideB = (pt >> 5) & 1;
         const int l = pt & 31;
-        const int quad = l & 7, j0 = (l >> 3) << 3;
+        const int quad = l & 7, j0 = (l >> 3) << 3;      // quad: 16-byte chunk of the stage
+        const float axs = ldexpf(1.0f, -axis_shift);
         const SidePlan sp = sideB ? plan.Y : plan.X;
         const int32_t *vsrc = sideB ? src.y : src.x;
         uint32_t sc = 0;                                  // global stage counter
@@ -410,32 +509,35 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 const int32_t *vp = vsrc + c0;
                 const int32_t *wp = src.w + c0;
                 const int first = (gq - (int)(sc & 3)) & 3;
-                int32_t vn[4], wn[4];
+                int32_t vn[kCq], wn[kCq];
                 auto fetch = [&](int kr0) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
+                    for (int q = 0; q < kCq; ++q) {
                         const int kr = kr0 + q;
                         const bool ok = kr < n;
                         vn[q] = ok ? __ldg(vp + kr) : 0;
                         wn[q] = ok ? (sideB ? 1 : __ldg(wp + kr)) : 0;
                     }
                 };
-                int kr0 = first * kBK + 4 * quad;
+                int kr0 = first * kBKp + kCq * quad;
                 fetch(kr0);
-                for (int64_t ks = c0; ks < c1; ks += kBK, ++sc) {
+                for (int64_t ks = c0; ks < c1; ks += kBKp, ++sc) {
                     const int my_slot = slot;
                     const uint32_t my_ph = ph;
                     if (++slot == kStages) { slot = 0; ph ^= 1; }
                     if ((int)(sc & 3) != gq) continue;
-                    int32_t v[4];
-                    float wt[4];
+                    int32_t v[kCq];
+                    float wt[kCq];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
-                    kr0 += kGroups * kBK;
+                    for (int q = 0; q < kCq; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
+                    kr0 += kGroups * kBKp;
                     if (!(plan.dbg & 16)) fetch(kr0);
                     mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
                     uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + sideB * kOpBytes;
-                    if (!(plan.dbg & 1)) produce<kFast>(op, quad, j0, p0, sp, v, wt, g, tab);
+                    if (!(plan.dbg & 1)) {
+                        if constexpr (kF16) produce_f16<kFast>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
+                        else produce<kFast>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
+                    }
                     if (!(plan.dbg & 8)) fence_proxy_async();
                     __syncwarp();
                     if (l == 0) mbar_arrive(FULL(my_slot));
@@ -461,7 +563,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     mbar_wait(TEMPTY(b), ((chunk_ctr >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + b * 128;
-                    const int nst = (int)((c1 - c0 + kBK - 1) / kBK);   // stages in this chunk
+                    const int nst = (int)((c1 - c0 + kBKp - 1) / kBKp);   // stages in this chunk
                     // two stages per iteration: the barrier waits, fences and the elect are paid once
                     // per 8 MMAs, so the single issuing warp stays ahead of the tensor pipe
                     for (int st = 0; st < nst; st += 2) {
@@ -476,16 +578,16 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         if (elect_one()) {
                             if (!no_mma) {
 #pragma unroll
-                                for (int u = 0; u < kBK / 8; ++u)
-                                    umma_tf32(d_tmem, adesc0 + off0 + 2 * u, bdesc0 + off0 + 2 * u,
-                                              (st > 0 || u > 0) ? 1u : 0u);
+                                for (int u = 0; u < 4; ++u)   // 4 MMAs of 32 B of K (8 tf32 / 16 fp16)
+                                    umma<kF16>(d_tmem, adesc0 + off0 + 2 * u, bdesc0 + off0 + 2 * u,
+                                               (st > 0 || u > 0) ? 1u : 0u);
                             }
                             umma_commit(EMPTY(stage));
                             if (two) {
                                 if (!no_mma) {
 #pragma unroll
-                                    for (int u = 0; u < kBK / 8; ++u)
-                                        umma_tf32(d_tmem, adesc0 + off1 + 2 * u, bdesc0 + off1 + 2 * u, 1u);
+                                    for (int u = 0; u < 4; ++u)
+                                        umma<kF16>(d_tmem, adesc0 + off1 + 2 * u, bdesc0 + off1 + 2 * u, 1u);
                                 }
                                 umma_commit(EMPTY(s1));
                             }
@@ -550,6 +652,19 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     for (int i = 0; i < 32; ++i) acc[i] += (double)xsrc[r * kXStride + i];
                 }
                 named_bar(1, kEpiWarps * 32);   // exchange buffer free for the next chunk / the P tile
+            }
+            if (kF16 && axis_shift) {   // undo the fp16 range scaling of the axis row / column
+                const double up = ldexp(1.0, axis_shift);
+                const int ax_l = (plan.X.axis && plan.X.nf / 32 == it.tix) ? plan.X.nf % 32 : -1;
+                const int ay_l = (plan.Y.axis && plan.Y.nf / 32 == it.tiy) ? plan.Y.nf % 32 : -1;
+                if (r == ax_l) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] *= up;
+                }
+                const int cb = hi_row ? 0 : 32;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (cb + i == ay_l) acc[i] *= up;
             }
             if (plan.dbg & 4) continue;
             if (!fuse) {
@@ -650,7 +765,7 @@ bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea) {
 }
 
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws, const EpiArgs *ea,
-                             void *F, cudaStream_t s) {
+                             void *F, bool f16, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     const int fuse = (ea && F && tf32_can_fuse(plan, *ea)) ? 1 : 0;
     EpiArgs e{};
@@ -660,17 +775,25 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     const tc::Smem L = tc::smem_layout(entries);
     const size_t smem = L.total + 1024;
     const bool fast = g.single && g.pow2;
-    auto kern = fast ? tc::k_gemm_tf32<true> : tc::k_gemm_tf32<false>;
-    static size_t attr[2] = {0, 0};
-    if (smem > attr[fast]) {
+    auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1> : tc::k_gemm_tf32<false, 1>)
+                    : (fast ? tc::k_gemm_tf32<true, 0> : tc::k_gemm_tf32<false, 0>);
+    const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
+    static size_t attr[4] = {0, 0, 0, 0};
+    if (smem > attr[ki]) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[fast] = smem;
+        attr[ki] = smem;
+    }
+    // fp16 range: coordinate weights (<= T) of the axis slot are scaled by 2^-shift, T 2^-shift <= 256
+    int shift = 0;
+    if (f16) {
+        const int tb = ilog2_ceil((int64_t)T + 1);
+        shift = tb > 8 ? tb - 8 : 0;
     }
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = plan.items < sms ? plan.items : sms;
-    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse);
+    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse, shift);
     FCFS_CHECK_LAUNCH("k_gemm_tf32");
     return FCFS_OK;
 }

@@ -62,7 +62,7 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
 // contract_tf32.cu
 fcfs_status tf32_supported(const GemmPlan &plan, int32_t T);
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
-                             const EpiArgs *ea, void *F, cudaStream_t s);
+                             const EpiArgs *ea, void *F, bool f16, cudaStream_t s);
 bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 
 static fcfs_status device_ok() {
@@ -163,7 +163,7 @@ struct CoeffWs {
 static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m_lo, int32_t m_hi) {
     EpiArgs ea{};
     ea.M = M; ea.m_lo = m_lo; ea.m_hi = m_hi;
-    return prec == FCFS_TF32X3 && tf32_can_fuse(p, ea);
+    return (prec == FCFS_TF32X3 || prec == FCFS_F16X3) && tf32_can_fuse(p, ea);
 }
 
 static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P = true) {
@@ -195,11 +195,12 @@ static fcfs_status run_gemm(const CornerSrc &src, const GemmPlan &plan, int32_t 
                             double *P, const EpiArgs &ea, void *F, cudaStream_t s, bool *fused) {
     *fused = false;
     if (prec == FCFS_FP64) return launch_gemm_fp64(src, plan, T, P, s);
-    if (prec == FCFS_TF32X3) {
+    if (prec == FCFS_TF32X3 || prec == FCFS_F16X3) {
         fcfs_status st = tf32_supported(plan, T);
         if (st != FCFS_OK) return st;
         *fused = tf32_can_fuse(plan, ea);
-        return launch_gemm_tf32(src, plan, T, P, &ea, F, s);   // P in phys layout 1 when not fused
+        // P in phys layout 1 when not fused
+        return launch_gemm_tf32(src, plan, T, P, &ea, F, prec == FCFS_F16X3, s);
     }
     set_error("bad precision %d", prec);
     return FCFS_E_INVALID;
@@ -316,7 +317,10 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     fcfs_status st = check_window(win);
     if (st != FCFS_OK) return st;
     if (K < 0 || (K > 0 && (!x || !y || !w)) || !F) { set_error("fcfs_coeffs: null pointer or K < 0"); return FCFS_E_INVALID; }
-    if (prec != FCFS_FP64 && prec != FCFS_TF32X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) {
+        set_error("bad precision %d", prec);
+        return FCFS_E_INVALID;
+    }
     int32_t m_lo, m_hi;
     st = resolve_rows(win, shard, m_lo, m_hi);
     if (st != FCFS_OK) return st;
@@ -334,7 +338,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     st = device_ok();
     if (st != FCFS_OK) return st;
     GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
-    plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
+    plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi));
@@ -343,7 +347,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     EpiArgs ea;
     ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
     ea.m_lo = m_lo; ea.m_hi = m_hi; ea.T = T; ea.area_dev = nullptr; ea.area_host = area;
-    ea.out_f32 = prec == FCFS_TF32X3 ? 1 : 0;
+    ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = 0;
     if (vblock) {
         st = launch_block_area(src, W.area, s);
@@ -382,12 +386,15 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
         set_error("fcfs_coeffs_batched: invalid sizes or null pointers");
         return FCFS_E_INVALID;
     }
-    if (prec != FCFS_FP64 && prec != FCFS_TF32X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) {
+        set_error("bad precision %d", prec);
+        return FCFS_E_INVALID;
+    }
     if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
     st = device_ok();
     if (st != FCFS_OK) return st;
     GemmPlan plan = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
-    plan.phys = prec == FCFS_TF32X3 ? 1 : 0;
+    plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M));
@@ -398,7 +405,7 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     EpiArgs ea;
     ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
     ea.m_lo = -win->M; ea.m_hi = win->M; ea.T = T; ea.area_dev = area; ea.area_host = 0;
-    ea.out_f32 = prec == FCFS_TF32X3 ? 1 : 0;
+    ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = fcfs_window_size(win);
     bool fused = false;
     {

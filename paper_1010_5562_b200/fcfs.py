@@ -25,10 +25,10 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 FCFS_OK, E_INVALID, E_RANGE, E_CAPACITY, E_WORKSPACE, E_UNSUPPORTED, E_CUDA = range(7)
-FP64, TF32X3 = 0, 1
+FP64, TF32X3, F16X3 = 0, 1, 2
 LAYOUT_DENSE, LAYOUT_PUPIL = 0, 1
 SHARD_NONE, SHARD_ROWS, SHARD_VERTEX_BLOCK = 0, 1, 2
-_PREC = {"fp64": FP64, "tf32x3": TF32X3, FP64: FP64, TF32X3: TF32X3}
+_PREC = {"fp64": FP64, "tf32x3": TF32X3, "f16x3": F16X3, FP64: FP64, TF32X3: TF32X3, F16X3: F16X3}
 _LAYOUT = {"dense": LAYOUT_DENSE, "pupil": LAYOUT_PUPIL, LAYOUT_DENSE: LAYOUT_DENSE, LAYOUT_PUPIL: LAYOUT_PUPIL}
 
 

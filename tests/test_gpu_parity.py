@@ -14,7 +14,7 @@ from paper_1010_5562_b200 import inputs
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp64": 1e-12, "tf32x3": 1e-5}
+TOL = {"fp64": 1e-12, "tf32x3": 1e-5, "f16x3": 1e-5}
 
 
 @pytest.fixture(scope="module")
@@ -123,7 +123,8 @@ def _oracle_window(g, T, M, N, r2=-1.0, layout="dense"):
     return ms, ns, F, B
 
 
-@pytest.mark.parametrize("cfg,prec", [("c1", "fp64"), ("c2", "fp64"), ("c1", "tf32x3"), ("c2", "tf32x3")])
+@pytest.mark.parametrize("cfg,prec", [("c1", "fp64"), ("c2", "fp64"), ("c1", "tf32x3"), ("c2", "tf32x3"),
+                                      ("c1", "f16x3"), ("c2", "f16x3")])
 def test_full_window_parity(fcfs, cfg, prec):
     wl = inputs.make(cfg)
     g, F = _clip_coeffs(fcfs, wl, prec)
@@ -134,7 +135,7 @@ def test_full_window_parity(fcfs, cfg, prec):
     assert np.array_equal(Fm.real, F.real) and np.array_equal(Fm.imag, -F.imag)
 
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_ragged_sizes_and_tiny_windows(fcfs, prec):
     # several tiles along both sides with ragged tails, non-power-of-two T, M != N, M = 0 / N = 0
     wl = inputs.c2(seed=7, n_poly=150, T=3000)
@@ -144,7 +145,7 @@ def test_ragged_sizes_and_tiny_windows(fcfs, prec):
         _assert_parity(F, Fr, B, prec, f"M={M} N={N}", ms, ns)
 
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_pupil_layouts_single_clip(fcfs, prec):
     wl = inputs.c1(seed=1)
     r2 = 300.5
@@ -154,7 +155,7 @@ def test_pupil_layouts_single_clip(fcfs, prec):
         _assert_parity(F, Fr, B, prec, f"pupil/{layout}", ms, ns)
 
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_empty_corner_list(fcfs, prec):
     x = torch.zeros(0, dtype=torch.int32, device="cuda")
     F = fcfs.coeffs(x, x, x, 0, 64, 3, 3, prec=prec)
@@ -164,7 +165,7 @@ def test_empty_corner_list(fcfs, prec):
 
 # ------------------------------------------------------------------ a6 building blocks: shards on one GPU
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_row_shards_concatenate_to_full(fcfs, prec):
     wl = inputs.c2(seed=3, n_poly=400)
     g = _gpu_extract(fcfs, wl)
@@ -181,7 +182,7 @@ def test_row_shards_concatenate_to_full(fcfs, prec):
     _assert_parity(full, Fr, B, prec, "full", ms, ns)
 
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_vertex_blocks_sum_to_full(fcfs, prec):
     wl = inputs.c2(seed=4, n_poly=600)
     g = _gpu_extract(fcfs, wl)
@@ -207,7 +208,7 @@ def test_vertex_blocks_sum_to_full(fcfs, prec):
 
 # ------------------------------------------------------------------ batched clips (a5)
 
-@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_batched_pupil_clips(fcfs, prec):
     wl = inputs.c3(clips=24)
     g = _gpu_extract(fcfs, wl)
@@ -242,7 +243,8 @@ def _sample_indices(M, N, n_rand=384, seed=0):
     return np.array([p[0] for p in pts], np.int32), np.array([p[1] for p in pts], np.int32)
 
 
-@pytest.mark.parametrize("cfg,prec", [("c4", "fp64"), ("c5", "fp64"), ("c4", "tf32x3"), ("c5", "tf32x3")])
+@pytest.mark.parametrize("cfg,prec", [("c4", "fp64"), ("c5", "fp64"), ("c4", "tf32x3"), ("c5", "tf32x3"),
+                                      ("c4", "f16x3"), ("c5", "f16x3")])
 def test_full_size_sampled(fcfs, cfg, prec):
     wl = inputs.make(cfg)
     g, F = _clip_coeffs(fcfs, wl, prec)
@@ -255,13 +257,14 @@ def test_full_size_sampled(fcfs, cfg, prec):
     assert np.array_equal(F[::-1].real, F.real) and np.array_equal(F[::-1].imag, -F.imag)
 
 
-def test_batched_full_c3_sampled_clips(fcfs):
+@pytest.mark.parametrize("prec", ["tf32x3", "f16x3"])
+def test_batched_full_c3_sampled_clips(fcfs, prec):
     """BASELINE configs[2] at full size (4096 clips) in the launch configuration bench.py
-    times (batched, pupil, TF32X3); the oracle checks a seeded sample of clips."""
+    times (batched, pupil, split precision); the oracle checks a seeded sample of clips."""
     wl = inputs.c3(clips=4096)
     g = _gpu_extract(fcfs, wl)
     F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], wl.T, wl.M, wl.N, wl.r2,
-                            "pupil", "tf32x3").cpu().numpy()
+                            "pupil", prec).cpu().numpy()
     ms, ns = oracle.window(wl.M, wl.N, wl.r2)
     cp = g["corner_ptr"].cpu().numpy()
     x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
@@ -270,5 +273,5 @@ def test_batched_full_c3_sampled_clips(fcfs):
     for b in sorted(set([0, 4095] + rng.integers(0, 4096, 6).tolist())):
         sl = slice(cp[b], cp[b + 1])
         Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], wl.T, ms, ns)
-        _assert_parity(F[b], Fr, B, "tf32x3", f"c3 clip {b}", ms, ns)
+        _assert_parity(F[b], Fr, B, prec, f"c3 clip {b}", ms, ns)
     assert np.all(np.isfinite(F))

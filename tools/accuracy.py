@@ -26,7 +26,7 @@ def main():
         cp = g["corner_ptr"].cpu().numpy()
         x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
         area = g["area"].cpu().numpy()
-        for prec in ["fp64", "tf32x3"]:
+        for prec in ["fp64", "tf32x3", "f16x3"]:
             F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], wl.T, wl.M, wl.N, wl.r2,
                                     layout, prec).cpu().numpy().astype(np.complex128)
             worst = 0.0
