@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3", "f16x3"])
     ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
+    ap.add_argument("--shard", default="rows", choices=["rows", "vblock"],
+                    help="single-clip configs (c1, c2, c4, c5) on N > 1 GPUs: frequency rows + all_gather, "
+                         "or vertex blocks + reduce_scatter")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -181,12 +184,24 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def traffic_for(cfg, prec):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/traffic.json), or None when no capture matches this config / precision."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t.get(f"{cfg}/{prec}")
+    except Exception:
+        return None
+
+
 def config_dict(args, wl, prec, world):
     W = inputs.window_count(wl.M, wl.N, wl.r2)
     d = {"workload": f"{wl.name}: T={wl.T}, {wl.B} clip(s)/GPU, R={wl.R} rects/GPU, window |m|,|n|<={wl.M}"
                      + (f" pupil r2={wl.r2:.2f}" if wl.r2 >= 0 else "") + f", W_out={W}/clip",
          "T": wl.T, "clips_per_gpu": wl.B, "rects_per_gpu": wl.R, "M": wl.M, "N": wl.N, "W_out": W,
-         "precision": prec, "parallelism": f"clip-sharded x{world}" if wl.B > 1 else f"replicas x{world}",
+         "precision": prec,
+         "parallelism": (f"clip-sharded x{world}" if wl.B > 1 else
+                         (f"{args.shard}-sharded x{world}" if world > 1 else "single GPU")),
          "l2": "flushed between steps (512 MiB write, outside the timed events)"}
     return d
 
@@ -231,6 +246,22 @@ def main():
         def coeffs():
             return plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area)
         out_bytes = plan.out.numel() * plan.out.element_size()
+    elif world > 1:
+        # one clip on N GPUs: every rank extracts the clip (same canonical corner list), computes its
+        # shard and the collective assembles the full window (strong scaling)
+        from paper_1010_5562_b200 import dist as fdist
+        area_h = int(vp.area[0].item())
+        full_n = (2 * wl.M + 1) * (2 * wl.N + 1)
+
+        class _P:
+            out = torch.empty(full_n, dtype=torch.complex128 if prec == "fp64" else torch.complex64, device=dev)
+        plan = _P()
+
+        def coeffs():
+            if args.shard == "rows":
+                return fdist.coeffs_rows_sharded(vp.x[:K], vp.y[:K], vp.w[:K], area_h, wl.T, wl.M, wl.N, prec)
+            return fdist.coeffs_vertex_sharded(vp.x[:K], vp.y[:K], vp.w[:K], wl.T, wl.M, wl.N, prec)
+        out_bytes = plan.out.numel() * plan.out.element_size()
     else:
         plan = fcfs.CoeffsPlan(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
         area_h = int(vp.area[0].item())
@@ -239,6 +270,9 @@ def main():
             return plan.run(vp.x[:K], vp.y[:K], vp.w[:K], area_h)
         out_bytes = plan.out.numel() * plan.out.element_size()
     terms = float(W) * float(K)                     # per rank per step
+    single_sharded = wl.B == 1 and world > 1
+    if single_sharded:
+        terms /= world                              # one clip split over the ranks: value = total terms / time
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step():
@@ -292,13 +326,19 @@ def main():
         peak_note = (f"TF32 dense = {src} bf16 {peaks['bf16_tflops']} x (1.1/2.25 nominal ratio) = {tf32:.1f} "
                      f"TF/s, / 3 (split-TF32: 3 TF32 MMAs per FP32-accurate product)")
         bound = "tensor"
+    elif prec == "f16x3":
+        peak = peaks["bf16_tflops"] / 3.0
+        peak_note = (f"FP16 dense = {src} bf16 {peaks['bf16_tflops']} TF/s (same nominal rate), / 3 "
+                     f"(split-FP16: 3 FP16 MMAs per FP32-accurate product)")
+        bound = "tensor"
     else:
         mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
         peak_note = f"FP64 DFMA: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived, B200 FP64 = 1/2 FP32 rate)"
         bound = "alu"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None, "kernel": "k_gemm_" + prec,
+            "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec),
+            "kernel": "k_gemm_" + prec,
             "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
             "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()}}
 
@@ -328,7 +368,7 @@ def main():
     if rank == 0:
         line = {"metric": "fourier_coeff_vertex_terms_per_sec", "value": round(value, 3), "unit": "Gterm/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong" if single_sharded else "weak", "vs_baseline": None,
                 "dtype": "tf32x3 (split-TF32, FP32-accurate; FP64 flush)" if prec == "tf32x3" else "f64",
                 "data": "synthetic", "config": config_dict(args, wl, prec, world),
                 "K_per_gpu": int(K), "terms_per_step_per_gpu": terms,

@@ -369,11 +369,10 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
                       int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t *counts, int64_t *area,
                       int32_t *err) {
     extern __shared__ __align__(16) unsigned char bsm[];
-    uint16_t *bx = (uint16_t *)bsm;                     // [cap] bucketed (unsorted) x
-    uint16_t *by = bx + kBucketCap;                     // [cap] bucket y
-    int16_t *bw = (int16_t *)(by + kBucketCap);         // [cap] bucketed weight
-    uint32_t *syx = (uint32_t *)(bw + kBucketCap);      // [cap] sorted (y << 16 | x)
-    int16_t *sw = (int16_t *)(syx + kBucketCap);        // [cap] sorted merged weight (0 = dropped)
+    uint32_t *bxw = (uint32_t *)bsm;                    // [cap] bucketed (x << 16 | w & 0xFFFF); later compacted (y << 16 | x)
+    uint32_t *syx = bxw + kBucketCap;                   // [cap] sorted (y << 16 | x)
+    int16_t *by = (int16_t *)(syx + kBucketCap);        // [cap] bucket y; later compacted weights
+    int16_t *sw = by + kBucketCap;                      // [cap] sorted merged weight (0 = dropped)
     int32_t *hist = (int32_t *)(sw + kBucketCap);       // [T + 2]: bucket start, then bucket end
     __shared__ int32_t wsum[kBucketThreads / 32];
     __shared__ long long asum[kBucketThreads / 32];
@@ -426,11 +425,11 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             if (!rok[j]) continue;
             const int4 q = rq[j];
             int p = atomicAdd(&hist[q.y], 2);
-            bx[p] = (uint16_t)q.x; by[p] = (uint16_t)q.y; bw[p] = 1;
-            bx[p + 1] = (uint16_t)q.z; by[p + 1] = (uint16_t)q.y; bw[p + 1] = -1;
+            bxw[p] = ((uint32_t)q.x << 16) | 0x0001u;       by[p] = (int16_t)q.y;
+            bxw[p + 1] = ((uint32_t)q.z << 16) | 0xFFFFu;   by[p + 1] = (int16_t)q.y;
             p = atomicAdd(&hist[q.w], 2);
-            bx[p] = (uint16_t)q.x; by[p] = (uint16_t)q.w; bw[p] = -1;
-            bx[p + 1] = (uint16_t)q.z; by[p + 1] = (uint16_t)q.w; bw[p + 1] = 1;
+            bxw[p] = ((uint32_t)q.x << 16) | 0xFFFFu;       by[p] = (int16_t)q.w;
+            bxw[p + 1] = ((uint32_t)q.z << 16) | 0x0001u;   by[p + 1] = (int16_t)q.w;
         }
         __syncthreads();
         const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
@@ -438,13 +437,17 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         for (int i = threadIdx.x; i < nv; i += kBucketThreads) {
             const int y = by[i];
             const int st = y ? hist[y - 1] : 0, en = hist[y];
-            const uint16_t xi = bx[i];
+            const uint32_t xi = bxw[i] >> 16;
             int rank = 0, wv = 0;
             bool first = true;
+#pragma unroll 2
             for (int j = st; j < en; ++j) {
-                const uint16_t xj = bx[j];
-                rank += (xj < xi) || (xj == xi && j < i);
-                if (xj == xi) { wv += bw[j]; first &= !(j < i); }
+                const uint32_t v = bxw[j];
+                const uint32_t xj = v >> 16;
+                const bool eq = xj == xi, before = j < i;
+                rank += (xj < xi) | (eq & before);
+                wv += eq ? (int)(int16_t)(v & 0xFFFFu) : 0;
+                first &= !(eq & before);
             }
             syx[st + rank] = ((uint32_t)y << 16) | xi;
             sw[st + rank] = first ? (int16_t)wv : (int16_t)0;
@@ -455,32 +458,38 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
         int cnt = 0;
         long long a = 0;
-        for (int i = lo; i < hi; ++i)
-            if (sw[i] != 0) {
+        for (int i = lo; i < hi; ++i) {
+            const int16_t wv = sw[i];
+            if (wv != 0) {
                 ++cnt;
-                a += (long long)sw[i] * (long long)(syx[i] & 0xFFFFu) * (long long)(syx[i] >> 16);
+                a += (long long)wv * (long long)(syx[i] & 0xFFFFu) * (long long)(syx[i] >> 16);
             }
+        }
         int incl = cnt;
         for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        __syncthreads();                                // wsum reuse
+        __syncthreads();                                // wsum reuse; bxw / by are free from here
         if (lane == 31) wsum[wid] = incl;
         if (lane == 0) asum[wid] = a;
         __syncthreads();
         int outp = incl - cnt;
         for (int i = 0; i < wid; ++i) outp += wsum[i];
-        const int64_t base = 4 * r0;
-        for (int i = lo; i < hi; ++i)
-            if (sw[i] != 0) {
-                xs[base + outp] = (int32_t)(syx[i] & 0xFFFFu);
-                ys[base + outp] = (int32_t)(syx[i] >> 16);
-                ws[base + outp] = sw[i];
-                ++outp;
-            }
+        for (int i = lo; i < hi; ++i) {
+            const int16_t wv = sw[i];
+            if (wv != 0) { bxw[outp] = syx[i]; by[outp] = wv; ++outp; }
+        }
         if (threadIdx.x == kBucketThreads - 1) tot_s = outp;     // the last thread ends at the clip total
         __syncthreads();
+        const int total = tot_s;
+        const int64_t base = 4 * r0;
+        for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores
+            const uint32_t yx = bxw[i];
+            xs[base + i] = (int32_t)(yx & 0xFFFFu);
+            ys[base + i] = (int32_t)(yx >> 16);
+            ws[base + i] = by[i];
+        }
         if (threadIdx.x == 0) {
-            counts[b] = tot_s;
+            counts[b] = total;
             long long t = 0;
             for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
             area[b] = t;

@@ -275,3 +275,31 @@ def test_batched_full_c3_sampled_clips(fcfs, prec):
         Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], wl.T, ms, ns)
         _assert_parity(F[b], Fr, B, prec, f"c3 clip {b}", ms, ns)
     assert np.all(np.isfinite(F))
+
+
+# ------------------------------------------------------------------ a6: NCCL path (world size 1 on the one GPU)
+
+def test_nccl_sharded_paths_world1(fcfs):
+    import socket
+    import torch.distributed as dist
+    from paper_1010_5562_b200 import dist as fdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        wl = inputs.c2(seed=9, n_poly=300)
+        g = _gpu_extract(fcfs, wl)
+        area = int(g["area"][0].item())
+        for prec in ("fp64", "tf32x3"):
+            full = fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, 20, 20, prec=prec)
+            rows = fdist.coeffs_rows_sharded(g["x"], g["y"], g["w"], area, wl.T, 20, 20, prec=prec)
+            vb = fdist.coeffs_vertex_sharded(g["x"], g["y"], g["w"], wl.T, 20, 20, prec=prec)
+            torch.cuda.synchronize()
+            assert torch.equal(rows, full)
+            ms, ns, Fr, B = _oracle_window(g, wl.T, 20, 20)
+            _assert_parity(vb.cpu().numpy(), Fr, B, prec, f"vblock/{prec}", ms, ns)
+    finally:
+        dist.destroy_process_group()
