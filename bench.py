@@ -332,10 +332,14 @@ def main():
                      f"(split-FP16: 3 FP16 MMAs per FP32-accurate product)")
         bound = "tensor"
     else:
-        mhz = peaks.get("sm_max_mhz", 1965.0)
-        peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
-        peak_note = f"FP64 DFMA: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived, B200 FP64 = 1/2 FP32 rate)"
-        bound = "alu"
+        try:
+            peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_m16n8k16_tflops"]
+            peak_note = "FP64 tensor (DMMA m16n8k16) measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json)"
+        except Exception:
+            mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
+            peak_note = f"FP64: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived)"
+        bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec),
             "kernel": "k_gemm_" + prec,

@@ -14,8 +14,8 @@
 // two-level table E(r) = E_hi(r >> L) * E_lo(r & (2^L - 1)) built in SMEM with sincospi,
 // so the twiddle matrices never touch HBM ("no full-length arrays").
 //
-// a3 (FP64): CUDA-core DFMA, 64x64 P tile per CTA, 4x4 register tile per thread,
-// double-buffered slabs of 16 corners.  Accumulation is hierarchical: a fresh register
+// a3 (FP64): FP64 tensor cores (mma.sync m16n8k16 .f64, SASS DMMA), 64x64 P tile per CTA,
+// 8 warps of 16x32, double-buffered slabs of 16 corners (one k16 MMA step per slab).  Accumulation is hierarchical: a fresh register
 // accumulator per chunk of <= kChunk corners is added into a running total, bounding
 // the rounding error by about (kChunk + K/kChunk) u B instead of K u B.
 #include "common.cuh"
@@ -25,10 +25,6 @@ namespace fcfs {
 static constexpr int kBK = 16;        // corners per slab
 static constexpr int kChunk = 2048;   // corners per register accumulator
 static constexpr int kThreads = 256;  // 16 x 16 threads, 4x4 outputs each
-
-struct TabPtrs {
-    double2 *hi, *lo;
-};
 
 __device__ __forceinline__ void build_tables(const TwiddleGeom &g, double2 *thi, double2 *tlo) {
     const int L = 1 << g.lbits;
@@ -65,19 +61,35 @@ __device__ __forceinline__ double2 side_pair(int p_global, const SidePlan &sp, i
     return make_double2(0.0, 0.0);
 }
 
+// FP64 tensor-core MMA (DMMA): D[16x8] += A[16x16] B[16x8], fragments per the sm_90+/sm_100
+// mma.sync.m16n8k16.f64 layout (g = lane / 4, t = lane % 4):
+//   a[j] = A[g + 8 (j & 1)][t + 4 (j >> 1)],  b[v] = B[t + 4 v][g],  c[v] = C[g + 8 (v >> 1)][2 t + (v & 1)]
+__device__ __forceinline__ void dmma16816(double (&d)[4], const double (&a)[8], const double (&b)[4]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+        "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+          "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+static constexpr int kLd = kTile + 4;   // padded smem row (doubles): conflict-free fragment loads
+
 __global__ void __launch_bounds__(kThreads, 2)
 k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_ws) {
     extern __shared__ __align__(16) double smem_d[];
     double2 *thi = (double2 *)smem_d;
     double2 *tlo = thi + g.nhi;
-    double *As = (double *)(tlo + (1 << g.lbits));   // [2][kBK][64]
-    double *Bs = As + 2 * kBK * kTile;               // [2][kBK][64]
+    double *As = (double *)(tlo + (1 << g.lbits));   // [2][kBK][kLd]
+    double *Bs = As + 2 * kBK * kLd;                 // [2][kBK][kLd]
 
     build_tables(g, thi, tlo);
 
     const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;          // output rows 4tx.., cols 4ty..
-    const int gp = tid & 31, gk = tid >> 5;          // generation: pair gp, corner gk (+8)
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;   // warp tile 16 x 32 (4 MMAs of n8)
+    const int lg = lane >> 2, lt = lane & 3;
+    const int gp = tid & 31, gk = tid >> 5;                  // generation: pair gp, corner gk (+8)
     const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
 
     for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
@@ -112,8 +124,8 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                 double2 a = side_pair(tix * (kTile / 2) + gp, plan.X, xv, wv, g, thi, tlo);
                 double2 b = side_pair(tiy * (kTile / 2) + gp, plan.Y, yv, 1.0, g, thi, tlo);
                 if (k >= kend) b = make_double2(0.0, 0.0);
-                *(double2 *)&As[(buf * kBK + kk) * kTile + 2 * gp] = a;
-                *(double2 *)&Bs[(buf * kBK + kk) * kTile + 2 * gp] = b;
+                *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
+                *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = b;
             }
         };
 
@@ -128,20 +140,17 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
             __syncthreads();
             for (int64_t ks = c0; ks < c1; ks += kBK) {
                 if (ks + kBK < c1) generate(buf ^ 1, ks + kBK, c1);
-                const double *Ab = As + buf * kBK * kTile + 4 * tx;
-                const double *Bb = Bs + buf * kBK * kTile + 4 * ty;
+                const double *Ab = As + buf * kBK * kLd;
+                const double *Bb = Bs + buf * kBK * kLd;
+                double a[8];
 #pragma unroll
-                for (int kk = 0; kk < kBK; ++kk) {
-                    double2 a01 = *(const double2 *)(Ab + kk * kTile);
-                    double2 a23 = *(const double2 *)(Ab + kk * kTile + 2);
-                    double2 b01 = *(const double2 *)(Bb + kk * kTile);
-                    double2 b23 = *(const double2 *)(Bb + kk * kTile + 2);
-                    double a[4] = {a01.x, a01.y, a23.x, a23.y};
-                    double b[4] = {b01.x, b01.y, b23.x, b23.y};
+                for (int j = 0; j < 8; ++j) a[j] = Ab[(lt + 4 * (j >> 1)) * kLd + wm + lg + 8 * (j & 1)];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                for (int t = 0; t < 4; ++t) {
+                    double bf[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                    for (int v = 0; v < 4; ++v) bf[v] = Bb[(lt + 4 * v) * kLd + wn + 8 * t + lg];
+                    dmma16816(acc[t], a, bf);
                 }
                 __syncthreads();
                 buf ^= 1;
@@ -154,10 +163,10 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
         }
         double *out = P_ws + item * (int64_t)(kTile * kTile);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            double *row = out + (4 * tx + i) * kTile + 4 * ty;
-            *(double2 *)row = make_double2(tot[i][0], tot[i][1]);
-            *(double2 *)(row + 2) = make_double2(tot[i][2], tot[i][3]);
+        for (int t = 0; t < 4; ++t) {
+            const int col = wn + 8 * t + 2 * lt;
+            *(double2 *)(out + (wm + lg) * kTile + col) = make_double2(tot[t][0], tot[t][1]);
+            *(double2 *)(out + (wm + lg + 8) * kTile + col) = make_double2(tot[t][2], tot[t][3]);
         }
     }
 }
@@ -166,7 +175,7 @@ fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t
                              cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     TwiddleGeom g = make_twiddle_geom(T);
-    size_t smem = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kTile;
+    size_t smem = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kLd;
     static bool attr = false;
     if (!attr) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));

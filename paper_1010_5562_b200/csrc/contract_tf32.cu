@@ -112,7 +112,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int spi
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
     while (!mbar_try(bar, parity)) {
-        __nanosleep(128);
+        __nanosleep(1024);
         if (++n > (1u << 24)) __trap();
     }
 }
