@@ -82,12 +82,32 @@ __host__ __device__ inline int phys_row(int p, int t, int phys) {
     return tile * kTile + (phys ? pp + (kTile / 2) * t : 2 * pp + t);
 }
 
-// Corner source of one contraction: either one clip [k_lo, k_hi) or B clips by CSR.
+// Corner source of one contraction: either one clip [k_lo, k_hi) or B clips by CSR, plus its
+// row buckets (buckets.cu): the contraction runs over buckets, bucket b = corners
+// [bptr[b], bptr[b+1]) sharing the row by[b]; clip c owns buckets [clip_bptr[c], clip_bptr[c+1]).
 struct CornerSrc {
     const int32_t *x, *y, *w;
     const int64_t *corner_ptr;   // device CSR [B+1] or nullptr
     int64_t k_lo, k_hi;          // used when corner_ptr == nullptr
+    const int32_t *bptr, *by;    // [nb+1], [nb] (workspace, padded for 16-byte bulk copies)
+    const int64_t *clip_bptr;    // [B+1] (B = 1 for a single range)
+    int64_t kend;                // length of the x / w arrays (bulk copies stay below kend & ~3)
 };
+
+// row-bucket workspace and pass (buckets.cu)
+struct BucketWs {
+    int32_t *bptr, *by;
+    int64_t *clip_bptr;
+    int32_t *counts, *offs;
+    void *cub_tmp;
+    size_t cub_bytes;
+};
+void carve_buckets(Carver &cv, int64_t K, int64_t B, BucketWs &w);
+size_t buckets_workspace_bytes(int64_t K, int64_t B);
+fcfs_status run_buckets(const int32_t *y, const int64_t *corner_ptr, int64_t B, int64_t k_lo, int64_t k_hi,
+                        int32_t cap, const BucketWs &w, cudaStream_t s);
+static constexpr int kRowBucketCapFp64 = 32;   // max corners per bucket (the FP64 kernel walks a bucket
+                                               // warp-uniformly: 32 pairs of one bucket per warp)
 
 struct EpiArgs {
     int32_t M, N, layout;

@@ -1,29 +1,33 @@
-// contract_fp64.cu — a2 + a3 (FP64): generated-operand real GEMM P = A diag(w) B^T.
+// contract_fp64.cu — a2 + a3 (FP64): generated-operand real GEMM over ROW BUCKETS.
 //
 // The interior coefficients of Eq. Fkl are the 2-D DFT of the
 // sparse +-1 image f~_xy (Step 4), evaluated directly ("Goertzel-like",
 // P:917-920) on a low-pass window.  Writing E = c - i s, the complex sum
 // sum_k w_k E_x[m,k] E_y[n,k] for (m, +-n) is recombined from the four real quadrant
-// products P_cc, P_cs, P_sc, P_ss of
-//     A[2j  ,k] = w_k cos(2 pi m_j x_k / T),   A[2j+1,k] = w_k sin(...),   A[2nf,k] = w_k x_k
-//     B[2j  ,k] =     cos(2 pi n_j y_k / T),   B[2j+1,k] =     sin(...),   B[2nf,k] = y_k
-// (the last rows carry the axis sums of Eqs. Fk0/F0l, Steps 2-3 P:870-888).
+// products P_cc, P_cs, P_sc, P_ss.  Step 4's row structure (corners on one row y share
+// E_y[n, y]) turns the sum over K corners into a sum over the R row buckets of buckets.cu:
+//     A[2j  ,b] = sum_{k in b} w_k cos(2 pi m_j x_k / T),  A[2j+1,b] = sum_{k in b} w_k sin(...),
+//     A[2nf ,b] = sum_{k in b} w_k x_k
+//     B[2j  ,b] = cos(2 pi n_j y_b / T),  B[2j+1,b] = sin(...),  B[2nf,b] = y_b
+// (the last rows carry the axis sums of Eqs. Fk0/F0l, Steps 2-3 P:870-888), so the GEMM has
+// inner dimension R instead of K (K/R = 15 on BASELINE.json configs[3]).
 //
-// a2 (twiddles) is fused: each CTA generates its K-slab of A and B in shared memory
+// a2 (twiddles) is fused: each CTA generates its bucket slab of A and B in shared memory
 // from the integer phase r = (m x) mod T (exact, lattice vertices P:860-862) through a
 // two-level table E(r) = E_hi(r >> L) * E_lo(r & (2^L - 1)) built in SMEM with sincospi,
 // so the twiddle matrices never touch HBM ("no full-length arrays").
 //
 // a3 (FP64): FP64 tensor cores (mma.sync m16n8k16 .f64, SASS DMMA), 64x64 P tile per CTA,
-// 8 warps of 16x32, double-buffered slabs of 16 corners (one k16 MMA step per slab).  Accumulation is hierarchical: a fresh register
-// accumulator per chunk of <= kChunk corners is added into a running total, bounding
-// the rounding error by about (kChunk + K/kChunk) u B instead of K u B.
+// 8 warps of 16x32, double-buffered slabs of 16 buckets (one k16 MMA step per slab).
+// Accumulation is hierarchical: a fresh register accumulator per chunk of <= kChunk buckets
+// is added into a running total, bounding the rounding error by about
+// (kRowBucketCapFp64 + kChunk + R/kChunk) u B instead of K u B.
 #include "common.cuh"
 
 namespace fcfs {
 
-static constexpr int kBK = 16;        // corners per slab
-static constexpr int kChunk = 2048;   // corners per register accumulator
+static constexpr int kBK = 16;        // row buckets per slab
+static constexpr int kChunk = 2048;   // buckets per register accumulator (<= kRowBucketCapFp64 corners each)
 static constexpr int kThreads = 256;  // 16 x 16 threads, 4x4 outputs each
 
 __device__ __forceinline__ void build_tables(const TwiddleGeom &g, double2 *thi, double2 *tlo) {
@@ -59,6 +63,38 @@ __device__ __forceinline__ double2 side_pair(int p_global, const SidePlan &sp, i
     }
     if (p_global == sp.nf && sp.axis) return make_double2(wt * (double)v, 0.0);
     return make_double2(0.0, 0.0);
+}
+
+// x-side pair of one row bucket: sum over its corners [cb, ce) of w_k (cos, sin)(2 pi f x_k / T)
+// (G of the row-bucketed Step 4, buckets.cu), or sum w_k x_k for the axis row.  The warp (32 pairs
+// of one bucket) runs the corner loop uniformly; x / w come through L1 (one line per warp).
+__device__ __forceinline__ double2 bucket_pair(int p_global, const SidePlan &sp, const int32_t *__restrict__ xs,
+                                               const int32_t *__restrict__ ws, int cb, int ce, const TwiddleGeom &g,
+                                               const double2 *thi, const double2 *tlo) {
+    double re = 0.0, im = 0.0;
+    if (p_global < sp.nf) {
+        const uint32_t f = (uint32_t)(sp.f0 + p_global);
+        int c = cb;
+        for (; c + 1 < ce; c += 2) {
+            const int32_t x0 = __ldg(xs + c), x1 = __ldg(xs + c + 1);
+            const double w0 = (double)__ldg(ws + c), w1 = (double)__ldg(ws + c + 1);
+            const double2 e0 = twiddle(phase_mod(f, (uint32_t)x0, g), g, thi, tlo);
+            const double2 e1 = twiddle(phase_mod(f, (uint32_t)x1, g), g, thi, tlo);
+            re = fma(w0, e0.x, re); im = fma(w0, e0.y, im);
+            re = fma(w1, e1.x, re); im = fma(w1, e1.y, im);
+        }
+        if (c < ce) {
+            const int32_t x0 = __ldg(xs + c);
+            const double w0 = (double)__ldg(ws + c);
+            const double2 e0 = twiddle(phase_mod(f, (uint32_t)x0, g), g, thi, tlo);
+            re = fma(w0, e0.x, re); im = fma(w0, e0.y, im);
+        }
+    } else if (p_global == sp.nf && sp.axis) {
+        long long a = 0;
+        for (int c = cb; c < ce; ++c) a += (long long)__ldg(ws + c) * (long long)__ldg(xs + c);
+        re = (double)a;
+    }
+    return make_double2(re, im);
 }
 
 // FP64 tensor-core MMA (DMMA): D[16x8] += A[16x16] B[16x8], fragments per the sm_90+/sm_100
@@ -99,9 +135,8 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
         rem -= (int64_t)tix * plan.tiles_y * plan.splits;
         const int tiy = (int)(rem / plan.splits);
         const int split = (int)(rem - (int64_t)tiy * plan.splits);
-        int64_t kb, ke;
-        if (src.corner_ptr) { kb = src.corner_ptr[clip]; ke = src.corner_ptr[clip + 1]; }
-        else { kb = src.k_lo; ke = src.k_hi; }
+        // bucket range of the item (the split partitions the clip's row buckets)
+        const int64_t kb = src.clip_bptr[clip], ke = src.clip_bptr[clip + 1];
         const int64_t span = ke - kb;
         const int64_t k0 = kb + span * split / plan.splits;
         const int64_t k1 = kb + span * (split + 1) / plan.splits;
@@ -113,19 +148,20 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
             for (int j = 0; j < 4; ++j) tot[i][j] = 0.0;
 
         __syncthreads();   // tables ready / previous item's smem reads done
+        // slab of kBK buckets [ks, ks + kBK) (zeros past kend): A = bucket sums, B = row twiddles
         auto generate = [&](int buf, int64_t ks, int64_t kend) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int kk = gk + 8 * h;
-                const int64_t k = ks + kk;
-                int32_t xv = 0, yv = 0;
-                double wv = 0.0;
-                if (k < kend) { xv = __ldg(src.x + k); yv = __ldg(src.y + k); wv = (double)__ldg(src.w + k); }
-                double2 a = side_pair(tix * (kTile / 2) + gp, plan.X, xv, wv, g, thi, tlo);
-                double2 b = side_pair(tiy * (kTile / 2) + gp, plan.Y, yv, 1.0, g, thi, tlo);
-                if (k >= kend) b = make_double2(0.0, 0.0);
+                const int64_t b = ks + kk;
+                double2 a = make_double2(0.0, 0.0), bv = make_double2(0.0, 0.0);
+                if (b < kend) {
+                    const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+                    a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
+                    bv = side_pair(tiy * (kTile / 2) + gp, plan.Y, __ldg(src.by + b), 1.0, g, thi, tlo);
+                }
                 *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
-                *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = b;
+                *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = bv;
             }
         };
 

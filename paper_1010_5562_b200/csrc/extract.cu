@@ -283,7 +283,9 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
         if (n > kClipRects) {
-            if (threadIdx.x == 0) atomicOr(err, 8);
+            // the caller falls back to the general path; the count must still be defined, since
+            // k_clip_pack runs before the host sees the flag
+            if (threadIdx.x == 0) { atomicOr(err, 8); counts[b] = 0; area[b] = 0; }
             continue;
         }
         uint32_t key[kClipItems];
@@ -384,7 +386,9 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
         if (n > kClipRects) {
-            if (threadIdx.x == 0) atomicOr(err, 8);
+            // the caller falls back to the general path; the count must still be defined, since
+            // k_clip_pack runs before the host sees the flag
+            if (threadIdx.x == 0) { atomicOr(err, 8); counts[b] = 0; area[b] = 0; }
             continue;
         }
         // all of this thread's rects are loaded up front (independent loads in flight)

@@ -157,6 +157,7 @@ static GemmPlan make_plan(int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int6
 struct CoeffWs {
     double *P;
     int64_t *area;
+    BucketWs bk;
 };
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (whole clip = one 64x64 tile)
@@ -166,9 +167,13 @@ static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m
     return (prec == FCFS_TF32X3 || prec == FCFS_F16X3) && tf32_can_fuse(p, ea);
 }
 
-static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P = true) {
+// the row buckets (buckets.cu) feed the FP64 contraction; the tcgen05 kernels walk corners
+static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, int64_t K, int64_t B,
+                        fcfs_precision prec) {
     w.P = cv.take<double>(need_P ? (size_t)p.items * kTile * kTile : 1);
     w.area = cv.take<int64_t>(1);
+    w.bk = BucketWs{};
+    if (prec == FCFS_FP64) carve_buckets(cv, K, B, w.bk);
 }
 
 static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard, int32_t &m_lo, int32_t &m_hi) {
@@ -306,7 +311,7 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi));
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi), K, 1, prec);
     return cv.used();
 }
 
@@ -341,7 +346,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi));
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi), K, 1, prec);
     if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     EpiArgs ea;
@@ -354,10 +359,12 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
         if (st != FCFS_OK) return st;
         ea.area_dev = W.area;
     }
+    src.bptr = W.bk.bptr; src.by = W.bk.by; src.clip_bptr = W.bk.clip_bptr; src.kend = K;
     bool fused = false;
     {
         StageScope scope(kStageContract, s);
-        st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
+        if (prec == FCFS_FP64) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
+        if (st == FCFS_OK) st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
     if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
@@ -366,12 +373,12 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
 
 size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,
                                     fcfs_precision prec) {
-    (void)K_total; (void)T; (void)prec;
+    (void)T;
     if (check_window(win) != FCFS_OK || B < 1) return 0;
     GemmPlan p = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, -win->M, win->M));
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, -win->M, win->M), K_total, B, prec);
     return cv.used();
 }
 
@@ -397,11 +404,12 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M));
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M), K_total, B, prec);
     if (!cv.fits()) { set_error("fcfs_coeffs_batched: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     CornerSrc src;
-    src.x = x; src.y = y; src.w = w; src.corner_ptr = corner_ptr; src.k_lo = 0; src.k_hi = 0;
+    src.x = x; src.y = y; src.w = w; src.corner_ptr = corner_ptr; src.k_lo = 0; src.k_hi = K_total;
+    src.bptr = W.bk.bptr; src.by = W.bk.by; src.clip_bptr = W.bk.clip_bptr; src.kend = K_total;
     EpiArgs ea;
     ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
     ea.m_lo = -win->M; ea.m_hi = win->M; ea.T = T; ea.area_dev = area; ea.area_host = 0;
@@ -410,7 +418,8 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     bool fused = false;
     {
         StageScope scope(kStageContract, s);
-        st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
+        if (prec == FCFS_FP64) st = run_buckets(y, corner_ptr, B, 0, K_total, kRowBucketCapFp64, W.bk, s);
+        if (st == FCFS_OK) st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
     if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);

@@ -303,3 +303,52 @@ def test_nccl_sharded_paths_world1(fcfs):
             _assert_parity(vb.cpu().numpy(), Fr, B, prec, f"vblock/{prec}", ms, ns)
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ row buckets (Step 4 row structure)
+
+def _long_row_clip():
+    """one clip whose rows hold thousands of corners: > kRowBucketCap corners per row and rows
+    crossing the 4096-corner segment boundaries of the bucket pass."""
+    T = 8192
+    xs = np.arange(0, 2 * 2600, 2, dtype=np.int32)
+    r = np.stack([xs, np.zeros_like(xs), xs + 1, np.full_like(xs, T)], axis=1)      # rows y = 0 and y = T
+    extra = np.array([[10, 5, 20, 40], [3000, 17, 3400, 18], [100, 4000, 8192, 4001]], np.int32)
+    return T, np.concatenate([r, extra]).astype(np.int32)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
+def test_long_rows_and_unsorted_corners(fcfs, prec):
+    T, rects = _long_row_clip()
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T)
+    area = int(g["area"][0].item())
+    M = N = 12
+    F = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec=prec).cpu().numpy()
+    ms, ns, Fr, B = _oracle_window(g, T, M, N)
+    _assert_parity(F, Fr, B, prec, "long rows", ms, ns)
+    # any corner order is valid (buckets are runs of equal consecutive y)
+    perm = torch.from_numpy(np.random.default_rng(5).permutation(g["K"])).cuda()
+    xp, yp, wp = (g[k][perm].contiguous() for k in ("x", "y", "w"))
+    Fp = fcfs.coeffs(xp, yp, wp, area, T, M, N, prec=prec).cpu().numpy()
+    _assert_parity(Fp, Fr, B, prec, "permuted corners", ms, ns)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
+def test_batched_empty_and_tiny_clips(fcfs, prec):
+    T, rects = _long_row_clip()
+    small = np.array([[1, 1, 2, 2], [5, 5, 9, 6], [7000, 8000, 8192, 8192]], np.int32)
+    allr = np.concatenate([small[:1], rects, small[1:]]).astype(np.int32)
+    n = len(rects)
+    cp = np.array([0, 1, 1, 1 + n, 1 + n, 3 + n], np.int64)          # clips: tiny, empty, long rows, empty, two rects
+    g = fcfs.vertices_from_rects(_dev(allr, torch.int32), T, None, _dev(cp, torch.int64))
+    M = N = 9
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, -1.0, "dense",
+                            prec).cpu().numpy()
+    ms, ns = oracle.window(M, N, -1.0)
+    cpc = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for b in range(5):
+        sl = slice(cpc[b], cpc[b + 1])
+        Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+        _assert_parity(F[b], Fr, B, prec, f"clip {b}", ms, ns)
