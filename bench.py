@@ -316,8 +316,16 @@ def main():
     peaks, src = load_peaks()
     c_ms, c_n = stages["contract"]
     c_ms_launch = c_ms / max(c_n, 1)
-    Kc = np.diff(cptr_h).astype(np.float64)
-    alg_flops = float(np.sum(8.0 * wl.M * wl.N * Kc))      # real quadrant GEMM 2M x 2N x K, 2 flop/MAC
+    # inner dimension of the contraction: corners (tcgen05 split-precision kernels) or row buckets
+    # (FP64 kernel: Step 4 row structure, fcfs_row_buckets with the cap fcfs_coeffs uses)
+    if prec == "fp64":
+        rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
+        Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
+        k_inner = "row buckets"
+    else:
+        Kc = np.diff(cptr_h).astype(np.float64)
+        k_inner = "corners"
+    alg_flops = float(np.sum(8.0 * wl.M * wl.N * Kc))      # real quadrant GEMM 2M x 2N x K_inner, 2 flop/MAC
     achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
     clocks = clk.summary()
     if prec == "tf32x3":
@@ -342,7 +350,8 @@ def main():
         bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec),
-            "kernel": "k_gemm_" + prec,
+            "kernel": "k_gemm_" + prec, "k_inner": f"{k_inner}: {int(Kc.sum())}",
+            "alg_flops_per_launch": alg_flops,
             "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
             "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()}}
 

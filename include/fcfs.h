@@ -145,6 +145,28 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
                                 const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
                                 size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Row buckets of a corner list — the row structure of Step 4: corners on one row
+ * y share E_y[n, y], so sum_k w_k E_x[m,k] E_y[n,k] = sum_b E_y[n, y_b] sum_{k in b} w_k E_x[m,k]
+ * and the FP64 contraction runs over buckets instead of corners.  fcfs_coeffs[_batched] compute
+ * them internally; this entry point exposes the same pass (for tests and planning).
+ *
+ * A bucket is a maximal run of CONSECUTIVE corners with equal y, cut at every clip start
+ * (corner_ptr[b]), at every corner index k with k % 4096 == 0 (the pass's segment size) and every
+ * `cap` corners inside a run (counted from the run start).  Any corner order is valid.
+ * y          int32 [K] (device), K = corner_ptr[B] (or the K argument when corner_ptr is NULL).
+ * corner_ptr int64 [B+1] (device) or NULL (one range [0, K), B must be 1).
+ * cap        1 .. 32.
+ * bptr       int32 [K + 1] out (device): global corner index of each bucket start; bptr[nb] = K.
+ * by         int32 [K] out (device): the bucket's y.
+ * clip_bptr  int64 [B+1] out (device): CSR of buckets per clip.
+ * nb_host    out (host): bucket count (this call synchronises `stream` once).
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B);
+fcfs_status fcfs_row_buckets(const int32_t *y, const int64_t *corner_ptr, int64_t B, int64_t K,
+                             int32_t cap, int32_t *bptr, int32_t *by, int64_t *clip_bptr,
+                             int64_t *nb_host, void *ws, size_t ws_bytes, void *stream);
+
 /* Host helpers. */
 int64_t fcfs_window_size(const fcfs_window *win);        /* outputs per clip; -1 if invalid */
 int64_t fcfs_pupil_indices(int32_t M, int32_t N, double r2, int32_t *m_out_host,

@@ -15,6 +15,8 @@
 //   3. CUB reduce-by-key (sum weights of equal keys; groups are SUMMED, reading A5).
 //   4. drop zero weights: flag + exclusive scan + scatter into x, y, w; int64 area atomics.
 //   5. corner_ptr by lower_bound of b<<42 in the compacted keys.
+// Batched clips of singleton groups take the per-clip paths below (one CTA per clip, SMEM sort,
+// look-back offsets, direct output) instead.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -243,9 +245,9 @@ __global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, 
 // Per-clip fast path (every rect its own group, clips of <= kClipRects rects, T < 2^16): one
 // CTA per clip builds the clip's 4n raw corners with 32-bit keys (y << 16 | x), sorts them in
 // shared memory (CUB BlockRadixSort), merges equal keys with a segmented block scan, drops zero
-// weights, and writes the compacted clip to a staging area at its raw offset 4*r0 together with
-// its exact int64 area.  A device scan of the per-clip counts gives corner_ptr; a copy kernel
-// packs the clips into x, y, w.  Same canonical (clip, y, x) order as the global path.
+// weights, finds its output offset by a decoupled look-back over the clips before it
+// (clip_lookback: corner_ptr without a separate scan) and writes the compacted clip straight
+// into x, y, w, with its exact int64 area.  Same canonical (clip, y, x) order as the global path.
 // ------------------------------------------------------------------------------------------
 static constexpr int kClipThreads = 512;
 static constexpr int kClipItems = 16;
@@ -265,9 +267,36 @@ struct SegSumOp {
     }
 };
 
+// Output offset of clip b by a decoupled look-back over the clips before it (one CTA per clip,
+// CTAs dispatched in clip order, so every predecessor is resident or done): publish this clip's
+// count, add predecessors' counts until one with a published inclusive prefix, publish ours.
+// Writes corner_ptr[b] (and corner_ptr[B] for the last clip).  Thread 0 only.
+static constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = (1ull << 62) - 1;
+__device__ int64_t clip_lookback(unsigned long long *status, int64_t b, int64_t B, int64_t count,
+                                 int64_t *corner_ptr) {
+    volatile unsigned long long *st = status;
+    int64_t prefix = 0;
+    if (b > 0) {
+        st[b] = kLbAgg | (unsigned long long)count;
+        __threadfence();
+        for (int64_t j = b - 1;; --j) {
+            unsigned long long v;
+            do { v = st[j]; } while ((v >> 62) == 0);
+            prefix += (int64_t)(v & kLbMask);
+            if ((v >> 62) == 2) break;
+        }
+    }
+    st[b] = kLbInc | (unsigned long long)(prefix + count);
+    __threadfence();
+    corner_ptr[b] = prefix;
+    if (b == B - 1) corner_ptr[B] = prefix + count;
+    return prefix;
+}
+
 __global__ void __launch_bounds__(kClipThreads, 1)
 k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
-               int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t *counts, int64_t *area, int32_t *err) {
+               int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
+               unsigned long long *status, int64_t *area, int32_t *err) {
     typedef cub::BlockRadixSort<uint32_t, kClipThreads, kClipItems, int32_t> Sort;
     typedef cub::BlockScan<SegSum, kClipThreads> SegScan;
     typedef cub::BlockScan<int, kClipThreads> IntScan;
@@ -279,13 +308,14 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
         typename Red::TempStorage red;
     } tmp;
     __shared__ uint32_t edge_first[kClipThreads], edge_last[kClipThreads];
+    __shared__ int64_t s_off;
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
         if (n > kClipRects) {
-            // the caller falls back to the general path; the count must still be defined, since
-            // k_clip_pack runs before the host sees the flag
-            if (threadIdx.x == 0) { atomicOr(err, 8); counts[b] = 0; area[b] = 0; }
+            // the caller falls back to the general path; the clip still publishes a count (0) so
+            // that the look-back of the clips after it completes
+            if (threadIdx.x == 0) { atomicOr(err, 8); area[b] = 0; clip_lookback(status, b, B, 0, corner_ptr); }
             continue;
         }
         uint32_t key[kClipItems];
@@ -336,20 +366,19 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
         int total = 0;
         IntScan(tmp.scan).ExclusiveSum(keep, pos, total);
         __syncthreads();
-        const int64_t base = 4 * r0;
+        if (threadIdx.x == 0) s_off = clip_lookback(status, b, B, total, corner_ptr);
+        __syncthreads();
+        const int64_t base = s_off;
 #pragma unroll
         for (int j = 0; j < kClipItems; ++j) {
-            if (keep[j]) {
+            if (keep[j] && base + pos[j] < cap) {
                 xs[base + pos[j]] = (int32_t)(key[j] & 0xFFFFu);
                 ys[base + pos[j]] = (int32_t)(key[j] >> 16);
                 ws[base + pos[j]] = seg[j].val;
             }
         }
         const long long asum = Red(tmp.red).Sum(a);
-        if (threadIdx.x == 0) {
-            counts[b] = total;
-            area[b] = asum;
-        }
+        if (threadIdx.x == 0) area[b] = asum;
         __syncthreads();
     }
 }
@@ -358,9 +387,9 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
 // one CTA per clip counting-sorts the clip's 4n corners by y into T+1 SMEM buckets (atomics);
 // then every corner finds its rank inside its (short) bucket by x, the first of equal (y, x)
 // carries the summed weight (groups are summed, reading A5), a block scan over the sorted
-// positions drops zero weights, and the clip is written in canonical (y, x) order to the
-// staging area at 4*r0 (coalesced), with its exact int64 area.  O(n * bucket) with all threads
-// busy, instead of a radix sort of 4n keys.
+// positions drops zero weights, and the clip is written in canonical (y, x) order straight to its
+// CSR position (look-back offset, coalesced), with its exact int64 area.  O(n * bucket) with all
+// threads busy, instead of a radix sort of 4n keys.
 static constexpr int kBucketThreads = 512;
 static constexpr int kBucketRectsPerThread = 4;   // kClipRects / kBucketThreads
 static constexpr int kBucketMaxT = 8191;
@@ -368,8 +397,8 @@ static constexpr int kBucketCap = 4 * kClipRects;
 
 __global__ void __launch_bounds__(kBucketThreads)
 k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
-                      int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t *counts, int64_t *area,
-                      int32_t *err) {
+                      int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
+                      unsigned long long *status, int64_t *area, int32_t *err) {
     extern __shared__ __align__(16) unsigned char bsm[];
     uint32_t *bxw = (uint32_t *)bsm;                    // [cap] bucketed (x << 16 | w & 0xFFFF); later compacted (y << 16 | x)
     uint32_t *syx = bxw + kBucketCap;                   // [cap] sorted (y << 16 | x)
@@ -379,6 +408,7 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
     __shared__ int32_t wsum[kBucketThreads / 32];
     __shared__ long long asum[kBucketThreads / 32];
     __shared__ int tot_s;
+    __shared__ int64_t s_off;
     const int nb = T + 1;                               // buckets y = 0..T
     const int per = (nb + kBucketThreads - 1) / kBucketThreads;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -386,9 +416,9 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
         if (n > kClipRects) {
-            // the caller falls back to the general path; the count must still be defined, since
-            // k_clip_pack runs before the host sees the flag
-            if (threadIdx.x == 0) { atomicOr(err, 8); counts[b] = 0; area[b] = 0; }
+            // the caller falls back to the general path; the clip still publishes a count (0) so
+            // that the look-back of the clips after it completes
+            if (threadIdx.x == 0) { atomicOr(err, 8); area[b] = 0; clip_lookback(status, b, B, 0, corner_ptr); }
             continue;
         }
         // all of this thread's rects are loaded up front (independent loads in flight)
@@ -485,15 +515,17 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         if (threadIdx.x == kBucketThreads - 1) tot_s = outp;     // the last thread ends at the clip total
         __syncthreads();
         const int total = tot_s;
-        const int64_t base = 4 * r0;
-        for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores
+        if (threadIdx.x == 0) s_off = clip_lookback(status, b, B, total, corner_ptr);
+        __syncthreads();
+        const int64_t base = s_off;
+        for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores, final positions
+            if (base + i >= cap) break;
             const uint32_t yx = bxw[i];
             xs[base + i] = (int32_t)(yx & 0xFFFFu);
             ys[base + i] = (int32_t)(yx >> 16);
             ws[base + i] = by[i];
         }
         if (threadIdx.x == 0) {
-            counts[b] = total;
             long long t = 0;
             for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
             area[b] = t;
@@ -502,42 +534,15 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
     }
 }
 
-// pack each clip's staged corners (at 4 r0) to its CSR position corner_ptr[b]
-__global__ void k_clip_pack(const int64_t *__restrict__ clip_ptr, int64_t B, const int64_t *__restrict__ corner_ptr,
-                            const int32_t *xs, const int32_t *ys, const int32_t *ws, int64_t cap, int32_t *x, int32_t *y,
-                            int32_t *w) {
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-        const int64_t src = 4 * (clip_ptr ? clip_ptr[b] : 0);
-        const int64_t dst = corner_ptr[b], n = corner_ptr[b + 1] - dst;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            if (dst + i < cap) {
-                x[dst + i] = xs[src + i];
-                y[dst + i] = ys[src + i];
-                w[dst + i] = ws[src + i];
-            }
-        }
-    }
-}
-
 struct ClipWs {
-    int32_t *xs, *ys, *ws;
-    int64_t *counts, *K;
+    unsigned long long *status;   // [B] look-back words (flag << 62 | count)
     int32_t *err;
-    void *cub_tmp;
-    size_t cub_bytes;
 };
 
 static void carve_clip(Carver &cv, int64_t R, int64_t B, ClipWs &w) {
-    w.xs = cv.take<int32_t>(4 * R + 1);
-    w.ys = cv.take<int32_t>(4 * R + 1);
-    w.ws = cv.take<int32_t>(4 * R + 1);
-    w.counts = cv.take<int64_t>(B + 1);
-    w.K = cv.take<int64_t>(1);
+    (void)R;
+    w.status = cv.take<unsigned long long>(B);
     w.err = cv.take<int32_t>(4);
-    size_t c = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, c, (int64_t *)nullptr, (int64_t *)nullptr, (int)(B + 1));
-    w.cub_tmp = cv.take<char>(c);
-    w.cub_bytes = c;
 }
 
 size_t extract_clip_workspace_bytes(int64_t R, int64_t B) {
@@ -559,7 +564,9 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
         return FCFS_E_WORKSPACE;
     }
     FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
-    int64_t grid = B < 148 * 2 * 16 ? B : 148 * 2 * 16;
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.status, 0, B * sizeof(unsigned long long), s));
+    // one CTA per clip (the look-back needs every predecessor clip's CTA dispatched before it)
+    const int64_t grid = B;
     if (T <= kBucketMaxT) {
         const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
         static bool battr = false;
@@ -569,20 +576,14 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
             battr = true;
         }
         k_clip_corners_bucket<<<(unsigned)grid, kBucketThreads, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T,
-                                                                            W.xs, W.ys, W.ws, W.counts, area,
-                                                                            W.err);
+                                                                            x, y, w, cap, corner_ptr, W.status,
+                                                                            area, W.err);
         FCFS_CHECK_LAUNCH("k_clip_corners_bucket");
     } else {
-        k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, W.xs, W.ys,
-                                                               W.ws, W.counts, area, W.err);
+        k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, x, y, w, cap,
+                                                               corner_ptr, W.status, area, W.err);
         FCFS_CHECK_LAUNCH("k_clip_corners");
     }
-    FCFS_TRY_CUDA(cudaMemsetAsync(W.counts + B, 0, sizeof(int64_t), s));
-    size_t tb = W.cub_bytes;
-    FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.counts, corner_ptr, (int)(B + 1), s));
-    count_launch(2);
-    k_clip_pack<<<(unsigned)grid, 256, 0, s>>>(clip_ptr, B, corner_ptr, W.xs, W.ys, W.ws, cap, x, y, w);
-    FCFS_CHECK_LAUNCH("k_clip_pack");
     int64_t Kh = 0;
     int32_t errh = 0;
     FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, corner_ptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

@@ -426,4 +426,38 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     return launch_epilogue(plan, W.P, ea, F, s);
 }
 
+size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B) {
+    if (K < 0 || B < 1) return 0;
+    return buckets_workspace_bytes(K, B);
+}
+
+fcfs_status fcfs_row_buckets(const int32_t *y, const int64_t *corner_ptr, int64_t B, int64_t K, int32_t cap,
+                             int32_t *bptr, int32_t *by, int64_t *clip_bptr, int64_t *nb_host, void *ws,
+                             size_t ws_bytes, void *stream) {
+    if (K < 0 || B < 1 || (K > 0 && !y) || !bptr || !by || !clip_bptr || !nb_host || cap < 1 || cap > 32 ||
+        (corner_ptr == nullptr && B != 1)) {
+        set_error("fcfs_row_buckets: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    Carver cv(ws, ws_bytes);
+    BucketWs W;
+    carve_buckets(cv, K, B, W);
+    if (!cv.fits()) { set_error("fcfs_row_buckets: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    st = run_buckets(y, corner_ptr, B, 0, K, cap, W, s);
+    if (st != FCFS_OK) return st;
+    // the pass writes into the workspace; copy the caller-visible arrays out
+    int64_t nb = 0;
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&nb, W.clip_bptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(bptr, W.bptr, sizeof(int32_t) * (nb + 1), cudaMemcpyDeviceToDevice, s));
+    if (nb > 0) FCFS_TRY_CUDA(cudaMemcpyAsync(by, W.by, sizeof(int32_t) * nb, cudaMemcpyDeviceToDevice, s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(clip_bptr, W.clip_bptr, sizeof(int64_t) * (B + 1), cudaMemcpyDeviceToDevice, s));
+    *nb_host = nb;
+    return FCFS_OK;
+}
+
 }  // extern "C"

@@ -71,6 +71,11 @@ _lib.fcfs_batched_workspace_bytes.restype = _sz
 _lib.fcfs_coeffs_batched.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _i32, _WP, _i32, _P, _P, _sz, _P]
 _lib.fcfs_coeffs_batched.restype = _i32
 
+_lib.fcfs_row_buckets_workspace_bytes.argtypes = [_i64, _i64]
+_lib.fcfs_row_buckets_workspace_bytes.restype = _sz
+_lib.fcfs_row_buckets.argtypes = [_P, _P, _i64, _i64, _i32, _P, _P, _P, ctypes.POINTER(_i64), _P, _sz, _P]
+_lib.fcfs_row_buckets.restype = _i32
+
 _lib.fcfs_profile_enable.argtypes = [_i32]
 _lib.fcfs_profile_enable.restype = _i32
 _lib.fcfs_profile_read.argtypes = [_P, _P, _i32]
@@ -79,7 +84,8 @@ _lib.fcfs_profile_read.restype = _i32
 EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_coeffs_workspace_bytes",
             "fcfs_coeffs", "fcfs_batched_workspace_bytes", "fcfs_coeffs_batched", "fcfs_window_size",
             "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
-            "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read"]
+            "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
+            "fcfs_row_buckets"]
 STAGES = ("extract", "contract", "epilogue")
 
 
@@ -278,3 +284,19 @@ def coeffs_batched(corner_ptr, x, y, w, area, T, M, N, r2=-1.0, layout="dense", 
         K_max = int((corner_ptr[1:] - corner_ptr[:-1]).max().item()) if B > 0 else 0
     plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device)
     return plan.run(corner_ptr, x, y, w, area, stream=stream)
+
+
+def row_buckets(y, corner_ptr=None, cap=32, stream=None):
+    """Row buckets of a corner list (fcfs_row_buckets): dict bptr [nb+1], by [nb], clip_bptr [B+1], nb."""
+    K = int(y.shape[0])
+    B = 1 if corner_ptr is None else int(corner_ptr.shape[0]) - 1
+    dev = y.device
+    bptr = torch.empty(K + 1, dtype=torch.int32, device=dev)
+    by = torch.empty(max(K, 1), dtype=torch.int32, device=dev)
+    clip_bptr = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    ws = _ws(_lib.fcfs_row_buckets_workspace_bytes(K, B), dev)
+    nb = _i64(0)
+    _check(_lib.fcfs_row_buckets(_ptr(y), _ptr(corner_ptr), B, K, int(cap), _ptr(bptr), _ptr(by), _ptr(clip_bptr),
+                                 ctypes.byref(nb), _ptr(ws), ws.numel(), _stream(stream)), "fcfs_row_buckets")
+    n = int(nb.value)
+    return {"bptr": bptr[:n + 1], "by": by[:n], "clip_bptr": clip_bptr, "nb": n}

@@ -352,3 +352,42 @@ def test_batched_empty_and_tiny_clips(fcfs, prec):
         sl = slice(cpc[b], cpc[b + 1])
         Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
         _assert_parity(F[b], Fr, B, prec, f"clip {b}", ms, ns)
+
+
+def _buckets_reference(y, corner_ptr, cap, seg=4096):
+    """the bucket rule of include/fcfs.h written out: runs of equal consecutive y, cut at clip
+    starts, at k % seg == 0 and every `cap` corners from the run start."""
+    K = len(y)
+    starts = set(int(c) for c in corner_ptr[:-1]) if corner_ptr is not None else {0}
+    bptr, by = [], []
+    run = 0
+    for k in range(K):
+        rs = k == 0 or k in starts or k % seg == 0 or y[k] != y[k - 1]
+        if rs:
+            run = k
+        if (k - run) % cap == 0:
+            bptr.append(k)
+            by.append(int(y[k]))
+    bptr.append(K)
+    b = np.asarray(bptr[:-1], np.int64)
+    cb = [int(np.searchsorted(b, c, side="left")) for c in (corner_ptr if corner_ptr is not None else [0, K])]
+    return np.asarray(bptr, np.int32), np.asarray(by, np.int32), np.asarray(cb, np.int64)
+
+
+@pytest.mark.parametrize("cap", [1, 4, 32])
+def test_row_buckets_bit_exact(fcfs, cap):
+    # batched clips (tiny, empty, long rows crossing 4096-corner segments) and one permuted clip
+    T, rects = _long_row_clip()
+    small = np.array([[1, 1, 2, 2], [5, 5, 9, 6], [7000, 8000, 8192, 8192]], np.int32)
+    allr = np.concatenate([small[:1], rects, small[1:]]).astype(np.int32)
+    n = len(rects)
+    cp = np.array([0, 1, 1, 1 + n, 1 + n, 3 + n], np.int64)
+    g = fcfs.vertices_from_rects(_dev(allr, torch.int32), T, None, _dev(cp, torch.int64))
+    for y, cptr in [(g["y"], g["corner_ptr"]),
+                    (g["y"][torch.from_numpy(np.random.default_rng(2).permutation(g["K"])).cuda()].contiguous(), None)]:
+        r = fcfs.row_buckets(y, cptr, cap)
+        bp, byr, cb = _buckets_reference(y.cpu().numpy(), None if cptr is None else cptr.cpu().numpy(), cap)
+        assert r["nb"] == len(byr)
+        assert np.array_equal(r["bptr"].cpu().numpy(), bp)
+        assert np.array_equal(r["by"].cpu().numpy(), byr)
+        assert np.array_equal(r["clip_bptr"].cpu().numpy(), cb)
