@@ -246,6 +246,32 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
     lo = v - hi;
 }
 
+// ---- packed FP32x2 arithmetic (SASS FFMA2 / FMUL2): two independent lanes of work per instruction
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%6, %7};\n"
+        " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// (re, im) <- (re, im) (c + i s) for two independent values, one per FP32x2 lane:
+// re' = re c - im s, im' = im c + re s (the same rounding sequence as the scalar fmaf form)
+__device__ __forceinline__ void rot2(float2 &re, float2 &im, float2 c, float2 sn) {
+    const float2 t = mul2(im, sn);
+    const float2 u = mul2(re, sn);
+    re = fma2(re, c, make_float2(-t.x, -t.y));
+    im = fma2(im, c, u);
+}
+
 // One producer task: 4 consecutive corners (16-byte chunk `quad` of the stage) x 8 consecutive
 // pair slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup
 // for the first frequency, pre-multiplied by the corner weight, and the angle-addition
@@ -291,14 +317,13 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         *(float4 *)(base + 4 * 1024) = im;         // row 32 + r
         *(float4 *)(base + 8 * 1024) = rl;         // row 64 + r
         *(float4 *)(base + 12 * 1024) = il;        // row 96 + r
-        if (i < 7) {
-            float4 nr, ni;
-            nr.x = fmaf(re.x, c1.x, -im.x * s1.x); ni.x = fmaf(im.x, c1.x, re.x * s1.x);
-            nr.y = fmaf(re.y, c1.y, -im.y * s1.y); ni.y = fmaf(im.y, c1.y, re.y * s1.y);
-            nr.z = fmaf(re.z, c1.z, -im.z * s1.z); ni.z = fmaf(im.z, c1.z, re.z * s1.z);
-            nr.w = fmaf(re.w, c1.w, -im.w * s1.w); ni.w = fmaf(im.w, c1.w, re.w * s1.w);
-            re = nr;
-            im = ni;
+        if (i < 7) {   // packed: corners (0, 1) and (2, 3) per instruction
+            float2 r01 = make_float2(re.x, re.y), r23 = make_float2(re.z, re.w);
+            float2 i01 = make_float2(im.x, im.y), i23 = make_float2(im.z, im.w);
+            rot2(r01, i01, make_float2(c1.x, c1.y), make_float2(s1.x, s1.y));
+            rot2(r23, i23, make_float2(c1.z, c1.w), make_float2(s1.z, s1.w));
+            re = make_float4(r01.x, r01.y, r23.x, r23.y);
+            im = make_float4(i01.x, i01.y, i23.x, i23.y);
         }
     }
     const int ia = sp.nf - p0;
@@ -363,7 +388,7 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
         *(uint4 *)(base + 4 * 1024) = make_uint4(hs[0], hs[1], hs[2], hs[3]);
         *(uint4 *)(base + 8 * 1024) = make_uint4(lc[0], lc[1], lc[2], lc[3]);
         *(uint4 *)(base + 12 * 1024) = make_uint4(ls[0], ls[1], ls[2], ls[3]);
-        if (i < 7) {
+        if (i < 7) {   // scalar here: the packed form spills at this register budget
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const float nr = fmaf(re[q], c1[q], -im[q] * s1[q]);
