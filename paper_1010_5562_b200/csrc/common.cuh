@@ -152,8 +152,17 @@ __device__ __forceinline__ uint32_t phase_mod(uint32_t m, uint32_t v, const Twid
 }
 
 // launchers (contract_fp64.cu, epilogue.cu)
+struct FpChunk {
+    const double *G;   // x-side bucket sums of the chunk, [tiles_x][cb][64]
+    int64_t chunk;     // chunk index
+    int64_t cb;        // buckets per chunk
+};
+static constexpr int64_t kFpChunkBuckets = 65536;
+int64_t fp64_chunk_buckets(int64_t K);
 fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
                              cudaStream_t s);
+fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, double *G,
+                                     double *P_ws, cudaStream_t s);
 fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F,
                             cudaStream_t s);
 fcfs_status launch_block_area(const CornerSrc &src, int64_t *area_dev, cudaStream_t s);

@@ -111,8 +111,13 @@ __device__ __forceinline__ void dmma16816(double (&d)[4], const double (&a)[8], 
 
 static constexpr int kLd = kTile + 4;   // padded smem row (doubles): conflict-free fragment loads
 
+// kLoadA = false: A (x-side bucket sums) generated per slab; one launch covers the whole bucket range.
+// kLoadA = true: A read from G (k_gsum_fp64: the sums of one chunk of ch.cb buckets, computed once
+// instead of once per column tile); the items cover that chunk and ADD into P_ws (zeroed before
+// the first chunk), so successive chunk launches accumulate the full sum in a fixed order.
+template <bool kLoadA>
 __global__ void __launch_bounds__(kThreads, 2)
-k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_ws) {
+k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_ws, FpChunk ch) {
     extern __shared__ __align__(16) double smem_d[];
     double2 *thi = (double2 *)smem_d;
     double2 *tlo = thi + g.nhi;
@@ -135,8 +140,14 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
         rem -= (int64_t)tix * plan.tiles_y * plan.splits;
         const int tiy = (int)(rem / plan.splits);
         const int split = (int)(rem - (int64_t)tiy * plan.splits);
-        // bucket range of the item (the split partitions the clip's row buckets)
-        const int64_t kb = src.clip_bptr[clip], ke = src.clip_bptr[clip + 1];
+        // bucket range of the item (the split partitions the clip's row buckets, or the chunk's)
+        int64_t kb = src.clip_bptr[clip], ke = src.clip_bptr[clip + 1];
+        const int64_t chunk0 = kb + ch.chunk * ch.cb;   // kLoadA: first bucket of the chunk
+        if (kLoadA) {
+            kb = chunk0;
+            if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
+            if (kb >= ke) continue;                     // past the clip's buckets: adds nothing
+        }
         const int64_t span = ke - kb;
         const int64_t k0 = kb + span * split / plan.splits;
         const int64_t k1 = kb + span * (split + 1) / plan.splits;
@@ -156,8 +167,12 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                 const int64_t b = ks + kk;
                 double2 a = make_double2(0.0, 0.0), bv = make_double2(0.0, 0.0);
                 if (b < kend) {
-                    const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
-                    a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
+                    if (kLoadA) {
+                        a = __ldg((const double2 *)(ch.G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile) + gp);
+                    } else {
+                        const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+                        a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
+                    }
                     bv = side_pair(tiy * (kTile / 2) + gp, plan.Y, __ldg(src.by + b), 1.0, g, thi, tlo);
                 }
                 *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
@@ -201,25 +216,98 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int col = wn + 8 * t + 2 * lt;
-            *(double2 *)(out + (wm + lg) * kTile + col) = make_double2(tot[t][0], tot[t][1]);
-            *(double2 *)(out + (wm + lg + 8) * kTile + col) = make_double2(tot[t][2], tot[t][3]);
+            double2 *o0 = (double2 *)(out + (wm + lg) * kTile + col), *o1 = (double2 *)(out + (wm + lg + 8) * kTile + col);
+            if (kLoadA) {   // this CTA owns the tile within the launch: plain read-modify-write
+                const double2 p0 = *o0, p1 = *o1;
+                *o0 = make_double2(p0.x + tot[t][0], p0.y + tot[t][1]);
+                *o1 = make_double2(p1.x + tot[t][2], p1.y + tot[t][3]);
+            } else {
+                *o0 = make_double2(tot[t][0], tot[t][1]);
+                *o1 = make_double2(tot[t][2], tot[t][3]);
+            }
         }
     }
+}
+
+// x-side bucket sums of one chunk of ch.cb buckets of a single clip, for every x tile:
+// G[(tix * cb + b) * 64 + 2p + t] = sum_{k in bucket} w_k (cos, sin)(2 pi f_p x_k / T) (t = 0, 1), with the
+// axis pair (f = nf) carrying sum w_k x_k.  Persistent blocks over (slab of 16 buckets, x tile) units.
+__global__ void __launch_bounds__(kThreads)
+k_gsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__restrict__ G) {
+    extern __shared__ __align__(16) double smem_d[];
+    double2 *thi = (double2 *)smem_d;
+    double2 *tlo = thi + g.nhi;
+    build_tables(g, thi, tlo);
+    __syncthreads();
+    const int gp = threadIdx.x & 31, gk = threadIdx.x >> 5;
+    const int64_t cb0 = src.clip_bptr[0], cb1 = src.clip_bptr[1];
+    const int64_t chunk0 = cb0 + ch.chunk * ch.cb;
+    const int64_t chunk1 = chunk0 + ch.cb < cb1 ? chunk0 + ch.cb : cb1;
+    if (chunk0 >= chunk1) return;
+    const int64_t nslab = (chunk1 - chunk0 + kBK - 1) / kBK;
+    const int64_t units = nslab * plan.tiles_x;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tix = (int)(u % plan.tiles_x);
+        const int64_t slab = u / plan.tiles_x;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t b = chunk0 + slab * kBK + gk + 8 * h;
+            if (b >= chunk1) continue;
+            const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+            const double2 a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
+            *((double2 *)(G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile) + gp) = a;
+        }
+    }
+}
+
+static size_t fp64_smem(const TwiddleGeom &g) {
+    return sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kLd;
 }
 
 fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
                              cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     TwiddleGeom g = make_twiddle_geom(T);
-    size_t smem = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kLd;
     static bool attr = false;
     if (!attr) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr = true;
     }
     int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
-    k_gemm_fp64<<<(unsigned)grid, kThreads, smem, s>>>(src, plan, g, P_ws);
+    k_gemm_fp64<false><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, FpChunk{nullptr, 0, 0});
     FCFS_CHECK_LAUNCH("k_gemm_fp64");
+    return FCFS_OK;
+}
+
+int64_t fp64_chunk_buckets(int64_t K) {
+    int64_t cb = K < kFpChunkBuckets ? K : kFpChunkBuckets;
+    cb = (cb + kBK - 1) / kBK * kBK;
+    return cb < kBK ? kBK : cb;
+}
+
+// single clip, chunked: G of each chunk once (k_gsum_fp64), then the DMMA GEMM reading it (P_ws +=)
+fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, double *G,
+                                     double *P_ws, cudaStream_t s) {
+    if (plan.items <= 0) return FCFS_OK;
+    TwiddleGeom g = make_twiddle_geom(T);
+    static bool attr = false;
+    if (!attr) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gsum_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
+    const int64_t cb = fp64_chunk_buckets(K);
+    const int64_t nchunk = K > 0 ? (K + cb - 1) / cb : 0;   // buckets <= corners: an upper bound
+    const size_t tsm = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits));
+    int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const FpChunk ch{G, c, cb};
+        k_gsum_fp64<<<148 * 4, kThreads, tsm, s>>>(src, plan, g, ch, G);
+        FCFS_CHECK_LAUNCH("k_gsum_fp64");
+        k_gemm_fp64<true><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, ch);
+        FCFS_CHECK_LAUNCH("k_gemm_fp64");
+    }
     return FCFS_OK;
 }
 

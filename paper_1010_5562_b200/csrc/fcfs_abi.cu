@@ -158,6 +158,7 @@ struct CoeffWs {
     double *P;
     int64_t *area;
     BucketWs bk;
+    double *G;   // FP64 single clip: x-side bucket sums of one chunk, [tiles_x][cb][64]
 };
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (whole clip = one 64x64 tile)
@@ -169,11 +170,13 @@ static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m
 
 // the row buckets (buckets.cu) feed the FP64 contraction; the tcgen05 kernels walk corners
 static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, int64_t K, int64_t B,
-                        fcfs_precision prec) {
+                        fcfs_precision prec, bool single = false) {
     w.P = cv.take<double>(need_P ? (size_t)p.items * kTile * kTile : 1);
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
+    w.G = nullptr;
     if (prec == FCFS_FP64) carve_buckets(cv, K, B, w.bk);
+    if (prec == FCFS_FP64 && single) w.G = cv.take<double>((size_t)p.tiles_x * fp64_chunk_buckets(K) * kTile);
 }
 
 static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard, int32_t &m_lo, int32_t &m_hi) {
@@ -311,7 +314,7 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi), K, 1, prec);
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi), k, 1, prec, true);
     return cv.used();
 }
 
@@ -346,7 +349,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi), K, 1, prec);
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi), src.k_hi - src.k_lo, 1, prec, true);
     if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     EpiArgs ea;
@@ -363,8 +366,13 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     bool fused = false;
     {
         StageScope scope(kStageContract, s);
-        if (prec == FCFS_FP64) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
-        if (st == FCFS_OK) st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
+        if (prec == FCFS_FP64) {
+            // one clip: x-side bucket sums once per chunk, then the DMMA GEMM over them
+            st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
+            if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.P, s);
+        } else {
+            st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
+        }
     }
     if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
