@@ -178,6 +178,16 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 #define TMEM_LD32(taddr, r)                                                                                  \
     asm volatile(                                                                                            \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
@@ -201,6 +211,34 @@ struct ItemInfo {
     int64_t k0, k1;
     int tix, tiy;
 };
+
+// chunked row-bucket mode (single clip): the x-side operand of every stage comes from G, the
+// pre-split bucket sums of chunk `chunk` (k_gsum_tc), [tiles_x][stages of the chunk][16 KB]
+struct TcChunk {
+    const uint8_t *G;
+    int64_t chunk, cb;    // chunk index, buckets per chunk (a multiple of kBK)
+};
+
+// item -> bucket range of the chunk, split at stage (kBK-bucket) boundaries
+__device__ __forceinline__ ItemInfo item_info_chunk(const CornerSrc &src, const GemmPlan &plan, const TcChunk &ch,
+                                                    int64_t item, int64_t &chunk0) {
+    const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
+    int64_t rem = item % per_clip;
+    ItemInfo it;
+    it.tix = (int)(rem / ((int64_t)plan.tiles_y * plan.splits));
+    rem -= (int64_t)it.tix * plan.tiles_y * plan.splits;
+    it.tiy = (int)(rem / plan.splits);
+    const int split = (int)(rem - (int64_t)it.tiy * plan.splits);
+    chunk0 = src.clip_bptr[0] + ch.chunk * ch.cb;
+    int64_t ke = src.clip_bptr[1];
+    if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
+    const int64_t nst = ke > chunk0 ? (ke - chunk0 + 31) / 32 : 0;
+    it.k0 = chunk0 + 32 * (nst * split / plan.splits);
+    it.k1 = chunk0 + 32 * (nst * (split + 1) / plan.splits);
+    if (it.k1 > ke) it.k1 = ke;
+    if (it.k0 > it.k1) it.k0 = it.k1;
+    return it;
+}
 
 __device__ __forceinline__ ItemInfo item_info(const CornerSrc &src, const GemmPlan &plan, int64_t item) {
     const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
@@ -417,10 +455,13 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
     }
 }
 
-template <bool kFast, int kF16>
+// kLoadA (tf32 only, single clip, row buckets): the x-side stage tile is a 16 KB bulk copy from the
+// chunk's pre-split bucket sums (k_gsum_tc) issued by the group's x-side warp; the y-side warp
+// generates one twiddle set per bucket (the bucket's row y); P tiles are ADDED into P_ws.
+template <bool kFast, int kF16, bool kLoadA = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse,
-            int axis_shift) {
+            int axis_shift, TcChunk ch) {
     constexpr int kBKp = kF16 ? 2 * kBK : kBK;          // corners per stage (one 128 B row of K)
     constexpr int kCq = kF16 ? 8 : 4;                    // corners per 16-byte chunk (per producer task)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -520,12 +561,14 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         const int quad = l & 7, j0 = (l >> 3) << 3;      // quad: 16-byte chunk of the stage
         const float axs = ldexpf(1.0f, -axis_shift);
         const SidePlan sp = sideB ? plan.Y : plan.X;
-        const int32_t *vsrc = sideB ? src.y : src.x;
+        const int32_t *vsrc = sideB ? (kLoadA ? src.by : src.y) : src.x;
+        const int64_t nst_chunk = kLoadA ? ch.cb / kBKp : 0;
         uint32_t sc = 0;                                  // global stage counter
         int slot = 0;                                     // sc % kStages
         uint32_t ph = 0;                                  // (sc / kStages) & 1
         for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
-            const ItemInfo it = item_info(src, plan, item);
+            int64_t chunk0 = 0;
+            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
             const int p0 = (sideB ? it.tiy : it.tix) * 32 + j0;
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
                 const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
@@ -545,7 +588,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     }
                 };
                 int kr0 = first * kBKp + kCq * quad;
-                fetch(kr0);
+                if (!(kLoadA && !sideB)) fetch(kr0);
                 for (int64_t ks = c0; ks < c1; ks += kBKp, ++sc) {
                     const int my_slot = slot;
                     const uint32_t my_ph = ph;
@@ -556,9 +599,21 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 #pragma unroll
                     for (int q = 0; q < kCq; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
                     kr0 += kGroups * kBKp;
-                    if (!(plan.dbg & 16)) fetch(kr0);
+                    if (!(kLoadA && !sideB) && !(plan.dbg & 16)) fetch(kr0);
                     mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
                     uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + sideB * kOpBytes;
+                    if (kLoadA && !sideB) {
+                        // x side: one bulk copy of the stage's pre-split tile; its expect_tx is this
+                        // warp's arrival on FULL and the copy's bytes complete the phase
+                        if (l == 0) {
+                            const int64_t sti = (ks - chunk0) / kBKp;
+                            const uint8_t *gsrc = ch.G + ((int64_t)it.tix * nst_chunk + sti) * kOpBytes;
+                            mbar_expect_tx(FULL(my_slot), kOpBytes);
+                            bulk_g2s(su32(op), gsrc, kOpBytes, FULL(my_slot));
+                        }
+                        __syncwarp();
+                        continue;
+                    }
                     if (!(plan.dbg & 1)) {
                         if constexpr (kF16) produce_f16<kFast>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
                         else produce<kFast>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
@@ -581,7 +636,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             const uint64_t adesc0 = umma_desc(smem_base), bdesc0 = umma_desc(smem_base + kOpBytes);
             const bool no_mma = (plan.dbg & 2) != 0;
             for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
-                const ItemInfo it = item_info(src, plan, item);
+                int64_t chunk0 = 0;
+            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
                 for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
                     const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
                     const uint32_t b = chunk_ctr & 1;
@@ -635,7 +691,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
         uint32_t chunk_ctr = 0;
         for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
-            const ItemInfo it = item_info(src, plan, item);
+            int64_t chunk0 = 0;
+            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
             double acc[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0.0;
@@ -694,8 +751,16 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             if (plan.dbg & 4) continue;
             if (!fuse) {
                 double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
+                if (kLoadA) {   // chunk partials add up in P_ws (zeroed before the first chunk)
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
+                    for (int i = 0; i < 32; i += 2) {
+                        const double2 p = *(const double2 *)(out + i);
+                        *(double2 *)(out + i) = make_double2(p.x + acc[i], p.y + acc[i + 1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) *(double2 *)(out + i) = make_double2(acc[i], acc[i + 1]);
+                }
                 continue;
             }
             // ---- fused a4 + a5: P tile (fp32; |dP| <= 2^-24 of the per-term bound B) -> SMEM ->
@@ -761,6 +826,75 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     }
 }
 
+// x-side bucket sums of one chunk for every x tile, split hi/lo and stored in the exact SW128
+// K-major stage layout of k_gemm_tf32<., 0, true> (16 KB per (x tile, 32-bucket stage)):
+// G[f, b] = sum_{k in bucket b} w_k E(f x_k) (one exact-phase table lookup per (corner, pair),
+// FP32 sums of <= 32 terms); the axis pair carries sum_k w_k x_k.  A block builds one 16 KB tile
+// in shared memory (warp w: buckets 4w .. 4w+3, lane: pair slot) and writes it out coalesced.
+template <bool kFast>
+__global__ void __launch_bounds__(256)
+k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ G) {
+    extern __shared__ __align__(1024) uint8_t gsm_raw[];
+    uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
+    uint8_t *tile = sm;
+    float2 *tab = (float2 *)(sm + kOpBytes);
+    const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
+    for (int i = threadIdx.x; i < tab_entries; i += blockDim.x) {
+        double sn, cs;
+        if (g.single) sincospi(2.0 * (double)i / (double)g.T, &sn, &cs);
+        else if (i < g.nhi) sincospi(2.0 * (double)((int64_t)i << g.lbits) / (double)g.T, &sn, &cs);
+        else sincospi(2.0 * (double)(i - g.nhi) / (double)g.T, &sn, &cs);
+        tab[i] = make_float2((float)cs, (float)sn);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t chunk0 = src.clip_bptr[0] + ch.chunk * ch.cb;
+    int64_t ke = src.clip_bptr[1];
+    if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
+    if (chunk0 >= ke) return;
+    const int64_t nst = (ke - chunk0 + kBK - 1) / kBK, nst_chunk = ch.cb / kBK;
+    const uint32_t M13 = 0xFFFFE000u;
+    for (int64_t u = blockIdx.x; u < nst * plan.tiles_x; u += gridDim.x) {
+        const int tix = (int)(u % plan.tiles_x);
+        const int64_t st = u / plan.tiles_x;
+        const int pg = tix * 32 + lane;
+        const uint32_t f = (uint32_t)(plan.X.f0 + pg);
+        const bool tw = pg < plan.X.nf, axis = plan.X.axis && pg == plan.X.nf;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+            const int kk = 4 * warp + q;
+            const int64_t b = chunk0 + st * kBK + kk;
+            float re = 0.f, im = 0.f;
+            if (b < ke) {
+                const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+                for (int c = cb; c < ce; ++c) {
+                    const int32_t x = __ldg(src.x + c);
+                    const float wt = (float)__ldg(src.w + c);
+                    if (tw) {
+                        const float2 e = twiddle<kFast>(phase<kFast>(f, (uint32_t)x, g), g, tab);
+                        re = fmaf(wt, e.x, re);
+                        im = fmaf(wt, e.y, im);
+                    } else if (axis) {
+                        re = fmaf(wt, (float)x, re);
+                    }
+                }
+            }
+            const float hr = __uint_as_float(__float_as_uint(re) & M13), hs = __uint_as_float(__float_as_uint(im) & M13);
+            const int r7 = lane & 7;
+            uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 2) ^ r7)) << 4) + ((kk & 3) << 2);
+            *(float *)(base) = re;                       // cos hi row (the MMA reads the top 19 bits)
+            *(float *)(base + 4 * 1024) = im;            // sin hi
+            *(float *)(base + 8 * 1024) = re - hr;       // cos lo
+            *(float *)(base + 12 * 1024) = im - hs;      // sin lo
+        }
+        __syncthreads();
+        uint4 *dst = (uint4 *)(G + ((int64_t)tix * nst_chunk + st) * kOpBytes);
+        const uint4 *srct = (const uint4 *)tile;
+        for (int i = threadIdx.x; i < kOpBytes / 16; i += blockDim.x) dst[i] = srct[i];
+        __syncthreads();
+    }
+}
+
 }  // namespace tc
 
 static tc::TabGeom make_tab(int32_t T) {
@@ -818,8 +952,53 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = plan.items < sms ? plan.items : sms;
-    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse, shift);
+    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse, shift, tc::TcChunk{nullptr, 0, 0});
     FCFS_CHECK_LAUNCH("k_gemm_tf32");
+    return FCFS_OK;
+}
+
+int64_t tc_chunk_buckets(int64_t K) {
+    int64_t cb = K < kFpChunkBuckets ? K : kFpChunkBuckets;
+    cb = (cb + tc::kBK - 1) / tc::kBK * tc::kBK;
+    return cb < tc::kBK ? tc::kBK : cb;
+}
+
+// one clip over row buckets, split-TF32: per chunk of buckets, the x-side tiles once (k_gsum_tc),
+// then the tcgen05 GEMM streaming them by bulk copy and adding into P_ws
+fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, uint8_t *G,
+                                     double *P_ws, cudaStream_t s) {
+    if (plan.items <= 0) return FCFS_OK;
+    FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
+    if (K <= 0) return FCFS_OK;
+    tc::TabGeom g = make_tab(T);
+    const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
+    const tc::Smem L = tc::smem_layout(entries);
+    const size_t smem = L.total + 1024;
+    const size_t gsmem = tc::kOpBytes + 1024 + (size_t)entries * 8;
+    const bool fast = g.single && g.pow2;
+    auto kern = fast ? tc::k_gemm_tf32<true, 0, true> : tc::k_gemm_tf32<false, 0, true>;
+    auto gk = fast ? tc::k_gsum_tc<true> : tc::k_gsum_tc<false>;
+    static size_t attr[2] = {0, 0};
+    const int ki = fast ? 1 : 0;
+    if (smem > attr[ki]) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+        attr[ki] = smem;
+    }
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = plan.items < sms ? plan.items : sms;
+    const int64_t cb = tc_chunk_buckets(K);
+    const int64_t nchunk = (K + cb - 1) / cb;   // buckets <= corners: an upper bound
+    EpiArgs e{};
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const tc::TcChunk ch{G, c, cb};
+        gk<<<(unsigned)(2 * sms), 256, gsmem, s>>>(src, plan, g, ch, G);
+        FCFS_CHECK_LAUNCH("k_gsum_tc");
+        kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, nullptr, 0, 0, ch);
+        FCFS_CHECK_LAUNCH("k_gemm_tf32");
+    }
     return FCFS_OK;
 }
 

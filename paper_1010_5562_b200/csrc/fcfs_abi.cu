@@ -161,8 +161,10 @@ struct CoeffWs {
     double *G;   // FP64 single clip: x-side bucket sums of one chunk, [tiles_x][cb][64]
 };
 
-// P_ws is not needed when the tcgen05 kernel fuses the epilogue (whole clip = one 64x64 tile)
-static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m_lo, int32_t m_hi) {
+// P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
+// tile).  A single split-TF32 clip always takes the chunked row-bucket path, which writes P.
+static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m_lo, int32_t m_hi, bool single = false) {
+    if (single && prec == FCFS_TF32X3) return false;
     EpiArgs ea{};
     ea.M = M; ea.m_lo = m_lo; ea.m_hi = m_hi;
     return (prec == FCFS_TF32X3 || prec == FCFS_F16X3) && tf32_can_fuse(p, ea);
@@ -175,8 +177,13 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
     w.G = nullptr;
-    if (prec == FCFS_FP64) carve_buckets(cv, K, B, w.bk);
-    if (prec == FCFS_FP64 && single) w.G = cv.take<double>((size_t)p.tiles_x * fp64_chunk_buckets(K) * kTile);
+    const bool bucketed = prec == FCFS_FP64 || (prec == FCFS_TF32X3 && single);
+    if (bucketed) carve_buckets(cv, K, B, w.bk);
+    if (bucketed && single) {
+        // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
+        const int64_t cb = fp64_chunk_buckets(K) > tc_chunk_buckets(K) ? fp64_chunk_buckets(K) : tc_chunk_buckets(K);
+        w.G = cv.take<double>((size_t)p.tiles_x * cb * kTile);
+    }
 }
 
 static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard, int32_t &m_lo, int32_t &m_hi) {
@@ -314,7 +321,7 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi), k, 1, prec, true);
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi, true), k, 1, prec, true);
     return cv.used();
 }
 
@@ -349,7 +356,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi), src.k_hi - src.k_lo, 1, prec, true);
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi, true), src.k_hi - src.k_lo, 1, prec, true);
     if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     EpiArgs ea;
@@ -370,6 +377,12 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
             // one clip: x-side bucket sums once per chunk, then the DMMA GEMM over them
             st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
             if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.P, s);
+        } else if (prec == FCFS_TF32X3) {
+            // the same chunked row-bucket scheme on the tcgen05 tensor cores
+            st = tf32_supported(plan, T);
+            if (st == FCFS_OK) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
+            if (st == FCFS_OK)
+                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, W.P, s);
         } else {
             st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
         }
