@@ -118,6 +118,7 @@ static constexpr int kLd = kTile + 4;   // padded smem row (doubles): conflict-f
 template <bool kLoadA>
 __global__ void __launch_bounds__(kThreads, 2)
 k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_ws, FpChunk ch) {
+    if (kLoadA && src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
     extern __shared__ __align__(16) double smem_d[];
     double2 *thi = (double2 *)smem_d;
     double2 *tlo = thi + g.nhi;
@@ -234,6 +235,7 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
 // axis pair (f = nf) carrying sum w_k x_k.  Persistent blocks over (slab of 16 buckets, x tile) units.
 __global__ void __launch_bounds__(kThreads)
 k_gsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__restrict__ G) {
+    if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
     extern __shared__ __align__(16) double smem_d[];
     double2 *thi = (double2 *)smem_d;
     double2 *tlo = thi + g.nhi;

@@ -462,6 +462,7 @@ template <bool kFast, int kF16, bool kLoadA = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse,
             int axis_shift, TcChunk ch) {
+    if (kLoadA && src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
     constexpr int kBKp = kF16 ? 2 * kBK : kBK;          // corners per stage (one 128 B row of K)
     constexpr int kCq = kF16 ? 8 : 4;                    // corners per 16-byte chunk (per producer task)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -834,6 +835,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 template <bool kFast>
 __global__ void __launch_bounds__(256)
 k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ G) {
+    if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
     extern __shared__ __align__(1024) uint8_t gsm_raw[];
     uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
     uint8_t *tile = sm;
@@ -860,16 +862,27 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
         const int pg = tix * 32 + lane;
         const uint32_t f = (uint32_t)(plan.X.f0 + pg);
         const bool tw = pg < plan.X.nf, axis = plan.X.axis && pg == plan.X.nf;
-#pragma unroll 1
+        // the 4 buckets' corners (<= 32 each) in one coalesced load per bucket: lane j holds corner
+        // cb + j; the sum loop broadcasts them with shuffles (no dependent global load per corner)
+        int cbq[4], cnq[4];
+        int32_t xq[4], wq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t b = chunk0 + st * kBK + 4 * warp + q;
+            cbq[q] = 0;
+            cnq[q] = 0;
+            if (b < ke) { cbq[q] = __ldg(src.bptr + b); cnq[q] = __ldg(src.bptr + b + 1) - cbq[q]; }
+            xq[q] = lane < cnq[q] ? __ldg(src.x + cbq[q] + lane) : 0;
+            wq[q] = lane < cnq[q] ? __ldg(src.w + cbq[q] + lane) : 0;
+        }
+#pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int kk = 4 * warp + q;
-            const int64_t b = chunk0 + st * kBK + kk;
             float re = 0.f, im = 0.f;
-            if (b < ke) {
-                const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
-                for (int c = cb; c < ce; ++c) {
-                    const int32_t x = __ldg(src.x + c);
-                    const float wt = (float)__ldg(src.w + c);
+            {
+                for (int j = 0; j < cnq[q]; ++j) {
+                    const int32_t x = __shfl_sync(0xffffffffu, xq[q], j);
+                    const float wt = (float)__shfl_sync(0xffffffffu, wq[q], j);
                     if (tw) {
                         const float2 e = twiddle<kFast>(phase<kFast>(f, (uint32_t)x, g), g, tab);
                         re = fmaf(wt, e.x, re);
