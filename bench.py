@@ -318,7 +318,7 @@ def main():
     c_ms_launch = c_ms / max(c_n, 1)
     # inner dimension of the contraction: corners (batched tcgen05 kernels) or row buckets (FP64, and
     # split-TF32 on one clip: Step 4 row structure, fcfs_row_buckets with the cap fcfs_coeffs uses)
-    if prec == "fp64" or (prec == "tf32x3" and wl.B == 1):
+    if prec == "fp64" or wl.B == 1:
         rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
         Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
         k_inner = "row buckets"

@@ -58,13 +58,16 @@ struct Smem {
     uint32_t total;
 };
 
-__host__ __device__ inline Smem smem_layout(int table_entries) {
+constexpr int kStagesLoadA = 6;                 // load-A mode: no fused-epilogue tables, one more stage
+
+// stages: operand ring depth; fused: room for the fused epilogue's output tables
+__host__ __device__ inline Smem smem_layout(int table_entries, int stages = kStages, bool fused = true) {
     Smem s;
     s.stage0 = 0;
-    s.table = kStages * kStageBytes;
+    s.table = stages * kStageBytes;
     s.xbuf = s.table + ((table_entries * 8 + 1023) & ~1023);
     s.bars = s.xbuf + 2 * 64 * kXStride * 4;       // xbuf also holds the fused epilogue's fp32 P tile (64 x 65)
-    s.total = s.bars + 256 + 4 * (kMaxFuseRows + 2) + 8 * 4 * kMaxFuseRows + 4 * kMaxFuseOut;
+    s.total = s.bars + 256 + (fused ? 4 * (kMaxFuseRows + 2) + 8 * 4 * kMaxFuseRows + 4 * kMaxFuseOut : 0);
     return s;
 }
 
@@ -220,6 +223,7 @@ struct TcChunk {
 };
 
 // item -> bucket range of the chunk, split at stage (kBK-bucket) boundaries
+template <int kBKp>
 __device__ __forceinline__ ItemInfo item_info_chunk(const CornerSrc &src, const GemmPlan &plan, const TcChunk &ch,
                                                     int64_t item, int64_t &chunk0) {
     const int64_t per_clip = (int64_t)plan.tiles_x * plan.tiles_y * plan.splits;
@@ -232,9 +236,9 @@ __device__ __forceinline__ ItemInfo item_info_chunk(const CornerSrc &src, const 
     chunk0 = src.clip_bptr[0] + ch.chunk * ch.cb;
     int64_t ke = src.clip_bptr[1];
     if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
-    const int64_t nst = ke > chunk0 ? (ke - chunk0 + 31) / 32 : 0;
-    it.k0 = chunk0 + 32 * (nst * split / plan.splits);
-    it.k1 = chunk0 + 32 * (nst * (split + 1) / plan.splits);
+    const int64_t nst = ke > chunk0 ? (ke - chunk0 + kBKp - 1) / kBKp : 0;
+    it.k0 = chunk0 + kBKp * (nst * split / plan.splits);
+    it.k1 = chunk0 + kBKp * (nst * (split + 1) / plan.splits);
     if (it.k1 > ke) it.k1 = ke;
     if (it.k0 > it.k1) it.k0 = it.k1;
     return it;
@@ -319,7 +323,7 @@ __device__ __forceinline__ void rot2(float2 &re, float2 &im, float2 c, float2 sn
 // the lo rows store the exact v - hi.  Padding slots (p > nf) keep recurrence values: they only
 // feed P entries nobody reads.  The axis slot (p == nf) is overwritten with the coordinate weight.
 // Bank use: a warp (one side) = 8 quads x 4 slot blocks; every STS.128 covers 4 full 128 B rows.
-template <bool kFast>
+template <bool kFast, int kSlots = 8>
 __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
                                         const int32_t v[4], const float wt[4], const TabGeom &g,
                                         const float2 *tab) {
@@ -337,10 +341,9 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         c1 = make_float4(e[0].x, e[1].x, e[2].x, e[3].x);
         s1 = make_float4(e[0].y, e[1].y, e[2].y, e[3].y);
     }
-    uint8_t *opq = op + (j0 >> 3) * 1024;
     const uint32_t M13 = 0xFFFFE000u;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
         float4 rl, il;
         rl.x = re.x - __uint_as_float(__float_as_uint(re.x) & M13);
         rl.y = re.y - __uint_as_float(__float_as_uint(re.y) & M13);
@@ -350,12 +353,13 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         il.y = im.y - __uint_as_float(__float_as_uint(im.y) & M13);
         il.z = im.z - __uint_as_float(__float_as_uint(im.z) & M13);
         il.w = im.w - __uint_as_float(__float_as_uint(im.w) & M13);
-        uint8_t *base = opq + i * kRowBytes + ((quad ^ i) << 4);   // row j0 + i (r % 8 == i)
+        const int r7 = (j0 + i) & 7;
+        uint8_t *base = op + ((j0 + i) >> 3) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);   // row j0 + i
         *(float4 *)(base) = re;                    // row r
         *(float4 *)(base + 4 * 1024) = im;         // row 32 + r
         *(float4 *)(base + 8 * 1024) = rl;         // row 64 + r
         *(float4 *)(base + 12 * 1024) = il;        // row 96 + r
-        if (i < 7) {   // packed: corners (0, 1) and (2, 3) per instruction
+        if (i < kSlots - 1) {   // packed: corners (0, 1) and (2, 3) per instruction
             float2 r01 = make_float2(re.x, re.y), r23 = make_float2(re.z, re.w);
             float2 i01 = make_float2(im.x, im.y), i23 = make_float2(im.z, im.w);
             rot2(r01, i01, make_float2(c1.x, c1.y), make_float2(s1.x, s1.y));
@@ -365,14 +369,15 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         }
     }
     const int ia = sp.nf - p0;
-    if (sp.axis && ia >= 0 && ia < 8) {
+    if (sp.axis && ia >= 0 && ia < kSlots) {
         float4 c, cl;
         c = make_float4(wt[0] * (float)v[0], wt[1] * (float)v[1], wt[2] * (float)v[2], wt[3] * (float)v[3]);
         cl.x = c.x - __uint_as_float(__float_as_uint(c.x) & M13);
         cl.y = c.y - __uint_as_float(__float_as_uint(c.y) & M13);
         cl.z = c.z - __uint_as_float(__float_as_uint(c.z) & M13);
         cl.w = c.w - __uint_as_float(__float_as_uint(c.w) & M13);
-        uint8_t *base = opq + ia * kRowBytes + ((quad ^ ia) << 4);
+        const int r7 = (j0 + ia) & 7;
+        uint8_t *base = op + ((j0 + ia) >> 3) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         *(float4 *)(base) = c;
         *(float4 *)(base + 4 * 1024) = z;
@@ -391,7 +396,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
 // normal values), lo = fp16(v - hi): |v - (hi + lo)| <= 2^-22 |v| + 2^-25 (fp16 subnormal step).
 // The axis slot carries the coordinate weight scaled by axs = 2^-s (exact) to stay in fp16
 // range; the epilogue multiplies the axis row / column of P back by 2^s.
-template <bool kFast>
+template <bool kFast, int kSlots = 8>
 __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0, const SidePlan &sp,
                                             const int32_t v[8], const float wt[8], float axs, const TabGeom &g,
                                             const float2 *tab) {
@@ -406,10 +411,9 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
         c1[q] = e.x;
         s1[q] = e.y;
     }
-    uint8_t *opq = op + (j0 >> 3) * 1024;
     const uint32_t M13 = 0xFFFFE000u;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
         uint32_t hc[4], hs[4], lc[4], ls[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -421,12 +425,13 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
             lc[h] = pack_h2(r0 - mr0, r1 - mr1);
             ls[h] = pack_h2(i0 - mi0, i1 - mi1);
         }
-        uint8_t *base = opq + i * kRowBytes + ((oct ^ i) << 4);   // row j0 + i (r % 8 == i)
+        const int r7 = (j0 + i) & 7;
+        uint8_t *base = op + ((j0 + i) >> 3) * 1024 + r7 * kRowBytes + ((oct ^ r7) << 4);   // row j0 + i
         *(uint4 *)(base) = make_uint4(hc[0], hc[1], hc[2], hc[3]);
         *(uint4 *)(base + 4 * 1024) = make_uint4(hs[0], hs[1], hs[2], hs[3]);
         *(uint4 *)(base + 8 * 1024) = make_uint4(lc[0], lc[1], lc[2], lc[3]);
         *(uint4 *)(base + 12 * 1024) = make_uint4(ls[0], ls[1], ls[2], ls[3]);
-        if (i < 7) {   // scalar here: the packed form spills at this register budget
+        if (i < kSlots - 1) {   // scalar here: the packed form spills at this register budget
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const float nr = fmaf(re[q], c1[q], -im[q] * s1[q]);
@@ -437,7 +442,7 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
         }
     }
     const int ia = sp.nf - p0;
-    if (sp.axis && ia >= 0 && ia < 8) {
+    if (sp.axis && ia >= 0 && ia < kSlots) {
         uint32_t hc[4], lc[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -446,7 +451,8 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
             hc[h] = pack_h2(m0, m1);
             lc[h] = pack_h2(c0 - m0, cc1 - m1);
         }
-        uint8_t *base = opq + ia * kRowBytes + ((oct ^ ia) << 4);
+        const int r7 = (j0 + ia) & 7;
+        uint8_t *base = op + ((j0 + ia) >> 3) * 1024 + r7 * kRowBytes + ((oct ^ r7) << 4);
         const uint4 z = make_uint4(0u, 0u, 0u, 0u);
         *(uint4 *)(base) = make_uint4(hc[0], hc[1], hc[2], hc[3]);
         *(uint4 *)(base + 4 * 1024) = z;
@@ -470,12 +476,13 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     // loads / stores compile to LDS / STS rather than generic LD / ST)
     uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
-    const Smem L = smem_layout(tab_entries);
+    constexpr int kS = kLoadA ? kStagesLoadA : kStages;   // operand ring depth of this instantiation
+    const Smem L = smem_layout(tab_entries, kS, !kLoadA);
     float2 *tab = (float2 *)(smem + L.table);
     float *xbuf = (float *)(smem + L.xbuf);
     uint64_t *bars = (uint64_t *)(smem + L.bars);
     // barrier indices: full[0..S), empty[S..2S), tfull[2S..2S+2), tempty[2S+2..2S+4)
-    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kStages + 4);
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kS + 4);
     int32_t *rowoff = (int32_t *)(smem + L.bars + 256);   // fused pupil layout: output offset per row
     // fused output tables: scale factors per |m| / |n| and the packed (m, n) of every output
     double *f_rows = (double *)(smem + L.bars + 256 + 4 * (kMaxFuseRows + 2));   // -1/(4 pi^2 a)
@@ -485,9 +492,9 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     uint32_t *f_mn = (uint32_t *)(f_axn + kMaxFuseRows);                        // (m+M) << 16 | (n+N), bit 31: masked
     const uint32_t bar0 = su32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
-    auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
-    auto TFULL = [&](int b) { return bar0 + 8u * (2 * kStages + b); };
-    auto TEMPTY = [&](int b) { return bar0 + 8u * (2 * kStages + 2 + b); };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (kS + s); };
+    auto TFULL = [&](int b) { return bar0 + 8u * (2 * kS + b); };
+    auto TEMPTY = [&](int b) { return bar0 + 8u * (2 * kS + 2 + b); };
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -512,7 +519,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     }
     if (tid == 0) {
         // FULL: one arrive per producer warp (after every lane's proxy fence + __syncwarp)
-        for (int s = 0; s < kStages; ++s) { mbar_init(FULL(s), kProdWarps / kGroups); mbar_init(EMPTY(s), 1); }
+        // FULL: one arrive per producer warp of the group (+ the x-side bulk copy's expect_tx in kLoadA)
+        for (int s = 0; s < kS; ++s) { mbar_init(FULL(s), kProdWarps / kGroups + (kLoadA ? 1 : 0)); mbar_init(EMPTY(s), 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(TFULL(b), 1); mbar_init(TEMPTY(b), kEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -559,18 +567,22 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         const int gq = pt >> 6;
         const int sideB = (pt >> 5) & 1;
         const int l = pt & 31;
-        const int quad = l & 7, j0 = (l >> 3) << 3;      // quad: 16-byte chunk of the stage
+        // kLoadA: both warps of a group make the y side (16 slots each, 4 per lane); lane 0 of warp 0
+        // also issues the x-side bulk copy
+        const int quad = l & 7;                           // quad: 16-byte chunk of the stage
+        const int j0 = kLoadA ? 16 * sideB + 4 * (l >> 3) : (l >> 3) << 3;
         const float axs = ldexpf(1.0f, -axis_shift);
-        const SidePlan sp = sideB ? plan.Y : plan.X;
-        const int32_t *vsrc = sideB ? (kLoadA ? src.by : src.y) : src.x;
+        const bool yside = kLoadA || sideB;
+        const SidePlan sp = yside ? plan.Y : plan.X;
+        const int32_t *vsrc = kLoadA ? src.by : (sideB ? src.y : src.x);
         const int64_t nst_chunk = kLoadA ? ch.cb / kBKp : 0;
         uint32_t sc = 0;                                  // global stage counter
         int slot = 0;                                     // sc % kStages
         uint32_t ph = 0;                                  // (sc / kStages) & 1
         for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
             int64_t chunk0 = 0;
-            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
-            const int p0 = (sideB ? it.tiy : it.tix) * 32 + j0;
+            const ItemInfo it = kLoadA ? item_info_chunk<kBKp>(src, plan, ch, item, chunk0) : item_info(src, plan, item);
+            const int p0 = (yside ? it.tiy : it.tix) * 32 + j0;
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
                 const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
                 // 32-bit corner offsets relative to the chunk base; one-own-stage-ahead prefetch
@@ -585,39 +597,36 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         const int kr = kr0 + q;
                         const bool ok = kr < n;
                         vn[q] = ok ? __ldg(vp + kr) : 0;
-                        wn[q] = ok ? (sideB ? 1 : __ldg(wp + kr)) : 0;
+                        wn[q] = ok ? (yside ? 1 : __ldg(wp + kr)) : 0;
                     }
                 };
                 int kr0 = first * kBKp + kCq * quad;
-                if (!(kLoadA && !sideB)) fetch(kr0);
+                fetch(kr0);
                 for (int64_t ks = c0; ks < c1; ks += kBKp, ++sc) {
                     const int my_slot = slot;
                     const uint32_t my_ph = ph;
-                    if (++slot == kStages) { slot = 0; ph ^= 1; }
+                    if (++slot == kS) { slot = 0; ph ^= 1; }
                     if ((int)(sc & 3) != gq) continue;
                     int32_t v[kCq];
                     float wt[kCq];
 #pragma unroll
                     for (int q = 0; q < kCq; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
                     kr0 += kGroups * kBKp;
-                    if (!(kLoadA && !sideB) && !(plan.dbg & 16)) fetch(kr0);
+                    if (!(plan.dbg & 16)) fetch(kr0);
                     mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
-                    uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + sideB * kOpBytes;
-                    if (kLoadA && !sideB) {
-                        // x side: one bulk copy of the stage's pre-split tile; its expect_tx is this
-                        // warp's arrival on FULL and the copy's bytes complete the phase
-                        if (l == 0) {
-                            const int64_t sti = (ks - chunk0) / kBKp;
-                            const uint8_t *gsrc = ch.G + ((int64_t)it.tix * nst_chunk + sti) * kOpBytes;
-                            mbar_expect_tx(FULL(my_slot), kOpBytes);
-                            bulk_g2s(su32(op), gsrc, kOpBytes, FULL(my_slot));
-                        }
-                        __syncwarp();
-                        continue;
+                    uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + (yside ? kOpBytes : 0);
+                    if (kLoadA && !sideB && l == 0) {
+                        // x side: one bulk copy of the stage's pre-split tile; its expect_tx is one
+                        // arrival on FULL and the copy's bytes complete the phase
+                        const int64_t sti = (ks - chunk0) / kBKp;
+                        const uint8_t *gsrc = ch.G + ((int64_t)it.tix * nst_chunk + sti) * kOpBytes;
+                        mbar_expect_tx(FULL(my_slot), kOpBytes);
+                        bulk_g2s(su32(op - kOpBytes), gsrc, kOpBytes, FULL(my_slot));
                     }
                     if (!(plan.dbg & 1)) {
-                        if constexpr (kF16) produce_f16<kFast>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
-                        else produce<kFast>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
+                        constexpr int kSl = kLoadA ? 4 : 8;
+                        if constexpr (kF16) produce_f16<kFast, kSl>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
+                        else produce<kFast, kSl>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
                     }
                     if (!(plan.dbg & 8)) fence_proxy_async();
                     __syncwarp();
@@ -638,7 +647,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             const bool no_mma = (plan.dbg & 2) != 0;
             for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
                 int64_t chunk0 = 0;
-            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
+            const ItemInfo it = kLoadA ? item_info_chunk<kBKp>(src, plan, ch, item, chunk0) : item_info(src, plan, item);
                 for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk, ++chunk_ctr) {
                     const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
                     const uint32_t b = chunk_ctr & 1;
@@ -650,8 +659,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     // per 8 MMAs, so the single issuing warp stays ahead of the tensor pipe
                     for (int st = 0; st < nst; st += 2) {
                         const int two = (st + 1 < nst) ? 1 : 0;
-                        const int s1 = (stage + 1 == kStages) ? 0 : stage + 1;
-                        const uint32_t p1 = (stage + 1 == kStages) ? phase_bit ^ 1 : phase_bit;
+                        const int s1 = (stage + 1 == kS) ? 0 : stage + 1;
+                        const uint32_t p1 = (stage + 1 == kS) ? phase_bit ^ 1 : phase_bit;
                         mbar_wait(FULL(stage), phase_bit);
                         if (two) mbar_wait(FULL(s1), p1);
                         tc_fence_after();
@@ -677,7 +686,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         __syncwarp();
                         stage = two ? s1 : stage;
                         phase_bit = two ? p1 : phase_bit;
-                        if (++stage == kStages) { stage = 0; phase_bit ^= 1; }
+                        if (++stage == kS) { stage = 0; phase_bit ^= 1; }
                     }
                     if (elect_one()) umma_commit(TFULL(b));
                     __syncwarp();
@@ -693,7 +702,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         uint32_t chunk_ctr = 0;
         for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
             int64_t chunk0 = 0;
-            const ItemInfo it = kLoadA ? item_info_chunk(src, plan, ch, item, chunk0) : item_info(src, plan, item);
+            const ItemInfo it = kLoadA ? item_info_chunk<kBKp>(src, plan, ch, item, chunk0) : item_info(src, plan, item);
             double acc[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0.0;
@@ -832,9 +841,13 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 // G[f, b] = sum_{k in bucket b} w_k E(f x_k) (one exact-phase table lookup per (corner, pair),
 // FP32 sums of <= 32 terms); the axis pair carries sum_k w_k x_k.  A block builds one 16 KB tile
 // in shared memory (warp w: buckets 4w .. 4w+3, lane: pair slot) and writes it out coalesced.
-template <bool kFast>
+// kF16: the fp16 hi/lo layout of k_gemm_tf32<., 1, true> (64 buckets per 128-byte row, 2 B per
+// element; the axis pair scaled by axs = 2^-axis_shift to stay in fp16 range)
+template <bool kFast, int kF16>
 __global__ void __launch_bounds__(256)
-k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ G) {
+k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ G, float axs) {
+    constexpr int kBKp = kF16 ? 2 * kBK : kBK;   // buckets per stage
+    constexpr int kPerWarp = kBKp / 8;           // buckets per warp
     if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
     extern __shared__ __align__(1024) uint8_t gsm_raw[];
     uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
@@ -854,7 +867,7 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
     int64_t ke = src.clip_bptr[1];
     if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
     if (chunk0 >= ke) return;
-    const int64_t nst = (ke - chunk0 + kBK - 1) / kBK, nst_chunk = ch.cb / kBK;
+    const int64_t nst = (ke - chunk0 + kBKp - 1) / kBKp, nst_chunk = ch.cb / kBKp;
     const uint32_t M13 = 0xFFFFE000u;
     for (int64_t u = blockIdx.x; u < nst * plan.tiles_x; u += gridDim.x) {
         const int tix = (int)(u % plan.tiles_x);
@@ -864,11 +877,11 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
         const bool tw = pg < plan.X.nf, axis = plan.X.axis && pg == plan.X.nf;
         // the 4 buckets' corners (<= 32 each) in one coalesced load per bucket: lane j holds corner
         // cb + j; the sum loop broadcasts them with shuffles (no dependent global load per corner)
-        int cbq[4], cnq[4];
-        int32_t xq[4], wq[4];
+        int cbq[kPerWarp], cnq[kPerWarp];
+        int32_t xq[kPerWarp], wq[kPerWarp];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t b = chunk0 + st * kBK + 4 * warp + q;
+        for (int q = 0; q < kPerWarp; ++q) {
+            const int64_t b = chunk0 + st * kBKp + kPerWarp * warp + q;
             cbq[q] = 0;
             cnq[q] = 0;
             if (b < ke) { cbq[q] = __ldg(src.bptr + b); cnq[q] = __ldg(src.bptr + b + 1) - cbq[q]; }
@@ -876,8 +889,8 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
             wq[q] = lane < cnq[q] ? __ldg(src.w + cbq[q] + lane) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int kk = 4 * warp + q;
+        for (int q = 0; q < kPerWarp; ++q) {
+            const int kk = kPerWarp * warp + q;
             float re = 0.f, im = 0.f;
             {
                 for (int j = 0; j < cnq[q]; ++j) {
@@ -892,13 +905,22 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
                     }
                 }
             }
+            if (kF16 && axis) re *= axs;
             const float hr = __uint_as_float(__float_as_uint(re) & M13), hs = __uint_as_float(__float_as_uint(im) & M13);
             const int r7 = lane & 7;
-            uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 2) ^ r7)) << 4) + ((kk & 3) << 2);
-            *(float *)(base) = re;                       // cos hi row (the MMA reads the top 19 bits)
-            *(float *)(base + 4 * 1024) = im;            // sin hi
-            *(float *)(base + 8 * 1024) = re - hr;       // cos lo
-            *(float *)(base + 12 * 1024) = im - hs;      // sin lo
+            if constexpr (!kF16) {
+                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 2) ^ r7)) << 4) + ((kk & 3) << 2);
+                *(float *)(base) = re;                       // cos hi row (the MMA reads the top 19 bits)
+                *(float *)(base + 4 * 1024) = im;            // sin hi
+                *(float *)(base + 8 * 1024) = re - hr;       // cos lo
+                *(float *)(base + 12 * 1024) = im - hs;      // sin lo
+            } else {                                         // hi: 11 significant bits, exact in fp16
+                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 3) ^ r7)) << 4) + ((kk & 7) << 1);
+                *(__half *)(base) = __float2half_rn(hr);
+                *(__half *)(base + 4 * 1024) = __float2half_rn(hs);
+                *(__half *)(base + 8 * 1024) = __float2half_rn(re - hr);
+                *(__half *)(base + 12 * 1024) = __float2half_rn(im - hs);
+            }
         }
         __syncthreads();
         uint4 *dst = (uint4 *)(G + ((int64_t)tix * nst_chunk + st) * kOpBytes);
@@ -970,29 +992,31 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     return FCFS_OK;
 }
 
-int64_t tc_chunk_buckets(int64_t K) {
+int64_t tc_chunk_buckets(int64_t K) {   // a multiple of both stage sizes (32 tf32 / 64 fp16 buckets)
     int64_t cb = K < kFpChunkBuckets ? K : kFpChunkBuckets;
-    cb = (cb + tc::kBK - 1) / tc::kBK * tc::kBK;
-    return cb < tc::kBK ? tc::kBK : cb;
+    cb = (cb + 2 * tc::kBK - 1) / (2 * tc::kBK) * (2 * tc::kBK);
+    return cb < 2 * tc::kBK ? 2 * tc::kBK : cb;
 }
 
 // one clip over row buckets, split-TF32: per chunk of buckets, the x-side tiles once (k_gsum_tc),
 // then the tcgen05 GEMM streaming them by bulk copy and adding into P_ws
 fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, uint8_t *G,
-                                     double *P_ws, cudaStream_t s) {
+                                     double *P_ws, bool f16, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
     if (K <= 0) return FCFS_OK;
     tc::TabGeom g = make_tab(T);
     const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
-    const tc::Smem L = tc::smem_layout(entries);
+    const tc::Smem L = tc::smem_layout(entries, tc::kStagesLoadA, false);
     const size_t smem = L.total + 1024;
     const size_t gsmem = tc::kOpBytes + 1024 + (size_t)entries * 8;
     const bool fast = g.single && g.pow2;
-    auto kern = fast ? tc::k_gemm_tf32<true, 0, true> : tc::k_gemm_tf32<false, 0, true>;
-    auto gk = fast ? tc::k_gsum_tc<true> : tc::k_gsum_tc<false>;
-    static size_t attr[2] = {0, 0};
-    const int ki = fast ? 1 : 0;
+    auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1, true> : tc::k_gemm_tf32<false, 1, true>)
+                    : (fast ? tc::k_gemm_tf32<true, 0, true> : tc::k_gemm_tf32<false, 0, true>);
+    auto gk = f16 ? (fast ? tc::k_gsum_tc<true, 1> : tc::k_gsum_tc<false, 1>)
+                  : (fast ? tc::k_gsum_tc<true, 0> : tc::k_gsum_tc<false, 0>);
+    static size_t attr[4] = {0, 0, 0, 0};
+    const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
     if (smem > attr[ki]) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         FCFS_TRY_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
@@ -1005,11 +1029,19 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
     const int64_t cb = tc_chunk_buckets(K);
     const int64_t nchunk = (K + cb - 1) / cb;   // buckets <= corners: an upper bound
     EpiArgs e{};
+    // fp16 range: the axis slots carry sums of <= kRowBucketCapFp64 coordinate weights (<= T |w|),
+    // scaled by 2^-shift so that 32 (T + 1) 2^-shift <= 2048
+    int shift = 0;
+    if (f16) {
+        const int tb = ilog2_ceil((int64_t)kRowBucketCapFp64 * ((int64_t)T + 1));
+        shift = tb > 11 ? tb - 11 : 0;
+    }
+    const float axs = ldexpf(1.0f, -shift);
     for (int64_t c = 0; c < nchunk; ++c) {
         const tc::TcChunk ch{G, c, cb};
-        gk<<<(unsigned)(2 * sms), 256, gsmem, s>>>(src, plan, g, ch, G);
+        gk<<<(unsigned)(2 * sms), 256, gsmem, s>>>(src, plan, g, ch, G, axs);
         FCFS_CHECK_LAUNCH("k_gsum_tc");
-        kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, nullptr, 0, 0, ch);
+        kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, nullptr, 0, shift, ch);
         FCFS_CHECK_LAUNCH("k_gemm_tf32");
     }
     return FCFS_OK;

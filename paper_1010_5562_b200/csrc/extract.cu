@@ -210,19 +210,35 @@ __global__ void k_flags(const int32_t *wts, const int64_t *num_runs, int64_t n, 
 __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, const int32_t *flags,
                           const int32_t *pos, int64_t n, int64_t cap, int32_t *x, int32_t *y, int32_t *w,
                           unsigned long long *ckeys, int64_t *area, int64_t *K) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (i == n - 1) *K = (int64_t)pos[i] + flags[i];
-        if (!flags[i]) continue;
-        unsigned long long key = ukeys[i];
-        int32_t xx = (int32_t)(key & ((1ull << kCoordBits) - 1));
-        int32_t yy = (int32_t)((key >> kCoordBits) & ((1ull << kCoordBits) - 1));
-        int64_t b = (int64_t)(key >> (2 * kCoordBits));
-        int64_t p = pos[i];
-        ckeys[p] = key;
-        if (p < cap) { x[p] = xx; y[p] = yy; w[p] = agg[i]; }
-        long long a = (long long)agg[i] * (long long)xx * (long long)yy;
-        atomicAdd((unsigned long long *)&area[b], (unsigned long long)a);
+    // warp-uniform loop: the area is reduced over the warp before the atomic (corners are sorted by
+    // clip, so a warp nearly always holds one clip: one atomic per warp instead of one per corner)
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const int64_t i = i0 + lane;
+        const bool valid = i < n;
+        long long a = 0;
+        int64_t b = -1;
+        if (valid) {
+            if (i == n - 1) *K = (int64_t)pos[i] + flags[i];
+            const unsigned long long key = ukeys[i];
+            b = (int64_t)(key >> (2 * kCoordBits));
+            if (flags[i]) {
+                const int32_t xx = (int32_t)(key & ((1ull << kCoordBits) - 1));
+                const int32_t yy = (int32_t)((key >> kCoordBits) & ((1ull << kCoordBits) - 1));
+                const int64_t p = pos[i];
+                ckeys[p] = key;
+                if (p < cap) { x[p] = xx; y[p] = yy; w[p] = agg[i]; }
+                a = (long long)agg[i] * (long long)xx * (long long)yy;
+            }
+        }
+        const int64_t b0 = __shfl_sync(0xffffffffu, b, 0);
+        if (__all_sync(0xffffffffu, !valid || b == b0)) {
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0 && a != 0) atomicAdd((unsigned long long *)&area[b0], (unsigned long long)a);
+        } else if (valid && a != 0) {
+            atomicAdd((unsigned long long *)&area[b], (unsigned long long)a);
+        }
     }
 }
 

@@ -162,9 +162,9 @@ struct CoeffWs {
 };
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
-// tile).  A single split-TF32 clip always takes the chunked row-bucket path, which writes P.
+// tile).  A single clip always takes the chunked row-bucket path, which writes P.
 static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m_lo, int32_t m_hi, bool single = false) {
-    if (single && prec == FCFS_TF32X3) return false;
+    if (single) return false;   // one clip: the chunked row-bucket path, which writes P
     EpiArgs ea{};
     ea.M = M; ea.m_lo = m_lo; ea.m_hi = m_hi;
     return (prec == FCFS_TF32X3 || prec == FCFS_F16X3) && tf32_can_fuse(p, ea);
@@ -177,7 +177,7 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
     w.G = nullptr;
-    const bool bucketed = prec == FCFS_FP64 || (prec == FCFS_TF32X3 && single);
+    const bool bucketed = prec == FCFS_FP64 || single;
     if (bucketed) carve_buckets(cv, K, B, w.bk);
     if (bucketed && single) {
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
@@ -377,12 +377,13 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
             // one clip: x-side bucket sums once per chunk, then the DMMA GEMM over them
             st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
             if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.P, s);
-        } else if (prec == FCFS_TF32X3) {
+        } else if (prec == FCFS_TF32X3 || prec == FCFS_F16X3) {
             // the same chunked row-bucket scheme on the tcgen05 tensor cores
             st = tf32_supported(plan, T);
             if (st == FCFS_OK) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
             if (st == FCFS_OK)
-                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, W.P, s);
+                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, W.P,
+                                              prec == FCFS_F16X3, s);
         } else {
             st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
         }
