@@ -165,7 +165,7 @@ fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan,
                                      double *P_ws, cudaStream_t s);
 int64_t tc_chunk_buckets(int64_t K);
 fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, uint8_t *G,
-                                     double *P_ws, bool f16, cudaStream_t s);
+                                     uint8_t *H, double *P_ws, bool f16, cudaStream_t s);
 fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F,
                             cudaStream_t s);
 fcfs_status launch_block_area(const CornerSrc &src, int64_t *area_dev, cudaStream_t s);

@@ -153,6 +153,19 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// ---- debug event trace (FCFS_DEBUG bit 256; CTA 0 only): clock64 << 24 | event << 16 | stage
+constexpr int kTraceMax = 1 << 16;
+__device__ unsigned long long g_trace[kTraceMax];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(int on, int ev, uint32_t sc) {
+#ifndef FCFS_TRACE
+    return;   // compiled in only with -DFCFS_TRACE (tools/trace_*.py)
+#endif
+    if (!on || blockIdx.x != 0) return;
+    const unsigned int i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceMax) g_trace[i] = ((unsigned long long)clock64() << 24) | ((unsigned long long)ev << 16) | (sc & 0xFFFFu);
+}
+
 __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -191,6 +204,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 #define TMEM_LD32(taddr, r)                                                                                  \
     asm volatile(                                                                                            \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
@@ -218,8 +235,9 @@ struct ItemInfo {
 // chunked row-bucket mode (single clip): the x-side operand of every stage comes from G, the
 // pre-split bucket sums of chunk `chunk` (k_gsum_tc), [tiles_x][stages of the chunk][16 KB]
 struct TcChunk {
-    const uint8_t *G;
-    int64_t chunk, cb;    // chunk index, buckets per chunk (a multiple of kBK)
+    const uint8_t *G;     // x side: pre-split bucket sums, [tiles_x][stages of the chunk][16 KB]
+    int64_t chunk, cb;    // chunk index, buckets per chunk (a multiple of 2 kBK)
+    const uint8_t *H;     // y side: pre-split row twiddles E_y[n, y_b], [tiles_y][stages][16 KB]
 };
 
 // item -> bucket range of the chunk, split at stage (kBK-bucket) boundaries
@@ -353,8 +371,9 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         il.y = im.y - __uint_as_float(__float_as_uint(im.y) & M13);
         il.z = im.z - __uint_as_float(__float_as_uint(im.z) & M13);
         il.w = im.w - __uint_as_float(__float_as_uint(im.w) & M13);
-        const int r7 = (j0 + i) & 7;
-        uint8_t *base = op + ((j0 + i) >> 3) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);   // row j0 + i
+        // row j0 + i; 8-slot blocks start on an 8-row atom (j0 % 8 == 0): r % 8 == i
+        const int r7 = kSlots == 8 ? i : ((j0 + i) & 7);
+        uint8_t *base = op + (kSlots == 8 ? (j0 >> 3) : ((j0 + i) >> 3)) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);
         *(float4 *)(base) = re;                    // row r
         *(float4 *)(base + 4 * 1024) = im;         // row 32 + r
         *(float4 *)(base + 8 * 1024) = rl;         // row 64 + r
@@ -425,8 +444,8 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
             lc[h] = pack_h2(r0 - mr0, r1 - mr1);
             ls[h] = pack_h2(i0 - mi0, i1 - mi1);
         }
-        const int r7 = (j0 + i) & 7;
-        uint8_t *base = op + ((j0 + i) >> 3) * 1024 + r7 * kRowBytes + ((oct ^ r7) << 4);   // row j0 + i
+        const int r7 = kSlots == 8 ? i : ((j0 + i) & 7);
+        uint8_t *base = op + (kSlots == 8 ? (j0 >> 3) : ((j0 + i) >> 3)) * 1024 + r7 * kRowBytes + ((oct ^ r7) << 4);
         *(uint4 *)(base) = make_uint4(hc[0], hc[1], hc[2], hc[3]);
         *(uint4 *)(base + 4 * 1024) = make_uint4(hs[0], hs[1], hs[2], hs[3]);
         *(uint4 *)(base + 8 * 1024) = make_uint4(lc[0], lc[1], lc[2], lc[3]);
@@ -498,6 +517,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int tr = plan.dbg & 256;
 
     // twiddle table (all threads), barriers (thread 0), TMEM (MMA warp)
     for (int i = tid; i < tab_entries; i += kThreads) {
@@ -520,7 +540,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     if (tid == 0) {
         // FULL: one arrive per producer warp (after every lane's proxy fence + __syncwarp)
         // FULL: one arrive per producer warp of the group (+ the x-side bulk copy's expect_tx in kLoadA)
-        for (int s = 0; s < kS; ++s) { mbar_init(FULL(s), kProdWarps / kGroups + (kLoadA ? 1 : 0)); mbar_init(EMPTY(s), 1); }
+        for (int s = 0; s < kS; ++s) { mbar_init(FULL(s), kLoadA ? 1 : kProdWarps / kGroups); mbar_init(EMPTY(s), 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(TFULL(b), 1); mbar_init(TEMPTY(b), kEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -613,15 +633,29 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     for (int q = 0; q < kCq; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
                     kr0 += kGroups * kBKp;
                     if (!(plan.dbg & 16)) fetch(kr0);
+                    if (l == 0) trace(tr, 10 + gq * 2 + sideB, sc);
                     mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
+                    if (l == 0) trace(tr, 20 + gq * 2 + sideB, sc);
                     uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + (yside ? kOpBytes : 0);
-                    if (kLoadA && !sideB && l == 0) {
-                        // x side: one bulk copy of the stage's pre-split tile; its expect_tx is one
-                        // arrival on FULL and the copy's bytes complete the phase
-                        const int64_t sti = (ks - chunk0) / kBKp;
-                        const uint8_t *gsrc = ch.G + ((int64_t)it.tix * nst_chunk + sti) * kOpBytes;
-                        mbar_expect_tx(FULL(my_slot), kOpBytes);
-                        bulk_g2s(su32(op - kOpBytes), gsrc, kOpBytes, FULL(my_slot));
+                    if (kLoadA) {
+                        // both operand tiles of the stage are precomputed (k_gsum_tc / k_hsum_tc): one
+                        // lane issues the two 16 KB bulk copies; its expect_tx is the only arrival on
+                        // FULL and the copies' bytes complete the phase.  The tiles 16 stages ahead are
+                        // prefetched into L2, so the copies that must wait for the slot find them on chip.
+                        if (!sideB && l == 0) {
+                            const int64_t sti = (ks - chunk0) / kBKp;
+                            const uint8_t *gsrc = ch.G + ((int64_t)it.tix * nst_chunk + sti) * kOpBytes;
+                            const uint8_t *hsrc = ch.H + ((int64_t)it.tiy * nst_chunk + sti) * kOpBytes;
+                            mbar_expect_tx(FULL(my_slot), 2 * kOpBytes);
+                            bulk_g2s(su32(op - kOpBytes), gsrc, kOpBytes, FULL(my_slot));
+                            bulk_g2s(su32(op), hsrc, kOpBytes, FULL(my_slot));
+                            if (ks + 16 * kBKp < it.k1) {
+                                prefetch_l2(gsrc + 16 * kOpBytes, kOpBytes);
+                                prefetch_l2(hsrc + 16 * kOpBytes, kOpBytes);
+                            }
+                        }
+                        __syncwarp();
+                        continue;
                     }
                     if (!(plan.dbg & 1)) {
                         constexpr int kSl = kLoadA ? 4 : 8;
@@ -630,7 +664,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     }
                     if (!(plan.dbg & 8)) fence_proxy_async();
                     __syncwarp();
-                    if (l == 0) mbar_arrive(FULL(my_slot));
+                    if (l == 0) { trace(tr, 30 + gq * 2 + sideB, sc); mbar_arrive(FULL(my_slot)); }
                 }
             }
         }
@@ -642,6 +676,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             int stage = 0;
             uint32_t phase_bit = 0;
             uint32_t chunk_ctr = 0;
+            uint32_t msc = 0;
             const uint32_t smem_base = su32(smem + L.stage0);
             const uint64_t adesc0 = umma_desc(smem_base), bdesc0 = umma_desc(smem_base + kOpBytes);
             const bool no_mma = (plan.dbg & 2) != 0;
@@ -657,12 +692,17 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     const int nst = (int)((c1 - c0 + kBKp - 1) / kBKp);   // stages in this chunk
                     // two stages per iteration: the barrier waits, fences and the elect are paid once
                     // per 8 MMAs, so the single issuing warp stays ahead of the tensor pipe
-                    for (int st = 0; st < nst; st += 2) {
-                        const int two = (st + 1 < nst) ? 1 : 0;
+                    // kLoadA: one stage at a time (a slot is released as soon as its own MMAs complete:
+                    // the bulk copies that refill it start earlier).  Per-corner mode: two stages per
+                    // iteration, so the waits, fences and the elect are paid once per 8 MMAs.
+                    constexpr int kPer = kLoadA ? 1 : 2;
+                    for (int st = 0; st < nst; st += kPer) {
+                        const int two = (kPer == 2 && st + 1 < nst) ? 1 : 0;
                         const int s1 = (stage + 1 == kS) ? 0 : stage + 1;
                         const uint32_t p1 = (stage + 1 == kS) ? phase_bit ^ 1 : phase_bit;
                         mbar_wait(FULL(stage), phase_bit);
                         if (two) mbar_wait(FULL(s1), p1);
+                        if (lane == 0) trace(tr, 50, msc);
                         tc_fence_after();
                         const uint64_t off0 = (uint64_t)((stage * kStageBytes) >> 4);
                         const uint64_t off1 = (uint64_t)((s1 * kStageBytes) >> 4);
@@ -684,6 +724,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                             }
                         }
                         __syncwarp();
+                        msc += 1 + two;
                         stage = two ? s1 : stage;
                         phase_bit = two ? p1 : phase_bit;
                         if (++stage == kS) { stage = 0; phase_bit ^= 1; }
@@ -930,6 +971,78 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
     }
 }
 
+// y-side row twiddles of one chunk for every y tile, split hi/lo, in the same stage layout:
+// H[n, b] = E(n y_b) (one exact-phase table lookup per (bucket, pair)); the axis pair carries y_b.
+template <bool kFast, int kF16>
+__global__ void __launch_bounds__(256)
+k_hsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ H, float axs) {
+    if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
+    constexpr int kBKp = kF16 ? 2 * kBK : kBK;
+    constexpr int kPerWarp = kBKp / 8;
+    extern __shared__ __align__(1024) uint8_t hsm_raw[];
+    uint8_t *sm = hsm_raw + ((1024u - (su32(hsm_raw) & 1023u)) & 1023u);
+    uint8_t *tile = sm;
+    float2 *tab = (float2 *)(sm + kOpBytes);
+    const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
+    for (int i = threadIdx.x; i < tab_entries; i += blockDim.x) {
+        double sn, cs;
+        if (g.single) sincospi(2.0 * (double)i / (double)g.T, &sn, &cs);
+        else if (i < g.nhi) sincospi(2.0 * (double)((int64_t)i << g.lbits) / (double)g.T, &sn, &cs);
+        else sincospi(2.0 * (double)(i - g.nhi) / (double)g.T, &sn, &cs);
+        tab[i] = make_float2((float)cs, (float)sn);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t chunk0 = src.clip_bptr[0] + ch.chunk * ch.cb;
+    int64_t ke = src.clip_bptr[1];
+    if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
+    const int64_t nst = (ke - chunk0 + kBKp - 1) / kBKp, nst_chunk = ch.cb / kBKp;
+    const uint32_t M13 = 0xFFFFE000u;
+    for (int64_t u = blockIdx.x; u < nst * plan.tiles_y; u += gridDim.x) {
+        const int tiy = (int)(u % plan.tiles_y);
+        const int64_t st = u / plan.tiles_y;
+        const int pg = tiy * 32 + lane;
+        const uint32_t f = (uint32_t)(plan.Y.f0 + pg);
+        const bool tw = pg < plan.Y.nf, axis = plan.Y.axis && pg == plan.Y.nf;
+#pragma unroll
+        for (int q = 0; q < kPerWarp; ++q) {
+            const int kk = kPerWarp * warp + q;
+            const int64_t b = chunk0 + st * kBKp + kk;
+            float re = 0.f, im = 0.f;
+            if (b < ke) {
+                const int32_t y = __ldg(src.by + b);
+                if (tw) {
+                    const float2 e = twiddle<kFast>(phase<kFast>(f, (uint32_t)y, g), g, tab);
+                    re = e.x;
+                    im = e.y;
+                } else if (axis) {
+                    re = (float)y * (kF16 ? axs : 1.f);
+                }
+            }
+            const float hr = __uint_as_float(__float_as_uint(re) & M13), hs = __uint_as_float(__float_as_uint(im) & M13);
+            const int r7 = lane & 7;
+            if constexpr (!kF16) {
+                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 2) ^ r7)) << 4) + ((kk & 3) << 2);
+                *(float *)(base) = re;
+                *(float *)(base + 4 * 1024) = im;
+                *(float *)(base + 8 * 1024) = re - hr;
+                *(float *)(base + 12 * 1024) = im - hs;
+            } else {
+                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 3) ^ r7)) << 4) + ((kk & 7) << 1);
+                *(__half *)(base) = __float2half_rn(hr);
+                *(__half *)(base + 4 * 1024) = __float2half_rn(hs);
+                *(__half *)(base + 8 * 1024) = __float2half_rn(re - hr);
+                *(__half *)(base + 12 * 1024) = __float2half_rn(im - hs);
+            }
+        }
+        __syncthreads();
+        uint4 *dst = (uint4 *)(H + ((int64_t)tiy * nst_chunk + st) * kOpBytes);
+        const uint4 *srct = (const uint4 *)tile;
+        for (int i = threadIdx.x; i < kOpBytes / 16; i += blockDim.x) dst[i] = srct[i];
+        __syncthreads();
+    }
+}
+
 }  // namespace tc
 
 static tc::TabGeom make_tab(int32_t T) {
@@ -987,7 +1100,7 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = plan.items < sms ? plan.items : sms;
-    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse, shift, tc::TcChunk{nullptr, 0, 0});
+    kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, F, fuse, shift, tc::TcChunk{nullptr, 0, 0, nullptr});
     FCFS_CHECK_LAUNCH("k_gemm_tf32");
     return FCFS_OK;
 }
@@ -1001,7 +1114,7 @@ int64_t tc_chunk_buckets(int64_t K) {   // a multiple of both stage sizes (32 tf
 // one clip over row buckets, split-TF32: per chunk of buckets, the x-side tiles once (k_gsum_tc),
 // then the tcgen05 GEMM streaming them by bulk copy and adding into P_ws
 fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, uint8_t *G,
-                                     double *P_ws, bool f16, cudaStream_t s) {
+                                     uint8_t *H, double *P_ws, bool f16, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
     if (K <= 0) return FCFS_OK;
@@ -1015,11 +1128,14 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
                     : (fast ? tc::k_gemm_tf32<true, 0, true> : tc::k_gemm_tf32<false, 0, true>);
     auto gk = f16 ? (fast ? tc::k_gsum_tc<true, 1> : tc::k_gsum_tc<false, 1>)
                   : (fast ? tc::k_gsum_tc<true, 0> : tc::k_gsum_tc<false, 0>);
+    auto hk = f16 ? (fast ? tc::k_hsum_tc<true, 1> : tc::k_hsum_tc<false, 1>)
+                  : (fast ? tc::k_hsum_tc<true, 0> : tc::k_hsum_tc<false, 0>);
     static size_t attr[4] = {0, 0, 0, 0};
     const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
     if (smem > attr[ki]) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         FCFS_TRY_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
         attr[ki] = smem;
     }
     int sms = 148;
@@ -1038,9 +1154,11 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
     }
     const float axs = ldexpf(1.0f, -shift);
     for (int64_t c = 0; c < nchunk; ++c) {
-        const tc::TcChunk ch{G, c, cb};
+        const tc::TcChunk ch{G, c, cb, H};
         gk<<<(unsigned)(2 * sms), 256, gsmem, s>>>(src, plan, g, ch, G, axs);
         FCFS_CHECK_LAUNCH("k_gsum_tc");
+        hk<<<(unsigned)(2 * sms), 256, gsmem, s>>>(src, plan, g, ch, H, axs);
+        FCFS_CHECK_LAUNCH("k_hsum_tc");
         kern<<<(unsigned)grid, tc::kThreads, smem, s>>>(src, plan, g, P_ws, e, nullptr, 0, shift, ch);
         FCFS_CHECK_LAUNCH("k_gemm_tf32");
     }
@@ -1048,3 +1166,15 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
 }
 
 }  // namespace fcfs
+
+// debug only (not in fcfs.h): copy the CTA-0 event trace of the last FCFS_DEBUG&256 run to the host
+extern "C" int64_t fcfs_debug_trace(unsigned long long *host, int64_t cap) {
+    unsigned int n = 0;
+    if (cudaMemcpyFromSymbol(&n, fcfs::tc::g_trace_n, sizeof(n)) != cudaSuccess) return -1;
+    int64_t m = n < (unsigned)fcfs::tc::kTraceMax ? n : fcfs::tc::kTraceMax;
+    if (m > cap) m = cap;
+    if (m > 0 && cudaMemcpyFromSymbol(host, fcfs::tc::g_trace, sizeof(unsigned long long) * m) != cudaSuccess) return -1;
+    const unsigned int z = 0;
+    cudaMemcpyToSymbol(fcfs::tc::g_trace_n, &z, sizeof(z));
+    return m;
+}

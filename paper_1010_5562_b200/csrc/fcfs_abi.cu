@@ -158,7 +158,8 @@ struct CoeffWs {
     double *P;
     int64_t *area;
     BucketWs bk;
-    double *G;   // FP64 single clip: x-side bucket sums of one chunk, [tiles_x][cb][64]
+    double *G;   // single clip: x-side bucket sums of one chunk, [tiles_x][cb][64 doubles or 128 tf32 rows]
+    double *H;   // single clip, split precisions: y-side row twiddles of the chunk, [tiles_y][cb][128 rows]
 };
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
@@ -177,12 +178,15 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
     w.G = nullptr;
+    w.H = nullptr;
     const bool bucketed = prec == FCFS_FP64 || single;
     if (bucketed) carve_buckets(cv, K, B, w.bk);
     if (bucketed && single) {
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
         const int64_t cb = fp64_chunk_buckets(K) > tc_chunk_buckets(K) ? fp64_chunk_buckets(K) : tc_chunk_buckets(K);
         w.G = cv.take<double>((size_t)p.tiles_x * cb * kTile);
+        // split precisions: the y-side row twiddles of the chunk as well (128 rows x 4 B per bucket)
+        if (prec != FCFS_FP64) w.H = cv.take<double>((size_t)p.tiles_y * cb * kTile);
     }
 }
 
@@ -382,8 +386,8 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
             st = tf32_supported(plan, T);
             if (st == FCFS_OK) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
             if (st == FCFS_OK)
-                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, W.P,
-                                              prec == FCFS_F16X3, s);
+                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, (uint8_t *)W.H,
+                                              W.P, prec == FCFS_F16X3, s);
         } else {
             st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
         }
