@@ -111,6 +111,13 @@ __device__ __forceinline__ void dmma16816(double (&d)[4], const double (&a)[8], 
 
 static constexpr int kLd = kTile + 4;   // padded smem row (doubles): conflict-free fragment loads
 
+// 16-byte asynchronous global -> shared copy (LDGSTS); src_size 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // kLoadA = false: A (x-side bucket sums) generated per slab; one launch covers the whole bucket range.
 // kLoadA = true: A read from G (k_gsum_fp64: the sums of one chunk of ch.cb buckets, computed once
 // instead of once per column tile); the items cover that chunk and ADD into P_ws (zeroed before
@@ -167,16 +174,19 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                 const int kk = gk + 8 * h;
                 const int64_t b = ks + kk;
                 double2 a = make_double2(0.0, 0.0), bv = make_double2(0.0, 0.0);
+                if (kLoadA) {   // x side: asynchronous copy of the precomputed sums (overlaps the DMMAs)
+                    const bool ok = b < kend;
+                    const double *gs = ok ? ch.G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile + 2 * gp : ch.G;
+                    cp_async16(&As[(buf * kBK + kk) * kLd + 2 * gp], gs, ok);
+                }
                 if (b < kend) {
-                    if (kLoadA) {
-                        a = __ldg((const double2 *)(ch.G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile) + gp);
-                    } else {
+                    if (!kLoadA) {
                         const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
                         a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
                     }
                     bv = side_pair(tiy * (kTile / 2) + gp, plan.Y, __ldg(src.by + b), 1.0, g, thi, tlo);
                 }
-                *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
+                if (!kLoadA) *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
                 *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = bv;
             }
         };
@@ -189,6 +199,7 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                 for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
             int buf = 0;
             generate(0, c0, c1);
+            if (kLoadA) cp_async_wait_all();
             __syncthreads();
             for (int64_t ks = c0; ks < c1; ks += kBK) {
                 if (ks + kBK < c1) generate(buf ^ 1, ks + kBK, c1);
@@ -204,6 +215,7 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                     for (int v = 0; v < 4; ++v) bf[v] = Bb[(lt + 4 * v) * kLd + wn + 8 * t + lg];
                     dmma16816(acc[t], a, bf);
                 }
+                if (kLoadA) cp_async_wait_all();   // the next slab's x-side copy has landed
                 __syncthreads();
                 buf ^= 1;
             }

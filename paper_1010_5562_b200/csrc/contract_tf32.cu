@@ -627,6 +627,16 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     const uint32_t my_ph = ph;
                     if (++slot == kS) { slot = 0; ph ^= 1; }
                     if ((int)(sc & 3) != gq) continue;
+                    // corner data 16 stages ahead -> L2 (the register prefetch below is only one own
+                    // stage = 4 stages ahead, about one HBM latency): one line per lane, per array
+                    if (!kLoadA && !(plan.dbg & 128)) {
+                        constexpr int kLines = kBKp * 4 / 128;          // 128-byte lines per array per stage
+                        const int64_t kp = ks + 16 * kBKp + (int64_t)(l % kLines) * 32;
+                        if (l < (yside ? 1 : 2) * kLines && kp < it.k1) {
+                            const int32_t *pa = (yside || l < kLines) ? vsrc : src.w;
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + kp));
+                        }
+                    }
                     int32_t v[kCq];
                     float wt[kCq];
 #pragma unroll
@@ -700,8 +710,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         const int two = (kPer == 2 && st + 1 < nst) ? 1 : 0;
                         const int s1 = (stage + 1 == kS) ? 0 : stage + 1;
                         const uint32_t p1 = (stage + 1 == kS) ? phase_bit ^ 1 : phase_bit;
-                        mbar_wait(FULL(stage), phase_bit);
-                        if (two) mbar_wait(FULL(s1), p1);
+                        mbar_wait(FULL(stage), phase_bit, plan.dbg & 64);
+                        if (two) mbar_wait(FULL(s1), p1, plan.dbg & 64);
                         if (lane == 0) trace(tr, 50, msc);
                         tc_fence_after();
                         const uint64_t off0 = (uint64_t)((stage * kStageBytes) >> 4);
