@@ -244,7 +244,11 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
 
 // x-side bucket sums of one chunk of ch.cb buckets of a single clip, for every x tile:
 // G[(tix * cb + b) * 64 + 2p + t] = sum_{k in bucket} w_k (cos, sin)(2 pi f_p x_k / T) (t = 0, 1), with the
-// axis pair (f = nf) carrying sum w_k x_k.  Persistent blocks over (slab of 16 buckets, x tile) units.
+// axis pair (f = nf) carrying sum w_k x_k.  Persistent blocks over (64 buckets, x tile) units; thread =
+// (bucket, block of 8 pairs): per corner two table lookups (E(f0 x) and the step E(x)) and the FP64
+// angle-addition recurrence over the 8 pairs (<= 7 steps, ~1 ulp each), i.e. a quarter of the
+// shared-memory lookups of one lookup per (corner, pair).
+static constexpr int kGsumBuckets = kThreads / 4;   // 64 buckets per unit
 __global__ void __launch_bounds__(kThreads)
 k_gsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__restrict__ G) {
     if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
@@ -253,23 +257,52 @@ k_gsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__r
     double2 *tlo = thi + g.nhi;
     build_tables(g, thi, tlo);
     __syncthreads();
-    const int gp = threadIdx.x & 31, gk = threadIdx.x >> 5;
+    const int kk = threadIdx.x >> 2, pb = threadIdx.x & 3;   // bucket in the unit, 8-pair block
     const int64_t cb0 = src.clip_bptr[0], cb1 = src.clip_bptr[1];
     const int64_t chunk0 = cb0 + ch.chunk * ch.cb;
     const int64_t chunk1 = chunk0 + ch.cb < cb1 ? chunk0 + ch.cb : cb1;
     if (chunk0 >= chunk1) return;
-    const int64_t nslab = (chunk1 - chunk0 + kBK - 1) / kBK;
-    const int64_t units = nslab * plan.tiles_x;
+    const int64_t nunit_b = (chunk1 - chunk0 + kGsumBuckets - 1) / kGsumBuckets;
+    const int64_t units = nunit_b * plan.tiles_x;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int tix = (int)(u % plan.tiles_x);
-        const int64_t slab = u / plan.tiles_x;
+        const int64_t b = chunk0 + (u / plan.tiles_x) * kGsumBuckets + kk;
+        if (b >= chunk1) continue;
+        const int p0 = tix * (kTile / 2) + 8 * pb;           // first pair (global) of the block
+        double re[8], im[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t b = chunk0 + slab * kBK + gk + 8 * h;
-            if (b >= chunk1) continue;
-            const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
-            const double2 a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
-            *((double2 *)(G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile) + gp) = a;
+        for (int i = 0; i < 8; ++i) { re[i] = 0.0; im[i] = 0.0; }
+        long long ax = 0;
+        const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+        const uint32_t f0 = (uint32_t)(plan.X.f0 + p0);
+        for (int c = cb; c < ce; ++c) {
+            const int32_t x = __ldg(src.x + c);
+            const int32_t wi = __ldg(src.w + c);
+            const double w = (double)wi;
+            ax += (long long)wi * (long long)x;
+            const double2 e0 = twiddle(phase_mod(f0, (uint32_t)x, g), g, thi, tlo);
+            const double2 e1 = twiddle(phase_mod(1u, (uint32_t)x, g), g, thi, tlo);
+            double cr = w * e0.x, ci = w * e0.y;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                re[i] += cr;
+                im[i] += ci;
+                if (i < 7) {
+                    const double nr = fma(cr, e1.x, -ci * e1.y);
+                    const double ni = fma(ci, e1.x, cr * e1.y);
+                    cr = nr;
+                    ci = ni;
+                }
+            }
+        }
+        double *out = G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile + 2 * 8 * pb;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int p = p0 + i;
+            double2 v = make_double2(0.0, 0.0);
+            if (p < plan.X.nf) v = make_double2(re[i], im[i]);
+            else if (p == plan.X.nf && plan.X.axis) v = make_double2((double)ax, 0.0);
+            *(double2 *)(out + 2 * i) = v;
         }
     }
 }
