@@ -26,7 +26,7 @@
 
 namespace fcfs {
 
-static constexpr int kBK = 16;        // row buckets per slab
+static constexpr int kBK = 32;        // row buckets per slab (two k16 DMMA steps per barrier)
 static constexpr int kChunk = 2048;   // buckets per register accumulator (<= kRowBucketCapFp64 corners each)
 static constexpr int kThreads = 256;  // 16 x 16 threads, 4x4 outputs each
 
@@ -170,7 +170,7 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
         // slab of kBK buckets [ks, ks + kBK) (zeros past kend): A = bucket sums, B = row twiddles
         auto generate = [&](int buf, int64_t ks, int64_t kend) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kBK / 8; ++h) {
                 const int kk = gk + 8 * h;
                 const int64_t b = ks + kk;
                 double2 a = make_double2(0.0, 0.0), bv = make_double2(0.0, 0.0);
@@ -203,17 +203,20 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
             __syncthreads();
             for (int64_t ks = c0; ks < c1; ks += kBK) {
                 if (ks + kBK < c1) generate(buf ^ 1, ks + kBK, c1);
-                const double *Ab = As + buf * kBK * kLd;
-                const double *Bb = Bs + buf * kBK * kLd;
-                double a[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = Ab[(lt + 4 * (j >> 1)) * kLd + wm + lg + 8 * (j & 1)];
+                for (int k16 = 0; k16 < kBK; k16 += 16) {
+                    const double *Ab = As + (buf * kBK + k16) * kLd;
+                    const double *Bb = Bs + (buf * kBK + k16) * kLd;
+                    double a[8];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    double bf[4];
+                    for (int j = 0; j < 8; ++j) a[j] = Ab[(lt + 4 * (j >> 1)) * kLd + wm + lg + 8 * (j & 1)];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) bf[v] = Bb[(lt + 4 * v) * kLd + wn + 8 * t + lg];
-                    dmma16816(acc[t], a, bf);
+                    for (int t = 0; t < 4; ++t) {
+                        double bf[4];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) bf[v] = Bb[(lt + 4 * v) * kLd + wn + 8 * t + lg];
+                        dmma16816(acc[t], a, bf);
+                    }
                 }
                 if (kLoadA) cp_async_wait_all();   // the next slab's x-side copy has landed
                 __syncthreads();
