@@ -156,13 +156,14 @@ struct FpChunk {
     const double *G;   // x-side bucket sums of the chunk, [tiles_x][cb][64]
     int64_t chunk;     // chunk index
     int64_t cb;        // buckets per chunk
+    const double *H;   // y-side row twiddles of the chunk, [tiles_y][cb][64]
 };
 static constexpr int64_t kFpChunkBuckets = 131072;
 int64_t fp64_chunk_buckets(int64_t K);
 fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
                              cudaStream_t s);
 fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, double *G,
-                                     double *P_ws, cudaStream_t s);
+                                     double *H, double *P_ws, cudaStream_t s);
 int64_t tc_chunk_buckets(int64_t K);
 fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, uint8_t *G,
                                      uint8_t *H, double *P_ws, bool f16, cudaStream_t s);

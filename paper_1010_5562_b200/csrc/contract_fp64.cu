@@ -179,15 +179,19 @@ k_gemm_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, double *__restrict__ P_
                     const double *gs = ok ? ch.G + ((int64_t)tix * ch.cb + (b - chunk0)) * kTile + 2 * gp : ch.G;
                     cp_async16(&As[(buf * kBK + kk) * kLd + 2 * gp], gs, ok);
                 }
-                if (b < kend) {
-                    if (!kLoadA) {
+                if (kLoadA) {   // y side: the precomputed row twiddles, likewise
+                    const bool ok = b < kend;
+                    const double *hs = ok ? ch.H + ((int64_t)tiy * ch.cb + (b - chunk0)) * kTile + 2 * gp : ch.H;
+                    cp_async16(&Bs[(buf * kBK + kk) * kLd + 2 * gp], hs, ok);
+                } else {
+                    if (b < kend) {
                         const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
                         a = bucket_pair(tix * (kTile / 2) + gp, plan.X, src.x, src.w, cb, ce, g, thi, tlo);
+                        bv = side_pair(tiy * (kTile / 2) + gp, plan.Y, __ldg(src.by + b), 1.0, g, thi, tlo);
                     }
-                    bv = side_pair(tiy * (kTile / 2) + gp, plan.Y, __ldg(src.by + b), 1.0, g, thi, tlo);
+                    *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
+                    *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = bv;
                 }
-                if (!kLoadA) *(double2 *)&As[(buf * kBK + kk) * kLd + 2 * gp] = a;
-                *(double2 *)&Bs[(buf * kBK + kk) * kLd + 2 * gp] = bv;
             }
         };
 
@@ -310,6 +314,48 @@ k_gsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__r
     }
 }
 
+// y-side row twiddles of one chunk for every y tile: H[(tiy * cb + b) * 64 + 2p + t] = (cos, sin)(2 pi n_p y_b / T),
+// the axis pair carrying y_b.  Same unit / thread mapping and recurrence as k_gsum_fp64, one row y per bucket.
+__global__ void __launch_bounds__(kThreads)
+k_hsum_fp64(CornerSrc src, GemmPlan plan, TwiddleGeom g, FpChunk ch, double *__restrict__ H) {
+    if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
+    extern __shared__ __align__(16) double smem_d[];
+    double2 *thi = (double2 *)smem_d;
+    double2 *tlo = thi + g.nhi;
+    build_tables(g, thi, tlo);
+    __syncthreads();
+    const int kk = threadIdx.x >> 2, pb = threadIdx.x & 3;
+    const int64_t cb0 = src.clip_bptr[0], cb1 = src.clip_bptr[1];
+    const int64_t chunk0 = cb0 + ch.chunk * ch.cb;
+    const int64_t chunk1 = chunk0 + ch.cb < cb1 ? chunk0 + ch.cb : cb1;
+    if (chunk0 >= chunk1) return;
+    const int64_t nunit_b = (chunk1 - chunk0 + kGsumBuckets - 1) / kGsumBuckets;
+    const int64_t units = nunit_b * plan.tiles_y;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tiy = (int)(u % plan.tiles_y);
+        const int64_t b = chunk0 + (u / plan.tiles_y) * kGsumBuckets + kk;
+        if (b >= chunk1) continue;
+        const int p0 = tiy * (kTile / 2) + 8 * pb;
+        const int32_t y = __ldg(src.by + b);
+        const double2 e0 = twiddle(phase_mod((uint32_t)(plan.Y.f0 + p0), (uint32_t)y, g), g, thi, tlo);
+        const double2 e1 = twiddle(phase_mod(1u, (uint32_t)y, g), g, thi, tlo);
+        double cr = e0.x, ci = e0.y;
+        double *out = H + ((int64_t)tiy * ch.cb + (b - chunk0)) * kTile + 2 * 8 * pb;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int p = p0 + i;
+            double2 v = make_double2(0.0, 0.0);
+            if (p < plan.Y.nf) v = make_double2(cr, ci);
+            else if (p == plan.Y.nf && plan.Y.axis) v = make_double2((double)y, 0.0);
+            *(double2 *)(out + 2 * i) = v;
+            const double nr = fma(cr, e1.x, -ci * e1.y);
+            const double ni = fma(ci, e1.x, cr * e1.y);
+            cr = nr;
+            ci = ni;
+        }
+    }
+}
+
 static size_t fp64_smem(const TwiddleGeom &g) {
     return sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits)) + sizeof(double) * 4 * kBK * kLd;
 }
@@ -324,7 +370,7 @@ fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t
         attr = true;
     }
     int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
-    k_gemm_fp64<false><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, FpChunk{nullptr, 0, 0});
+    k_gemm_fp64<false><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, FpChunk{nullptr, 0, 0, nullptr});
     FCFS_CHECK_LAUNCH("k_gemm_fp64");
     return FCFS_OK;
 }
@@ -337,13 +383,14 @@ int64_t fp64_chunk_buckets(int64_t K) {
 
 // single clip, chunked: G of each chunk once (k_gsum_fp64), then the DMMA GEMM reading it (P_ws +=)
 fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan, int32_t T, int64_t K, double *G,
-                                     double *P_ws, cudaStream_t s) {
+                                     double *H, double *P_ws, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     TwiddleGeom g = make_twiddle_geom(T);
     static bool attr = false;
     if (!attr) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gsum_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_hsum_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         attr = true;
     }
     FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
@@ -352,9 +399,11 @@ fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan,
     const size_t tsm = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits));
     int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
     for (int64_t c = 0; c < nchunk; ++c) {
-        const FpChunk ch{G, c, cb};
+        const FpChunk ch{G, c, cb, H};
         k_gsum_fp64<<<148 * 4, kThreads, tsm, s>>>(src, plan, g, ch, G);
         FCFS_CHECK_LAUNCH("k_gsum_fp64");
+        k_hsum_fp64<<<148 * 4, kThreads, tsm, s>>>(src, plan, g, ch, H);
+        FCFS_CHECK_LAUNCH("k_hsum_fp64");
         k_gemm_fp64<true><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, ch);
         FCFS_CHECK_LAUNCH("k_gemm_fp64");
     }

@@ -185,8 +185,8 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
         const int64_t cb = fp64_chunk_buckets(K) > tc_chunk_buckets(K) ? fp64_chunk_buckets(K) : tc_chunk_buckets(K);
         w.G = cv.take<double>((size_t)p.tiles_x * cb * kTile);
-        // split precisions: the y-side row twiddles of the chunk as well (128 rows x 4 B per bucket)
-        if (prec != FCFS_FP64) w.H = cv.take<double>((size_t)p.tiles_y * cb * kTile);
+        // the y-side row twiddles of the chunk as well (64 doubles or 128 tf32 rows x 4 B per bucket)
+        w.H = cv.take<double>((size_t)p.tiles_y * cb * kTile);
     }
 }
 
@@ -380,7 +380,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
         if (prec == FCFS_FP64) {
             // one clip: x-side bucket sums once per chunk, then the DMMA GEMM over them
             st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
-            if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.P, s);
+            if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.H, W.P, s);
         } else if (prec == FCFS_TF32X3 || prec == FCFS_F16X3) {
             // the same chunked row-bucket scheme on the tcgen05 tensor cores
             st = tf32_supported(plan, T);
