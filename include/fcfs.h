@@ -119,9 +119,11 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
  * x, y, w  int32 [K] corners (device) as produced by fcfs_vertices_from_rects (any order
  *          is accepted; results are order-independent up to rounding).
  * area     sum_k w_k x_k y_k (host value), used for F[0,0] = area/T^2.
- * win      host struct, see fcfs_window.   prec  FCFS_FP64 or FCFS_TF32X3.
+ * win      host struct, see fcfs_window.   prec  FCFS_FP64, FCFS_TF32X3 or FCFS_F16X3.
  * shard    host struct or NULL (= FCFS_SHARD_NONE).
- * F        out (device): complex128 (FP64) or complex64 (TF32X3) in the window layout.
+ * F        out (device): complex128 (FP64) or complex64 (TF32X3 / F16X3) in the window layout.
+ * The corners are contracted over their row buckets (fcfs_row_buckets, cap 32), in chunks of
+ * buckets sized to stay in L2; the call synchronises `stream` once to read the bucket count.
  * ------------------------------------------------------------------------------------------ */
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
                                    fcfs_precision prec, const fcfs_shard *shard);

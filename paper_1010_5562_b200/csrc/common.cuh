@@ -159,6 +159,15 @@ struct FpChunk {
     const double *H;   // y-side row twiddles of the chunk, [tiles_y][cb][64]
 };
 static constexpr int64_t kFpChunkBuckets = 131072;
+// Buckets per chunk of the single-clip paths (the chunk's x- and y-side tiles live in the workspace,
+// 512 B per bucket per tile): large chunks, since every chunk re-reads and re-writes the P partials
+// (measured: L2-sized chunks of ~4K buckets were slower on configs[3] / [4]); a multiple of 64.
+inline int64_t chunk_buckets(int64_t K, int tiles_x, int tiles_y) {
+    (void)tiles_x; (void)tiles_y;
+    int64_t cb = (K + 63) / 64 * 64;
+    if (cb > kFpChunkBuckets) cb = kFpChunkBuckets;
+    return cb < 64 ? 64 : cb;
+}
 int64_t fp64_chunk_buckets(int64_t K);
 fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
                              cudaStream_t s);

@@ -394,8 +394,8 @@ fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan,
         attr = true;
     }
     FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
-    const int64_t cb = fp64_chunk_buckets(K);
-    const int64_t nchunk = K > 0 ? (K + cb - 1) / cb : 0;   // buckets <= corners: an upper bound
+    const int64_t cb = chunk_buckets(K, plan.tiles_x, plan.tiles_y);
+    const int64_t nchunk = K > 0 ? (K + cb - 1) / cb : 0;   // K = the clip's bucket count here
     const size_t tsm = sizeof(double2) * (size_t)(g.nhi + (1 << g.lbits));
     int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
     for (int64_t c = 0; c < nchunk; ++c) {

@@ -1152,8 +1152,8 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = plan.items < sms ? plan.items : sms;
-    const int64_t cb = tc_chunk_buckets(K);
-    const int64_t nchunk = (K + cb - 1) / cb;   // buckets <= corners: an upper bound
+    const int64_t cb = chunk_buckets(K, plan.tiles_x, plan.tiles_y);
+    const int64_t nchunk = (K + cb - 1) / cb;   // K = the clip's bucket count here
     EpiArgs e{};
     // fp16 range: the axis slots carry sums of <= kRowBucketCapFp64 coordinate weights (<= T |w|),
     // scaled by 2^-shift so that 32 (T + 1) 2^-shift <= 2048

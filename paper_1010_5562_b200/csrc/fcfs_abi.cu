@@ -171,6 +171,16 @@ static bool fusable(const GemmPlan &p, fcfs_precision prec, int32_t M, int32_t m
     return (prec == FCFS_TF32X3 || prec == FCFS_F16X3) && tf32_can_fuse(p, ea);
 }
 
+// number of row buckets of a single range (the chunk loop of the single-clip paths runs on the
+// host): one stream synchronisation
+static fcfs_status bucket_count_host(const BucketWs &bk, int64_t &nb, cudaStream_t s) {
+    int64_t h[2] = {0, 0};
+    FCFS_TRY_CUDA(cudaMemcpyAsync(h, bk.clip_bptr, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    nb = h[1] - h[0];
+    return FCFS_OK;
+}
+
 // the row buckets (buckets.cu) feed the FP64 contraction; the tcgen05 kernels walk corners
 static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, int64_t K, int64_t B,
                         fcfs_precision prec, bool single = false) {
@@ -183,7 +193,7 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     if (bucketed) carve_buckets(cv, K, B, w.bk);
     if (bucketed && single) {
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
-        const int64_t cb = fp64_chunk_buckets(K) > tc_chunk_buckets(K) ? fp64_chunk_buckets(K) : tc_chunk_buckets(K);
+        const int64_t cb = chunk_buckets(K, p.tiles_x, p.tiles_y);
         w.G = cv.take<double>((size_t)p.tiles_x * cb * kTile);
         // the y-side row twiddles of the chunk as well (64 doubles or 128 tf32 rows x 4 B per bucket)
         w.H = cv.take<double>((size_t)p.tiles_y * cb * kTile);
@@ -380,14 +390,18 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
         if (prec == FCFS_FP64) {
             // one clip: x-side bucket sums once per chunk, then the DMMA GEMM over them
             st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
-            if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, src.k_hi - src.k_lo, W.G, W.H, W.P, s);
+            int64_t nb = 0;
+            if (st == FCFS_OK) st = bucket_count_host(W.bk, nb, s);
+            if (st == FCFS_OK) st = launch_gemm_fp64_chunked(src, plan, T, nb, W.G, W.H, W.P, s);
         } else if (prec == FCFS_TF32X3 || prec == FCFS_F16X3) {
             // the same chunked row-bucket scheme on the tcgen05 tensor cores
             st = tf32_supported(plan, T);
             if (st == FCFS_OK) st = run_buckets(y, nullptr, 1, src.k_lo, src.k_hi, kRowBucketCapFp64, W.bk, s);
+            int64_t nb = 0;
+            if (st == FCFS_OK) st = bucket_count_host(W.bk, nb, s);
             if (st == FCFS_OK)
-                st = launch_gemm_tf32_chunked(src, plan, T, src.k_hi - src.k_lo, (uint8_t *)W.G, (uint8_t *)W.H,
-                                              W.P, prec == FCFS_F16X3, s);
+                st = launch_gemm_tf32_chunked(src, plan, T, nb, (uint8_t *)W.G, (uint8_t *)W.H, W.P, prec == FCFS_F16X3,
+                                              s);
         } else {
             st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
         }
