@@ -888,22 +888,21 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 }
 
 // x-side bucket sums of one chunk for every x tile, split hi/lo and stored in the exact SW128
-// K-major stage layout of k_gemm_tf32<., 0, true> (16 KB per (x tile, 32-bucket stage)):
-// G[f, b] = sum_{k in bucket b} w_k E(f x_k) (one exact-phase table lookup per (corner, pair),
-// FP32 sums of <= 32 terms); the axis pair carries sum_k w_k x_k.  A block builds one 16 KB tile
-// in shared memory (warp w: buckets 4w .. 4w+3, lane: pair slot) and writes it out coalesced.
-// kF16: the fp16 hi/lo layout of k_gemm_tf32<., 1, true> (64 buckets per 128-byte row, 2 B per
-// element; the axis pair scaled by axs = 2^-axis_shift to stay in fp16 range)
+// K-major stage layout of k_gemm_tf32<., kF16, true> (16 KB per (x tile, stage of 32 / 64 buckets)):
+// G[f, b] = sum_{k in bucket b} w_k E(f x_k); the axis pair carries sum_k w_k x_k (x axs for fp16).
+// A block builds the tiles of 64 buckets of one x tile in shared memory and writes them out
+// coalesced; thread = (bucket, block of 8 pairs): per corner two exact-phase table lookups (E(f0 x),
+// step E(x)) and the angle-addition recurrence over the 8 pairs, FP32 sums of <= 32 terms.
 template <bool kFast, int kF16>
 __global__ void __launch_bounds__(256)
 k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restrict__ G, float axs) {
-    constexpr int kBKp = kF16 ? 2 * kBK : kBK;   // buckets per stage
-    constexpr int kPerWarp = kBKp / 8;           // buckets per warp
     if (src.clip_bptr[0] + ch.chunk * ch.cb >= src.clip_bptr[1]) return;   // chunk past the buckets
+    constexpr int kBKp = kF16 ? 2 * kBK : kBK;   // buckets per stage tile
+    constexpr int kTiles = 64 / kBKp;            // stage tiles per 64-bucket unit (tf32: 2, fp16: 1)
     extern __shared__ __align__(1024) uint8_t gsm_raw[];
     uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
-    uint8_t *tile = sm;
-    float2 *tab = (float2 *)(sm + kOpBytes);
+    uint8_t *tile = sm;                                       // kTiles x 16 KB
+    float2 *tab = (float2 *)(sm + 2 * kOpBytes);
     const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
     for (int i = threadIdx.x; i < tab_entries; i += blockDim.x) {
         double sn, cs;
@@ -913,70 +912,77 @@ k_gsum_tc(CornerSrc src, GemmPlan plan, TabGeom g, TcChunk ch, uint8_t *__restri
         tab[i] = make_float2((float)cs, (float)sn);
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kk = threadIdx.x >> 2, pb = threadIdx.x & 3;   // bucket of the unit, 8-pair block
     const int64_t chunk0 = src.clip_bptr[0] + ch.chunk * ch.cb;
     int64_t ke = src.clip_bptr[1];
     if (ke > chunk0 + ch.cb) ke = chunk0 + ch.cb;
     if (chunk0 >= ke) return;
-    const int64_t nst = (ke - chunk0 + kBKp - 1) / kBKp, nst_chunk = ch.cb / kBKp;
+    const int64_t nunit = (ke - chunk0 + 63) / 64, nst_chunk = ch.cb / kBKp;
     const uint32_t M13 = 0xFFFFE000u;
-    for (int64_t u = blockIdx.x; u < nst * plan.tiles_x; u += gridDim.x) {
+    for (int64_t u = blockIdx.x; u < nunit * plan.tiles_x; u += gridDim.x) {
         const int tix = (int)(u % plan.tiles_x);
-        const int64_t st = u / plan.tiles_x;
-        const int pg = tix * 32 + lane;
-        const uint32_t f = (uint32_t)(plan.X.f0 + pg);
-        const bool tw = pg < plan.X.nf, axis = plan.X.axis && pg == plan.X.nf;
-        // the 4 buckets' corners (<= 32 each) in one coalesced load per bucket: lane j holds corner
-        // cb + j; the sum loop broadcasts them with shuffles (no dependent global load per corner)
-        int cbq[kPerWarp], cnq[kPerWarp];
-        int32_t xq[kPerWarp], wq[kPerWarp];
+        const int64_t unit = u / plan.tiles_x;
+        const int64_t b = chunk0 + unit * 64 + kk;
+        const int p0 = tix * 32 + 8 * pb;                     // first pair (global) of the block
+        const uint32_t f0 = (uint32_t)(plan.X.f0 + p0);
+        float re[8], im[8];
 #pragma unroll
-        for (int q = 0; q < kPerWarp; ++q) {
-            const int64_t b = chunk0 + st * kBKp + kPerWarp * warp + q;
-            cbq[q] = 0;
-            cnq[q] = 0;
-            if (b < ke) { cbq[q] = __ldg(src.bptr + b); cnq[q] = __ldg(src.bptr + b + 1) - cbq[q]; }
-            xq[q] = lane < cnq[q] ? __ldg(src.x + cbq[q] + lane) : 0;
-            wq[q] = lane < cnq[q] ? __ldg(src.w + cbq[q] + lane) : 0;
-        }
+        for (int i = 0; i < 8; ++i) { re[i] = 0.f; im[i] = 0.f; }
+        float ax = 0.f;
+        if (b < ke) {
+            const int cb = __ldg(src.bptr + b), ce = __ldg(src.bptr + b + 1);
+            for (int c = cb; c < ce; ++c) {
+                const int32_t x = __ldg(src.x + c);
+                const float wt = (float)__ldg(src.w + c);
+                ax = fmaf(wt, (float)x, ax);
+                const float2 a = twiddle<kFast>(phase<kFast>(f0, (uint32_t)x, g), g, tab);
+                const float2 e = twiddle<kFast>(phase<kFast>(1u, (uint32_t)x, g), g, tab);
+                float cr = wt * a.x, ci = wt * a.y;
 #pragma unroll
-        for (int q = 0; q < kPerWarp; ++q) {
-            const int kk = kPerWarp * warp + q;
-            float re = 0.f, im = 0.f;
-            {
-                for (int j = 0; j < cnq[q]; ++j) {
-                    const int32_t x = __shfl_sync(0xffffffffu, xq[q], j);
-                    const float wt = (float)__shfl_sync(0xffffffffu, wq[q], j);
-                    if (tw) {
-                        const float2 e = twiddle<kFast>(phase<kFast>(f, (uint32_t)x, g), g, tab);
-                        re = fmaf(wt, e.x, re);
-                        im = fmaf(wt, e.y, im);
-                    } else if (axis) {
-                        re = fmaf(wt, (float)x, re);
+                for (int i = 0; i < 8; ++i) {
+                    re[i] += cr;
+                    im[i] += ci;
+                    if (i < 7) {
+                        const float nr = fmaf(cr, e.x, -ci * e.y);
+                        const float ni = fmaf(ci, e.x, cr * e.y);
+                        cr = nr;
+                        ci = ni;
                     }
                 }
             }
-            if (kF16 && axis) re *= axs;
-            const float hr = __uint_as_float(__float_as_uint(re) & M13), hs = __uint_as_float(__float_as_uint(im) & M13);
-            const int r7 = lane & 7;
+        }
+        uint8_t *tl = tile + (kk / kBKp) * kOpBytes;          // stage tile of this bucket
+        const int kq = kk % kBKp;                             // K position inside the tile
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int p = p0 + i, r = 8 * pb + i, r7 = r & 7;
+            float vr = 0.f, vi = 0.f;
+            if (p < plan.X.nf) { vr = re[i]; vi = im[i]; }
+            else if (plan.X.axis && p == plan.X.nf) vr = ax * (kF16 ? axs : 1.f);
+            const float hr = __uint_as_float(__float_as_uint(vr) & M13), hs = __uint_as_float(__float_as_uint(vi) & M13);
             if constexpr (!kF16) {
-                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 2) ^ r7)) << 4) + ((kk & 3) << 2);
-                *(float *)(base) = re;                       // cos hi row (the MMA reads the top 19 bits)
-                *(float *)(base + 4 * 1024) = im;            // sin hi
-                *(float *)(base + 8 * 1024) = re - hr;       // cos lo
-                *(float *)(base + 12 * 1024) = im - hs;      // sin lo
-            } else {                                         // hi: 11 significant bits, exact in fp16
-                uint8_t *base = tile + (lane >> 3) * 1024 + r7 * kRowBytes + ((((kk >> 3) ^ r7)) << 4) + ((kk & 7) << 1);
+                uint8_t *base = tl + (r >> 3) * 1024 + r7 * kRowBytes + ((((kq >> 2) ^ r7)) << 4) + ((kq & 3) << 2);
+                *(float *)(base) = vr;                        // cos hi row (the MMA reads the top 19 bits)
+                *(float *)(base + 4 * 1024) = vi;             // sin hi
+                *(float *)(base + 8 * 1024) = vr - hr;        // cos lo
+                *(float *)(base + 12 * 1024) = vi - hs;       // sin lo
+            } else {                                          // hi: 11 significant bits, exact in fp16
+                uint8_t *base = tl + (r >> 3) * 1024 + r7 * kRowBytes + ((((kq >> 3) ^ r7)) << 4) + ((kq & 7) << 1);
                 *(__half *)(base) = __float2half_rn(hr);
                 *(__half *)(base + 4 * 1024) = __float2half_rn(hs);
-                *(__half *)(base + 8 * 1024) = __float2half_rn(re - hr);
-                *(__half *)(base + 12 * 1024) = __float2half_rn(im - hs);
+                *(__half *)(base + 8 * 1024) = __float2half_rn(vr - hr);
+                *(__half *)(base + 12 * 1024) = __float2half_rn(vi - hs);
             }
         }
         __syncthreads();
-        uint4 *dst = (uint4 *)(G + ((int64_t)tix * nst_chunk + st) * kOpBytes);
-        const uint4 *srct = (const uint4 *)tile;
-        for (int i = threadIdx.x; i < kOpBytes / 16; i += blockDim.x) dst[i] = srct[i];
+#pragma unroll
+        for (int t = 0; t < kTiles; ++t) {
+            const int64_t st = unit * kTiles + t;             // stage index within the chunk
+            if (st * kBKp >= ke - chunk0) break;
+            uint4 *dst = (uint4 *)(G + ((int64_t)tix * nst_chunk + st) * kOpBytes);
+            const uint4 *srct = (const uint4 *)(tile + t * kOpBytes);
+            for (int i = threadIdx.x; i < kOpBytes / 16; i += blockDim.x) dst[i] = srct[i];
+        }
         __syncthreads();
     }
 }
@@ -1132,7 +1138,7 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
     const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
     const tc::Smem L = tc::smem_layout(entries, tc::kStagesLoadA, false);
     const size_t smem = L.total + 1024;
-    const size_t gsmem = tc::kOpBytes + 1024 + (size_t)entries * 8;
+    const size_t gsmem = 2 * tc::kOpBytes + 1024 + (size_t)entries * 8;
     const bool fast = g.single && g.pow2;
     auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1, true> : tc::k_gemm_tf32<false, 1, true>)
                     : (fast ? tc::k_gemm_tf32<true, 0, true> : tc::k_gemm_tf32<false, 0, true>);
