@@ -411,7 +411,7 @@ static constexpr int kBucketRectsPerThread = 4;   // kClipRects / kBucketThreads
 static constexpr int kBucketMaxT = 8191;
 static constexpr int kBucketCap = 4 * kClipRects;
 
-__global__ void __launch_bounds__(kBucketThreads)
+__global__ void __launch_bounds__(kBucketThreads, 3)
 k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
                       int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
                       unsigned long long *status, int64_t *area, int32_t *err) {
@@ -589,6 +589,8 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
         if (!battr) {
             FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                kBucketCap * 12 + (kBucketMaxT + 2) * 4));
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               100));
             battr = true;
         }
         k_clip_corners_bucket<<<(unsigned)grid, kBucketThreads, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T,
