@@ -47,6 +47,8 @@ def _load():
         i64, i32 = ctypes.c_int64, ctypes.c_int32
         lib.oracle_extract.argtypes = [P, i64, P, i64, P, i64, i32, P, P, P, i64, P, P, P]
         lib.oracle_extract.restype = ctypes.c_int
+        lib.oracle_extract_polygons.argtypes = [P, P, P, i64, P, i64, i32, P, P, P, i64, P, P, P]
+        lib.oracle_extract_polygons.restype = ctypes.c_int
         lib.oracle_coeffs.argtypes = [P, P, P, i64, i64, i32, P, P, i64, P, P, P, ctypes.c_int]
         lib.oracle_coeffs.restype = ctypes.c_int
         lib.oracle_window.argtypes = [i32, i32, ctypes.c_double, P, P, i64]
@@ -101,6 +103,40 @@ def extract(rects, T, group_ptr=None, clip_ptr=None):
                             _ptr(x), _ptr(y), _ptr(w), cap, _ptr(cptr), _ptr(area), ctypes.byref(K))
     if rc != OR_OK:
         raise OracleError(f"oracle_extract failed rc={rc}")
+    return dict(x=x[:cap], y=y[:cap], w=w[:cap], corner_ptr=cptr, area=area, K=cap)
+
+
+def extract_polygons(vx, vy, poly_ptr, T, clip_ptr=None):
+    """Signed corners of f = sum of the polygons' indicators per clip (Alg. 2 on vertex lists).
+
+    vx, vy: int32 [V] vertices; poly_ptr: int64 [P+1] CSR over vertices (closed polygons, either
+    orientation); clip_ptr: int64 [B+1] over polygons or None (one clip).
+    Returns dict(x, y, w (int32), corner_ptr (int64 [B+1]), area (int64 [B]), K).
+    """
+    lib = _load()
+    vx = np.ascontiguousarray(vx, dtype=np.int32)
+    vy = np.ascontiguousarray(vy, dtype=np.int32)
+    poly_ptr = np.ascontiguousarray(poly_ptr, dtype=np.int64)
+    P = poly_ptr.shape[0] - 1
+    if clip_ptr is not None:
+        clip_ptr = np.ascontiguousarray(clip_ptr, dtype=np.int64)
+        B = clip_ptr.shape[0] - 1
+    else:
+        B = 1
+    cptr = np.zeros(B + 1, np.int64)
+    area = np.zeros(B, np.int64)
+    K = ctypes.c_int64(0)
+    args = (_ptr(vx), _ptr(vy), _ptr(poly_ptr), P, _ptr(clip_ptr), B, int(T))
+    rc = lib.oracle_extract_polygons(*args, None, None, None, 0, _ptr(cptr), _ptr(area), ctypes.byref(K))
+    if rc not in (OR_OK, OR_E_CAPACITY):
+        raise OracleError(f"oracle_extract_polygons failed rc={rc}")
+    cap = K.value
+    x = np.zeros(max(cap, 1), np.int32)
+    y = np.zeros(max(cap, 1), np.int32)
+    w = np.zeros(max(cap, 1), np.int32)
+    rc = lib.oracle_extract_polygons(*args, _ptr(x), _ptr(y), _ptr(w), cap, _ptr(cptr), _ptr(area), ctypes.byref(K))
+    if rc != OR_OK:
+        raise OracleError(f"oracle_extract_polygons failed rc={rc}")
     return dict(x=x[:cap], y=y[:cap], w=w[:cap], corner_ptr=cptr, area=area, K=cap)
 
 

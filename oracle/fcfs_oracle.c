@@ -39,7 +39,10 @@
  * equal keys and drop zeros.  The area is computed twice (sum w x y and sum of
  * covered compressed-cell areas) and the two must agree.
  *
- * Parity is pinned in tests/test_oracle_pins.py (P1..P12 of DESIGN.md).
+ * Polygon vertex lists (oracle_extract_polygons): Alg. 2 lines 9-10 on every horizontal edge of
+ * the clockwise list (+1 end, -1 start), counter-clockwise lists reversed, polygons summed.
+ *
+ * Parity is pinned in tests/test_oracle_pins.py (P1..P12 and E1..E8 of DESIGN.md).
  */
 #include <math.h>
 #include <stdint.h>
@@ -194,6 +197,115 @@ int oracle_extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, in
     }
     *K_out = K;
     free(cand); free(area_cells); free(area_w);
+    if (rc != OR_OK) return rc;
+    return K > cap ? OR_E_CAPACITY : OR_OK;
+}
+
+/*
+ * Extraction from polygon vertex lists (the paper's own input, Alg. 2 REQUIRE and lines 1-14,
+ * P:930-950).  vx, vy: int32[V] vertices; poly_ptr: int64[P+1] CSR over vertices; every polygon is
+ * closed (edge i runs from vertex i to vertex (i+1) mod n); clip_ptr: int64[B+1] CSR over polygons
+ * or NULL (one clip).  Every edge is horizontal or vertical with non-zero length (else
+ * OR_E_INVALID) and every vertex lies in [0,T]^2 (else OR_E_RANGE).
+ *
+ * Step by step, per polygon:
+ *   1. orientation: A = sum over horizontal edges a->b of y_a (x_b - x_a) (the vertex form of
+ *      Eq. Fdc) is the area, > 0 for a clockwise (y up) list ("which we
+ *      arbitrarily choose to be clockwise").  A list with A < 0 is the counter-clockwise list of
+ *      the same polygon: it is REVERSED first (reading A17 of DESIGN.md);
+ *   2. Alg. 2 lines 9-10 / Step 4: every horizontal edge a->b of the
+ *      clockwise list puts +1 at its end (x_b, y_a) and -1 at its start (x_a, y_a).  The loop runs
+ *      over EVERY edge and tests it, so lists need not start with a horizontal edge and may hold
+ *      collinear vertices (their +1 / -1 cancel);
+ * then the entries of all polygons of a clip are SUMMED (the signal model f = sum of indicator
+ * functions), sorted by (clip, y, x), equal keys merged, zeros dropped.
+ * Self-check: sum_k w_k x_k y_k == sum over the clip's polygons of |A| (exact, __int128).
+ */
+int oracle_extract_polygons(const int32_t *vx, const int32_t *vy, const int64_t *poly_ptr, int64_t P,
+                            const int64_t *clip_ptr, int64_t B, int32_t T,
+                            int32_t *x, int32_t *y, int32_t *w, int64_t cap,
+                            int64_t *corner_ptr, int64_t *area, int64_t *K_out) {
+    if (T <= 0 || P < 0 || B < 1 || poly_ptr == NULL || K_out == NULL || corner_ptr == NULL || area == NULL)
+        return OR_E_INVALID;
+    if (clip_ptr == NULL && B != 1) return OR_E_INVALID;
+    const int64_t V = poly_ptr[P];
+    if (poly_ptr[0] != 0) return OR_E_INVALID;
+    for (int64_t p = 0; p < P; ++p)
+        if (poly_ptr[p + 1] < poly_ptr[p]) return OR_E_INVALID;
+    for (int64_t v = 0; v < V; ++v)
+        if (vx[v] < 0 || vy[v] < 0 || vx[v] > T || vy[v] > T) return OR_E_RANGE;
+    or_corner *cand = (or_corner *)malloc(sizeof(or_corner) * (size_t)(2 * V > 0 ? 2 * V : 1));
+    __int128 *area_poly = (__int128 *)calloc((size_t)B, sizeof(__int128));
+    int64_t *px = (int64_t *)malloc(sizeof(int64_t) * (size_t)(V > 0 ? V : 1));
+    int64_t *py = (int64_t *)malloc(sizeof(int64_t) * (size_t)(V > 0 ? V : 1));
+    if (!cand || !area_poly || !px || !py) { free(cand); free(area_poly); free(px); free(py); return OR_E_NOMEM; }
+    int64_t nc = 0;
+    int rc = OR_OK;
+    for (int64_t b = 0; b < B && rc == OR_OK; ++b) {
+        int64_t p0 = clip_ptr ? clip_ptr[b] : 0, p1 = clip_ptr ? clip_ptr[b + 1] : P;
+        if (p0 < 0 || p1 < p0 || p1 > P) { rc = OR_E_INVALID; break; }
+        for (int64_t p = p0; p < p1; ++p) {
+            const int64_t v0 = poly_ptr[p], n = poly_ptr[p + 1] - v0;
+            if (n == 0) continue;
+            for (int64_t i = 0; i < n; ++i) { px[i] = vx[v0 + i]; py[i] = vy[v0 + i]; }
+            /* edges: horizontal or vertical, non-zero */
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t j = (i + 1) % n;
+                const int hor = py[i] == py[j] && px[i] != px[j];
+                const int ver = px[i] == px[j] && py[i] != py[j];
+                if (!hor && !ver) rc = OR_E_INVALID;
+            }
+            if (rc != OR_OK) break;
+            /* 1. orientation */
+            __int128 A = 0;
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t j = (i + 1) % n;
+                if (py[i] == py[j]) A += (__int128)py[i] * (px[j] - px[i]);
+            }
+            if (A < 0) {   /* counter-clockwise: reverse the list */
+                for (int64_t i = 0, j = n - 1; i < j; ++i, --j) {
+                    int64_t t = px[i]; px[i] = px[j]; px[j] = t;
+                    t = py[i]; py[i] = py[j]; py[j] = t;
+                }
+                A = -A;
+            }
+            area_poly[b] += A;
+            /* 2. +1 at the end, -1 at the start of every horizontal edge */
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t j = (i + 1) % n;
+                if (py[i] != py[j]) continue;
+                cand[nc].clip = b; cand[nc].y = py[i]; cand[nc].x = px[j]; cand[nc].w = +1; ++nc;
+                cand[nc].clip = b; cand[nc].y = py[i]; cand[nc].x = px[i]; cand[nc].w = -1; ++nc;
+            }
+        }
+    }
+    free(px); free(py);
+    if (rc != OR_OK) { free(cand); free(area_poly); return rc; }
+    qsort(cand, (size_t)nc, sizeof(or_corner), cmp_corner);
+    int64_t K = 0;
+    for (int64_t b = 0; b <= B; ++b) corner_ptr[b] = 0;
+    __int128 *area_w = (__int128 *)calloc((size_t)B, sizeof(__int128));
+    int64_t i = 0;
+    while (i < nc) {
+        int64_t j = i, s = 0;
+        while (j < nc && cand[j].clip == cand[i].clip && cand[j].y == cand[i].y && cand[j].x == cand[i].x) s += cand[j++].w;
+        if (s != 0) {
+            if (K < cap && x && y && w) {
+                x[K] = (int32_t)cand[i].x; y[K] = (int32_t)cand[i].y; w[K] = (int32_t)s;
+            }
+            corner_ptr[cand[i].clip + 1] += 1;
+            area_w[cand[i].clip] += (__int128)s * cand[i].x * cand[i].y;
+            ++K;
+        }
+        i = j;
+    }
+    for (int64_t b = 0; b < B; ++b) corner_ptr[b + 1] += corner_ptr[b];
+    for (int64_t b = 0; b < B; ++b) {
+        if (area_w[b] != area_poly[b]) rc = OR_E_SELFCHECK;
+        area[b] = (int64_t)area_w[b];
+    }
+    *K_out = K;
+    free(cand); free(area_poly); free(area_w);
     if (rc != OR_OK) return rc;
     return K > cap ? OR_E_CAPACITY : OR_OK;
 }

@@ -177,6 +177,110 @@ def c5(seed: int = 0, T: int = 262_144, n_rects: int = 1_000_000, M: int = 1024)
     return Workload("c5", T, M, M, -1.0, np.concatenate([lines, rest]), None, None, ("fp64", "tf32x3"))
 
 
+# ------------------------------------------------------------------ polygon vertex lists
+
+@dataclasses.dataclass
+class PolygonSet:
+    """Closed rectilinear polygons as vertex lists (the paper's input, Alg. 2 REQUIRE P:930-935).
+
+    vx, vy    int32 [V] vertices; poly_ptr int64 [P+1] CSR over vertices;
+    clip_ptr  int64 [B+1] CSR over polygons, or None (= one clip).
+    """
+    T: int
+    vx: np.ndarray
+    vy: np.ndarray
+    poly_ptr: np.ndarray
+    clip_ptr: np.ndarray | None
+
+    @property
+    def B(self) -> int:
+        return 1 if self.clip_ptr is None else int(self.clip_ptr.shape[0] - 1)
+
+    @property
+    def P(self) -> int:
+        return int(self.poly_ptr.shape[0] - 1)
+
+
+def _pack(polys, T, per_clip=None) -> PolygonSet:
+    sizes = np.array([len(p) for p in polys], np.int64)
+    pp = np.zeros(len(polys) + 1, np.int64)
+    pp[1:] = np.cumsum(sizes)
+    V = np.concatenate([np.asarray(p, np.int64).reshape(-1, 2) for p in polys]) if polys else np.zeros((0, 2), np.int64)
+    cp = None
+    if per_clip is not None:
+        cp = np.zeros(len(per_clip) + 1, np.int64)
+        cp[1:] = np.cumsum(per_clip)
+    return PolygonSet(T, V[:, 0].astype(np.int32), V[:, 1].astype(np.int32), pp, cp)
+
+
+def skyline_polygon(rng, T, max_cols=6, size=None, collinear=0.0):
+    """A random simple rectilinear polygon as a vertex list: a 'skyline' of 1..max_cols columns
+    (widths / heights U{1..size}), in a random one of the 8 axis symmetries, placed at random inside
+    [0,T]^2, listed in a random orientation from a random start vertex; with probability
+    `collinear` per edge an extra vertex splits it (collinear vertices).  Pure vertex drawing."""
+    size = size or max(1, T // (2 * max_cols))
+    k = int(rng.integers(1, max_cols + 1))
+    ws = rng.integers(1, size + 1, k)
+    hs = rng.integers(1, size + 1, k)
+    xs = np.concatenate([[0], np.cumsum(ws)])
+    v = [(0, 0), (0, int(hs[0]))]
+    for i in range(k):
+        v.append((int(xs[i + 1]), int(hs[i])))
+        v.append((int(xs[i + 1]), int(hs[i + 1]) if i + 1 < k else 0))
+    # drop coincident consecutive vertices (equal neighbouring heights): the top edge just continues
+    u = []
+    for p in v:
+        if not u or u[-1] != p:
+            u.append(p)
+    while len(u) > 1 and u[-1] == u[0]:
+        u.pop()
+    W, H = int(xs[-1]), int(hs.max())
+    if rng.integers(0, 2):
+        u = [(y, x) for x, y in u]
+        W, H = H, W
+    if rng.integers(0, 2):
+        u = [(W - x, y) for x, y in u]
+    if rng.integers(0, 2):
+        u = [(x, H - y) for x, y in u]
+    ox = int(rng.integers(0, T - W + 1)) if W <= T else 0
+    oy = int(rng.integers(0, T - H + 1)) if H <= T else 0
+    u = [(min(x + ox, T), min(y + oy, T)) for x, y in u]
+    if rng.integers(0, 2):
+        u = u[::-1]
+    r = int(rng.integers(0, len(u)))
+    u = u[r:] + u[:r]
+    if collinear > 0:
+        out = []
+        for i, (a, b) in enumerate(u):
+            out.append((a, b))
+            c, d = u[(i + 1) % len(u)]
+            if rng.random() < collinear and (abs(c - a) >= 2 or abs(d - b) >= 2):
+                out.append(((a + c) // 2, (b + d) // 2))
+        u = out
+    return u
+
+
+def polygon_clips(seed: int = 0, clips: int = 4, T: int = 256, n_poly: int = 20, max_cols: int = 6,
+                  size=None, collinear: float = 0.2) -> PolygonSet:
+    """`clips` clips of `n_poly` skyline polygons each (overlaps allowed: polygons are summed)."""
+    polys = []
+    for b in range(clips):
+        rng = _rng(seed, b)
+        polys += [skyline_polygon(rng, T, max_cols, size, collinear) for _ in range(n_poly)]
+    return _pack(polys, T, [n_poly] * clips)
+
+
+def rects_as_polygons(rects, T, clip_ptr=None) -> PolygonSet:
+    """Every rect (x0, y0, x1, y1) as the clockwise (y up) list (x0,y1) (x1,y1) (x1,y0) (x0,y0),
+    one polygon per rect; clip_ptr (over rects) carries over."""
+    r = np.asarray(rects, np.int64).reshape(-1, 4)
+    V = np.stack([np.stack([r[:, 0], r[:, 3]], 1), np.stack([r[:, 2], r[:, 3]], 1),
+                  np.stack([r[:, 2], r[:, 1]], 1), np.stack([r[:, 0], r[:, 1]], 1)], 1).reshape(-1, 2)
+    pp = np.arange(0, 4 * r.shape[0] + 1, 4, dtype=np.int64)
+    cp = None if clip_ptr is None else np.asarray(clip_ptr, np.int64).copy()
+    return PolygonSet(T, V[:, 0].astype(np.int32), V[:, 1].astype(np.int32), pp, cp)
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
 
 

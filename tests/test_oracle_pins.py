@@ -435,3 +435,111 @@ def test_E4_window_and_pupil_counts():
     g = np.arange(-27, 28)
     assert len(ms) == int(((g[:, None] ** 2 + g[None, :] ** 2) <= r2).sum()) == 2337
     assert inputs.window_count(27, 27, r2) == 2337
+
+
+# ---------------------------------------------------------------- E5..E8: extraction from polygon vertex lists
+
+def _raster_polygons(ps, b):
+    """f[a, c] = sum over clip b's polygons of 1[cell centre (a+1/2, c+1/2) inside]: crossing parity of
+    a ray towards +x against the polygon's vertical edges (point-in-polygon, not the corner rule)."""
+    T = ps.T
+    img = np.zeros((T, T), np.int64)
+    cx = np.arange(T) + 0.5
+    p0, p1 = (0, ps.P) if ps.clip_ptr is None else (ps.clip_ptr[b], ps.clip_ptr[b + 1])
+    for p in range(p0, p1):
+        a, e = ps.poly_ptr[p], ps.poly_ptr[p + 1]
+        xs, ys = ps.vx[a:e].astype(np.int64), ps.vy[a:e].astype(np.int64)
+        inside = np.zeros((T, T), bool)
+        for i in range(len(xs)):
+            j = (i + 1) % len(xs)
+            if xs[i] == xs[j] and ys[i] != ys[j]:
+                lo, hi = min(ys[i], ys[j]), max(ys[i], ys[j])
+                inside ^= (xs[i] > cx)[:, None] & ((lo < cx) & (cx < hi))[None, :]
+        img += inside
+    return img
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_E5_polygon_extraction_matches_raster(seed):
+    """Alg. 2 lines 9-10 on vertex lists == corners of the point-in-polygon raster, for
+    skyline polygons in all 8 axis symmetries, both orientations, any start vertex, collinear
+    vertices, overlapping polygons summed."""
+    ps = inputs.polygon_clips(seed, clips=3, T=48, n_poly=6, max_cols=5, size=6, collinear=0.3)
+    e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
+    for b in range(ps.B):
+        img = _raster_polygons(ps, b)
+        xs, ys, ws = _corners_from_raster(img)
+        k0, k1 = e["corner_ptr"][b], e["corner_ptr"][b + 1]
+        assert np.array_equal(e["x"][k0:k1], xs) and np.array_equal(e["y"][k0:k1], ys)
+        assert np.array_equal(e["w"][k0:k1], ws)
+        assert e["area"][b] == img.sum()
+
+
+@pytest.mark.parametrize("shape", list(_SHAPES))
+def test_E6_polygons_equal_rect_unions(shape):
+    """A polygon and the union of rects covering it have the same corners (Prop. 1),
+    in every orientation / start vertex; rects given as 4-vertex polygons == rect extraction."""
+    T = 64
+    V = [(5 + 7 * a, 9 + 7 * c) for a, c in _SHAPES[shape]]
+    rects = np.array([(5 + 7 * a, 9 + 7 * c, 5 + 7 * g, 9 + 7 * d) for a, c, g, d in _SHAPE_RECTS[shape]], np.int32)
+    ref = oracle.extract(rects, T, np.array([0, len(rects)]))
+    for rev in (False, True):
+        for r in range(len(V)):
+            u = V[::-1] if rev else V
+            u = u[r:] + u[:r]
+            vx = np.array([p[0] for p in u], np.int32)
+            vy = np.array([p[1] for p in u], np.int32)
+            e = oracle.extract_polygons(vx, vy, np.array([0, len(u)]), T)
+            for k in ("x", "y", "w"):
+                assert np.array_equal(e[k], ref[k]), (shape, rev, r, k)
+            assert e["area"][0] == ref["area"][0]
+    w = inputs.c3(seed=0, clips=3, T=2048, n_lines=40)
+    ps = inputs.rects_as_polygons(w.rects, w.T, w.clip_ptr)
+    e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
+    ref = oracle.extract(w.rects, w.T, None, w.clip_ptr)
+    for k in ("x", "y", "w", "corner_ptr", "area"):
+        assert np.array_equal(e[k], ref[k]), k
+
+
+def test_E7_polygon_edge_cases():
+    T = 16
+    ok = lambda vx, vy: oracle.extract_polygons(np.array(vx, np.int32), np.array(vy, np.int32),
+                                                np.array([0, len(vx)]), T)
+    # empty input; collinear vertex on every edge of the unit square is harmless
+    e = oracle.extract_polygons(np.zeros(0, np.int32), np.zeros(0, np.int32), np.array([0]), T)
+    assert e["K"] == 0 and e["area"][0] == 0
+    e = ok([0, 1, 2, 2, 2, 1, 0, 0], [2, 2, 2, 1, 0, 0, 0, 1])
+    assert e["area"][0] == 4 and e["K"] == 4
+    # counter-clockwise list == clockwise list (reversed internally)
+    a = ok([0, 3, 3, 0], [2, 2, 0, 0])
+    b = ok([0, 0, 3, 3], [2, 0, 0, 2])
+    assert all(np.array_equal(a[k], b[k]) for k in ("x", "y", "w")) and a["area"][0] == 6
+    # vertices on the tile boundary (x = T) are kept (reading A7)
+    e = ok([10, T, T, 10], [T, T, 3, 3])
+    assert T in e["x"].tolist() and T in e["y"].tolist()
+    # two overlapping copies are summed: weights +-2 (P:589-595)
+    e = oracle.extract_polygons(np.array([0, 3, 3, 0] * 2, np.int32), np.array([2, 2, 0, 0] * 2, np.int32),
+                                np.array([0, 4, 8]), T)
+    assert set(e["w"].tolist()) == {2, -2} and e["area"][0] == 12
+    for vx, vy in (([0, 3, 3, 0], [2, 2, 0, 1]),          # diagonal edge
+                   ([0, 3, 3, 3, 0], [2, 2, 2, 0, 0]),    # zero-length edge
+                   ([0, T + 1, T + 1, 0], [2, 2, 0, 0])):  # outside [0, T]
+        with pytest.raises(oracle.OracleError):
+            ok(vx, vy)
+
+
+@pytest.mark.parametrize("shape", list(_SHAPES))
+def test_E8_polygon_corners_give_paper_prop3(shape):
+    """Coefficients of the corners extracted from the vertex list == the paper's edge-length
+    Prop. 3 on the same list, x T (reading A1)."""
+    rng = np.random.default_rng(7)
+    T = 256
+    s = int(rng.integers(3, 40))
+    ox, oy = rng.integers(0, T - 3 * s, 2)
+    V = [(int(ox + s * a), int(oy + s * c)) for a, c in _SHAPES[shape]]
+    e = oracle.extract_polygons(np.array([p[0] for p in V], np.int32), np.array([p[1] for p in V], np.int32),
+                                np.array([0, len(V)]), T)
+    ms, ns = oracle.window(6, 6)
+    F, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
+    ref = np.array([_paper_prop3(V, int(m), int(n), T) for m, n in zip(ms, ns)])
+    _check(T * F, ref, T * B + 1e-300, 1e-13, f"Prop.3 polygon {shape}")
