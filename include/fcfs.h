@@ -112,6 +112,32 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
                                      void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * a1 from polygon vertex lists (the paper's own input: Alg. 2 REQUIRE "clockwise vertex lists",
+ * P:930-935; lines 9-10 "+1 at the end, -1 at the start of each horizontal edge").
+ *
+ * vx, vy     int32 [V] vertices, device.  Polygon p is vertices [poly_ptr[p], poly_ptr[p+1]),
+ *            closed (edge i runs from vertex i to vertex i+1 mod n).  Any start vertex, either
+ *            orientation (reading A16: a list whose area sum_h y_a (x_b - x_a) is negative is
+ *            taken reversed), collinear vertices allowed; every edge must be horizontal or
+ *            vertical with non-zero length.  Self-intersection is not checked.
+ * poly_ptr   int64 [P+1] CSR over vertices, device (poly_ptr[0] == 0, poly_ptr[P] == V).
+ * clip_ptr   int64 [B+1] CSR over polygons, device; NULL => one clip (B == 1).
+ *            The polygons of a clip are SUMMED (signal model).
+ * x, y, w, corner_ptr, area, K_total_host: as fcfs_vertices_from_rects (bit-exact canonical
+ *            corners sorted by (clip, y, x); one stream sync).
+ * Errors: FCFS_E_INVALID for a diagonal or zero-length edge (device-checked), FCFS_E_RANGE for a
+ * vertex outside [0,T]^2, FCFS_E_CAPACITY if K > cap (K_total_host still written).
+ * Limits: T <= 2^20, B < 2^22, V < 2^31.
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_polygons_workspace_bytes(int64_t V, int64_t P, int64_t B);
+fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, int64_t V,
+                                        const int64_t *poly_ptr, int64_t P, const int64_t *clip_ptr,
+                                        int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
+                                        int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                        int64_t *K_total_host, void *ws, size_t ws_bytes,
+                                        void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * a2-a5 — coefficients of ONE clip: phase reduction + twiddles (a2), the separable
  * contraction P = A diag(w) B^T over cos/sin quadrant rows (a3), axes + DC (a4) and the
  * window / pupil epilogue with exact conj mirroring F[-m,-n] = conj F[m,n] (a5).

@@ -190,6 +190,51 @@ __global__ void k_group_corners(const int4 *__restrict__ rects, const int64_t *_
     }
 }
 
+// Polygon vertex lists (the paper's input, Alg. 2): one warp per polygon.  Every vertex
+// is the end of its incoming edge and the start of its outgoing one, so with s = +1 for a clockwise
+// (y up) list and -1 for a counter-clockwise one (sign of the vertex-form area sum_h y_a (x_b - x_a),
+// reading A16), Alg. 2 lines 9-10 ("+1 at the end, -1 at the start of each horizontal edge",
+// P:945-946) give vertex i the raw weight s ([edge i-1 horizontal] - [edge i horizontal]): one raw
+// corner per vertex, no counting pass.  Collinear vertices get 0.  A diagonal or zero-length edge
+// sets err bit 16, a vertex outside [0,T]^2 bit 1; the polygon then contributes nothing.
+__global__ void k_polygon_corners(const int32_t *__restrict__ vx, const int32_t *__restrict__ vy,
+                                  const int64_t *__restrict__ poly_ptr, int64_t P,
+                                  const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
+                                  unsigned long long *keys, int32_t *wts, int32_t *err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
+        const int64_t v0 = poly_ptr[p];
+        const int64_t n = poly_ptr[p + 1] - v0;
+        if (n <= 0) continue;
+        const int64_t b = find_clip(clip_ptr, B, p);
+        long long A = 0;
+        bool bad = false, range = false;
+        for (int64_t i = lane; i < n; i += 32) {
+            const int64_t j = i + 1 == n ? 0 : i + 1;
+            const int32_t xi = vx[v0 + i], yi = vy[v0 + i], xj = vx[v0 + j], yj = vy[v0 + j];
+            range |= xi < 0 || yi < 0 || xi > T || yi > T;
+            const bool hor = yi == yj && xi != xj, ver = xi == xj && yi != yj;
+            bad |= !(hor || ver);
+            if (hor) A += (long long)yi * (long long)(xj - xi);
+        }
+        for (int o = 16; o > 0; o >>= 1) A += __shfl_xor_sync(0xffffffffu, A, o);
+        bad = __any_sync(0xffffffffu, bad);
+        range = __any_sync(0xffffffffu, range);
+        if (lane == 0 && (bad || range)) atomicOr(err, (bad ? 16 : 0) | (range ? 1 : 0));
+        const int s = A < 0 ? -1 : 1;
+        for (int64_t i = lane; i < n; i += 32) {
+            const int64_t h = i == 0 ? n - 1 : i - 1, j = i + 1 == n ? 0 : i + 1;
+            const int32_t xi = vx[v0 + i], yi = vy[v0 + i];
+            const bool hin = vy[v0 + h] == yi && vx[v0 + h] != xi;
+            const bool hout = vy[v0 + j] == yi && vx[v0 + j] != xi;
+            const bool ok = !(bad || range);
+            keys[v0 + i] = ok ? make_key(b, yi, xi) : make_key(b, 0, 0);
+            wts[v0 + i] = ok ? s * ((int)hin - (int)hout) : 0;
+        }
+    }
+}
+
 __global__ void k_fill_sentinel(unsigned long long *keys, int32_t *wts, int64_t n,
                                 const unsigned long long *raw_count) {
     int64_t start = raw_count ? (int64_t)*raw_count : 0;
@@ -623,6 +668,39 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
     return FCFS_OK;
 }
 
+// steps 2-5 of the general path on the raw (key, weight) list in W.keys_a / W.w_a: sort, merge
+// equal keys (sum), drop zeros, scatter + area, corner_ptr; one stream sync for K and the error bits
+static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int end_bit, int64_t B, int64_t cap, int32_t *x,
+                                  int32_t *y, int32_t *w, int64_t *corner_ptr, int64_t *area, int64_t &Kh,
+                                  int32_t &errh, cudaStream_t s) {
+    const int threads = 256;
+    size_t tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, W.keys_a, W.keys_b, W.w_a, W.w_b, (int)cap_raw,
+                                                  0, end_bit, s));
+    count_launch(4);
+    tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceReduce::ReduceByKey(W.cub_tmp, tb, W.keys_b, W.keys_a, W.w_b, W.w_a, W.num_runs,
+                                                 cub::Sum(), (int)cap_raw, s));
+    count_launch(2);
+    int64_t blocks = (cap_raw + threads - 1) / threads;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_flags<<<(unsigned)blocks, threads, 0, s>>>(W.w_a, W.num_runs, cap_raw, W.flags);
+    FCFS_CHECK_LAUNCH("k_flags");
+    tb = W.cub_bytes;
+    FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.flags, W.pos, (int)cap_raw, s));
+    count_launch(2);
+    k_scatter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, W.flags, W.pos, cap_raw, cap, x, y, w,
+                                                   W.keys_b, area, W.K);
+    FCFS_CHECK_LAUNCH("k_scatter");
+    int64_t pb = (B + 1 + threads - 1) / threads;
+    k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr);
+    FCFS_CHECK_LAUNCH("k_corner_ptr");
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, W.K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    return FCFS_OK;
+}
+
 static int64_t raw_capacity(int64_t R, int64_t max_group, bool singleton) {
     if (singleton) return 4 * R;
     int64_t g = max_group < 1 ? 1 : max_group;
@@ -738,32 +816,10 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         k_fill_sentinel<<<148 * 4, 256, 0, s>>>(W.keys_a, W.w_a, cap_raw, raw_count);
         FCFS_CHECK_LAUNCH("k_fill_sentinel");
     }
-    size_t tb = W.cub_bytes;
-    FCFS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, W.keys_a, W.keys_b, W.w_a, W.w_b, (int)cap_raw,
-                                                  0, end_bit, s));
-    count_launch(4);
-    tb = W.cub_bytes;
-    FCFS_TRY_CUDA(cub::DeviceReduce::ReduceByKey(W.cub_tmp, tb, W.keys_b, W.keys_a, W.w_b, W.w_a, W.num_runs,
-                                                 cub::Sum(), (int)cap_raw, s));
-    count_launch(2);
-    int64_t blocks = (cap_raw + threads - 1) / threads;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    k_flags<<<(unsigned)blocks, threads, 0, s>>>(W.w_a, W.num_runs, cap_raw, W.flags);
-    FCFS_CHECK_LAUNCH("k_flags");
-    tb = W.cub_bytes;
-    FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.flags, W.pos, (int)cap_raw, s));
-    count_launch(2);
-    k_scatter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, W.flags, W.pos, cap_raw, cap, x, y, w,
-                                                   W.keys_b, area, W.K);
-    FCFS_CHECK_LAUNCH("k_scatter");
-    int64_t pb = (B + 1 + threads - 1) / threads;
-    k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr);
-    FCFS_CHECK_LAUNCH("k_corner_ptr");
     int64_t Kh = 0;
     int32_t errh = 0;
-    FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, W.K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    fcfs_status st = finish_corners(W, cap_raw, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
+    if (st != FCFS_OK) return st;
     if (K_host) *K_host = Kh;
     if (errh & 1) {
         set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");
@@ -779,6 +835,67 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
     }
     if (Kh > cap) {
         set_error("fcfs_vertices_from_rects: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
+        return FCFS_E_CAPACITY;
+    }
+    return FCFS_OK;
+}
+
+size_t extract_polygons_workspace_bytes(int64_t V, int64_t B) {
+    const int64_t cap = V < 1 ? 1 : V;
+    Carver cv(nullptr, 0);
+    ExtractWs w;
+    carve(cv, cap, cub_bytes_for(cap, 2 * kCoordBits + clip_bits(B)), w);
+    return cv.used();
+}
+
+// polygon vertex lists -> canonical corners: one raw corner per vertex (k_polygon_corners), then the
+// general path's sort / merge / compaction (polygons of a clip are summed)
+fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, const int64_t *poly_ptr, int64_t P,
+                             const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
+                             int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
+                             size_t ws_bytes, cudaStream_t s) {
+    const int64_t cap_raw = V < 1 ? 1 : V;
+    if (cap_raw >= (int64_t(1) << 31)) {
+        set_error("fcfs_vertices_from_polygons: %lld vertices exceed 2^31", (long long)V);
+        return FCFS_E_UNSUPPORTED;
+    }
+    const int end_bit = 2 * kCoordBits + clip_bits(B);
+    Carver cv(ws, ws_bytes);
+    ExtractWs W;
+    carve(cv, cap_raw, cub_bytes_for(cap_raw, end_bit), W);
+    if (!cv.fits()) {
+        set_error("fcfs_vertices_from_polygons: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.num_runs, 0, 2 * sizeof(int64_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(area, 0, B * sizeof(int64_t), s));
+    // sentinels first: vertices outside every polygon's CSR range are never visited
+    k_fill_sentinel<<<(unsigned)(cap_raw < 148 * 4 * 256 ? (cap_raw + 255) / 256 : 148 * 4), 256, 0, s>>>(
+        W.keys_a, W.w_a, cap_raw, nullptr);
+    FCFS_CHECK_LAUNCH("k_fill_sentinel");
+    if (P > 0 && V > 0) {
+        int64_t blocks = (P + 7) / 8;   // 8 warps (polygons) per block
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        k_polygon_corners<<<(unsigned)blocks, 256, 0, s>>>(vx, vy, poly_ptr, P, clip_ptr, B, T, W.keys_a, W.w_a,
+                                                           W.err);
+        FCFS_CHECK_LAUNCH("k_polygon_corners");
+    }
+    int64_t Kh = 0;
+    int32_t errh = 0;
+    fcfs_status st = finish_corners(W, cap_raw, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
+    if (st != FCFS_OK) return st;
+    if (K_host) *K_host = Kh;
+    if (errh & 16) {
+        set_error("fcfs_vertices_from_polygons: a polygon edge is diagonal or of zero length");
+        return FCFS_E_INVALID;
+    }
+    if (errh & 1) {
+        set_error("fcfs_vertices_from_polygons: a vertex lies outside [0,T]^2");
+        return FCFS_E_RANGE;
+    }
+    if (Kh > cap) {
+        set_error("fcfs_vertices_from_polygons: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
         return FCFS_E_CAPACITY;
     }
     return FCFS_OK;

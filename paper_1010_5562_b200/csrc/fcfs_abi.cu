@@ -59,6 +59,11 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                     int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s);
+size_t extract_polygons_workspace_bytes(int64_t V, int64_t B);
+fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, const int64_t *poly_ptr, int64_t P,
+                             const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
+                             int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
+                             size_t ws_bytes, cudaStream_t s);
 // contract_tf32.cu
 fcfs_status tf32_supported(const GemmPlan &plan, int32_t T);
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
@@ -322,6 +327,31 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
     StageScope scope(kStageExtract, (cudaStream_t)stream);
     return extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
                    K_total_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t fcfs_polygons_workspace_bytes(int64_t V, int64_t P, int64_t B) {
+    (void)P;
+    return extract_polygons_workspace_bytes(V, B);
+}
+
+fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, int64_t V, const int64_t *poly_ptr,
+                                        int64_t P, const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x,
+                                        int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                        int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    if (V < 0 || P < 0 || B < 1 || B >= (int64_t(1) << 22) || (V > 0 && (!vx || !vy)) || !poly_ptr || !corner_ptr ||
+        !area || !K_total_host) {
+        set_error("fcfs_vertices_from_polygons: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (cap > 0 && (!x || !y || !w)) { set_error("null corner output with cap > 0"); return FCFS_E_INVALID; }
+    if (clip_ptr == nullptr && B != 1) { set_error("clip_ptr NULL requires B == 1"); return FCFS_E_INVALID; }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageExtract, (cudaStream_t)stream);
+    return extract_polygons(vx, vy, V, poly_ptr, P, clip_ptr, B, T, x, y, w, cap, corner_ptr, area, K_total_host,
+                            ws, ws_bytes, (cudaStream_t)stream);
 }
 
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,

@@ -62,6 +62,11 @@ _lib.fcfs_vertices_workspace_bytes.restype = _sz
 _lib.fcfs_vertices_from_rects.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P,
                                           ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_vertices_from_rects.restype = _i32
+_lib.fcfs_polygons_workspace_bytes.argtypes = [_i64, _i64, _i64]
+_lib.fcfs_polygons_workspace_bytes.restype = _sz
+_lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _i32, _P, _P, _P, _i64, _P, _P,
+                                             ctypes.POINTER(_i64), _P, _sz, _P]
+_lib.fcfs_vertices_from_polygons.restype = _i32
 _lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
 _lib.fcfs_coeffs_workspace_bytes.restype = _sz
 _lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _P, _P, _sz, _P]
@@ -85,7 +90,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_coeffs", "fcfs_batched_workspace_bytes", "fcfs_coeffs_batched", "fcfs_window_size",
             "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
-            "fcfs_row_buckets"]
+            "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons"]
 STAGES = ("extract", "contract", "epilogue")
 
 
@@ -186,6 +191,32 @@ def vertices_from_rects(rects, T, group_ptr=None, clip_ptr=None, max_group=None,
                                        _ptr(x), _ptr(y), _ptr(w), cap, _ptr(cptr), _ptr(area), ctypes.byref(K),
                                        _ptr(ws), ws.numel(), _stream(stream))
     _check(st, "fcfs_vertices_from_rects")
+    k = K.value
+    return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
+
+
+def vertices_from_polygons(vx, vy, poly_ptr, T, clip_ptr=None, stream=None):
+    """a1 from polygon vertex lists.  vx, vy int32 cuda [V]; poly_ptr int64 cuda [P+1];
+    clip_ptr int64 cuda [B+1] over polygons or None.  At most one corner per vertex.
+
+    Returns dict(x, y, w (int32 cuda [K]), corner_ptr (int64 cuda [B+1]), area (int64 cuda [B]), K).
+    """
+    dev = poly_ptr.device
+    vx, vy = vx.contiguous(), vy.contiguous()
+    V = vx.shape[0]
+    P = poly_ptr.shape[0] - 1
+    B = 1 if clip_ptr is None else clip_ptr.shape[0] - 1
+    x = torch.empty(max(V, 1), dtype=torch.int32, device=dev)
+    y = torch.empty_like(x)
+    w = torch.empty_like(x)
+    cptr = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    area = torch.empty(B, dtype=torch.int64, device=dev)
+    ws = _ws(_lib.fcfs_polygons_workspace_bytes(V, P, B), dev)
+    K = ctypes.c_int64(0)
+    st = _lib.fcfs_vertices_from_polygons(_ptr(vx), _ptr(vy), V, _ptr(poly_ptr), P, _ptr(clip_ptr), B, int(T),
+                                          _ptr(x), _ptr(y), _ptr(w), V, _ptr(cptr), _ptr(area), ctypes.byref(K),
+                                          _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "fcfs_vertices_from_polygons")
     k = K.value
     return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
 

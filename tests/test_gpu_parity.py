@@ -391,3 +391,106 @@ def test_row_buckets_bit_exact(fcfs, cap):
         assert np.array_equal(r["bptr"].cpu().numpy(), bp)
         assert np.array_equal(r["by"].cpu().numpy(), byr)
         assert np.array_equal(r["clip_bptr"].cpu().numpy(), cb)
+
+
+# ------------------------------------------------------------------ a1 from polygon vertex lists (NEXT-3)
+
+def _gpu_polys(fcfs, ps):
+    return fcfs.vertices_from_polygons(_dev(ps.vx, torch.int32), _dev(ps.vy, torch.int32),
+                                       _dev(ps.poly_ptr, torch.int64), ps.T, _dev(ps.clip_ptr, torch.int64))
+
+
+def _sub_polys(ps, clips):
+    """The polygons of the listed clips as their own PolygonSet (for per-clip oracle checks)."""
+    polys, per = [], []
+    for b in clips:
+        p0, p1 = int(ps.clip_ptr[b]), int(ps.clip_ptr[b + 1])
+        for p in range(p0, p1):
+            a, e = int(ps.poly_ptr[p]), int(ps.poly_ptr[p + 1])
+            polys.append(list(zip(ps.vx[a:e].tolist(), ps.vy[a:e].tolist())))
+        per.append(p1 - p0)
+    return inputs._pack(polys, ps.T, per)
+
+
+@pytest.mark.parametrize("case", ["small", "many_clips", "one_big_clip", "long_polygons"])
+def test_polygon_extraction_bit_exact(fcfs, case):
+    if case == "small":
+        ps = inputs.polygon_clips(0, clips=4, T=256, n_poly=20)
+    elif case == "many_clips":
+        ps = inputs.polygon_clips(1, clips=300, T=2048, n_poly=100, max_cols=8, size=60)
+    elif case == "one_big_clip":
+        ps = inputs.polygon_clips(2, clips=1, T=65536, n_poly=40000, max_cols=8, size=3000)
+        ps.clip_ptr = None
+    else:                                            # polygons of 100s of vertices (warp loops > 1 pass)
+        ps = inputs.polygon_clips(3, clips=3, T=8192, n_poly=30, max_cols=200, size=20, collinear=0.5)
+    e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
+    g = _gpu_polys(fcfs, ps)
+    _assert_extract_equal(g, e)
+
+
+def test_polygon_extraction_full_c3_as_polygons(fcfs):
+    """BASELINE configs[2] rects given as 4-vertex polygons (4096 clips): identical to the rect
+    extraction, and seeded clips bit-exact against the oracle's polygon extraction."""
+    wl = inputs.c3(clips=4096)
+    ps = inputs.rects_as_polygons(wl.rects, wl.T, wl.clip_ptr)
+    g = _gpu_polys(fcfs, ps)
+    gr = _gpu_extract(fcfs, wl)
+    for k in ("x", "y", "w", "corner_ptr", "area"):
+        assert torch.equal(g[k], gr[k]), k
+    rng = np.random.default_rng(3)
+    clips = sorted(set([0, 4095] + rng.integers(0, 4096, 6).tolist()))
+    e = oracle.extract_polygons(*(lambda s: (s.vx, s.vy, s.poly_ptr, s.T, s.clip_ptr))(_sub_polys(ps, clips)))
+    cp = g["corner_ptr"].cpu().numpy()
+    for i, b in enumerate(clips):
+        sl = slice(cp[b], cp[b + 1])
+        el = slice(e["corner_ptr"][i], e["corner_ptr"][i + 1])
+        for k in ("x", "y", "w"):
+            assert np.array_equal(g[k][sl].cpu().numpy(), e[k][el]), (b, k)
+        assert g["area"][b].item() == e["area"][i]
+
+
+def test_polygon_edge_cases_and_errors(fcfs):
+    T = 16
+    one = lambda vx, vy: fcfs.vertices_from_polygons(_dev(np.array(vx), torch.int32), _dev(np.array(vy), torch.int32),
+                                                     _dev(np.array([0, len(vx)]), torch.int64), T)
+    # empty input; an empty polygon and an empty clip among non-empty ones
+    g = fcfs.vertices_from_polygons(torch.zeros(0, dtype=torch.int32, device="cuda"),
+                                    torch.zeros(0, dtype=torch.int32, device="cuda"),
+                                    torch.zeros(1, dtype=torch.int64, device="cuda"), T)
+    assert g["K"] == 0 and g["area"].item() == 0
+    vx = np.array([0, 3, 3, 0, 10, 16, 16, 10, 0, 1, 2, 2, 2, 1, 0, 0], np.int32)
+    vy = np.array([2, 2, 0, 0, 16, 16, 3, 3, 2, 2, 2, 1, 0, 0, 0, 1], np.int32)
+    pp = np.array([0, 4, 4, 8, 16], np.int64)          # polygon 1 empty; polygon 3 has collinear vertices
+    cp = np.array([0, 2, 2, 4], np.int64)              # clip 1 empty
+    e = oracle.extract_polygons(vx, vy, pp, T, cp)
+    g = fcfs.vertices_from_polygons(_dev(vx, torch.int32), _dev(vy, torch.int32), _dev(pp, torch.int64), T,
+                                    _dev(cp, torch.int64))
+    _assert_extract_equal(g, e)
+    # counter-clockwise == clockwise
+    a, b = one([0, 3, 3, 0], [2, 2, 0, 0]), one([0, 0, 3, 3], [2, 0, 0, 2])
+    assert all(torch.equal(a[k], b[k]) for k in ("x", "y", "w", "area"))
+    for vx, vy, st in (([0, 3, 3, 0], [2, 2, 0, 1], fcfs.E_INVALID),        # diagonal edge
+                       ([0, 3, 3, 3, 0], [2, 2, 2, 0, 0], fcfs.E_INVALID),  # zero-length edge
+                       ([0, T + 1, T + 1, 0], [2, 2, 0, 0], fcfs.E_RANGE)):  # outside [0, T]
+        with pytest.raises(fcfs.FcfsError) as ei:
+            one(vx, vy)
+        assert ei.value.status == st
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_polygon_clips_coefficients(fcfs, prec):
+    """Polygon input through the batched pupil path: clips against the oracle (corners and F)."""
+    ps = inputs.polygon_clips(4, clips=16, T=2048, n_poly=120, max_cols=8, size=80)
+    g = _gpu_polys(fcfs, ps)
+    e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
+    _assert_extract_equal(g, e)
+    r2 = inputs.pupil_r2(ps.T)
+    M = int(np.floor(np.sqrt(r2)))
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], ps.T, M, M, r2, "pupil",
+                            prec).cpu().numpy()
+    ms, ns = oracle.window(M, M, r2)
+    cp = e["corner_ptr"]
+    for b in (0, 5, 15):
+        sl = slice(cp[b], cp[b + 1])
+        Fr, B = oracle.coeffs(e["x"][sl], e["y"][sl], e["w"][sl], e["area"][b], ps.T, ms, ns)
+        _assert_parity(F[b], Fr, B, prec, f"polygon clip {b}", ms, ns)
