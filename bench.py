@@ -45,6 +45,9 @@ def parse():
                     help="single-clip configs (c1, c2, c4, c5) on N > 1 GPUs: frequency rows + all_gather, "
                          "or vertex blocks + reduce_scatter")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--input", default="rects", choices=["rects", "polygons"],
+                    help="a1 input: rects (fcfs_vertices_from_rects) or the same rects as 4-vertex polygon "
+                         "lists (fcfs_vertices_from_polygons; workloads with one group per rect)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
@@ -204,6 +207,8 @@ def config_dict(args, wl, prec, world):
          "parallelism": (f"clip-sharded x{world}" if wl.B > 1 else
                          (f"{args.shard}-sharded x{world}" if world > 1 else "single GPU")),
          "l2": "flushed between steps (512 MiB write, outside the timed events)"}
+    if getattr(args, "input", "rects") == "polygons":
+        d["input"] = "each rect as a clockwise 4-vertex polygon (fcfs_vertices_from_polygons)"
     return d
 
 
@@ -237,8 +242,22 @@ def main():
     cp = None if wl.clip_ptr is None else torch.from_numpy(wl.clip_ptr).to(dev)
     mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
     G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
-    vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=gp is not None, device=dev)
-    K = vp.run(rects, gp, cp)
+    if args.input == "polygons":
+        if wl.group_ptr is not None:
+            raise SystemExit("--input polygons needs a workload with one group per rect (c3, c4, c5)")
+        ps = inputs.rects_as_polygons(wl.rects, wl.T, wl.clip_ptr)
+        pvx, pvy = torch.from_numpy(ps.vx).to(dev), torch.from_numpy(ps.vy).to(dev)
+        ppp = torch.from_numpy(ps.poly_ptr).to(dev)
+        vp = fcfs.PolygonsPlan(ps.vx.shape[0], ps.P, wl.T, wl.B, device=dev)
+
+        def extract():
+            return vp.run(pvx, pvy, ppp, cp)
+    else:
+        vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=gp is not None, device=dev)
+
+        def extract():
+            return vp.run(rects, gp, cp)
+    K = extract()
     cptr_h = vp.corner_ptr.cpu().numpy()
     kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
     if wl.B > 1:
@@ -277,7 +296,7 @@ def main():
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step():
-        vp.run(rects, gp, cp)
+        extract()
         return coeffs()
 
     for _ in range(args.warmup):
@@ -363,7 +382,7 @@ def main():
     # the compute of the next.  Every byte of every step's input and output still crosses PCIe inside
     # the timed region (start / end events bracket all three streams).  One clip: sequential.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.input == "rects":
         e2e_steps = max(2, min(args.steps, 5))
         h2d_bytes = int(rects_h.numel() * 4)
         if wl.B > 1 and wl.B % args.e2e_split == 0 and wl.group_ptr is None:

@@ -456,6 +456,104 @@ static constexpr int kBucketRectsPerThread = 4;   // kClipRects / kBucketThreads
 static constexpr int kBucketMaxT = 8191;
 static constexpr int kBucketCap = 4 * kClipRects;
 
+// exclusive scan of the nb bucket sizes in hist (thread t owns buckets [t*per, (t+1)*per)); ends
+// with a __syncthreads
+__device__ __forceinline__ void bucket_scan(int32_t *hist, int nb, int32_t *wsum) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int per = (nb + kBucketThreads - 1) / kBucketThreads;
+    const int lo = threadIdx.x * per, hi = min(lo + per, nb);
+    int sown = 0;
+    for (int i = lo; i < hi; ++i) sown += hist[i];
+    int incl = sown;
+    for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int run = incl - sown;
+    for (int i = 0; i < wid; ++i) run += wsum[i];
+    for (int i = lo; i < hi; ++i) { const int c = hist[i]; hist[i] = run; run += c; }
+    __syncthreads();
+}
+
+// Second half of the per-clip bucket paths (shared by rects and polygons): the clip's nv corners sit
+// in y buckets (bxw = x << 16 | w & 0xFFFF, by = y; hist[y] = end of bucket y).  Every corner finds
+// its rank inside its (short) bucket by x, the first of equal (y, x) carries the summed weight
+// (groups / polygons are summed), a block scan over the sorted positions drops zero weights, and the
+// clip is written in canonical (y, x) order straight to its CSR position (look-back offset,
+// coalesced), with its exact int64 area.  Ends with a __syncthreads.
+__device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32_t *bxw, uint32_t *syx, int16_t *by,
+                                            int16_t *sw, int32_t *hist, int32_t *wsum, long long *asum,
+                                            int *tot_s, int64_t *s_off, int32_t *xs, int32_t *ys, int32_t *ws,
+                                            int64_t cap, int64_t *corner_ptr, unsigned long long *status,
+                                            int64_t *area) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
+    // rank inside the bucket by x (ties by index); the first of equal x carries the run sum
+    for (int i = threadIdx.x; i < nv; i += kBucketThreads) {
+        const int y = by[i];
+        const int st = y ? hist[y - 1] : 0, en = hist[y];
+        const uint32_t xi = bxw[i] >> 16;
+        int rank = 0, wv = 0;
+        bool first = true;
+#pragma unroll 2
+        for (int j = st; j < en; ++j) {
+            const uint32_t v = bxw[j];
+            const uint32_t xj = v >> 16;
+            const bool eq = xj == xi, before = j < i;
+            rank += (xj < xi) | (eq & before);
+            wv += eq ? (int)(int16_t)(v & 0xFFFFu) : 0;
+            first &= !(eq & before);
+        }
+        syx[st + rank] = ((uint32_t)y << 16) | xi;
+        sw[st + rank] = first ? (int16_t)wv : (int16_t)0;
+    }
+    __syncthreads();
+    // compact the non-zero sorted entries: thread t owns sorted positions [t*pp, (t+1)*pp)
+    const int pp = (nv + kBucketThreads - 1) / kBucketThreads;
+    const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
+    int cnt = 0;
+    long long a = 0;
+    for (int i = lo; i < hi; ++i) {
+        const int16_t wv = sw[i];
+        if (wv != 0) {
+            ++cnt;
+            a += (long long)wv * (long long)(syx[i] & 0xFFFFu) * (long long)(syx[i] >> 16);
+        }
+    }
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    __syncthreads();                                // wsum reuse; bxw / by are free from here
+    if (lane == 31) wsum[wid] = incl;
+    if (lane == 0) asum[wid] = a;
+    __syncthreads();
+    int outp = incl - cnt;
+    for (int i = 0; i < wid; ++i) outp += wsum[i];
+    for (int i = lo; i < hi; ++i) {
+        const int16_t wv = sw[i];
+        if (wv != 0) { bxw[outp] = syx[i]; by[outp] = wv; ++outp; }
+    }
+    if (threadIdx.x == kBucketThreads - 1) *tot_s = outp;     // the last thread ends at the clip total
+    __syncthreads();
+    const int total = *tot_s;
+    if (threadIdx.x == 0) *s_off = clip_lookback(status, b, B, total, corner_ptr);
+    __syncthreads();
+    const int64_t base = *s_off;
+    for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores, final positions
+        if (base + i >= cap) break;
+        const uint32_t yx = bxw[i];
+        xs[base + i] = (int32_t)(yx & 0xFFFFu);
+        ys[base + i] = (int32_t)(yx >> 16);
+        ws[base + i] = by[i];
+    }
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
+        area[b] = t;
+    }
+    __syncthreads();
+}
+
+
 __global__ void __launch_bounds__(kBucketThreads, 3)
 k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
                       int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
@@ -471,8 +569,6 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
     __shared__ int tot_s;
     __shared__ int64_t s_off;
     const int nb = T + 1;                               // buckets y = 0..T
-    const int per = (nb + kBucketThreads - 1) / kBucketThreads;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
@@ -501,19 +597,7 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             atomicAdd(&hist[rq[j].w], 2);
         }
         __syncthreads();
-        {   // exclusive scan of bucket sizes: thread t owns buckets [t*per, (t+1)*per)
-            const int lo = threadIdx.x * per, hi = min(lo + per, nb);
-            int sown = 0;
-            for (int i = lo; i < hi; ++i) sown += hist[i];
-            int incl = sown;
-            for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
-            if (lane == 31) wsum[wid] = incl;
-            __syncthreads();
-            int run = incl - sown;
-            for (int i = 0; i < wid; ++i) run += wsum[i];
-            for (int i = lo; i < hi; ++i) { const int c = hist[i]; hist[i] = run; run += c; }
-        }
-        __syncthreads();
+        bucket_scan(hist, nb, wsum);
         // scatter into buckets: afterwards hist[y] = end of bucket y (= start of bucket y + 1)
 #pragma unroll
         for (int j = 0; j < kBucketRectsPerThread; ++j) {
@@ -527,71 +611,136 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             bxw[p + 1] = ((uint32_t)q.z << 16) | 0x0001u;   by[p + 1] = (int16_t)q.w;
         }
         __syncthreads();
-        const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
-        // rank inside the bucket by x (ties by index); the first of equal x carries the run sum
-        for (int i = threadIdx.x; i < nv; i += kBucketThreads) {
-            const int y = by[i];
-            const int st = y ? hist[y - 1] : 0, en = hist[y];
-            const uint32_t xi = bxw[i] >> 16;
-            int rank = 0, wv = 0;
-            bool first = true;
-#pragma unroll 2
-            for (int j = st; j < en; ++j) {
-                const uint32_t v = bxw[j];
-                const uint32_t xj = v >> 16;
-                const bool eq = xj == xi, before = j < i;
-                rank += (xj < xi) | (eq & before);
-                wv += eq ? (int)(int16_t)(v & 0xFFFFu) : 0;
-                first &= !(eq & before);
+        bucket_emit(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
+                    status, area);
+    }
+}
+
+static constexpr int kSmallPoly = 32;                          // thread per polygon up to this size
+static constexpr int kMaxLarge = kBucketCap / kSmallPoly + 1;  // longer polygons of one clip (warp each)
+
+// Per-clip bucket path for polygon vertex lists (T <= kBucketMaxT, <= kBucketCap vertices per clip):
+// a thread (a warp for polygons of > kSmallPoly vertices) per polygon computes the orientation (sign of the vertex-form area, reading A16), checks the
+// edges and writes every vertex's raw weight s ([edge i-1 horizontal] - [edge i horizontal]) (Alg. 2
+// lines 9-10) into shared memory; the non-zero ones are counting-sorted into y buckets,
+// then bucket_emit as for rects.
+__global__ void __launch_bounds__(kBucketThreads, 2)
+k_clip_polygons_bucket(const int32_t *__restrict__ vx, const int32_t *__restrict__ vy,
+                       const int64_t *__restrict__ poly_ptr, int64_t P, const int64_t *__restrict__ clip_ptr,
+                       int64_t B, int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
+                       unsigned long long *status, int64_t *area, int32_t *err) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    uint32_t *bxw = (uint32_t *)bsm;                    // [cap] bucketed (x << 16 | w & 0xFFFF)
+    uint32_t *syx = bxw + kBucketCap;                   // [cap] raw (y << 16 | x), then sorted
+    int16_t *by = (int16_t *)(syx + kBucketCap);        // [cap] bucket y
+    int16_t *sw = by + kBucketCap;                      // [cap] raw weight, then sorted merged weight
+    int32_t *hist = (int32_t *)(sw + kBucketCap);       // [T + 2]
+    __shared__ int32_t wsum[kBucketThreads / 32];
+    __shared__ long long asum[kBucketThreads / 32];
+    __shared__ int tot_s;
+    __shared__ int64_t s_off;
+    __shared__ int n_large;
+    __shared__ int32_t large[kMaxLarge];
+    const int nb = T + 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        const int64_t p0 = clip_ptr ? clip_ptr[b] : 0, p1 = clip_ptr ? clip_ptr[b + 1] : P;
+        const int64_t vbase = poly_ptr[p0];
+        const int64_t nvr = poly_ptr[p1] - vbase;       // raw corners = vertices of the clip
+        if (nvr > kBucketCap) {
+            if (threadIdx.x == 0) { atomicOr(err, 8); area[b] = 0; clip_lookback(status, b, B, 0, corner_ptr); }
+            continue;
+        }
+        for (int i = threadIdx.x; i < nb + 1; i += kBucketThreads) hist[i] = 0;
+        if (threadIdx.x == 0) n_large = 0;
+        __syncthreads();
+        // raw corners: thread per polygon of <= kSmallPoly vertices (two passes over its vertices:
+        // orientation + edge checks, then weights); longer polygons are queued for warps
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += kBucketThreads) {
+            const int64_t v0 = poly_ptr[p];
+            const int n = (int)(poly_ptr[p + 1] - v0);
+            if (n > kSmallPoly) {
+                const int q = atomicAdd(&n_large, 1);
+                if (q < kMaxLarge) large[q] = (int32_t)(p - p0);
+                continue;
             }
-            syx[st + rank] = ((uint32_t)y << 16) | xi;
-            sw[st + rank] = first ? (int16_t)wv : (int16_t)0;
-        }
-        __syncthreads();
-        // compact the non-zero sorted entries: thread t owns sorted positions [t*pp, (t+1)*pp)
-        const int pp = (nv + kBucketThreads - 1) / kBucketThreads;
-        const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
-        int cnt = 0;
-        long long a = 0;
-        for (int i = lo; i < hi; ++i) {
-            const int16_t wv = sw[i];
-            if (wv != 0) {
-                ++cnt;
-                a += (long long)wv * (long long)(syx[i] & 0xFFFFu) * (long long)(syx[i] >> 16);
+            if (n == 0) continue;
+            long long A = 0;
+            bool bad = false, range = false;
+            int32_t xf = vx[v0], yf = vy[v0], xi = xf, yi = yf;
+            for (int i = 0; i < n; ++i) {
+                const int32_t xj = i + 1 < n ? vx[v0 + i + 1] : xf, yj = i + 1 < n ? vy[v0 + i + 1] : yf;
+                range |= xi < 0 || yi < 0 || xi > T || yi > T;
+                const bool hor = yi == yj && xi != xj, ver = xi == xj && yi != yj;
+                bad |= !(hor || ver);
+                if (hor) A += (long long)yi * (long long)(xj - xi);
+                xi = xj; yi = yj;
+            }
+            if (bad || range) atomicOr(err, (bad ? 16 : 0) | (range ? 1 : 0));
+            const int sg = A < 0 ? -1 : 1;
+            const bool ok = !(bad || range);
+            int32_t xh = vx[v0 + n - 1], yh = vy[v0 + n - 1];
+            xi = xf; yi = yf;
+            for (int i = 0; i < n; ++i) {
+                const int32_t xj = i + 1 < n ? vx[v0 + i + 1] : xf, yj = i + 1 < n ? vy[v0 + i + 1] : yf;
+                const bool hin = yh == yi && xh != xi, hout = yj == yi && xj != xi;
+                const int64_t o = v0 + i - vbase;
+                syx[o] = ok ? ((uint32_t)yi << 16) | (uint32_t)xi : 0u;
+                sw[o] = ok ? (int16_t)(sg * ((int)hin - (int)hout)) : (int16_t)0;
+                xh = xi; yh = yi; xi = xj; yi = yj;
             }
         }
-        int incl = cnt;
-        for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        __syncthreads();                                // wsum reuse; bxw / by are free from here
-        if (lane == 31) wsum[wid] = incl;
-        if (lane == 0) asum[wid] = a;
         __syncthreads();
-        int outp = incl - cnt;
-        for (int i = 0; i < wid; ++i) outp += wsum[i];
-        for (int i = lo; i < hi; ++i) {
+        if (n_large > kMaxLarge) {   // cannot happen (kMaxLarge * kSmallPoly >= kBucketCap); guard anyway
+            if (threadIdx.x == 0) atomicOr(err, 8);
+        }
+        // long polygons: warp per polygon
+        for (int q = wid; q < min(n_large, kMaxLarge); q += kBucketThreads / 32) {
+            const int64_t p = p0 + large[q];
+            const int64_t v0 = poly_ptr[p];
+            const int n = (int)(poly_ptr[p + 1] - v0);
+            long long A = 0;
+            bool bad = false, range = false;
+            for (int i = lane; i < n; i += 32) {
+                const int j = i + 1 == n ? 0 : i + 1;
+                const int32_t xi = vx[v0 + i], yi = vy[v0 + i], xj = vx[v0 + j], yj = vy[v0 + j];
+                range |= xi < 0 || yi < 0 || xi > T || yi > T;
+                const bool hor = yi == yj && xi != xj, ver = xi == xj && yi != yj;
+                bad |= !(hor || ver);
+                if (hor) A += (long long)yi * (long long)(xj - xi);
+            }
+            for (int o = 16; o > 0; o >>= 1) A += __shfl_xor_sync(0xffffffffu, A, o);
+            bad = __any_sync(0xffffffffu, bad);
+            range = __any_sync(0xffffffffu, range);
+            if (lane == 0 && (bad || range)) atomicOr(err, (bad ? 16 : 0) | (range ? 1 : 0));
+            const int sg = A < 0 ? -1 : 1;
+            const bool ok = !(bad || range);
+            for (int i = lane; i < n; i += 32) {
+                const int h = i == 0 ? n - 1 : i - 1, j = i + 1 == n ? 0 : i + 1;
+                const int32_t xi = vx[v0 + i], yi = vy[v0 + i];
+                const bool hin = vy[v0 + h] == yi && vx[v0 + h] != xi;
+                const bool hout = vy[v0 + j] == yi && vx[v0 + j] != xi;
+                const int64_t o = v0 + i - vbase;
+                syx[o] = ok ? ((uint32_t)yi << 16) | (uint32_t)xi : 0u;
+                sw[o] = ok ? (int16_t)(sg * ((int)hin - (int)hout)) : (int16_t)0;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nvr; i += kBucketThreads)
+            if (sw[i] != 0) atomicAdd(&hist[syx[i] >> 16], 1);
+        __syncthreads();
+        bucket_scan(hist, nb, wsum);
+        for (int i = threadIdx.x; i < nvr; i += kBucketThreads) {
             const int16_t wv = sw[i];
-            if (wv != 0) { bxw[outp] = syx[i]; by[outp] = wv; ++outp; }
-        }
-        if (threadIdx.x == kBucketThreads - 1) tot_s = outp;     // the last thread ends at the clip total
-        __syncthreads();
-        const int total = tot_s;
-        if (threadIdx.x == 0) s_off = clip_lookback(status, b, B, total, corner_ptr);
-        __syncthreads();
-        const int64_t base = s_off;
-        for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores, final positions
-            if (base + i >= cap) break;
-            const uint32_t yx = bxw[i];
-            xs[base + i] = (int32_t)(yx & 0xFFFFu);
-            ys[base + i] = (int32_t)(yx >> 16);
-            ws[base + i] = by[i];
-        }
-        if (threadIdx.x == 0) {
-            long long t = 0;
-            for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
-            area[b] = t;
+            if (wv == 0) continue;
+            const uint32_t yx = syx[i];
+            const int p = atomicAdd(&hist[yx >> 16], 1);
+            bxw[p] = ((yx & 0xFFFFu) << 16) | ((uint32_t)(int32_t)wv & 0xFFFFu);
+            by[p] = (int16_t)(yx >> 16);
         }
         __syncthreads();
+        bucket_emit(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
+                    status, area);
     }
 }
 
@@ -845,7 +994,61 @@ size_t extract_polygons_workspace_bytes(int64_t V, int64_t B) {
     Carver cv(nullptr, 0);
     ExtractWs w;
     carve(cv, cap, cub_bytes_for(cap, 2 * kCoordBits + clip_bits(B)), w);
-    return cv.used();
+    const size_t a = cv.used(), b = extract_clip_workspace_bytes(0, B);
+    return a > b ? a : b;
+}
+
+// per-clip bucket path for polygons; FCFS_E_UNSUPPORTED (after its sync) if a clip has more than
+// kBucketCap vertices: the caller falls back to the general path
+static fcfs_status extract_polygon_clips(const int32_t *vx, const int32_t *vy, const int64_t *poly_ptr, int64_t P,
+                                         const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y,
+                                         int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                         int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    ClipWs W;
+    carve_clip(cv, 0, B, W);
+    if (!cv.fits()) {
+        set_error("fcfs_vertices_from_polygons: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.status, 0, B * sizeof(unsigned long long), s));
+    const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
+    static bool pattr = false;
+    if (!pattr) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_polygons_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kBucketCap * 12 + (kBucketMaxT + 2) * 4));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_polygons_bucket, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           100));
+        pattr = true;
+    }
+    // one CTA per clip (the look-back needs every predecessor clip's CTA dispatched before it)
+    k_clip_polygons_bucket<<<(unsigned)B, kBucketThreads, bsmem, s>>>(vx, vy, poly_ptr, P, clip_ptr, B, T, x, y, w,
+                                                                      cap, corner_ptr, W.status, area, W.err);
+    FCFS_CHECK_LAUNCH("k_clip_polygons_bucket");
+    int64_t Kh = 0;
+    int32_t errh = 0;
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, corner_ptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (errh & 8) {
+        set_error("a clip has more than %d vertices", kBucketCap);
+        return FCFS_E_UNSUPPORTED;
+    }
+    if (K_host) *K_host = Kh;
+    if (errh & 16) {
+        set_error("fcfs_vertices_from_polygons: a polygon edge is diagonal or of zero length");
+        return FCFS_E_INVALID;
+    }
+    if (errh & 1) {
+        set_error("fcfs_vertices_from_polygons: a vertex lies outside [0,T]^2");
+        return FCFS_E_RANGE;
+    }
+    if (Kh > cap) {
+        set_error("fcfs_vertices_from_polygons: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
+        return FCFS_E_CAPACITY;
+    }
+    return FCFS_OK;
 }
 
 // polygon vertex lists -> canonical corners: one raw corner per vertex (k_polygon_corners), then the
@@ -854,6 +1057,11 @@ fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, co
                              const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
                              int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
                              size_t ws_bytes, cudaStream_t s) {
+    if (T <= kBucketMaxT && B >= 1 && V > 0 && (clip_ptr != nullptr || V <= kBucketCap)) {
+        fcfs_status st = extract_polygon_clips(vx, vy, poly_ptr, P, clip_ptr, B, T, x, y, w, cap, corner_ptr, area,
+                                               K_host, ws, ws_bytes, s);
+        if (st != FCFS_E_UNSUPPORTED) return st;   // else: a clip is too large for the per-clip path
+    }
     const int64_t cap_raw = V < 1 ? 1 : V;
     if (cap_raw >= (int64_t(1) << 31)) {
         set_error("fcfs_vertices_from_polygons: %lld vertices exceed 2^31", (long long)V);

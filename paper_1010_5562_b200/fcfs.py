@@ -221,6 +221,31 @@ def vertices_from_polygons(vx, vy, poly_ptr, T, clip_ptr=None, stream=None):
     return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
 
 
+class PolygonsPlan:
+    """Pre-allocated outputs + workspace for repeated ``fcfs_vertices_from_polygons`` calls."""
+
+    def __init__(self, V, P, T, B=1, device="cuda"):
+        self.V, self.P, self.T, self.B = int(V), int(P), int(T), int(B)
+        self.cap = self.V
+        self.x = torch.empty(max(self.cap, 1), dtype=torch.int32, device=device)
+        self.y = torch.empty_like(self.x)
+        self.w = torch.empty_like(self.x)
+        self.corner_ptr = torch.empty(self.B + 1, dtype=torch.int64, device=device)
+        self.area = torch.empty(self.B, dtype=torch.int64, device=device)
+        self.ws = _ws(_lib.fcfs_polygons_workspace_bytes(self.V, self.P, self.B), device)
+        self.K = 0
+
+    def run(self, vx, vy, poly_ptr, clip_ptr=None, stream=None):
+        K = ctypes.c_int64(0)
+        st = _lib.fcfs_vertices_from_polygons(_ptr(vx), _ptr(vy), self.V, _ptr(poly_ptr), self.P, _ptr(clip_ptr),
+                                              self.B, self.T, _ptr(self.x), _ptr(self.y), _ptr(self.w), self.cap,
+                                              _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K), _ptr(self.ws),
+                                              self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_vertices_from_polygons")
+        self.K = K.value
+        return self.K
+
+
 class VerticesPlan:
     """Pre-allocated outputs + workspace for repeated ``fcfs_vertices_from_rects`` calls."""
 

@@ -412,7 +412,8 @@ def _sub_polys(ps, clips):
     return inputs._pack(polys, ps.T, per)
 
 
-@pytest.mark.parametrize("case", ["small", "many_clips", "one_big_clip", "long_polygons"])
+@pytest.mark.parametrize("case", ["small", "many_clips", "one_big_clip", "long_polygons", "long_perclip",
+                                  "oversized_clip_fallback"])
 def test_polygon_extraction_bit_exact(fcfs, case):
     if case == "small":
         ps = inputs.polygon_clips(0, clips=4, T=256, n_poly=20)
@@ -421,8 +422,13 @@ def test_polygon_extraction_bit_exact(fcfs, case):
     elif case == "one_big_clip":
         ps = inputs.polygon_clips(2, clips=1, T=65536, n_poly=40000, max_cols=8, size=3000)
         ps.clip_ptr = None
-    else:                                            # polygons of 100s of vertices (warp loops > 1 pass)
+    elif case == "long_polygons":                    # polygons of 100s of vertices, general path (T > 8191)
         ps = inputs.polygon_clips(3, clips=3, T=8192, n_poly=30, max_cols=200, size=20, collinear=0.5)
+    elif case == "long_perclip":                     # the same on the per-clip bucket path (T <= 8191)
+        ps = inputs.polygon_clips(5, clips=4, T=4096, n_poly=8, max_cols=200, size=10, collinear=0.5)
+    else:                                            # a clip of > 8192 vertices: per-clip path falls back
+        ps = inputs.polygon_clips(6, clips=3, T=2048, n_poly=700, max_cols=8, size=60)
+        assert np.diff(ps.poly_ptr[ps.clip_ptr]).max() > 8192
     e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
     g = _gpu_polys(fcfs, ps)
     _assert_extract_equal(g, e)
