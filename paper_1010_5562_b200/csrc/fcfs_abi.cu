@@ -165,6 +165,8 @@ struct CoeffWs {
     BucketWs bk;
     double *G;   // single clip: x-side bucket sums of one chunk, [tiles_x][cb][64 doubles or 128 tf32 rows]
     double *H;   // single clip, split precisions: y-side row twiddles of the chunk, [tiles_y][cb][128 rows]
+    void *fft;   // single FP64 clip: the lattice-FFT route's workspace (overlaps bk / G / H: one or the other)
+    size_t fft_bytes;
 };
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
@@ -188,12 +190,21 @@ static fcfs_status bucket_count_host(const BucketWs &bk, int64_t &nb, cudaStream
 
 // the row buckets (buckets.cu) feed the FP64 contraction; the tcgen05 kernels walk corners
 static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, int64_t K, int64_t B,
-                        fcfs_precision prec, bool single = false) {
+                        fcfs_precision prec, bool single = false, const FftPlan *fp = nullptr) {
     w.P = cv.take<double>(need_P ? (size_t)p.items * kTile * kTile : 1);
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
     w.G = nullptr;
     w.H = nullptr;
+    w.fft = nullptr;
+    w.fft_bytes = 0;
+    const size_t mark = cv.off;
+    if (fp) {   // the FFT route's region, overlapping the row-bucket path's (never both in one call)
+        w.fft_bytes = fft_route_ws_bytes(*fp);
+        w.fft = cv.take<char>(w.fft_bytes);
+    }
+    const size_t fft_end = cv.off;
+    cv.off = mark;
     const bool bucketed = prec == FCFS_FP64 || single;
     if (bucketed) carve_buckets(cv, K, B, w.bk);
     if (bucketed && single) {
@@ -203,6 +214,7 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
         // the y-side row twiddles of the chunk as well (64 doubles or 128 tf32 rows x 4 B per bucket)
         w.H = cv.take<double>((size_t)p.tiles_y * cb * kTile);
     }
+    if (cv.off < fft_end) cv.off = fft_end;
 }
 
 static fcfs_status resolve_rows(const fcfs_window *win, const fcfs_shard *shard, int32_t &m_lo, int32_t &m_hi) {
@@ -356,16 +368,17 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
 
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
                                    const fcfs_shard *shard) {
-    (void)T; (void)prec;
     if (check_window(win) != FCFS_OK) return 0;
     int32_t m_lo, m_hi;
     if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
     int64_t k = K;
     if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
+    FftPlan fp;
+    const bool fft = prec == FCFS_FP64 && valid_T(T) && fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, fp);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi, true), k, 1, prec, true);
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi, true), k, 1, prec, true, fft ? &fp : nullptr);
     return cv.used();
 }
 
@@ -398,9 +411,12 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     if (st != FCFS_OK) return st;
     GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
+    FftPlan fp;
+    const bool fft = prec == FCFS_FP64 && fft_route_plan(T, win->M, win->N, m_lo, m_hi, src.k_hi - src.k_lo, fp);
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi, true), src.k_hi - src.k_lo, 1, prec, true);
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi, true), src.k_hi - src.k_lo, 1, prec, true,
+                fft ? &fp : nullptr);
     if (!cv.fits()) { set_error("fcfs_coeffs: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     EpiArgs ea;
@@ -414,6 +430,14 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
         ea.area_dev = W.area;
     }
     src.bptr = W.bk.bptr; src.by = W.bk.by; src.clip_bptr = W.bk.clip_bptr; src.kend = K;
+    if (fft) {
+        // the lattice-FFT route (y-sorted corner lists; otherwise the row-bucket GEMM below)
+        StageScope scope(kStageContract, s);
+        bool sorted = false;
+        st = fft_route_prepare(y, src.k_lo, src.k_hi - src.k_lo, fp, W.fft, W.fft_bytes, sorted, s);
+        if (st != FCFS_OK) return st;
+        if (sorted) return fft_route_run(x, w, src.k_lo, fp, W.fft, W.fft_bytes, ea, F, s);
+    }
     bool fused = false;
     {
         StageScope scope(kStageContract, s);

@@ -1,0 +1,551 @@
+// fft_route.cu — SURVEY §8(f) NEXT-2: the lattice-FFT route for one clip in FP64.
+//
+// Step 4 of the paper evaluates the interior coefficients as DFTs of the sparse image f~_xy
+// (P:890-904).  The vertices lie on the integer lattice, so along y these are length-T
+// DFTs, which the paper's TD-FFT route does with FFTs.  For a window
+// |n| <= N this route computes, per row |m|:
+//
+//   G[m, y] = sum_{k: y_k = y (mod T)} w_k e^{-2 pi i m x_k / T}          (row sums over the corners)
+//   S[m, n] = sum_y G[m, y] e^{-2 pi i n y / T}                           (length-T DFT along y)
+//           = sum_{y1 < T1} e^{-2 pi i n y1 / T} Z_{y1}[n mod T2],  Z_{y1} = DFT_T2(G[m, y1 + T1 y2])
+//
+// with T = T1 T2 and T2 >= 2N+1 (an output-pruned two-step split: distinct n stay distinct mod T2),
+// i.e. T1 FFTs of length T2 and (2N+1) T1 twiddled adds per row, instead of the 2N R MACs per row of
+// the row-bucket GEMM (R = distinct rows, about T on configs[3] / [4]).  Then (Prop. 3)
+//
+//   F[m, n] = -S[m, n] / (4 pi^2 m n)                                     (Eq. Fkl, alpha case 4)
+//   F[m, 0] = i / (2 pi m T) * sum_k w_k y_k e^{-2 pi i m x_k / T}        (Eq. Fk0; raw y_k: a corner
+//             at y = T counts with T although its phase wraps to 0, reading A7)
+//   F[0, n] = i / (2 pi n T) * DFT(G0)[n],  G0[y] = sum_{k: y_k = y} w_k x_k   (Eq. F0l)
+//   F[0, 0] = area / T^2,  F[-m, -n] = conj F[m, n] (bitwise).
+//
+// Kernels: k_fr_yptr (CSR of the y-sorted corner list over y, sortedness flag), k_fr_table (the
+// two-level e^{-2 pi i p / T} table), k_fr_row0 / k_fr_rows (G, thread = one y and 8 consecutive m:
+// two exact-phase lookups per corner and the angle-addition recurrence over the 8 m; written in the
+// [row][y1][y2] order the FFT reads), k_fr_fft (CTA per row: the T1 sub-rows streamed by TMA bulk
+// copies into a double-buffered staging area, Stockham radix-16 FFT in shared memory, outer
+// twiddled accumulation in registers) and k_fr_epilogue (window / pupil / rows, axes, DC, mirror).
+// Error (FP64): the FFT's is ~log2(T2) u ||G||_2 per output and ||G|| <= sum |w| (the L1 bound B up
+// to the 1/(4 pi^2 m n) factor), far inside 1e-12 B.
+#include <cstdlib>
+#include <cstring>
+
+#include "coeff.cuh"
+
+namespace fcfs {
+namespace fr {
+
+constexpr int kThreads = 256;
+constexpr int kRowsPerThread = 8;   // consecutive m per k_fr_rows thread (recurrence length)
+constexpr int kMaxT2 = 4096;
+constexpr int kMaxNJ = kMaxT2 / kThreads;   // n values per thread in k_fr_fft (2N+1 <= T2)
+
+struct Geo {
+    int32_t T, T1, T2;
+    int32_t t1bits, t2bits;
+    int32_t lbits, nhi;     // two-level table of T: hi[p >> lbits] * lo[p & (2^lbits - 1)]
+    int32_t b2, nhi2;       // two-level table of T2
+};
+
+// e^{-2 pi i p / T} from a two-level table holding e^{-2 pi i j / T} (already conjugated)
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 tw_ldg(const double2 *tab, uint32_t p, int lbits, int nhi) {
+    return cmul(__ldg(tab + (p >> lbits)), __ldg(tab + nhi + (p & ((1u << lbits) - 1u))));
+}
+__device__ __forceinline__ double2 tw_smem(const double2 *tab, uint32_t p, int lbits, int nhi) {
+    return cmul(tab[p >> lbits], tab[nhi + (p & ((1u << lbits) - 1u))]);
+}
+
+// two-level table of e^{-2 pi i j / L}: entries [0, nhi) = hi steps (j << lbits), [nhi, nhi + 2^lbits) = lo
+__device__ __forceinline__ double2 tw_entry(int i, int L, int lbits, int nhi) {
+    const int64_t j = i < nhi ? ((int64_t)i << lbits) : (int64_t)(i - nhi);
+    double s, c;
+    sincospi(2.0 * (double)j / (double)L, &s, &c);
+    return make_double2(c, -s);
+}
+
+__global__ void k_fr_table(double2 *tab, Geo g) {
+    const int n = g.nhi + (1 << g.lbits);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        tab[i] = tw_entry(i, g.T, g.lbits, g.nhi);
+}
+
+// yptr[v] = #corners in [k_lo, k_hi) with y < v, v in [0, T+1]; flag = 1 if y decreases somewhere
+__global__ void k_fr_yptr(const int32_t *__restrict__ y, int64_t k_lo, int64_t K, int32_t T, int32_t *yptr,
+                          int32_t *flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= (int64_t)T + 1; v += stride) {
+        int64_t lo = 0, hi = K;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (y[k_lo + mid] < v) lo = mid + 1; else hi = mid;
+        }
+        yptr[v] = (int32_t)lo;
+    }
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; k < K; k += stride)
+        if (y[k_lo + k] < y[k_lo + k - 1]) *flag = 1;
+}
+
+// y of linear index t in the [y1][y2] order: t = y1 T2 + y2, y = y1 + T1 y2
+__device__ __forceinline__ int32_t y_of(int64_t t, const Geo &g) {
+    return (int32_t)((t >> g.t2bits) + ((t & (g.T2 - 1)) << g.t1bits));
+}
+
+// the x-weighted row G0[y] = sum_{y_k = y mod T} w_k x_k (exact integer sum), as complex (row 0)
+__global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
+                          const int32_t *__restrict__ yptr, Geo g, double2 *Gd) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t yv = y_of(t, g);
+        long long s = 0;
+        for (int32_t k = yptr[yv]; k < yptr[yv + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
+        if (yv == 0)
+            for (int32_t k = yptr[g.T]; k < yptr[g.T + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
+        Gd[t] = make_double2((double)s, 0.0);
+    }
+}
+
+// rows m = m0 .. m0+7 (m0 = m_first + 8 blockIdx.y, up to m_last) of G, written to Gd rows
+// row0_off + 8 blockIdx.y + j; GT[row] = the y = T run's share of G[m, 0] (for the axis sum)
+__global__ void __launch_bounds__(kThreads)
+k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
+          const int32_t *__restrict__ yptr, const double2 *__restrict__ tab, Geo g, int32_t m_first,
+          int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
+    const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.y;
+    const uint32_t mask = (uint32_t)g.T - 1u;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t yv = y_of(t, g);
+        double2 acc[kRowsPerThread], accT[kRowsPerThread];
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) { acc[j] = make_double2(0.0, 0.0); accT[j] = acc[j]; }
+        auto run = [&](int32_t k0, int32_t k1, double2 (&a)[kRowsPerThread]) {
+            for (int32_t k = k0; k < k1; ++k) {
+                const uint32_t xx = (uint32_t)x[k_lo + k];
+                const double ww = (double)w[k_lo + k];
+                double2 e = tw_ldg(tab, ((uint32_t)m0 * xx) & mask, g.lbits, g.nhi);
+                const double2 step = tw_ldg(tab, xx & mask, g.lbits, g.nhi);
+                a[0].x = fma(ww, e.x, a[0].x); a[0].y = fma(ww, e.y, a[0].y);
+#pragma unroll
+                for (int j = 1; j < kRowsPerThread; ++j) {
+                    e = cmul(e, step);
+                    a[j].x = fma(ww, e.x, a[j].x); a[j].y = fma(ww, e.y, a[j].y);
+                }
+            }
+        };
+        run(yptr[yv], yptr[yv + 1], acc);
+        if (yv == 0) run(yptr[g.T], yptr[g.T + 1], accT);
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) {
+            if (m0 + j > m_last) break;
+            const int64_t row = row_off + kRowsPerThread * (int64_t)blockIdx.y + j;
+            Gd[row * g.T + t] = cadd(acc[j], accT[j]);
+            if (yv == 0) GT[row] = accT[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- the per-row FFT
+
+__device__ __forceinline__ double2 w16(int q) {   // e^{-2 pi i q / 16}, q in [0, 8)
+    const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+    switch (q) {
+        case 0: return make_double2(1.0, 0.0);
+        case 1: return make_double2(c1, -s1);
+        case 2: return make_double2(h, -h);
+        case 3: return make_double2(s1, -c1);
+        case 4: return make_double2(0.0, -1.0);
+        case 5: return make_double2(-s1, -c1);
+        case 6: return make_double2(-h, -h);
+        default: return make_double2(-c1, -s1);
+    }
+}
+
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
+
+// radix-4 butterfly in place: (a0..a3) -> DFT_4
+__device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, double2 &a3) {
+    const double2 b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3), b3 = mul_mi(csub(a1, a3));
+    a0 = cadd(b0, b2); a2 = csub(b0, b2); a1 = cadd(b1, b3); a3 = csub(b1, b3);
+}
+
+// in-register DFT of size R (natural order in and out): R = 2, 4, or the four-step split
+// R = 4 x 4 (16) / 2 x 4 (8) with the W_R^{r0 k1} twiddles as constants
+template <int R>
+__device__ __forceinline__ void dft(double2 (&v)[R]) {
+    if constexpr (R == 2) {
+        const double2 a = v[0];
+        v[0] = cadd(a, v[1]); v[1] = csub(a, v[1]);
+    } else if constexpr (R == 4) {
+        bfly4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        // x[r0 + 2 r1]: DFT_4 over r1 for r0 = 0, 1; twiddle W8^{r0 k1}; DFT_2 over r0
+        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        bfly4(e[0], e[1], e[2], e[3]);
+        bfly4(o[0], o[1], o[2], o[3]);
+        o[1] = cmul(o[1], w16(2)); o[2] = mul_mi(o[2]); o[3] = cmul(o[3], w16(6));
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) { v[k1] = cadd(e[k1], o[k1]); v[k1 + 4] = csub(e[k1], o[k1]); }
+    } else {
+        static_assert(R == 16, "radix");
+        // x[r0 + 4 r1]: DFT_4 over r1 for each r0; twiddle W16^{r0 k1}; DFT_4 over r0 -> X[k1 + 4 k2]
+        double2 y[4][4];
+#pragma unroll
+        for (int r0 = 0; r0 < 4; ++r0) {
+            y[r0][0] = v[r0]; y[r0][1] = v[r0 + 4]; y[r0][2] = v[r0 + 8]; y[r0][3] = v[r0 + 12];
+            bfly4(y[r0][0], y[r0][1], y[r0][2], y[r0][3]);
+        }
+        y[1][1] = cmul(y[1][1], w16(1)); y[1][2] = cmul(y[1][2], w16(2)); y[1][3] = cmul(y[1][3], w16(3));
+        y[2][1] = cmul(y[2][1], w16(2)); y[2][2] = mul_mi(y[2][2]);         y[2][3] = cmul(y[2][3], w16(6));
+        y[3][1] = cmul(y[3][1], w16(3)); y[3][2] = cmul(y[3][2], w16(6));
+        y[3][3] = cmul(y[3][3], make_double2(-w16(1).x, -w16(1).y));       // W16^9 = -W16^1
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            bfly4(y[0][k1], y[1][k1], y[2][k1], y[3][k1]);
+            v[k1] = y[0][k1]; v[k1 + 4] = y[1][k1]; v[k1 + 8] = y[2][k1]; v[k1 + 12] = y[3][k1];
+        }
+    }
+}
+
+// one Stockham pass of radix R over length L (Ns = product of the previous radices); the first pass
+// (Ns == 1) also accumulates the coordinate-weighted sum sum_y y G[y] of this sub-row (axis column)
+template <int R>
+__device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, int L, int Ns, const double2 *tw2,
+                                              const Geo &g, int y1, double2 &ax) {
+    const int nb = L / R;
+    for (int i = threadIdx.x; i < nb; i += kThreads) {
+        const int k = i & (Ns - 1);
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[i + r * nb];
+        if (Ns == 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double yy = (double)(y1 + ((i + r * nb) << g.t1bits));
+                ax.x = fma(yy, v[r].x, ax.x); ax.y = fma(yy, v[r].y, ax.y);
+            }
+        } else {
+            const int sc = L / (Ns * R);
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw_smem(tw2, (uint32_t)(r * k * sc), g.b2, g.nhi2));
+        }
+        dft<R>(v);
+        const int j = (i - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[j + r * Ns] = v[r];
+    }
+}
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// CTA per row of Gd (chunk-local r; global row r_first + r): X[n] = S[m, n] for n in [-N, N];
+// thread owns n = -N + threadIdx.x + 256 j, j < kNJ (2N+1 <= 256 kNJ)
+template <int kNJ>
+__global__ void __launch_bounds__(kThreads, 1)
+k_fr_fft(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT, Geo g,
+         int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
+    extern __shared__ __align__(16) double2 fsm[];
+    double2 *S0 = fsm, *S1 = fsm + g.T2, *Fb = fsm + 2 * g.T2;
+    double2 *tw2 = fsm + 3 * g.T2;
+    __shared__ __align__(8) unsigned long long bar[2];
+    __shared__ double2 red[kThreads / 32];
+    const int r = blockIdx.x;
+    const double2 *grow = Gd + (int64_t)r * g.T;
+    const int ntw = g.nhi2 + (1 << g.b2);
+    for (int i = threadIdx.x; i < ntw; i += kThreads) tw2[i] = tw_entry(i, g.T2, g.b2, g.nhi2);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t bytes = (uint32_t)g.T2 * 16u;
+    auto issue = [&](int y1) {
+        double2 *dst = (y1 & 1) ? S1 : S0;
+        const uint32_t b = su32(&bar[y1 & 1]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(dst)), "l"(grow + (int64_t)y1 * g.T2), "r"(bytes), "r"(b)
+                     : "memory");
+    };
+    if (threadIdx.x == 0) issue(0);
+    const int nn = 2 * N + 1;
+    double2 X[kNJ];
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) X[j] = make_double2(0.0, 0.0);
+    double2 ax = make_double2(0.0, 0.0);
+    const uint32_t maskT = (uint32_t)g.T - 1u;
+    const int lead = g.t2bits & 3;   // first pass radix 2^lead (if any), then radix-16 passes
+    for (int y1 = 0; y1 < g.T1; ++y1) {
+        if (threadIdx.x == 0 && y1 + 1 < g.T1) issue(y1 + 1);
+        {   // wait for this sub-row
+            const uint32_t b = su32(&bar[y1 & 1]), par = (uint32_t)((y1 >> 1) & 1);
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                             " selp.u32 %0, 1, 0, p;\n}"
+                             : "=r"(ok) : "r"(b), "r"(par) : "memory");
+        }
+        double2 *cur = (y1 & 1) ? S1 : S0, *oth = Fb;
+        int Ns = 1;
+        if (lead) {
+            if (lead == 1) stockham_pass<2>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
+            else if (lead == 2) stockham_pass<4>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
+            else stockham_pass<8>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
+            Ns <<= lead;
+            __syncthreads();
+            double2 *t = cur; cur = oth; oth = t;
+        }
+        for (; Ns < g.T2; Ns <<= 4) {
+            stockham_pass<16>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
+            __syncthreads();
+            double2 *t = cur; cur = oth; oth = t;
+        }
+        // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) {
+            const int o = threadIdx.x + j * kThreads;
+            if (o < nn) {
+                const int n = o - N;
+                const double2 z = cur[n >= 0 ? n : n + g.T2];
+                const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
+                X[j] = cadd(X[j], cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z));
+            }
+        }
+        // the staging buffer of this sub-row is refilled by TMA two iterations on: order this
+        // thread's generic accesses before that async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+    }
+    const int rg = r_first + r;
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+        const int o = threadIdx.x + j * kThreads;
+        if (o < nn) Xs[(int64_t)rg * nn + o] = X[j];
+    }
+    // axis: block sum of sum_y y G[y] (+ T x the y = T run, which sits in slot y = 0)
+    for (int o = 16; o > 0; o >>= 1) {
+        ax.x += __shfl_xor_sync(0xffffffffu, ax.x, o);
+        ax.y += __shfl_xor_sync(0xffffffffu, ax.y, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i]);
+        const double2 gt = GT[r];
+        Axis[rg] = make_double2(fma((double)g.T, gt.x, a.x), fma((double)g.T, gt.y, a.y));
+    }
+}
+
+// outputs of rows m in [m_lo, m_hi]: grid.x = rows; Xs row of |m|: 0 -> row 0 (if present), else
+// row0 + (|m| - mA)
+__global__ void k_fr_epilogue(const double2 *__restrict__ Xs, const double2 *__restrict__ Axis, EpiArgs ea,
+                              int32_t row0, int32_t mA, void *F) {
+    const int m = ea.m_lo + (int)blockIdx.x;
+    if (m > ea.m_hi) return;
+    const double pi = 3.141592653589793238462643383279502884;
+    const int64_t area = ea.area_dev ? ea.area_dev[0] : ea.area_host;
+    const double dc = (double)area / ((double)ea.T * (double)ea.T);
+    const int nn = 2 * ea.N + 1;
+    int64_t off;
+    int nlo, nhi;
+    if (ea.layout == FCFS_LAYOUT_PUPIL) {
+        off = 0;
+        for (int mm = -ea.M; mm < m; ++mm) {
+            const int c = pupil_nmax(mm, ea.r2, ea.N);
+            off += c < 0 ? 0 : 2 * c + 1;
+        }
+        const int c = pupil_nmax(m, ea.r2, ea.N);
+        if (c < 0) return;
+        nlo = -c; nhi = c;
+    } else {
+        off = (int64_t)(m - ea.m_lo) * nn;
+        nlo = -ea.N; nhi = ea.N;
+    }
+    for (int n = nlo + (int)threadIdx.x; n <= nhi; n += blockDim.x) {
+        double2 v = make_double2(0.0, 0.0);
+        const bool keep = !(ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0 &&
+                            (double)m * (double)m + (double)n * (double)n > ea.r2);
+        if (keep) {
+            if (m == 0 && n == 0) {
+                v = make_double2(dc, 0.0);
+            } else {
+                int mp = m, np = n;
+                const bool neg = (m < 0) || (m == 0 && n < 0);
+                if (neg) { mp = -m; np = -n; }
+                double re, im;
+                if (mp == 0) {              // F[0, n] = i S0[n] / (2 pi n T)
+                    const double2 s = Xs[np + ea.N];
+                    const double d = 2.0 * pi * (double)np * (double)ea.T;
+                    re = -s.y / d; im = s.x / d;
+                } else {
+                    const int64_t row = row0 + (mp - mA);
+                    if (np == 0) {          // F[m, 0] = i (sum_k w y E_x) / (2 pi m T)
+                        const double2 s = Axis[row];
+                        const double d = 2.0 * pi * (double)mp * (double)ea.T;
+                        re = -s.y / d; im = s.x / d;
+                    } else {                // F[m, n] = -S[m, n] / (4 pi^2 m n)
+                        const double2 s = Xs[row * nn + np + ea.N];
+                        const double d = -4.0 * pi * pi * (double)mp * (double)np;
+                        re = s.x / d; im = s.y / d;
+                    }
+                }
+                v = make_double2(re, neg ? -im : im);
+            }
+        }
+        store_out(F, off + (n - nlo), v, ea.out_f32);
+    }
+}
+
+}  // namespace fr
+
+// ---------------------------------------------------------------- host side
+
+static int ilog2_exact(int64_t v) {
+    int b = 0;
+    while ((int64_t(1) << b) < v) ++b;
+    return b;
+}
+
+static fr::Geo make_geo(int32_t T, int32_t T2) {
+    fr::Geo g;
+    g.T = T; g.T2 = T2; g.T1 = T / T2;
+    g.t2bits = ilog2_exact(T2); g.t1bits = ilog2_exact(g.T1);
+    const int tb = ilog2_exact(T);
+    g.lbits = (tb + 1) / 2;
+    g.nhi = (int32_t)((T + (1 << g.lbits) - 1) >> g.lbits);
+    g.b2 = (g.t2bits + 1) / 2;
+    g.nhi2 = (int32_t)((T2 + (1 << g.b2) - 1) >> g.b2);
+    return g;
+}
+
+// geometry + cost model; FCFS_ROUTE=fft / gemm (environment) forces the choice where possible
+bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, FftPlan &p) {
+    p = FftPlan{};
+    if (T < 64 || (T & (T - 1)) != 0 || K <= 0 || K >= (int64_t(1) << 31)) return false;
+    int64_t T2 = 64;
+    while (T2 < 2 * (int64_t)N + 1) T2 <<= 1;
+    if (T2 > fr::kMaxT2 || T2 > T) return false;
+    p.T = T; p.T2 = (int32_t)T2; p.N = N;
+    p.row0 = (m_lo <= 0 && 0 <= m_hi) ? 1 : 0;
+    int32_t a, b;
+    if (m_lo > 0) { a = m_lo; b = m_hi; }
+    else if (m_hi < 0) { a = -m_hi; b = -m_lo; }
+    else { a = 1; b = (-m_lo > m_hi) ? -m_lo : m_hi; }
+    p.mA = a;
+    p.nm = b >= a ? b - a + 1 : 0;
+    p.nr = p.row0 + p.nm;
+    // rows per chunk: the G rows of a chunk (16 T bytes each) within ~4.5 GB, a multiple of 8
+    int64_t rc = (int64_t)(4.5e9 / (16.0 * (double)T));
+    rc = rc / 8 * 8;
+    if (rc < 8) rc = 8;
+    p.rc = rc;
+    const char *env = getenv("FCFS_ROUTE");
+    if (env && !strcmp(env, "gemm")) return false;
+    if (env && !strcmp(env, "fft")) return true;
+    const double lg = log2((double)T2);
+    const double fft = (double)p.nr * ((double)T * (5.0 * lg + 16.0) + (double)(T / T2) * (2.0 * N + 1) * 8.0) +
+                       9.0 * (double)K * (double)p.nm;
+    const double rows = (double)(K < (int64_t)T + 1 ? K : (int64_t)T + 1);
+    const double gemm = 8.0 * (double)p.nm * (double)N * rows;
+    return fft * 2.0 < gemm;
+}
+
+struct FftWs {
+    int32_t *yptr, *flag;
+    double2 *tab, *Gd, *GT, *Xs, *Axis;
+};
+
+static void carve_fft(Carver &cv, const FftPlan &p, FftWs &w) {
+    const fr::Geo g = make_geo(p.T, p.T2);
+    const int64_t rc = p.rc < p.nr ? p.rc : p.nr;
+    w.yptr = cv.take<int32_t>((size_t)p.T + 2);
+    w.flag = cv.take<int32_t>(1);
+    w.tab = cv.take<double2>((size_t)g.nhi + ((size_t)1 << g.lbits));
+    w.Gd = cv.take<double2>((size_t)(rc > 0 ? rc : 1) * (size_t)p.T);
+    w.GT = cv.take<double2>((size_t)(rc > 0 ? rc : 1));
+    w.Xs = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1) * (size_t)(2 * p.N + 1));
+    w.Axis = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1));
+}
+
+size_t fft_route_ws_bytes(const FftPlan &p) {
+    Carver cv(nullptr, 0);
+    FftWs w;
+    carve_fft(cv, p, w);
+    return cv.used();
+}
+
+// y-CSR of the corner range and whether its y are non-decreasing (one stream sync)
+fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const FftPlan &p, void *ws, size_t ws_bytes,
+                              bool &sorted, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    FftWs W;
+    carve_fft(cv, p, W);
+    if (!cv.fits()) { set_error("fft route: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.flag, 0, sizeof(int32_t), s));
+    int64_t n = (int64_t)p.T + 2 > K ? (int64_t)p.T + 2 : K;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    fr::k_fr_yptr<<<(unsigned)blocks, 256, 0, s>>>(y, k_lo, K, p.T, W.yptr, W.flag);
+    FCFS_CHECK_LAUNCH("k_fr_yptr");
+    int32_t f = 0;
+    FCFS_TRY_CUDA(cudaMemcpyAsync(&f, W.flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+    sorted = f == 0;
+    return FCFS_OK;
+}
+
+fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, const FftPlan &p, void *ws,
+                          size_t ws_bytes, const EpiArgs &ea, void *F, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    FftWs W;
+    carve_fft(cv, p, W);
+    if (!cv.fits()) { set_error("fft route: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    const fr::Geo g = make_geo(p.T, p.T2);
+    const int ntab = g.nhi + (1 << g.lbits);
+    fr::k_fr_table<<<(unsigned)((ntab + 255) / 256), 256, 0, s>>>(W.tab, g);
+    FCFS_CHECK_LAUNCH("k_fr_table");
+    const size_t fsmem = (size_t)(3 * p.T2 + g.nhi2 + (1 << g.b2)) * sizeof(double2);
+    const int nj = (2 * p.N + 1 + fr::kThreads - 1) / fr::kThreads;
+    auto fk = nj <= 4 ? fr::k_fr_fft<4> : nj <= 8 ? fr::k_fr_fft<8> : nj <= 12 ? fr::k_fr_fft<12> : fr::k_fr_fft<16>;
+    const int ki = nj <= 4 ? 0 : nj <= 8 ? 1 : nj <= 12 ? 2 : 3;
+    static size_t fattr[4] = {0, 0, 0, 0};
+    if (fsmem > fattr[ki]) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+        fattr[ki] = fsmem;
+    }
+    int64_t tblocks = p.T / 256;
+    if (tblocks > 512) tblocks = 512;
+    if (tblocks < 1) tblocks = 1;
+    for (int64_t c0 = 0; c0 < p.nr; c0 += p.rc) {
+        const int64_t c1 = c0 + p.rc < p.nr ? c0 + p.rc : p.nr;
+        FCFS_TRY_CUDA(cudaMemsetAsync(W.GT, 0, sizeof(double2) * (size_t)(c1 - c0), s));
+        if (c0 == 0 && p.row0) {
+            fr::k_fr_row0<<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, g, W.Gd);
+            FCFS_CHECK_LAUNCH("k_fr_row0");
+        }
+        const int64_t ra = c0 > p.row0 ? c0 : p.row0;   // first |m| >= 1 row of the chunk
+        if (ra < c1) {
+            const int32_t m_first = p.mA + (int32_t)(ra - p.row0), m_last = p.mA + (int32_t)(c1 - 1 - p.row0);
+            const int64_t rb = (m_last - m_first + fr::kRowsPerThread) / fr::kRowsPerThread;
+            dim3 grid((unsigned)tblocks, (unsigned)rb);
+            fr::k_fr_rows<<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.tab, g, m_first, m_last,
+                                                        (int32_t)(ra - c0), W.Gd, W.GT);
+            FCFS_CHECK_LAUNCH("k_fr_rows");
+        }
+        fk<<<(unsigned)(c1 - c0), fr::kThreads, fsmem, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0, W.Xs,
+                                                                      W.Axis);
+        FCFS_CHECK_LAUNCH("k_fr_fft");
+    }
+    const int rows = ea.m_hi - ea.m_lo + 1;
+    if (rows > 0) {
+        fr::k_fr_epilogue<<<(unsigned)rows, 128, 0, s>>>(W.Xs, W.Axis, ea, p.row0, p.mA, F);
+        FCFS_CHECK_LAUNCH("k_fr_epilogue");
+    }
+    return FCFS_OK;
+}
+
+}  // namespace fcfs
