@@ -20,8 +20,8 @@
 //   F[0, 0] = area / T^2,  F[-m, -n] = conj F[m, n] (bitwise).
 //
 // Kernels: k_fr_yptr (CSR of the y-sorted corner list over y, sortedness flag), k_fr_table (the
-// two-level e^{-2 pi i p / T} table), k_fr_row0 / k_fr_rows (G, thread = one y and 8 consecutive m:
-// two exact-phase lookups per corner and the angle-addition recurrence over the 8 m; written in the
+// two-level e^{-2 pi i p / T} table), k_fr_row0 / k_fr_rows (G, thread = one y and 16 consecutive m:
+// two exact-phase lookups per corner and the angle-addition recurrence over 16 m; written in the
 // [row][y1][y2] order the FFT reads), k_fr_fft (CTA per row: the T1 sub-rows streamed by TMA bulk
 // copies into a double-buffered staging area, Stockham radix-16 FFT in shared memory, outer
 // twiddled accumulation in registers) and k_fr_epilogue (window / pupil / rows, axes, DC, mirror).
@@ -36,7 +36,7 @@ namespace fcfs {
 namespace fr {
 
 constexpr int kThreads = 256;
-constexpr int kRowsPerThread = 8;   // consecutive m per k_fr_rows thread (recurrence length)
+constexpr int kRowsPerThread = 16;  // consecutive m per k_fr_rows thread (recurrence length)
 constexpr int kMaxT2 = 4096;
 constexpr int kMaxNJ = kMaxT2 / kThreads;   // n values per thread in k_fr_fft (2N+1 <= T2)
 
@@ -108,42 +108,97 @@ __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restri
     }
 }
 
-// rows m = m0 .. m0+7 (m0 = m_first + 8 blockIdx.y, up to m_last) of G, written to Gd rows
-// row0_off + 8 blockIdx.y + j; GT[row] = the y = T run's share of G[m, 0] (for the axis sum)
-__global__ void __launch_bounds__(kThreads)
+// rows m = m0 .. m0+15 (m0 = m_first + 16 blockIdx.y, up to m_last) of G, written to Gd rows
+// row_off + 16 blockIdx.y + j.  Two corners per iteration (independent recurrence chains).
+__global__ void __launch_bounds__(kThreads, 2)
 k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
           const int32_t *__restrict__ yptr, const double2 *__restrict__ tab, Geo g, int32_t m_first,
-          int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
+          int32_t m_last, int32_t row_off, double2 *Gd) {
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.y;
     const uint32_t mask = (uint32_t)g.T - 1u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t yv = y_of(t, g);
-        double2 acc[kRowsPerThread], accT[kRowsPerThread];
+        double2 acc[kRowsPerThread];
 #pragma unroll
-        for (int j = 0; j < kRowsPerThread; ++j) { acc[j] = make_double2(0.0, 0.0); accT[j] = acc[j]; }
-        auto run = [&](int32_t k0, int32_t k1, double2 (&a)[kRowsPerThread]) {
-            for (int32_t k = k0; k < k1; ++k) {
-                const uint32_t xx = (uint32_t)x[k_lo + k];
-                const double ww = (double)w[k_lo + k];
-                double2 e = tw_ldg(tab, ((uint32_t)m0 * xx) & mask, g.lbits, g.nhi);
-                const double2 step = tw_ldg(tab, xx & mask, g.lbits, g.nhi);
-                a[0].x = fma(ww, e.x, a[0].x); a[0].y = fma(ww, e.y, a[0].y);
+        for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
+        auto run = [&](int32_t k0, int32_t k1) {
+            int32_t k = k0;
+            for (; k + 1 < k1; k += 2) {
+                const uint32_t xa = (uint32_t)__ldg(x + k_lo + k), xb = (uint32_t)__ldg(x + k_lo + k + 1);
+                const double wa = (double)__ldg(w + k_lo + k), wb = (double)__ldg(w + k_lo + k + 1);
+                double2 ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                double2 eb = tw_ldg(tab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
+                const double2 sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi), sb = tw_ldg(tab, xb & mask, g.lbits, g.nhi);
 #pragma unroll
-                for (int j = 1; j < kRowsPerThread; ++j) {
-                    e = cmul(e, step);
-                    a[j].x = fma(ww, e.x, a[j].x); a[j].y = fma(ww, e.y, a[j].y);
+                for (int j = 0; j < kRowsPerThread; ++j) {
+                    if (j) { ea = cmul(ea, sa); eb = cmul(eb, sb); }
+                    acc[j].x = fma(wa, ea.x, fma(wb, eb.x, acc[j].x));
+                    acc[j].y = fma(wa, ea.y, fma(wb, eb.y, acc[j].y));
+                }
+            }
+            if (k < k1) {
+                const uint32_t xa = (uint32_t)__ldg(x + k_lo + k);
+                const double wa = (double)__ldg(w + k_lo + k);
+                double2 ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                const double2 sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
+#pragma unroll
+                for (int j = 0; j < kRowsPerThread; ++j) {
+                    if (j) ea = cmul(ea, sa);
+                    acc[j].x = fma(wa, ea.x, acc[j].x);
+                    acc[j].y = fma(wa, ea.y, acc[j].y);
                 }
             }
         };
-        run(yptr[yv], yptr[yv + 1], acc);
-        if (yv == 0) run(yptr[g.T], yptr[g.T + 1], accT);
+        run(yptr[yv], yptr[yv + 1]);   // the y = T run (phase of row 0) is added by k_fr_rowsT
 #pragma unroll
         for (int j = 0; j < kRowsPerThread; ++j) {
             if (m0 + j > m_last) break;
-            const int64_t row = row_off + kRowsPerThread * (int64_t)blockIdx.y + j;
-            Gd[row * g.T + t] = cadd(acc[j], accT[j]);
-            if (yv == 0) GT[row] = accT[j];
+            Gd[(row_off + kRowsPerThread * (int64_t)blockIdx.y + j) * g.T + t] = acc[j];
         }
+    }
+}
+
+// the y = T run (its phase wraps to row y = 0; the axis sum weights it with T): block per 16 rows,
+// threads over the run's corners (the run can hold thousands of corners: the lines clipped at the
+// tile edge), block reduction; GT[row] = its share, added into G[m, 0]
+__global__ void __launch_bounds__(kThreads)
+k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
+           const int32_t *__restrict__ yptr, const double2 *__restrict__ tab, Geo g, int32_t m_first,
+           int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
+    __shared__ double2 red[kThreads / 32][kRowsPerThread];
+    const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.x;
+    const uint32_t mask = (uint32_t)g.T - 1u;
+    double2 acc[kRowsPerThread];
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
+    for (int32_t k = yptr[g.T] + (int32_t)threadIdx.x; k < yptr[g.T + 1]; k += kThreads) {
+        const uint32_t xa = (uint32_t)x[k_lo + k];
+        const double wa = (double)w[k_lo + k];
+        double2 e = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+        const double2 st = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
+#pragma unroll
+        for (int j = 0; j < kRowsPerThread; ++j) {
+            if (j) e = cmul(e, st);
+            acc[j].x = fma(wa, e.x, acc[j].x);
+            acc[j].y = fma(wa, e.y, acc[j].y);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) {
+        for (int o = 16; o > 0; o >>= 1) {
+            acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, o);
+            acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, o);
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = acc[j];
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (j < kRowsPerThread && m0 + j <= m_last) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i][j]);
+        const int64_t row = row_off + kRowsPerThread * (int64_t)blockIdx.x + j;
+        GT[row] = a;
+        Gd[row * g.T] = cadd(Gd[row * g.T], a);
     }
 }
 
@@ -211,6 +266,11 @@ __device__ __forceinline__ void dft(double2 (&v)[R]) {
 
 // one Stockham pass of radix R over length L (Ns = product of the previous radices); the first pass
 // (Ns == 1) also accumulates the coordinate-weighted sum sum_y y G[y] of this sub-row (axis column)
+// shared-memory FFT buffers hold element i at i + i/16 (one pad slot per 16): the first pass's
+// radix-16 stores (stride 16 elements) then fall on distinct banks; the TMA-filled staging input of
+// the first pass is unpadded
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
 template <int R>
 __device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, int L, int Ns, const double2 *tw2,
                                               const Geo &g, int y1, double2 &ax) {
@@ -219,7 +279,7 @@ __device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, i
         const int k = i & (Ns - 1);
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = in[i + r * nb];
+        for (int r = 0; r < R; ++r) v[r] = in[Ns == 1 ? i + r * nb : pad(i + r * nb)];
         if (Ns == 1) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -234,7 +294,7 @@ __device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, i
         dft<R>(v);
         const int j = (i - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[j + r * Ns] = v[r];
+        for (int r = 0; r < R; ++r) out[pad(j + r * Ns)] = v[r];
     }
 }
 
@@ -247,8 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_fr_fft(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT, Geo g,
          int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
     extern __shared__ __align__(16) double2 fsm[];
-    double2 *S0 = fsm, *S1 = fsm + g.T2, *Fb = fsm + 2 * g.T2;
-    double2 *tw2 = fsm + 3 * g.T2;
+    const int LP = g.T2 + g.T2 / 16;   // padded buffer length
+    double2 *S0 = fsm, *S1 = fsm + LP, *Fb = fsm + 2 * LP;
+    double2 *tw2 = fsm + 3 * LP;
     __shared__ __align__(8) unsigned long long bar[2];
     __shared__ double2 red[kThreads / 32];
     const int r = blockIdx.x;
@@ -309,7 +370,7 @@ k_fr_fft(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const d
             const int o = threadIdx.x + j * kThreads;
             if (o < nn) {
                 const int n = o - N;
-                const double2 z = cur[n >= 0 ? n : n + g.T2];
+                const double2 z = cur[pad(n >= 0 ? n : n + g.T2)];
                 const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
                 X[j] = cadd(X[j], cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z));
             }
@@ -508,7 +569,7 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
     const int ntab = g.nhi + (1 << g.lbits);
     fr::k_fr_table<<<(unsigned)((ntab + 255) / 256), 256, 0, s>>>(W.tab, g);
     FCFS_CHECK_LAUNCH("k_fr_table");
-    const size_t fsmem = (size_t)(3 * p.T2 + g.nhi2 + (1 << g.b2)) * sizeof(double2);
+    const size_t fsmem = (size_t)(3 * (p.T2 + p.T2 / 16) + g.nhi2 + (1 << g.b2)) * sizeof(double2);
     const int nj = (2 * p.N + 1 + fr::kThreads - 1) / fr::kThreads;
     auto fk = nj <= 4 ? fr::k_fr_fft<4> : nj <= 8 ? fr::k_fr_fft<8> : nj <= 12 ? fr::k_fr_fft<12> : fr::k_fr_fft<16>;
     const int ki = nj <= 4 ? 0 : nj <= 8 ? 1 : nj <= 12 ? 2 : 3;
@@ -533,8 +594,11 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
             const int64_t rb = (m_last - m_first + fr::kRowsPerThread) / fr::kRowsPerThread;
             dim3 grid((unsigned)tblocks, (unsigned)rb);
             fr::k_fr_rows<<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.tab, g, m_first, m_last,
-                                                        (int32_t)(ra - c0), W.Gd, W.GT);
+                                                        (int32_t)(ra - c0), W.Gd);
             FCFS_CHECK_LAUNCH("k_fr_rows");
+            fr::k_fr_rowsT<<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.tab, g, m_first, m_last,
+                                                                 (int32_t)(ra - c0), W.Gd, W.GT);
+            FCFS_CHECK_LAUNCH("k_fr_rowsT");
         }
         fk<<<(unsigned)(c1 - c0), fr::kThreads, fsmem, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0, W.Xs,
                                                                       W.Axis);
