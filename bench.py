@@ -188,12 +188,13 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def traffic_for(cfg, prec):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu --set full
-    capture (profiles/traffic.json), or None when no capture matches this config / precision."""
+def traffic_for(cfg, prec, route=""):
+    """dram read+write bytes per launch of the dominant kernel (or, for the FFT route, of the contract
+    stage's kernels) from the committed ncu --set full captures (profiles/traffic.json), or None when
+    no capture matches this config / precision / route."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return t.get(f"{cfg}/{prec}")
+        return t.get(f"{cfg}/{prec}" + (f"/{route}" if route else ""))
     except Exception:
         return None
 
@@ -336,41 +337,64 @@ def main():
     peaks, src = load_peaks()
     c_ms, c_n = stages["contract"]
     c_ms_launch = c_ms / max(c_n, 1)
-    # inner dimension of the contraction: corners (batched tcgen05 kernels) or row buckets (FP64, and
-    # split-TF32 on one clip: Step 4 row structure, fcfs_row_buckets with the cap fcfs_coeffs uses)
-    if prec == "fp64" or wl.B == 1:
-        rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
-        Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
-        k_inner = "row buckets"
+    fft_route = (wl.B == 1 and world == 1 and
+                 fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec) == 1)
+    if fft_route:
+        # lattice-FFT route (NEXT-2, FP64 CUDA cores): algorithmic work of the contract stage =
+        # G rows (one complex rotation + real-weighted complex MAC per corner and row: 10 flop) +
+        # the T1 length-T2 FFTs per row (5 T2 log2 T2) + the outer twiddled sum (8 flop per n and y1)
+        T2 = 64
+        while T2 < 2 * wl.N + 1:
+            T2 *= 2
+        T1 = wl.T // T2
+        rows = wl.M + 1
+        alg_flops = (10.0 * K * wl.M + rows * T1 * (5.0 * T2 * math.log2(T2) + 8.0 * (2 * wl.N + 1)))
+        achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
+        clocks = clk.summary()
+        pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        peak = pk["dfma_tflops"]
+        peak_note = ("FP64 CUDA-core DFMA measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json); "
+                     f"the stage = k_fr_rows + k_fr_fft + small kernels, T2={T2}, T1={T1}")
+        bound = "alu"
+        k_inner = "lattice-FFT route"
+        Kc = np.array([float(K)])
     else:
-        Kc = np.diff(cptr_h).astype(np.float64)
-        k_inner = "corners"
-    alg_flops = float(np.sum(8.0 * wl.M * wl.N * Kc))      # real quadrant GEMM 2M x 2N x K_inner, 2 flop/MAC
-    achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
-    clocks = clk.summary()
-    if prec == "tf32x3":
-        tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
-        peak = tf32 / 3.0
-        peak_note = (f"TF32 dense = {src} bf16 {peaks['bf16_tflops']} x (1.1/2.25 nominal ratio) = {tf32:.1f} "
-                     f"TF/s, / 3 (split-TF32: 3 TF32 MMAs per FP32-accurate product)")
-        bound = "tensor"
-    elif prec == "f16x3":
-        peak = peaks["bf16_tflops"] / 3.0
-        peak_note = (f"FP16 dense = {src} bf16 {peaks['bf16_tflops']} TF/s (same nominal rate), / 3 "
-                     f"(split-FP16: 3 FP16 MMAs per FP32-accurate product)")
-        bound = "tensor"
-    else:
-        try:
-            peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_m16n8k16_tflops"]
-            peak_note = "FP64 tensor (DMMA m16n8k16) measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json)"
-        except Exception:
-            mhz = peaks.get("sm_max_mhz", 1965.0)
-            peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
-            peak_note = f"FP64: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived)"
-        bound = "tensor"
+        # inner dimension of the contraction: corners (batched tcgen05 kernels) or row buckets (FP64, and
+        # split-TF32 on one clip: Step 4 row structure, fcfs_row_buckets with the cap fcfs_coeffs uses)
+        if prec == "fp64" or wl.B == 1:
+            rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
+            Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
+            k_inner = "row buckets"
+        else:
+            Kc = np.diff(cptr_h).astype(np.float64)
+            k_inner = "corners"
+        alg_flops = float(np.sum(8.0 * wl.M * wl.N * Kc))      # real quadrant GEMM 2M x 2N x K_inner, 2 flop/MAC
+        achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
+        clocks = clk.summary()
+        if prec == "tf32x3":
+            tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+            peak = tf32 / 3.0
+            peak_note = (f"TF32 dense = {src} bf16 {peaks['bf16_tflops']} x (1.1/2.25 nominal ratio) = {tf32:.1f} "
+                         f"TF/s, / 3 (split-TF32: 3 TF32 MMAs per FP32-accurate product)")
+            bound = "tensor"
+        elif prec == "f16x3":
+            peak = peaks["bf16_tflops"] / 3.0
+            peak_note = (f"FP16 dense = {src} bf16 {peaks['bf16_tflops']} TF/s (same nominal rate), / 3 "
+                         f"(split-FP16: 3 FP16 MMAs per FP32-accurate product)")
+            bound = "tensor"
+        else:
+            try:
+                peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_m16n8k16_tflops"]
+                peak_note = "FP64 tensor (DMMA m16n8k16) measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json)"
+            except Exception:
+                mhz = peaks.get("sm_max_mhz", 1965.0)
+                peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
+                peak_note = f"FP64: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived)"
+            bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec),
-            "kernel": "k_gemm_" + prec, "k_inner": f"{k_inner}: {int(Kc.sum())}",
+            "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else ""),
+            "kernel": ("contract stage (k_fr_rows + k_fr_fft)" if fft_route else "k_gemm_" + prec),
+            "k_inner": f"{k_inner}: {int(Kc.sum())}",
             "alg_flops_per_launch": alg_flops,
             "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
             "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()}}

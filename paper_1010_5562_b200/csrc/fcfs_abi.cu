@@ -382,6 +382,17 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     return cv.used();
 }
 
+int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
+                          const fcfs_shard *shard) {
+    if (!valid_T(T) || check_window(win) != FCFS_OK || prec != FCFS_FP64) return 0;
+    int32_t m_lo, m_hi;
+    if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
+    int64_t k = K;
+    if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
+    FftPlan fp;
+    return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, fp) ? 1 : 0;
+}
+
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
                         const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard, void *F, void *ws,
                         size_t ws_bytes, void *stream) {

@@ -287,9 +287,17 @@ __device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, i
                 ax.x = fma(yy, v[r].x, ax.x); ax.y = fma(yy, v[r].y, ax.y);
             }
         } else {
-            const int sc = L / (Ns * R);
+            // W^r, W = e^{-2 pi i k / (Ns R)}: one table lookup, then powers by multiplication (no
+            // per-r shared-memory lookups: those conflicted on the bank groups)
+            double2 pw[R];
+            pw[1] = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw_smem(tw2, (uint32_t)(r * k * sc), g.b2, g.nhi2));
+            for (int r = 2; r < R; ++r) {   // shallow product tree: W^r = W^(2^b) W^(r - 2^b)
+                const int hb = (r & (r - 1)) == 0 ? r / 2 : (1 << (31 - __clz(r)));
+                pw[r] = cmul(pw[hb], pw[r - hb]);
+            }
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], pw[r]);
         }
         dft<R>(v);
         const int j = (i - k) * R + k;

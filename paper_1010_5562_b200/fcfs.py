@@ -69,6 +69,8 @@ _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _
 _lib.fcfs_vertices_from_polygons.restype = _i32
 _lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
 _lib.fcfs_coeffs_workspace_bytes.restype = _sz
+_lib.fcfs_coeffs_route.argtypes = [_i64, _i32, _WP, _i32, _SP]
+_lib.fcfs_coeffs_route.restype = _i32
 _lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _P, _P, _sz, _P]
 _lib.fcfs_coeffs.restype = _i32
 _lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32]
@@ -90,7 +92,8 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_coeffs", "fcfs_batched_workspace_bytes", "fcfs_coeffs_batched", "fcfs_window_size",
             "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
-            "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons"]
+            "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
+            "fcfs_coeffs_route"]
 STAGES = ("extract", "contract", "epilogue")
 
 
@@ -302,6 +305,13 @@ class CoeffsPlan:
                               self.prec, sp, _ptr(out), _ptr(self.ws), self.ws.numel(), _stream(stream))
         _check(st, "fcfs_coeffs")
         return out
+
+
+def coeffs_route(K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None):
+    """1 if fcfs_coeffs takes the lattice-FFT route for these sizes (y-sorted corners), else 0."""
+    win = make_window(M, N, r2, layout)
+    sp = ctypes.byref(shard) if shard is not None else None
+    return int(_lib.fcfs_coeffs_route(int(K), int(T), ctypes.byref(win), _PREC[prec], sp))
 
 
 def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, stream=None):
