@@ -123,9 +123,20 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
         for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
         auto run = [&](int32_t k0, int32_t k1) {
             int32_t k = k0;
+            // corner coordinates / weights one pair ahead (their loads overlap the current pair's math)
+            uint32_t nxa = 0, nxb = 0;
+            int32_t nwa = 0, nwb = 0;
+            if (k + 1 < k1) {
+                nxa = (uint32_t)__ldg(x + k_lo + k); nxb = (uint32_t)__ldg(x + k_lo + k + 1);
+                nwa = __ldg(w + k_lo + k); nwb = __ldg(w + k_lo + k + 1);
+            }
             for (; k + 1 < k1; k += 2) {
-                const uint32_t xa = (uint32_t)__ldg(x + k_lo + k), xb = (uint32_t)__ldg(x + k_lo + k + 1);
-                const double wa = (double)__ldg(w + k_lo + k), wb = (double)__ldg(w + k_lo + k + 1);
+                const uint32_t xa = nxa, xb = nxb;
+                const double wa = (double)nwa, wb = (double)nwb;
+                if (k + 3 < k1) {
+                    nxa = (uint32_t)__ldg(x + k_lo + k + 2); nxb = (uint32_t)__ldg(x + k_lo + k + 3);
+                    nwa = __ldg(w + k_lo + k + 2); nwb = __ldg(w + k_lo + k + 3);
+                }
                 double2 ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
                 double2 eb = tw_ldg(tab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
                 const double2 sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi), sb = tw_ldg(tab, xb & mask, g.lbits, g.nhi);
