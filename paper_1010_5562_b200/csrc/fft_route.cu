@@ -420,6 +420,116 @@ k_fr_fft(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const d
     }
 }
 
+// In-place Stockham pass (all reads, barrier, all writes) of radix R over length L <= R * kThreads;
+// the first pass (Ns == 1) reads the unpadded TMA layout and accumulates sum_y y G[y] (axis)
+template <int R>
+__device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const double2 *tw2, const Geo &g, int y1,
+                                             double2 &ax) {
+    const int nb = L / R;
+    const int i = threadIdx.x;
+    double2 v[R];
+    const int k = i & (Ns - 1);
+    if (i < nb) {   // read and transform; the barrier orders every read before any write
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = buf[Ns == 1 ? i + r * nb : pad(i + r * nb)];
+        if (Ns == 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double yy = (double)(y1 + ((i + r * nb) << g.t1bits));
+                ax.x = fma(yy, v[r].x, ax.x); ax.y = fma(yy, v[r].y, ax.y);
+            }
+        } else {
+            const double2 w1 = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
+            double2 wr = w1;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                v[r] = cmul(v[r], wr);
+                if (r + 1 < R) wr = cmul(wr, w1);
+            }
+        }
+        dft<R>(v);
+    }
+    __syncthreads();
+    if (i < nb) {
+        const int j = (i - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad(j + r * Ns)] = v[r];
+    }
+    __syncthreads();
+}
+
+// CTA per row (2 CTAs / SM): one padded work buffer that the TMA bulk copy fills with the next
+// sub-row and the passes transform in place; X[n] accumulates in shared memory
+__global__ void __launch_bounds__(kThreads, 2)
+k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT, Geo g,
+          int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
+    extern __shared__ __align__(16) double2 fsm[];
+    const int LP = g.T2 + g.T2 / 16;
+    const int nn = 2 * N + 1;
+    double2 *buf = fsm, *X = fsm + LP, *tw2 = fsm + LP + nn;
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 red[kThreads / 32];
+    const int r = blockIdx.x;
+    const double2 *grow = Gd + (int64_t)r * g.T;
+    const int ntw = g.nhi2 + (1 << g.b2);
+    for (int i = threadIdx.x; i < ntw; i += kThreads) tw2[i] = tw_entry(i, g.T2, g.b2, g.nhi2);
+    for (int o = threadIdx.x; o < nn; o += kThreads) X[o] = make_double2(0.0, 0.0);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t bytes = (uint32_t)g.T2 * 16u;
+    double2 ax = make_double2(0.0, 0.0);
+    const uint32_t maskT = (uint32_t)g.T - 1u;
+    const int lead = g.t2bits & 3;
+    for (int y1 = 0; y1 < g.T1; ++y1) {
+        if (threadIdx.x == 0) {
+            const uint32_t b = su32(&bar);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(buf)), "l"(grow + (int64_t)y1 * g.T2), "r"(bytes), "r"(b)
+                         : "memory");
+        }
+        {
+            const uint32_t b = su32(&bar), par = (uint32_t)(y1 & 1);
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                             " selp.u32 %0, 1, 0, p;\n}"
+                             : "=r"(ok) : "r"(b), "r"(par) : "memory");
+        }
+        int Ns = 1;
+        if (lead == 1) { pass_inplace<2>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 2; }
+        else if (lead == 2) { pass_inplace<4>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 4; }
+        else if (lead == 3) { pass_inplace<8>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 8; }
+        for (; Ns < g.T2; Ns <<= 4) pass_inplace<16>(buf, g.T2, Ns, tw2, g, y1, ax);
+        // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
+        for (int o = threadIdx.x; o < nn; o += kThreads) {
+            const int n = o - N;
+            const double2 z = buf[pad(n >= 0 ? n : n + g.T2)];
+            const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
+            X[o] = cadd(X[o], cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+    }
+    const int rg = r_first + r;
+    for (int o = threadIdx.x; o < nn; o += kThreads) Xs[(int64_t)rg * nn + o] = X[o];
+    for (int o = 16; o > 0; o >>= 1) {
+        ax.x += __shfl_xor_sync(0xffffffffu, ax.x, o);
+        ax.y += __shfl_xor_sync(0xffffffffu, ax.y, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i]);
+        const double2 gt = GT[r];
+        Axis[rg] = make_double2(fma((double)g.T, gt.x, a.x), fma((double)g.T, gt.y, a.y));
+    }
+}
+
 // outputs of rows m in [m_lo, m_hi]: grid.x = rows; Xs row of |m|: 0 -> row 0 (if present), else
 // row0 + (|m| - mA)
 __global__ void k_fr_epilogue(const double2 *__restrict__ Xs, const double2 *__restrict__ Axis, EpiArgs ea,
@@ -597,6 +707,15 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
         FCFS_TRY_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
         fattr[ki] = fsmem;
     }
+    const size_t fsmem2 = (size_t)((p.T2 + p.T2 / 16) + (2 * p.N + 1) + g.nhi2 + (1 << g.b2)) * sizeof(double2);
+    static size_t fattr2 = 0;
+    if (fsmem2 > fattr2) {
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem2));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        fattr2 = fsmem2;
+    }
+    const char *fv = getenv("FCFS_FFT_KERNEL");
+    const bool v1 = fv && !strcmp(fv, "1");
     int64_t tblocks = p.T / 256;
     if (tblocks > 512) tblocks = 512;
     if (tblocks < 1) tblocks = 1;
@@ -619,8 +738,11 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
                                                                  (int32_t)(ra - c0), W.Gd, W.GT);
             FCFS_CHECK_LAUNCH("k_fr_rowsT");
         }
-        fk<<<(unsigned)(c1 - c0), fr::kThreads, fsmem, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0, W.Xs,
-                                                                      W.Axis);
+        if (v1)
+            fk<<<(unsigned)(c1 - c0), fr::kThreads, fsmem, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0, W.Xs, W.Axis);
+        else
+            fr::k_fr_fft2<<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0,
+                                                                             W.Xs, W.Axis);
         FCFS_CHECK_LAUNCH("k_fr_fft");
     }
     const int rows = ea.m_hi - ea.m_lo + 1;
