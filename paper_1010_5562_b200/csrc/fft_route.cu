@@ -38,7 +38,6 @@ namespace fr {
 constexpr int kThreads = 256;
 constexpr int kRowsPerThread = 16;  // consecutive m per k_fr_rows thread (recurrence length)
 constexpr int kMaxT2 = 4096;
-constexpr int kMaxNJ = kMaxT2 / kThreads;   // n values per thread in k_fr_fft (2N+1 <= T2)
 
 struct Geo {
     int32_t T, T1, T2;
@@ -90,16 +89,49 @@ __global__ void k_fr_yptr(const int32_t *__restrict__ y, int64_t k_lo, int64_t K
         if (y[k_lo + k] < y[k_lo + k - 1]) *flag = 1;
 }
 
-// y of linear index t in the [y1][y2] order: t = y1 T2 + y2, y = y1 + T1 y2
-__device__ __forceinline__ int32_t y_of(int64_t t, const Geo &g) {
-    return (int32_t)((t >> g.t2bits) + ((t & (g.T2 - 1)) << g.t1bits));
+// Load balance of the row-sum kernels: within each sub-row y1 the T2 columns y2 (y = y1 + T1 y2) are
+// stored in decreasing order of their corner-run length, so the 32 lanes of a warp get runs of about
+// the same length (the y runs of the configs are uneven: a warp of 32 consecutive y2 idles ~45% of its
+// lanes).  perm[y1 T2 + pos] = y2 and pinv[y1 T2 + y2] = pos (int16: T2 <= 4096); the FFT reads each
+// sub-row back in y2 order through pinv.  G[m, y] does not depend on the thread that computes it, so
+// the order changes no result bit (counting sort by run length with shared atomics, not stable).
+__global__ void __launch_bounds__(kThreads)
+k_fr_perm(const int32_t *__restrict__ yptr, Geo g, int16_t *perm, int16_t *pinv) {
+    constexpr int kBins = 64;   // run lengths >= 63 share the first bin
+    __shared__ int32_t cnt[kBins];
+    const int y1 = blockIdx.x;
+    if (threadIdx.x < kBins) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int y2 = threadIdx.x; y2 < g.T2; y2 += kThreads) {
+        const int32_t y = y1 + (y2 << g.t1bits);
+        const int len = yptr[y + 1] - yptr[y];
+        atomicAdd(&cnt[kBins - 1 - min(len, kBins - 1)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < kBins; ++b) { const int c = cnt[b]; cnt[b] = run; run += c; }
+    }
+    __syncthreads();
+    for (int y2 = threadIdx.x; y2 < g.T2; y2 += kThreads) {
+        const int32_t y = y1 + (y2 << g.t1bits);
+        const int len = yptr[y + 1] - yptr[y];
+        const int pos = atomicAdd(&cnt[kBins - 1 - min(len, kBins - 1)], 1);
+        perm[(int64_t)y1 * g.T2 + pos] = (int16_t)y2;
+        pinv[(int64_t)y1 * g.T2 + y2] = (int16_t)pos;
+    }
+}
+
+// y of storage index t = y1 T2 + pos (pos = the permuted column of sub-row y1): y = y1 + T1 perm[t]
+__device__ __forceinline__ int32_t y_of(int64_t t, const Geo &g, const int16_t *__restrict__ perm) {
+    return (int32_t)((t >> g.t2bits) + ((int32_t)(uint16_t)__ldg(perm + t) << g.t1bits));
 }
 
 // the x-weighted row G0[y] = sum_{y_k = y mod T} w_k x_k (exact integer sum), as complex (row 0)
 __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-                          const int32_t *__restrict__ yptr, Geo g, double2 *Gd) {
+                          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, Geo g, double2 *Gd) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t yv = y_of(t, g);
+        const int32_t yv = y_of(t, g, perm);
         long long s = 0;
         for (int32_t k = yptr[yv]; k < yptr[yv + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
         if (yv == 0)
@@ -112,12 +144,12 @@ __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restri
 // row_off + 16 blockIdx.y + j.  Two corners per iteration (independent recurrence chains).
 __global__ void __launch_bounds__(kThreads, 2)
 k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-          const int32_t *__restrict__ yptr, const double2 *__restrict__ tab, Geo g, int32_t m_first,
-          int32_t m_last, int32_t row_off, double2 *Gd) {
+          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, const double2 *__restrict__ tab, Geo g,
+          int32_t m_first, int32_t m_last, int32_t row_off, double2 *Gd) {
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.y;
     const uint32_t mask = (uint32_t)g.T - 1u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t yv = y_of(t, g);
+        const int32_t yv = y_of(t, g, perm);
         double2 acc[kRowsPerThread];
 #pragma unroll
         for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
@@ -174,8 +206,8 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
 // tile edge), block reduction; GT[row] = its share, added into G[m, 0]
 __global__ void __launch_bounds__(kThreads)
 k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-           const int32_t *__restrict__ yptr, const double2 *__restrict__ tab, Geo g, int32_t m_first,
-           int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
+           const int32_t *__restrict__ yptr, const int16_t *__restrict__ pinv, const double2 *__restrict__ tab, Geo g,
+           int32_t m_first, int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
     __shared__ double2 red[kThreads / 32][kRowsPerThread];
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.x;
     const uint32_t mask = (uint32_t)g.T - 1u;
@@ -209,7 +241,8 @@ k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t
         for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i][j]);
         const int64_t row = row_off + kRowsPerThread * (int64_t)blockIdx.x + j;
         GT[row] = a;
-        Gd[row * g.T] = cadd(Gd[row * g.T], a);
+        const int64_t t0 = (uint16_t)pinv[0];   // storage slot of y = 0
+        Gd[row * g.T + t0] = cadd(Gd[row * g.T + t0], a);
     }
 }
 
@@ -275,163 +308,24 @@ __device__ __forceinline__ void dft(double2 (&v)[R]) {
     }
 }
 
-// one Stockham pass of radix R over length L (Ns = product of the previous radices); the first pass
-// (Ns == 1) also accumulates the coordinate-weighted sum sum_y y G[y] of this sub-row (axis column)
 // shared-memory FFT buffers hold element i at i + i/16 (one pad slot per 16): the first pass's
-// radix-16 stores (stride 16 elements) then fall on distinct banks; the TMA-filled staging input of
-// the first pass is unpadded
+// radix-16 stores (stride 16 elements) then fall on distinct banks; the TMA-filled input is unpadded
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 
-template <int R>
-__device__ __forceinline__ void stockham_pass(const double2 *in, double2 *out, int L, int Ns, const double2 *tw2,
-                                              const Geo &g, int y1, double2 &ax) {
-    const int nb = L / R;
-    for (int i = threadIdx.x; i < nb; i += kThreads) {
-        const int k = i & (Ns - 1);
-        double2 v[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = in[Ns == 1 ? i + r * nb : pad(i + r * nb)];
-        if (Ns == 1) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double yy = (double)(y1 + ((i + r * nb) << g.t1bits));
-                ax.x = fma(yy, v[r].x, ax.x); ax.y = fma(yy, v[r].y, ax.y);
-            }
-        } else {
-            // W^r, W = e^{-2 pi i k / (Ns R)}: one table lookup, then powers by multiplication (no
-            // per-r shared-memory lookups: those conflicted on the bank groups)
-            double2 pw[R];
-            pw[1] = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
-#pragma unroll
-            for (int r = 2; r < R; ++r) {   // shallow product tree: W^r = W^(2^b) W^(r - 2^b)
-                const int hb = (r & (r - 1)) == 0 ? r / 2 : (1 << (31 - __clz(r)));
-                pw[r] = cmul(pw[hb], pw[r - hb]);
-            }
-#pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], pw[r]);
-        }
-        dft<R>(v);
-        const int j = (i - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) out[pad(j + r * Ns)] = v[r];
-    }
-}
-
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// CTA per row of Gd (chunk-local r; global row r_first + r): X[n] = S[m, n] for n in [-N, N];
-// thread owns n = -N + threadIdx.x + 256 j, j < kNJ (2N+1 <= 256 kNJ)
-template <int kNJ>
-__global__ void __launch_bounds__(kThreads, 1)
-k_fr_fft(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT, Geo g,
-         int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
-    extern __shared__ __align__(16) double2 fsm[];
-    const int LP = g.T2 + g.T2 / 16;   // padded buffer length
-    double2 *S0 = fsm, *S1 = fsm + LP, *Fb = fsm + 2 * LP;
-    double2 *tw2 = fsm + 3 * LP;
-    __shared__ __align__(8) unsigned long long bar[2];
-    __shared__ double2 red[kThreads / 32];
-    const int r = blockIdx.x;
-    const double2 *grow = Gd + (int64_t)r * g.T;
-    const int ntw = g.nhi2 + (1 << g.b2);
-    for (int i = threadIdx.x; i < ntw; i += kThreads) tw2[i] = tw_entry(i, g.T2, g.b2, g.nhi2);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t bytes = (uint32_t)g.T2 * 16u;
-    auto issue = [&](int y1) {
-        double2 *dst = (y1 & 1) ? S1 : S0;
-        const uint32_t b = su32(&bar[y1 & 1]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(su32(dst)), "l"(grow + (int64_t)y1 * g.T2), "r"(bytes), "r"(b)
-                     : "memory");
-    };
-    if (threadIdx.x == 0) issue(0);
-    const int nn = 2 * N + 1;
-    double2 X[kNJ];
-#pragma unroll
-    for (int j = 0; j < kNJ; ++j) X[j] = make_double2(0.0, 0.0);
-    double2 ax = make_double2(0.0, 0.0);
-    const uint32_t maskT = (uint32_t)g.T - 1u;
-    const int lead = g.t2bits & 3;   // first pass radix 2^lead (if any), then radix-16 passes
-    for (int y1 = 0; y1 < g.T1; ++y1) {
-        if (threadIdx.x == 0 && y1 + 1 < g.T1) issue(y1 + 1);
-        {   // wait for this sub-row
-            const uint32_t b = su32(&bar[y1 & 1]), par = (uint32_t)((y1 >> 1) & 1);
-            uint32_t ok = 0;
-            while (!ok)
-                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                             " selp.u32 %0, 1, 0, p;\n}"
-                             : "=r"(ok) : "r"(b), "r"(par) : "memory");
-        }
-        double2 *cur = (y1 & 1) ? S1 : S0, *oth = Fb;
-        int Ns = 1;
-        if (lead) {
-            if (lead == 1) stockham_pass<2>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
-            else if (lead == 2) stockham_pass<4>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
-            else stockham_pass<8>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
-            Ns <<= lead;
-            __syncthreads();
-            double2 *t = cur; cur = oth; oth = t;
-        }
-        for (; Ns < g.T2; Ns <<= 4) {
-            stockham_pass<16>(cur, oth, g.T2, Ns, tw2, g, y1, ax);
-            __syncthreads();
-            double2 *t = cur; cur = oth; oth = t;
-        }
-        // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
-#pragma unroll
-        for (int j = 0; j < kNJ; ++j) {
-            const int o = threadIdx.x + j * kThreads;
-            if (o < nn) {
-                const int n = o - N;
-                const double2 z = cur[pad(n >= 0 ? n : n + g.T2)];
-                const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
-                X[j] = cadd(X[j], cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z));
-            }
-        }
-        // the staging buffer of this sub-row is refilled by TMA two iterations on: order this
-        // thread's generic accesses before that async-proxy write
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-    }
-    const int rg = r_first + r;
-#pragma unroll
-    for (int j = 0; j < kNJ; ++j) {
-        const int o = threadIdx.x + j * kThreads;
-        if (o < nn) Xs[(int64_t)rg * nn + o] = X[j];
-    }
-    // axis: block sum of sum_y y G[y] (+ T x the y = T run, which sits in slot y = 0)
-    for (int o = 16; o > 0; o >>= 1) {
-        ax.x += __shfl_xor_sync(0xffffffffu, ax.x, o);
-        ax.y += __shfl_xor_sync(0xffffffffu, ax.y, o);
-    }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double2 a = make_double2(0.0, 0.0);
-        for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i]);
-        const double2 gt = GT[r];
-        Axis[rg] = make_double2(fma((double)g.T, gt.x, a.x), fma((double)g.T, gt.y, a.y));
-    }
-}
 
 // In-place Stockham pass (all reads, barrier, all writes) of radix R over length L <= R * kThreads;
 // the first pass (Ns == 1) reads the unpadded TMA layout and accumulates sum_y y G[y] (axis)
 template <int R>
 __device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const double2 *tw2, const Geo &g, int y1,
-                                             double2 &ax) {
+                                             double2 &ax, const int16_t *pv) {
     const int nb = L / R;
     const int i = threadIdx.x;
     double2 v[R];
     const int k = i & (Ns - 1);
     if (i < nb) {   // read and transform; the barrier orders every read before any write
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = buf[Ns == 1 ? i + r * nb : pad(i + r * nb)];
+        for (int r = 0; r < R; ++r) v[r] = buf[Ns == 1 ? (int)(uint16_t)pv[i + r * nb] : pad(i + r * nb)];
         if (Ns == 1) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -461,12 +355,13 @@ __device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const 
 // CTA per row (2 CTAs / SM): one padded work buffer that the TMA bulk copy fills with the next
 // sub-row and the passes transform in place; X[n] accumulates in shared memory
 __global__ void __launch_bounds__(kThreads, 2)
-k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT, Geo g,
-          int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
+k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT,
+          const int16_t *__restrict__ pinv, Geo g, int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
     extern __shared__ __align__(16) double2 fsm[];
     const int LP = g.T2 + g.T2 / 16;
     const int nn = 2 * N + 1;
     double2 *buf = fsm, *X = fsm + LP, *tw2 = fsm + LP + nn;
+    int16_t *pv = (int16_t *)(tw2 + g.nhi2 + (1 << g.b2));   // the sub-row's pinv (T2 x int16)
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double2 red[kThreads / 32];
     const int r = blockIdx.x;
@@ -479,16 +374,20 @@ k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const uint32_t bytes = (uint32_t)g.T2 * 16u;
+    const uint32_t bytes = (uint32_t)g.T2 * 16u, pbytes = (uint32_t)g.T2 * 2u;
     double2 ax = make_double2(0.0, 0.0);
     const uint32_t maskT = (uint32_t)g.T - 1u;
     const int lead = g.t2bits & 3;
     for (int y1 = 0; y1 < g.T1; ++y1) {
         if (threadIdx.x == 0) {
             const uint32_t b = su32(&bar);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes + pbytes)
+                         : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(su32(buf)), "l"(grow + (int64_t)y1 * g.T2), "r"(bytes), "r"(b)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(pv)), "l"(pinv + (int64_t)y1 * g.T2), "r"(pbytes), "r"(b)
                          : "memory");
         }
         {
@@ -500,10 +399,10 @@ k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const 
                              : "=r"(ok) : "r"(b), "r"(par) : "memory");
         }
         int Ns = 1;
-        if (lead == 1) { pass_inplace<2>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 2; }
-        else if (lead == 2) { pass_inplace<4>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 4; }
-        else if (lead == 3) { pass_inplace<8>(buf, g.T2, Ns, tw2, g, y1, ax); Ns = 8; }
-        for (; Ns < g.T2; Ns <<= 4) pass_inplace<16>(buf, g.T2, Ns, tw2, g, y1, ax);
+        if (lead == 1) { pass_inplace<2>(buf, g.T2, Ns, tw2, g, y1, ax, pv); Ns = 2; }
+        else if (lead == 2) { pass_inplace<4>(buf, g.T2, Ns, tw2, g, y1, ax, pv); Ns = 4; }
+        else if (lead == 3) { pass_inplace<8>(buf, g.T2, Ns, tw2, g, y1, ax, pv); Ns = 8; }
+        for (; Ns < g.T2; Ns <<= 4) pass_inplace<16>(buf, g.T2, Ns, tw2, g, y1, ax, pv);
         // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
         for (int o = threadIdx.x; o < nn; o += kThreads) {
             const int n = o - N;
@@ -646,6 +545,7 @@ bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi,
 
 struct FftWs {
     int32_t *yptr, *flag;
+    int16_t *perm, *pinv;
     double2 *tab, *Gd, *GT, *Xs, *Axis;
 };
 
@@ -654,6 +554,8 @@ static void carve_fft(Carver &cv, const FftPlan &p, FftWs &w) {
     const int64_t rc = p.rc < p.nr ? p.rc : p.nr;
     w.yptr = cv.take<int32_t>((size_t)p.T + 2);
     w.flag = cv.take<int32_t>(1);
+    w.perm = cv.take<int16_t>((size_t)p.T);
+    w.pinv = cv.take<int16_t>((size_t)p.T);
     w.tab = cv.take<double2>((size_t)g.nhi + ((size_t)1 << g.lbits));
     w.Gd = cv.take<double2>((size_t)(rc > 0 ? rc : 1) * (size_t)p.T);
     w.GT = cv.take<double2>((size_t)(rc > 0 ? rc : 1));
@@ -698,24 +600,16 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
     const int ntab = g.nhi + (1 << g.lbits);
     fr::k_fr_table<<<(unsigned)((ntab + 255) / 256), 256, 0, s>>>(W.tab, g);
     FCFS_CHECK_LAUNCH("k_fr_table");
-    const size_t fsmem = (size_t)(3 * (p.T2 + p.T2 / 16) + g.nhi2 + (1 << g.b2)) * sizeof(double2);
-    const int nj = (2 * p.N + 1 + fr::kThreads - 1) / fr::kThreads;
-    auto fk = nj <= 4 ? fr::k_fr_fft<4> : nj <= 8 ? fr::k_fr_fft<8> : nj <= 12 ? fr::k_fr_fft<12> : fr::k_fr_fft<16>;
-    const int ki = nj <= 4 ? 0 : nj <= 8 ? 1 : nj <= 12 ? 2 : 3;
-    static size_t fattr[4] = {0, 0, 0, 0};
-    if (fsmem > fattr[ki]) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-        fattr[ki] = fsmem;
-    }
-    const size_t fsmem2 = (size_t)((p.T2 + p.T2 / 16) + (2 * p.N + 1) + g.nhi2 + (1 << g.b2)) * sizeof(double2);
+    fr::k_fr_perm<<<(unsigned)g.T1, fr::kThreads, 0, s>>>(W.yptr, g, W.perm, W.pinv);
+    FCFS_CHECK_LAUNCH("k_fr_perm");
+    const size_t fsmem2 = (size_t)((p.T2 + p.T2 / 16) + (2 * p.N + 1) + g.nhi2 + (1 << g.b2)) * sizeof(double2) +
+                          (size_t)p.T2 * sizeof(int16_t);
     static size_t fattr2 = 0;
     if (fsmem2 > fattr2) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem2));
         FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         fattr2 = fsmem2;
     }
-    const char *fv = getenv("FCFS_FFT_KERNEL");
-    const bool v1 = fv && !strcmp(fv, "1");
     int64_t tblocks = p.T / 256;
     if (tblocks > 512) tblocks = 512;
     if (tblocks < 1) tblocks = 1;
@@ -723,7 +617,7 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
         const int64_t c1 = c0 + p.rc < p.nr ? c0 + p.rc : p.nr;
         FCFS_TRY_CUDA(cudaMemsetAsync(W.GT, 0, sizeof(double2) * (size_t)(c1 - c0), s));
         if (c0 == 0 && p.row0) {
-            fr::k_fr_row0<<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, g, W.Gd);
+            fr::k_fr_row0<<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, W.perm, g, W.Gd);
             FCFS_CHECK_LAUNCH("k_fr_row0");
         }
         const int64_t ra = c0 > p.row0 ? c0 : p.row0;   // first |m| >= 1 row of the chunk
@@ -731,17 +625,14 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
             const int32_t m_first = p.mA + (int32_t)(ra - p.row0), m_last = p.mA + (int32_t)(c1 - 1 - p.row0);
             const int64_t rb = (m_last - m_first + fr::kRowsPerThread) / fr::kRowsPerThread;
             dim3 grid((unsigned)tblocks, (unsigned)rb);
-            fr::k_fr_rows<<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.tab, g, m_first, m_last,
+            fr::k_fr_rows<<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.perm, W.tab, g, m_first, m_last,
                                                         (int32_t)(ra - c0), W.Gd);
             FCFS_CHECK_LAUNCH("k_fr_rows");
-            fr::k_fr_rowsT<<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.tab, g, m_first, m_last,
+            fr::k_fr_rowsT<<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.pinv, W.tab, g, m_first, m_last,
                                                                  (int32_t)(ra - c0), W.Gd, W.GT);
             FCFS_CHECK_LAUNCH("k_fr_rowsT");
         }
-        if (v1)
-            fk<<<(unsigned)(c1 - c0), fr::kThreads, fsmem, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0, W.Xs, W.Axis);
-        else
-            fr::k_fr_fft2<<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(W.Gd, W.GT, W.tab, g, p.N, (int32_t)c0,
+        fr::k_fr_fft2<<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(W.Gd, W.GT, W.tab, W.pinv, g, p.N, (int32_t)c0,
                                                                              W.Xs, W.Axis);
         FCFS_CHECK_LAUNCH("k_fr_fft");
     }
