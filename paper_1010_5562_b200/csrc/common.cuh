@@ -183,12 +183,13 @@ fcfs_status launch_block_area(const CornerSrc &src, int64_t *area_dev, cudaStrea
 // the lattice-FFT route of one FP64 clip (fft_route.cu)
 struct FftPlan {
     int32_t T, T2, N;
+    int32_t f32;       // 1: FP32 arithmetic (split-precision contract), 0: FP64
     int32_t row0;      // the x-weighted row (m = 0) is needed
     int32_t mA, nm;    // rows |m| = mA .. mA + nm - 1
     int32_t nr;        // row0 + nm
     int64_t rc;        // rows per chunk of the G workspace
 };
-bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, FftPlan &p);
+bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p);
 size_t fft_route_ws_bytes(const FftPlan &p);
 fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const FftPlan &p, void *ws, size_t ws_bytes,
                               bool &sorted, cudaStream_t s);

@@ -1146,13 +1146,18 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
                   : (fast ? tc::k_gsum_tc<true, 0> : tc::k_gsum_tc<false, 0>);
     auto hk = f16 ? (fast ? tc::k_hsum_tc<true, 1> : tc::k_hsum_tc<false, 1>)
                   : (fast ? tc::k_hsum_tc<true, 0> : tc::k_hsum_tc<false, 0>);
-    static size_t attr[4] = {0, 0, 0, 0};
+    // the GEMM's and the operand kernels' shared memory grow differently with the table size (the
+    // GEMM rounds its table to 1 KB): track both
+    static size_t attr[4] = {0, 0, 0, 0}, gattr[4] = {0, 0, 0, 0};
     const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
     if (smem > attr[ki]) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[ki] = smem;
+    }
+    if (gsmem > gattr[ki]) {
         FCFS_TRY_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
         FCFS_TRY_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
-        attr[ki] = smem;
+        gattr[ki] = gsmem;
     }
     int sms = 148;
     int dev = 0;

@@ -375,7 +375,8 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     FftPlan fp;
-    const bool fft = prec == FCFS_FP64 && valid_T(T) && fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, fp);
+    const bool fft = valid_T(T) && (prec == FCFS_FP64 || prec == FCFS_TF32X3 || prec == FCFS_F16X3) &&
+                     fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp);
     Carver cv(nullptr, 0);
     CoeffWs w;
     carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi, true), k, 1, prec, true, fft ? &fp : nullptr);
@@ -384,13 +385,14 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
 
 int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
                           const fcfs_shard *shard) {
-    if (!valid_T(T) || check_window(win) != FCFS_OK || prec != FCFS_FP64) return 0;
+    if (!valid_T(T) || check_window(win) != FCFS_OK) return 0;
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) return 0;
     int32_t m_lo, m_hi;
     if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
     int64_t k = K;
     if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
     FftPlan fp;
-    return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, fp) ? 1 : 0;
+    return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp) ? 1 : 0;
 }
 
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
@@ -423,7 +425,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     FftPlan fp;
-    const bool fft = prec == FCFS_FP64 && fft_route_plan(T, win->M, win->N, m_lo, m_hi, src.k_hi - src.k_lo, fp);
+    const bool fft = fft_route_plan(T, win->M, win->N, m_lo, m_hi, src.k_hi - src.k_lo, prec != FCFS_FP64, fp);
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi, true), src.k_hi - src.k_lo, 1, prec, true,

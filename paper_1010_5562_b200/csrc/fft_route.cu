@@ -46,31 +46,57 @@ struct Geo {
     int32_t b2, nhi2;       // two-level table of T2
 };
 
-// e^{-2 pi i p / T} from a two-level table holding e^{-2 pi i j / T} (already conjugated)
+// complex arithmetic on double2 (FP64 route) and float2 (FP32 route of the split precisions)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 tw_ldg(const double2 *tab, uint32_t p, int lbits, int nhi) {
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+template <class V> struct Cx;
+template <> struct Cx<double2> {
+    using S = double;
+    static __device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
+};
+template <> struct Cx<float2> {
+    using S = float;
+    static __device__ __forceinline__ float2 mk(double a, double b) { return make_float2((float)a, (float)b); }
+};
+template <class V>
+__device__ __forceinline__ double2 to_d(V a) { return make_double2((double)a.x, (double)a.y); }
+
+// e^{-2 pi i p / T} from a two-level table holding e^{-2 pi i j / T} (already conjugated)
+template <class V>
+__device__ __forceinline__ V tw_ldg(const V *tab, uint32_t p, int lbits, int nhi) {
     return cmul(__ldg(tab + (p >> lbits)), __ldg(tab + nhi + (p & ((1u << lbits) - 1u))));
 }
-__device__ __forceinline__ double2 tw_smem(const double2 *tab, uint32_t p, int lbits, int nhi) {
+template <class V>
+__device__ __forceinline__ V tw_smem(const V *tab, uint32_t p, int lbits, int nhi) {
     return cmul(tab[p >> lbits], tab[nhi + (p & ((1u << lbits) - 1u))]);
 }
 
 // two-level table of e^{-2 pi i j / L}: entries [0, nhi) = hi steps (j << lbits), [nhi, nhi + 2^lbits) = lo
-__device__ __forceinline__ double2 tw_entry(int i, int L, int lbits, int nhi) {
+// (FP64 sincospi, rounded once to the route's precision)
+template <class V>
+__device__ __forceinline__ V tw_entry(int i, int L, int lbits, int nhi) {
     const int64_t j = i < nhi ? ((int64_t)i << lbits) : (int64_t)(i - nhi);
     double s, c;
     sincospi(2.0 * (double)j / (double)L, &s, &c);
-    return make_double2(c, -s);
+    return Cx<V>::mk(c, -s);
 }
 
-__global__ void k_fr_table(double2 *tab, Geo g) {
+template <class V>
+__global__ void k_fr_table(V *tab, Geo g) {
     const int n = g.nhi + (1 << g.lbits);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        tab[i] = tw_entry(i, g.T, g.lbits, g.nhi);
+        tab[i] = tw_entry<V>(i, g.T, g.lbits, g.nhi);
 }
 
 // yptr[v] = #corners in [k_lo, k_hi) with y < v, v in [0, T+1]; flag = 1 if y decreases somewhere
@@ -128,31 +154,34 @@ __device__ __forceinline__ int32_t y_of(int64_t t, const Geo &g, const int16_t *
 }
 
 // the x-weighted row G0[y] = sum_{y_k = y mod T} w_k x_k (exact integer sum), as complex (row 0)
+template <class V>
 __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-                          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, Geo g, double2 *Gd) {
+                          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, Geo g, V *Gd) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t yv = y_of(t, g, perm);
         long long s = 0;
         for (int32_t k = yptr[yv]; k < yptr[yv + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
         if (yv == 0)
             for (int32_t k = yptr[g.T]; k < yptr[g.T + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
-        Gd[t] = make_double2((double)s, 0.0);
+        Gd[t] = Cx<V>::mk((double)s, 0.0);
     }
 }
 
 // rows m = m0 .. m0+15 (m0 = m_first + 16 blockIdx.y, up to m_last) of G, written to Gd rows
 // row_off + 16 blockIdx.y + j.  Two corners per iteration (independent recurrence chains).
-__global__ void __launch_bounds__(kThreads, 2)
+template <class V>
+__global__ void __launch_bounds__(kThreads, sizeof(V) == 16 ? 2 : 3)
 k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, const double2 *__restrict__ tab, Geo g,
-          int32_t m_first, int32_t m_last, int32_t row_off, double2 *Gd) {
+          const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, const V *__restrict__ tab, Geo g,
+          int32_t m_first, int32_t m_last, int32_t row_off, V *Gd) {
+    using S = typename Cx<V>::S;
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.y;
     const uint32_t mask = (uint32_t)g.T - 1u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t yv = y_of(t, g, perm);
-        double2 acc[kRowsPerThread];
+        V acc[kRowsPerThread];
 #pragma unroll
-        for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
+        for (int j = 0; j < kRowsPerThread; ++j) acc[j] = Cx<V>::mk(0.0, 0.0);
         auto run = [&](int32_t k0, int32_t k1) {
             int32_t k = k0;
             // corner coordinates / weights one pair ahead (their loads overlap the current pair's math)
@@ -164,14 +193,14 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
             }
             for (; k + 1 < k1; k += 2) {
                 const uint32_t xa = nxa, xb = nxb;
-                const double wa = (double)nwa, wb = (double)nwb;
+                const S wa = (S)nwa, wb = (S)nwb;
                 if (k + 3 < k1) {
                     nxa = (uint32_t)__ldg(x + k_lo + k + 2); nxb = (uint32_t)__ldg(x + k_lo + k + 3);
                     nwa = __ldg(w + k_lo + k + 2); nwb = __ldg(w + k_lo + k + 3);
                 }
-                double2 ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
-                double2 eb = tw_ldg(tab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
-                const double2 sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi), sb = tw_ldg(tab, xb & mask, g.lbits, g.nhi);
+                V ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                V eb = tw_ldg(tab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
+                const V sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi), sb = tw_ldg(tab, xb & mask, g.lbits, g.nhi);
 #pragma unroll
                 for (int j = 0; j < kRowsPerThread; ++j) {
                     if (j) { ea = cmul(ea, sa); eb = cmul(eb, sb); }
@@ -181,9 +210,9 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
             }
             if (k < k1) {
                 const uint32_t xa = (uint32_t)__ldg(x + k_lo + k);
-                const double wa = (double)__ldg(w + k_lo + k);
-                double2 ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
-                const double2 sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
+                const S wa = (S)__ldg(w + k_lo + k);
+                V ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                const V sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
 #pragma unroll
                 for (int j = 0; j < kRowsPerThread; ++j) {
                     if (j) ea = cmul(ea, sa);
@@ -204,21 +233,23 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
 // the y = T run (its phase wraps to row y = 0; the axis sum weights it with T): block per 16 rows,
 // threads over the run's corners (the run can hold thousands of corners: the lines clipped at the
 // tile edge), block reduction; GT[row] = its share, added into G[m, 0]
+template <class V>
 __global__ void __launch_bounds__(kThreads)
 k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
-           const int32_t *__restrict__ yptr, const int16_t *__restrict__ pinv, const double2 *__restrict__ tab, Geo g,
-           int32_t m_first, int32_t m_last, int32_t row_off, double2 *Gd, double2 *GT) {
-    __shared__ double2 red[kThreads / 32][kRowsPerThread];
+           const int32_t *__restrict__ yptr, const int16_t *__restrict__ pinv, const V *__restrict__ tab, Geo g,
+           int32_t m_first, int32_t m_last, int32_t row_off, V *Gd, double2 *GT) {
+    using S = typename Cx<V>::S;
+    __shared__ V red[kThreads / 32][kRowsPerThread];
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.x;
     const uint32_t mask = (uint32_t)g.T - 1u;
-    double2 acc[kRowsPerThread];
+    V acc[kRowsPerThread];
 #pragma unroll
-    for (int j = 0; j < kRowsPerThread; ++j) acc[j] = make_double2(0.0, 0.0);
+    for (int j = 0; j < kRowsPerThread; ++j) acc[j] = Cx<V>::mk(0.0, 0.0);
     for (int32_t k = yptr[g.T] + (int32_t)threadIdx.x; k < yptr[g.T + 1]; k += kThreads) {
         const uint32_t xa = (uint32_t)x[k_lo + k];
-        const double wa = (double)w[k_lo + k];
-        double2 e = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
-        const double2 st = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
+        const S wa = (S)w[k_lo + k];
+        V e = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+        const V st = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
 #pragma unroll
         for (int j = 0; j < kRowsPerThread; ++j) {
             if (j) e = cmul(e, st);
@@ -237,10 +268,10 @@ k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t
     __syncthreads();
     const int j = threadIdx.x;
     if (j < kRowsPerThread && m0 + j <= m_last) {
-        double2 a = make_double2(0.0, 0.0);
+        V a = Cx<V>::mk(0.0, 0.0);
         for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i][j]);
         const int64_t row = row_off + kRowsPerThread * (int64_t)blockIdx.x + j;
-        GT[row] = a;
+        GT[row] = to_d(a);
         const int64_t t0 = (uint16_t)pinv[0];   // storage slot of y = 0
         Gd[row * g.T + t0] = cadd(Gd[row * g.T + t0], a);
     }
@@ -248,58 +279,59 @@ k_fr_rowsT(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t
 
 // ---------------------------------------------------------------- the per-row FFT
 
-__device__ __forceinline__ double2 w16(int q) {   // e^{-2 pi i q / 16}, q in [0, 8)
+template <class V>
+__device__ __forceinline__ V w16(int q) {   // e^{-2 pi i q / 16}, q in [0, 8)
     const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
     switch (q) {
-        case 0: return make_double2(1.0, 0.0);
-        case 1: return make_double2(c1, -s1);
-        case 2: return make_double2(h, -h);
-        case 3: return make_double2(s1, -c1);
-        case 4: return make_double2(0.0, -1.0);
-        case 5: return make_double2(-s1, -c1);
-        case 6: return make_double2(-h, -h);
-        default: return make_double2(-c1, -s1);
+        case 0: return Cx<V>::mk(1.0, 0.0);
+        case 1: return Cx<V>::mk(c1, -s1);
+        case 2: return Cx<V>::mk(h, -h);
+        case 3: return Cx<V>::mk(s1, -c1);
+        case 4: return Cx<V>::mk(0.0, -1.0);
+        case 5: return Cx<V>::mk(-s1, -c1);
+        case 6: return Cx<V>::mk(-h, -h);
+        default: return Cx<V>::mk(-c1, -s1);
     }
 }
 
-__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
-
 // radix-4 butterfly in place: (a0..a3) -> DFT_4
-__device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, double2 &a3) {
-    const double2 b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3), b3 = mul_mi(csub(a1, a3));
+template <class V>
+__device__ __forceinline__ void bfly4(V &a0, V &a1, V &a2, V &a3) {
+    const V b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3), b3 = mul_mi(csub(a1, a3));
     a0 = cadd(b0, b2); a2 = csub(b0, b2); a1 = cadd(b1, b3); a3 = csub(b1, b3);
 }
 
 // in-register DFT of size R (natural order in and out): R = 2, 4, or the four-step split
 // R = 4 x 4 (16) / 2 x 4 (8) with the W_R^{r0 k1} twiddles as constants
-template <int R>
-__device__ __forceinline__ void dft(double2 (&v)[R]) {
+template <int R, class V>
+__device__ __forceinline__ void dft(V (&v)[R]) {
     if constexpr (R == 2) {
-        const double2 a = v[0];
+        const V a = v[0];
         v[0] = cadd(a, v[1]); v[1] = csub(a, v[1]);
     } else if constexpr (R == 4) {
         bfly4(v[0], v[1], v[2], v[3]);
     } else if constexpr (R == 8) {
         // x[r0 + 2 r1]: DFT_4 over r1 for r0 = 0, 1; twiddle W8^{r0 k1}; DFT_2 over r0
-        double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+        V e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
         bfly4(e[0], e[1], e[2], e[3]);
         bfly4(o[0], o[1], o[2], o[3]);
-        o[1] = cmul(o[1], w16(2)); o[2] = mul_mi(o[2]); o[3] = cmul(o[3], w16(6));
+        o[1] = cmul(o[1], w16<V>(2)); o[2] = mul_mi(o[2]); o[3] = cmul(o[3], w16<V>(6));
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1) { v[k1] = cadd(e[k1], o[k1]); v[k1 + 4] = csub(e[k1], o[k1]); }
     } else {
         static_assert(R == 16, "radix");
         // x[r0 + 4 r1]: DFT_4 over r1 for each r0; twiddle W16^{r0 k1}; DFT_4 over r0 -> X[k1 + 4 k2]
-        double2 y[4][4];
+        V y[4][4];
 #pragma unroll
         for (int r0 = 0; r0 < 4; ++r0) {
             y[r0][0] = v[r0]; y[r0][1] = v[r0 + 4]; y[r0][2] = v[r0 + 8]; y[r0][3] = v[r0 + 12];
             bfly4(y[r0][0], y[r0][1], y[r0][2], y[r0][3]);
         }
-        y[1][1] = cmul(y[1][1], w16(1)); y[1][2] = cmul(y[1][2], w16(2)); y[1][3] = cmul(y[1][3], w16(3));
-        y[2][1] = cmul(y[2][1], w16(2)); y[2][2] = mul_mi(y[2][2]);         y[2][3] = cmul(y[2][3], w16(6));
-        y[3][1] = cmul(y[3][1], w16(3)); y[3][2] = cmul(y[3][2], w16(6));
-        y[3][3] = cmul(y[3][3], make_double2(-w16(1).x, -w16(1).y));       // W16^9 = -W16^1
+        y[1][1] = cmul(y[1][1], w16<V>(1)); y[1][2] = cmul(y[1][2], w16<V>(2)); y[1][3] = cmul(y[1][3], w16<V>(3));
+        y[2][1] = cmul(y[2][1], w16<V>(2)); y[2][2] = mul_mi(y[2][2]);            y[2][3] = cmul(y[2][3], w16<V>(6));
+        y[3][1] = cmul(y[3][1], w16<V>(3)); y[3][2] = cmul(y[3][2], w16<V>(6));
+        const V w9 = w16<V>(1);
+        y[3][3] = cmul(y[3][3], Cx<V>::mk(-(double)w9.x, -(double)w9.y));       // W16^9 = -W16^1
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1) {
             bfly4(y[0][k1], y[1][k1], y[2][k1], y[3][k1]);
@@ -316,12 +348,12 @@ __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvt
 
 // In-place Stockham pass (all reads, barrier, all writes) of radix R over length L <= R * kThreads;
 // the first pass (Ns == 1) reads the unpadded TMA layout and accumulates sum_y y G[y] (axis)
-template <int R>
-__device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const double2 *tw2, const Geo &g, int y1,
+template <int R, class V>
+__device__ __forceinline__ void pass_inplace(V *buf, int L, int Ns, const V *tw2, const Geo &g, int y1,
                                              double2 &ax, const int16_t *pv) {
     const int nb = L / R;
     const int i = threadIdx.x;
-    double2 v[R];
+    V v[R];
     const int k = i & (Ns - 1);
     if (i < nb) {   // read and transform; the barrier orders every read before any write
 #pragma unroll
@@ -330,11 +362,11 @@ __device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const 
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const double yy = (double)(y1 + ((i + r * nb) << g.t1bits));
-                ax.x = fma(yy, v[r].x, ax.x); ax.y = fma(yy, v[r].y, ax.y);
+                ax.x = fma(yy, (double)v[r].x, ax.x); ax.y = fma(yy, (double)v[r].y, ax.y);
             }
         } else {
-            const double2 w1 = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
-            double2 wr = w1;
+            const V w1 = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
+            V wr = w1;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 v[r] = cmul(v[r], wr);
@@ -354,27 +386,31 @@ __device__ __forceinline__ void pass_inplace(double2 *buf, int L, int Ns, const 
 
 // CTA per row (2 CTAs / SM): one padded work buffer that the TMA bulk copy fills with the next
 // sub-row and the passes transform in place; X[n] accumulates in shared memory
+template <class V>
 __global__ void __launch_bounds__(kThreads, 2)
-k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const double2 *__restrict__ tabT,
+k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__restrict__ tabT,
           const int16_t *__restrict__ pinv, Geo g, int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
-    extern __shared__ __align__(16) double2 fsm[];
+    extern __shared__ __align__(16) unsigned char fsm_raw[];
     const int LP = g.T2 + g.T2 / 16;
     const int nn = 2 * N + 1;
-    double2 *buf = fsm, *X = fsm + LP, *tw2 = fsm + LP + nn;
-    int16_t *pv = (int16_t *)(tw2 + g.nhi2 + (1 << g.b2));   // the sub-row's pinv (T2 x int16)
+    // [buf: LP x V][X: nn x double2 (the outer sum in FP64 for both routes)][tw2: V][pinv row: T2 x int16]
+    V *buf = (V *)fsm_raw;
+    double2 *X = (double2 *)(fsm_raw + (size_t)LP * sizeof(V));
+    V *tw2 = (V *)(X + nn);
+    int16_t *pv = (int16_t *)(tw2 + g.nhi2 + (1 << g.b2));
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double2 red[kThreads / 32];
     const int r = blockIdx.x;
-    const double2 *grow = Gd + (int64_t)r * g.T;
+    const V *grow = Gd + (int64_t)r * g.T;
     const int ntw = g.nhi2 + (1 << g.b2);
-    for (int i = threadIdx.x; i < ntw; i += kThreads) tw2[i] = tw_entry(i, g.T2, g.b2, g.nhi2);
+    for (int i = threadIdx.x; i < ntw; i += kThreads) tw2[i] = tw_entry<V>(i, g.T2, g.b2, g.nhi2);
     for (int o = threadIdx.x; o < nn; o += kThreads) X[o] = make_double2(0.0, 0.0);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const uint32_t bytes = (uint32_t)g.T2 * 16u, pbytes = (uint32_t)g.T2 * 2u;
+    const uint32_t bytes = (uint32_t)(g.T2 * sizeof(V)), pbytes = (uint32_t)g.T2 * 2u;
     double2 ax = make_double2(0.0, 0.0);
     const uint32_t maskT = (uint32_t)g.T - 1u;
     const int lead = g.t2bits & 3;
@@ -406,9 +442,9 @@ k_fr_fft2(const double2 *__restrict__ Gd, const double2 *__restrict__ GT, const 
         // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
         for (int o = threadIdx.x; o < nn; o += kThreads) {
             const int n = o - N;
-            const double2 z = buf[pad(n >= 0 ? n : n + g.T2)];
+            const V z = buf[pad(n >= 0 ? n : n + g.T2)];
             const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
-            X[o] = cadd(X[o], cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z));
+            X[o] = cadd(X[o], to_d(cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z)));
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
@@ -511,14 +547,15 @@ static fr::Geo make_geo(int32_t T, int32_t T2) {
     return g;
 }
 
-// geometry + cost model; FCFS_ROUTE=fft / gemm (environment) forces the choice where possible
-bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, FftPlan &p) {
+// geometry + cost model; FCFS_ROUTE=fft / gemm (environment) forces the choice where possible.
+// f32: the FP32 variant for the split precisions (same 1e-5 B contract as their tensor GEMM)
+bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p) {
     p = FftPlan{};
     if (T < 64 || (T & (T - 1)) != 0 || K <= 0 || K >= (int64_t(1) << 31)) return false;
     int64_t T2 = 64;
     while (T2 < 2 * (int64_t)N + 1) T2 <<= 1;
     if (T2 > fr::kMaxT2 || T2 > T) return false;
-    p.T = T; p.T2 = (int32_t)T2; p.N = N;
+    p.T = T; p.T2 = (int32_t)T2; p.N = N; p.f32 = f32 ? 1 : 0;
     p.row0 = (m_lo <= 0 && 0 <= m_hi) ? 1 : 0;
     int32_t a, b;
     if (m_lo > 0) { a = m_lo; b = m_hi; }
@@ -527,8 +564,8 @@ bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi,
     p.mA = a;
     p.nm = b >= a ? b - a + 1 : 0;
     p.nr = p.row0 + p.nm;
-    // rows per chunk: the G rows of a chunk (16 T bytes each) within ~4.5 GB, a multiple of 8
-    int64_t rc = (int64_t)(4.5e9 / (16.0 * (double)T));
+    // rows per chunk: the G rows of a chunk (8 or 16 T bytes each) within ~4.5 GB, a multiple of 8
+    int64_t rc = (int64_t)(4.5e9 / ((f32 ? 8.0 : 16.0) * (double)T));
     rc = rc / 8 * 8;
     if (rc < 8) rc = 8;
     p.rc = rc;
@@ -540,24 +577,27 @@ bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi,
                        9.0 * (double)K * (double)p.nm;
     const double rows = (double)(K < (int64_t)T + 1 ? K : (int64_t)T + 1);
     const double gemm = 8.0 * (double)p.nm * (double)N * rows;
-    return fft * 2.0 < gemm;
+    // the tensor GEMMs run ~2x (DMMA vs FP64 route) / ~3x (split tcgen05 vs FP32 route) more flop/s
+    return fft * (f32 ? 3.0 : 2.0) < gemm;
 }
 
 struct FftWs {
     int32_t *yptr, *flag;
     int16_t *perm, *pinv;
-    double2 *tab, *Gd, *GT, *Xs, *Axis;
+    void *tab, *Gd;      // double2 (FP64 route) or float2 (FP32 route)
+    double2 *GT, *Xs, *Axis;
 };
 
 static void carve_fft(Carver &cv, const FftPlan &p, FftWs &w) {
     const fr::Geo g = make_geo(p.T, p.T2);
     const int64_t rc = p.rc < p.nr ? p.rc : p.nr;
+    const size_t vb = p.f32 ? sizeof(float2) : sizeof(double2);
     w.yptr = cv.take<int32_t>((size_t)p.T + 2);
     w.flag = cv.take<int32_t>(1);
     w.perm = cv.take<int16_t>((size_t)p.T);
     w.pinv = cv.take<int16_t>((size_t)p.T);
-    w.tab = cv.take<double2>((size_t)g.nhi + ((size_t)1 << g.lbits));
-    w.Gd = cv.take<double2>((size_t)(rc > 0 ? rc : 1) * (size_t)p.T);
+    w.tab = cv.take<char>(vb * ((size_t)g.nhi + ((size_t)1 << g.lbits)));
+    w.Gd = cv.take<char>(vb * (size_t)(rc > 0 ? rc : 1) * (size_t)p.T);
     w.GT = cv.take<double2>((size_t)(rc > 0 ? rc : 1));
     w.Xs = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1) * (size_t)(2 * p.N + 1));
     w.Axis = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1));
@@ -590,24 +630,22 @@ fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const F
     return FCFS_OK;
 }
 
-fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, const FftPlan &p, void *ws,
-                          size_t ws_bytes, const EpiArgs &ea, void *F, cudaStream_t s) {
-    Carver cv(ws, ws_bytes);
-    FftWs W;
-    carve_fft(cv, p, W);
-    if (!cv.fits()) { set_error("fft route: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+template <class V>
+static fcfs_status run_route(const int32_t *x, const int32_t *w, int64_t k_lo, const FftPlan &p, FftWs &W,
+                             const EpiArgs &ea, void *F, cudaStream_t s) {
     const fr::Geo g = make_geo(p.T, p.T2);
+    V *tab = (V *)W.tab, *Gd = (V *)W.Gd;
     const int ntab = g.nhi + (1 << g.lbits);
-    fr::k_fr_table<<<(unsigned)((ntab + 255) / 256), 256, 0, s>>>(W.tab, g);
+    fr::k_fr_table<V><<<(unsigned)((ntab + 255) / 256), 256, 0, s>>>(tab, g);
     FCFS_CHECK_LAUNCH("k_fr_table");
     fr::k_fr_perm<<<(unsigned)g.T1, fr::kThreads, 0, s>>>(W.yptr, g, W.perm, W.pinv);
     FCFS_CHECK_LAUNCH("k_fr_perm");
-    const size_t fsmem2 = (size_t)((p.T2 + p.T2 / 16) + (2 * p.N + 1) + g.nhi2 + (1 << g.b2)) * sizeof(double2) +
-                          (size_t)p.T2 * sizeof(int16_t);
+    const size_t fsmem2 = (size_t)(p.T2 + p.T2 / 16 + g.nhi2 + (1 << g.b2)) * sizeof(V) +
+                          (size_t)(2 * p.N + 1) * sizeof(double2) + (size_t)p.T2 * sizeof(int16_t);
     static size_t fattr2 = 0;
     if (fsmem2 > fattr2) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem2));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem2));
+        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2<V>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         fattr2 = fsmem2;
     }
     int64_t tblocks = p.T / 256;
@@ -617,7 +655,7 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
         const int64_t c1 = c0 + p.rc < p.nr ? c0 + p.rc : p.nr;
         FCFS_TRY_CUDA(cudaMemsetAsync(W.GT, 0, sizeof(double2) * (size_t)(c1 - c0), s));
         if (c0 == 0 && p.row0) {
-            fr::k_fr_row0<<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, W.perm, g, W.Gd);
+            fr::k_fr_row0<V><<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, W.perm, g, Gd);
             FCFS_CHECK_LAUNCH("k_fr_row0");
         }
         const int64_t ra = c0 > p.row0 ? c0 : p.row0;   // first |m| >= 1 row of the chunk
@@ -625,15 +663,15 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
             const int32_t m_first = p.mA + (int32_t)(ra - p.row0), m_last = p.mA + (int32_t)(c1 - 1 - p.row0);
             const int64_t rb = (m_last - m_first + fr::kRowsPerThread) / fr::kRowsPerThread;
             dim3 grid((unsigned)tblocks, (unsigned)rb);
-            fr::k_fr_rows<<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.perm, W.tab, g, m_first, m_last,
-                                                        (int32_t)(ra - c0), W.Gd);
+            fr::k_fr_rows<V><<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.perm, tab, g, m_first, m_last,
+                                                           (int32_t)(ra - c0), Gd);
             FCFS_CHECK_LAUNCH("k_fr_rows");
-            fr::k_fr_rowsT<<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.pinv, W.tab, g, m_first, m_last,
-                                                                 (int32_t)(ra - c0), W.Gd, W.GT);
+            fr::k_fr_rowsT<V><<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.pinv, tab, g, m_first,
+                                                                    m_last, (int32_t)(ra - c0), Gd, W.GT);
             FCFS_CHECK_LAUNCH("k_fr_rowsT");
         }
-        fr::k_fr_fft2<<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(W.Gd, W.GT, W.tab, W.pinv, g, p.N, (int32_t)c0,
-                                                                             W.Xs, W.Axis);
+        fr::k_fr_fft2<V><<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(Gd, W.GT, tab, W.pinv, g, p.N,
+                                                                             (int32_t)c0, W.Xs, W.Axis);
         FCFS_CHECK_LAUNCH("k_fr_fft");
     }
     const int rows = ea.m_hi - ea.m_lo + 1;
@@ -642,6 +680,15 @@ fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, cons
         FCFS_CHECK_LAUNCH("k_fr_epilogue");
     }
     return FCFS_OK;
+}
+
+fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, const FftPlan &p, void *ws,
+                          size_t ws_bytes, const EpiArgs &ea, void *F, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    FftWs W;
+    carve_fft(cv, p, W);
+    if (!cv.fits()) { set_error("fft route: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    return p.f32 ? run_route<float2>(x, w, k_lo, p, W, ea, F, s) : run_route<double2>(x, w, k_lo, p, W, ea, F, s);
 }
 
 }  // namespace fcfs

@@ -512,24 +512,27 @@ def route(monkeypatch):
     yield set_route
 
 
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 @pytest.mark.parametrize("r", ["fft", "gemm"])
 @pytest.mark.parametrize("cfg,M,N", [("c1", 32, 32), ("c2", 64, 64), ("c2", 40, 23), ("c2", 7, 0), ("c2", 0, 9),
                                      ("c1", 20, 2047)])
-def test_fft_route_full_window(fcfs, route, r, cfg, M, N):
-    """Both FP64 routes against the oracle on full windows (T2 = 64 .. 4096, M != N, M = 0, N = 0)."""
+def test_fft_route_full_window(fcfs, route, r, prec, cfg, M, N):
+    """Both routes (FP64, and the FP32 route of the split precisions) against the oracle on full windows
+    (T2 = 64 .. 4096, M != N, M = 0, N = 0)."""
     route(r)
     wl = inputs.make(cfg)
     if N == 2047:
         wl = inputs.c1(seed=2, T=8192)              # 2N+1 = 4095 <= T2 = 4096 (the largest FFT)
-    g, F = _clip_coeffs(fcfs, wl, "fp64", M=M, N=N, r2=-1.0)
+    g, F = _clip_coeffs(fcfs, wl, prec, M=M, N=N, r2=-1.0)
     ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
-    _assert_parity(F, Fr, B, "fp64", f"{r} {cfg} M={M} N={N}", ms, ns)
+    _assert_parity(F, Fr, B, prec, f"{r} {cfg} M={M} N={N}", ms, ns)
     Fm = F[::-1]
     assert np.array_equal(Fm.real, F.real) and np.array_equal(Fm.imag, -F.imag)
 
 
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
 @pytest.mark.parametrize("r", ["fft", "gemm"])
-def test_fft_route_shards_pupil_and_boundary(fcfs, route, r):
+def test_fft_route_shards_pupil_and_boundary(fcfs, route, r, prec):
     """ROWS shards (negative-only, across 0, positive), VERTEX_BLOCK partials, pupil layouts and corners
     on y = T / x = T (the raw y weight of the axis column, reading A7) through both routes."""
     route(r)
@@ -543,31 +546,33 @@ def test_fft_route_shards_pupil_and_boundary(fcfs, route, r):
     area = int(g["area"][0].item())
     M = N = 50
     ms, ns, Fr, B = _oracle_window(g, T, M, N)
-    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec="fp64").cpu().numpy()
-    _assert_parity(full, Fr, B, "fp64", f"{r} full", ms, ns)
-    parts = [fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec="fp64",
+    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec=prec).cpu().numpy()
+    _assert_parity(full, Fr, B, prec, f"{r} full", ms, ns)
+    parts = [fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec=prec,
                          shard=fcfs.Shard(fcfs.SHARD_ROWS, lo, hi, 0, 0)).cpu().numpy()
              for lo, hi in [(-50, -20), (-19, 5), (6, 6), (7, 50)]]
-    _assert_parity(np.concatenate(parts), Fr, B, "fp64", f"{r} row shards", ms, ns)
+    _assert_parity(np.concatenate(parts), Fr, B, prec, f"{r} row shards", ms, ns)
     K = g["K"]
     acc = 0
     for a, b in [(0, K // 3), (K // 3, K - 7), (K - 7, K)]:
         sh = fcfs.Shard(fcfs.SHARD_VERTEX_BLOCK, 0, 0, a, b)
-        acc = acc + fcfs.coeffs(g["x"], g["y"], g["w"], 0, T, M, N, prec="fp64", shard=sh).cpu().numpy()
+        acc = acc + fcfs.coeffs(g["x"], g["y"], g["w"], 0, T, M, N, prec=prec, shard=sh).cpu().numpy().astype(np.complex128)
     dc = (ms == 0) & (ns == 0)
-    _assert_parity(acc[~dc], Fr[~dc], B[~dc], "fp64", f"{r} vertex blocks")
-    assert acc[dc][0] == Fr[dc][0]
+    _assert_parity(acc[~dc], Fr[~dc], B[~dc], prec, f"{r} vertex blocks")
+    if prec == "fp64":
+        assert acc[dc][0] == Fr[dc][0]
     r2 = 1234.5
     for layout in ("pupil", "dense"):
-        F = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, r2, layout, "fp64").cpu().numpy()
+        F = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, r2, layout, prec).cpu().numpy()
         ms2, ns2, Fr2, B2 = _oracle_window(g, T, M, N, r2, layout)
-        _assert_parity(F, Fr2, B2, "fp64", f"{r} {layout}", ms2, ns2)
+        _assert_parity(F, Fr2, B2, prec, f"{r} {layout}", ms2, ns2)
 
 
-def test_fft_route_small_T2_many_subrows(fcfs, route):
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_fft_route_small_T2_many_subrows(fcfs, route, prec):
     """T2 = 64 with T1 = 1024 sub-rows (narrow window on a large tile), forced FFT route."""
     route("fft")
     wl = inputs.c4(seed=1, n_poly=20000)
-    g, F = _clip_coeffs(fcfs, wl, "fp64", M=9, N=10, r2=-1.0)
+    g, F = _clip_coeffs(fcfs, wl, prec, M=9, N=10, r2=-1.0)
     ms, ns, Fr, B = _oracle_window(g, wl.T, 9, 10)
-    _assert_parity(F, Fr, B, "fp64", "T2=64", ms, ns)
+    _assert_parity(F, Fr, B, prec, "T2=64", ms, ns)
