@@ -340,7 +340,7 @@ def main():
     fft_route = (wl.B == 1 and world == 1 and
                  fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec) == 1)
     if fft_route:
-        # lattice-FFT route (NEXT-2, FP64 CUDA cores): algorithmic work of the contract stage =
+        # lattice-FFT route (NEXT-2, FP64 or FP32 CUDA cores): algorithmic work of the contract stage =
         # G rows (one complex rotation + real-weighted complex MAC per corner and row: 10 flop) +
         # the T1 length-T2 FFTs per row (5 T2 log2 T2) + the outer twiddled sum (8 flop per n and y1)
         T2 = 64
@@ -351,10 +351,17 @@ def main():
         alg_flops = (10.0 * K * wl.M + rows * T1 * (5.0 * T2 * math.log2(T2) + 8.0 * (2 * wl.N + 1)))
         achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
         clocks = clk.summary()
-        pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
-        peak = pk["dfma_tflops"]
-        peak_note = ("FP64 CUDA-core DFMA measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json); "
-                     f"the stage = k_fr_rows + k_fr_fft + small kernels, T2={T2}, T1={T1}")
+        if prec == "fp64":
+            pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+            peak = pk["dfma_tflops"]
+            peak_note = ("FP64 CUDA-core DFMA measured by tools/fp64_peak.cu on this pool (profiles/fp64_peak.json); "
+                         f"the stage = k_fr_rows + k_fr_fft2 + small kernels, T2={T2}, T1={T1}")
+        else:
+            mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+            peak_note = (f"FP32 CUDA-core FFMA, derived: 148 SM x 128 lanes x 2 flop x {mhz:.0f} MHz (the FP32 "
+                         f"route of the split precisions); stage = k_fr_rows + k_fr_fft2 + small kernels, "
+                         f"T2={T2}, T1={T1}")
         bound = "alu"
         k_inner = "lattice-FFT route"
         Kc = np.array([float(K)])
@@ -393,7 +400,8 @@ def main():
             bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else ""),
-            "kernel": ("contract stage (k_fr_rows + k_fr_fft)" if fft_route else "k_gemm_" + prec),
+            "kernel": (f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
+                       if fft_route else "k_gemm_" + prec),
             "k_inner": f"{k_inner}: {int(Kc.sum())}",
             "alg_flops_per_launch": alg_flops,
             "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
@@ -482,7 +490,11 @@ def main():
         line = {"metric": "fourier_coeff_vertex_terms_per_sec", "value": round(value, 3), "unit": "Gterm/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
                 "higher_is_better": True, "scaling": "strong" if single_sharded else "weak", "vs_baseline": None,
-                "dtype": "tf32x3 (split-TF32, FP32-accurate; FP64 flush)" if prec == "tf32x3" else "f64",
+                "dtype": ("f64" if prec == "fp64" else
+                          "f32 (lattice-FFT route on FP32 CUDA cores, FP64 outer sums; the split-precision contract)"
+                          if fft_route else
+                          "tf32x3 (split-TF32, FP32-accurate; FP64 flush)" if prec == "tf32x3" else
+                          "f16x3 (split-FP16, FP32-accurate; FP64 flush)"),
                 "data": "synthetic", "config": config_dict(args, wl, prec, world),
                 "K_per_gpu": int(K), "terms_per_step_per_gpu": terms,
                 "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),

@@ -154,11 +154,13 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
                                    fcfs_precision prec, const fcfs_shard *shard);
 /* Which single-clip route fcfs_coeffs takes for these sizes (planning / reporting; no device work):
- * 1 = the lattice-FFT route (FCFS_FP64, power-of-two T >= 64, 2N+1 <= min(T, 4096), chosen by a
- * cost model over the row-bucket GEMM; taken only if the corner list is y-sorted, as
- * fcfs_vertices_from_* produce it — fcfs_coeffs checks on the device and otherwise falls back),
- * 0 = the row-bucket GEMM (tensor cores).  The environment variable FCFS_ROUTE=fft|gemm overrides
- * the cost model (testing).  Both routes meet the same tolerance. */
+ * 1 = the lattice-FFT route (power-of-two T >= 64, 2N+1 <= min(T, 4096), chosen by a cost model over
+ * the row-bucket GEMM; taken only if the corner list is y-sorted, as fcfs_vertices_from_* produce it
+ * — fcfs_coeffs checks on the device and otherwise falls back).  FCFS_FP64 runs it in FP64;
+ * FCFS_TF32X3 / FCFS_F16X3 run it in FP32 on the CUDA cores (FP64 outer and axis sums) under their
+ * 1e-5 B contract and complex64 output.  0 = the row-bucket GEMM on the tensor cores (DMMA, or the
+ * split tcgen05 kernels).  The environment variable FCFS_ROUTE=fft|gemm overrides the cost model
+ * (testing).  Both routes meet the same tolerance. */
 int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
                           const fcfs_shard *shard);
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K,
