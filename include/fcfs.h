@@ -148,8 +148,11 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
  * win      host struct, see fcfs_window.   prec  FCFS_FP64, FCFS_TF32X3 or FCFS_F16X3.
  * shard    host struct or NULL (= FCFS_SHARD_NONE).
  * F        out (device): complex128 (FP64) or complex64 (TF32X3 / F16X3) in the window layout.
- * The corners are contracted over their row buckets (fcfs_row_buckets, cap 32), in chunks of
- * buckets sized to stay in L2; the call synchronises `stream` once to read the bucket count.
+ * Two routes (fcfs_coeffs_route): the lattice-FFT route (Step 4 as row DFTs, then an output-pruned
+ * FFT along y) when it is cheaper and the corners are y-sorted, else the
+ * row-bucket GEMM: the corners contracted over their row buckets (fcfs_row_buckets, cap 32) in
+ * chunks of <= 128K buckets.  Either way the call synchronises `stream` once (sortedness flag or
+ * bucket count).
  * ------------------------------------------------------------------------------------------ */
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
                                    fcfs_precision prec, const fcfs_shard *shard);
