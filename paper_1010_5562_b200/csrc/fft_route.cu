@@ -153,7 +153,8 @@ __device__ __forceinline__ int32_t y_of(int64_t t, const Geo &g, const int16_t *
     return (int32_t)((t >> g.t2bits) + ((int32_t)(uint16_t)__ldg(perm + t) << g.t1bits));
 }
 
-// the x-weighted row G0[y] = sum_{y_k = y mod T} w_k x_k (exact integer sum), as complex (row 0)
+// the x-weighted row G0[y] = sum_{y_k = y mod T} w_k x_k (exact integer sum), as complex (row 0); the
+// y = T run is added by k_fr_row0T
 template <class V>
 __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
                           const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, Geo g, V *Gd) {
@@ -161,9 +162,30 @@ __global__ void k_fr_row0(const int32_t *__restrict__ x, const int32_t *__restri
         const int32_t yv = y_of(t, g, perm);
         long long s = 0;
         for (int32_t k = yptr[yv]; k < yptr[yv + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
-        if (yv == 0)
-            for (int32_t k = yptr[g.T]; k < yptr[g.T + 1]; ++k) s += (long long)w[k_lo + k] * x[k_lo + k];
         Gd[t] = Cx<V>::mk((double)s, 0.0);
+    }
+}
+
+// one block: the y = T run's sum of w x (exact, int64) added into G0 at y = 0 (storage slot pinv[0]);
+// the run holds thousands of corners on the configs (lines clipped at the tile edge)
+template <class V>
+__global__ void __launch_bounds__(kThreads)
+k_fr_row0T(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t k_lo,
+           const int32_t *__restrict__ yptr, const int16_t *__restrict__ pinv, Geo g, V *Gd) {
+    __shared__ long long red[kThreads / 32];
+    long long s = 0;
+    for (int32_t k = yptr[g.T] + (int32_t)threadIdx.x; k < yptr[g.T + 1]; k += kThreads)
+        s += (long long)w[k_lo + k] * x[k_lo + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0;
+        for (int i = 0; i < kThreads / 32; ++i) a += red[i];
+        const int64_t t0 = (uint16_t)pinv[0];
+        const V v = Gd[t0];
+        // both integers below 2^53: the FP64 sum is exact (FP32 route: rounded once)
+        Gd[t0] = Cx<V>::mk((double)v.x + (double)a, 0.0);
     }
 }
 
@@ -657,6 +679,8 @@ static fcfs_status run_route(const int32_t *x, const int32_t *w, int64_t k_lo, c
         if (c0 == 0 && p.row0) {
             fr::k_fr_row0<V><<<(unsigned)tblocks, 256, 0, s>>>(x, w, k_lo, W.yptr, W.perm, g, Gd);
             FCFS_CHECK_LAUNCH("k_fr_row0");
+            fr::k_fr_row0T<V><<<1, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.pinv, g, Gd);
+            FCFS_CHECK_LAUNCH("k_fr_row0T");
         }
         const int64_t ra = c0 > p.row0 ? c0 : p.row0;   // first |m| >= 1 row of the chunk
         if (ra < c1) {
