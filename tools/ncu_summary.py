@@ -19,8 +19,12 @@ RAW_KEYS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
     "smsp__warps_eligible.avg.per_cycle_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
+    "dram__bytes.sum.per_second",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread",
     "launch__grid_size",
     "launch__block_size",

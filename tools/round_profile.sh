@@ -1,21 +1,34 @@
 #!/bin/bash
-# One GPU session of measurements for profiles/: bench lines (no profiler), the launch list of the
-# default c3 step, and ncu --set full captures of the dominant kernels.  Usage (under gpurun):
-#   bash tools/round_profile.sh <tag>
+# One GPU session of measurements for profiles/: bench lines (no profiler), launch lists and
+# ncu --set full captures of the dominant kernels.  Usage (under gpurun): bash tools/round_profile.sh <tag>
 set -u
 T=${1:-r01}
 O=gpurun_out
-B3="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
-B4="python bench.py --config c4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+NB="--no-cpu-baseline --no-e2e"
+# ---- bench lines (each command exits before any profiler run of the same command)
 timeout 300 python bench.py --steps 10 --warmup 3 > $O/${T}_bench_c3.json 2> $O/${T}_bench_c3.err
+timeout 300 python bench.py --prec f16x3 --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_f16x3.json 2>/dev/null
 for c in c1 c2 c4 c5; do
-  timeout 400 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline > $O/${T}_bench_${c}_fp64.json 2>/dev/null
+  timeout 400 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $O/${T}_bench_${c}_fp64.json 2>/dev/null
 done
-timeout 300 python bench.py --config c4 --prec tf32x3 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/${T}_bench_c4_tf32x3.json 2>/dev/null
-timeout 300 python bench.py --prec f16x3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/${T}_bench_c3_f16x3.json 2>/dev/null
-$B3 > $O/plain3.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $O/${T}_launches_c3.csv $B3 > $O/ncu_a.log 2>&1
-$B3 > $O/plain3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf32 $B3 > $O/ncu_b.log 2>&1
-$B3 > $O/plain3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_clip_corners -s 1 -c 1 -o $O/${T}_prof_c3_extract $B3 > $O/ncu_c.log 2>&1
-$B4 > $O/plain4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/${T}_launches_c4.csv $B4 > $O/ncu_d.log 2>&1
-$B4 > $O/plain4.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_gemm_fp64|k_gsum_fp64" -s 4 -c 2 -o $O/${T}_prof_c4_fp64 $B4 > $O/ncu_e.log 2>&1
-ls -la $O | tail -30
+for c in c4 c5; do for p in tf32x3 f16x3; do
+  timeout 300 python bench.py --config $c --prec $p --steps 5 --warmup 3 $NB > $O/${T}_bench_${c}_${p}.json 2>/dev/null
+done; done
+FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_fp64_gemm.json 2>/dev/null
+FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --prec tf32x3 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_tf32x3_gemm.json 2>/dev/null
+# ---- launch lists (serialised, cold; shares not absolutes)
+B3="python bench.py --steps 2 --warmup 1 $NB"
+B4="python bench.py --config c4 --steps 1 --warmup 1 $NB"
+B5="python bench.py --config c5 --steps 1 --warmup 1 $NB"
+$B3 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $O/${T}_launches_c3.csv $B3 > $O/ncu_l3.log 2>&1
+$B4 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/${T}_launches_c4_fp64.csv $B4 > $O/ncu_l4.log 2>&1
+$B5 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/${T}_launches_c5_fp64.csv $B5 > $O/ncu_l5.log 2>&1
+# ---- ncu --set full of the dominant kernels
+F="ncu --set full --clock-control none --import-source on"
+$B3 > /dev/null 2>&1 && $F -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf32 $B3 > $O/ncu_f1.log 2>&1
+$B3 > /dev/null 2>&1 && $F -k regex:k_clip_corners -s 1 -c 1 -o $O/${T}_prof_c3_extract $B3 > $O/ncu_f2.log 2>&1
+$B4 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2|k_fr_row0" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_fft $B4 > $O/ncu_f3.log 2>&1
+FCFS_ROUTE=gemm $B4 > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_fp64|k_gsum_fp64|k_hsum_fp64" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_gemm $B4 > $O/ncu_f4.log 2>&1
+B4t="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
+FCFS_ROUTE=gemm $B4t > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_tf32|k_gsum_tc|k_hsum_tc" -s 0 -c 3 -o $O/${T}_prof_c4_tf32_gemm $B4t > $O/ncu_f5.log 2>&1
+ls -la $O | grep $T
