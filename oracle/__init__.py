@@ -49,6 +49,8 @@ def _load():
         lib.oracle_extract.restype = ctypes.c_int
         lib.oracle_extract_polygons.argtypes = [P, P, P, i64, P, i64, i32, P, P, P, i64, P, P, P]
         lib.oracle_extract_polygons.restype = ctypes.c_int
+        lib.oracle_chop_rects.argtypes = [P, i64, i32, i32, i32, P, i64, P, P]
+        lib.oracle_chop_rects.restype = ctypes.c_int
         lib.oracle_coeffs.argtypes = [P, P, P, i64, i64, i32, P, P, i64, P, P, P, ctypes.c_int]
         lib.oracle_coeffs.restype = ctypes.c_int
         lib.oracle_window.argtypes = [i32, i32, ctypes.c_double, P, P, i64]
@@ -138,6 +140,26 @@ def extract_polygons(vx, vy, poly_ptr, T, clip_ptr=None):
     if rc != OR_OK:
         raise OracleError(f"oracle_extract_polygons failed rc={rc}")
     return dict(x=x[:cap], y=y[:cap], w=w[:cap], corner_ptr=cptr, area=area, K=cap)
+
+
+def chop_rects(rects, T, tiles_x, tiles_y):
+    """Rects (layout coordinates) chopped into T x T tiles: dict(rects (int32 [n,4], tile-local),
+    tile_ptr (int64 [tiles+1], row-major tiles), n)."""
+    lib = _load()
+    rects = np.ascontiguousarray(rects, dtype=np.int32).reshape(-1, 4)
+    nt = int(tiles_x) * int(tiles_y)
+    tp = np.zeros(nt + 1, np.int64)
+    n = ctypes.c_int64(0)
+    rc = lib.oracle_chop_rects(_ptr(rects), rects.shape[0], int(T), int(tiles_x), int(tiles_y), None, 0, _ptr(tp),
+                               ctypes.byref(n))
+    if rc not in (OR_OK, OR_E_CAPACITY):
+        raise OracleError(f"oracle_chop_rects failed rc={rc}")
+    out = np.zeros((max(n.value, 1), 4), np.int32)
+    rc = lib.oracle_chop_rects(_ptr(rects), rects.shape[0], int(T), int(tiles_x), int(tiles_y), _ptr(out), n.value,
+                               _ptr(tp), ctypes.byref(n))
+    if rc != OR_OK:
+        raise OracleError(f"oracle_chop_rects failed rc={rc}")
+    return dict(rects=out[:n.value], tile_ptr=tp, n=n.value)
 
 
 def window(M, N, r2=-1.0):

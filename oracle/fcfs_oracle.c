@@ -39,10 +39,12 @@
  * equal keys and drop zeros.  The area is computed twice (sum w x y and sum of
  * covered compressed-cell areas) and the two must agree.
  *
+ * Chopping (oracle_chop_rects): every rect intersected with every T x T tile it overlaps, pieces in
+ * tile-local coordinates, ordered by tile then rect.
  * Polygon vertex lists (oracle_extract_polygons): Alg. 2 lines 9-10 on every horizontal edge of
  * the clockwise list (+1 end, -1 start), counter-clockwise lists reversed, polygons summed.
  *
- * Parity is pinned in tests/test_oracle_pins.py (P1..P12 and E1..E8 of DESIGN.md).
+ * Parity is pinned in tests/test_oracle_pins.py (P1..P12 and E1..E10 of DESIGN.md).
  */
 #include <math.h>
 #include <stdint.h>
@@ -308,6 +310,52 @@ int oracle_extract_polygons(const int32_t *vx, const int32_t *vy, const int64_t 
     free(cand); free(area_poly); free(area_w);
     if (rc != OR_OK) return rc;
     return K > cap ? OR_E_CAPACITY : OR_OK;
+}
+
+/*
+ * Chopping a layout into tiles (the paper's flow: "chops polygons and places them in their
+ * corresponding tiles. Each tile is then transformed individually").  rects: int32[R][4]
+ * (x0, y0, x1, y1) half-open in layout coordinates, 0 <= x0 < x1 <= tiles_x T, 0 <= y0 < y1 <= tiles_y T.
+ * Tile (tx, ty) = [tx T, (tx+1) T) x [ty T, (ty+1) T), index ty * tiles_x + tx (row-major).  Every
+ * rect is intersected with every tile it overlaps; each non-empty piece is emitted in the tile's
+ * local coordinates (0 <= x0 < x1 <= T).  Pieces are ordered by tile, and by rect index within a
+ * tile.  out: int32[cap][4]; tile_ptr: int64[tiles+1]; *n_out = number of pieces.
+ */
+int oracle_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_x, int32_t tiles_y,
+                      int32_t *out, int64_t cap, int64_t *tile_ptr, int64_t *n_out) {
+    if (T <= 0 || tiles_x <= 0 || tiles_y <= 0 || R < 0 || tile_ptr == NULL || n_out == NULL) return OR_E_INVALID;
+    const int64_t W = (int64_t)tiles_x * T, H = (int64_t)tiles_y * T, nt = (int64_t)tiles_x * tiles_y;
+    for (int64_t r = 0; r < R; ++r) {
+        const int32_t *q = rects + 4 * r;
+        if (q[0] < 0 || q[1] < 0 || q[2] > W || q[3] > H || q[0] >= q[2] || q[1] >= q[3]) return OR_E_RANGE;
+    }
+    for (int64_t t = 0; t <= nt; ++t) tile_ptr[t] = 0;
+    /* pass 1: pieces per tile */
+    for (int64_t r = 0; r < R; ++r) {
+        const int32_t *q = rects + 4 * r;
+        for (int64_t ty = q[1] / T; ty * T < q[3]; ++ty)
+            for (int64_t tx = q[0] / T; tx * T < q[2]; ++tx) tile_ptr[ty * tiles_x + tx + 1] += 1;
+    }
+    for (int64_t t = 0; t < nt; ++t) tile_ptr[t + 1] += tile_ptr[t];
+    *n_out = tile_ptr[nt];
+    if (out == NULL || cap < tile_ptr[nt]) return tile_ptr[nt] > cap ? OR_E_CAPACITY : OR_OK;
+    /* pass 2: emit in rect order into each tile's slots */
+    int64_t *fill = (int64_t *)calloc((size_t)nt, sizeof(int64_t));
+    if (!fill) return OR_E_NOMEM;
+    for (int64_t r = 0; r < R; ++r) {
+        const int32_t *q = rects + 4 * r;
+        for (int64_t ty = q[1] / T; ty * T < q[3]; ++ty)
+            for (int64_t tx = q[0] / T; tx * T < q[2]; ++tx) {
+                const int64_t t = ty * tiles_x + tx, o = tile_ptr[t] + fill[t]++;
+                const int64_t ax = tx * T, ay = ty * T;
+                out[4 * o + 0] = (int32_t)((q[0] > ax ? q[0] : ax) - ax);
+                out[4 * o + 1] = (int32_t)((q[1] > ay ? q[1] : ay) - ay);
+                out[4 * o + 2] = (int32_t)((q[2] < ax + T ? q[2] : ax + T) - ax);
+                out[4 * o + 3] = (int32_t)((q[3] < ay + T ? q[3] : ay + T) - ay);
+            }
+    }
+    free(fill);
+    return OR_OK;
 }
 
 /* Neumaier compensated accumulator */

@@ -281,6 +281,37 @@ def rects_as_polygons(rects, T, clip_ptr=None) -> PolygonSet:
     return PolygonSet(T, V[:, 0].astype(np.int32), V[:, 1].astype(np.int32), pp, cp)
 
 
+# ------------------------------------------------------------------ layouts chopped into tiles (NEXT-3)
+
+@dataclasses.dataclass
+class Layout:
+    """Rects over a tiles_x T x tiles_y T layout (layout coordinates), to be chopped into T x T tiles."""
+    name: str
+    T: int
+    tiles_x: int
+    tiles_y: int
+    rects: np.ndarray      # int32 [R, 4], one group per rect
+
+
+def layout(seed: int = 0, T: int = 2048, tiles_x: int = 64, tiles_y: int = 64, lines_per_tile: int = 1200) -> Layout:
+    """c3-style standard-cell lines (rows of pitch 64 over the whole height, widths U{20..60}, lengths
+    U{40..400}, x0 U{0..W-1}) at c3's density, over a layout of tiles_x x tiles_y tiles of side T; lines
+    cross tile edges (the chop step splits them) and are clipped at the layout edge."""
+    rng = _rng(seed, 1 << 20)
+    Wd, Ht = tiles_x * T, tiles_y * T
+    n = lines_per_tile * tiles_x * tiles_y
+    row = rng.integers(0, Ht // 64, n)
+    width = rng.integers(20, 61, n)
+    yoff = rng.integers(0, 65 - width)
+    length = rng.integers(40, 401, n)
+    x0 = rng.integers(0, Wd, n)
+    y0 = 64 * row + yoff
+    x1 = np.minimum(x0 + length, Wd)
+    y1 = np.minimum(y0 + width, Ht)
+    r = np.stack([x0, y0, x1, y1], 1).astype(np.int32)
+    return Layout("layout", T, tiles_x, tiles_y, r)
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
 
 

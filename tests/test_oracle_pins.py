@@ -543,3 +543,56 @@ def test_E8_polygon_corners_give_paper_prop3(shape):
     F, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
     ref = np.array([_paper_prop3(V, int(m), int(n), T) for m, n in zip(ms, ns)])
     _check(T * F, ref, T * B + 1e-300, 1e-13, f"Prop.3 polygon {shape}")
+
+
+# ---------------------------------------------------------------- E9..E10: chopping a layout into tiles
+
+def _layout_raster(rects, W, H):
+    img = np.zeros((W, H), np.int64)
+    for x0, y0, x1, y1 in rects:
+        img[x0:x1, y0:y1] += 1
+    return img
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_E9_chop_reassembles_the_layout_raster(seed):
+    """Pieces are non-empty, inside [0,T]^2, and the tiles' rasters placed at their offsets reproduce
+    the raster of the whole layout (each rect its own group: rasters add)."""
+    rng = np.random.default_rng(seed)
+    T, tx, ty = 16, 5, 3
+    W, H = T * tx, T * ty
+    x0 = rng.integers(0, W - 1, 60); y0 = rng.integers(0, H - 1, 60)
+    x1 = np.minimum(x0 + rng.integers(1, 40, 60), W); y1 = np.minimum(y0 + rng.integers(1, 30, 60), H)
+    rects = np.stack([x0, y0, x1, y1], 1).astype(np.int32)
+    rects[0] = (0, 0, W, H)                               # spans every tile
+    rects[1] = (T - 1, T - 1, T + 1, T + 1)               # a 2x2 piece at a tile corner
+    ch = oracle.chop_rects(rects, T, tx, ty)
+    p = ch["rects"]
+    assert np.all(p[:, 0] >= 0) and np.all(p[:, 2] <= T) and np.all(p[:, 0] < p[:, 2]) and np.all(p[:, 1] < p[:, 3])
+    full = _layout_raster(rects, W, H)
+    re = np.zeros_like(full)
+    for t in range(tx * ty):
+        a, b = ch["tile_ptr"][t], ch["tile_ptr"][t + 1]
+        ox, oy = (t % tx) * T, (t // tx) * T
+        re[ox:ox + T, oy:oy + T] = _layout_raster(p[a:b], T, T)
+    assert np.array_equal(re, full)
+    assert ch["tile_ptr"][-1] == ch["n"]
+
+
+def test_E10_tile_coefficients_from_chopped_pieces_match_the_cropped_raster():
+    """F of one tile from its chopped pieces (extraction + coefficients) == the exact raster identity (P6)
+    on the layout raster cropped to the tile."""
+    lay = inputs.layout(seed=3, T=64, tiles_x=3, tiles_y=2, lines_per_tile=40)
+    ch = oracle.chop_rects(lay.rects, lay.T, lay.tiles_x, lay.tiles_y)
+    full = _layout_raster(lay.rects, lay.T * lay.tiles_x, lay.T * lay.tiles_y)
+    T = lay.T
+    for t in (0, 4):
+        a, b = ch["tile_ptr"][t], ch["tile_ptr"][t + 1]
+        e = oracle.extract(ch["rects"][a:b], T)
+        ms, ns = oracle.window(6, 6)
+        F, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
+        ox, oy = (t % lay.tiles_x) * T, (t // lay.tiles_x) * T
+        img = full[ox:ox + T, oy:oy + T].astype(np.float64)
+        D = np.fft.fft2(img)
+        ref = D[ms % T, ns % T] * _cell_transfer(ms, T) * _cell_transfer(ns, T) / (T * T)
+        _check(F, ref, B + 1e-300, 1e-12, f"tile {t}")
