@@ -138,6 +138,25 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
                                         void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Layout -> tiles (the paper's flow: "chops polygons and places them in their corresponding tiles.
+ * Each tile is then transformed individually"; reading A17).
+ *
+ * rects      int32 [R][4] (x0, y0, x1, y1) half-open in layout coordinates, device,
+ *            0 <= x0 < x1 <= tiles_x T, 0 <= y0 < y1 <= tiles_y T (else FCFS_E_RANGE).
+ * Tile (tx, ty) = [tx T, (tx+1) T) x [ty T, (ty+1) T), index ty * tiles_x + tx.
+ * out_rects  int32 [cap][4] out: every rect cut at the tile edges into non-empty pieces in tile-local
+ *            coordinates (0 <= x0 < x1 <= T), ordered by tile, then by rect (deterministic).
+ * tile_ptr   int64 [tiles_x tiles_y + 1] out: CSR of pieces per tile — pass it as clip_ptr (with
+ *            group_ptr NULL) to fcfs_vertices_from_rects to get every tile's corners as one batch.
+ * n_host     out (host): the number of pieces (written also when it exceeds cap: FCFS_E_CAPACITY).
+ * The call synchronises `stream` once.  Limits: tiles and pieces < 2^31, tiles_x T and tiles_y T < 2^31.
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_chop_workspace_bytes(int64_t R, int64_t cap, int32_t tiles_x, int32_t tiles_y);
+fcfs_status fcfs_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_x, int32_t tiles_y,
+                            int32_t *out_rects, int64_t cap, int64_t *tile_ptr, int64_t *n_host,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * a2-a5 — coefficients of ONE clip: phase reduction + twiddles (a2), the separable
  * contraction P = A diag(w) B^T over cos/sin quadrant rows (a3), axes + DC (a4) and the
  * window / pupil epilogue with exact conj mirroring F[-m,-n] = conj F[m,n] (a5).

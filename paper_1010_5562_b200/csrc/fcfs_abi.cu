@@ -64,6 +64,11 @@ fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, co
                              const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
                              int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
                              size_t ws_bytes, cudaStream_t s);
+// chop.cu
+size_t chop_workspace_bytes(int64_t R, int64_t cap, int64_t tiles);
+fcfs_status chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_x, int32_t tiles_y,
+                       int32_t *out, int64_t cap, int64_t *tile_ptr, int64_t *n_host, void *ws, size_t ws_bytes,
+                       cudaStream_t s);
 // contract_tf32.cu
 fcfs_status tf32_supported(const GemmPlan &plan, int32_t T);
 fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t T, double *P_ws,
@@ -339,6 +344,30 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
     StageScope scope(kStageExtract, (cudaStream_t)stream);
     return extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
                    K_total_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t fcfs_chop_workspace_bytes(int64_t R, int64_t cap, int32_t tiles_x, int32_t tiles_y) {
+    if (R < 0 || cap < 0 || tiles_x < 1 || tiles_y < 1) return 0;
+    return chop_workspace_bytes(R, cap, (int64_t)tiles_x * tiles_y);
+}
+
+fcfs_status fcfs_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_x, int32_t tiles_y,
+                            int32_t *out_rects, int64_t cap, int64_t *tile_ptr, int64_t *n_host, void *ws,
+                            size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    if (R < 0 || (R > 0 && !rects) || tiles_x < 1 || tiles_y < 1 || !tile_ptr || !n_host || cap < 0 ||
+        (cap > 0 && !out_rects) || (int64_t)tiles_x * tiles_y >= (int64_t(1) << 31) ||
+        (int64_t)tiles_x * T >= (int64_t(1) << 31) || (int64_t)tiles_y * T >= (int64_t(1) << 31) ||
+        cap >= (int64_t(1) << 31)) {
+        set_error("fcfs_chop_rects: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageExtract, (cudaStream_t)stream);
+    return chop_rects(rects, R, T, tiles_x, tiles_y, out_rects, cap, tile_ptr, n_host, ws, ws_bytes,
+                      (cudaStream_t)stream);
 }
 
 size_t fcfs_polygons_workspace_bytes(int64_t V, int64_t P, int64_t B) {

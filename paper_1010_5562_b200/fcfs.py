@@ -69,6 +69,10 @@ _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _
 _lib.fcfs_vertices_from_polygons.restype = _i32
 _lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
 _lib.fcfs_coeffs_workspace_bytes.restype = _sz
+_lib.fcfs_chop_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32]
+_lib.fcfs_chop_workspace_bytes.restype = _sz
+_lib.fcfs_chop_rects.argtypes = [_P, _i64, _i32, _i32, _i32, _P, _i64, _P, ctypes.POINTER(_i64), _P, _sz, _P]
+_lib.fcfs_chop_rects.restype = _i32
 _lib.fcfs_coeffs_route.argtypes = [_i64, _i32, _WP, _i32, _SP]
 _lib.fcfs_coeffs_route.restype = _i32
 _lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _P, _P, _sz, _P]
@@ -93,7 +97,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
-            "fcfs_coeffs_route"]
+            "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects"]
 STAGES = ("extract", "contract", "epilogue")
 
 
@@ -222,6 +226,43 @@ def vertices_from_polygons(vx, vy, poly_ptr, T, clip_ptr=None, stream=None):
     _check(st, "fcfs_vertices_from_polygons")
     k = K.value
     return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
+
+
+class ChopPlan:
+    """Pre-allocated outputs + workspace for repeated ``fcfs_chop_rects`` calls (layout -> tiles).
+    cap: piece capacity (default R + R/2 + 1024; a call that needs more raises E_CAPACITY)."""
+
+    def __init__(self, R, T, tiles_x, tiles_y, cap=None, device="cuda"):
+        self.R, self.T, self.tx, self.ty = int(R), int(T), int(tiles_x), int(tiles_y)
+        self.cap = int(cap) if cap is not None else self.R + self.R // 2 + 1024
+        self.out = torch.empty((max(self.cap, 1), 4), dtype=torch.int32, device=device)
+        self.tile_ptr = torch.empty(self.tx * self.ty + 1, dtype=torch.int64, device=device)
+        self.ws = _ws(_lib.fcfs_chop_workspace_bytes(self.R, self.cap, self.tx, self.ty), device)
+        self.n = 0
+
+    def run(self, rects, stream=None):
+        n = ctypes.c_int64(0)
+        st = _lib.fcfs_chop_rects(_ptr(rects), self.R, self.T, self.tx, self.ty, _ptr(self.out), self.cap,
+                                  _ptr(self.tile_ptr), ctypes.byref(n), _ptr(self.ws), self.ws.numel(),
+                                  _stream(stream))
+        self.n = n.value
+        _check(st, "fcfs_chop_rects")
+        return self.n
+
+
+def chop_rects(rects, T, tiles_x, tiles_y, stream=None):
+    """Layout rects (int32 cuda [R,4]) cut into T x T tiles: dict(rects (tile-local pieces in tile order),
+    tile_ptr (int64 [tiles+1]), n).  Retries once with the exact capacity if the default is too small."""
+    R = rects.shape[0]
+    plan = ChopPlan(R, T, tiles_x, tiles_y, device=rects.device)
+    try:
+        plan.run(rects.contiguous(), stream)
+    except FcfsError as ex:
+        if ex.status != E_CAPACITY:
+            raise
+        plan = ChopPlan(R, T, tiles_x, tiles_y, cap=plan.n if plan.n else None, device=rects.device)
+        plan.run(rects.contiguous(), stream)
+    return dict(rects=plan.out[:plan.n], tile_ptr=plan.tile_ptr, n=plan.n)
 
 
 class PolygonsPlan:

@@ -576,3 +576,54 @@ def test_fft_route_small_T2_many_subrows(fcfs, route, prec):
     g, F = _clip_coeffs(fcfs, wl, prec, M=9, N=10, r2=-1.0)
     ms, ns, Fr, B = _oracle_window(g, wl.T, 9, 10)
     _assert_parity(F, Fr, B, prec, "T2=64", ms, ns)
+
+
+# ------------------------------------------------------------------ NEXT-3: a layout chopped into tiles
+
+def test_chop_bit_exact_and_errors(fcfs):
+    rng = np.random.default_rng(5)
+    T, tx, ty = 64, 5, 3
+    W, H = T * tx, T * ty
+    x0 = rng.integers(0, W - 1, 400); y0 = rng.integers(0, H - 1, 400)
+    x1 = np.minimum(x0 + rng.integers(1, 200, 400), W); y1 = np.minimum(y0 + rng.integers(1, 150, 400), H)
+    rects = np.stack([x0, y0, x1, y1], 1).astype(np.int32)
+    rects[0] = (0, 0, W, H)
+    rects[1] = (T - 1, T - 1, T + 1, T + 1)
+    e = oracle.chop_rects(rects, T, tx, ty)
+    g = fcfs.chop_rects(_dev(rects, torch.int32), T, tx, ty)
+    assert g["n"] == e["n"]
+    assert np.array_equal(g["rects"].cpu().numpy(), e["rects"])
+    assert np.array_equal(g["tile_ptr"].cpu().numpy(), e["tile_ptr"])
+    # capacity: a too-small plan reports the count, the helper retries
+    plan = fcfs.ChopPlan(len(rects), T, tx, ty, cap=10)
+    with pytest.raises(fcfs.FcfsError) as ei:
+        plan.run(_dev(rects, torch.int32))
+    assert ei.value.status == fcfs.E_CAPACITY and plan.n == e["n"]
+    # empty layout; a rect outside the layout
+    g = fcfs.chop_rects(torch.zeros((0, 4), dtype=torch.int32, device="cuda"), T, tx, ty)
+    assert g["n"] == 0 and int(g["tile_ptr"].sum()) == 0
+    with pytest.raises(fcfs.FcfsError) as ei:
+        fcfs.chop_rects(_dev(np.array([[0, 0, W + 1, 5]]), torch.int32), T, tx, ty)
+    assert ei.value.status == fcfs.E_RANGE
+
+
+@pytest.mark.parametrize("prec", ["tf32x3", "fp64"])
+def test_layout_tiles_end_to_end(fcfs, prec):
+    """Layout -> chop -> batched extraction -> batched pupil coefficients; seeded tiles against the
+    oracle's chop + extraction + direct sums."""
+    lay = inputs.layout(seed=2, T=2048, tiles_x=6, tiles_y=5)
+    ch = fcfs.chop_rects(_dev(lay.rects, torch.int32), lay.T, lay.tiles_x, lay.tiles_y)
+    g = fcfs.vertices_from_rects(ch["rects"], lay.T, None, ch["tile_ptr"])
+    r2 = inputs.pupil_r2(lay.T)
+    M = int(np.floor(np.sqrt(r2)))
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], lay.T, M, M, r2, "pupil",
+                            prec).cpu().numpy()
+    eo = oracle.chop_rects(lay.rects, lay.T, lay.tiles_x, lay.tiles_y)
+    ex = oracle.extract(eo["rects"], lay.T, None, eo["tile_ptr"])
+    _assert_extract_equal(g, ex)
+    ms, ns = oracle.window(M, M, r2)
+    cp = ex["corner_ptr"]
+    for t in (0, 7, 29):
+        sl = slice(cp[t], cp[t + 1])
+        Fr, B = oracle.coeffs(ex["x"][sl], ex["y"][sl], ex["w"][sl], ex["area"][t], lay.T, ms, ns)
+        _assert_parity(F[t], Fr, B, prec, f"tile {t}", ms, ns)
