@@ -38,7 +38,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "layout"],
+                    help="layout: c3-style lines over a tiles x tiles layout of T=2048 tiles, chopped into tiles "
+                         "on the GPU (fcfs_chop_rects) and transformed as one batch (the paper's flow, P:1060-1062)")
+    ap.add_argument("--tiles", type=int, default=64, help="layout: tiles per side")
     ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3", "f16x3"])
     ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
     ap.add_argument("--shard", default="rows", choices=["rows", "vblock"],
@@ -63,7 +66,17 @@ def load_peaks():
             "fallback"
 
 
-def workload(cfg, seed, rank, clips):
+def workload(cfg, seed, rank, clips, tiles=64):
+    if cfg == "layout":
+        T = 2048
+        lay = inputs.layout(seed + rank, T=T, tiles_x=tiles, tiles_y=tiles)
+        r2 = inputs.pupil_r2(T)
+        M = int(math.floor(math.sqrt(r2)))
+        # clip_ptr is a placeholder of the tile count (the tiles are made on the GPU by the chop step)
+        wl = inputs.Workload("layout", T, M, M, r2, lay.rects, None, np.zeros(tiles * tiles + 1, np.int64),
+                             ("tf32x3",))
+        wl.layout = lay
+        return wl
     if cfg == "c3":
         # weak scaling: each rank its own clip range (seed streams (seed, clip) with clip offset by rank)
         T = 2048
@@ -130,6 +143,13 @@ def cpu_baseline(wl, target_s, prec):
     import oracle
     cores = oracle.max_threads()
     ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    chop_s = 0.0
+    if getattr(wl, "layout", None) is not None:
+        lay = wl.layout
+        t0 = time.perf_counter()
+        ch = oracle.chop_rects(lay.rects, lay.T, lay.tiles_x, lay.tiles_y)
+        chop_s = time.perf_counter() - t0
+        wl = inputs.Workload("layout tiles", wl.T, wl.M, wl.N, wl.r2, ch["rects"], None, ch["tile_ptr"], ())
     terms = 0
     t0 = time.perf_counter()
     b = 0
@@ -158,7 +178,9 @@ def cpu_baseline(wl, target_s, prec):
         sample = f"{nclips} clips (extraction + all {len(ms)} coefficients each)"
         if time.perf_counter() - t0 > target_s or nclips >= wl.B:
             break
-    dt = time.perf_counter() - t0
+    dt = time.perf_counter() - t0 + chop_s * nclips / max(wl.B, 1)
+    if chop_s:
+        sample += f"; + the host chop of the whole layout ({chop_s:.2f} s) charged pro rata"
     return {"value": terms / dt / 1e9, "unit": "Gterm/s", "cores": cores, "kind": "oracle", "sample": sample,
             "seconds": round(dt, 3)}
 
@@ -167,8 +189,8 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle (this tier's reference arm) on the same workload."""
     if rank != 0:
         return
-    wl = workload(args.config, args.seed, 0, args.clips)
-    prec = args.prec or ("tf32x3" if args.config == "c3" else "fp64")
+    wl = workload(args.config, args.seed, 0, args.clips, args.tiles)
+    prec = args.prec or ("tf32x3" if args.config in ("c3", "layout") else "fp64")
     per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_baseline(wl, per_step / 4, prec)
@@ -210,6 +232,12 @@ def config_dict(args, wl, prec, world):
          "l2": "flushed between steps (512 MiB write, outside the timed events)"}
     if getattr(args, "input", "rects") == "polygons":
         d["input"] = "each rect as a clockwise 4-vertex polygon (fcfs_vertices_from_polygons)"
+    if getattr(wl, "layout", None) is not None:
+        lay = wl.layout
+        d["workload"] = (f"layout: {lay.tiles_x}x{lay.tiles_y} tiles of T={lay.T} ({lay.tiles_x * lay.T}^2 grid), "
+                         f"R={wl.R} c3-style lines; step = chop into tiles + extraction + pupil coefficients "
+                         f"(|m|,|n|<={wl.M}, r2={wl.r2:.2f}, W_out={W}/tile)")
+        d["tiles"] = lay.tiles_x * lay.tiles_y
     return d
 
 
@@ -231,8 +259,8 @@ def main():
     from paper_1010_5562_b200 import fcfs
 
     fcfs.device_check()
-    prec = args.prec or ("tf32x3" if args.config == "c3" else "fp64")
-    wl = workload(args.config, args.seed, rank, args.clips)
+    prec = args.prec or ("tf32x3" if args.config in ("c3", "layout") else "fp64")
+    wl = workload(args.config, args.seed, rank, args.clips, args.tiles)
     layout = "pupil" if wl.r2 >= 0 else "dense"
     W = inputs.window_count(wl.M, wl.N, wl.r2)
 
@@ -243,7 +271,17 @@ def main():
     cp = None if wl.clip_ptr is None else torch.from_numpy(wl.clip_ptr).to(dev)
     mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
     G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
-    if args.input == "polygons":
+    if args.config == "layout":
+        # layout -> tiles on the GPU, then the tiles' corners as one batch
+        lay = wl.layout
+        chop = fcfs.ChopPlan(wl.R, wl.T, lay.tiles_x, lay.tiles_y, device=dev)
+        n_pieces = chop.run(rects)
+        vp = fcfs.VerticesPlan(n_pieces, wl.T, n_pieces, wl.B, 1, grouped=False, device=dev)
+
+        def extract():
+            chop.run(rects)
+            return vp.run(chop.out[:n_pieces], None, chop.tile_ptr)
+    elif args.input == "polygons":
         if wl.group_ptr is not None:
             raise SystemExit("--input polygons needs a workload with one group per rect (c3, c4, c5)")
         ps = inputs.rects_as_polygons(wl.rects, wl.T, wl.clip_ptr)
@@ -417,7 +455,7 @@ def main():
     if not args.no_e2e and args.input == "rects":
         e2e_steps = max(2, min(args.steps, 5))
         h2d_bytes = int(rects_h.numel() * 4)
-        if wl.B > 1 and wl.B % args.e2e_split == 0 and wl.group_ptr is None:
+        if wl.B > 1 and wl.B % args.e2e_split == 0 and wl.group_ptr is None and args.config != "layout":
             S = args.e2e_split
             bs = wl.B // S
             r_per = wl.clip_ptr[bs] - wl.clip_ptr[0]        # rects per sub-batch (equal clip sizes, c3)
@@ -473,7 +511,7 @@ def main():
             ea.record()
             for _ in range(e2e_steps):
                 rects.copy_(rects_h, non_blocking=True)
-                vp.run(rects, gp, cp)
+                extract()
                 o = coeffs()
                 out_h.copy_(o.reshape(-1), non_blocking=True)
             eb.record()

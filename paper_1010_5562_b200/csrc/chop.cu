@@ -5,9 +5,10 @@
 //
 //   1. k_chop_count: thread per rect: range check, number of overlapped tiles;
 //   2. CUB exclusive scan: each rect's first piece;
-//   3. k_chop_emit: thread per rect: its pieces (tile id, tile-local half-open rect), ty-major;
-//   4. CUB radix sort of (tile id, piece index) — stable, so pieces stay in rect order within a tile;
-//   5. k_chop_gather: pieces in tile order; k_chop_tile_ptr: CSR over tiles by lower_bound.
+//   3. k_chop_emit: thread per rect: one (tile id, rect index) pair per overlapped tile, ty-major;
+//   4. CUB radix sort of the pairs by tile id — stable, so pieces stay in rect order within a tile;
+//   5. k_chop_gather: each sorted pair's piece (the rect cut to its tile, tile-local) in tile order;
+//      k_chop_tile_ptr: CSR over tiles by lower_bound.
 // One stream sync (the piece count).
 #include <cub/cub.cuh>
 
@@ -19,7 +20,6 @@ struct ChopWs {
     int64_t *cnt, *off;
     uint32_t *key_a, *key_b;
     int32_t *idx_a, *idx_b;
-    int4 *piece;
     int64_t *n;
     int32_t *err;
     void *cub_tmp;
@@ -43,7 +43,7 @@ __global__ void k_chop_count(const int4 *__restrict__ rects, int64_t R, int32_t 
 
 __global__ void k_chop_emit(const int4 *__restrict__ rects, int64_t R, int32_t T, int32_t tiles_x,
                             const int64_t *__restrict__ cnt, const int64_t *__restrict__ off, int64_t cap,
-                            uint32_t *keys, int32_t *idx, int4 *piece) {
+                            uint32_t *keys, int32_t *idx) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
         if (cnt[r] == 0) continue;
         const int4 q = rects[r];
@@ -51,18 +51,21 @@ __global__ void k_chop_emit(const int4 *__restrict__ rects, int64_t R, int32_t T
         for (int32_t ty = q.y / T; (int64_t)ty * T < q.w; ++ty)
             for (int32_t tx = q.x / T; (int64_t)tx * T < q.z; ++tx, ++o) {
                 if (o >= cap) return;
-                const int32_t ax = tx * T, ay = ty * T;
                 keys[o] = (uint32_t)ty * (uint32_t)tiles_x + (uint32_t)tx;
-                idx[o] = (int32_t)o;
-                piece[o] = make_int4(max(q.x, ax) - ax, max(q.y, ay) - ay, min(q.z, ax + T) - ax, min(q.w, ay + T) - ay);
+                idx[o] = (int32_t)r;
             }
     }
 }
 
-__global__ void k_chop_gather(const int32_t *__restrict__ idx, const int4 *__restrict__ piece, int64_t n,
-                              int4 *out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = piece[idx[i]];
+// piece i of the tile order: rect idx[i] cut to tile keys[i], in tile-local coordinates
+__global__ void k_chop_gather(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
+                              const int32_t *__restrict__ idx, int64_t n, int32_t T, int32_t tiles_x, int4 *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 q = rects[idx[i]];
+        const uint32_t t = keys[i];
+        const int32_t ax = (int32_t)(t % (uint32_t)tiles_x) * T, ay = (int32_t)(t / (uint32_t)tiles_x) * T;
+        out[i] = make_int4(max(q.x, ax) - ax, max(q.y, ay) - ay, min(q.z, ax + T) - ax, min(q.w, ay + T) - ay);
+    }
 }
 
 // tile_ptr[t] = first sorted piece with tile id >= t, t in [0, tiles]
@@ -99,7 +102,6 @@ static void carve_chop(Carver &cv, int64_t R, int64_t cap, int64_t tiles, ChopWs
     w.key_b = cv.take<uint32_t>(c1);
     w.idx_a = cv.take<int32_t>(c1);
     w.idx_b = cv.take<int32_t>(c1);
-    w.piece = cv.take<int4>(c1);
     w.n = cv.take<int64_t>(1);
     w.err = cv.take<int32_t>(4);
     w.cub_bytes = chop_cub_bytes(R, cap, tiles);
@@ -154,7 +156,7 @@ fcfs_status chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles
             return FCFS_E_CAPACITY;
         }
         k_chop_emit<<<(unsigned)blocks, threads, 0, s>>>((const int4 *)rects, R, T, tiles_x, W.cnt, W.off, cap,
-                                                         W.key_a, W.idx_a, W.piece);
+                                                         W.key_a, W.idx_a);
         FCFS_CHECK_LAUNCH("k_chop_emit");
         tb = W.cub_bytes;
         FCFS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, W.key_a, W.key_b, W.idx_a, W.idx_b, (int)n, 0,
@@ -163,7 +165,8 @@ fcfs_status chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles
         int64_t gb = (n + threads - 1) / threads;
         if (gb > 148 * 16) gb = 148 * 16;
         if (gb < 1) gb = 1;
-        k_chop_gather<<<(unsigned)gb, threads, 0, s>>>(W.idx_b, W.piece, n, (int4 *)out);
+        k_chop_gather<<<(unsigned)gb, threads, 0, s>>>((const int4 *)rects, W.key_b, W.idx_b, n, T, tiles_x,
+                                                       (int4 *)out);
         FCFS_CHECK_LAUNCH("k_chop_gather");
     } else if (n_host) {
         *n_host = 0;
