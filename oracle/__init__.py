@@ -51,6 +51,8 @@ def _load():
         lib.oracle_extract_polygons.restype = ctypes.c_int
         lib.oracle_chop_rects.argtypes = [P, i64, i32, i32, i32, P, i64, P, P]
         lib.oracle_chop_rects.restype = ctypes.c_int
+        lib.oracle_haar.argtypes = [P, P, P, i64, i32, P]
+        lib.oracle_haar.restype = ctypes.c_int
         lib.oracle_coeffs.argtypes = [P, P, P, i64, i64, i32, P, P, i64, P, P, P, ctypes.c_int]
         lib.oracle_coeffs.restype = ctypes.c_int
         lib.oracle_window.argtypes = [i32, i32, ctypes.c_double, P, P, i64]
@@ -160,6 +162,19 @@ def chop_rects(rects, T, tiles_x, tiles_y):
     if rc != OR_OK:
         raise OracleError(f"oracle_chop_rects failed rc={rc}")
     return dict(rects=out[:n.value], tile_ptr=tp, n=n.value)
+
+
+def haar(x, y, w, T):
+    """Continuous Haar transform of one clip's corners: float64 [T, T] in the layout of reading A18."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    w = np.ascontiguousarray(w, dtype=np.int32)
+    out = np.zeros((int(T), int(T)), np.float64)
+    rc = lib.oracle_haar(_ptr(x), _ptr(y), _ptr(w), x.shape[0], int(T), _ptr(out))
+    if rc != OR_OK:
+        raise OracleError(f"oracle_haar failed rc={rc}")
+    return out
 
 
 def window(M, N, r2=-1.0):

@@ -39,12 +39,13 @@
  * equal keys and drop zeros.  The area is computed twice (sum w x y and sum of
  * covered compressed-cell areas) and the two must agree.
  *
+ * Haar (oracle_haar): the continuous Haar transform from child-cell areas of the corner form.
  * Chopping (oracle_chop_rects): every rect intersected with every T x T tile it overlaps, pieces in
  * tile-local coordinates, ordered by tile then rect.
  * Polygon vertex lists (oracle_extract_polygons): Alg. 2 lines 9-10 on every horizontal edge of
  * the clockwise list (+1 end, -1 start), counter-clockwise lists reversed, polygons summed.
  *
- * Parity is pinned in tests/test_oracle_pins.py (P1..P12 and E1..E10 of DESIGN.md).
+ * Parity is pinned in tests/test_oracle_pins.py (P1..P12, E1..E10 and H1..H4 of DESIGN.md).
  */
 #include <math.h>
 #include <stdint.h>
@@ -355,6 +356,57 @@ int oracle_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_
             }
     }
     free(fill);
+    return OR_OK;
+}
+
+/*
+ * Continuous Haar transform of one clip (NEXT-4; the paper's CHT, Lemma polyip P:633-642,
+ * IntersectionArea Alg. 1): the dyadic 2D (nonstandard) Haar basis over [0,T)^2, T = 2^J,
+ *   phi_{j,kx,ky} = (2^j / T) 1[cell_{j,kx,ky}],  cell side T / 2^j,
+ *   psi^{(ab)}_{j,kx,ky} = sum_{n,m} a_n b_m phi_{j+1, 2kx+n, 2ky+m},  g = (1, 1)/sqrt2, h = (1, -1)/sqrt2,
+ * (n indexes x, m indexes y).  Coefficients are inner products with f = sum_k w_k H(x - x_k) H(y - y_k):
+ *   X_{0,0,0} = area(f) / T,
+ *   C^{(ab)}_{j,kx,ky} = (2^j / T) sum_{n,m} s^a_n s^b_m A_{j+1, 2kx+n, 2ky+m},  s^g = (1, 1), s^h = (1, -1),
+ * with A = the integral of f over a child cell, computed from the corners (the corner form of the
+ * intersection area of Alg. 1): A([a1,a2) x [b1,b2)) = sum_k w_k clamp(a2 - max(a1, x_k)) clamp(b2 - max(b1, y_k)).
+ * Areas are exact integers (int64 / __int128); each coefficient is an integer times a power of two.
+ * Output layout (reading A18): out[r * T + c], r = y-index, c = x-index: (0,0) = X_{0,0,0}; level j:
+ * hg at (ky, 2^j + kx), gh at (2^j + ky, kx), hh at (2^j + ky, 2^j + kx).
+ */
+static __int128 or_area(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K,
+                        int64_t a1, int64_t a2, int64_t b1, int64_t b2) {
+    __int128 s = 0;
+    for (int64_t k = 0; k < K; ++k) {
+        int64_t lx = a2 - (x[k] > a1 ? x[k] : a1), ly = b2 - (y[k] > b1 ? y[k] : b1);
+        if (lx <= 0 || ly <= 0) continue;
+        s += (__int128)w[k] * lx * ly;
+    }
+    return s;
+}
+
+int oracle_haar(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int32_t T, double *out) {
+    if (T < 2 || (T & (T - 1)) != 0 || out == NULL) return OR_E_INVALID;
+    int J = 0;
+    while ((1 << J) < T) ++J;
+    out[0] = (double)or_area(x, y, w, K, 0, T, 0, T) / (double)T;
+    for (int j = 0; j < J; ++j) {
+        const int64_t n = (int64_t)1 << j, s = T >> j, h = s / 2;
+        const double scale = (double)n / (double)T;
+        for (int64_t ky = 0; ky < n; ++ky)
+            for (int64_t kx = 0; kx < n; ++kx) {
+                const int64_t a1 = kx * s, b1 = ky * s;
+                __int128 A[2][2];   /* A[n][m]: child 2kx+n (x), 2ky+m (y) */
+                for (int i = 0; i < 2; ++i)
+                    for (int l = 0; l < 2; ++l)
+                        A[i][l] = or_area(x, y, w, K, a1 + i * h, a1 + (i + 1) * h, b1 + l * h, b1 + (l + 1) * h);
+                const __int128 hg = A[0][0] + A[0][1] - A[1][0] - A[1][1];
+                const __int128 gh = A[0][0] - A[0][1] + A[1][0] - A[1][1];
+                const __int128 hh = A[0][0] - A[0][1] - A[1][0] + A[1][1];
+                out[ky * T + (n + kx)] = (double)hg * scale;
+                out[(n + ky) * T + kx] = (double)gh * scale;
+                out[(n + ky) * T + (n + kx)] = (double)hh * scale;
+            }
+    }
     return OR_OK;
 }
 

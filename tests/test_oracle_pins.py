@@ -596,3 +596,76 @@ def test_E10_tile_coefficients_from_chopped_pieces_match_the_cropped_raster():
         D = np.fft.fft2(img)
         ref = D[ms % T, ns % T] * _cell_transfer(ms, T) * _cell_transfer(ns, T) / (T * T)
         _check(F, ref, B + 1e-300, 1e-12, f"tile {t}")
+
+
+# ---------------------------------------------------------------- H1..H4: continuous Haar transform (NEXT-4)
+
+def _dht(img):
+    """Orthonormal 2D (nonstandard) Haar filter bank on the unit-cell raster img[x, y]: the scaling
+    coefficients of unit cells are the raster values (2^J / T = 1), then X_j = (sum of 4 children) / 2
+    and the three details with h = (1, -1) / sqrt2, g = (1, 1) / sqrt2.  Output out[y, x]."""
+    T = img.shape[0]
+    out = np.zeros((T, T))
+    X = img.astype(np.float64)
+    n = T // 2
+    while n >= 1:
+        a, b, c, d = X[0::2, 0::2], X[0::2, 1::2], X[1::2, 0::2], X[1::2, 1::2]   # (n, m) = (0,0) (0,1) (1,0) (1,1)
+        out[0:n, n:2 * n] = ((a + b - c - d) / 2).T    # hg: h along x
+        out[n:2 * n, 0:n] = ((a - b + c - d) / 2).T    # gh
+        out[n:2 * n, n:2 * n] = ((a - b - c + d) / 2).T
+        X = (a + b + c + d) / 2
+        n //= 2
+    out[0, 0] = X[0, 0]
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_H1_haar_equals_the_discrete_haar_of_the_raster(seed):
+    """CHT == DHT for rectilinear patterns on the unit lattice: the oracle (child-cell areas
+    of the corner form) against the filter-bank FWT of the raster, exactly (dyadic values)."""
+    rng = np.random.default_rng(seed)
+    T = 32
+    rects = inputs.random_rects(rng, 12, T, 1, 14)
+    gp = np.array([0, 5, 12], np.int64)                 # two union groups, summed (overlaps give f = 2)
+    e = oracle.extract(rects, T, gp)
+    H = oracle.haar(e["x"], e["y"], e["w"], T)
+    assert np.array_equal(H, _dht(_raster(rects, T, gp)))
+
+
+def test_H2_parseval_and_dc():
+    rng = np.random.default_rng(4)
+    T = 64
+    rects = inputs.random_rects(rng, 20, T, 2, 30)
+    e = oracle.extract(rects, T)
+    H = oracle.haar(e["x"], e["y"], e["w"], T)
+    img = _raster(rects, T)
+    assert H[0, 0] == e["area"][0] / T
+    assert abs((H ** 2).sum() - (img.astype(np.float64) ** 2).sum()) <= 1e-9 * (img ** 2).sum()
+
+
+def test_H3_hh_details_are_local_to_corners():
+    """psi^(hh) of a cell is non-zero only if a corner lies strictly inside the cell (the h factor is a
+    tent supported inside the cell along each axis)."""
+    rng = np.random.default_rng(5)
+    T = 32
+    rects = inputs.random_rects(rng, 6, T, 2, 12)
+    e = oracle.extract(rects, T)
+    H = oracle.haar(e["x"], e["y"], e["w"], T)
+    n = 1
+    while n < T:
+        s = T // n
+        for ky in range(n):
+            for kx in range(n):
+                inside = np.any((e["x"] > kx * s) & (e["x"] < (kx + 1) * s) & (e["y"] > ky * s) & (e["y"] < (ky + 1) * s))
+                if not inside:
+                    assert H[n + ky, n + kx] == 0
+        n *= 2
+
+
+def test_H4_single_rect_hand_values():
+    """[1,5) x [2,7) in T = 8: DC = 20/8; level 0 hg = (A00 + A01 - A10 - A11) / 8 with the 4x4 quadrant
+    areas A00 = 3*2, A01 = 3*3, A10 = 1*2, A11 = 1*3 -> (6 + 9 - 2 - 3) / 8 = 1.25 (hand computation)."""
+    e = oracle.extract(np.array([[1, 2, 5, 7]], np.int32), 8)
+    H = oracle.haar(e["x"], e["y"], e["w"], 8)
+    assert H[0, 0] == 2.5 and H[0, 1] == 1.25
+    assert H[1, 0] == (6 - 9 + 2 - 3) / 8 and H[1, 1] == (6 - 9 - 2 + 3) / 8
