@@ -138,6 +138,22 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
                                         void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * The continuous Haar transform of B clips (the paper's CHT / PCHT; reading
+ * A18): the dyadic nonstandard 2D Haar basis over [0,T)^2, T = 2^J (2 <= T <= 4096), J = log2 T
+ * levels, h = (1,-1)/sqrt2 (first half positive), psi^(hg) = h along x.
+ *
+ * corner_ptr int64 [B+1] CSR over corners (device), or NULL for B == 1;  x, y, w  int32 [K] corners
+ *            as produced by fcfs_vertices_from_* (any order);  area  int64 [B] (device).
+ * out        double [B][T][T] (device): out[b][r][c], r = y index: (0,0) = X_{0,0,0} = area/T; level j:
+ *            hg at (ky, 2^j + kx), gh at (2^j + ky, kx), hh at (2^j + ky, 2^j + kx).  Every value is
+ *            exact (an integer times 2^j / T).  Workspace: 5 (T^2 - 1) / 3 int64 per clip.
+ * ------------------------------------------------------------------------------------------ */
+size_t fcfs_haar_workspace_bytes(int64_t B, int32_t T);
+fcfs_status fcfs_haar(const int64_t *corner_ptr, int64_t B, int64_t K, const int32_t *x, const int32_t *y,
+                      const int32_t *w, const int64_t *area, int32_t T, double *out, void *ws,
+                      size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * Layout -> tiles (the paper's flow: "chops polygons and places them in their corresponding tiles.
  * Each tile is then transformed individually"; reading A17).
  *

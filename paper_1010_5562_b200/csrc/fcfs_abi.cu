@@ -64,6 +64,11 @@ fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, co
                              const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
                              int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
                              size_t ws_bytes, cudaStream_t s);
+// haar.cu
+size_t haar_workspace_bytes(int64_t B, int32_t T);
+fcfs_status haar_clips(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *corner_ptr, int64_t B,
+                       int64_t K, const int64_t *area, int32_t T, double *out, void *ws, size_t ws_bytes,
+                       cudaStream_t s);
 // chop.cu
 size_t chop_workspace_bytes(int64_t R, int64_t cap, int64_t tiles);
 fcfs_status chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t tiles_x, int32_t tiles_y,
@@ -344,6 +349,24 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
     StageScope scope(kStageExtract, (cudaStream_t)stream);
     return extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
                    K_total_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t fcfs_haar_workspace_bytes(int64_t B, int32_t T) { return haar_workspace_bytes(B, T); }
+
+fcfs_status fcfs_haar(const int64_t *corner_ptr, int64_t B, int64_t K, const int32_t *x, const int32_t *y,
+                      const int32_t *w, const int64_t *area, int32_t T, double *out, void *ws, size_t ws_bytes,
+                      void *stream) {
+    if (T < 2 || T > 4096 || (T & (T - 1)) != 0) { set_error("fcfs_haar: T=%d not a power of two in [2, 4096]", T); return FCFS_E_INVALID; }
+    if (B < 1 || K < 0 || (K > 0 && (!x || !y || !w)) || !area || !out || (corner_ptr == nullptr && B != 1) ||
+        K >= (int64_t(1) << 31)) {
+        set_error("fcfs_haar: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageContract, (cudaStream_t)stream);
+    return haar_clips(x, y, w, corner_ptr, B, K, area, T, out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 size_t fcfs_chop_workspace_bytes(int64_t R, int64_t cap, int32_t tiles_x, int32_t tiles_y) {

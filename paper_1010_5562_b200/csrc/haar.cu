@@ -1,0 +1,188 @@
+// haar.cu — the continuous Haar transform of clips (the paper's CHT / PCHT,
+// P:453-480).  Basis (reading A18 of DESIGN.md): phi_{j,kx,ky} = (2^j / T) 1[cell],
+// psi^{(ab)} = sum_{n,m} a_n b_m phi_{j+1,2kx+n,2ky+m}, g = (1,1)/sqrt2, h = (1,-1)/sqrt2, J = log2 T.
+//
+// The paper's PCHT recurses over the quadtree and intersects each boundary cell with the polygons
+// (Alg. 1).  Here the same coefficients come straight from the signed corners, f = sum_k w_k H(x-x_k)
+// H(y-y_k), because the basis is separable (Lemma polyip):
+//
+//   C^{(ab)}_{j,kx,ky} = (2^j / T) sum_k w_k I_a(x_k) I_b(y_k),
+//   I_g(x) = integral of H(. - x) over the cell's x-range = clamp(a2 - max(a1, x)),
+//   I_h(x) = (left half) - (right half) = -tent(x): -(x - a1) on [a1, mid], -(a2 - x) on [mid, a2], else 0.
+//
+// I_h is supported inside the cell, so a corner touches ONE cell per level through an h factor: the
+// hh numerators are a scatter of the corners; hg (h in x, g in y) = the corner's own cell (partial
+// g = b2 - y) plus, for every cell above it in its column, s I_h(x) (full g): a column prefix sum of
+// per-cell totals; gh likewise along rows.  That is the pruning of the PCHT — only cells crossed by
+// the boundary get non-zero details — without a recursion: O(K J) atomics + O(T^2) prefix sums and
+// output writes.  Every numerator is an exact integer (int64 atomics: order-independent), every
+// coefficient an integer times 2^j / T: the FP64 output is exact.
+#include "common.cuh"
+
+namespace fcfs {
+
+namespace haar {
+
+constexpr int kThreads = 256;
+
+// scratch per clip: for each level j (n = 2^j cells per side) five int64 n x n arrays at
+// level_off(j) = 5 (4^j - 1) / 3: [0] hh, [1] hg partial, [2] hg column totals, [3] gh partial,
+// [4] gh row totals
+__host__ __device__ inline int64_t level_off(int j) { return 5 * ((((int64_t)1) << (2 * j)) - 1) / 3; }
+__host__ __device__ inline int64_t clip_scratch(int J) { return level_off(J); }
+
+__device__ __forceinline__ void add64(int64_t *p, int64_t v) {
+    if (v) atomicAdd((unsigned long long *)p, (unsigned long long)v);
+}
+
+// thread per (corner, level)
+__global__ void k_haar_scatter(const int32_t *__restrict__ x, const int32_t *__restrict__ y,
+                               const int32_t *__restrict__ w, const int64_t *__restrict__ corner_ptr, int64_t B,
+                               int64_t K, int32_t T, int J, int64_t *scratch) {
+    const int64_t total = K * J;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / J;
+        const int j = (int)(i - k * J);
+        const int32_t xk = x[k], yk = y[k];
+        if (xk >= T || yk >= T) continue;   // corners on x = T or y = T touch no cell
+        // clip of corner k (last b with corner_ptr[b] <= k)
+        int64_t b = 0;
+        if (corner_ptr) {
+            int64_t lo = 0, hi = B - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (corner_ptr[mid] <= k) lo = mid; else hi = mid - 1;
+            }
+            b = lo;
+        }
+        const int64_t wk = w[k];
+        const int sh = J - j;                      // cell side s = 2^sh
+        const int32_t s = 1 << sh, hs = s >> 1;
+        const int32_t kx = xk >> sh, ky = yk >> sh;
+        const int32_t ax = kx * s, ay = ky * s;
+        const int32_t dx = xk - ax, dy = yk - ay;  // in [0, s)
+        const int64_t ihx = -(int64_t)(dx <= hs ? dx : s - dx), ihy = -(int64_t)(dy <= hs ? dy : s - dy);
+        const int64_t igx = s - dx, igy = s - dy;  // own-cell partial g
+        const int64_t n = (int64_t)1 << j;
+        int64_t *L = scratch + b * clip_scratch(J) + level_off(j);
+        const int64_t c = (int64_t)ky * n + kx;
+        add64(L + 0 * n * n + c, wk * ihx * ihy);
+        add64(L + 1 * n * n + c, wk * ihx * igy);
+        add64(L + 2 * n * n + c, wk * ihx);
+        add64(L + 3 * n * n + c, wk * igx * ihy);
+        add64(L + 4 * n * n + c, wk * ihy);
+    }
+}
+
+// (clip, level, line) of the flattened line index r in [0, B (T - 1)): level j has 2^j lines
+__device__ __forceinline__ void line_of(int64_t i, int32_t T, int64_t &b, int &j, int64_t &line) {
+    const int64_t per_clip = T - 1;
+    b = i / per_clip;
+    int64_t r = i - b * per_clip;
+    j = 0;
+    while (r >= ((int64_t)1 << j)) { r -= (int64_t)1 << j; ++j; }
+    line = r;
+}
+
+// thread per (clip, level, column kx): hg = own-cell partial + s x (exclusive prefix over ky of the
+// column totals), scaled by 2^j / T (exact); consecutive threads write consecutive columns
+__global__ void k_haar_cols(const int64_t *__restrict__ scratch, const int64_t *__restrict__ area, int64_t B,
+                            int32_t T, int J, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B * (int64_t)(T - 1);
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b, kx;
+        int j;
+        line_of(i, T, b, j, kx);
+        const int64_t n = (int64_t)1 << j, s = (int64_t)T >> j;
+        const double scale = (double)n / (double)T;
+        const int64_t *L = scratch + b * clip_scratch(J) + level_off(j);
+        double *o = out + b * (int64_t)T * T;
+        if (j == 0) o[0] = (double)area[b] / (double)T;   // X_{0,0,0}
+        int64_t run = 0;
+        for (int64_t ky = 0; ky < n; ++ky) {
+            const int64_t c = ky * n + kx;
+            o[ky * T + n + kx] = (double)(L[1 * n * n + c] + s * run) * scale;
+            run += L[2 * n * n + c];
+        }
+    }
+}
+
+// warp per (clip, level, row ky): gh = own-cell partial + s x (exclusive prefix over kx of the row
+// totals; warp scan, 32 columns at a time, coalesced) and hh, scaled by 2^j / T
+__global__ void k_haar_rows(const int64_t *__restrict__ scratch, int64_t B, int32_t T, int J, double *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B * (int64_t)(T - 1); i += nwarps) {
+        int64_t b, ky;
+        int j;
+        line_of(i, T, b, j, ky);
+        const int64_t n = (int64_t)1 << j, s = (int64_t)T >> j;
+        const double scale = (double)n / (double)T;
+        const int64_t *L = scratch + b * clip_scratch(J) + level_off(j);
+        double *o = out + b * (int64_t)T * T + (n + ky) * T;
+        int64_t carry = 0;
+        for (int64_t k0 = 0; k0 < n; k0 += 32) {
+            const int64_t kx = k0 + lane;
+            const bool ok = kx < n;
+            const int64_t c = ky * n + kx;
+            const int64_t tot = ok ? L[4 * n * n + c] : 0;
+            int64_t inc = tot;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int64_t v = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += v;
+            }
+            if (ok) {
+                o[kx] = (double)(L[3 * n * n + c] + s * (carry + inc - tot)) * scale;
+                o[n + kx] = (double)L[0 * n * n + c] * scale;
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+}
+
+}  // namespace haar
+
+static int log2_exact(int32_t T) {
+    int J = 0;
+    while ((1 << J) < T) ++J;
+    return (1 << J) == T ? J : -1;
+}
+
+size_t haar_workspace_bytes(int64_t B, int32_t T) {
+    const int J = log2_exact(T);
+    if (J < 1 || B < 1) return 0;
+    Carver cv(nullptr, 0);
+    cv.take<int64_t>((size_t)(B * haar::clip_scratch(J)));
+    return cv.used();
+}
+
+fcfs_status haar_clips(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *corner_ptr, int64_t B,
+                       int64_t K, const int64_t *area, int32_t T, double *out, void *ws, size_t ws_bytes,
+                       cudaStream_t s) {
+    const int J = log2_exact(T);
+    Carver cv(ws, ws_bytes);
+    int64_t *scratch = cv.take<int64_t>((size_t)(B * haar::clip_scratch(J)));
+    if (!cv.fits()) {
+        set_error("fcfs_haar: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (size_t)(B * haar::clip_scratch(J)), s));
+    if (K > 0) {
+        int64_t blocks = (K * J + haar::kThreads - 1) / haar::kThreads;
+        if (blocks > 148 * 32) blocks = 148 * 32;
+        haar::k_haar_scatter<<<(unsigned)blocks, haar::kThreads, 0, s>>>(x, y, w, corner_ptr, B, K, T, J, scratch);
+        FCFS_CHECK_LAUNCH("k_haar_scatter");
+    }
+    const int64_t lines = B * (int64_t)(T - 1);
+    int64_t lb = (lines + 127) / 128;
+    if (lb > 148 * 32) lb = 148 * 32;
+    haar::k_haar_cols<<<(unsigned)lb, 128, 0, s>>>(scratch, area, B, T, J, out);
+    FCFS_CHECK_LAUNCH("k_haar_cols");
+    int64_t rb = (lines * 32 + 255) / 256;
+    if (rb > 148 * 32) rb = 148 * 32;
+    haar::k_haar_rows<<<(unsigned)rb, 256, 0, s>>>(scratch, B, T, J, out);
+    FCFS_CHECK_LAUNCH("k_haar_rows");
+    return FCFS_OK;
+}
+
+}  // namespace fcfs

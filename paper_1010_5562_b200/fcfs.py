@@ -69,6 +69,10 @@ _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _
 _lib.fcfs_vertices_from_polygons.restype = _i32
 _lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
 _lib.fcfs_coeffs_workspace_bytes.restype = _sz
+_lib.fcfs_haar_workspace_bytes.argtypes = [_i64, _i32]
+_lib.fcfs_haar_workspace_bytes.restype = _sz
+_lib.fcfs_haar.argtypes = [_P, _i64, _i64, _P, _P, _P, _P, _i32, _P, _P, _sz, _P]
+_lib.fcfs_haar.restype = _i32
 _lib.fcfs_chop_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32]
 _lib.fcfs_chop_workspace_bytes.restype = _sz
 _lib.fcfs_chop_rects.argtypes = [_P, _i64, _i32, _i32, _i32, _P, _i64, _P, ctypes.POINTER(_i64), _P, _sz, _P]
@@ -97,7 +101,8 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_pupil_indices", "fcfs_status_string", "fcfs_last_error", "fcfs_device_check",
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
-            "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects"]
+            "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
+            "fcfs_haar_workspace_bytes", "fcfs_haar"]
 STAGES = ("extract", "contract", "epilogue")
 
 
@@ -226,6 +231,30 @@ def vertices_from_polygons(vx, vy, poly_ptr, T, clip_ptr=None, stream=None):
     _check(st, "fcfs_vertices_from_polygons")
     k = K.value
     return dict(x=x[:k], y=y[:k], w=w[:k], corner_ptr=cptr, area=area, K=k)
+
+
+class HaarPlan:
+    """Pre-allocated workspace + output for repeated ``fcfs_haar`` calls (B clips of side T)."""
+
+    def __init__(self, B, T, device="cuda"):
+        self.B, self.T = int(B), int(T)
+        nb = _lib.fcfs_haar_workspace_bytes(self.B, self.T)
+        if nb == 0:
+            raise FcfsError(E_INVALID, "fcfs_haar_workspace_bytes")
+        self.ws = _ws(nb, device)
+        self.out = torch.empty((self.B, self.T, self.T), dtype=torch.float64, device=device)
+
+    def run(self, x, y, w, area, corner_ptr=None, stream=None):
+        st = _lib.fcfs_haar(_ptr(corner_ptr), self.B, int(x.shape[0]), _ptr(x), _ptr(y), _ptr(w), _ptr(area), self.T,
+                            _ptr(self.out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_haar")
+        return self.out
+
+
+def haar(x, y, w, area, T, corner_ptr=None, stream=None):
+    """Continuous Haar transform: float64 cuda [B, T, T] (reading A18 layout, exact values)."""
+    B = 1 if corner_ptr is None else corner_ptr.shape[0] - 1
+    return HaarPlan(B, T, device=area.device).run(x, y, w, area, corner_ptr, stream)
 
 
 class ChopPlan:

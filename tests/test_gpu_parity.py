@@ -627,3 +627,36 @@ def test_layout_tiles_end_to_end(fcfs, prec):
         sl = slice(cp[t], cp[t + 1])
         Fr, B = oracle.coeffs(ex["x"][sl], ex["y"][sl], ex["w"][sl], ex["area"][t], lay.T, ms, ns)
         _assert_parity(F[t], Fr, B, prec, f"tile {t}", ms, ns)
+
+
+# ------------------------------------------------------------------ NEXT-4: the continuous Haar transform
+
+@pytest.mark.parametrize("case", ["c1_union_groups", "batched_polygons", "edges_at_T"])
+def test_haar_bit_exact(fcfs, case):
+    """Exact dyadic coefficients: bitwise equal to the oracle (child-cell areas of the corner form)."""
+    if case == "c1_union_groups":
+        wl = inputs.c1(seed=3, T=256, n_rects=40)
+        g = _gpu_extract(fcfs, wl)
+        H = fcfs.haar(g["x"], g["y"], g["w"], g["area"], wl.T).cpu().numpy()
+        ref = oracle.haar(g["x"].cpu().numpy(), g["y"].cpu().numpy(), g["w"].cpu().numpy(), wl.T)
+        assert np.array_equal(H[0], ref)
+        return
+    if case == "batched_polygons":
+        ps = inputs.polygon_clips(7, clips=4, T=128, n_poly=12, max_cols=6, size=12)
+        ps.clip_ptr[2] = ps.clip_ptr[1]             # clip 1 empty
+        ps = inputs._pack([list(zip(ps.vx[a:b].tolist(), ps.vy[a:b].tolist()))
+                           for a, b in zip(ps.poly_ptr[:-1], ps.poly_ptr[1:])], ps.T, np.diff(ps.clip_ptr).tolist())
+        g = _gpu_polys(fcfs, ps)
+        T = ps.T
+    else:
+        T = 64
+        rects = np.array([[0, 0, 64, 64], [5, 60, 64, 64], [60, 3, 64, 9], [1, 1, 2, 2]], np.int32)
+        wl = inputs.Workload("edge", T, 1, 1, -1.0, rects, np.array([0, 1, 4], np.int64), None, ("fp64",))
+        g = _gpu_extract(fcfs, wl)
+        g["corner_ptr"] = None
+    H = fcfs.haar(g["x"], g["y"], g["w"], g["area"], T, g["corner_ptr"]).cpu().numpy()
+    cp = g["corner_ptr"].cpu().numpy() if g["corner_ptr"] is not None else np.array([0, g["K"]])
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    for b in range(len(cp) - 1):
+        sl = slice(cp[b], cp[b + 1])
+        assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], T)), f"clip {b}"
