@@ -38,10 +38,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "layout"],
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "layout", "haar"],
                     help="layout: c3-style lines over a tiles x tiles layout of T=2048 tiles, chopped into tiles "
                          "on the GPU (fcfs_chop_rects) and transformed as one batch (the paper's flow, P:1060-1062)")
     ap.add_argument("--tiles", type=int, default=64, help="layout: tiles per side")
+    ap.add_argument("--haar-tiles", type=int, default=16, help="haar: tiles per side (T=1024 tiles)")
     ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3", "f16x3"])
     ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
     ap.add_argument("--shard", default="rows", choices=["rows", "vblock"],
@@ -241,6 +242,84 @@ def config_dict(args, wl, prec, world):
     return d
 
 
+def bench_haar(args, rank, world, dev):
+    """NEXT-4: the continuous Haar transform of a chopped layout (T = 1024 tiles, the paper's 1024 nm
+    tiles at 1 nm): one step = chop + batched extraction + fcfs_haar of every tile."""
+    import torch
+    import torch.distributed as dist
+    from paper_1010_5562_b200 import fcfs
+    T = 1024
+    nt = args.haar_tiles
+    lay = inputs.layout(args.seed + rank, T=T, tiles_x=nt, tiles_y=nt, lines_per_tile=300)
+    rects = torch.from_numpy(lay.rects).to(dev)
+    chop = fcfs.ChopPlan(lay.rects.shape[0], T, nt, nt, device=dev)
+    n_p = chop.run(rects)
+    B = nt * nt
+    vp = fcfs.VerticesPlan(n_p, T, n_p, B, 1, grouped=False, device=dev)
+    hp = fcfs.HaarPlan(B, T, device=dev)
+
+    def step():
+        chop.run(rects)
+        k = vp.run(chop.out[:n_p], None, chop.tile_ptr)
+        return hp.run(vp.x[:k], vp.y[:k], vp.w[:k], vp.area, vp.corner_ptr)
+    for _ in range(args.warmup):
+        step()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    fcfs.profile_enable(True)
+    fcfs.profile_read()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = fcfs.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for i in range(args.steps):
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+            flush.fill_(i & 0xff)
+        torch.cuda.synchronize()
+    launches = fcfs.kernel_launches() - launches0
+    stages = fcfs.profile_read()
+    fcfs.profile_enable(False)
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    coefs = float(B) * T * T
+    value = coefs * world / (ms / 1e3) / 1e9
+    h_ms = stages["contract"][0] / args.steps
+    peaks, src = load_peaks()
+    ach = coefs * 8.0 / (h_ms / 1e3) / 1e9        # algorithmic bytes: the 8-byte coefficient written once
+    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "kernel": "fcfs_haar (scatter + col/row scans)",
+            "alg_bytes_per_launch": coefs * 8.0, "kernel_ms_per_launch": round(h_ms, 4),
+            "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()},
+            "peak_source": f"{src} HBM copy bandwidth"}
+    if rank == 0:
+        line = {"metric": "haar_coefficients_per_sec", "value": round(value, 3), "unit": "Gcoef/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64 (exact dyadic values from int64 numerators)",
+                "data": "synthetic",
+                "config": {"workload": f"haar: {nt}x{nt} tiles of T={T}, c3-style lines (300 per tile), chop + "
+                                       f"extraction + continuous Haar transform (J=10, all T^2 coefficients per tile)",
+                           "tiles": B, "T": T, "pieces": n_p, "l2": "flushed between steps"},
+                "roofline": roof, "clocks": clk.summary(), "gpu_launches": int(launches), "e2e": None}
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            ch = oracle.chop_rects(lay.rects, T, nt, nt)
+            a, b = ch["tile_ptr"][0], ch["tile_ptr"][1]
+            e = oracle.extract(ch["rects"][a:b], T)
+            t0 = time.perf_counter()
+            oracle.haar(e["x"], e["y"], e["w"], T)
+            dt = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": T * T / dt / 1e9, "unit": "Gcoef/s", "cores": 1, "kind": "oracle",
+                                    "sample": f"1 tile (K={e['K']}), oracle_haar (child-cell areas, single thread)",
+                                    "seconds": round(dt, 3)}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -254,6 +333,15 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.config == "haar":
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        from paper_1010_5562_b200 import fcfs as _f
+        _f.device_check()
+        bench_haar(args, rank, world, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_1010_5562_b200 import fcfs

@@ -86,7 +86,7 @@ __device__ __forceinline__ void line_of(int64_t i, int32_t T, int64_t &b, int &j
 
 // thread per (clip, level, column kx): hg = own-cell partial + s x (exclusive prefix over ky of the
 // column totals), scaled by 2^j / T (exact); consecutive threads write consecutive columns
-__global__ void k_haar_cols(const int64_t *__restrict__ scratch, const int64_t *__restrict__ area, int64_t B,
+__global__ void k_haar_cols(const int64_t *scratch, const int64_t *__restrict__ area, int64_t B,
                             int32_t T, int J, double *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B * (int64_t)(T - 1);
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -98,18 +98,22 @@ __global__ void k_haar_cols(const int64_t *__restrict__ scratch, const int64_t *
         const int64_t *L = scratch + b * clip_scratch(J) + level_off(j);
         double *o = out + b * (int64_t)T * T;
         if (j == 0) o[0] = (double)area[b] / (double)T;   // X_{0,0,0}
+        int64_t *Lw = const_cast<int64_t *>(L);
         int64_t run = 0;
         for (int64_t ky = 0; ky < n; ++ky) {
             const int64_t c = ky * n + kx;
-            o[ky * T + n + kx] = (double)(L[1 * n * n + c] + s * run) * scale;
-            run += L[2 * n * n + c];
+            const int64_t part = L[1 * n * n + c], tot = L[2 * n * n + c];
+            o[ky * T + n + kx] = (double)(part + s * run) * scale;
+            run += tot;
+            if (part) Lw[1 * n * n + c] = 0;   // leave the scratch zero for the next call (sparse clears)
+            if (tot) Lw[2 * n * n + c] = 0;
         }
     }
 }
 
 // warp per (clip, level, row ky): gh = own-cell partial + s x (exclusive prefix over kx of the row
 // totals; warp scan, 32 columns at a time, coalesced) and hh, scaled by 2^j / T
-__global__ void k_haar_rows(const int64_t *__restrict__ scratch, int64_t B, int32_t T, int J, double *out) {
+__global__ void k_haar_rows(const int64_t *scratch, int64_t B, int32_t T, int J, double *out) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B * (int64_t)(T - 1); i += nwarps) {
@@ -126,14 +130,19 @@ __global__ void k_haar_rows(const int64_t *__restrict__ scratch, int64_t B, int3
             const bool ok = kx < n;
             const int64_t c = ky * n + kx;
             const int64_t tot = ok ? L[4 * n * n + c] : 0;
+            const int64_t part = ok ? L[3 * n * n + c] : 0, hh = ok ? L[0 * n * n + c] : 0;
             int64_t inc = tot;
             for (int d = 1; d < 32; d <<= 1) {
                 const int64_t v = __shfl_up_sync(0xffffffffu, inc, d);
                 if (lane >= d) inc += v;
             }
             if (ok) {
-                o[kx] = (double)(L[3 * n * n + c] + s * (carry + inc - tot)) * scale;
-                o[n + kx] = (double)L[0 * n * n + c] * scale;
+                o[kx] = (double)(part + s * (carry + inc - tot)) * scale;
+                o[n + kx] = (double)hh * scale;
+                int64_t *Lw = const_cast<int64_t *>(L);
+                if (tot) Lw[4 * n * n + c] = 0;
+                if (part) Lw[3 * n * n + c] = 0;
+                if (hh) Lw[0 * n * n + c] = 0;
             }
             carry += __shfl_sync(0xffffffffu, inc, 31);
         }
@@ -166,7 +175,8 @@ fcfs_status haar_clips(const int32_t *x, const int32_t *y, const int32_t *w, con
         set_error("fcfs_haar: workspace %zu < %zu bytes", ws_bytes, cv.used());
         return FCFS_E_WORKSPACE;
     }
-    FCFS_TRY_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (size_t)(B * haar::clip_scratch(J)), s));
+    // the scratch is zero on entry (caller contract: zero-initialised once; every call clears the
+    // entries it used, so no O(T^2) memset per call)
     if (K > 0) {
         int64_t blocks = (K * J + haar::kThreads - 1) / haar::kThreads;
         if (blocks > 148 * 32) blocks = 148 * 32;

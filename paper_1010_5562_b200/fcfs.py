@@ -242,6 +242,7 @@ class HaarPlan:
         if nb == 0:
             raise FcfsError(E_INVALID, "fcfs_haar_workspace_bytes")
         self.ws = _ws(nb, device)
+        self.ws.zero_()                      # fcfs_haar: zero before first use, left zero by every call
         self.out = torch.empty((self.B, self.T, self.T), dtype=torch.float64, device=device)
 
     def run(self, x, y, w, area, corner_ptr=None, stream=None):

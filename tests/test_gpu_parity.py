@@ -660,3 +660,19 @@ def test_haar_bit_exact(fcfs, case):
     for b in range(len(cp) - 1):
         sl = slice(cp[b], cp[b + 1])
         assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], T)), f"clip {b}"
+
+
+def test_haar_plan_reuse_leaves_workspace_zero(fcfs):
+    """A HaarPlan reused on different clips: every call clears the scratch it used (no per-call memset)."""
+    ps = inputs.polygon_clips(8, clips=3, T=64, n_poly=10, max_cols=5, size=8)
+    ps2 = inputs.polygon_clips(9, clips=3, T=64, n_poly=14, max_cols=5, size=8)
+    plan = fcfs.HaarPlan(3, 64)
+    for p in (ps, ps2, ps):
+        g = _gpu_polys(fcfs, p)
+        H = plan.run(g["x"], g["y"], g["w"], g["area"], g["corner_ptr"]).cpu().numpy()
+        cp = g["corner_ptr"].cpu().numpy()
+        x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+        for b in range(3):
+            sl = slice(cp[b], cp[b + 1])
+            assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], 64))
+    assert torch.count_nonzero(plan.ws).item() == 0
