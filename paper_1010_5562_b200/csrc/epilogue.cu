@@ -33,48 +33,45 @@ __device__ double2 coeff(const double *P_ws, const GemmPlan &pl, const EpiArgs &
     return coeff_from_P(get, pl.X, pl.Y, ea.T, m, n, dc);
 }
 
-// grid: (output rows, clips); block loops over n
+// grid: (output rows, clips, grid-stride over clips beyond 65535); block loops over n
 __global__ void k_epilogue(const double *__restrict__ P_ws, GemmPlan pl, EpiArgs ea, void *F) {
-    const int64_t clip = blockIdx.y;
     const int m = ea.m_lo + (int)blockIdx.x;
     if (m > ea.m_hi) return;
-    const int64_t area = ea.area_dev ? ea.area_dev[clip] : ea.area_host;
-    const double dc = (double)area / ((double)ea.T * (double)ea.T);
-    int64_t off;
-    int nlo, nhi;
-    if (ea.layout == FCFS_LAYOUT_PUPIL) {
-        off = 0;
-        for (int mm = -ea.M; mm < m; ++mm) {
-            int c = pupil_nmax(mm, ea.r2, ea.N);
-            off += c < 0 ? 0 : 2 * c + 1;
+    for (int64_t clip = blockIdx.y; clip < pl.B; clip += gridDim.y) {
+        const int64_t area = ea.area_dev ? ea.area_dev[clip] : ea.area_host;
+        const double dc = (double)area / ((double)ea.T * (double)ea.T);
+        int64_t off;
+        int nlo, nhi;
+        if (ea.layout == FCFS_LAYOUT_PUPIL) {
+            off = 0;
+            for (int mm = -ea.M; mm < m; ++mm) {
+                int c = pupil_nmax(mm, ea.r2, ea.N);
+                off += c < 0 ? 0 : 2 * c + 1;
+            }
+            int c = pupil_nmax(m, ea.r2, ea.N);
+            if (c < 0) return;
+            nlo = -c; nhi = c;
+        } else {
+            off = (int64_t)(m - ea.m_lo) * (2 * ea.N + 1);
+            nlo = -ea.N; nhi = ea.N;
         }
-        int c = pupil_nmax(m, ea.r2, ea.N);
-        if (c < 0) return;
-        nlo = -c; nhi = c;
-    } else {
-        off = (int64_t)(m - ea.m_lo) * (2 * ea.N + 1);
-        nlo = -ea.N; nhi = ea.N;
-    }
-    off += clip * ea.out_per_clip;
-    for (int n = nlo + (int)threadIdx.x; n <= nhi; n += blockDim.x) {
-        double2 v;
-        bool keep = true;
-        if (ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0)
-            keep = (double)m * (double)m + (double)n * (double)n <= ea.r2;
-        v = keep ? coeff(P_ws, pl, ea, clip, m, n, dc) : make_double2(0.0, 0.0);
-        const int64_t o = off + (n - nlo);
-        store_out(F, o, v, ea.out_f32);
+        off += clip * ea.out_per_clip;
+        for (int n = nlo + (int)threadIdx.x; n <= nhi; n += blockDim.x) {
+            double2 v;
+            bool keep = true;
+            if (ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0)
+                keep = (double)m * (double)m + (double)n * (double)n <= ea.r2;
+            v = keep ? coeff(P_ws, pl, ea, clip, m, n, dc) : make_double2(0.0, 0.0);
+            const int64_t o = off + (n - nlo);
+            store_out(F, o, v, ea.out_f32);
+        }
     }
 }
 
 fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F, cudaStream_t s) {
     const int rows = ea.m_hi - ea.m_lo + 1;
     if (rows <= 0 || plan.B <= 0) return FCFS_OK;
-    if (plan.B > 65535) {
-        set_error("epilogue: %lld clips exceed the grid limit", (long long)plan.B);
-        return FCFS_E_UNSUPPORTED;
-    }
-    dim3 grid((unsigned)rows, (unsigned)plan.B);
+    dim3 grid((unsigned)rows, (unsigned)(plan.B < 65535 ? plan.B : 65535));
     k_epilogue<<<grid, 128, 0, s>>>(P_ws, plan, ea, F);
     FCFS_CHECK_LAUNCH("k_epilogue");
     return FCFS_OK;

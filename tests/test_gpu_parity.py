@@ -676,3 +676,66 @@ def test_haar_plan_reuse_leaves_workspace_zero(fcfs):
             sl = slice(cp[b], cp[b + 1])
             assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], 64))
     assert torch.count_nonzero(plan.ws).item() == 0
+
+
+# ------------------------------------------------------------------ maximum sizes and degenerate cases
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("r", ["fft", "gemm"])
+def test_max_T_single_clip(fcfs, route, r, prec):
+    """T = 2^20 (the ABI's limit): exact integer phases (m x) mod T near 2^40 and corners on x = T / y = T,
+    through both single-clip routes."""
+    route(r)
+    T = 1 << 20
+    rng = np.random.default_rng(21)
+    x0 = rng.integers(0, T - 5000, 150); y0 = rng.integers(0, T - 5000, 150)
+    rects = np.stack([x0, y0, x0 + rng.integers(1, 5000, 150), y0 + rng.integers(1, 5000, 150)], 1).astype(np.int32)
+    rects[:10, 2] = T
+    rects[10:20, 3] = T
+    wl = inputs.Workload("maxT", T, 40, 40, -1.0, rects, None, None, ("fp64",))
+    g, F = _clip_coeffs(fcfs, wl, prec)
+    ms, ns, Fr, B = _oracle_window(g, T, 40, 40)
+    _assert_parity(F, Fr, B, prec, f"T=2^20 {r}", ms, ns)
+
+
+@pytest.mark.parametrize("prec", ["tf32x3", "fp64"])
+def test_many_tiny_clips(fcfs, prec):
+    """70,000 clips (more than a 65,535 grid dimension) of 1-3 rects, pupil window: every clip checked
+    against the closed form of its rect sum through the oracle on a sample, and empty clips give 0."""
+    rng = np.random.default_rng(22)
+    T = 256
+    B = 70000
+    sizes = rng.integers(0, 4, B)
+    cp = np.zeros(B + 1, np.int64); cp[1:] = np.cumsum(sizes)
+    R = int(cp[-1])
+    rects = inputs.random_rects(rng, R, T, 1, 60)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    r2 = 30.5
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, 5, 5, r2, "pupil",
+                            prec).cpu().numpy()
+    ms, ns = oracle.window(5, 5, r2)
+    e = oracle.extract(rects, T, None, cp)
+    assert np.array_equal(g["corner_ptr"].cpu().numpy(), e["corner_ptr"])
+    for b in [0, 1, 65534, 65535, 65536, B - 1] + rng.integers(0, B, 20).tolist():
+        a, c = e["corner_ptr"][b], e["corner_ptr"][b + 1]
+        if a == c:
+            assert not np.any(F[b]), f"empty clip {b}"
+            continue
+        Fr, Bd = oracle.coeffs(e["x"][a:c], e["y"][a:c], e["w"][a:c], e["area"][b], T, ms, ns)
+        _assert_parity(F[b], Fr, Bd, prec, f"clip {b}", ms, ns)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
+def test_degenerate_full_tile_and_window_beyond_T(fcfs, prec):
+    """The full tile is a delta (P9: F = delta_{m0} delta_{n0}); a window wider than the tile (|m| > T/2,
+    frequencies alias on the lattice but the CFS does not) still matches the oracle."""
+    T = 64
+    wl = inputs.Workload("full", T, 5, 5, -1.0, np.array([[0, 0, T, T]], np.int32), None, None, ("fp64",))
+    g, F = _clip_coeffs(fcfs, wl, prec)
+    ref = np.zeros_like(F); ref[len(F) // 2] = 1.0
+    assert np.allclose(F, ref, atol=1e-12 if prec == "fp64" else 1e-6)
+    rng = np.random.default_rng(23)
+    wl = inputs.Workload("wide", T, 40, 40, -1.0, inputs.random_rects(rng, 10, T, 2, 30), None, None, ("fp64",))
+    g, F = _clip_coeffs(fcfs, wl, prec)
+    ms, ns, Fr, B = _oracle_window(g, T, 40, 40)
+    _assert_parity(F, Fr, B, prec, "window beyond T", ms, ns)
