@@ -452,15 +452,15 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
 // CSR position (look-back offset, coalesced), with its exact int64 area.  O(n * bucket) with all
 // threads busy, instead of a radix sort of 4n keys.
 static constexpr int kBucketThreads = 512;
-static constexpr int kBucketRectsPerThread = 4;   // kClipRects / kBucketThreads
 static constexpr int kBucketMaxT = 8191;
 static constexpr int kBucketCap = 4 * kClipRects;
+static constexpr int kSmallRects = 448 * 3;        // the small per-clip bucket variant (3 CTAs / SM)
 
 // exclusive scan of the nb bucket sizes in hist (thread t owns buckets [t*per, (t+1)*per)); ends
 // with a __syncthreads
 __device__ __forceinline__ void bucket_scan(int32_t *hist, int nb, int32_t *wsum) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int per = (nb + kBucketThreads - 1) / kBucketThreads;
+    const int per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
     const int lo = threadIdx.x * per, hi = min(lo + per, nb);
     int sown = 0;
     for (int i = lo; i < hi; ++i) sown += hist[i];
@@ -488,7 +488,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
     // rank inside the bucket by x (ties by index); the first of equal x carries the run sum
-    for (int i = threadIdx.x; i < nv; i += kBucketThreads) {
+    for (int i = threadIdx.x; i < nv; i += (int)blockDim.x) {
         const int y = by[i];
         const int st = y ? hist[y - 1] : 0, en = hist[y];
         const uint32_t xi = bxw[i] >> 16;
@@ -508,7 +508,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     }
     __syncthreads();
     // compact the non-zero sorted entries: thread t owns sorted positions [t*pp, (t+1)*pp)
-    const int pp = (nv + kBucketThreads - 1) / kBucketThreads;
+    const int pp = (nv + (int)blockDim.x - 1) / (int)blockDim.x;
     const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
     int cnt = 0;
     long long a = 0;
@@ -532,13 +532,13 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
         const int16_t wv = sw[i];
         if (wv != 0) { bxw[outp] = syx[i]; by[outp] = wv; ++outp; }
     }
-    if (threadIdx.x == kBucketThreads - 1) *tot_s = outp;     // the last thread ends at the clip total
+    if (threadIdx.x == (int)blockDim.x - 1) *tot_s = outp;     // the last thread ends at the clip total
     __syncthreads();
     const int total = *tot_s;
     if (threadIdx.x == 0) *s_off = clip_lookback(status, b, B, total, corner_ptr);
     __syncthreads();
     const int64_t base = *s_off;
-    for (int i = threadIdx.x; i < total; i += kBucketThreads) {   // coalesced stores, final positions
+    for (int i = threadIdx.x; i < total; i += (int)blockDim.x) {   // coalesced stores, final positions
         if (base + i >= cap) break;
         const uint32_t yx = bxw[i];
         xs[base + i] = (int32_t)(yx & 0xFFFFu);
@@ -547,50 +547,55 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     }
     if (threadIdx.x == 0) {
         long long t = 0;
-        for (int i = 0; i < kBucketThreads / 32; ++i) t += asum[i];
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += asum[i];
         area[b] = t;
     }
     __syncthreads();
 }
 
 
-__global__ void __launch_bounds__(kBucketThreads, 3)
+// kThr threads x kRPT rects per thread per clip (corner capacity 4 kThr kRPT, 12 B per corner of
+// shared memory): <448, 3> (1344 rects, 72 KB: 3 CTAs / SM) runs first, <512, 4> (2048 rects) if a
+// clip is larger
+template <int kThr, int kRPT>
+__global__ void __launch_bounds__(kThr, 3)
 k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
                       int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
                       unsigned long long *status, int64_t *area, int32_t *err) {
+    constexpr int kCap = 4 * kThr * kRPT;
     extern __shared__ __align__(16) unsigned char bsm[];
     uint32_t *bxw = (uint32_t *)bsm;                    // [cap] bucketed (x << 16 | w & 0xFFFF); later compacted (y << 16 | x)
-    uint32_t *syx = bxw + kBucketCap;                   // [cap] sorted (y << 16 | x)
-    int16_t *by = (int16_t *)(syx + kBucketCap);        // [cap] bucket y; later compacted weights
-    int16_t *sw = by + kBucketCap;                      // [cap] sorted merged weight (0 = dropped)
-    int32_t *hist = (int32_t *)(sw + kBucketCap);       // [T + 2]: bucket start, then bucket end
-    __shared__ int32_t wsum[kBucketThreads / 32];
-    __shared__ long long asum[kBucketThreads / 32];
+    uint32_t *syx = bxw + kCap;                         // [cap] sorted (y << 16 | x)
+    int16_t *by = (int16_t *)(syx + kCap);              // [cap] bucket y; later compacted weights
+    int16_t *sw = by + kCap;                            // [cap] sorted merged weight (0 = dropped)
+    int32_t *hist = (int32_t *)(sw + kCap);             // [T + 2]: bucket start, then bucket end
+    __shared__ int32_t wsum[kThr / 32];
+    __shared__ long long asum[kThr / 32];
     __shared__ int tot_s;
     __shared__ int64_t s_off;
     const int nb = T + 1;                               // buckets y = 0..T
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
         const int64_t r0 = clip_ptr ? clip_ptr[b] : 0, r1 = clip_ptr ? clip_ptr[b + 1] : R;
         const int n = (int)(r1 - r0);
-        if (n > kClipRects) {
+        if (n > kThr * kRPT) {
             // the caller falls back to the general path; the clip still publishes a count (0) so
             // that the look-back of the clips after it completes
             if (threadIdx.x == 0) { atomicOr(err, 8); area[b] = 0; clip_lookback(status, b, B, 0, corner_ptr); }
             continue;
         }
         // all of this thread's rects are loaded up front (independent loads in flight)
-        int4 rq[kBucketRectsPerThread];
-        bool rok[kBucketRectsPerThread];
+        int4 rq[kRPT];
+        bool rok[kRPT];
 #pragma unroll
-        for (int j = 0; j < kBucketRectsPerThread; ++j) {
-            const int r = threadIdx.x + j * kBucketThreads;
+        for (int j = 0; j < kRPT; ++j) {
+            const int r = threadIdx.x + j * kThr;
             rok[j] = r < n;
             rq[j] = rok[j] ? rects[r0 + r] : make_int4(0, 0, 0, 0);
         }
-        for (int i = threadIdx.x; i < nb + 1; i += kBucketThreads) hist[i] = 0;
+        for (int i = threadIdx.x; i < nb + 1; i += kThr) hist[i] = 0;
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kBucketRectsPerThread; ++j) {
+        for (int j = 0; j < kRPT; ++j) {
             if (!rok[j]) continue;
             if (!rect_ok(rq[j], T)) { atomicOr(err, 1); rok[j] = false; continue; }
             atomicAdd(&hist[rq[j].y], 2);
@@ -600,7 +605,7 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
         bucket_scan(hist, nb, wsum);
         // scatter into buckets: afterwards hist[y] = end of bucket y (= start of bucket y + 1)
 #pragma unroll
-        for (int j = 0; j < kBucketRectsPerThread; ++j) {
+        for (int j = 0; j < kRPT; ++j) {
             if (!rok[j]) continue;
             const int4 q = rq[j];
             int p = atomicAdd(&hist[q.y], 2);
@@ -762,6 +767,23 @@ size_t extract_clip_workspace_bytes(int64_t R, int64_t B) {
     return cv.used();
 }
 
+static fcfs_status clips_result(int64_t Kh, int32_t errh, int64_t cap, int64_t *K_host) {
+    if (errh & 8) {
+        set_error("a clip has more than %d rects", kClipRects);
+        return FCFS_E_UNSUPPORTED;
+    }
+    if (K_host) *K_host = Kh;
+    if (errh & 1) {
+        set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");
+        return FCFS_E_RANGE;
+    }
+    if (Kh > cap) {
+        set_error("fcfs_vertices_from_rects: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
+        return FCFS_E_CAPACITY;
+    }
+    return FCFS_OK;
+}
+
 // returns FCFS_E_UNSUPPORTED (after a sync) if a clip exceeds kClipRects: the caller falls back
 fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B, int32_t T,
                           int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
@@ -778,19 +800,52 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
     // one CTA per clip (the look-back needs every predecessor clip's CTA dispatched before it)
     const int64_t grid = B;
     if (T <= kBucketMaxT) {
-        const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
+        // the 1344-rect variant (3 CTAs / SM) unless the average clip is larger; if a clip overflows it,
+        // the 2048-rect variant reruns the batch (same outputs), and beyond that the general path
+        const bool small = R <= (int64_t)kSmallRects * B;
         static bool battr = false;
         if (!battr) {
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                kBucketCap * 12 + (kBucketMaxT + 2) * 4));
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket, cudaFuncAttributePreferredSharedMemoryCarveout,
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<512, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               100));
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<448, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               4 * kSmallRects * 12 + (kBucketMaxT + 2) * 4));
+            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<448, 3>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                100));
             battr = true;
         }
-        k_clip_corners_bucket<<<(unsigned)grid, kBucketThreads, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T,
-                                                                            x, y, w, cap, corner_ptr, W.status,
-                                                                            area, W.err);
-        FCFS_CHECK_LAUNCH("k_clip_corners_bucket");
+        auto launch = [&](bool large) -> fcfs_status {
+            if (large) {
+                const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
+                k_clip_corners_bucket<512, 4><<<(unsigned)grid, 512, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R,
+                                                                                T, x, y, w, cap, corner_ptr, W.status,
+                                                                                area, W.err);
+            } else {
+                const size_t bsmem = 4 * kSmallRects * 12 + (size_t)(T + 2) * 4;
+                k_clip_corners_bucket<448, 3><<<(unsigned)grid, 448, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R,
+                                                                                T, x, y, w, cap, corner_ptr, W.status,
+                                                                                area, W.err);
+            }
+            FCFS_CHECK_LAUNCH("k_clip_corners_bucket");
+            return FCFS_OK;
+        };
+        fcfs_status st = launch(!small);
+        if (st != FCFS_OK) return st;
+        if (small) {
+            // the result read-back below syncs once; only if the small variant overflowed (err bit 8)
+            // does the batch rerun with the large one
+            int64_t Kh = 0;
+            int32_t errh = 0;
+            FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, corner_ptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+            if (!(errh & 8)) return clips_result(Kh, errh, cap, K_host);
+            FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+            FCFS_TRY_CUDA(cudaMemsetAsync(W.status, 0, B * sizeof(unsigned long long), s));
+            st = launch(true);
+            if (st != FCFS_OK) return st;
+        }
     } else {
         k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, x, y, w, cap,
                                                                corner_ptr, W.status, area, W.err);
@@ -801,20 +856,7 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
     FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, corner_ptr + B, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaStreamSynchronize(s));
-    if (errh & 8) {
-        set_error("a clip has more than %d rects", kClipRects);
-        return FCFS_E_UNSUPPORTED;
-    }
-    if (K_host) *K_host = Kh;
-    if (errh & 1) {
-        set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");
-        return FCFS_E_RANGE;
-    }
-    if (Kh > cap) {
-        set_error("fcfs_vertices_from_rects: K=%lld > cap=%lld", (long long)Kh, (long long)cap);
-        return FCFS_E_CAPACITY;
-    }
-    return FCFS_OK;
+    return clips_result(Kh, errh, cap, K_host);
 }
 
 // steps 2-5 of the general path on the raw (key, weight) list in W.keys_a / W.w_a: sort, merge

@@ -739,3 +739,16 @@ def test_degenerate_full_tile_and_window_beyond_T(fcfs, prec):
     g, F = _clip_coeffs(fcfs, wl, prec)
     ms, ns, Fr, B = _oracle_window(g, T, 40, 40)
     _assert_parity(F, Fr, B, prec, "window beyond T", ms, ns)
+
+
+def test_extraction_small_variant_overflow_reruns(fcfs):
+    """Clips averaging under 1344 rects run the small per-clip kernel; one clip of 1500 rects overflows it
+    and the batch reruns with the 2048-rect kernel: bit-exact either way."""
+    rng = np.random.default_rng(31)
+    T = 2048
+    sizes = np.array([100, 1500, 80, 0, 300, 1344, 1345, 20], np.int64)
+    cp = np.zeros(len(sizes) + 1, np.int64); cp[1:] = np.cumsum(sizes)
+    rects = inputs.random_rects(rng, int(cp[-1]), T, 4, 300)
+    e = oracle.extract(rects, T, None, cp)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    _assert_extract_equal(g, e)
