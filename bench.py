@@ -190,6 +190,30 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle (this tier's reference arm) on the same workload."""
     if rank != 0:
         return
+    if args.config == "haar":
+        # the oracle's continuous Haar transform (child-cell areas) on one chopped tile per step
+        import oracle
+        T, nt = 1024, args.haar_tiles
+        lay = inputs.layout(args.seed, T=T, tiles_x=nt, tiles_y=nt, lines_per_tile=300)
+        ch = oracle.chop_rects(lay.rects, T, nt, nt)
+        vals = []
+        for i in range(args.warmup + args.steps):
+            a, b = ch["tile_ptr"][i % (nt * nt)], ch["tile_ptr"][i % (nt * nt) + 1]
+            e = oracle.extract(ch["rects"][a:b], T)
+            t0 = time.perf_counter()
+            oracle.haar(e["x"], e["y"], e["w"], T)
+            if i >= args.warmup:
+                vals.append(T * T / (time.perf_counter() - t0) / 1e9)
+        v = statistics.median(vals)
+        line = {"impl": "reference", "metric": "haar_coefficients_per_sec", "value": v, "unit": "Gcoef/s",
+                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "exact integer areas (int64 / int128)", "data": "synthetic",
+                "config": {"workload": f"haar: one T={T} tile per step of the {nt}x{nt}-tile layout"},
+                "cpu_baseline": {"value": v, "unit": "Gcoef/s", "cores": 1, "kind": "oracle",
+                                 "sample": "one tile per step, oracle_haar single thread"},
+                "e2e": {"value": v, "unit": "Gcoef/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     wl = workload(args.config, args.seed, 0, args.clips, args.tiles)
     prec = args.prec or ("tf32x3" if args.config in ("c3", "layout") else "fp64")
     per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
