@@ -11,6 +11,9 @@ namespace fcfs {
 void set_error(const char *fmt, ...);
 fcfs_status cuda_status(cudaError_t e, const char *where);
 void count_launch(int n = 1);
+// raise a kernel's dynamic shared-memory limit (and optionally its carveout to the maximum) on the
+// current device, once per (device, kernel, size): thread-safe
+fcfs_status ensure_smem(const void *fn, size_t bytes, bool max_carveout = false);
 
 // stage timing (fcfs_profile_*): RAII pair of events around a stage on stream s
 enum Stage { kStageExtract = 0, kStageContract = 1, kStageEpilogue = 2, kNumStages = 3 };
@@ -22,6 +25,11 @@ struct StageScope {
     ~StageScope() { profile_mark(stage, 0, s); }
 };
 
+#define FCFS_TRY(expr)                                            \
+    do {                                                          \
+        fcfs_status _st = (expr);                                 \
+        if (_st != FCFS_OK) return _st;                           \
+    } while (0)
 #define FCFS_TRY_CUDA(expr)                                      \
     do {                                                         \
         cudaError_t _e = (expr);                                 \

@@ -364,11 +364,7 @@ fcfs_status launch_gemm_fp64(const CornerSrc &src, const GemmPlan &plan, int32_t
                              cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     TwiddleGeom g = make_twiddle_geom(T);
-    static bool attr = false;
-    if (!attr) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        attr = true;
-    }
+    FCFS_TRY(ensure_smem((const void *)k_gemm_fp64<false>, 100 * 1024));
     int64_t grid = plan.items < 148 * 16 ? plan.items : 148 * 16;
     k_gemm_fp64<false><<<(unsigned)grid, kThreads, fp64_smem(g), s>>>(src, plan, g, P_ws, FpChunk{nullptr, 0, 0, nullptr});
     FCFS_CHECK_LAUNCH("k_gemm_fp64");
@@ -386,13 +382,9 @@ fcfs_status launch_gemm_fp64_chunked(const CornerSrc &src, const GemmPlan &plan,
                                      double *H, double *P_ws, cudaStream_t s) {
     if (plan.items <= 0) return FCFS_OK;
     TwiddleGeom g = make_twiddle_geom(T);
-    static bool attr = false;
-    if (!attr) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gemm_fp64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_gsum_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_hsum_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        attr = true;
-    }
+    FCFS_TRY(ensure_smem((const void *)k_gemm_fp64<true>, 100 * 1024));
+    FCFS_TRY(ensure_smem((const void *)k_gsum_fp64, 100 * 1024));
+    FCFS_TRY(ensure_smem((const void *)k_hsum_fp64, 100 * 1024));
     FCFS_TRY_CUDA(cudaMemsetAsync(P_ws, 0, sizeof(double) * (size_t)plan.items * kTile * kTile, s));
     const int64_t cb = chunk_buckets(K, plan.tiles_x, plan.tiles_y);
     const int64_t nchunk = K > 0 ? (K + cb - 1) / cb : 0;   // K = the clip's bucket count here

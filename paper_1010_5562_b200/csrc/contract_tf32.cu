@@ -1100,12 +1100,7 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     const bool fast = g.single && g.pow2;
     auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1> : tc::k_gemm_tf32<false, 1>)
                     : (fast ? tc::k_gemm_tf32<true, 0> : tc::k_gemm_tf32<false, 0>);
-    const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
-    static size_t attr[4] = {0, 0, 0, 0};
-    if (smem > attr[ki]) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[ki] = smem;
-    }
+    FCFS_TRY(ensure_smem((const void *)kern, smem));
     // fp16 range: coordinate weights (<= T) of the axis slot are scaled by 2^-shift, T 2^-shift <= 256
     int shift = 0;
     if (f16) {
@@ -1146,19 +1141,10 @@ fcfs_status launch_gemm_tf32_chunked(const CornerSrc &src, const GemmPlan &plan,
                   : (fast ? tc::k_gsum_tc<true, 0> : tc::k_gsum_tc<false, 0>);
     auto hk = f16 ? (fast ? tc::k_hsum_tc<true, 1> : tc::k_hsum_tc<false, 1>)
                   : (fast ? tc::k_hsum_tc<true, 0> : tc::k_hsum_tc<false, 0>);
-    // the GEMM's and the operand kernels' shared memory grow differently with the table size (the
-    // GEMM rounds its table to 1 KB): track both
-    static size_t attr[4] = {0, 0, 0, 0}, gattr[4] = {0, 0, 0, 0};
-    const int ki = (f16 ? 2 : 0) + (fast ? 1 : 0);
-    if (smem > attr[ki]) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[ki] = smem;
-    }
-    if (gsmem > gattr[ki]) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
-        gattr[ki] = gsmem;
-    }
+    // (the GEMM's and the operand kernels' shared memory grow differently with the table size)
+    FCFS_TRY(ensure_smem((const void *)kern, smem));
+    FCFS_TRY(ensure_smem((const void *)gk, gsmem));
+    FCFS_TRY(ensure_smem((const void *)hk, gsmem));
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -803,18 +803,10 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
         // the 1344-rect variant (3 CTAs / SM) unless the average clip is larger; if a clip overflows it,
         // the 2048-rect variant reruns the batch (same outputs), and beyond that the general path
         const bool small = R <= (int64_t)kSmallRects * B;
-        static bool battr = false;
-        if (!battr) {
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               kBucketCap * 12 + (kBucketMaxT + 2) * 4));
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<512, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                               100));
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<448, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               4 * kSmallRects * 12 + (kBucketMaxT + 2) * 4));
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_corners_bucket<448, 3>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                               100));
-            battr = true;
-        }
+        FCFS_TRY(ensure_smem((const void *)k_clip_corners_bucket<512, 4>, kBucketCap * 12 + (kBucketMaxT + 2) * 4,
+                             true));
+        FCFS_TRY(ensure_smem((const void *)k_clip_corners_bucket<448, 3>,
+                             4 * kSmallRects * 12 + (kBucketMaxT + 2) * 4, true));
         auto launch = [&](bool large) -> fcfs_status {
             if (large) {
                 const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
@@ -992,12 +984,7 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         int mg = (int)(max_group < 1 ? 1 : max_group);
         size_t smem = sizeof(int4) * kMaxGroup + sizeof(int32_t) * (10 * kMaxGroup + 2) +
                       sizeof(int32_t) * (size_t)(2 * mg) * (2 * mg) + 16;
-        static bool attr_set = false;
-        if (!attr_set) {
-            FCFS_TRY_CUDA(cudaFuncSetAttribute(k_group_corners, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               210 * 1024));
-            attr_set = true;
-        }
+        FCFS_TRY(ensure_smem((const void *)k_group_corners, 210 * 1024));
         if (G > 0) {
             int64_t blocks = G < 148 * 8 ? G : 148 * 8;
             k_group_corners<<<(unsigned)blocks, 256, smem, s>>>((const int4 *)rects, group_ptr, G, clip_ptr, B, T,
@@ -1056,14 +1043,7 @@ static fcfs_status extract_polygon_clips(const int32_t *vx, const int32_t *vy, c
     FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
     FCFS_TRY_CUDA(cudaMemsetAsync(W.status, 0, B * sizeof(unsigned long long), s));
     const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
-    static bool pattr = false;
-    if (!pattr) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_polygons_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kBucketCap * 12 + (kBucketMaxT + 2) * 4));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(k_clip_polygons_bucket, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                           100));
-        pattr = true;
-    }
+    FCFS_TRY(ensure_smem((const void *)k_clip_polygons_bucket, kBucketCap * 12 + (kBucketMaxT + 2) * 4, true));
     // one CTA per clip (the look-back needs every predecessor clip's CTA dispatched before it)
     k_clip_polygons_bucket<<<(unsigned)B, kBucketThreads, bsmem, s>>>(vx, vy, poly_ptr, P, clip_ptr, B, T, x, y, w,
                                                                       cap, corner_ptr, W.status, area, W.err);

@@ -5,6 +5,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -27,6 +30,21 @@ fcfs_status cuda_status(cudaError_t e, const char *where) {
 }
 
 void count_launch(int n) { g_launches += n; }
+
+fcfs_status ensure_smem(const void *fn, size_t bytes, bool max_carveout) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> done;
+    int dev = 0;
+    FCFS_TRY_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(dev, fn);
+    const auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return FCFS_OK;
+    FCFS_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (max_carveout) FCFS_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    done[key] = bytes;
+    return FCFS_OK;
+}
 
 struct ProfRec {
     cudaEvent_t a, b;

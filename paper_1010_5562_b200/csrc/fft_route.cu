@@ -664,12 +664,7 @@ static fcfs_status run_route(const int32_t *x, const int32_t *w, int64_t k_lo, c
     FCFS_CHECK_LAUNCH("k_fr_perm");
     const size_t fsmem2 = (size_t)(p.T2 + p.T2 / 16 + g.nhi2 + (1 << g.b2)) * sizeof(V) +
                           (size_t)(2 * p.N + 1) * sizeof(double2) + (size_t)p.T2 * sizeof(int16_t);
-    static size_t fattr2 = 0;
-    if (fsmem2 > fattr2) {
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem2));
-        FCFS_TRY_CUDA(cudaFuncSetAttribute(fr::k_fr_fft2<V>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        fattr2 = fsmem2;
-    }
+    FCFS_TRY(ensure_smem((const void *)fr::k_fr_fft2<V>, fsmem2, true));
     int64_t tblocks = p.T / 256;
     if (tblocks > 512) tblocks = 512;
     if (tblocks < 1) tblocks = 1;
