@@ -16,6 +16,9 @@ for c in c4 c5; do for p in tf32x3 f16x3; do
 done; done
 FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_fp64_gemm.json 2>/dev/null
 FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --prec tf32x3 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_tf32x3_gemm.json 2>/dev/null
+timeout 300 python bench.py --config layout --steps 5 --warmup 3 --no-cpu-baseline > $O/${T}_bench_layout.json 2>/dev/null
+timeout 300 python bench.py --config haar --steps 5 --warmup 3 > $O/${T}_bench_haar.json 2>/dev/null
+timeout 300 python bench.py --input polygons --steps 5 --warmup 3 $NB > $O/${T}_bench_c3_polygons.json 2>/dev/null
 # ---- launch lists (serialised, cold; shares not absolutes)
 B3="python bench.py --steps 2 --warmup 1 $NB"
 B4="python bench.py --config c4 --steps 1 --warmup 1 $NB"
@@ -27,8 +30,16 @@ $B5 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control non
 F="ncu --set full --clock-control none --import-source on"
 $B3 > /dev/null 2>&1 && $F -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf32 $B3 > $O/ncu_f1.log 2>&1
 $B3 > /dev/null 2>&1 && $F -k regex:k_clip_corners -s 1 -c 1 -o $O/${T}_prof_c3_extract $B3 > $O/ncu_f2.log 2>&1
-$B4 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2|k_fr_row0" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_fft $B4 > $O/ncu_f3.log 2>&1
+$B4 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2|k_fr_row0" -s 0 -c 4 -o $O/${T}_prof_c4_fp64_fft $B4 > $O/ncu_f3.log 2>&1
 FCFS_ROUTE=gemm $B4 > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_fp64|k_gsum_fp64|k_hsum_fp64" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_gemm $B4 > $O/ncu_f4.log 2>&1
 B4t="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
 FCFS_ROUTE=gemm $B4t > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_tf32|k_gsum_tc|k_hsum_tc" -s 0 -c 3 -o $O/${T}_prof_c4_tf32_gemm $B4t > $O/ncu_f5.log 2>&1
+B4t2="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
+$B4t2 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2" -s 0 -c 2 -o $O/${T}_prof_c4_f32_fft $B4t2 > $O/ncu_f6.log 2>&1
+BL="python bench.py --config layout --steps 1 --warmup 1 $NB"
+$BL > /dev/null 2>&1 && $F -k regex:"k_chop" -s 0 -c 4 -o $O/${T}_prof_layout_chop $BL > $O/ncu_f7.log 2>&1
+BH="python bench.py --config haar --steps 1 --warmup 1 --no-cpu-baseline"
+$BH > /dev/null 2>&1 && $F -k regex:"k_haar" -s 0 -c 3 -o $O/${T}_prof_haar $BH > $O/ncu_f8.log 2>&1
+BP="python bench.py --input polygons --steps 1 --warmup 1 $NB"
+$BP > /dev/null 2>&1 && $F -k regex:"k_clip_polygons" -s 0 -c 1 -o $O/${T}_prof_c3_polygons $BP > $O/ncu_f9.log 2>&1
 ls -la $O | grep $T
