@@ -16,7 +16,17 @@
  * with E_x[m,k] = e^{-2 pi i ((m x_k) mod T)/T}; phases are reduced exactly in integers
  * because the vertices lie on the integer lattice.  The contraction is the
  * paper's "Goertzel-like" direct evaluation restricted to a low-pass window
- * or pupil disk (future work P:1247-1255), run in parallel (future work P:1257-1259).
+ * or pupil disk (future work P:1247-1255), run in parallel (future work P:1257-1259); for
+ * one large clip the library may instead take the paper's Step 4 as row DFTs followed by
+ * an output-pruned FFT along y (fcfs_coeffs_route).
+ *
+ * Entry points:
+ *   a1   fcfs_vertices_from_rects, fcfs_vertices_from_polygons, fcfs_chop_rects (layout -> tiles)
+ *   a2-5 fcfs_coeffs (one clip, optional ROWS / VERTEX_BLOCK shard), fcfs_coeffs_batched,
+ *        fcfs_coeffs_route, fcfs_row_buckets
+ *   CHT  fcfs_haar (the paper's continuous Haar transform of the same corners)
+ *   misc *_workspace_bytes, fcfs_window_size, fcfs_pupil_indices, fcfs_status_string,
+ *        fcfs_last_error, fcfs_device_check, fcfs_kernel_launches, fcfs_profile_enable/read
  *
  * Conventions for every entry point:
  *  - All array pointers are DEVICE pointers owned by the caller unless the name ends in
