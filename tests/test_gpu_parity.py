@@ -752,3 +752,17 @@ def test_extraction_small_variant_overflow_reruns(fcfs):
     e = oracle.extract(rects, T, None, cp)
     g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
     _assert_extract_equal(g, e)
+
+
+@pytest.mark.parametrize("cfg,prec", [("c4", "fp64"), ("c4", "tf32x3"), ("c4", "f16x3"), ("c5", "fp64")])
+def test_full_size_sampled_gemm_route(fcfs, route, cfg, prec):
+    """The row-bucket GEMM routes (FP64 DMMA, split tcgen05) at the full BASELINE sizes: the lattice-FFT
+    route is the default there, so the GEMMs are forced here (sampled outputs vs the oracle)."""
+    route("gemm")
+    wl = inputs.make(cfg)
+    g, F = _clip_coeffs(fcfs, wl, prec)
+    ms, ns = _sample_indices(wl.M, wl.N, n_rand=96 if cfg == "c5" else 160)
+    idx = (ms + wl.M) * (2 * wl.N + 1) + (ns + wl.N)
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    Fr, B = oracle.coeffs(x, y, w, int(g["area"][0].item()), wl.T, ms, ns)
+    _assert_parity(F[idx], Fr, B, prec, f"{cfg} gemm route sampled", ms, ns)
