@@ -196,6 +196,7 @@ struct FftPlan {
     int32_t mA, nm;    // rows |m| = mA .. mA + nm - 1
     int32_t nr;        // row0 + nm
     int64_t rc;        // rows per chunk of the G workspace
+    int32_t sp;        // sub-row ranges per row in k_fr_fft2 (partial X sums, added in fixed order)
 };
 bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p);
 size_t fft_route_ws_bytes(const FftPlan &p);

@@ -406,12 +406,13 @@ __device__ __forceinline__ void pass_inplace(V *buf, int L, int Ns, const V *tw2
     __syncthreads();
 }
 
-// CTA per row (2 CTAs / SM): one padded work buffer that the TMA bulk copy fills with the next
+// CTA per (row, sub-row range blockIdx.y of gridDim.y) (2 CTAs / SM): one padded work buffer that the TMA bulk copy fills with the next
 // sub-row and the passes transform in place; X[n] accumulates in shared memory
 template <class V>
 __global__ void __launch_bounds__(kThreads, 2)
 k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__restrict__ tabT,
-          const int16_t *__restrict__ pinv, Geo g, int32_t N, int32_t r_first, double2 *Xs, double2 *Axis) {
+          const int16_t *__restrict__ pinv, Geo g, int32_t N, int32_t r_first, int32_t nr, double2 *Xs,
+          double2 *Axis) {
     extern __shared__ __align__(16) unsigned char fsm_raw[];
     const int LP = g.T2 + g.T2 / 16;
     const int nn = 2 * N + 1;
@@ -436,7 +437,8 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
     double2 ax = make_double2(0.0, 0.0);
     const uint32_t maskT = (uint32_t)g.T - 1u;
     const int lead = g.t2bits & 3;
-    for (int y1 = 0; y1 < g.T1; ++y1) {
+    const int ya = (int)((int64_t)g.T1 * blockIdx.y / gridDim.y), yb = (int)((int64_t)g.T1 * (blockIdx.y + 1) / gridDim.y);
+    for (int y1 = ya; y1 < yb; ++y1) {
         if (threadIdx.x == 0) {
             const uint32_t b = su32(&bar);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes + pbytes)
@@ -449,7 +451,7 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
                          : "memory");
         }
         {
-            const uint32_t b = su32(&bar), par = (uint32_t)(y1 & 1);
+            const uint32_t b = su32(&bar), par = (uint32_t)((y1 - ya) & 1);
             uint32_t ok = 0;
             while (!ok)
                 asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
@@ -471,8 +473,8 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
     }
-    const int rg = r_first + r;
-    for (int o = threadIdx.x; o < nn; o += kThreads) Xs[(int64_t)rg * nn + o] = X[o];
+    const int64_t rg = (int64_t)blockIdx.y * nr + r_first + r;   // partial of range blockIdx.y
+    for (int o = threadIdx.x; o < nn; o += kThreads) Xs[rg * nn + o] = X[o];
     for (int o = 16; o > 0; o >>= 1) {
         ax.x += __shfl_xor_sync(0xffffffffu, ax.x, o);
         ax.y += __shfl_xor_sync(0xffffffffu, ax.y, o);
@@ -482,15 +484,21 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
     if (threadIdx.x == 0) {
         double2 a = make_double2(0.0, 0.0);
         for (int i = 0; i < kThreads / 32; ++i) a = cadd(a, red[i]);
-        const double2 gt = GT[r];
+        const double2 gt = blockIdx.y == 0 ? GT[r] : make_double2(0.0, 0.0);
         Axis[rg] = make_double2(fma((double)g.T, gt.x, a.x), fma((double)g.T, gt.y, a.y));
     }
 }
 
 // outputs of rows m in [m_lo, m_hi]: grid.x = rows; Xs row of |m|: 0 -> row 0 (if present), else
-// row0 + (|m| - mA)
+// row0 + (|m| - mA); each row is the sum of the sp sub-row-range partials
+__device__ __forceinline__ double2 psum(const double2 *__restrict__ a, int64_t i, int64_t stride, int sp) {
+    double2 v = a[i];
+    for (int q = 1; q < sp; ++q) v = cadd(v, a[i + q * stride]);   // fixed order: deterministic
+    return v;
+}
+
 __global__ void k_fr_epilogue(const double2 *__restrict__ Xs, const double2 *__restrict__ Axis, EpiArgs ea,
-                              int32_t row0, int32_t mA, void *F) {
+                              int32_t row0, int32_t mA, int32_t nr, int32_t sp, void *F) {
     const int m = ea.m_lo + (int)blockIdx.x;
     if (m > ea.m_hi) return;
     const double pi = 3.141592653589793238462643383279502884;
@@ -525,17 +533,17 @@ __global__ void k_fr_epilogue(const double2 *__restrict__ Xs, const double2 *__r
                 if (neg) { mp = -m; np = -n; }
                 double re, im;
                 if (mp == 0) {              // F[0, n] = i S0[n] / (2 pi n T)
-                    const double2 s = Xs[np + ea.N];
+                    const double2 s = psum(Xs, np + ea.N, (int64_t)nr * nn, sp);
                     const double d = 2.0 * pi * (double)np * (double)ea.T;
                     re = -s.y / d; im = s.x / d;
                 } else {
                     const int64_t row = row0 + (mp - mA);
                     if (np == 0) {          // F[m, 0] = i (sum_k w y E_x) / (2 pi m T)
-                        const double2 s = Axis[row];
+                        const double2 s = psum(Axis, row, nr, sp);
                         const double d = 2.0 * pi * (double)mp * (double)ea.T;
                         re = -s.y / d; im = s.x / d;
                     } else {                // F[m, n] = -S[m, n] / (4 pi^2 m n)
-                        const double2 s = Xs[row * nn + np + ea.N];
+                        const double2 s = psum(Xs, row * nn + np + ea.N, (int64_t)nr * nn, sp);
                         const double d = -4.0 * pi * pi * (double)mp * (double)np;
                         re = s.x / d; im = s.y / d;
                     }
@@ -591,6 +599,16 @@ bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi,
     rc = rc / 8 * 8;
     if (rc < 8) rc = 8;
     p.rc = rc;
+    // sub-row ranges per row: ~4 waves of 2 x 148 CTAs when there are few rows, >= 2 sub-rows each
+    {
+        const int64_t rows = rc < p.nr ? rc : p.nr;
+        int64_t sp = rows > 0 ? (4 * 2 * 148) / rows : 1;
+        const int64_t t1h = (T / T2) / 2;
+        if (sp > t1h) sp = t1h;
+        if (sp > 16) sp = 16;
+        if (sp < 1) sp = 1;
+        p.sp = (int32_t)sp;
+    }
     const char *env = getenv("FCFS_ROUTE");
     if (env && !strcmp(env, "gemm")) return false;
     if (env && !strcmp(env, "fft")) return true;
@@ -621,8 +639,8 @@ static void carve_fft(Carver &cv, const FftPlan &p, FftWs &w) {
     w.tab = cv.take<char>(vb * ((size_t)g.nhi + ((size_t)1 << g.lbits)));
     w.Gd = cv.take<char>(vb * (size_t)(rc > 0 ? rc : 1) * (size_t)p.T);
     w.GT = cv.take<double2>((size_t)(rc > 0 ? rc : 1));
-    w.Xs = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1) * (size_t)(2 * p.N + 1));
-    w.Axis = cv.take<double2>((size_t)(p.nr > 0 ? p.nr : 1));
+    w.Xs = cv.take<double2>((size_t)p.sp * (size_t)(p.nr > 0 ? p.nr : 1) * (size_t)(2 * p.N + 1));
+    w.Axis = cv.take<double2>((size_t)p.sp * (size_t)(p.nr > 0 ? p.nr : 1));
 }
 
 size_t fft_route_ws_bytes(const FftPlan &p) {
@@ -689,13 +707,15 @@ static fcfs_status run_route(const int32_t *x, const int32_t *w, int64_t k_lo, c
                                                                     m_last, (int32_t)(ra - c0), Gd, W.GT);
             FCFS_CHECK_LAUNCH("k_fr_rowsT");
         }
-        fr::k_fr_fft2<V><<<(unsigned)(c1 - c0), fr::kThreads, fsmem2, s>>>(Gd, W.GT, tab, W.pinv, g, p.N,
-                                                                             (int32_t)c0, W.Xs, W.Axis);
+        dim3 fgrid((unsigned)(c1 - c0), (unsigned)p.sp);
+        fr::k_fr_fft2<V><<<fgrid, fr::kThreads, fsmem2, s>>>(Gd, W.GT, tab, W.pinv, g, p.N, (int32_t)c0,
+                                                             (int32_t)(p.nr > 0 ? p.nr : 1), W.Xs, W.Axis);
         FCFS_CHECK_LAUNCH("k_fr_fft");
     }
     const int rows = ea.m_hi - ea.m_lo + 1;
     if (rows > 0) {
-        fr::k_fr_epilogue<<<(unsigned)rows, 128, 0, s>>>(W.Xs, W.Axis, ea, p.row0, p.mA, F);
+        fr::k_fr_epilogue<<<(unsigned)rows, 128, 0, s>>>(W.Xs, W.Axis, ea, p.row0, p.mA,
+                                                        (int32_t)(p.nr > 0 ? p.nr : 1), p.sp, F);
         FCFS_CHECK_LAUNCH("k_fr_epilogue");
     }
     return FCFS_OK;
