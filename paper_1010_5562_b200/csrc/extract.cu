@@ -38,9 +38,16 @@ struct ExtractWs {
     int64_t cap_raw;
 };
 
-__device__ __forceinline__ unsigned long long make_key(int64_t clip, int32_t y, int32_t x) {
-    return ((unsigned long long)clip << (2 * kCoordBits)) | ((unsigned long long)y << kCoordBits) |
-           (unsigned long long)x;
+// key = clip | y | x with cb = coord_bits(T) bits per coordinate (0..T): the radix sort runs over
+// 2 cb + clip_bits(B) bits only (c2, T = 4096: 27 bits, 4 onesweep passes instead of 6)
+__host__ __device__ inline int coord_bits(int32_t T) {
+    int b = 1;
+    while ((int64_t(1) << b) <= (int64_t)T) ++b;
+    return b;
+}
+
+__device__ __forceinline__ unsigned long long make_key(int64_t clip, int32_t y, int32_t x, int cb) {
+    return ((unsigned long long)clip << (2 * cb)) | ((unsigned long long)y << cb) | (unsigned long long)x;
 }
 
 __device__ __forceinline__ int64_t find_clip(const int64_t *clip_ptr, int64_t B, int64_t g) {
@@ -62,6 +69,7 @@ __device__ __forceinline__ bool rect_ok(int4 q, int32_t T) {
 __global__ void k_singleton_corners(const int4 *__restrict__ rects, int64_t R,
                                     const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
                                     unsigned long long *keys, int32_t *wts, int32_t *err) {
+    const int cb = coord_bits(T);
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
          r += (int64_t)gridDim.x * blockDim.x) {
         int4 q = rects[r];
@@ -70,10 +78,10 @@ __global__ void k_singleton_corners(const int4 *__restrict__ rects, int64_t R,
             atomicOr(err, 1);
             q = make_int4(0, 0, 0, 0);
         }
-        keys[4 * r + 0] = make_key(b, q.y, q.x); wts[4 * r + 0] = 1;
-        keys[4 * r + 1] = make_key(b, q.y, q.z); wts[4 * r + 1] = -1;
-        keys[4 * r + 2] = make_key(b, q.w, q.x); wts[4 * r + 2] = -1;
-        keys[4 * r + 3] = make_key(b, q.w, q.z); wts[4 * r + 3] = 1;
+        keys[4 * r + 0] = make_key(b, q.y, q.x, cb); wts[4 * r + 0] = 1;
+        keys[4 * r + 1] = make_key(b, q.y, q.z, cb); wts[4 * r + 1] = -1;
+        keys[4 * r + 2] = make_key(b, q.w, q.x, cb); wts[4 * r + 2] = -1;
+        keys[4 * r + 3] = make_key(b, q.w, q.z, cb); wts[4 * r + 3] = 1;
         if (q.x == q.z) { wts[4 * r + 0] = wts[4 * r + 1] = wts[4 * r + 2] = wts[4 * r + 3] = 0; }
     }
 }
@@ -113,6 +121,7 @@ __global__ void k_group_corners(const int4 *__restrict__ rects, const int64_t *_
                                 int64_t G, const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
                                 unsigned long long *keys, int32_t *wts, int64_t cap_raw,
                                 unsigned long long *raw_count, int32_t *err) {
+    const int cb = coord_bits(T);
     extern __shared__ __align__(16) unsigned char smem[];
     int4 *sr = (int4 *)smem;                                  // [kMaxGroup]
     int32_t *vx = (int32_t *)(sr + kMaxGroup);                // [2*kMaxGroup]
@@ -179,7 +188,7 @@ __global__ void k_group_corners(const int4 *__restrict__ rects, const int64_t *_
             if (wv != 0) {
                 unsigned long long slot = atomicAdd(raw_count, 1ull);
                 if ((int64_t)slot < cap_raw) {
-                    keys[slot] = make_key(b, uy[j], ux[i]);
+                    keys[slot] = make_key(b, uy[j], ux[i], cb);
                     wts[slot] = wv;
                 } else {
                     atomicOr(err, 4);
@@ -201,6 +210,7 @@ __global__ void k_polygon_corners(const int32_t *__restrict__ vx, const int32_t 
                                   const int64_t *__restrict__ poly_ptr, int64_t P,
                                   const int64_t *__restrict__ clip_ptr, int64_t B, int32_t T,
                                   unsigned long long *keys, int32_t *wts, int32_t *err) {
+    const int cb = coord_bits(T);
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += nwarps) {
@@ -229,7 +239,7 @@ __global__ void k_polygon_corners(const int32_t *__restrict__ vx, const int32_t 
             const bool hin = vy[v0 + h] == yi && vx[v0 + h] != xi;
             const bool hout = vy[v0 + j] == yi && vx[v0 + j] != xi;
             const bool ok = !(bad || range);
-            keys[v0 + i] = ok ? make_key(b, yi, xi) : make_key(b, 0, 0);
+            keys[v0 + i] = ok ? make_key(b, yi, xi, cb) : make_key(b, 0, 0, cb);
             wts[v0 + i] = ok ? s * ((int)hin - (int)hout) : 0;
         }
     }
@@ -254,7 +264,7 @@ __global__ void k_flags(const int32_t *wts, const int64_t *num_runs, int64_t n, 
 
 __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, const int32_t *flags,
                           const int32_t *pos, int64_t n, int64_t cap, int32_t *x, int32_t *y, int32_t *w,
-                          unsigned long long *ckeys, int64_t *area, int64_t *K) {
+                          unsigned long long *ckeys, int64_t *area, int64_t *K, int cb) {
     // warp-uniform loop: the area is reduced over the warp before the atomic (corners are sorted by
     // clip, so a warp nearly always holds one clip: one atomic per warp instead of one per corner)
     const int lane = threadIdx.x & 31;
@@ -267,10 +277,10 @@ __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, c
         if (valid) {
             if (i == n - 1) *K = (int64_t)pos[i] + flags[i];
             const unsigned long long key = ukeys[i];
-            b = (int64_t)(key >> (2 * kCoordBits));
+            b = (int64_t)(key >> (2 * cb));
             if (flags[i]) {
-                const int32_t xx = (int32_t)(key & ((1ull << kCoordBits) - 1));
-                const int32_t yy = (int32_t)((key >> kCoordBits) & ((1ull << kCoordBits) - 1));
+                const int32_t xx = (int32_t)(key & ((1ull << cb) - 1));
+                const int32_t yy = (int32_t)((key >> cb) & ((1ull << cb) - 1));
                 const int64_t p = pos[i];
                 ckeys[p] = key;
                 if (p < cap) { x[p] = xx; y[p] = yy; w[p] = agg[i]; }
@@ -287,12 +297,13 @@ __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, c
     }
 }
 
-__global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, int64_t B, int64_t *corner_ptr) {
+__global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, int64_t B, int64_t *corner_ptr,
+                             int cb) {
     int64_t n = *K;
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= B;
          b += (int64_t)gridDim.x * blockDim.x) {
         if (b == B) { corner_ptr[b] = n; continue; }
-        unsigned long long target = (unsigned long long)b << (2 * kCoordBits);
+        unsigned long long target = (unsigned long long)b << (2 * cb);
         int64_t lo = 0, hi = n;
         while (lo < hi) {
             int64_t mid = (lo + hi) >> 1;
@@ -853,7 +864,7 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
 
 // steps 2-5 of the general path on the raw (key, weight) list in W.keys_a / W.w_a: sort, merge
 // equal keys (sum), drop zeros, scatter + area, corner_ptr; one stream sync for K and the error bits
-static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int end_bit, int64_t B, int64_t cap, int32_t *x,
+static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int cb, int end_bit, int64_t B, int64_t cap, int32_t *x,
                                   int32_t *y, int32_t *w, int64_t *corner_ptr, int64_t *area, int64_t &Kh,
                                   int32_t &errh, cudaStream_t s) {
     const int threads = 256;
@@ -873,10 +884,10 @@ static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int end_bit, in
     FCFS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, W.flags, W.pos, (int)cap_raw, s));
     count_launch(2);
     k_scatter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, W.flags, W.pos, cap_raw, cap, x, y, w,
-                                                   W.keys_b, area, W.K);
+                                                   W.keys_b, area, W.K, cb);
     FCFS_CHECK_LAUNCH("k_scatter");
     int64_t pb = (B + 1 + threads - 1) / threads;
-    k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr);
+    k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr, cb);
     FCFS_CHECK_LAUNCH("k_corner_ptr");
     FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, W.K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -955,10 +966,12 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         set_error("fcfs_vertices_from_rects: %lld raw corners exceed 2^31", (long long)cap_raw);
         return FCFS_E_UNSUPPORTED;
     }
-    const int end_bit = 2 * kCoordBits + clip_bits(B);
+    int cb = coord_bits(T), end_bit = 2 * cb + clip_bits(B);
+    const size_t cub_max = cub_bytes_for(cap_raw, 2 * kCoordBits + clip_bits(B));   // as the size query
+    if (cub_bytes_for(cap_raw, end_bit) > cub_max) { cb = kCoordBits; end_bit = 2 * cb + clip_bits(B); }
     Carver cv(ws, ws_bytes);
     ExtractWs W;
-    carve(cv, cap_raw, cub_bytes_for(cap_raw, end_bit), W);
+    carve(cv, cap_raw, cub_max, W);
     if (!cv.fits()) {
         set_error("fcfs_vertices_from_rects: workspace %zu < %zu bytes", ws_bytes, cv.used());
         return FCFS_E_WORKSPACE;
@@ -996,7 +1009,7 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
     }
     int64_t Kh = 0;
     int32_t errh = 0;
-    fcfs_status st = finish_corners(W, cap_raw, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
+    fcfs_status st = finish_corners(W, cap_raw, cb, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
     if (st != FCFS_OK) return st;
     if (K_host) *K_host = Kh;
     if (errh & 1) {
@@ -1089,10 +1102,12 @@ fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, co
         set_error("fcfs_vertices_from_polygons: %lld vertices exceed 2^31", (long long)V);
         return FCFS_E_UNSUPPORTED;
     }
-    const int end_bit = 2 * kCoordBits + clip_bits(B);
+    int cb = coord_bits(T), end_bit = 2 * cb + clip_bits(B);
+    const size_t cub_max = cub_bytes_for(cap_raw, 2 * kCoordBits + clip_bits(B));   // as the size query
+    if (cub_bytes_for(cap_raw, end_bit) > cub_max) { cb = kCoordBits; end_bit = 2 * cb + clip_bits(B); }
     Carver cv(ws, ws_bytes);
     ExtractWs W;
-    carve(cv, cap_raw, cub_bytes_for(cap_raw, end_bit), W);
+    carve(cv, cap_raw, cub_max, W);
     if (!cv.fits()) {
         set_error("fcfs_vertices_from_polygons: workspace %zu < %zu bytes", ws_bytes, cv.used());
         return FCFS_E_WORKSPACE;
@@ -1113,7 +1128,7 @@ fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, co
     }
     int64_t Kh = 0;
     int32_t errh = 0;
-    fcfs_status st = finish_corners(W, cap_raw, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
+    fcfs_status st = finish_corners(W, cap_raw, cb, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
     if (st != FCFS_OK) return st;
     if (K_host) *K_host = Kh;
     if (errh & 16) {
