@@ -86,7 +86,8 @@ __global__ void k_singleton_corners(const int4 *__restrict__ rects, int64_t R,
     }
 }
 
-// sort v[0..n) (stable rank sort, O(n) per thread) and unique it into uniq[0..*nu)
+// sort v[0..n) (stable rank sort, O(n) per thread) and unique it into uniq[0..*nu) (each distinct
+// value's slot = number of distinct values before it, O(n) per thread: no serial pass)
 __device__ __forceinline__ void compress(const int32_t *v, int n, int32_t *tmp, int32_t *uniq, int32_t *nu) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         int32_t vi = v[i];
@@ -98,11 +99,13 @@ __device__ __forceinline__ void compress(const int32_t *v, int n, int32_t *tmp, 
         tmp[rank] = vi;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const bool first = i == 0 || tmp[i] != tmp[i - 1];
+        if (!first && i != n - 1) continue;
         int c = 0;
-        for (int i = 0; i < n; ++i)
-            if (i == 0 || tmp[i] != tmp[i - 1]) uniq[c++] = tmp[i];
-        *nu = c;
+        for (int j = 1; j <= i; ++j) c += tmp[j] != tmp[j - 1];
+        if (first) uniq[c] = tmp[i];
+        if (i == n - 1) *nu = c + 1;
     }
     __syncthreads();
 }
@@ -166,27 +169,56 @@ __global__ void k_group_corners(const int4 *__restrict__ rects, const int64_t *_
             atomicAdd(&grid[i1 * ny + j1], 1);
         }
         __syncthreads();
-        // prefix sums: along j for each i, then along i for each j -> coverage count of cell (i, j)
-        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-            int s = 0;
-            for (int j = 0; j < ny; ++j) { s += grid[i * ny + j]; grid[i * ny + j] = s; }
+        // prefix sums (warp per line, shuffle scans): along j for each i, then along i for each j ->
+        // coverage count of cell (i, j), kept as the union indicator
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int i = warp; i < nx; i += nw) {
+            int carry = 0;
+            for (int j0 = 0; j0 < ny; j0 += 32) {
+                const int j = j0 + lane;
+                int v = j < ny ? grid[i * ny + j] : 0;
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, v, d);
+                    if (lane >= d) v += u;
+                }
+                if (j < ny) grid[i * ny + j] = carry + v;
+                carry += __shfl_sync(0xffffffffu, v, 31);
+            }
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < ny; j += blockDim.x) {
-            int s = 0;
-            for (int i = 0; i < nx; ++i) { s += grid[i * ny + j]; grid[i * ny + j] = (s > 0 ? 1 : 0); }
+        for (int j = warp; j < ny; j += nw) {
+            int carry = 0;
+            for (int i0 = 0; i0 < nx; i0 += 32) {
+                const int i = i0 + lane;
+                int v = i < nx ? grid[i * ny + j] : 0;
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, v, d);
+                    if (lane >= d) v += u;
+                }
+                if (i < nx) grid[i * ny + j] = carry + v > 0 ? 1 : 0;
+                carry += __shfl_sync(0xffffffffu, v, 31);
+            }
         }
         __syncthreads();
-        // mixed difference of the union indicator at every grid point
-        for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) {
-            int i = t / ny, j = t - i * ny;
-            int c00 = grid[t];
-            int cm0 = i > 0 ? grid[t - ny] : 0;
-            int c0m = j > 0 ? grid[t - 1] : 0;
-            int cmm = (i > 0 && j > 0) ? grid[t - ny - 1] : 0;
-            int wv = c00 - cm0 - c0m + cmm;
+        // mixed difference of the union indicator at every grid point; one slot reservation per warp
+        for (int t0 = warp * 32; t0 < nx * ny; t0 += blockDim.x) {
+            const int t = t0 + lane;
+            int wv = 0, i = 0, j = 0;
+            if (t < nx * ny) {
+                i = t / ny; j = t - i * ny;
+                const int c00 = grid[t];
+                const int cm0 = i > 0 ? grid[t - ny] : 0;
+                const int c0m = j > 0 ? grid[t - 1] : 0;
+                const int cmm = (i > 0 && j > 0) ? grid[t - ny - 1] : 0;
+                wv = c00 - cm0 - c0m + cmm;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, wv != 0);
+            if (m == 0) continue;
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(raw_count, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
             if (wv != 0) {
-                unsigned long long slot = atomicAdd(raw_count, 1ull);
+                const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
                 if ((int64_t)slot < cap_raw) {
                     keys[slot] = make_key(b, uy[j], ux[i], cb);
                     wts[slot] = wv;
@@ -1000,7 +1032,8 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         FCFS_TRY(ensure_smem((const void *)k_group_corners, 210 * 1024));
         if (G > 0) {
             int64_t blocks = G < 148 * 8 ? G : 148 * 8;
-            k_group_corners<<<(unsigned)blocks, 256, smem, s>>>((const int4 *)rects, group_ptr, G, clip_ptr, B, T,
+            const int gthreads = mg <= 8 ? 128 : (mg <= 32 ? 256 : 512);   // (2 mg)^2 grid cells per group
+            k_group_corners<<<(unsigned)blocks, gthreads, smem, s>>>((const int4 *)rects, group_ptr, G, clip_ptr, B, T,
                                                                  W.keys_a, W.w_a, cap_raw, raw_count, W.err);
             FCFS_CHECK_LAUNCH("k_group_corners");
         }
