@@ -100,7 +100,18 @@ struct CornerSrc {
     const int32_t *bptr, *by;    // [nb+1], [nb] (workspace, padded for 16-byte bulk copies)
     const int64_t *clip_bptr;    // [B+1] (B = 1 for a single range)
     int64_t kend;                // length of the x / w arrays (bulk copies stay below kend & ~3)
+    // edge form (edges.cu; batched split-TF32): clip b's edges are [corner_ptr[b], + ecnt[b]) of
+    // (exa, exb, ey, ec); ecnt == nullptr: corner form
+    const int32_t *exa, *exb, *ey, *ec, *ecnt;
 };
+
+// edge pairing pre-pass (edges.cu)
+struct EdgeWs {
+    int32_t *xa, *xb, *y, *c, *cnt;
+};
+void carve_edges(Carver &cv, int64_t K, int64_t B, EdgeWs &e);
+fcfs_status run_edges(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *corner_ptr, int64_t B,
+                      const EdgeWs &e, cudaStream_t s);
 
 // row-bucket workspace and pass (buckets.cu)
 struct BucketWs {

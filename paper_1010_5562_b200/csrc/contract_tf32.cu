@@ -272,8 +272,12 @@ __device__ __forceinline__ ItemInfo item_info(const CornerSrc &src, const GemmPl
     it.tiy = (int)(rem / plan.splits);
     const int split = (int)(rem - (int64_t)it.tiy * plan.splits);
     int64_t kb, ke;
-    if (src.corner_ptr) { kb = src.corner_ptr[clip]; ke = src.corner_ptr[clip + 1]; }
-    else { kb = src.k_lo; ke = src.k_hi; }
+    if (src.corner_ptr) {
+        kb = src.corner_ptr[clip];
+        ke = src.ecnt ? kb + src.ecnt[clip] : src.corner_ptr[clip + 1];   // edge form: the clip's edges
+    } else {
+        kb = src.k_lo; ke = src.k_hi;
+    }
     const int64_t span = ke - kb;
     it.k0 = kb + span * split / plan.splits;
     it.k1 = kb + span * (split + 1) / plan.splits;
@@ -323,6 +327,19 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
 }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+        " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// lo part of the hi/lo split for two values: v - (v with the low 13 mantissa bits cleared), exact
+__device__ __forceinline__ float2 lo2(float2 v) {
+    return sub2(v, make_float2(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u)));
+}
 // (re, im) <- (re, im) (c + i s) for two independent values, one per FP32x2 lane:
 // re' = re c - im s, im' = im c + re s (the same rounding sequence as the scalar fmaf form)
 __device__ __forceinline__ void rot2(float2 &re, float2 &im, float2 c, float2 sn) {
@@ -362,15 +379,9 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
     const uint32_t M13 = 0xFFFFE000u;
 #pragma unroll
     for (int i = 0; i < kSlots; ++i) {
-        float4 rl, il;
-        rl.x = re.x - __uint_as_float(__float_as_uint(re.x) & M13);
-        rl.y = re.y - __uint_as_float(__float_as_uint(re.y) & M13);
-        rl.z = re.z - __uint_as_float(__float_as_uint(re.z) & M13);
-        rl.w = re.w - __uint_as_float(__float_as_uint(re.w) & M13);
-        il.x = im.x - __uint_as_float(__float_as_uint(im.x) & M13);
-        il.y = im.y - __uint_as_float(__float_as_uint(im.y) & M13);
-        il.z = im.z - __uint_as_float(__float_as_uint(im.z) & M13);
-        il.w = im.w - __uint_as_float(__float_as_uint(im.w) & M13);
+        const float2 rl01 = lo2(make_float2(re.x, re.y)), rl23 = lo2(make_float2(re.z, re.w));
+        const float2 il01 = lo2(make_float2(im.x, im.y)), il23 = lo2(make_float2(im.z, im.w));
+        const float4 rl = make_float4(rl01.x, rl01.y, rl23.x, rl23.y), il = make_float4(il01.x, il01.y, il23.x, il23.y);
         // row j0 + i; 8-slot blocks start on an 8-row atom (j0 % 8 == 0): r % 8 == i
         const int r7 = kSlots == 8 ? i : ((j0 + i) & 7);
         uint8_t *base = op + (kSlots == 8 ? (j0 >> 3) : ((j0 + i) >> 3)) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);
@@ -401,6 +412,87 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         *(float4 *)(base) = c;
         *(float4 *)(base + 4 * 1024) = z;
         *(float4 *)(base + 8 * 1024) = cl;
+        *(float4 *)(base + 12 * 1024) = z;
+    }
+}
+
+// Edge-form producer task (kEdge, edges.cu): 4 consecutive edges x kSlots pair slots of the x side.
+// Edge (x_a, x_b, c) contributes c (E(f x_a) - E(f x_b)); both ends run their own angle-addition
+// recurrence and the difference is split and stored exactly like a corner's value (x_b < 0: one
+// end).  The axis slot carries c (x_a - x_b) (an exact integer, |.| < 2^24).
+template <bool kFast, int kSlots>
+__device__ __forceinline__ void produce_edge(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
+                                             const int32_t xa[4], const int32_t xb[4], const int32_t c[4],
+                                             const TabGeom &g, const float2 *tab) {
+    const uint32_t f0 = (uint32_t)(sp.f0 + p0);
+    float2 ra01, ra23, ia01, ia23, rb01, rb23, ib01, ib23;   // end a / end b, edges (0,1) and (2,3)
+    float2 ca01, ca23, sa01, sa23, cb01, cb23, sb01, sb23;
+    {
+        float2 a[4], e[4], bb[4], eb[4];
+        float wa[4], wb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t vb = xb[q] >= 0 ? (uint32_t)xb[q] : 0u;
+            a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)xa[q], g), g, tab);
+            e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)xa[q], g), g, tab);
+            bb[q] = twiddle<kFast>(phase<kFast>(f0, vb, g), g, tab);
+            eb[q] = twiddle<kFast>(phase<kFast>(1u, vb, g), g, tab);
+            wa[q] = (float)c[q];
+            wb[q] = xb[q] >= 0 ? (float)c[q] : 0.f;
+        }
+        ra01 = make_float2(wa[0] * a[0].x, wa[1] * a[1].x); ra23 = make_float2(wa[2] * a[2].x, wa[3] * a[3].x);
+        ia01 = make_float2(wa[0] * a[0].y, wa[1] * a[1].y); ia23 = make_float2(wa[2] * a[2].y, wa[3] * a[3].y);
+        rb01 = make_float2(wb[0] * bb[0].x, wb[1] * bb[1].x); rb23 = make_float2(wb[2] * bb[2].x, wb[3] * bb[3].x);
+        ib01 = make_float2(wb[0] * bb[0].y, wb[1] * bb[1].y); ib23 = make_float2(wb[2] * bb[2].y, wb[3] * bb[3].y);
+        ca01 = make_float2(e[0].x, e[1].x); ca23 = make_float2(e[2].x, e[3].x);
+        sa01 = make_float2(e[0].y, e[1].y); sa23 = make_float2(e[2].y, e[3].y);
+        cb01 = make_float2(eb[0].x, eb[1].x); cb23 = make_float2(eb[2].x, eb[3].x);
+        sb01 = make_float2(eb[0].y, eb[1].y); sb23 = make_float2(eb[2].y, eb[3].y);
+    }
+    const uint32_t M13 = 0xFFFFE000u;
+#pragma unroll
+    for (int i = 0; i < kSlots; ++i) {
+        const float4 re = make_float4(ra01.x - rb01.x, ra01.y - rb01.y, ra23.x - rb23.x, ra23.y - rb23.y);
+        const float4 im = make_float4(ia01.x - ib01.x, ia01.y - ib01.y, ia23.x - ib23.x, ia23.y - ib23.y);
+        float4 rl, il;
+        rl.x = re.x - __uint_as_float(__float_as_uint(re.x) & M13);
+        rl.y = re.y - __uint_as_float(__float_as_uint(re.y) & M13);
+        rl.z = re.z - __uint_as_float(__float_as_uint(re.z) & M13);
+        rl.w = re.w - __uint_as_float(__float_as_uint(re.w) & M13);
+        il.x = im.x - __uint_as_float(__float_as_uint(im.x) & M13);
+        il.y = im.y - __uint_as_float(__float_as_uint(im.y) & M13);
+        il.z = im.z - __uint_as_float(__float_as_uint(im.z) & M13);
+        il.w = im.w - __uint_as_float(__float_as_uint(im.w) & M13);
+        const int r7 = (j0 + i) & 7;
+        uint8_t *base = op + ((j0 + i) >> 3) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);
+        *(float4 *)(base) = re;
+        *(float4 *)(base + 4 * 1024) = im;
+        *(float4 *)(base + 8 * 1024) = rl;
+        *(float4 *)(base + 12 * 1024) = il;
+        if (i < kSlots - 1) {
+            rot2(ra01, ia01, ca01, sa01);
+            rot2(ra23, ia23, ca23, sa23);
+            rot2(rb01, ib01, cb01, sb01);
+            rot2(rb23, ib23, cb23, sb23);
+        }
+    }
+    const int ia = sp.nf - p0;
+    if (sp.axis && ia >= 0 && ia < kSlots) {
+        float4 v, vl;
+        v.x = (float)(c[0] * (xa[0] - (xb[0] >= 0 ? xb[0] : 0)));
+        v.y = (float)(c[1] * (xa[1] - (xb[1] >= 0 ? xb[1] : 0)));
+        v.z = (float)(c[2] * (xa[2] - (xb[2] >= 0 ? xb[2] : 0)));
+        v.w = (float)(c[3] * (xa[3] - (xb[3] >= 0 ? xb[3] : 0)));
+        vl.x = v.x - __uint_as_float(__float_as_uint(v.x) & M13);
+        vl.y = v.y - __uint_as_float(__float_as_uint(v.y) & M13);
+        vl.z = v.z - __uint_as_float(__float_as_uint(v.z) & M13);
+        vl.w = v.w - __uint_as_float(__float_as_uint(v.w) & M13);
+        const int r7 = (j0 + ia) & 7;
+        uint8_t *base = op + ((j0 + ia) >> 3) * 1024 + r7 * kRowBytes + ((quad ^ r7) << 4);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        *(float4 *)(base) = v;
+        *(float4 *)(base + 4 * 1024) = z;
+        *(float4 *)(base + 8 * 1024) = vl;
         *(float4 *)(base + 12 * 1024) = z;
     }
 }
@@ -483,7 +575,9 @@ __device__ __forceinline__ void produce_f16(uint8_t *op, int oct, int j0, int p0
 // kLoadA (tf32 only, single clip, row buckets): the x-side stage tile is a 16 KB bulk copy from the
 // chunk's pre-split bucket sums (k_gsum_tc) issued by the group's x-side warp; the y-side warp
 // generates one twiddle set per bucket (the bucket's row y); P tiles are ADDED into P_ws.
-template <bool kFast, int kF16, bool kLoadA = false>
+// kEdge (tf32, batched, edges.cu): stages of 32 edges; both warps of a group make both sides
+// (16 slots each, 4 per lane): the x side evaluates both ends of each edge, the y side one twiddle.
+template <bool kFast, int kF16, bool kLoadA = false, bool kEdge = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, EpiArgs ea, void *F, int fuse,
             int axis_shift, TcChunk ch) {
@@ -590,7 +684,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
         // kLoadA: both warps of a group make the y side (16 slots each, 4 per lane); lane 0 of warp 0
         // also issues the x-side bulk copy
         const int quad = l & 7;                           // quad: 16-byte chunk of the stage
-        const int j0 = kLoadA ? 16 * sideB + 4 * (l >> 3) : (l >> 3) << 3;
+        const int j0 = (kLoadA || kEdge) ? 16 * sideB + 4 * (l >> 3) : (l >> 3) << 3;
         const float axs = ldexpf(1.0f, -axis_shift);
         const bool yside = kLoadA || sideB;
         const SidePlan sp = yside ? plan.Y : plan.X;
@@ -603,6 +697,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             int64_t chunk0 = 0;
             const ItemInfo it = kLoadA ? item_info_chunk<kBKp>(src, plan, ch, item, chunk0) : item_info(src, plan, item);
             const int p0 = (yside ? it.tiy : it.tix) * 32 + j0;
+            const int p0x = it.tix * 32 + j0, p0y = it.tiy * 32 + j0;   // kEdge: both sides
             for (int64_t c0 = it.k0; c0 < it.k1; c0 += kChunk) {
                 const int64_t c1 = c0 + kChunk < it.k1 ? c0 + kChunk : it.k1;
                 // 32-bit corner offsets relative to the chunk base; one-own-stage-ahead prefetch
@@ -611,13 +706,21 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 const int32_t *wp = src.w + c0;
                 const int first = (gq - (int)(sc & 3)) & 3;
                 int32_t vn[kCq], wn[kCq];
+                int32_t an[kEdge ? 4 : 1], bn[kEdge ? 4 : 1];   // kEdge: x_a, x_b (vn = y, wn = c)
                 auto fetch = [&](int kr0) {
 #pragma unroll
                     for (int q = 0; q < kCq; ++q) {
                         const int kr = kr0 + q;
                         const bool ok = kr < n;
-                        vn[q] = ok ? __ldg(vp + kr) : 0;
-                        wn[q] = ok ? (yside ? 1 : __ldg(wp + kr)) : 0;
+                        if constexpr (kEdge) {
+                            an[q] = ok ? __ldg(src.exa + c0 + kr) : 0;
+                            bn[q] = ok ? __ldg(src.exb + c0 + kr) : -1;
+                            vn[q] = ok ? __ldg(src.ey + c0 + kr) : 0;
+                            wn[q] = ok ? __ldg(src.ec + c0 + kr) : 0;
+                        } else {
+                            vn[q] = ok ? __ldg(vp + kr) : 0;
+                            wn[q] = ok ? (yside ? 1 : __ldg(wp + kr)) : 0;
+                        }
                     }
                 };
                 int kr0 = first * kBKp + kCq * quad;
@@ -629,7 +732,13 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     if ((int)(sc & 3) != gq) continue;
                     // corner data 16 stages ahead -> L2 (the register prefetch below is only one own
                     // stage = 4 stages ahead, about one HBM latency): one line per lane, per array
-                    if (!kLoadA && !(plan.dbg & 128)) {
+                    if (kEdge && !(plan.dbg & 128)) {   // one 128-byte line per edge array per stage
+                        const int64_t kp = ks + 16 * kBKp;
+                        if (sideB == 0 && l < 4 && kp < it.k1) {
+                            const int32_t *pa = l == 0 ? src.exa : l == 1 ? src.exb : l == 2 ? src.ey : src.ec;
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + kp));
+                        }
+                    } else if (!kLoadA && !(plan.dbg & 128)) {
                         constexpr int kLines = kBKp * 4 / 128;          // 128-byte lines per array per stage
                         const int64_t kp = ks + 16 * kBKp + (int64_t)(l % kLines) * 32;
                         if (l < (yside ? 1 : 2) * kLines && kp < it.k1) {
@@ -639,8 +748,13 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     }
                     int32_t v[kCq];
                     float wt[kCq];
+                    int32_t xa[kEdge ? 4 : 1], xb[kEdge ? 4 : 1], ci[kEdge ? 4 : 1];
 #pragma unroll
-                    for (int q = 0; q < kCq; ++q) { v[q] = vn[q]; wt[q] = (float)wn[q]; }
+                    for (int q = 0; q < kCq; ++q) {
+                        v[q] = vn[q];
+                        wt[q] = kEdge ? 1.f : (float)wn[q];
+                        if constexpr (kEdge) { xa[q] = an[q]; xb[q] = bn[q]; ci[q] = wn[q]; }
+                    }
                     kr0 += kGroups * kBKp;
                     if (!(plan.dbg & 16)) fetch(kr0);
                     if (l == 0) trace(tr, 10 + gq * 2 + sideB, sc);
@@ -668,9 +782,17 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         continue;
                     }
                     if (!(plan.dbg & 1)) {
-                        constexpr int kSl = kLoadA ? 4 : 8;
-                        if constexpr (kF16) produce_f16<kFast, kSl>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
-                        else produce<kFast, kSl>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
+                        constexpr int kSl = (kLoadA || kEdge) ? 4 : 8;
+                        if constexpr (kEdge) {
+                            uint8_t *opx = smem + L.stage0 + my_slot * kStageBytes;
+                            produce_edge<kFast, 4>(opx, quad, j0, p0x, plan.X, xa, xb, ci, g, tab);
+                            produce<kFast, 4>(opx + kOpBytes, quad, j0, p0y, plan.Y, (const int32_t *)v,
+                                              (const float *)wt, g, tab);
+                        } else if constexpr (kF16) {
+                            produce_f16<kFast, kSl>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
+                        } else {
+                            produce<kFast, kSl>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
+                        }
                     }
                     if (!(plan.dbg & 8)) fence_proxy_async();
                     __syncwarp();
@@ -1098,8 +1220,10 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     const tc::Smem L = tc::smem_layout(entries);
     const size_t smem = L.total + 1024;
     const bool fast = g.single && g.pow2;
+    const bool edge = src.ecnt != nullptr && !f16;
     auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1> : tc::k_gemm_tf32<false, 1>)
-                    : (fast ? tc::k_gemm_tf32<true, 0> : tc::k_gemm_tf32<false, 0>);
+                    : edge ? (fast ? tc::k_gemm_tf32<true, 0, false, true> : tc::k_gemm_tf32<false, 0, false, true>)
+                           : (fast ? tc::k_gemm_tf32<true, 0> : tc::k_gemm_tf32<false, 0>);
     FCFS_TRY(ensure_smem((const void *)kern, smem));
     // fp16 range: coordinate weights (<= T) of the axis slot are scaled by 2^-shift, T 2^-shift <= 256
     int shift = 0;

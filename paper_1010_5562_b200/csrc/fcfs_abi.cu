@@ -195,7 +195,14 @@ struct CoeffWs {
     double *H;   // single clip, split precisions: y-side row twiddles of the chunk, [tiles_y][cb][128 rows]
     void *fft;   // single FP64 clip: the lattice-FFT route's workspace (overlaps bk / G / H: one or the other)
     size_t fft_bytes;
+    EdgeWs edges;   // batched split-TF32: the edge form of the corner lists (edges.cu)
 };
+
+// the batched split-TF32 contraction runs on edges unless FCFS_EDGES=0 (corner form; A/B tests)
+static bool edges_enabled() {
+    const char *e = getenv("FCFS_EDGES");
+    return !(e && !strcmp(e, "0"));
+}
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
 // tile).  A single clip always takes the chunked row-bucket path, which writes P.
@@ -235,6 +242,8 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     cv.off = mark;
     const bool bucketed = prec == FCFS_FP64 || single;
     if (bucketed) carve_buckets(cv, K, B, w.bk);
+    w.edges = EdgeWs{};
+    if (!single && prec == FCFS_TF32X3) carve_edges(cv, K, B, w.edges);
     if (bucketed && single) {
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
         const int64_t cb = chunk_buckets(K, p.tiles_x, p.tiles_y);
@@ -479,7 +488,7 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     int32_t m_lo, m_hi;
     st = resolve_rows(win, shard, m_lo, m_hi);
     if (st != FCFS_OK) return st;
-    CornerSrc src;
+    CornerSrc src{};
     src.x = x; src.y = y; src.w = w; src.corner_ptr = nullptr; src.k_lo = 0; src.k_hi = K;
     bool vblock = shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK;
     if (vblock) {
@@ -584,7 +593,7 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M), K_total, B, prec);
     if (!cv.fits()) { set_error("fcfs_coeffs_batched: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
-    CornerSrc src;
+    CornerSrc src{};
     src.x = x; src.y = y; src.w = w; src.corner_ptr = corner_ptr; src.k_lo = 0; src.k_hi = K_total;
     src.bptr = W.bk.bptr; src.by = W.bk.by; src.clip_bptr = W.bk.clip_bptr; src.kend = K_total;
     EpiArgs ea;
@@ -596,6 +605,11 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     {
         StageScope scope(kStageContract, s);
         if (prec == FCFS_FP64) st = run_buckets(y, corner_ptr, B, 0, K_total, kRowBucketCapFp64, W.bk, s);
+        if (prec == FCFS_TF32X3 && K_total > 0 && edges_enabled()) {   // the K/2-term edge form (edges.cu)
+            st = run_edges(x, y, w, corner_ptr, B, W.edges, s);
+            src.exa = W.edges.xa; src.exb = W.edges.xb; src.ey = W.edges.y; src.ec = W.edges.c;
+            src.ecnt = W.edges.cnt;
+        }
         if (st == FCFS_OK) st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
     if (st != FCFS_OK || fused) return st;

@@ -354,6 +354,54 @@ def test_batched_empty_and_tiny_clips(fcfs, prec):
         _assert_parity(F[b], Fr, B, prec, f"clip {b}", ms, ns)
 
 
+def _edge_test_clips(rng, T):
+    """corner lists for the edge form (edges.cu): canonical, permuted, an odd alternating chain on
+    one row, arbitrary weights (zeros, +-2, +-3, duplicates) on few rows, one corner, empty."""
+    r = inputs.random_rects(rng, 12, T, 8, 200)
+    e = oracle.extract(r, T, np.array([0, len(r)], np.int64))
+    canon = (e["x"], e["y"], e["w"])
+    p = rng.permutation(len(e["x"]))
+    perm = (e["x"][p], e["y"][p], e["w"][p])
+    n = 9
+    chain = (np.arange(10, 10 + 20 * n, 20, dtype=np.int32), np.full(n, 33, np.int32),
+             np.array([1 if i % 2 == 0 else -1 for i in range(n)], np.int32))
+    k = 700
+    arb = (rng.integers(0, T + 1, k).astype(np.int32), rng.choice([0, 5, 6, T], k).astype(np.int32),
+           rng.integers(-3, 4, k).astype(np.int32))
+    one = (np.array([7], np.int32), np.array([9], np.int32), np.array([-2], np.int32))
+    empty = (np.zeros(0, np.int32),) * 3
+    # chains across the 32-corner chunks and 256-corner load groups of k_edges: alternating weights
+    # on long runs of one row, with breaks (equal signs, row changes) at seeded places
+    n = 1500
+    ly = np.repeat(np.array([3, 4, 3, 90], np.int32), [333, 300, 600, 267])
+    lw = np.where(np.arange(n) % 2 == 0, 1, -1).astype(np.int32)
+    lw[rng.choice(n, 25, replace=False)] *= -1
+    longc = (rng.integers(0, T + 1, n).astype(np.int32), ly, lw)
+    return [canon, perm, chain, arb, one, empty, longc]
+
+
+@pytest.mark.parametrize("edges", ["1", "0"])
+def test_batched_edge_form_any_corner_list(fcfs, monkeypatch, edges):
+    """The batched split-TF32 contraction pairs corners into edges (edges.cu); the pairing is a
+    term-by-term identity, so any corner list (order, weights) must give the oracle's result."""
+    monkeypatch.setenv("FCFS_EDGES", edges)
+    T, M, N = 512, 15, 13
+    clips = _edge_test_clips(np.random.default_rng(11), T)
+    cp = np.zeros(len(clips) + 1, np.int64)
+    cp[1:] = np.cumsum([len(c[0]) for c in clips])
+    x, y, w = (np.concatenate([c[i] for c in clips]).astype(np.int32) for i in range(3))
+    area = np.array([int(np.sum(c[2].astype(np.int64) * c[0] * c[1])) for c in clips], np.int64)
+    for prec in ("tf32x3", "f16x3"):
+        F = fcfs.coeffs_batched(_dev(cp, torch.int64), _dev(x, torch.int32), _dev(y, torch.int32),
+                                _dev(w, torch.int32), _dev(area, torch.int64), T, M, N, -1.0, "dense",
+                                prec).cpu().numpy()
+        ms, ns = oracle.window(M, N, -1.0)
+        for b in range(len(clips)):
+            sl = slice(cp[b], cp[b + 1])
+            Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+            _assert_parity(F[b], Fr, B, prec, f"{prec} clip {b} edges={edges}", ms, ns)
+
+
 def _buckets_reference(y, corner_ptr, cap, seg=4096):
     """the bucket rule of include/fcfs.h written out: runs of equal consecutive y, cut at clip
     starts, at k % seg == 0 and every `cap` corners from the run start."""
