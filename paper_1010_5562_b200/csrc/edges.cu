@@ -13,73 +13,113 @@
 // alternating +-1 along x, as fcfs_vertices_from_* emit them) give about K/2 edges.
 //
 // Layout: the edges of clip b occupy [corner_ptr[b], corner_ptr[b] + ecnt[b]) of four int32 arrays
-// (a clip never has more edges than corners), so no global compaction and no host sync.
+// (a clip never has more edges than corners), so no global compaction and no host sync.  The edges
+// keep the corner order (each edge sits at its head corner's rank among the emitted corners).
 #include "common.cuh"
 
 namespace fcfs {
 
-// warp per clip; groups of kG chunks of 32 corners whose loads are all issued together (the loop is
-// otherwise one dependent HBM round trip per chunk); the chain start is carried across chunks
-constexpr int kG = 8;
+// warp per clip, 4 consecutive corners per lane (128 per step).  The next step's corners are loaded
+// while this one is processed; inside a lane the links, chain starts and emits are local; across
+// lanes one ballot finds the last chain start before each lane and one warp scan places the edges.
+constexpr int kCpl = 4;   // corners per lane per step
 
-__global__ void k_edges(const int32_t *__restrict__ x, const int32_t *__restrict__ y, const int32_t *__restrict__ w,
-                        const int64_t *__restrict__ corner_ptr, int64_t B, int32_t *exa, int32_t *exb, int32_t *ey,
-                        int32_t *ec, int32_t *ecnt) {
+__global__ void __launch_bounds__(256)
+k_edges(const int32_t *__restrict__ x, const int32_t *__restrict__ y, const int32_t *__restrict__ w,
+        const int64_t *__restrict__ corner_ptr, int64_t B, int32_t *exa, int32_t *exb, int32_t *ey, int32_t *ec,
+        int32_t *ecnt) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nw) {
         const int64_t kb = corner_ptr[b], ke = corner_ptr[b + 1];
-        int64_t cstart = kb;   // start of the chain the next chunk's first corner may continue
+        int64_t cstart = kb;            // last chain start before the current step
+        int32_t py = 0, pw = 0;         // the corner before the current step (valid if g0 > kb)
         int32_t cnt = 0;
-        for (int64_t g0 = kb; g0 < ke; g0 += 32 * kG) {
-            int32_t X[kG], Y[kG], W[kG];
+        int32_t X[kCpl], Y[kCpl], W[kCpl], NX = 0, NY = 0, NW = 0;   // a step + the corner after it
+        auto load = [&](int64_t g0) {
 #pragma unroll
-            for (int j = 0; j < kG; ++j) {
-                const int64_t k = g0 + 32 * j + lane;
+            for (int i = 0; i < kCpl; ++i) {
+                const int64_t k = g0 + kCpl * lane + i;
                 const bool ok = k < ke;
-                X[j] = ok ? __ldg(x + k) : 0;
-                Y[j] = ok ? __ldg(y + k) : 0;
-                W[j] = ok ? __ldg(w + k) : 0;
+                X[i] = ok ? __ldg(x + k) : 0;
+                Y[i] = ok ? __ldg(y + k) : 0;
+                W[i] = ok ? __ldg(w + k) : 0;
             }
-            const int64_t gn = g0 + 32 * kG;
-            const int32_t yprev = g0 > kb ? __ldg(y + g0 - 1) : 0, wprev = g0 > kb ? __ldg(w + g0 - 1) : 0;
-            const int32_t xnext = gn < ke ? __ldg(x + gn) : 0, ynext = gn < ke ? __ldg(y + gn) : 0,
-                          wnext = gn < ke ? __ldg(w + gn) : 0;
+            const int64_t kn = g0 + 32 * kCpl;
+            if (lane == 31 && kn < ke) { NX = __ldg(x + kn); NY = __ldg(y + kn); NW = __ldg(w + kn); }
+        };
+        load(kb);
+        for (int64_t g0 = kb; g0 < ke; g0 += 32 * kCpl) {
+            int32_t cx[kCpl], cy[kCpl], cw[kCpl];
 #pragma unroll
-            for (int j = 0; j < kG; ++j) {
-                const int64_t k0 = g0 + 32 * j;
-                if (k0 >= ke) break;   // warp-uniform
-                const int64_t k = k0 + lane;
+            for (int i = 0; i < kCpl; ++i) { cx[i] = X[i]; cy[i] = Y[i]; cw[i] = W[i]; }
+            const int32_t cnx = NX, cny = NY, cnw = NW;
+            const int64_t gn = g0 + 32 * kCpl;
+            if (gn < ke) load(gn);      // in flight while this step is processed
+            const int64_t k0 = g0 + kCpl * lane;
+            // neighbours across lanes
+            int32_t ly = __shfl_up_sync(0xffffffffu, cy[kCpl - 1], 1), lw = __shfl_up_sync(0xffffffffu, cw[kCpl - 1], 1);
+            if (lane == 0) { ly = py; lw = pw; }
+            int32_t nx = __shfl_down_sync(0xffffffffu, cx[0], 1), ny = __shfl_down_sync(0xffffffffu, cy[0], 1),
+                    nw_ = __shfl_down_sync(0xffffffffu, cw[0], 1);
+            if (lane == 31) { nx = cnx; ny = cny; nw_ = cnw; }   // the corner after the step (or unused)
+            bool lin[kCpl], lout[kCpl];
+#pragma unroll
+            for (int i = 0; i < kCpl; ++i) {
+                const int64_t k = k0 + i;
                 const bool valid = k < ke;
-                const int32_t xk = X[j], yk = Y[j], wk = W[j];
-                // neighbours: inside the chunk by shuffles, across chunks from the adjacent registers
-                const int32_t pl_y = j > 0 ? __shfl_sync(0xffffffffu, Y[j > 0 ? j - 1 : 0], 31) : yprev;
-                const int32_t pl_w = j > 0 ? __shfl_sync(0xffffffffu, W[j > 0 ? j - 1 : 0], 31) : wprev;
-                const int32_t nf_x = j + 1 < kG ? __shfl_sync(0xffffffffu, X[j + 1 < kG ? j + 1 : 0], 0) : xnext;
-                const int32_t nf_y = j + 1 < kG ? __shfl_sync(0xffffffffu, Y[j + 1 < kG ? j + 1 : 0], 0) : ynext;
-                const int32_t nf_w = j + 1 < kG ? __shfl_sync(0xffffffffu, W[j + 1 < kG ? j + 1 : 0], 0) : wnext;
-                int32_t yp = __shfl_up_sync(0xffffffffu, yk, 1), wp = __shfl_up_sync(0xffffffffu, wk, 1);
-                if (lane == 0) { yp = pl_y; wp = pl_w; }
-                int32_t xn = __shfl_down_sync(0xffffffffu, xk, 1), yn = __shfl_down_sync(0xffffffffu, yk, 1),
-                        wn = __shfl_down_sync(0xffffffffu, wk, 1);
-                if (lane == 31) { xn = nf_x; yn = nf_y; wn = nf_w; }
-                const bool link_in = valid && k > kb && yp == yk && wp == -wk;        // (k-1, k) may pair
-                const bool link_out = valid && k + 1 < ke && yn == yk && wn == -wk;   // (k, k+1) may pair
-                const unsigned starts = __ballot_sync(0xffffffffu, !link_in);
-                const unsigned upto = starts & (0xffffffffu >> (31 - lane));
-                const int64_t st = upto ? k0 + (31 - __clz(upto)) : cstart;
-                const bool emit = valid && ((k - st) & 1) == 0;   // a pair's head, or an unpaired corner
-                const unsigned em = __ballot_sync(0xffffffffu, emit);
-                if (emit) {
-                    const int64_t p = kb + cnt + __popc(em & ((1u << lane) - 1u));
-                    exa[p] = xk;
-                    exb[p] = link_out ? xn : -1;
-                    ey[p] = yk;
-                    ec[p] = wk;
-                }
-                cnt += __popc(em);
-                if (starts) cstart = k0 + (31 - __clz(starts));
+                const int32_t yp = i ? cy[i - 1] : ly, wp = i ? cw[i - 1] : lw;
+                lin[i] = valid && k > kb && yp == cy[i] && wp == -cw[i];
+                const int32_t yn = i + 1 < kCpl ? cy[i + 1 < kCpl ? i + 1 : 0] : ny;
+                const int32_t wn = i + 1 < kCpl ? cw[i + 1 < kCpl ? i + 1 : 0] : nw_;
+                lout[i] = valid && k + 1 < ke && yn == cy[i] && wn == -cw[i];
             }
+            // last chain start in this lane (-1: none), then the last one before this lane
+            int lst = -1;
+#pragma unroll
+            for (int i = 0; i < kCpl; ++i)
+                if (k0 + i < ke && !lin[i]) lst = i;
+            const unsigned has = __ballot_sync(0xffffffffu, lst >= 0);
+            const unsigned before = has & ((1u << lane) - 1u);
+            const int src = before ? 31 - __clz(before) : 0;
+            const int lst_src = __shfl_sync(0xffffffffu, lst, src);
+            int64_t st = before ? g0 + kCpl * src + lst_src : cstart;
+            int n_emit = 0;
+            bool em[kCpl];
+#pragma unroll
+            for (int i = 0; i < kCpl; ++i) {
+                const int64_t k = k0 + i;
+                if (k < ke && !lin[i]) st = k;
+                em[i] = k < ke && ((k - st) & 1) == 0;
+                n_emit += em[i];
+            }
+            int inc = n_emit;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += v;
+            }
+            int64_t p = kb + cnt + (inc - n_emit);
+#pragma unroll
+            for (int i = 0; i < kCpl; ++i) {
+                if (em[i]) {
+                    const int32_t xn = i + 1 < kCpl ? cx[i + 1 < kCpl ? i + 1 : 0] : nx;
+                    exa[p] = cx[i];
+                    exb[p] = lout[i] ? xn : -1;
+                    ey[p] = cy[i];
+                    ec[p] = cw[i];
+                    ++p;
+                }
+            }
+            cnt += __shfl_sync(0xffffffffu, inc, 31);
+            if (has) {
+                const int ls = 31 - __clz(has);
+                cstart = g0 + kCpl * ls + __shfl_sync(0xffffffffu, lst, ls);
+            } else {
+                (void)__shfl_sync(0xffffffffu, lst, 0);
+            }
+            py = __shfl_sync(0xffffffffu, cy[kCpl - 1], 31);
+            pw = __shfl_sync(0xffffffffu, cw[kCpl - 1], 31);
         }
         if (lane == 0) ecnt[b] = cnt;
     }
