@@ -235,6 +235,25 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def edge_counts(vp, K, cptr_h):
+    """Inner dimension of the batched split-TF32 kernel in edge form (edges.cu): per clip, the corners
+    that head a pair or stay single.  A link joins corners k-1, k of one clip with equal y and
+    opposite weights; chains of links pair up at even positions.  Counted here on the host from the
+    extracted corners (outside the timed region) for the roofline's algorithmic flops."""
+    y = vp.y[:K].cpu().numpy().astype(np.int64)
+    w = vp.w[:K].cpu().numpy().astype(np.int64)
+    k = np.arange(K)
+    first = np.zeros(K, bool)
+    first[cptr_h[:-1][cptr_h[:-1] < K]] = True
+    link = np.zeros(K, bool)
+    link[1:] = (y[1:] == y[:-1]) & (w[1:] == -w[:-1])
+    link &= ~first
+    start = np.maximum.accumulate(np.where(~link, k, 0))
+    emit = ((k - start) % 2) == 0
+    clip = np.searchsorted(cptr_h, k, side="right") - 1
+    return np.bincount(clip, weights=emit, minlength=len(cptr_h) - 1).astype(np.float64)
+
+
 def traffic_for(cfg, prec, route=""):
     """dram read+write bytes per launch of the dominant kernel (or, for the FFT route, of the contract
     stage's kernels) from the committed ncu --set full captures (profiles/traffic.json), or None when
@@ -527,6 +546,9 @@ def main():
             rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
             Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
             k_inner = "row buckets"
+        elif prec == "tf32x3" and os.environ.get("FCFS_EDGES", "1") != "0":
+            Kc = edge_counts(vp, K, cptr_h)
+            k_inner = "edges (K/2-term form)"
         else:
             Kc = np.diff(cptr_h).astype(np.float64)
             k_inner = "corners"
@@ -554,7 +576,8 @@ def main():
                 peak_note = f"FP64: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz (derived)"
             bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else ""),
+            "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else
+                                   ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else "")),
             "kernel": (f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
                        if fft_route else "k_gemm_" + prec),
             "k_inner": f"{k_inner}: {int(Kc.sum())}",
