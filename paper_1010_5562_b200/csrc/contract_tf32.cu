@@ -349,6 +349,15 @@ __device__ __forceinline__ void rot2(float2 &re, float2 &im, float2 c, float2 sn
     im = fma2(im, c, u);
 }
 
+// (cos, sin)(2 pi r / T) on the SFU (MUFU.SIN/COS, |err| <~ 2^-21 on [-pi, pi]) instead of a table load
+__device__ __forceinline__ float2 twiddle_sfu(uint32_t r, int32_t T, float w2pi) {
+    int32_t rr = (int32_t)r;
+    if (rr > (T >> 1)) rr -= T;
+    float sn, cs;
+    __sincosf((float)rr * w2pi, &sn, &cs);
+    return make_float2(cs, sn);
+}
+
 // One producer task: 4 consecutive corners (16-byte chunk `quad` of the stage) x 8 consecutive
 // pair slots (p0 .. p0+7) of one side.  (cos, sin)(f v) comes from an exact-phase table lookup
 // for the first frequency, pre-multiplied by the corner weight, and the angle-addition
@@ -358,7 +367,7 @@ __device__ __forceinline__ void rot2(float2 &re, float2 &im, float2 c, float2 sn
 // the lo rows store the exact v - hi.  Padding slots (p > nf) keep recurrence values: they only
 // feed P entries nobody reads.  The axis slot (p == nf) is overwritten with the coordinate weight.
 // Bank use: a warp (one side) = 8 quads x 4 slot blocks; every STS.128 covers 4 full 128 B rows.
-template <bool kFast, int kSlots = 8>
+template <bool kFast, int kSlots = 8, bool kSfu = false>
 __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
                                         const int32_t v[4], const float wt[4], const TabGeom &g,
                                         const float2 *tab) {
@@ -368,8 +377,14 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
         float2 a[4], e[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[q], g), g, tab);
-            e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[q], g), g, tab);
+            if constexpr (kSfu) {
+                const float w2pi = 6.28318530717958647692f / (float)g.T;
+                a[q] = twiddle_sfu(phase<kFast>(f0, (uint32_t)v[q], g), g.T, w2pi);
+                e[q] = twiddle_sfu(phase<kFast>(1u, (uint32_t)v[q], g), g.T, w2pi);
+            } else {
+                a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)v[q], g), g, tab);
+                e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)v[q], g), g, tab);
+            }
         }
         re = make_float4(wt[0] * a[0].x, wt[1] * a[1].x, wt[2] * a[2].x, wt[3] * a[3].x);
         im = make_float4(wt[0] * a[0].y, wt[1] * a[1].y, wt[2] * a[2].y, wt[3] * a[3].y);
@@ -420,7 +435,7 @@ __device__ __forceinline__ void produce(uint8_t *op, int quad, int j0, int p0, c
 // Edge (x_a, x_b, c) contributes c (E(f x_a) - E(f x_b)); both ends run their own angle-addition
 // recurrence and the difference is split and stored exactly like a corner's value (x_b < 0: one
 // end).  The axis slot carries c (x_a - x_b) (an exact integer, |.| < 2^24).
-template <bool kFast, int kSlots>
+template <bool kFast, int kSlots, bool kSfu = false>
 __device__ __forceinline__ void produce_edge(uint8_t *op, int quad, int j0, int p0, const SidePlan &sp,
                                              const int32_t xa[4], const int32_t xb[4], const int32_t c[4],
                                              const TabGeom &g, const float2 *tab) {
@@ -433,10 +448,18 @@ __device__ __forceinline__ void produce_edge(uint8_t *op, int quad, int j0, int 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint32_t vb = xb[q] >= 0 ? (uint32_t)xb[q] : 0u;
-            a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)xa[q], g), g, tab);
-            e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)xa[q], g), g, tab);
-            bb[q] = twiddle<kFast>(phase<kFast>(f0, vb, g), g, tab);
-            eb[q] = twiddle<kFast>(phase<kFast>(1u, vb, g), g, tab);
+            if constexpr (kSfu) {
+                const float w2pi = 6.28318530717958647692f / (float)g.T;
+                a[q] = twiddle_sfu(phase<kFast>(f0, (uint32_t)xa[q], g), g.T, w2pi);
+                bb[q] = twiddle_sfu(phase<kFast>(f0, vb, g), g.T, w2pi);
+                e[q] = twiddle_sfu(phase<kFast>(1u, (uint32_t)xa[q], g), g.T, w2pi);
+                eb[q] = twiddle_sfu(phase<kFast>(1u, vb, g), g.T, w2pi);
+            } else {
+                a[q] = twiddle<kFast>(phase<kFast>(f0, (uint32_t)xa[q], g), g, tab);
+                bb[q] = twiddle<kFast>(phase<kFast>(f0, vb, g), g, tab);
+                e[q] = twiddle<kFast>(phase<kFast>(1u, (uint32_t)xa[q], g), g, tab);
+                eb[q] = twiddle<kFast>(phase<kFast>(1u, vb, g), g, tab);
+            }
             wa[q] = (float)c[q];
             wb[q] = xb[q] >= 0 ? (float)c[q] : 0.f;
         }
@@ -785,8 +808,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         constexpr int kSl = (kLoadA || kEdge) ? 4 : 8;
                         if constexpr (kEdge) {
                             uint8_t *opx = smem + L.stage0 + my_slot * kStageBytes;
-                            produce_edge<kFast, 4>(opx, quad, j0, p0x, plan.X, xa, xb, ci, g, tab);
-                            produce<kFast, 4>(opx + kOpBytes, quad, j0, p0y, plan.Y, (const int32_t *)v,
+                            produce_edge<kFast, 4, true>(opx, quad, j0, p0x, plan.X, xa, xb, ci, g, tab);
+                            produce<kFast, 4, true>(opx + kOpBytes, quad, j0, p0y, plan.Y, (const int32_t *)v,
                                               (const float *)wt, g, tab);
                         } else if constexpr (kF16) {
                             produce_f16<kFast, kSl>(op, quad, j0, p0, sp, v, wt, axs, g, tab);
