@@ -59,6 +59,8 @@ struct Smem {
 };
 
 constexpr int kStagesLoadA = 6;                 // load-A mode: no fused-epilogue tables, one more stage
+constexpr int kStagesEdge = 5;                  // edge mode (SFU twiddles, no table): 6 fits but measured no faster
+constexpr int kBarBytes = 192;                  // mbarriers (<= 2 x 6 + 4) + the TMEM address slot
 
 // stages: operand ring depth; fused: room for the fused epilogue's output tables
 __host__ __device__ inline Smem smem_layout(int table_entries, int stages = kStages, bool fused = true) {
@@ -67,7 +69,7 @@ __host__ __device__ inline Smem smem_layout(int table_entries, int stages = kSta
     s.table = stages * kStageBytes;
     s.xbuf = s.table + ((table_entries * 8 + 1023) & ~1023);
     s.bars = s.xbuf + 2 * 64 * kXStride * 4;       // xbuf also holds the fused epilogue's fp32 P tile (64 x 65)
-    s.total = s.bars + 256 + (fused ? 4 * (kMaxFuseRows + 2) + 8 * 4 * kMaxFuseRows + 4 * kMaxFuseOut : 0);
+    s.total = s.bars + kBarBytes + (fused ? 4 * (kMaxFuseRows + 2) + 8 * 3 * kMaxFuseRows + 4 * kMaxFuseOut : 0);
     return s;
 }
 
@@ -611,21 +613,20 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
     // 1024-align by offset arithmetic on the __shared__ array (keeps the shared address space, so
     // loads / stores compile to LDS / STS rather than generic LD / ST)
     uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-    const int tab_entries = g.single ? g.T : g.nhi + (1 << g.lbits);
-    constexpr int kS = kLoadA ? kStagesLoadA : kStages;   // operand ring depth of this instantiation
+    const int tab_entries = kEdge ? 0 : (g.single ? g.T : g.nhi + (1 << g.lbits));   // edge: SFU twiddles
+    constexpr int kS = kLoadA ? kStagesLoadA : (kEdge ? kStagesEdge : kStages);   // operand ring depth
     const Smem L = smem_layout(tab_entries, kS, !kLoadA);
     float2 *tab = (float2 *)(smem + L.table);
     float *xbuf = (float *)(smem + L.xbuf);
     uint64_t *bars = (uint64_t *)(smem + L.bars);
     // barrier indices: full[0..S), empty[S..2S), tfull[2S..2S+2), tempty[2S+2..2S+4)
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kS + 4);
-    int32_t *rowoff = (int32_t *)(smem + L.bars + 256);   // fused pupil layout: output offset per row
+    int32_t *rowoff = (int32_t *)(smem + L.bars + kBarBytes);   // fused pupil layout: output offset per row
     // fused output tables: scale factors per |m| / |n| and the packed (m, n) of every output
-    double *f_rows = (double *)(smem + L.bars + 256 + 4 * (kMaxFuseRows + 2));   // -1/(4 pi^2 a)
+    double *f_rows = (double *)(smem + L.bars + kBarBytes + 4 * (kMaxFuseRows + 2));   // -1/(4 pi^2 a)
     double *f_invn = f_rows + kMaxFuseRows;                                      // 1/b
     double *f_axm = f_invn + kMaxFuseRows;                                       // 1/(2 pi a T)
-    double *f_axn = f_axm + kMaxFuseRows;                                        // 1/(2 pi b T)
-    uint32_t *f_mn = (uint32_t *)(f_axn + kMaxFuseRows);                        // (m+M) << 16 | (n+N), bit 31: masked
+    uint32_t *f_mn = (uint32_t *)(f_axm + kMaxFuseRows);                        // (m+M) << 16 | (n+N), bit 31: masked
     const uint32_t bar0 = su32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
     auto EMPTY = [&](int s) { return bar0 + 8u * (kS + s); };
@@ -678,7 +679,6 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             f_rows[a] = a ? -1.0 / (4.0 * pi * pi * (double)a) : 0.0;
             f_invn[a] = a ? 1.0 / (double)a : 0.0;
             f_axm[a] = a ? 1.0 / (2.0 * pi * (double)a * (double)ea.T) : 0.0;
-            f_axn[a] = f_axm[a];
         }
         // packed (m, n) of every output, row by row (rows in the layout's order)
         for (int i = 0; i <= 2 * ea.M; ++i) {
@@ -1001,7 +1001,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                             } else if (m == 0) {     // axis row x (pair ax) x columns c_n / s_n
                                 const int pn = n - 1;
                                 const double sre = Ps[ax * 65 + pn], sim = -(double)Ps[ax * 65 + 32 + pn];
-                                re = -sim * f_axn[n]; im = sre * f_axn[n];
+                                re = -sim * f_axm[n]; im = sre * f_axm[n];   // 1/(2 pi n T)
                             } else {
                                 const int an = n < 0 ? -n : n;
                                 const int pm = m - 1, pn = an - 1;
@@ -1240,10 +1240,10 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
     if (ea) e = *ea;
     tc::TabGeom g = make_tab(T);
     const int entries = g.single ? g.T : g.nhi + (1 << g.lbits);
-    const tc::Smem L = tc::smem_layout(entries);
+    const bool edge = src.ecnt != nullptr && !f16;
+    const tc::Smem L = edge ? tc::smem_layout(0, tc::kStagesEdge) : tc::smem_layout(entries);
     const size_t smem = L.total + 1024;
     const bool fast = g.single && g.pow2;
-    const bool edge = src.ecnt != nullptr && !f16;
     auto kern = f16 ? (fast ? tc::k_gemm_tf32<true, 1> : tc::k_gemm_tf32<false, 1>)
                     : edge ? (fast ? tc::k_gemm_tf32<true, 0, false, true> : tc::k_gemm_tf32<false, 0, false, true>)
                            : (fast ? tc::k_gemm_tf32<true, 0> : tc::k_gemm_tf32<false, 0>);
