@@ -1,7 +1,7 @@
 """debug: err/B on a dense random sample; list the bad entries with their tile/slot coordinates."""
 import os, sys
-sys.path.insert(0, os.environ.get("FCFS_PKG_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
-sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("FCFS_PKG_ROOT", os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))))
+sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle
 from paper_1010_5562_b200 import fcfs, inputs
