@@ -265,9 +265,11 @@ fcfs_status fcfs_device_check(void);                      /* FCFS_OK iff current
 int32_t fcfs_kernel_launches(void);                       /* kernels launched by this thread so far */
 
 /* Stage timing for the bench (CUDA events recorded on the caller's stream around each stage
- * while enabled).  Stages: 0 = a1 extraction, 1 = a2+a3 contraction, 2 = a4+a5 epilogue.
+ * while enabled).  Stages: 0 = a1 extraction, 1 = a2+a3 contraction, 2 = a4+a5 epilogue,
+ * 3 = the edge pairing pre-pass of the batched split-TF32 contraction.
  * fcfs_profile_read synchronises the recorded events, writes the summed milliseconds and the
- * number of recorded launches per stage (n_stages <= 3), and clears the record. */
+ * number of recorded launches per stage (n_stages <= 4; stages >= n_stages are dropped), and
+ * clears the record. */
 fcfs_status fcfs_profile_enable(int32_t on);
 fcfs_status fcfs_profile_read(double *ms_host, int64_t *count_host, int32_t n_stages);
 

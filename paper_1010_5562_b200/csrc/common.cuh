@@ -16,7 +16,7 @@ void count_launch(int n = 1);
 fcfs_status ensure_smem(const void *fn, size_t bytes, bool max_carveout = false);
 
 // stage timing (fcfs_profile_*): RAII pair of events around a stage on stream s
-enum Stage { kStageExtract = 0, kStageContract = 1, kStageEpilogue = 2, kNumStages = 3 };
+enum Stage { kStageExtract = 0, kStageContract = 1, kStageEpilogue = 2, kStagePair = 3, kNumStages = 4 };
 void profile_mark(int stage, int begin, cudaStream_t s);
 struct StageScope {
     int stage;

@@ -602,14 +602,15 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = fcfs_window_size(win);
     bool fused = false;
-    {
+    if (prec == FCFS_TF32X3 && K_total > 0 && edges_enabled()) {   // the K/2-term edge form (edges.cu)
+        StageScope scope(kStagePair, s);
+        st = run_edges(x, y, w, corner_ptr, B, W.edges, s);
+        src.exa = W.edges.xa; src.exb = W.edges.xb; src.ey = W.edges.y; src.ec = W.edges.c;
+        src.ecnt = W.edges.cnt;
+    }
+    if (st == FCFS_OK) {
         StageScope scope(kStageContract, s);
         if (prec == FCFS_FP64) st = run_buckets(y, corner_ptr, B, 0, K_total, kRowBucketCapFp64, W.bk, s);
-        if (prec == FCFS_TF32X3 && K_total > 0 && edges_enabled()) {   // the K/2-term edge form (edges.cu)
-            st = run_edges(x, y, w, corner_ptr, B, W.edges, s);
-            src.exa = W.edges.xa; src.exb = W.edges.xb; src.ey = W.edges.y; src.ec = W.edges.c;
-            src.ecnt = W.edges.cnt;
-        }
         if (st == FCFS_OK) st = run_gemm(src, plan, T, prec, W.P, ea, F, s, &fused);
     }
     if (st != FCFS_OK || fused) return st;

@@ -103,7 +103,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
             "fcfs_haar_workspace_bytes", "fcfs_haar"]
-STAGES = ("extract", "contract", "epilogue")
+STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
 class FcfsError(RuntimeError):
@@ -167,10 +167,11 @@ def profile_enable(on=True):
 
 def profile_read():
     """{stage: (ms_total, launches)} of the CUDA-event-timed stages since the last read."""
-    ms = (ctypes.c_double * 3)()
-    cnt = (ctypes.c_int64 * 3)()
-    _check(_lib.fcfs_profile_read(ms, cnt, 3), "fcfs_profile_read")
-    return {STAGES[i]: (float(ms[i]), int(cnt[i])) for i in range(3)}
+    n = len(STAGES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    _check(_lib.fcfs_profile_read(ms, cnt, n), "fcfs_profile_read")
+    return {STAGES[i]: (float(ms[i]), int(cnt[i])) for i in range(n)}
 
 
 def _max_group_host(group_ptr):
