@@ -23,7 +23,7 @@
  * Entry points:
  *   a1   fcfs_vertices_from_rects, fcfs_vertices_from_polygons, fcfs_chop_rects (layout -> tiles)
  *   a2-5 fcfs_coeffs (one clip, optional ROWS / VERTEX_BLOCK shard), fcfs_coeffs_batched,
- *        fcfs_coeffs_route, fcfs_row_buckets
+ *        fcfs_coeffs_route, fcfs_row_buckets, fcfs_edges
  *   CHT  fcfs_haar (the paper's continuous Haar transform of the same corners)
  *   misc *_workspace_bytes, fcfs_window_size, fcfs_pupil_indices, fcfs_status_string,
  *        fcfs_last_error, fcfs_device_check, fcfs_kernel_launches, fcfs_profile_enable/read
@@ -250,6 +250,29 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
  * clip_bptr  int64 [B+1] out (device): CSR of buckets per clip.
  * nb_host    out (host): bucket count (this call synchronises `stream` once).
  * ------------------------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------------------------
+ * Edge pairing of a corner list — the K/2-term form of Eq. Fkl: two consecutive
+ * corners k, k+1 of one clip with equal y and w_{k+1} = -w_k are one horizontal edge,
+ *     w_k E_x[m,k] E_y[n,k] + w_{k+1} E_x[m,k+1] E_y[n,k+1] = w_k (E_x[m,k] - E_x[m,k+1]) E_y[n,k].
+ * fcfs_coeffs_batched (FCFS_TF32X3) runs its contraction over these edges; this entry point
+ * exposes the same pass (for tests and planning).
+ *
+ * Rule: a link joins k-1 and k when both lie in one clip, y[k-1] == y[k] and w[k-1] == -w[k];
+ * along each maximal chain of links the corners at even chain positions (0, 2, ...) each emit
+ * one edge: a pair's head (x_a = x[k], x_b = x[k+1], y[k], c = w[k]) when k+1 continues the
+ * chain, else a one-ended edge (x_b = -1).  Exact for any corner list (order, weights).
+ * x, y, w    int32 [K] (device), K = corner_ptr[B].
+ * corner_ptr int64 [B+1] (device).
+ * xa, xb, ye, c  int32 [K] out (device): clip b's edges, in corner order, at
+ *            [corner_ptr[b], corner_ptr[b] + ecnt[b]); the rest of [corner_ptr[b], corner_ptr[b+1])
+ *            is left unwritten.
+ * ecnt       int32 [B] out (device): edges per clip.
+ * Asynchronous on `stream`; no workspace, no host synchronisation.
+ * ------------------------------------------------------------------------------------------ */
+fcfs_status fcfs_edges(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *corner_ptr,
+                       int64_t B, int32_t *xa, int32_t *xb, int32_t *ye, int32_t *c, int32_t *ecnt,
+                       void *stream);
+
 size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B);
 fcfs_status fcfs_row_buckets(const int32_t *y, const int64_t *corner_ptr, int64_t B, int64_t K,
                              int32_t cap, int32_t *bptr, int32_t *by, int64_t *clip_bptr,

@@ -618,6 +618,20 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     return launch_epilogue(plan, W.P, ea, F, s);
 }
 
+fcfs_status fcfs_edges(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *corner_ptr,
+                       int64_t B, int32_t *xa, int32_t *xb, int32_t *ye, int32_t *c, int32_t *ecnt,
+                       void *stream) {
+    if (B < 1 || !corner_ptr || !x || !y || !w || !xa || !xb || !ye || !c || !ecnt) {
+        set_error("fcfs_edges: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    EdgeWs e;
+    e.xa = xa; e.xb = xb; e.y = ye; e.c = c; e.cnt = ecnt;
+    return run_edges(x, y, w, corner_ptr, B, e, (cudaStream_t)stream);
+}
+
 size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B) {
     if (K < 0 || B < 1) return 0;
     return buckets_workspace_bytes(K, B);

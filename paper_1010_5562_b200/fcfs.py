@@ -95,6 +95,8 @@ _lib.fcfs_profile_enable.argtypes = [_i32]
 _lib.fcfs_profile_enable.restype = _i32
 _lib.fcfs_profile_read.argtypes = [_P, _P, _i32]
 _lib.fcfs_profile_read.restype = _i32
+_lib.fcfs_edges.argtypes = [_P, _P, _P, _P, _i64, _P, _P, _P, _P, _P, _P]
+_lib.fcfs_edges.restype = _i32
 
 EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_coeffs_workspace_bytes",
             "fcfs_coeffs", "fcfs_batched_workspace_bytes", "fcfs_coeffs_batched", "fcfs_window_size",
@@ -102,7 +104,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
-            "fcfs_haar_workspace_bytes", "fcfs_haar"]
+            "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -422,6 +424,20 @@ def coeffs_batched(corner_ptr, x, y, w, area, T, M, N, r2=-1.0, layout="dense", 
         K_max = int((corner_ptr[1:] - corner_ptr[:-1]).max().item()) if B > 0 else 0
     plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device)
     return plan.run(corner_ptr, x, y, w, area, stream=stream)
+
+
+def edges(corner_ptr, x, y, w, stream=None):
+    """Edge pairing of a corner list (fcfs_edges): dict xa, xb, y, c (int32 [K], clip b's edges at
+    [corner_ptr[b], corner_ptr[b] + ecnt[b])) and ecnt (int32 [B])."""
+    K = int(x.shape[0])
+    B = int(corner_ptr.shape[0]) - 1
+    dev = x.device
+    out = {k: torch.full((max(K, 1),), -7, dtype=torch.int32, device=dev) for k in ("xa", "xb", "y", "c")}
+    ecnt = torch.empty(max(B, 1), dtype=torch.int32, device=dev)
+    _check(_lib.fcfs_edges(_ptr(x), _ptr(y), _ptr(w), _ptr(corner_ptr), B, _ptr(out["xa"]), _ptr(out["xb"]),
+                           _ptr(out["y"]), _ptr(out["c"]), _ptr(ecnt), _stream(stream)), "fcfs_edges")
+    out["ecnt"] = ecnt[:B]
+    return out
 
 
 def row_buckets(y, corner_ptr=None, cap=32, stream=None):

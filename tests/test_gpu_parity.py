@@ -402,6 +402,52 @@ def test_batched_edge_form_any_corner_list(fcfs, monkeypatch, edges):
             _assert_parity(F[b], Fr, B, prec, f"{prec} clip {b} edges={edges}", ms, ns)
 
 
+def _edges_reference(x, y, w, cp):
+    """the pairing rule of include/fcfs.h (fcfs_edges) written out: links join consecutive corners of
+    one clip with equal y and opposite weights; even chain positions emit an edge."""
+    out = {"xa": [], "xb": [], "y": [], "c": [], "ecnt": []}
+    for b in range(len(cp) - 1):
+        n0 = len(out["xa"])
+        pos = 0
+        for k in range(cp[b], cp[b + 1]):
+            link_in = k > cp[b] and y[k - 1] == y[k] and w[k - 1] == -w[k]
+            pos = pos + 1 if link_in else 0
+            if pos % 2 == 0:
+                nxt = k + 1 < cp[b + 1] and y[k + 1] == y[k] and w[k + 1] == -w[k]
+                out["xa"].append(x[k]); out["xb"].append(x[k + 1] if nxt else -1)
+                out["y"].append(y[k]); out["c"].append(w[k])
+        out["ecnt"].append(len(out["xa"]) - n0)
+    return {k: np.array(v, np.int64) for k, v in out.items()}
+
+
+def test_edge_pairing_bit_exact(fcfs):
+    """fcfs_edges (the pre-pass of the batched split-TF32 contraction) against the rule written out:
+    every clip's edge list bit-exact, on adversarial lists and on canonical c3 clips."""
+    T = 512
+    clips = _edge_test_clips(np.random.default_rng(11), T)
+    wl = inputs.c3(clips=12)
+    e3 = oracle.extract(wl.rects, wl.T, None, wl.clip_ptr)
+    for b in range(12):
+        sl = slice(e3["corner_ptr"][b], e3["corner_ptr"][b + 1])
+        clips.append((e3["x"][sl], e3["y"][sl], e3["w"][sl]))
+    cp = np.zeros(len(clips) + 1, np.int64)
+    cp[1:] = np.cumsum([len(c[0]) for c in clips])
+    x, y, w = (np.concatenate([c[i] for c in clips]).astype(np.int32) for i in range(3))
+    g = fcfs.edges(_dev(cp, torch.int64), _dev(x, torch.int32), _dev(y, torch.int32), _dev(w, torch.int32))
+    ref = _edges_reference(x.tolist(), y.tolist(), w.tolist(), cp.tolist())
+    ecnt = g["ecnt"].cpu().numpy()
+    assert np.array_equal(ecnt, ref["ecnt"])
+    got = {k: g[k].cpu().numpy() for k in ("xa", "xb", "y", "c")}
+    r0 = 0
+    for b in range(len(clips)):
+        n = int(ecnt[b])
+        for k in ("xa", "xb", "y", "c"):
+            assert np.array_equal(got[k][cp[b]:cp[b] + n], ref[k][r0:r0 + n]), f"clip {b} {k}"
+        r0 += n
+    # canonical lists pair up: about half as many edges as corners on c3
+    assert ecnt[-12:].sum() < 0.6 * (cp[-1] - cp[-13])
+
+
 def _buckets_reference(y, corner_ptr, cap, seg=4096):
     """the bucket rule of include/fcfs.h written out: runs of equal consecutive y, cut at clip
     starts, at k % seg == 0 and every `cap` corners from the run start."""
