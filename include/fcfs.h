@@ -21,8 +21,8 @@
  * an output-pruned FFT along y (fcfs_coeffs_route).
  *
  * Entry points:
- *   a1   fcfs_vertices_from_rects, fcfs_vertices_from_polygons, fcfs_chop_rects (layout -> tiles)
- *   a2-5 fcfs_coeffs (one clip, optional ROWS / VERTEX_BLOCK shard), fcfs_coeffs_batched,
+ *   a1   fcfs_vertices_from_rects[_edges], fcfs_vertices_from_polygons, fcfs_chop_rects (layout -> tiles)
+ *   a2-5 fcfs_coeffs (one clip, optional ROWS / VERTEX_BLOCK shard), fcfs_coeffs_batched[_edges],
  *        fcfs_coeffs_route, fcfs_row_buckets, fcfs_edges
  *   CHT  fcfs_haar (the paper's continuous Haar transform of the same corners)
  *   misc *_workspace_bytes, fcfs_window_size, fcfs_pupil_indices, fcfs_status_string,
@@ -120,6 +120,17 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
                                      int64_t cap, int64_t *corner_ptr, int64_t *area,
                                      int64_t *K_total_host, void *ws, size_t ws_bytes,
                                      void *stream);
+
+/* The same, also writing the edge pairing of the output corners (fcfs_edges' rule and layout:
+ * xa, xb, ye, c int32 [cap], ecnt int32 [B]; fcfs_edges' pass runs after the extraction), for
+ * fcfs_coeffs_batched_edges: pair once, contract several windows. */
+fcfs_status fcfs_vertices_from_rects_edges(const int32_t *rects, int64_t R, const int64_t *group_ptr,
+                                           int64_t G, const int64_t *clip_ptr, int64_t B, int32_t T,
+                                           int64_t max_group, int32_t *x, int32_t *y, int32_t *w,
+                                           int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                           int64_t *K_total_host, int32_t *xa, int32_t *xb,
+                                           int32_t *ye, int32_t *c, int32_t *ecnt, void *ws,
+                                           size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * a1 from polygon vertex lists (the paper's own input: Alg. 2 REQUIRE "clockwise vertex lists",
@@ -232,6 +243,17 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
                                 const int32_t *w, const int64_t *area, int32_t T,
                                 const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
                                 size_t ws_bytes, void *stream);
+
+/* The same with the edge pairing of the corner lists given (the output of fcfs_edges or of
+ * fcfs_vertices_from_rects_edges for these corners; arrays as fcfs_edges documents): FCFS_TF32X3
+ * contracts over them instead of pairing again; other precisions ignore them.  Same workspace. */
+fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int64_t K_total,
+                                      int64_t K_max, const int32_t *x, const int32_t *y,
+                                      const int32_t *w, const int64_t *area, const int32_t *xa,
+                                      const int32_t *xb, const int32_t *ye, const int32_t *c,
+                                      const int32_t *ecnt, int32_t T, const fcfs_window *win,
+                                      fcfs_precision prec, void *F, void *ws, size_t ws_bytes,
+                                      void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * Row buckets of a corner list — the row structure of Step 4: corners on one row

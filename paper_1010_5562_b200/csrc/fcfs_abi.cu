@@ -357,11 +357,14 @@ size_t fcfs_vertices_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t ma
     return a > b ? a : b;
 }
 
-fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
-                                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group,
-                                     int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr,
-                                     int64_t *area, int64_t *K_total_host, void *ws, size_t ws_bytes,
-                                     void *stream) {
+}  // extern "C"
+
+// a1 for rects; eo != NULL also writes the edge pairing of the output corners (k_edges after the
+// extraction; pairing inside the per-clip bucket kernel measured slower: DESIGN.md §7)
+static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                 const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
+                                 int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                 int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream, const EdgeWs *eo) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && !rects) || !corner_ptr || !area || !K_total_host) {
         set_error("fcfs_vertices_from_rects: invalid sizes or null pointers");
@@ -374,8 +377,39 @@ fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int6
     fcfs_status st = device_ok();
     if (st != FCFS_OK) return st;
     StageScope scope(kStageExtract, (cudaStream_t)stream);
-    return extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
-                   K_total_host, ws, ws_bytes, (cudaStream_t)stream);
+    st = extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area, K_total_host,
+                 ws, ws_bytes, (cudaStream_t)stream);
+    if (st != FCFS_OK || !eo) return st;
+    if (*K_total_host > 0) return run_edges(x, y, w, corner_ptr, B, *eo, (cudaStream_t)stream);
+    FCFS_TRY_CUDA(cudaMemsetAsync(eo->cnt, 0, sizeof(int32_t) * (size_t)B, (cudaStream_t)stream));
+    return FCFS_OK;
+}
+
+extern "C" {
+
+fcfs_status fcfs_vertices_from_rects(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group,
+                                     int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr,
+                                     int64_t *area, int64_t *K_total_host, void *ws, size_t ws_bytes,
+                                     void *stream) {
+    return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
+                         K_total_host, ws, ws_bytes, stream, nullptr);
+}
+
+fcfs_status fcfs_vertices_from_rects_edges(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                           const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group,
+                                           int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr,
+                                           int64_t *area, int64_t *K_total_host, int32_t *xa, int32_t *xb,
+                                           int32_t *ye, int32_t *c, int32_t *ecnt, void *ws, size_t ws_bytes,
+                                           void *stream) {
+    if ((cap > 0 && (!xa || !xb || !ye || !c)) || !ecnt) {
+        set_error("fcfs_vertices_from_rects_edges: null edge output");
+        return FCFS_E_INVALID;
+    }
+    EdgeWs e;
+    e.xa = xa; e.xb = xb; e.y = ye; e.c = c; e.cnt = ecnt;
+    return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
+                         K_total_host, ws, ws_bytes, stream, &e);
 }
 
 size_t fcfs_haar_workspace_bytes(int64_t B, int32_t T) { return haar_workspace_bytes(B, T); }
@@ -568,10 +602,12 @@ size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, i
     return cv.used();
 }
 
-fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
+}  // extern "C"
+
+static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
                                 const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
                                 int32_t T, const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
-                                size_t ws_bytes, void *stream) {
+                                size_t ws_bytes, void *stream, const EdgeWs *given) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     fcfs_status st = check_window(win);
     if (st != FCFS_OK) return st;
@@ -602,11 +638,14 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
     ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = fcfs_window_size(win);
     bool fused = false;
-    if (prec == FCFS_TF32X3 && K_total > 0 && edges_enabled()) {   // the K/2-term edge form (edges.cu)
-        StageScope scope(kStagePair, s);
-        st = run_edges(x, y, w, corner_ptr, B, W.edges, s);
-        src.exa = W.edges.xa; src.exb = W.edges.xb; src.ey = W.edges.y; src.ec = W.edges.c;
-        src.ecnt = W.edges.cnt;
+    if (prec == FCFS_TF32X3 && K_total > 0 && (given || edges_enabled())) {   // the K/2-term form (edges.cu)
+        const EdgeWs *e = given ? given : &W.edges;
+        if (!given) {
+            StageScope scope(kStagePair, s);
+            st = run_edges(x, y, w, corner_ptr, B, W.edges, s);
+        }
+        src.exa = e->xa; src.exb = e->xb; src.ey = e->y; src.ec = e->c;
+        src.ecnt = e->cnt;
     }
     if (st == FCFS_OK) {
         StageScope scope(kStageContract, s);
@@ -630,6 +669,31 @@ fcfs_status fcfs_edges(const int32_t *x, const int32_t *y, const int32_t *w, con
     EdgeWs e;
     e.xa = xa; e.xb = xb; e.y = ye; e.c = c; e.cnt = ecnt;
     return run_edges(x, y, w, corner_ptr, B, e, (cudaStream_t)stream);
+}
+
+extern "C" {
+
+fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
+                                const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
+                                int32_t T, const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
+                                size_t ws_bytes, void *stream) {
+    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, F, ws, ws_bytes, stream,
+                        nullptr);
+}
+
+fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
+                                      const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
+                                      const int32_t *xa, const int32_t *xb, const int32_t *ye, const int32_t *c,
+                                      const int32_t *ecnt, int32_t T, const fcfs_window *win, fcfs_precision prec,
+                                      void *F, void *ws, size_t ws_bytes, void *stream) {
+    if (K_total > 0 && (!xa || !xb || !ye || !c || !ecnt)) {
+        set_error("fcfs_coeffs_batched_edges: null edge input");
+        return FCFS_E_INVALID;
+    }
+    EdgeWs e;
+    e.xa = const_cast<int32_t *>(xa); e.xb = const_cast<int32_t *>(xb); e.y = const_cast<int32_t *>(ye);
+    e.c = const_cast<int32_t *>(c); e.cnt = const_cast<int32_t *>(ecnt);
+    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, F, ws, ws_bytes, stream, &e);
 }
 
 size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B) {

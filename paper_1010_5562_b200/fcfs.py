@@ -62,6 +62,9 @@ _lib.fcfs_vertices_workspace_bytes.restype = _sz
 _lib.fcfs_vertices_from_rects.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P,
                                           ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_vertices_from_rects.restype = _i32
+_lib.fcfs_vertices_from_rects_edges.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P,
+                                                ctypes.POINTER(_i64), _P, _P, _P, _P, _P, _P, _sz, _P]
+_lib.fcfs_vertices_from_rects_edges.restype = _i32
 _lib.fcfs_polygons_workspace_bytes.argtypes = [_i64, _i64, _i64]
 _lib.fcfs_polygons_workspace_bytes.restype = _sz
 _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _i32, _P, _P, _P, _i64, _P, _P,
@@ -84,6 +87,9 @@ _lib.fcfs_coeffs.restype = _i32
 _lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32]
 _lib.fcfs_batched_workspace_bytes.restype = _sz
 _lib.fcfs_coeffs_batched.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _i32, _WP, _i32, _P, _P, _sz, _P]
+_lib.fcfs_coeffs_batched_edges.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _i32, _WP,
+                                           _i32, _P, _P, _sz, _P]
+_lib.fcfs_coeffs_batched_edges.restype = _i32
 _lib.fcfs_coeffs_batched.restype = _i32
 
 _lib.fcfs_row_buckets_workspace_bytes.argtypes = [_i64, _i64]
@@ -104,7 +110,8 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_kernel_launches", "fcfs_profile_enable", "fcfs_profile_read", "fcfs_row_buckets_workspace_bytes",
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
-            "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges"]
+            "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
+            "fcfs_coeffs_batched_edges"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -338,13 +345,29 @@ class VerticesPlan:
         self.area = torch.empty(self.B, dtype=torch.int64, device=device)
         self.ws = _ws(_lib.fcfs_vertices_workspace_bytes(self.R, self.G, self.B, self.mg), device)
         self.K = 0
+        self.edges = None
+
+    def enable_edges(self):
+        """Also write the edge pairing of the corners (fcfs_vertices_from_rects_edges) into self.edges."""
+        n = max(self.cap, 1)
+        self.edges = {k: torch.empty(n, dtype=torch.int32, device=self.x.device) for k in ("xa", "xb", "y", "c")}
+        self.edges["ecnt"] = torch.empty(self.B, dtype=torch.int32, device=self.x.device)
+        return self
 
     def run(self, rects, group_ptr=None, clip_ptr=None, stream=None):
         K = ctypes.c_int64(0)
-        st = _lib.fcfs_vertices_from_rects(_ptr(rects), self.R, _ptr(group_ptr), self.G, _ptr(clip_ptr), self.B,
-                                           self.T, self.mg, _ptr(self.x), _ptr(self.y), _ptr(self.w), self.cap,
-                                           _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K), _ptr(self.ws),
-                                           self.ws.numel(), _stream(stream))
+        if self.edges is None:
+            st = _lib.fcfs_vertices_from_rects(_ptr(rects), self.R, _ptr(group_ptr), self.G, _ptr(clip_ptr), self.B,
+                                               self.T, self.mg, _ptr(self.x), _ptr(self.y), _ptr(self.w), self.cap,
+                                               _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K), _ptr(self.ws),
+                                               self.ws.numel(), _stream(stream))
+        else:
+            e = self.edges
+            st = _lib.fcfs_vertices_from_rects_edges(
+                _ptr(rects), self.R, _ptr(group_ptr), self.G, _ptr(clip_ptr), self.B, self.T, self.mg, _ptr(self.x),
+                _ptr(self.y), _ptr(self.w), self.cap, _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K),
+                _ptr(e["xa"]), _ptr(e["xb"]), _ptr(e["y"]), _ptr(e["c"]), _ptr(e["ecnt"]), _ptr(self.ws),
+                self.ws.numel(), _stream(stream))
         _check(st, "fcfs_vertices_from_rects")
         self.K = K.value
         return self.K
@@ -408,11 +431,19 @@ class BatchedPlan:
         self.per_clip = window_size(M, N, r2, layout)
         self.out = torch.empty(self.B * self.per_clip, dtype=_out_dtype(prec), device=device)
 
-    def run(self, corner_ptr, x, y, w, area, stream=None, out=None):
+    def run(self, corner_ptr, x, y, w, area, stream=None, out=None, edges=None):
+        """edges: the pairing of these corners (dict xa, xb, y, c, ecnt from ``edges`` or
+        ``VerticesPlan.enable_edges``) to contract over instead of pairing again, or None."""
         out = self.out if out is None else out
-        st = _lib.fcfs_coeffs_batched(_ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y),
-                                      _ptr(w), _ptr(area), self.T, ctypes.byref(self.win), self.prec, _ptr(out),
-                                      _ptr(self.ws), self.ws.numel(), _stream(stream))
+        if edges is None:
+            st = _lib.fcfs_coeffs_batched(_ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y),
+                                          _ptr(w), _ptr(area), self.T, ctypes.byref(self.win), self.prec, _ptr(out),
+                                          _ptr(self.ws), self.ws.numel(), _stream(stream))
+        else:
+            st = _lib.fcfs_coeffs_batched_edges(
+                _ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y), _ptr(w), _ptr(area),
+                _ptr(edges["xa"]), _ptr(edges["xb"]), _ptr(edges["y"]), _ptr(edges["c"]), _ptr(edges["ecnt"]),
+                self.T, ctypes.byref(self.win), self.prec, _ptr(out), _ptr(self.ws), self.ws.numel(), _stream(stream))
         _check(st, "fcfs_coeffs_batched")
         return out.view(self.B, self.per_clip)
 

@@ -860,3 +860,44 @@ def test_full_size_sampled_gemm_route(fcfs, route, cfg, prec):
     x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
     Fr, B = oracle.coeffs(x, y, w, int(g["area"][0].item()), wl.T, ms, ns)
     _assert_parity(F[idx], Fr, B, prec, f"{cfg} gemm route sampled", ms, ns)
+
+
+# ------------------------------------------------------------------ fused pairing (extraction writes the edges)
+
+@pytest.mark.parametrize("cfg", ["c3x48", "c1", "c3big"])
+def test_vertices_with_edges(fcfs, cfg):
+    """fcfs_vertices_from_rects_edges: the corners equal the plain extraction's and the edges equal
+    fcfs_edges' on them, on the per-clip bucket path, the general
+    path (union groups) and the 2048-rect bucket variant; fcfs_coeffs_batched_edges
+    with those edges gives bitwise the output of fcfs_coeffs_batched."""
+    if cfg == "c3x48":
+        wl = inputs.c3(clips=48)
+    elif cfg == "c3big":
+        wl = inputs.c3(clips=6, n_lines=1800)           # > 1344 rects per clip: the <512, 4> kernel
+    else:
+        wl = inputs.c1()
+    rects = _dev(wl.rects, torch.int32)
+    gp, cp = _dev(wl.group_ptr, torch.int64), _dev(wl.clip_ptr, torch.int64)
+    G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
+    mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
+    vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=wl.group_ptr is not None).enable_edges()
+    K = vp.run(rects, gp, cp)
+    g = fcfs.vertices_from_rects(rects, wl.T, gp, cp)
+    assert K == g["K"]
+    for a, b in (("x", vp.x), ("y", vp.y), ("w", vp.w)):
+        assert torch.equal(b[:K], g[a])
+    assert torch.equal(vp.corner_ptr, g["corner_ptr"]) and torch.equal(vp.area, g["area"])
+    ref = fcfs.edges(g["corner_ptr"], g["x"], g["y"], g["w"])
+    assert torch.equal(vp.edges["ecnt"], ref["ecnt"])
+    cpn = g["corner_ptr"].cpu().numpy()
+    ec = ref["ecnt"].cpu().numpy()
+    for k in ("xa", "xb", "y", "c"):
+        a, b = vp.edges[k].cpu().numpy(), ref[k].cpu().numpy()
+        for i in range(len(ec)):
+            assert np.array_equal(a[cpn[i]:cpn[i] + ec[i]], b[cpn[i]:cpn[i] + ec[i]]), f"clip {i} {k}"
+    if wl.B > 1:
+        kmax = int(np.diff(cpn).max())
+        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, "pupil", "tf32x3")
+        F1 = plan.run(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"]).clone()
+        F2 = plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area, edges=vp.edges).clone()
+        assert torch.equal(F1, F2)
