@@ -901,3 +901,52 @@ def test_vertices_with_edges(fcfs, cfg):
         F1 = plan.run(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"]).clone()
         F2 = plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area, edges=vp.edges).clone()
         assert torch.equal(F1, F2)
+
+
+# ------------------------------------------------------------------ seeded random sweep
+
+@pytest.mark.parametrize("seed", list(range(32)))
+def test_random_sweep(fcfs, seed):
+    """Seeded random cases across the axes the paths branch on: T (power of two or not, small to
+    5000), union groups or singleton rects, window M x N (M != N, zero), dense / pupil layout,
+    precision, one clip (fcfs_coeffs: GEMM or FFT route) or a batch (fcfs_coeffs_batched: fused tcgen05
+    kernel, edge form).  Every output against the oracle within its precision's bound."""
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.choice([64, 100, 256, 1000, 2048, 4096, 5000]))
+    prec = ["fp64", "tf32x3", "f16x3"][seed % 3]
+    M, N = int(rng.integers(0, 24)), int(rng.integers(0, 24))
+    layout = "pupil" if seed % 4 == 1 else "dense"
+    r2 = float(rng.uniform(10, 2 * max(M, N, 1) ** 2)) if layout == "pupil" else -1.0
+    batched = seed % 2 == 1
+    B = 3 if batched else 1
+    rects, cps = [], [0]
+    for b in range(B):
+        n = int(rng.integers(1, 60))
+        r = inputs.random_rects(rng, n, T, 1, max(2, T // 6))
+        rects.append(r)
+        cps.append(cps[-1] + len(r))
+    rects = np.concatenate(rects).astype(np.int32)
+    cp = np.array(cps, np.int64)
+    grouped = (not batched) and seed % 3 == 0
+    gp = np.array([0, len(rects)], np.int64) if grouped else None
+    e = oracle.extract(rects, T, gp, cp if batched else None)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, _dev(gp, torch.int64),
+                                 _dev(cp, torch.int64) if batched else None)
+    _assert_extract_equal(g, e)
+    ms, ns = oracle.window(M, N, r2 if layout == "pupil" else -1.0)
+    if batched:
+        F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, r2, layout,
+                                prec).cpu().numpy()
+        cpn = e["corner_ptr"]
+        for b in range(B):
+            sl = slice(cpn[b], cpn[b + 1])
+            Fr, Bd = oracle.coeffs(e["x"][sl], e["y"][sl], e["w"][sl], e["area"][b], T, ms, ns)
+            if layout == "dense" and r2 >= 0:
+                out = (ms.astype(np.float64) ** 2 + ns.astype(np.float64) ** 2) > r2
+                Fr[out] = 0
+                Bd[out] = 0
+            _assert_parity(F[b], Fr, Bd, prec, f"seed {seed} clip {b}", ms, ns)
+    else:
+        F = fcfs.coeffs(g["x"], g["y"], g["w"], int(e["area"][0]), T, M, N, r2, layout, prec).cpu().numpy()
+        Fr, Bd = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
+        _assert_parity(F, Fr, Bd, prec, f"seed {seed}", ms, ns)
