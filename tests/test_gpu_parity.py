@@ -906,7 +906,7 @@ def test_vertices_with_edges(fcfs, cfg):
 # ------------------------------------------------------------------ seeded random sweep
 
 @pytest.mark.parametrize("seed", list(range(32)))
-def test_random_sweep(fcfs, seed):
+def test_random_sweep(fcfs, seed, monkeypatch):
     """Seeded random cases across the axes the paths branch on: T (power of two or not, small to
     5000), union groups or singleton rects, window M x N (M != N, zero), dense / pupil layout,
     precision, one clip (fcfs_coeffs: GEMM or FFT route) or a batch (fcfs_coeffs_batched: fused tcgen05
@@ -947,6 +947,11 @@ def test_random_sweep(fcfs, seed):
                 Bd[out] = 0
             _assert_parity(F[b], Fr, Bd, prec, f"seed {seed} clip {b}", ms, ns)
     else:
-        F = fcfs.coeffs(g["x"], g["y"], g["w"], int(e["area"][0]), T, M, N, r2, layout, prec).cpu().numpy()
-        Fr, Bd = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
-        _assert_parity(F, Fr, Bd, prec, f"seed {seed}", ms, ns)
+        # single clip: the route the cost model picks, and (where eligible) the lattice-FFT route forced
+        for route in (None, "fft"):
+            if route:
+                monkeypatch.setenv("FCFS_ROUTE", route)
+            F = fcfs.coeffs(g["x"], g["y"], g["w"], int(e["area"][0]), T, M, N, r2, layout, prec).cpu().numpy()
+            Fr, Bd = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
+            _assert_parity(F, Fr, Bd, prec, f"seed {seed} route {route}", ms, ns)
+        monkeypatch.delenv("FCFS_ROUTE", raising=False)
