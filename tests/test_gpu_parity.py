@@ -955,3 +955,27 @@ def test_random_sweep(fcfs, seed, monkeypatch):
             Fr, Bd = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
             _assert_parity(F, Fr, Bd, prec, f"seed {seed} route {route}", ms, ns)
         monkeypatch.delenv("FCFS_ROUTE", raising=False)
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_haar_random_sweep(fcfs, seed):
+    """Seeded random batches for fcfs_haar: T = 2 .. 512 (every level count), singleton or union
+    rects, up to 3 clips with an empty one; bitwise equal to the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    T = int(2 ** rng.integers(1, 10))
+    B = int(rng.integers(1, 4))
+    rects, cps = [], [0]
+    for b in range(B):
+        n = 0 if (B > 1 and b == 1) else int(rng.integers(1, 40))
+        r = inputs.random_rects(rng, n, T, 1, max(1, T // 3)) if n else np.zeros((0, 4), np.int32)
+        rects.append(r)
+        cps.append(cps[-1] + len(r))
+    rects = np.concatenate(rects).astype(np.int32)
+    cp = np.array(cps, np.int64)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    H = fcfs.haar(g["x"], g["y"], g["w"], g["area"], T, g["corner_ptr"]).cpu().numpy()
+    cpn = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    for b in range(B):
+        sl = slice(cpn[b], cpn[b + 1])
+        assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], T)), f"seed {seed} clip {b} T {T}"
