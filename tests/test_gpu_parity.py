@@ -979,3 +979,26 @@ def test_haar_random_sweep(fcfs, seed):
     for b in range(B):
         sl = slice(cpn[b], cpn[b + 1])
         assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], T)), f"seed {seed} clip {b} T {T}"
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_polygon_random_sweep(fcfs, seed):
+    """Seeded random skyline-polygon batches (either orientation, collinear vertices, overlaps summed):
+    extraction bit-exact against the oracle, then the batched split-TF32 coefficients of every clip."""
+    rng = np.random.default_rng(3000 + seed)
+    T = int(rng.choice([64, 200, 512, 2048]))
+    clips = int(rng.integers(1, 5))
+    ps = inputs.polygon_clips(4000 + seed, clips=clips, T=T, n_poly=int(rng.integers(1, 25)),
+                              max_cols=int(rng.integers(2, 9)), collinear=float(rng.uniform(0, 0.5)))
+    g = _gpu_polys(fcfs, ps)
+    e = oracle.extract_polygons(ps.vx, ps.vy, ps.poly_ptr, ps.T, ps.clip_ptr)
+    _assert_extract_equal(g, e)
+    M, N = int(rng.integers(1, 20)), int(rng.integers(1, 20))
+    F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, -1.0, "dense",
+                            "tf32x3").cpu().numpy()
+    ms, ns = oracle.window(M, N, -1.0)
+    cpn = e["corner_ptr"]
+    for b in range(clips):
+        sl = slice(cpn[b], cpn[b + 1])
+        Fr, Bd = oracle.coeffs(e["x"][sl], e["y"][sl], e["w"][sl], e["area"][b], T, ms, ns)
+        _assert_parity(F[b], Fr, Bd, "tf32x3", f"seed {seed} clip {b}", ms, ns)
