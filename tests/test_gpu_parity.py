@@ -1002,3 +1002,24 @@ def test_polygon_random_sweep(fcfs, seed):
         sl = slice(cpn[b], cpn[b + 1])
         Fr, Bd = oracle.coeffs(e["x"][sl], e["y"][sl], e["w"][sl], e["area"][b], T, ms, ns)
         _assert_parity(F[b], Fr, Bd, "tf32x3", f"seed {seed} clip {b}", ms, ns)
+
+
+@pytest.mark.parametrize("seed", list(range(6)))
+def test_chop_random_sweep(fcfs, seed):
+    """Seeded random layouts for fcfs_chop_rects: T, tile grid and rect sizes drawn so rects span
+    0 .. several tiles, some on tile boundaries; pieces and tile CSR bit-exact against the oracle."""
+    rng = np.random.default_rng(5000 + seed)
+    T = int(rng.choice([1, 7, 64, 100, 256]))
+    tx, ty = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+    W, H = T * tx, T * ty
+    n = int(rng.integers(0, 600))
+    x0 = rng.integers(0, W, n); y0 = rng.integers(0, H, n)
+    x1 = np.minimum(x0 + rng.integers(1, 3 * T + 2, n), W); y1 = np.minimum(y0 + rng.integers(1, 3 * T + 2, n), H)
+    snap = rng.random(n) < 0.2                      # some corners exactly on tile lines
+    x0 = np.where(snap, (x0 // T) * T, x0)
+    rects = np.stack([x0, y0, x1, y1], 1).astype(np.int32).reshape(-1, 4)
+    e = oracle.chop_rects(rects, T, tx, ty)
+    g = fcfs.chop_rects(_dev(rects, torch.int32), T, tx, ty)
+    assert g["n"] == e["n"]
+    assert np.array_equal(g["rects"].cpu().numpy().reshape(-1, 4), np.asarray(e["rects"]).reshape(-1, 4))
+    assert np.array_equal(g["tile_ptr"].cpu().numpy(), e["tile_ptr"])
