@@ -755,13 +755,9 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     if ((int)(sc & 3) != gq) continue;
                     // corner data 16 stages ahead -> L2 (the register prefetch below is only one own
                     // stage = 4 stages ahead, about one HBM latency): one line per lane, per array
-                    if (kEdge && !(plan.dbg & 128)) {   // one 128-byte line per edge array per stage
-                        const int64_t kp = ks + 16 * kBKp;
-                        if (sideB == 0 && l < 4 && kp < it.k1) {
-                            const int32_t *pa = l == 0 ? src.exa : l == 1 ? src.exb : l == 2 ? src.ey : src.ec;
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + kp));
-                        }
-                    } else if (!kLoadA && !(plan.dbg & 128)) {
+                    // edge form: no L2 prefetch — the edges were just written by k_edges and the
+                    // prefetch instructions cost more issue slots than they saved (0.997 vs 1.027 ms)
+                    if (!kEdge && !kLoadA && !(plan.dbg & 128)) {
                         constexpr int kLines = kBKp * 4 / 128;          // 128-byte lines per array per stage
                         const int64_t kp = ks + 16 * kBKp + (int64_t)(l % kLines) * 32;
                         if (l < (yside ? 1 : 2) * kLines && kp < it.k1) {
