@@ -30,9 +30,18 @@ def _dev(a, dtype):
     return None if a is None else torch.as_tensor(np.asarray(a), dtype=dtype).cuda()
 
 
-def _gpu_extract(fcfs, wl):
-    return fcfs.vertices_from_rects(_dev(wl.rects, torch.int32), wl.T, _dev(wl.group_ptr, torch.int64),
-                                    _dev(wl.clip_ptr, torch.int64))
+def _gpu_extract(fcfs, wl, check=True):
+    """GPU extraction of a workload; with check (the default) it is first asserted bit-exact against
+    oracle.extract on the same rects, so every coefficient test below runs on verified corners."""
+    return _extract_checked(fcfs, wl.rects, wl.T, wl.group_ptr, wl.clip_ptr, check)
+
+
+def _extract_checked(fcfs, rects, T, group_ptr=None, clip_ptr=None, check=True):
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, _dev(group_ptr, torch.int64),
+                                 _dev(clip_ptr, torch.int64))
+    if check:
+        _assert_extract_equal(g, oracle.extract(rects, T, group_ptr, clip_ptr))
+    return g
 
 
 def _assert_extract_equal(g, e):
@@ -320,7 +329,7 @@ def _long_row_clip():
 @pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_long_rows_and_unsorted_corners(fcfs, prec):
     T, rects = _long_row_clip()
-    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T)
+    g = _extract_checked(fcfs, rects, T)
     area = int(g["area"][0].item())
     M = N = 12
     F = fcfs.coeffs(g["x"], g["y"], g["w"], area, T, M, N, prec=prec).cpu().numpy()
@@ -340,7 +349,7 @@ def test_batched_empty_and_tiny_clips(fcfs, prec):
     allr = np.concatenate([small[:1], rects, small[1:]]).astype(np.int32)
     n = len(rects)
     cp = np.array([0, 1, 1, 1 + n, 1 + n, 3 + n], np.int64)          # clips: tiny, empty, long rows, empty, two rects
-    g = fcfs.vertices_from_rects(_dev(allr, torch.int32), T, None, _dev(cp, torch.int64))
+    g = _extract_checked(fcfs, allr, T, None, cp)
     M = N = 9
     F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, -1.0, "dense",
                             prec).cpu().numpy()
@@ -476,7 +485,7 @@ def test_row_buckets_bit_exact(fcfs, cap):
     allr = np.concatenate([small[:1], rects, small[1:]]).astype(np.int32)
     n = len(rects)
     cp = np.array([0, 1, 1, 1 + n, 1 + n, 3 + n], np.int64)
-    g = fcfs.vertices_from_rects(_dev(allr, torch.int32), T, None, _dev(cp, torch.int64))
+    g = _extract_checked(fcfs, allr, T, None, cp)
     for y, cptr in [(g["y"], g["corner_ptr"]),
                     (g["y"][torch.from_numpy(np.random.default_rng(2).permutation(g["K"])).cuda()].contiguous(), None)]:
         r = fcfs.row_buckets(y, cptr, cap)
@@ -804,12 +813,12 @@ def test_many_tiny_clips(fcfs, prec):
     R = int(cp[-1])
     rects = inputs.random_rects(rng, R, T, 1, 60)
     g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    e = oracle.extract(rects, T, None, cp)
+    _assert_extract_equal(g, e)
     r2 = 30.5
     F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, 5, 5, r2, "pupil",
                             prec).cpu().numpy()
     ms, ns = oracle.window(5, 5, r2)
-    e = oracle.extract(rects, T, None, cp)
-    assert np.array_equal(g["corner_ptr"].cpu().numpy(), e["corner_ptr"])
     for b in [0, 1, 65534, 65535, 65536, B - 1] + rng.integers(0, B, 20).tolist():
         a, c = e["corner_ptr"][b], e["corner_ptr"][b + 1]
         if a == c:
@@ -883,6 +892,7 @@ def test_vertices_with_edges(fcfs, cfg):
     vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=wl.group_ptr is not None).enable_edges()
     K = vp.run(rects, gp, cp)
     g = fcfs.vertices_from_rects(rects, wl.T, gp, cp)
+    _assert_extract_equal(g, oracle.extract(wl.rects, wl.T, wl.group_ptr, wl.clip_ptr))
     assert K == g["K"]
     for a, b in (("x", vp.x), ("y", vp.y), ("w", vp.w)):
         assert torch.equal(b[:K], g[a])
@@ -972,7 +982,7 @@ def test_haar_random_sweep(fcfs, seed):
         cps.append(cps[-1] + len(r))
     rects = np.concatenate(rects).astype(np.int32)
     cp = np.array(cps, np.int64)
-    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    g = _extract_checked(fcfs, rects, T, None, cp)
     H = fcfs.haar(g["x"], g["y"], g["w"], g["area"], T, g["corner_ptr"]).cpu().numpy()
     cpn = g["corner_ptr"].cpu().numpy()
     x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))

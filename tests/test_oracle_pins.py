@@ -669,3 +669,75 @@ def test_H4_single_rect_hand_values():
     H = oracle.haar(e["x"], e["y"], e["w"], 8)
     assert H[0, 0] == 2.5 and H[0, 1] == 1.25
     assert H[1, 0] == (6 - 9 + 2 - 3) / 8 and H[1, 1] == (6 - 9 - 2 + 3) / 8
+
+
+# ---------------------------------------------------------------- B1-B4: the L1 bound B[m,n] = sum_k |term_k|
+# B is the tolerance scale of every GPU parity assertion (1e-12 B / 1e-5 B), so it is pinned to values
+# derived by hand from the Prop. 3 terms (P:829-858; reading A12), not to the oracle's own formula.
+# Each term of Eq. Fkl is w_k E_x E_y / (-4 pi^2 m n) with |E| = 1, each term of Eq. Fk0 is
+# i w_k y_k E_x / (2 pi m T), each of Eq. F0l i w_k x_k E_y / (2 pi n T); F[0,0] is compared exactly.
+
+def test_B1_single_rect_hand_values():
+    """[3,10) x [5,20), T = 32: corners (3,5,+1) (10,5,-1) (3,20,-1) (10,20,+1) written out by hand.
+    Interior B = 4 / (4 pi^2 |m n|); n = 0: sum |w y| = 5+5+20+20 = 50 -> 50 / (2 pi |m| T);
+    m = 0: sum |w x| = 3+10+3+10 = 26 -> 26 / (2 pi |n| T); B[0,0] = 0."""
+    T = 32
+    x = np.array([3, 10, 3, 10], np.int32)
+    y = np.array([5, 5, 20, 20], np.int32)
+    w = np.array([1, -1, -1, 1], np.int32)
+    ms = np.array([1, -1, 3, 7, -5, 2, -9, 0, 0, 0, 4, -31], np.int32)
+    ns = np.array([1, 2, -3, 5, -6, 0, 0, 4, -11, 0, 33, 1], np.int32)
+    _, B = oracle.coeffs(x, y, w, 7 * 15, T, ms, ns)
+    pi = math.pi
+    for i, (m, n) in enumerate(zip(ms.tolist(), ns.tolist())):
+        if m == 0 and n == 0:
+            want = 0.0
+        elif n == 0:
+            want = 50.0 / (2 * pi * abs(m) * T)
+        elif m == 0:
+            want = 26.0 / (2 * pi * abs(n) * T)
+        else:
+            want = 4.0 / (4 * pi * pi * abs(m * n))
+        assert B[i] == pytest.approx(want, rel=1e-14, abs=0.0), (m, n, B[i], want)
+
+
+def test_B2_weights_beyond_one_hand_values():
+    """A hand corner list with |w| = 2 and 3 (pinch points / summed groups, reading A6), T = 16:
+    (1,1,+2) (4,1,-1) (2,3,-3) (7,7,+2).  sum |w| = 8; sum |w y| = 2+1+9+14 = 26; sum |w x| = 2+4+6+14 = 26."""
+    T = 16
+    x = np.array([1, 4, 2, 7], np.int32)
+    y = np.array([1, 1, 3, 7], np.int32)
+    w = np.array([2, -1, -3, 2], np.int32)
+    ms = np.array([1, 2, -3, 5, 0, 6], np.int32)
+    ns = np.array([1, -4, 0, 0, 3, -7], np.int32)
+    _, B = oracle.coeffs(x, y, w, 0, T, ms, ns)
+    pi = math.pi
+    want = [8 / (4 * pi * pi * 1), 8 / (4 * pi * pi * 8), 26 / (2 * pi * 3 * T), 26 / (2 * pi * 5 * T),
+            26 / (2 * pi * 3 * T), 8 / (4 * pi * pi * 42)]
+    assert np.allclose(B, want, rtol=1e-14, atol=0.0)
+
+
+@pytest.mark.parametrize("corner", [(0, 0, 1), (5, 9, -1), (13, 2, 3), (31, 31, -2)])
+def test_B3_single_corner_bound_is_attained(corner):
+    """One term: |F[m,n]| equals B[m,n] exactly (|E| = 1), so a B scaled by any constant != 1 fails.
+    Axis entries need a non-zero coordinate weight (x, y > 0) to be non-trivial."""
+    T = 32
+    x = np.array([corner[0]], np.int32)
+    y = np.array([corner[1]], np.int32)
+    w = np.array([corner[2]], np.int32)
+    ms, ns = oracle.window(9, 7)
+    F, B = oracle.coeffs(x, y, w, 0, T, ms, ns)
+    nz = ~((ms == 0) & (ns == 0))
+    assert np.allclose(np.abs(F[nz]), B[nz], rtol=1e-14, atol=1e-300)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_B4_triangle_inequality(cfg):
+    """|F[m,n]| <= B[m,n] at every window entry (triangle inequality over the terms), and B > 0 off DC
+    for a clip whose corner weights do not all vanish."""
+    wl = inputs.c1(seed=2) if cfg == "c1" else inputs.c2(seed=5, n_poly=80)
+    e = oracle.extract(wl.rects, wl.T, wl.group_ptr)
+    ms, ns, F, B = _window_coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, 24, 20)
+    nz = ~((ms == 0) & (ns == 0))
+    assert np.all(np.abs(F[nz]) <= B[nz] * (1 + 1e-12))
+    assert np.all(B[nz] > 0)
