@@ -49,6 +49,10 @@ def parse():
                     help="single-clip configs (c1, c2, c4, c5) on N > 1 GPUs: frequency rows + all_gather, "
                          "or vertex blocks + reduce_scatter")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--route", default=None, choices=["auto", "gemm", "fft"],
+                    help="single-clip configs: fcfs_options.route (default: the library's cost model)")
+    ap.add_argument("--form", default=None, choices=["auto", "edge", "corner"],
+                    help="batched split precisions: fcfs_options.form (default: the library's choice)")
     ap.add_argument("--input", default="rects", choices=["rects", "polygons"],
                     help="a1 input: rects (fcfs_vertices_from_rects) or the same rects as 4-vertex polygon "
                          "lists (fcfs_vertices_from_polygons; workloads with one group per rect)")
@@ -431,7 +435,7 @@ def main():
     cptr_h = vp.corner_ptr.cpu().numpy()
     kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
     if wl.B > 1:
-        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
+        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, form=args.form)
 
         def coeffs():
             return plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area)
@@ -453,7 +457,7 @@ def main():
             return fdist.coeffs_vertex_sharded(vp.x[:K], vp.y[:K], vp.w[:K], wl.T, wl.M, wl.N, prec)
         out_bytes = plan.out.numel() * plan.out.element_size()
     else:
-        plan = fcfs.CoeffsPlan(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
+        plan = fcfs.CoeffsPlan(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, route=args.route)
         area_h = int(vp.area[0].item())
 
         def coeffs():
@@ -507,7 +511,7 @@ def main():
     c_ms, c_n = stages["contract"]
     c_ms_launch = c_ms / max(c_n, 1)
     fft_route = (wl.B == 1 and world == 1 and
-                 fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec) == 1)
+                 fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, route=args.route) == 1)
     if fft_route:
         # lattice-FFT route (NEXT-2, FP64 or FP32 CUDA cores): algorithmic work of the contract stage =
         # G rows (one complex rotation + real-weighted complex MAC per corner and row: 10 flop) +
@@ -546,7 +550,7 @@ def main():
             rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
             Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
             k_inner = "row buckets"
-        elif prec == "tf32x3" and os.environ.get("FCFS_EDGES", "1") != "0":
+        elif getattr(plan, "form", 0) == fcfs.FORM_EDGE:
             Kc = edge_counts(vp, K, cptr_h)
             k_inner = "edges (K/2-term form)"
         else:
@@ -606,7 +610,8 @@ def main():
                 vps = fcfs.VerticesPlan(r1 - r0, wl.T, r1 - r0, bs, 1, grouped=False, device=dev)
                 Ki = vps.run(rects[r0:r1].contiguous(), None, cps)
                 kmi = int(np.diff(vps.corner_ptr.cpu().numpy()).max())
-                pls = fcfs.BatchedPlan(bs, Ki, kmi, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev)
+                pls = fcfs.BatchedPlan(bs, Ki, kmi, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev,
+                                       form=args.form)
                 subs.append({"r0": r0, "r1": r1, "cp": cps, "vp": vps, "plan": pls,
                              "dev": torch.empty((r1 - r0, 4), dtype=torch.int32, device=dev),
                              "out_h": torch.empty(pls.out.numel(), dtype=pls.out.dtype).pin_memory()})

@@ -85,6 +85,23 @@ typedef struct {
     int32_t layout;     /* FCFS_LAYOUT_DENSE or FCFS_LAYOUT_PUPIL */
 } fcfs_window;
 
+/* Explicit kernel-route options (the library reads no environment variables: what it computes is fixed
+ * by its arguments).  Pass NULL for the defaults (every field AUTO).  Every route and form meets the same
+ * accuracy contract of `prec`; the options exist for A/B measurement and for the tests that force each
+ * route on the same inputs. */
+#define FCFS_ROUTE_AUTO 0   /* fcfs_coeffs: the cost model picks (fcfs_coeffs_route)                      */
+#define FCFS_ROUTE_GEMM 1   /* fcfs_coeffs: the row-bucket GEMM on the tensor cores                      */
+#define FCFS_ROUTE_FFT 2    /* fcfs_coeffs: the lattice-FFT route wherever it applies (power-of-two T >= 64,
+                               2N+1 <= min(T, 4096), y-sorted corners); elsewhere the row-bucket GEMM   */
+#define FCFS_FORM_AUTO 0    /* fcfs_coeffs_batched (split precisions): the library's choice               */
+#define FCFS_FORM_EDGE 1    /* FCFS_TF32X3: contract over edges (fcfs_edges; the K/2-term form of Eq. Fkl) */
+#define FCFS_FORM_CORNER 2  /* contract over corners (the K-term form of Eq. Fkl)                         */
+typedef struct {
+    int32_t route;      /* FCFS_ROUTE_*  */
+    int32_t form;       /* FCFS_FORM_*   */
+    int32_t reserved[6];/* must be 0     */
+} fcfs_options;
+
 /* Work partition of one clip (BASELINE.json north_star (6); linearity Prop. 2). */
 #define FCFS_SHARD_NONE 0
 #define FCFS_SHARD_ROWS 1          /* rows m in [m_lo, m_hi] (signed, inside [-M, M]) of the DENSE
@@ -213,21 +230,22 @@ fcfs_status fcfs_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t 
  * bucket count).
  * ------------------------------------------------------------------------------------------ */
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
-                                   fcfs_precision prec, const fcfs_shard *shard);
+                                   fcfs_precision prec, const fcfs_shard *shard,
+                                   const fcfs_options *opt);
 /* Which single-clip route fcfs_coeffs takes for these sizes (planning / reporting; no device work):
  * 1 = the lattice-FFT route (power-of-two T >= 64, 2N+1 <= min(T, 4096), chosen by a cost model over
  * the row-bucket GEMM; taken only if the corner list is y-sorted, as fcfs_vertices_from_* produce it
  * — fcfs_coeffs checks on the device and otherwise falls back).  FCFS_FP64 runs it in FP64;
  * FCFS_TF32X3 / FCFS_F16X3 run it in FP32 on the CUDA cores (FP64 outer and axis sums) under their
  * 1e-5 B contract and complex64 output.  0 = the row-bucket GEMM on the tensor cores (DMMA, or the
- * split tcgen05 kernels).  The environment variable FCFS_ROUTE=fft|gemm overrides the cost model
- * (testing).  Both routes meet the same tolerance. */
+ * split tcgen05 kernels).  opt->route (FCFS_ROUTE_GEMM / FCFS_ROUTE_FFT) overrides the cost model;
+ * opt NULL = FCFS_ROUTE_AUTO.  Both routes meet the same tolerance. */
 int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
-                          const fcfs_shard *shard);
+                          const fcfs_shard *shard, const fcfs_options *opt);
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K,
                         int64_t area, int32_t T, const fcfs_window *win, fcfs_precision prec,
-                        const fcfs_shard *shard, void *F, void *ws, size_t ws_bytes,
-                        void *stream);
+                        const fcfs_shard *shard, const fcfs_options *opt, void *F, void *ws,
+                        size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * a3-a5 batched — B independent clips (the paper's tiles) in one launch sequence.
@@ -237,23 +255,30 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
  * F out: B consecutive output blocks of fcfs_window_size(win) entries each.
  * ------------------------------------------------------------------------------------------ */
 size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T,
-                                    const fcfs_window *win, fcfs_precision prec);
+                                    const fcfs_window *win, fcfs_precision prec,
+                                    const fcfs_options *opt);
+/* Which contraction form fcfs_coeffs_batched runs for these sizes (FCFS_FORM_EDGE / FCFS_FORM_CORNER;
+ * 0 for FCFS_FP64, which contracts over row buckets): planning / reporting, no device work. */
+int32_t fcfs_coeffs_batched_form(int64_t B, int64_t K_total, int64_t K_max, int32_t T,
+                                 const fcfs_window *win, fcfs_precision prec, const fcfs_options *opt);
 fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total,
                                 int64_t K_max, const int32_t *x, const int32_t *y,
                                 const int32_t *w, const int64_t *area, int32_t T,
-                                const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
-                                size_t ws_bytes, void *stream);
+                                const fcfs_window *win, fcfs_precision prec,
+                                const fcfs_options *opt, void *F, void *ws, size_t ws_bytes,
+                                void *stream);
 
 /* The same with the edge pairing of the corner lists given (the output of fcfs_edges or of
  * fcfs_vertices_from_rects_edges for these corners; arrays as fcfs_edges documents): FCFS_TF32X3
- * contracts over them instead of pairing again; other precisions ignore them.  Same workspace. */
+ * contracts over them instead of pairing again (the edge form, whatever opt->form says); other precisions
+ * ignore them.  Same workspace. */
 fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int64_t K_total,
                                       int64_t K_max, const int32_t *x, const int32_t *y,
                                       const int32_t *w, const int64_t *area, const int32_t *xa,
                                       const int32_t *xb, const int32_t *ye, const int32_t *c,
                                       const int32_t *ecnt, int32_t T, const fcfs_window *win,
-                                      fcfs_precision prec, void *F, void *ws, size_t ws_bytes,
-                                      void *stream);
+                                      fcfs_precision prec, const fcfs_options *opt, void *F, void *ws,
+                                      size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * Row buckets of a corner list — the row structure of Step 4: corners on one row

@@ -79,7 +79,7 @@ struct GemmPlan {
     int32_t tiles_x, tiles_y, splits;
     int64_t B;                // clips
     int64_t items;            // B * tiles_x * tiles_y * splits
-    int32_t dbg;              // experiments only (env FCFS_DEBUG): 1 = producers skip generation, 2 = no MMA
+    int32_t dbg;              // ablation build only (-DFCFS_ABLATE, env FCFS_DEBUG); 0 in the shipped library
     int32_t phys;             // P_ws row order inside a 64-row tile: 0 = (c0,s0,c1,s1,...) [FP64 kernel],
                               // 1 = (c0..c31, s0..s31) [tcgen05 kernel]
 };
@@ -209,7 +209,8 @@ struct FftPlan {
     int64_t rc;        // rows per chunk of the G workspace
     int32_t sp;        // sub-row ranges per row in k_fr_fft2 (partial X sums, added in fixed order)
 };
-bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p);
+bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p,
+                    int32_t route = FCFS_ROUTE_AUTO);
 size_t fft_route_ws_bytes(const FftPlan &p);
 fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const FftPlan &p, void *ws, size_t ws_bytes,
                               bool &sorted, cudaStream_t s);

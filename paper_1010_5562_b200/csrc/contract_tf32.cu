@@ -14,7 +14,7 @@
 //
 // a2 is fused: producer warps reduce the phase (f * v) mod T exactly in integers (lattice
 // vertices), look up e^{i 2 pi r/T} in an SMEM table and write the split operand
-// tiles straight into the canonical no-swizzle K-major UMMA layout; the twiddle matrices
+// tiles straight into the canonical SWIZZLE_128B K-major UMMA layout; the twiddle matrices
 // never exist in HBM ("no full-length arrays").
 //
 // Warp roles (416 threads, 1 CTA per SM, persistent over work items):
@@ -30,6 +30,14 @@
 
 namespace fcfs {
 namespace tc {
+
+// Ablation switches (experiments only): compiled in only with -DFCFS_ABLATE (tools/ablate_build.sh builds
+// that variant as a separate libfcfs_ablate.so); in the shipped library every ABL(bit) is the constant 0.
+#ifdef FCFS_ABLATE
+#define ABL(bit) (plan.dbg & (bit))
+#else
+#define ABL(bit) 0
+#endif
 
 constexpr int kBK = 32;                         // corners per stage (K of 4 MMAs)
 constexpr int kStages = 5;                      // ring depth (> kGroups: no self-wait)
@@ -635,7 +643,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int tr = plan.dbg & 256;
+    const int tr = ABL(256);
 
     // twiddle table (all threads), barriers (thread 0), TMEM (MMA warp)
     for (int i = tid; i < tab_entries; i += kThreads) {
@@ -757,7 +765,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                     // stage = 4 stages ahead, about one HBM latency): one line per lane, per array
                     // edge form: no L2 prefetch — the edges were just written by k_edges and the
                     // prefetch instructions cost more issue slots than they saved (0.997 vs 1.027 ms)
-                    if (!kEdge && !kLoadA && !(plan.dbg & 128)) {
+                    if (!kEdge && !kLoadA && !(ABL(128))) {
                         constexpr int kLines = kBKp * 4 / 128;          // 128-byte lines per array per stage
                         const int64_t kp = ks + 16 * kBKp + (int64_t)(l % kLines) * 32;
                         if (l < (yside ? 1 : 2) * kLines && kp < it.k1) {
@@ -775,9 +783,9 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         if constexpr (kEdge) { xa[q] = an[q]; xb[q] = bn[q]; ci[q] = wn[q]; }
                     }
                     kr0 += kGroups * kBKp;
-                    if (!(plan.dbg & 16)) fetch(kr0);
+                    if (!(ABL(16))) fetch(kr0);
                     if (l == 0) trace(tr, 10 + gq * 2 + sideB, sc);
-                    mbar_wait(EMPTY(my_slot), my_ph ^ 1, plan.dbg & 32);
+                    mbar_wait(EMPTY(my_slot), my_ph ^ 1, ABL(32));
                     if (l == 0) trace(tr, 20 + gq * 2 + sideB, sc);
                     uint8_t *op = smem + L.stage0 + my_slot * kStageBytes + (yside ? kOpBytes : 0);
                     if (kLoadA) {
@@ -800,7 +808,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         __syncwarp();
                         continue;
                     }
-                    if (!(plan.dbg & 1)) {
+                    if (!(ABL(1))) {
                         constexpr int kSl = (kLoadA || kEdge) ? 4 : 8;
                         if constexpr (kEdge) {
                             uint8_t *opx = smem + L.stage0 + my_slot * kStageBytes;
@@ -813,7 +821,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                             produce<kFast, kSl>(op, quad, j0, p0, sp, (const int32_t *)v, (const float *)wt, g, tab);
                         }
                     }
-                    if (!(plan.dbg & 8)) fence_proxy_async();
+                    if (!(ABL(8))) fence_proxy_async();
                     __syncwarp();
                     if (l == 0) { trace(tr, 30 + gq * 2 + sideB, sc); mbar_arrive(FULL(my_slot)); }
                 }
@@ -830,7 +838,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
             uint32_t msc = 0;
             const uint32_t smem_base = su32(smem + L.stage0);
             const uint64_t adesc0 = umma_desc(smem_base), bdesc0 = umma_desc(smem_base + kOpBytes);
-            const bool no_mma = (plan.dbg & 2) != 0;
+            const bool no_mma = (ABL(2)) != 0;
             for (int64_t item = blockIdx.x; item < plan.items; item += gridDim.x) {
                 int64_t chunk0 = 0;
             const ItemInfo it = kLoadA ? item_info_chunk<kBKp>(src, plan, ch, item, chunk0) : item_info(src, plan, item);
@@ -851,8 +859,8 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         const int two = (kPer == 2 && st + 1 < nst) ? 1 : 0;
                         const int s1 = (stage + 1 == kS) ? 0 : stage + 1;
                         const uint32_t p1 = (stage + 1 == kS) ? phase_bit ^ 1 : phase_bit;
-                        mbar_wait(FULL(stage), phase_bit, plan.dbg & 64);
-                        if (two) mbar_wait(FULL(s1), p1, plan.dbg & 64);
+                        mbar_wait(FULL(stage), phase_bit, ABL(64));
+                        if (two) mbar_wait(FULL(s1), p1, ABL(64));
                         if (lane == 0) trace(tr, 50, msc);
                         tc_fence_after();
                         const uint64_t off0 = (uint64_t)((stage * kStageBytes) >> 4);
@@ -902,7 +910,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 const uint32_t b = chunk_ctr & 1;
                 mbar_wait_sleep(TFULL(b), (chunk_ctr >> 1) & 1);
                 tc_fence_after();
-                if (plan.dbg & 4) {
+                if (ABL(4)) {
                     tc_fence_before();
                     mbar_arrive(TEMPTY(b));
                     continue;
@@ -950,7 +958,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 for (int i = 0; i < 32; ++i)
                     if (cb + i == ay_l) acc[i] *= up;
             }
-            if (plan.dbg & 4) continue;
+            if (ABL(4)) continue;
             if (!fuse) {
                 double *out = P_ws + item * (int64_t)(kTile * kTile) + r * kTile + (hi_row ? 0 : 32);
                 if (kLoadA) {   // chunk partials add up in P_ws (zeroed before the first chunk)

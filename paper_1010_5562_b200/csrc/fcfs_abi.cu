@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -98,19 +99,23 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
                              const EpiArgs *ea, void *F, bool f16, cudaStream_t s);
 bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 
+// sm_100 check, cached per device (atomics: several host threads call this concurrently)
 static fcfs_status device_ok() {
-    static int cached = -1;
-    if (cached < 0) {
-        int dev = 0, major = 0, minor = 0;
-        cudaError_t e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    static std::atomic<int> cached[64];   // 0 = unknown, 1 = sm_100, 2 = other
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "device query");
+    int c = (dev >= 0 && dev < 64) ? cached[dev].load(std::memory_order_relaxed) : 0;
+    int major = 0, minor = 0;
+    if (c == 0) {
+        e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
         if (e != cudaSuccess) return cuda_status(e, "device query");
-        cached = (major == 10 && minor == 0) ? 1 : 0;
-        if (!cached) set_error("device is sm_%d%d; libfcfs.so is built for sm_100a only", major, minor);
+        c = (major == 10 && minor == 0) ? 1 : 2;
+        if (dev >= 0 && dev < 64) cached[dev].store(c, std::memory_order_relaxed);
     }
-    if (!cached) {
-        set_error("device is not sm_100; libfcfs.so is built for sm_100a only");
+    if (c != 1) {
+        set_error("device %d is not sm_100; libfcfs.so is built for sm_100a only", dev);
         return FCFS_E_UNSUPPORTED;
     }
     return FCFS_OK;
@@ -182,8 +187,12 @@ static GemmPlan make_plan(int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int6
     p.B = B;
     p.items = B * tiles * splits;
     p.phys = 0;
-    const char *dbg = getenv("FCFS_DEBUG");
+#ifdef FCFS_ABLATE
+    const char *dbg = getenv("FCFS_DEBUG");   // ablation build only (libfcfs_ablate.so), never shipped
     p.dbg = dbg ? atoi(dbg) : 0;
+#else
+    p.dbg = 0;
+#endif
     return p;
 }
 
@@ -198,10 +207,25 @@ struct CoeffWs {
     EdgeWs edges;   // batched split-TF32: the edge form of the corner lists (edges.cu)
 };
 
-// the batched split-TF32 contraction runs on edges unless FCFS_EDGES=0 (corner form; A/B tests)
-static bool edges_enabled() {
-    const char *e = getenv("FCFS_EDGES");
-    return !(e && !strcmp(e, "0"));
+static const fcfs_options kDefaultOptions = {FCFS_ROUTE_AUTO, FCFS_FORM_AUTO, {0, 0, 0, 0, 0, 0}};
+
+static fcfs_status check_options(const fcfs_options *&opt) {
+    if (!opt) { opt = &kDefaultOptions; return FCFS_OK; }
+    if (opt->route < FCFS_ROUTE_AUTO || opt->route > FCFS_ROUTE_FFT || opt->form < FCFS_FORM_AUTO ||
+        opt->form > FCFS_FORM_CORNER) {
+        set_error("bad options: route %d form %d", opt->route, opt->form);
+        return FCFS_E_INVALID;
+    }
+    for (int i = 0; i < 6; ++i)
+        if (opt->reserved[i]) { set_error("fcfs_options.reserved[%d] != 0", i); return FCFS_E_INVALID; }
+    return FCFS_OK;
+}
+
+// the batched split-TF32 contraction form: edges (the K/2-term form) unless the caller asks for corners
+static int32_t batched_form(fcfs_precision prec, const fcfs_options *opt) {
+    if (prec == FCFS_FP64) return 0;
+    if (prec == FCFS_F16X3) return FCFS_FORM_CORNER;   // split-FP16 keeps the corner form
+    return opt->form == FCFS_FORM_CORNER ? FCFS_FORM_CORNER : FCFS_FORM_EDGE;
 }
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
@@ -480,8 +504,8 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
 }
 
 size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
-                                   const fcfs_shard *shard) {
-    if (check_window(win) != FCFS_OK) return 0;
+                                   const fcfs_shard *shard, const fcfs_options *opt) {
+    if (check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK) return 0;
     int32_t m_lo, m_hi;
     if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
     int64_t k = K;
@@ -489,7 +513,7 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
     GemmPlan p = make_plan(win->M, win->N, m_lo, m_hi, 1, k, false);
     FftPlan fp;
     const bool fft = valid_T(T) && (prec == FCFS_FP64 || prec == FCFS_TF32X3 || prec == FCFS_F16X3) &&
-                     fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp);
+                     fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp, opt->route);
     Carver cv(nullptr, 0);
     CoeffWs w;
     carve_coeff(cv, p, w, !fusable(p, prec, win->M, m_lo, m_hi, true), k, 1, prec, true, fft ? &fp : nullptr);
@@ -497,22 +521,23 @@ size_t fcfs_coeffs_workspace_bytes(int64_t K, int32_t T, const fcfs_window *win,
 }
 
 int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_precision prec,
-                          const fcfs_shard *shard) {
-    if (!valid_T(T) || check_window(win) != FCFS_OK) return 0;
+                          const fcfs_shard *shard, const fcfs_options *opt) {
+    if (!valid_T(T) || check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK) return 0;
     if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) return 0;
     int32_t m_lo, m_hi;
     if (resolve_rows(win, shard, m_lo, m_hi) != FCFS_OK) return 0;
     int64_t k = K;
     if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
     FftPlan fp;
-    return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp) ? 1 : 0;
+    return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp, opt->route) ? 1 : 0;
 }
 
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
-                        const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard, void *F, void *ws,
-                        size_t ws_bytes, void *stream) {
+                        const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard,
+                        const fcfs_options *opt, void *F, void *ws, size_t ws_bytes, void *stream) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     fcfs_status st = check_window(win);
+    if (st == FCFS_OK) st = check_options(opt);
     if (st != FCFS_OK) return st;
     if (K < 0 || (K > 0 && (!x || !y || !w)) || !F) { set_error("fcfs_coeffs: null pointer or K < 0"); return FCFS_E_INVALID; }
     if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) {
@@ -538,7 +563,8 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     GemmPlan plan = make_plan(win->M, win->N, m_lo, m_hi, 1, src.k_hi - src.k_lo, false);
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     FftPlan fp;
-    const bool fft = fft_route_plan(T, win->M, win->N, m_lo, m_hi, src.k_hi - src.k_lo, prec != FCFS_FP64, fp);
+    const bool fft = fft_route_plan(T, win->M, win->N, m_lo, m_hi, src.k_hi - src.k_lo, prec != FCFS_FP64, fp,
+                                    opt->route);
     Carver cv(ws, ws_bytes);
     CoeffWs W;
     carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, m_lo, m_hi, true), src.k_hi - src.k_lo, 1, prec, true,
@@ -592,9 +618,9 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
 }
 
 size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,
-                                    fcfs_precision prec) {
+                                    fcfs_precision prec, const fcfs_options *opt) {
     (void)T;
-    if (check_window(win) != FCFS_OK || B < 1) return 0;
+    if (check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK || B < 1) return 0;
     GemmPlan p = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
     Carver cv(nullptr, 0);
     CoeffWs w;
@@ -602,14 +628,23 @@ size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, i
     return cv.used();
 }
 
+int32_t fcfs_coeffs_batched_form(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,
+                                 fcfs_precision prec, const fcfs_options *opt) {
+    (void)B; (void)K_total; (void)K_max; (void)T;
+    if (check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK) return 0;
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) return 0;
+    return batched_form(prec, opt);
+}
+
 }  // extern "C"
 
 static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
                                 const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
-                                int32_t T, const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
-                                size_t ws_bytes, void *stream, const EdgeWs *given) {
+                                int32_t T, const fcfs_window *win, fcfs_precision prec, const fcfs_options *opt,
+                                void *F, void *ws, size_t ws_bytes, void *stream, const EdgeWs *given) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     fcfs_status st = check_window(win);
+    if (st == FCFS_OK) st = check_options(opt);
     if (st != FCFS_OK) return st;
     if (B < 1 || !corner_ptr || !area || !F || K_total < 0 || K_max < 0 || (K_total > 0 && (!x || !y || !w))) {
         set_error("fcfs_coeffs_batched: invalid sizes or null pointers");
@@ -638,7 +673,7 @@ static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_
     ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = fcfs_window_size(win);
     bool fused = false;
-    if (prec == FCFS_TF32X3 && K_total > 0 && (given || edges_enabled())) {   // the K/2-term form (edges.cu)
+    if (prec == FCFS_TF32X3 && K_total > 0 && (given || batched_form(prec, opt) == FCFS_FORM_EDGE)) {   // K/2-term form
         const EdgeWs *e = given ? given : &W.edges;
         if (!given) {
             StageScope scope(kStagePair, s);
@@ -675,9 +710,9 @@ extern "C" {
 
 fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total, int64_t K_max,
                                 const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
-                                int32_t T, const fcfs_window *win, fcfs_precision prec, void *F, void *ws,
-                                size_t ws_bytes, void *stream) {
-    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, F, ws, ws_bytes, stream,
+                                int32_t T, const fcfs_window *win, fcfs_precision prec, const fcfs_options *opt,
+                                void *F, void *ws, size_t ws_bytes, void *stream) {
+    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, opt, F, ws, ws_bytes, stream,
                         nullptr);
 }
 
@@ -685,7 +720,7 @@ fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int6
                                       const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *area,
                                       const int32_t *xa, const int32_t *xb, const int32_t *ye, const int32_t *c,
                                       const int32_t *ecnt, int32_t T, const fcfs_window *win, fcfs_precision prec,
-                                      void *F, void *ws, size_t ws_bytes, void *stream) {
+                                      const fcfs_options *opt, void *F, void *ws, size_t ws_bytes, void *stream) {
     if (K_total > 0 && (!xa || !xb || !ye || !c || !ecnt)) {
         set_error("fcfs_coeffs_batched_edges: null edge input");
         return FCFS_E_INVALID;
@@ -693,7 +728,7 @@ fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int6
     EdgeWs e;
     e.xa = const_cast<int32_t *>(xa); e.xb = const_cast<int32_t *>(xb); e.y = const_cast<int32_t *>(ye);
     e.c = const_cast<int32_t *>(c); e.cnt = const_cast<int32_t *>(ecnt);
-    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, F, ws, ws_bytes, stream, &e);
+    return batched_impl(corner_ptr, B, K_total, K_max, x, y, w, area, T, win, prec, opt, F, ws, ws_bytes, stream, &e);
 }
 
 size_t fcfs_row_buckets_workspace_bytes(int64_t K, int64_t B) {

@@ -577,9 +577,10 @@ static fr::Geo make_geo(int32_t T, int32_t T2) {
     return g;
 }
 
-// geometry + cost model; FCFS_ROUTE=fft / gemm (environment) forces the choice where possible.
-// f32: the FP32 variant for the split precisions (same 1e-5 B contract as their tensor GEMM)
-bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p) {
+// geometry + cost model; route (fcfs_options.route) = FCFS_ROUTE_FFT / FCFS_ROUTE_GEMM forces the choice
+// where possible.  f32: the FP32 variant for the split precisions (same 1e-5 B contract as their tensor GEMM)
+bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p,
+                    int32_t route) {
     p = FftPlan{};
     if (T < 64 || (T & (T - 1)) != 0 || K <= 0 || K >= (int64_t(1) << 31)) return false;
     int64_t T2 = 64;
@@ -609,9 +610,8 @@ bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi,
         if (sp < 1) sp = 1;
         p.sp = (int32_t)sp;
     }
-    const char *env = getenv("FCFS_ROUTE");
-    if (env && !strcmp(env, "gemm")) return false;
-    if (env && !strcmp(env, "fft")) return true;
+    if (route == FCFS_ROUTE_GEMM) return false;
+    if (route == FCFS_ROUTE_FFT) return true;
     const double lg = log2((double)T2);
     const double fft = (double)p.nr * ((double)T * (5.0 * lg + 16.0) + (double)(T / T2) * (2.0 * N + 1) * 8.0) +
                        9.0 * (double)K * (double)p.nm;

@@ -28,6 +28,12 @@ FCFS_OK, E_INVALID, E_RANGE, E_CAPACITY, E_WORKSPACE, E_UNSUPPORTED, E_CUDA = ra
 FP64, TF32X3, F16X3 = 0, 1, 2
 LAYOUT_DENSE, LAYOUT_PUPIL = 0, 1
 SHARD_NONE, SHARD_ROWS, SHARD_VERTEX_BLOCK = 0, 1, 2
+ROUTE_AUTO, ROUTE_GEMM, ROUTE_FFT = 0, 1, 2
+FORM_AUTO, FORM_EDGE, FORM_CORNER = 0, 1, 2
+_ROUTE = {"auto": ROUTE_AUTO, "gemm": ROUTE_GEMM, "fft": ROUTE_FFT, None: ROUTE_AUTO,
+          ROUTE_AUTO: ROUTE_AUTO, ROUTE_GEMM: ROUTE_GEMM, ROUTE_FFT: ROUTE_FFT}
+_FORM = {"auto": FORM_AUTO, "edge": FORM_EDGE, "corner": FORM_CORNER, None: FORM_AUTO,
+         FORM_AUTO: FORM_AUTO, FORM_EDGE: FORM_EDGE, FORM_CORNER: FORM_CORNER}
 _PREC = {"fp64": FP64, "tf32x3": TF32X3, "f16x3": F16X3, FP64: FP64, TF32X3: TF32X3, F16X3: F16X3}
 _LAYOUT = {"dense": LAYOUT_DENSE, "pupil": LAYOUT_PUPIL, LAYOUT_DENSE: LAYOUT_DENSE, LAYOUT_PUPIL: LAYOUT_PUPIL}
 
@@ -42,8 +48,18 @@ class Shard(ctypes.Structure):
                 ("k_lo", ctypes.c_int64), ("k_hi", ctypes.c_int64)]
 
 
+class Options(ctypes.Structure):
+    _fields_ = [("route", ctypes.c_int32), ("form", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+
+
+def make_options(route=None, form=None):
+    """fcfs_options: route "auto" | "gemm" | "fft" (fcfs_coeffs), form "auto" | "edge" | "corner"
+    (fcfs_coeffs_batched, split precisions)."""
+    return Options(_ROUTE[route], _FORM[form])
+
+
 _P, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
-_WP, _SP = ctypes.POINTER(Window), ctypes.POINTER(Shard)
+_WP, _SP, _OP = ctypes.POINTER(Window), ctypes.POINTER(Shard), ctypes.POINTER(Options)
 
 _lib.fcfs_status_string.argtypes = [_i32]
 _lib.fcfs_status_string.restype = ctypes.c_char_p
@@ -70,7 +86,7 @@ _lib.fcfs_polygons_workspace_bytes.restype = _sz
 _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _i32, _P, _P, _P, _i64, _P, _P,
                                              ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_vertices_from_polygons.restype = _i32
-_lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP]
+_lib.fcfs_coeffs_workspace_bytes.argtypes = [_i64, _i32, _WP, _i32, _SP, _OP]
 _lib.fcfs_coeffs_workspace_bytes.restype = _sz
 _lib.fcfs_haar_workspace_bytes.argtypes = [_i64, _i32]
 _lib.fcfs_haar_workspace_bytes.restype = _sz
@@ -80,15 +96,17 @@ _lib.fcfs_chop_workspace_bytes.argtypes = [_i64, _i64, _i32, _i32]
 _lib.fcfs_chop_workspace_bytes.restype = _sz
 _lib.fcfs_chop_rects.argtypes = [_P, _i64, _i32, _i32, _i32, _P, _i64, _P, ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_chop_rects.restype = _i32
-_lib.fcfs_coeffs_route.argtypes = [_i64, _i32, _WP, _i32, _SP]
+_lib.fcfs_coeffs_route.argtypes = [_i64, _i32, _WP, _i32, _SP, _OP]
 _lib.fcfs_coeffs_route.restype = _i32
-_lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _P, _P, _sz, _P]
+_lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _OP, _P, _P, _sz, _P]
 _lib.fcfs_coeffs.restype = _i32
-_lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32]
+_lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32, _OP]
 _lib.fcfs_batched_workspace_bytes.restype = _sz
-_lib.fcfs_coeffs_batched.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _i32, _WP, _i32, _P, _P, _sz, _P]
+_lib.fcfs_coeffs_batched_form.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32, _OP]
+_lib.fcfs_coeffs_batched_form.restype = _i32
+_lib.fcfs_coeffs_batched.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _i32, _WP, _i32, _OP, _P, _P, _sz, _P]
 _lib.fcfs_coeffs_batched_edges.argtypes = [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _i32, _WP,
-                                           _i32, _P, _P, _sz, _P]
+                                           _i32, _OP, _P, _P, _sz, _P]
 _lib.fcfs_coeffs_batched_edges.restype = _i32
 _lib.fcfs_coeffs_batched.restype = _i32
 
@@ -111,7 +129,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
-            "fcfs_coeffs_batched_edges"]
+            "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -378,14 +396,17 @@ def _out_dtype(prec):
 
 
 class CoeffsPlan:
-    """Pre-allocated workspace + output for repeated ``fcfs_coeffs`` calls on one clip."""
+    """Pre-allocated workspace + output for repeated ``fcfs_coeffs`` calls on one clip.
+    route: "auto" (the cost model), "gemm" or "fft" (fcfs_options.route)."""
 
-    def __init__(self, K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, device="cuda"):
+    def __init__(self, K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, device="cuda", route=None):
         self.K, self.T, self.prec = int(K), int(T), _PREC[prec]
         self.win = make_window(M, N, r2, layout)
         self.shard = shard
+        self.opt = make_options(route=route)
         sp = ctypes.byref(shard) if shard is not None else None
-        nbytes = _lib.fcfs_coeffs_workspace_bytes(self.K, self.T, ctypes.byref(self.win), self.prec, sp)
+        nbytes = _lib.fcfs_coeffs_workspace_bytes(self.K, self.T, ctypes.byref(self.win), self.prec, sp,
+                                                  ctypes.byref(self.opt))
         if nbytes == 0:
             raise FcfsError(E_INVALID, "fcfs_coeffs_workspace_bytes")
         self.ws = _ws(nbytes, device)
@@ -399,37 +420,44 @@ class CoeffsPlan:
         out = self.out if out is None else out
         sp = ctypes.byref(self.shard) if self.shard is not None else None
         st = _lib.fcfs_coeffs(_ptr(x), _ptr(y), _ptr(w), self.K, int(area), self.T, ctypes.byref(self.win),
-                              self.prec, sp, _ptr(out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+                              self.prec, sp, ctypes.byref(self.opt), _ptr(out), _ptr(self.ws), self.ws.numel(),
+                              _stream(stream))
         _check(st, "fcfs_coeffs")
         return out
 
 
-def coeffs_route(K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None):
+def coeffs_route(K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, route=None):
     """1 if fcfs_coeffs takes the lattice-FFT route for these sizes (y-sorted corners), else 0."""
     win = make_window(M, N, r2, layout)
     sp = ctypes.byref(shard) if shard is not None else None
-    return int(_lib.fcfs_coeffs_route(int(K), int(T), ctypes.byref(win), _PREC[prec], sp))
+    opt = make_options(route=route)
+    return int(_lib.fcfs_coeffs_route(int(K), int(T), ctypes.byref(win), _PREC[prec], sp, ctypes.byref(opt)))
 
 
-def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, stream=None):
+def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, stream=None, route=None):
     """a2-a5 for one clip.  Returns complex128 (fp64) or complex64 (tf32x3) cuda tensor."""
-    plan = CoeffsPlan(x.shape[0], T, M, N, r2, layout, prec, shard, device=x.device)
+    plan = CoeffsPlan(x.shape[0], T, M, N, r2, layout, prec, shard, device=x.device, route=route)
     return plan.run(x, y, w, area, stream=stream)
 
 
 class BatchedPlan:
-    """Pre-allocated workspace + output for repeated ``fcfs_coeffs_batched`` calls."""
+    """Pre-allocated workspace + output for repeated ``fcfs_coeffs_batched`` calls.
+    form: "auto", "edge" or "corner" (fcfs_options.form; split precisions)."""
 
-    def __init__(self, B, K_total, K_max, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", device="cuda"):
+    def __init__(self, B, K_total, K_max, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", device="cuda",
+                 form=None):
         self.B, self.K_total, self.K_max, self.T, self.prec = int(B), int(K_total), int(K_max), int(T), _PREC[prec]
         self.win = make_window(M, N, r2, layout)
+        self.opt = make_options(form=form)
         nbytes = _lib.fcfs_batched_workspace_bytes(self.B, self.K_total, self.K_max, self.T,
-                                                   ctypes.byref(self.win), self.prec)
+                                                   ctypes.byref(self.win), self.prec, ctypes.byref(self.opt))
         if nbytes == 0:
             raise FcfsError(E_INVALID, "fcfs_batched_workspace_bytes")
         self.ws = _ws(nbytes, device)
         self.per_clip = window_size(M, N, r2, layout)
         self.out = torch.empty(self.B * self.per_clip, dtype=_out_dtype(prec), device=device)
+        self.form = int(_lib.fcfs_coeffs_batched_form(self.B, self.K_total, self.K_max, self.T,
+                                                      ctypes.byref(self.win), self.prec, ctypes.byref(self.opt)))
 
     def run(self, corner_ptr, x, y, w, area, stream=None, out=None, edges=None):
         """edges: the pairing of these corners (dict xa, xb, y, c, ecnt from ``edges`` or
@@ -437,23 +465,25 @@ class BatchedPlan:
         out = self.out if out is None else out
         if edges is None:
             st = _lib.fcfs_coeffs_batched(_ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y),
-                                          _ptr(w), _ptr(area), self.T, ctypes.byref(self.win), self.prec, _ptr(out),
-                                          _ptr(self.ws), self.ws.numel(), _stream(stream))
+                                          _ptr(w), _ptr(area), self.T, ctypes.byref(self.win), self.prec,
+                                          ctypes.byref(self.opt), _ptr(out), _ptr(self.ws), self.ws.numel(),
+                                          _stream(stream))
         else:
             st = _lib.fcfs_coeffs_batched_edges(
                 _ptr(corner_ptr), self.B, self.K_total, self.K_max, _ptr(x), _ptr(y), _ptr(w), _ptr(area),
                 _ptr(edges["xa"]), _ptr(edges["xb"]), _ptr(edges["y"]), _ptr(edges["c"]), _ptr(edges["ecnt"]),
-                self.T, ctypes.byref(self.win), self.prec, _ptr(out), _ptr(self.ws), self.ws.numel(), _stream(stream))
+                self.T, ctypes.byref(self.win), self.prec, ctypes.byref(self.opt), _ptr(out), _ptr(self.ws),
+                self.ws.numel(), _stream(stream))
         _check(st, "fcfs_coeffs_batched")
         return out.view(self.B, self.per_clip)
 
 
 def coeffs_batched(corner_ptr, x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", K_max=None,
-                   stream=None):
+                   stream=None, form=None):
     B = corner_ptr.shape[0] - 1
     if K_max is None:
         K_max = int((corner_ptr[1:] - corner_ptr[:-1]).max().item()) if B > 0 else 0
-    plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device)
+    plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device, form=form)
     return plan.run(corner_ptr, x, y, w, area, stream=stream)
 
 

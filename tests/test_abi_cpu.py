@@ -48,6 +48,7 @@ def test_library_is_sm100a_only(fcfs):
 def test_struct_layouts(fcfs):
     assert ctypes.sizeof(fcfs.Window) == 24 and fcfs.Window.pupil_r2.offset == 8 and fcfs.Window.layout.offset == 16
     assert ctypes.sizeof(fcfs.Shard) == 32 and fcfs.Shard.k_lo.offset == 16 and fcfs.Shard.k_hi.offset == 24
+    assert ctypes.sizeof(fcfs.Options) == 32 and fcfs.Options.form.offset == 4 and fcfs.Options.reserved.offset == 8
 
 
 def test_window_helpers_match_oracle(fcfs):
@@ -76,7 +77,32 @@ def test_status_strings_and_no_gpu_behaviour(fcfs):
 
 def test_workspace_queries_are_positive(fcfs):
     w = fcfs.make_window(512, 512)
-    assert fcfs._lib.fcfs_coeffs_workspace_bytes(1_000_000, 65536, ctypes.byref(w), 0, None) > 0
+    assert fcfs._lib.fcfs_coeffs_workspace_bytes(1_000_000, 65536, ctypes.byref(w), 0, None, None) > 0
     assert fcfs._lib.fcfs_vertices_workspace_bytes(250_000, 250_000, 1, 1) > 250_000 * 4 * 8
     wp = fcfs.make_window(27, 27, inputs.pupil_r2(2048), "pupil")
-    assert fcfs._lib.fcfs_batched_workspace_bytes(4096, 4096 * 4800, 5000, 2048, ctypes.byref(wp), 1) > 0
+    assert fcfs._lib.fcfs_batched_workspace_bytes(4096, 4096 * 4800, 5000, 2048, ctypes.byref(wp), 1, None) > 0
+
+
+def test_options_are_validated_and_route_forcing_is_explicit(fcfs):
+    """The library reads no environment variable: routes and forms are fcfs_options fields, and a bad
+    option (unknown enum, non-zero reserved word) is rejected by the planning queries (no device needed)."""
+    import subprocess
+    out = subprocess.run(["strings", fcfs.LIB_PATH], capture_output=True, text=True).stdout
+    for env in ("FCFS_DEBUG", "FCFS_EDGES", "FCFS_ROUTE"):
+        assert env not in out
+    w = fcfs.make_window(512, 512)
+    good = fcfs.make_options(route="fft")
+    assert fcfs._lib.fcfs_coeffs_route(1_000_000, 65536, ctypes.byref(w), 0, None, ctypes.byref(good)) == 1
+    gemm = fcfs.make_options(route="gemm")
+    assert fcfs._lib.fcfs_coeffs_route(1_000_000, 65536, ctypes.byref(w), 0, None, ctypes.byref(gemm)) == 0
+    bad = fcfs.make_options()
+    bad.reserved[3] = 1
+    assert fcfs._lib.fcfs_coeffs_workspace_bytes(1000, 4096, ctypes.byref(w), 0, None, ctypes.byref(bad)) == 0
+    bad = fcfs.Options(7, 0)
+    assert fcfs._lib.fcfs_coeffs_route(1000, 4096, ctypes.byref(w), 0, None, ctypes.byref(bad)) == 0
+    wp = fcfs.make_window(27, 27, inputs.pupil_r2(2048), "pupil")
+    form = fcfs._lib.fcfs_coeffs_batched_form
+    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, None) == fcfs.FORM_EDGE
+    c = fcfs.make_options(form="corner")
+    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, ctypes.byref(c)) == fcfs.FORM_CORNER
+    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 2, None) == fcfs.FORM_CORNER

@@ -389,11 +389,10 @@ def _edge_test_clips(rng, T):
     return [canon, perm, chain, arb, one, empty, longc]
 
 
-@pytest.mark.parametrize("edges", ["1", "0"])
-def test_batched_edge_form_any_corner_list(fcfs, monkeypatch, edges):
+@pytest.mark.parametrize("edges", ["edge", "corner"])
+def test_batched_edge_form_any_corner_list(fcfs, edges):
     """The batched split-TF32 contraction pairs corners into edges (edges.cu); the pairing is a
     term-by-term identity, so any corner list (order, weights) must give the oracle's result."""
-    monkeypatch.setenv("FCFS_EDGES", edges)
     T, M, N = 512, 15, 13
     clips = _edge_test_clips(np.random.default_rng(11), T)
     cp = np.zeros(len(clips) + 1, np.int64)
@@ -403,7 +402,7 @@ def test_batched_edge_form_any_corner_list(fcfs, monkeypatch, edges):
     for prec in ("tf32x3", "f16x3"):
         F = fcfs.coeffs_batched(_dev(cp, torch.int64), _dev(x, torch.int32), _dev(y, torch.int32),
                                 _dev(w, torch.int32), _dev(area, torch.int64), T, M, N, -1.0, "dense",
-                                prec).cpu().numpy()
+                                prec, form=edges).cpu().numpy()
         ms, ns = oracle.window(M, N, -1.0)
         for b in range(len(clips)):
             sl = slice(cp[b], cp[b + 1])
@@ -608,10 +607,14 @@ def test_polygon_clips_coefficients(fcfs, prec):
 # ------------------------------------------------------------------ NEXT-2: the lattice-FFT route (FP64, one clip)
 
 @pytest.fixture
-def route(monkeypatch):
-    """FCFS_ROUTE=fft|gemm forces the single-clip FP64 route (read by libfcfs at every call)."""
+def route(monkeypatch, fcfs):
+    """route("fft" | "gemm") forces the single-clip route of every fcfs.coeffs call in the test
+    (fcfs_options.route through the C-ABI)."""
+    import functools
+    orig = fcfs.coeffs
+
     def set_route(r):
-        monkeypatch.setenv("FCFS_ROUTE", r)
+        monkeypatch.setattr(fcfs, "coeffs", functools.partial(orig, route=r))
     yield set_route
 
 
@@ -916,7 +919,7 @@ def test_vertices_with_edges(fcfs, cfg):
 # ------------------------------------------------------------------ seeded random sweep
 
 @pytest.mark.parametrize("seed", list(range(32)))
-def test_random_sweep(fcfs, seed, monkeypatch):
+def test_random_sweep(fcfs, seed):
     """Seeded random cases across the axes the paths branch on: T (power of two or not, small to
     5000), union groups or singleton rects, window M x N (M != N, zero), dense / pupil layout,
     precision, one clip (fcfs_coeffs: GEMM or FFT route) or a batch (fcfs_coeffs_batched: fused tcgen05
@@ -959,12 +962,10 @@ def test_random_sweep(fcfs, seed, monkeypatch):
     else:
         # single clip: the route the cost model picks, and (where eligible) the lattice-FFT route forced
         for route in (None, "fft"):
-            if route:
-                monkeypatch.setenv("FCFS_ROUTE", route)
-            F = fcfs.coeffs(g["x"], g["y"], g["w"], int(e["area"][0]), T, M, N, r2, layout, prec).cpu().numpy()
+            F = fcfs.coeffs(g["x"], g["y"], g["w"], int(e["area"][0]), T, M, N, r2, layout, prec,
+                            route=route).cpu().numpy()
             Fr, Bd = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
             _assert_parity(F, Fr, Bd, prec, f"seed {seed} route {route}", ms, ns)
-        monkeypatch.delenv("FCFS_ROUTE", raising=False)
 
 
 @pytest.mark.parametrize("seed", list(range(8)))

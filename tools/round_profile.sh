@@ -8,15 +8,15 @@ NB="--no-cpu-baseline --no-e2e"
 # ---- bench lines (each command exits before any profiler run of the same command)
 timeout 300 python bench.py --steps 10 --warmup 3 > $O/${T}_bench_c3.json 2> $O/${T}_bench_c3.err
 timeout 300 python bench.py --prec f16x3 --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_f16x3.json 2>/dev/null
-FCFS_EDGES=0 timeout 300 python bench.py --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_corners.json 2>/dev/null
+timeout 300 python bench.py --form corner --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_corners.json 2>/dev/null
 for c in c1 c2 c4 c5; do
   timeout 400 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $O/${T}_bench_${c}_fp64.json 2>/dev/null
 done
 for c in c4 c5; do for p in tf32x3 f16x3; do
   timeout 300 python bench.py --config $c --prec $p --steps 5 --warmup 3 $NB > $O/${T}_bench_${c}_${p}.json 2>/dev/null
 done; done
-FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_fp64_gemm.json 2>/dev/null
-FCFS_ROUTE=gemm timeout 300 python bench.py --config c4 --prec tf32x3 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_tf32x3_gemm.json 2>/dev/null
+timeout 300 python bench.py --route gemm --config c4 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_fp64_gemm.json 2>/dev/null
+timeout 300 python bench.py --route gemm --config c4 --prec tf32x3 --steps 5 --warmup 3 $NB > $O/${T}_bench_c4_tf32x3_gemm.json 2>/dev/null
 timeout 300 python bench.py --config layout --steps 5 --warmup 3 --no-cpu-baseline > $O/${T}_bench_layout.json 2>/dev/null
 timeout 300 python bench.py --config haar --steps 5 --warmup 3 > $O/${T}_bench_haar.json 2>/dev/null
 timeout 300 python bench.py --input polygons --steps 5 --warmup 3 $NB > $O/${T}_bench_c3_polygons.json 2>/dev/null
@@ -33,9 +33,9 @@ $B3 > /dev/null 2>&1 && $F -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf3
 $B3 > /dev/null 2>&1 && $F -k regex:k_clip_corners -s 1 -c 1 -o $O/${T}_prof_c3_extract $B3 > $O/ncu_f2.log 2>&1
 $B3 > /dev/null 2>&1 && $F -k regex:k_edges -s 1 -c 1 -o $O/${T}_prof_c3_edges $B3 > $O/ncu_f2e.log 2>&1
 $B4 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2|k_fr_row0" -s 0 -c 4 -o $O/${T}_prof_c4_fp64_fft $B4 > $O/ncu_f3.log 2>&1
-FCFS_ROUTE=gemm $B4 > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_fp64|k_gsum_fp64|k_hsum_fp64" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_gemm $B4 > $O/ncu_f4.log 2>&1
+$B4 --route gemm > /dev/null 2>&1 && $F -k regex:"k_gemm_fp64|k_gsum_fp64|k_hsum_fp64" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_gemm $B4 --route gemm > $O/ncu_f4.log 2>&1
 B4t="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
-FCFS_ROUTE=gemm $B4t > /dev/null 2>&1 && FCFS_ROUTE=gemm $F -k regex:"k_gemm_tf32|k_gsum_tc|k_hsum_tc" -s 0 -c 3 -o $O/${T}_prof_c4_tf32_gemm $B4t > $O/ncu_f5.log 2>&1
+$B4t --route gemm > /dev/null 2>&1 && $F -k regex:"k_gemm_tf32|k_gsum_tc|k_hsum_tc" -s 0 -c 3 -o $O/${T}_prof_c4_tf32_gemm $B4t --route gemm > $O/ncu_f5.log 2>&1
 B4t2="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
 $B4t2 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2" -s 0 -c 2 -o $O/${T}_prof_c4_f32_fft $B4t2 > $O/ncu_f6.log 2>&1
 BL="python bench.py --config layout --steps 1 --warmup 1 $NB"
