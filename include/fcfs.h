@@ -96,10 +96,16 @@ typedef struct {
 #define FCFS_FORM_AUTO 0    /* fcfs_coeffs_batched (split precisions): the library's choice               */
 #define FCFS_FORM_EDGE 1    /* FCFS_TF32X3: contract over edges (fcfs_edges; the K/2-term form of Eq. Fkl) */
 #define FCFS_FORM_CORNER 2  /* contract over corners (the K-term form of Eq. Fkl)                         */
+#define FCFS_FORM_LATTICE 3 /* FCFS_TF32X3: contract over the T+1 lattice rows (Step 4 as row DFTs, then the
+                               DFT along y as a tensor-core GEMM against a fixed table).  Needs
+                               T % 4 == 0, T <= 4096, M, N <= 31 and y-sorted corner lists; where a condition
+                               fails the library takes the edge form instead                               */
 typedef struct {
     int32_t route;      /* FCFS_ROUTE_*  */
     int32_t form;       /* FCFS_FORM_*   */
-    int32_t reserved[6];/* must be 0     */
+    int32_t sorted_y;   /* 1: the caller guarantees every clip's corners are sorted by y (fcfs_vertices_from_*
+                           output is); 0: the lattice-row form checks it on the device (one stream sync)   */
+    int32_t reserved[5];/* must be 0     */
 } fcfs_options;
 
 /* Work partition of one clip (BASELINE.json north_star (6); linearity Prop. 2). */
@@ -257,8 +263,10 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
 size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T,
                                     const fcfs_window *win, fcfs_precision prec,
                                     const fcfs_options *opt);
-/* Which contraction form fcfs_coeffs_batched runs for these sizes (FCFS_FORM_EDGE / FCFS_FORM_CORNER;
- * 0 for FCFS_FP64, which contracts over row buckets): planning / reporting, no device work. */
+/* Which contraction form fcfs_coeffs_batched runs for these sizes (FCFS_FORM_LATTICE / FCFS_FORM_EDGE /
+ * FCFS_FORM_CORNER; 0 for FCFS_FP64, which contracts over row buckets), assuming y-sorted corner lists:
+ * planning / reporting, no device work.  FCFS_FORM_AUTO takes the lattice-row form where it applies and the
+ * clips hold at least (T+1)/4 corners on average, else the edge form (FCFS_TF32X3). */
 int32_t fcfs_coeffs_batched_form(int64_t B, int64_t K_total, int64_t K_max, int32_t T,
                                  const fcfs_window *win, fcfs_precision prec, const fcfs_options *opt);
 fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_total,

@@ -27,6 +27,7 @@
 #include <cuda_fp16.h>
 
 #include "coeff.cuh"
+#include "umma.cuh"
 
 namespace fcfs {
 namespace tc {
@@ -48,7 +49,6 @@ constexpr int kOpBytes = kRows * kRowBytes;     // 16 KB per operand per stage
 constexpr int kStageBytes = 2 * kOpBytes;       // A + B
 constexpr int kChunk = 1024;                    // corners per TMEM accumulation (FP64 flush)
 constexpr int kEpiWarps = 4, kProdWarps = 8;
-constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kThreads = (kEpiWarps + kProdWarps + 1) * 32;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kTmemCols = 256;                  // 2 accumulators x 128 fp32 columns
@@ -79,88 +79,6 @@ __host__ __device__ inline Smem smem_layout(int table_entries, int stages = kSta
     s.bars = s.xbuf + 2 * 64 * kXStride * 4;       // xbuf also holds the fused epilogue's fp32 P tile (64 x 65)
     s.total = s.bars + kBarBytes + (fused ? 4 * (kMaxFuseRows + 2) + 8 * 3 * kMaxFuseRows + 4 * kMaxFuseOut : 0);
     return s;
-}
-
-__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// bounded spin: a protocol bug traps (kernel error) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int spin = 0) {
-    uint32_t n = 0;
-    if (spin) {
-        while (!mbar_test(bar, parity)) {
-            if (++n > (1u << 30)) __trap();
-        }
-        return;
-    }
-    while (!mbar_try(bar, parity)) {
-        if (++n > (1u << 26)) __trap();
-    }
-}
-// the same for waits that are long by construction (epilogue per chunk): back off with nanosleep
-// so idle warps do not take issue slots from the producers
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-    uint32_t n = 0;
-    while (!mbar_try(bar, parity)) {
-        __nanosleep(1024);
-        if (++n > (1u << 24)) __trap();
-    }
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ uint32_t tf32_rna(float v) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-    return r;
-}
-
-// canonical K-major SWIZZLE_128B UMMA smem descriptor: rows of 128 B (32 tf32 corners), 8-row
-// atoms of 1024 B (SBO); inside an atom the 16-byte chunk c of row r sits at chunk c ^ (r % 8).
-// byte offset of (row r, corner k) = (r/8) 1024 + (r%8) 128 + (((k/4) ^ (r%8)) 16) + (k%4) 4.
-// The K step of one MMA (8 tf32 = 32 B) advances the start address by 32 B inside the atom.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)1 << 16;                          // LBO: unused for swizzled K-major
-    d |= (uint64_t)((1024 >> 4) & 0x3FFFu) << 32;    // SBO: 8-row atom stride
-    d |= (uint64_t)1 << 46;                          // descriptor version for sm_100
-    d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
-    return d;
-}
-
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}"
-        : "+r"(pred)
-        : "r"(0xffffffffu));
-    return pred != 0;
 }
 
 // ---- debug event trace (FCFS_DEBUG bit 256; CTA 0 only): clock64 << 24 | event << 16 | stage
@@ -198,44 +116,6 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t b
     if (kF16) umma_f16(d_tmem, adesc, bdesc, accumulate);
     else umma_tf32(d_tmem, adesc, bdesc, accumulate);
 }
-
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
-#define TMEM_LD32(taddr, r)                                                                                  \
-    asm volatile(                                                                                            \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),             \
-          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),           \
-          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),           \
-          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                                \
-        : "r"(taddr))
-#define TMEM_LD16(taddr, r)                                                                                  \
-    asm volatile(                                                                                            \
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),             \
-          "=r"(r[15])                                                                                          \
-        : "r"(taddr))
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct ItemInfo {
     int64_t k0, k1;

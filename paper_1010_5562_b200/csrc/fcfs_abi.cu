@@ -100,6 +100,14 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
 bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 
 // sm_100 check, cached per device (atomics: several host threads call this concurrently)
+// lattice.cu
+bool lattice_eligible(int32_t T, const EpiArgs &ea);
+size_t lattice_ws_bytes(int64_t B, int32_t T);
+fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int32_t T, int32_t N,
+                                   void *ws, int32_t *unsorted_dev, cudaStream_t s);
+fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *x, const int32_t *y, const int32_t *w,
+                           int32_t T, const EpiArgs &ea, void *F, void *ws, cudaStream_t s);
+
 static fcfs_status device_ok() {
     static std::atomic<int> cached[64];   // 0 = unknown, 1 = sm_100, 2 = other
     int dev = 0;
@@ -205,27 +213,39 @@ struct CoeffWs {
     void *fft;   // single FP64 clip: the lattice-FFT route's workspace (overlaps bk / G / H: one or the other)
     size_t fft_bytes;
     EdgeWs edges;   // batched split-TF32: the edge form of the corner lists (edges.cu)
+    void *lat;      // batched split-TF32, lattice-row form: B chunk table + chunk pointers (lattice.cu)
+    int32_t *flag;  // device flag (unsorted corner list)
 };
 
-static const fcfs_options kDefaultOptions = {FCFS_ROUTE_AUTO, FCFS_FORM_AUTO, {0, 0, 0, 0, 0, 0}};
+static const fcfs_options kDefaultOptions = {FCFS_ROUTE_AUTO, FCFS_FORM_AUTO, 0, {0, 0, 0, 0, 0}};
 
 static fcfs_status check_options(const fcfs_options *&opt) {
     if (!opt) { opt = &kDefaultOptions; return FCFS_OK; }
     if (opt->route < FCFS_ROUTE_AUTO || opt->route > FCFS_ROUTE_FFT || opt->form < FCFS_FORM_AUTO ||
-        opt->form > FCFS_FORM_CORNER) {
-        set_error("bad options: route %d form %d", opt->route, opt->form);
+        opt->form > FCFS_FORM_LATTICE || opt->sorted_y < 0 || opt->sorted_y > 1) {
+        set_error("bad options: route %d form %d sorted_y %d", opt->route, opt->form, opt->sorted_y);
         return FCFS_E_INVALID;
     }
-    for (int i = 0; i < 6; ++i)
+    for (int i = 0; i < 5; ++i)
         if (opt->reserved[i]) { set_error("fcfs_options.reserved[%d] != 0", i); return FCFS_E_INVALID; }
     return FCFS_OK;
 }
 
-// the batched split-TF32 contraction form: edges (the K/2-term form) unless the caller asks for corners
-static int32_t batched_form(fcfs_precision prec, const fcfs_options *opt) {
+// the batched split-TF32 contraction form (assuming y-sorted lists): the lattice-row form where it applies
+// (and, under AUTO, where the clips are dense enough in corners for its T+1 rows), else the edge form
+// (the K/2-term form) unless the caller asks for corners
+static int32_t batched_form(fcfs_precision prec, const fcfs_options *opt, int64_t B, int64_t K_total, int32_t T,
+                            const fcfs_window *win) {
     if (prec == FCFS_FP64) return 0;
     if (prec == FCFS_F16X3) return FCFS_FORM_CORNER;   // split-FP16 keeps the corner form
-    return opt->form == FCFS_FORM_CORNER ? FCFS_FORM_CORNER : FCFS_FORM_EDGE;
+    if (opt->form == FCFS_FORM_CORNER) return FCFS_FORM_CORNER;
+    if (opt->form == FCFS_FORM_EDGE) return FCFS_FORM_EDGE;
+    EpiArgs ea{};
+    ea.M = win->M; ea.N = win->N; ea.m_lo = -win->M; ea.m_hi = win->M; ea.out_f32 = 1;
+    if (lattice_eligible(T, ea) &&
+        (opt->form == FCFS_FORM_LATTICE || (B > 0 && 4 * K_total >= B * ((int64_t)T + 1))))
+        return FCFS_FORM_LATTICE;
+    return FCFS_FORM_EDGE;
 }
 
 // P_ws is not needed when the tcgen05 kernel fuses the epilogue (batched: whole clip = one 64x64
@@ -249,7 +269,7 @@ static fcfs_status bucket_count_host(const BucketWs &bk, int64_t &nb, cudaStream
 
 // the row buckets (buckets.cu) feed the FP64 contraction; the tcgen05 kernels walk corners
 static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, int64_t K, int64_t B,
-                        fcfs_precision prec, bool single = false, const FftPlan *fp = nullptr) {
+                        fcfs_precision prec, bool single = false, const FftPlan *fp = nullptr, int32_t lat_T = 0) {
     w.P = cv.take<double>(need_P ? (size_t)p.items * kTile * kTile : 1);
     w.area = cv.take<int64_t>(1);
     w.bk = BucketWs{};
@@ -267,7 +287,13 @@ static void carve_coeff(Carver &cv, const GemmPlan &p, CoeffWs &w, bool need_P, 
     const bool bucketed = prec == FCFS_FP64 || single;
     if (bucketed) carve_buckets(cv, K, B, w.bk);
     w.edges = EdgeWs{};
-    if (!single && prec == FCFS_TF32X3) carve_edges(cv, K, B, w.edges);
+    w.lat = nullptr;
+    w.flag = nullptr;
+    if (!single && prec == FCFS_TF32X3) {
+        carve_edges(cv, K, B, w.edges);
+        w.flag = cv.take<int32_t>(64);
+        if (lat_T > 0) w.lat = cv.take<char>(lattice_ws_bytes(B, lat_T));
+    }
     if (bucketed && single) {
         // x-side bucket sums of one chunk: 64 doubles (FP64) or 128 tf32 rows x 4 B (split-TF32) per bucket
         const int64_t cb = chunk_buckets(K, p.tiles_x, p.tiles_y);
@@ -624,16 +650,17 @@ size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, i
     GemmPlan p = make_plan(win->M, win->N, -win->M, win->M, B, K_max, true);
     Carver cv(nullptr, 0);
     CoeffWs w;
-    carve_coeff(cv, p, w, !fusable(p, prec, win->M, -win->M, win->M), K_total, B, prec);
+    const bool lat = valid_T(T) && batched_form(prec, opt, B, K_total, T, win) == FCFS_FORM_LATTICE;
+    carve_coeff(cv, p, w, !fusable(p, prec, win->M, -win->M, win->M), K_total, B, prec, false, nullptr, lat ? T : 0);
     return cv.used();
 }
 
 int32_t fcfs_coeffs_batched_form(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,
                                  fcfs_precision prec, const fcfs_options *opt) {
-    (void)B; (void)K_total; (void)K_max; (void)T;
-    if (check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK) return 0;
+    (void)K_max;
+    if (!valid_T(T) || check_window(win) != FCFS_OK || check_options(opt) != FCFS_OK) return 0;
     if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) return 0;
-    return batched_form(prec, opt);
+    return batched_form(prec, opt, B, K_total, T, win);
 }
 
 }  // extern "C"
@@ -661,7 +688,10 @@ static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_
     plan.phys = prec == FCFS_FP64 ? 0 : 1;
     Carver cv(ws, ws_bytes);
     CoeffWs W;
-    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M), K_total, B, prec);
+    int32_t form = batched_form(prec, opt, B, K_total, T, win);
+    if (given && form == FCFS_FORM_LATTICE && opt->form != FCFS_FORM_LATTICE) form = FCFS_FORM_EDGE;
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M), K_total, B, prec, false, nullptr,
+                form == FCFS_FORM_LATTICE ? T : 0);
     if (!cv.fits()) { set_error("fcfs_coeffs_batched: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     CornerSrc src{};
@@ -673,7 +703,23 @@ static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_
     ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = fcfs_window_size(win);
     bool fused = false;
-    if (prec == FCFS_TF32X3 && K_total > 0 && (given || batched_form(prec, opt) == FCFS_FORM_EDGE)) {   // K/2-term form
+    if (form == FCFS_FORM_LATTICE) {
+        // the lattice-row form (lattice.cu): B chunk table + chunk pointers, then one kernel with the fused
+        // epilogue.  Unless the caller guarantees y-sorted lists, the chunk pass's flag is read back (one
+        // stream sync) and an unsorted batch takes the edge form instead
+        StageScope scope(kStageContract, s);
+        FCFS_TRY_CUDA(cudaMemsetAsync(W.flag, 0, sizeof(int32_t), s));
+        st = launch_lattice_prepare(corner_ptr, B, y, T, win->N, W.lat, W.flag, s);
+        if (st != FCFS_OK) return st;
+        int32_t unsorted = 0;
+        if (!opt->sorted_y) {
+            FCFS_TRY_CUDA(cudaMemcpyAsync(&unsorted, W.flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+        }
+        if (!unsorted) return launch_lattice(corner_ptr, B, x, y, w, T, ea, F, W.lat, s);
+        form = FCFS_FORM_EDGE;
+    }
+    if (prec == FCFS_TF32X3 && K_total > 0 && (given || form == FCFS_FORM_EDGE)) {   // K/2-term form
         const EdgeWs *e = given ? given : &W.edges;
         if (!given) {
             StageScope scope(kStagePair, s);

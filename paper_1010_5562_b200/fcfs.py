@@ -29,11 +29,11 @@ FP64, TF32X3, F16X3 = 0, 1, 2
 LAYOUT_DENSE, LAYOUT_PUPIL = 0, 1
 SHARD_NONE, SHARD_ROWS, SHARD_VERTEX_BLOCK = 0, 1, 2
 ROUTE_AUTO, ROUTE_GEMM, ROUTE_FFT = 0, 1, 2
-FORM_AUTO, FORM_EDGE, FORM_CORNER = 0, 1, 2
+FORM_AUTO, FORM_EDGE, FORM_CORNER, FORM_LATTICE = 0, 1, 2, 3
 _ROUTE = {"auto": ROUTE_AUTO, "gemm": ROUTE_GEMM, "fft": ROUTE_FFT, None: ROUTE_AUTO,
           ROUTE_AUTO: ROUTE_AUTO, ROUTE_GEMM: ROUTE_GEMM, ROUTE_FFT: ROUTE_FFT}
-_FORM = {"auto": FORM_AUTO, "edge": FORM_EDGE, "corner": FORM_CORNER, None: FORM_AUTO,
-         FORM_AUTO: FORM_AUTO, FORM_EDGE: FORM_EDGE, FORM_CORNER: FORM_CORNER}
+_FORM = {"auto": FORM_AUTO, "edge": FORM_EDGE, "corner": FORM_CORNER, "lattice": FORM_LATTICE, None: FORM_AUTO,
+         FORM_AUTO: FORM_AUTO, FORM_EDGE: FORM_EDGE, FORM_CORNER: FORM_CORNER, FORM_LATTICE: FORM_LATTICE}
 _PREC = {"fp64": FP64, "tf32x3": TF32X3, "f16x3": F16X3, FP64: FP64, TF32X3: TF32X3, F16X3: F16X3}
 _LAYOUT = {"dense": LAYOUT_DENSE, "pupil": LAYOUT_PUPIL, LAYOUT_DENSE: LAYOUT_DENSE, LAYOUT_PUPIL: LAYOUT_PUPIL}
 
@@ -49,13 +49,15 @@ class Shard(ctypes.Structure):
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("route", ctypes.c_int32), ("form", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+    _fields_ = [("route", ctypes.c_int32), ("form", ctypes.c_int32), ("sorted_y", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
-def make_options(route=None, form=None):
-    """fcfs_options: route "auto" | "gemm" | "fft" (fcfs_coeffs), form "auto" | "edge" | "corner"
-    (fcfs_coeffs_batched, split precisions)."""
-    return Options(_ROUTE[route], _FORM[form])
+def make_options(route=None, form=None, sorted_y=False):
+    """fcfs_options: route "auto" | "gemm" | "fft" (fcfs_coeffs), form "auto" | "edge" | "corner" | "lattice"
+    (fcfs_coeffs_batched, split precisions), sorted_y: the caller guarantees y-sorted clips (as
+    fcfs_vertices_from_* emit them; skips the lattice form's device check and its stream sync)."""
+    return Options(_ROUTE[route], _FORM[form], 1 if sorted_y else 0)
 
 
 _P, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
@@ -442,13 +444,14 @@ def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=N
 
 class BatchedPlan:
     """Pre-allocated workspace + output for repeated ``fcfs_coeffs_batched`` calls.
-    form: "auto", "edge" or "corner" (fcfs_options.form; split precisions)."""
+    form: "auto", "edge", "corner" or "lattice" (fcfs_options.form; split precisions); sorted_y: see
+    make_options."""
 
     def __init__(self, B, K_total, K_max, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", device="cuda",
-                 form=None):
+                 form=None, sorted_y=False):
         self.B, self.K_total, self.K_max, self.T, self.prec = int(B), int(K_total), int(K_max), int(T), _PREC[prec]
         self.win = make_window(M, N, r2, layout)
-        self.opt = make_options(form=form)
+        self.opt = make_options(form=form, sorted_y=sorted_y)
         nbytes = _lib.fcfs_batched_workspace_bytes(self.B, self.K_total, self.K_max, self.T,
                                                    ctypes.byref(self.win), self.prec, ctypes.byref(self.opt))
         if nbytes == 0:
@@ -479,11 +482,12 @@ class BatchedPlan:
 
 
 def coeffs_batched(corner_ptr, x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="tf32x3", K_max=None,
-                   stream=None, form=None):
+                   stream=None, form=None, sorted_y=False):
     B = corner_ptr.shape[0] - 1
     if K_max is None:
         K_max = int((corner_ptr[1:] - corner_ptr[:-1]).max().item()) if B > 0 else 0
-    plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device, form=form)
+    plan = BatchedPlan(B, x.shape[0], K_max, T, M, N, r2, layout, prec, device=x.device, form=form,
+                       sorted_y=sorted_y)
     return plan.run(corner_ptr, x, y, w, area, stream=stream)
 
 

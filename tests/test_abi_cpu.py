@@ -48,7 +48,8 @@ def test_library_is_sm100a_only(fcfs):
 def test_struct_layouts(fcfs):
     assert ctypes.sizeof(fcfs.Window) == 24 and fcfs.Window.pupil_r2.offset == 8 and fcfs.Window.layout.offset == 16
     assert ctypes.sizeof(fcfs.Shard) == 32 and fcfs.Shard.k_lo.offset == 16 and fcfs.Shard.k_hi.offset == 24
-    assert ctypes.sizeof(fcfs.Options) == 32 and fcfs.Options.form.offset == 4 and fcfs.Options.reserved.offset == 8
+    assert ctypes.sizeof(fcfs.Options) == 32 and fcfs.Options.form.offset == 4 and fcfs.Options.sorted_y.offset == 8 \
+        and fcfs.Options.reserved.offset == 12
 
 
 def test_window_helpers_match_oracle(fcfs):
@@ -102,7 +103,15 @@ def test_options_are_validated_and_route_forcing_is_explicit(fcfs):
     assert fcfs._lib.fcfs_coeffs_route(1000, 4096, ctypes.byref(w), 0, None, ctypes.byref(bad)) == 0
     wp = fcfs.make_window(27, 27, inputs.pupil_r2(2048), "pupil")
     form = fcfs._lib.fcfs_coeffs_batched_form
-    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, None) == fcfs.FORM_EDGE
+    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, None) == fcfs.FORM_LATTICE     # c3: dense clips
+    assert form(4096, 4096 * 40, 50, 2048, ctypes.byref(wp), 1, None) == fcfs.FORM_EDGE       # sparse clips
+    e = fcfs.make_options(form="edge")
+    assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, ctypes.byref(e)) == fcfs.FORM_EDGE
+    lat = fcfs.make_options(form="lattice")
+    assert form(4096, 4096 * 40, 50, 2048, ctypes.byref(wp), 1, ctypes.byref(lat)) == fcfs.FORM_LATTICE
+    assert form(4096, 1 << 24, 5000, 2050, ctypes.byref(wp), 1, ctypes.byref(lat)) == fcfs.FORM_EDGE   # T % 4
+    wide = fcfs.make_window(40, 27)
+    assert form(16, 1 << 16, 5000, 2048, ctypes.byref(wide), 1, ctypes.byref(lat)) == fcfs.FORM_EDGE  # M > 31
     c = fcfs.make_options(form="corner")
     assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, ctypes.byref(c)) == fcfs.FORM_CORNER
     assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 2, None) == fcfs.FORM_CORNER

@@ -410,6 +410,133 @@ def test_batched_edge_form_any_corner_list(fcfs, edges):
             _assert_parity(F[b], Fr, B, prec, f"{prec} clip {b} edges={edges}", ms, ns)
 
 
+@pytest.mark.parametrize("form", ["edge", "corner"])
+@pytest.mark.parametrize("layout", ["dense", "pupil"])
+def test_batched_multi_tile_windows(fcfs, form, layout):
+    """Windows wider than one 32-frequency tile (M = 40, N = 33: 2 x 2 tiles, the unfused batched path that
+    writes P tiles and runs the stand-alone epilogue), non-power-of-two T, split-TF32 edge and corner forms
+    and split-FP16, every clip against the oracle."""
+    rng = np.random.default_rng(77)
+    T, M, N = 3000, 40, 33
+    sizes = [40, 0, 25, 60]
+    cp = np.zeros(len(sizes) + 1, np.int64)
+    cp[1:] = np.cumsum(sizes)
+    rects = inputs.random_rects(rng, int(cp[-1]), T, 4, 700)
+    g = _extract_checked(fcfs, rects, T, None, cp)
+    r2 = 1300.5 if layout == "pupil" else -1.0
+    ms, ns = oracle.window(M, N, r2)
+    cpn = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for prec in ("tf32x3", "f16x3"):
+        F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, r2, layout, prec,
+                                form=form).cpu().numpy()
+        for b in range(len(sizes)):
+            sl = slice(cpn[b], cpn[b + 1])
+            Fr, B = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+            _assert_parity(F[b], Fr, B, prec, f"{prec} {form} {layout} clip {b}", ms, ns)
+
+
+# ------------------------------------------------------------------ lattice-row form (lattice.cu)
+
+def _lattice_clips(rng, T, n_clips, sizes=None):
+    """rect clips for the lattice-row form: random rects (summed groups: |w| up to 3 at coinciding corners),
+    rects touching x = T / y = T and corners on the quarter-wave boundaries T/4, T/2, 3T/4."""
+    rects, cps = [], [0]
+    for b in range(n_clips):
+        n = int(rng.integers(0, 50)) if sizes is None else sizes[b]
+        r = inputs.random_rects(rng, n, T, 1, max(2, T // 5)) if n else np.zeros((0, 4), np.int32)
+        if n >= 6:
+            r[0] = [T // 4, T // 2, 3 * T // 4, T]                  # quarter-wave boundaries, y = T
+            r[1] = [0, 0, T, max(1, T // 7)]                        # x = 0 .. T
+            r[2] = r[3]                                             # duplicate: |w| = 2
+            r[4] = [T // 2 - 1, 3, T // 2 + 1, T // 4]
+        rects.append(r.astype(np.int32))
+        cps.append(cps[-1] + len(r))
+    return np.concatenate(rects).astype(np.int32), np.array(cps, np.int64)
+
+
+@pytest.mark.parametrize("T,M,N,layout", [(2048, 27, 27, "pupil"), (64, 31, 31, "dense"), (100, 9, 0, "dense"),
+                                          (1000, 0, 13, "dense"), (4096, 20, 31, "masked"), (512, 31, 7, "pupil"),
+                                          (8, 3, 3, "dense")])
+def test_lattice_form_parity(fcfs, T, M, N, layout):
+    """The lattice-row form against the oracle on every clip: T from 8 to 4096 (one table row per quarter
+    wave up to T/4 + 1 = 1025), M, N from 0 to 31 (the kernel's limits), pupil / dense / masked-dense
+    layouts, clip counts that are not a multiple of the 4-clip work item, empty clips, corners on x = T,
+    y = T and the quarter-wave boundaries, weights |w| > 1."""
+    rng = np.random.default_rng(T * 7 + M)
+    B = 11
+    rects, cp = _lattice_clips(rng, T, B)
+    g = _extract_checked(fcfs, rects, T, None, cp)
+    r2 = -1.0 if layout == "dense" else (0.7 * (M * M + N * N) + 1.5)
+    lay = "pupil" if layout == "pupil" else "dense"
+    assert fcfs.BatchedPlan(B, g["K"], 50 * 4, T, M, N, r2, lay, "tf32x3", form="lattice").form == fcfs.FORM_LATTICE
+    for sorted_y in (False, True):
+        F = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], T, M, N, r2, lay, "tf32x3",
+                                form="lattice", sorted_y=sorted_y).cpu().numpy()
+        ms, ns = oracle.window(M, N, r2 if lay == "pupil" else -1.0)
+        cpn = g["corner_ptr"].cpu().numpy()
+        x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+        area = g["area"].cpu().numpy()
+        for b in range(B):
+            sl = slice(cpn[b], cpn[b + 1])
+            Fr, Bd = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+            if layout == "masked":
+                out = (ms.astype(np.float64) ** 2 + ns.astype(np.float64) ** 2) > r2
+                Fr[out] = 0
+                Bd[out] = 0
+            _assert_parity(F[b], Fr, Bd, "tf32x3", f"lattice T={T} clip {b} sorted_y={sorted_y}", ms, ns)
+        assert np.array_equal(F.real, F[:, ::-1].real) and np.array_equal(F.imag, -F[:, ::-1].imag)
+
+
+def test_lattice_form_unsorted_lists_fall_back(fcfs):
+    """The lattice-row form needs y-sorted clips: an unsorted batch is detected on the device and takes the
+    edge form (the result is still the oracle's)."""
+    rng = np.random.default_rng(91)
+    T, M, N = 2048, 27, 27
+    rects, cp = _lattice_clips(rng, T, 6, sizes=[30, 40, 0, 25, 33, 8])
+    g = _extract_checked(fcfs, rects, T, None, cp)
+    cpn = g["corner_ptr"].cpu().numpy()
+    perm = np.arange(g["K"])
+    for b in range(6):
+        perm[cpn[b]:cpn[b + 1]] = cpn[b] + rng.permutation(cpn[b + 1] - cpn[b])
+    pt = torch.from_numpy(perm).cuda()
+    xp, yp, wp = (g[k][pt].contiguous() for k in ("x", "y", "w"))
+    r2 = inputs.pupil_r2(T)
+    F = fcfs.coeffs_batched(g["corner_ptr"], xp, yp, wp, g["area"], T, M, N, r2, "pupil", "tf32x3",
+                            form="lattice").cpu().numpy()
+    ms, ns = oracle.window(M, N, r2)
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for b in range(6):
+        sl = slice(cpn[b], cpn[b + 1])
+        Fr, Bd = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+        _assert_parity(F[b], Fr, Bd, "tf32x3", f"unsorted clip {b}", ms, ns)
+
+
+def test_lattice_form_c3_all_clips_and_forms_agree(fcfs):
+    """c3-shaped clips (BASELINE configs[2] statistics, 37 clips): the lattice-row form (AUTO picks it) checked
+    clip by clip against the oracle, and against the edge form within twice the contract."""
+    wl = inputs.c3(clips=37)
+    g = _gpu_extract(fcfs, wl)
+    kw = dict(prec="tf32x3")
+    plan = fcfs.BatchedPlan(wl.B, g["K"], int(np.diff(g["corner_ptr"].cpu().numpy()).max()), wl.T, wl.M, wl.N,
+                            wl.r2, "pupil", "tf32x3", sorted_y=True)
+    assert plan.form == fcfs.FORM_LATTICE
+    F = plan.run(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"]).cpu().numpy()
+    Fe = fcfs.coeffs_batched(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"], wl.T, wl.M, wl.N, wl.r2, "pupil",
+                             form="edge", **kw).cpu().numpy()
+    ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    cpn = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for b in range(wl.B):
+        sl = slice(cpn[b], cpn[b + 1])
+        Fr, Bd = oracle.coeffs(x[sl], y[sl], w[sl], area[b], wl.T, ms, ns)
+        _assert_parity(F[b], Fr, Bd, "tf32x3", f"c3 lattice clip {b}", ms, ns)
+        assert np.all(np.abs(F[b].astype(np.complex128) - Fe[b]) <= 2e-5 * Bd + 1e-7 * np.abs(Fr)), f"forms {b}"
+
+
 def _edges_reference(x, y, w, cp):
     """the pairing rule of include/fcfs.h (fcfs_edges) written out: links join consecutive corners of
     one clip with equal y and opposite weights; even chain positions emit an edge."""
@@ -927,7 +1054,7 @@ def test_random_sweep(fcfs, seed):
     rng = np.random.default_rng(1000 + seed)
     T = int(rng.choice([64, 100, 256, 1000, 2048, 4096, 5000]))
     prec = ["fp64", "tf32x3", "f16x3"][seed % 3]
-    M, N = int(rng.integers(0, 24)), int(rng.integers(0, 24))
+    M, N = int(rng.integers(0, 49)), int(rng.integers(0, 49))
     layout = "pupil" if seed % 4 == 1 else "dense"
     r2 = float(rng.uniform(10, 2 * max(M, N, 1) ** 2)) if layout == "pupil" else -1.0
     batched = seed % 2 == 1
