@@ -278,7 +278,7 @@ fcfs_status fcfs_coeffs_batched(const int64_t *corner_ptr, int64_t B, int64_t K_
 
 /* The same with the edge pairing of the corner lists given (the output of fcfs_edges or of
  * fcfs_vertices_from_rects_edges for these corners; arrays as fcfs_edges documents): FCFS_TF32X3
- * contracts over them instead of pairing again (the edge form, whatever opt->form says); other precisions
+ * contracts over them instead of pairing again (the edge form unless opt->form is FCFS_FORM_LATTICE); other precisions
  * ignore them.  Same workspace. */
 fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int64_t K_total,
                                       int64_t K_max, const int32_t *x, const int32_t *y,
