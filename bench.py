@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--route", default=None, choices=["auto", "gemm", "fft"],
                     help="single-clip configs: fcfs_options.route (default: the library's cost model)")
-    ap.add_argument("--form", default=None, choices=["auto", "edge", "corner"],
+    ap.add_argument("--form", default=None, choices=["auto", "edge", "corner", "lattice"],
                     help="batched split precisions: fcfs_options.form (default: the library's choice)")
     ap.add_argument("--input", default="rects", choices=["rects", "polygons"],
                     help="a1 input: rects (fcfs_vertices_from_rects) or the same rects as 4-vertex polygon "
@@ -435,7 +435,8 @@ def main():
     cptr_h = vp.corner_ptr.cpu().numpy()
     kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
     if wl.B > 1:
-        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, form=args.form)
+        plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, form=args.form,
+                                sorted_y=True)   # corners from fcfs_vertices_from_* are y-sorted per clip
 
         def coeffs():
             return plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area)
@@ -550,6 +551,10 @@ def main():
             rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
             Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
             k_inner = "row buckets"
+        elif getattr(plan, "form", 0) == fcfs.FORM_LATTICE:
+            # lattice-row form: the tensor GEMM contracts over the T+1 lattice rows of every clip
+            Kc = np.full(wl.B, float(wl.T + 1))
+            k_inner = "lattice rows (T+1 per clip)"
         elif getattr(plan, "form", 0) == fcfs.FORM_EDGE:
             Kc = edge_counts(vp, K, cptr_h)
             k_inner = "edges (K/2-term form)"
@@ -583,7 +588,8 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else
                                    ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else "")),
             "kernel": (f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
-                       if fft_route else "k_gemm_" + prec),
+                       if fft_route else ("contract stage (lattice-row form: k_lat_btab + k_lat_cptr + k_lattice)"
+                                          if getattr(plan, "form", 0) == fcfs.FORM_LATTICE else "k_gemm_" + prec)),
             "k_inner": f"{k_inner}: {int(Kc.sum())}",
             "alg_flops_per_launch": alg_flops,
             "kernel_ms_per_launch": round(c_ms_launch, 4), "peak_source": peak_note,
@@ -611,7 +617,7 @@ def main():
                 Ki = vps.run(rects[r0:r1].contiguous(), None, cps)
                 kmi = int(np.diff(vps.corner_ptr.cpu().numpy()).max())
                 pls = fcfs.BatchedPlan(bs, Ki, kmi, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev,
-                                       form=args.form)
+                                       form=args.form, sorted_y=True)
                 subs.append({"r0": r0, "r1": r1, "cp": cps, "vp": vps, "plan": pls,
                              "dev": torch.empty((r1 - r0, 4), dtype=torch.int32, device=dev),
                              "out_h": torch.empty(pls.out.numel(), dtype=pls.out.dtype).pin_memory()})

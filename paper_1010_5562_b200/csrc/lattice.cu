@@ -31,41 +31,42 @@ namespace fcfs {
 namespace lat {
 using namespace fcfs::tc;
 
-constexpr int kYC = 32;                     // lattice rows per chunk (the K of 4 MMAs per product)
+constexpr int kYC = 16;                     // lattice rows per A chunk (the K of 2 MMAs per product)
+constexpr int kBY = 32;                     // lattice rows per B chunk (one SW128 row of K; serves 2 A chunks)
 constexpr int kClips = 4;                   // clips per work item: clip q on TMEM lanes 32q .. 32q+31
-constexpr int kAS = 3;                      // A stages in TMEM (128 columns each)
+constexpr int kAS = 4;                      // A stages in TMEM (64 columns each); A chunk j uses stage j % 4
 constexpr int kBS = 4;                      // B chunk ring in SMEM
-constexpr int kProd = 8;                    // producer warps: sub-partition q = w & 3, chunk parity w >> 2
-constexpr int kEpi = 8;                     // epilogue warps: sub-partition q = e & 3, cos (e < 4) / sin
+constexpr int kProd = 16;                   // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod 4)
+constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA + B-loader warp
-constexpr int kThreads = (kMma + 1) * 32;   // 544
-constexpr int kBTile = 64 * kYC * 4;        // 8 KB: 64 B rows x 32 lattice rows, tf32, SW128 K-major
+constexpr int kThreads = (kMma + 1) * 32;   // 672
+constexpr int kBTile = 64 * kBY * 4;        // 8 KB: 64 B rows x 32 lattice rows, tf32, SW128 K-major
 constexpr int kBChunk = 2 * kBTile;         // hi + lo
-constexpr int kFlush = 8;                   // chunks per FP32 TMEM accumulation block
-constexpr int kXS = 65;                     // exchange row stride (floats)
-constexpr int kStageBytesPerWarp = 32 * 12; // decoded corner records {a, wcs} + x-weight prefixes
+constexpr int kFlush = 16;                  // A chunks per FP32 TMEM accumulation block (256 rows, 96 MMA roundings)
+constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
+constexpr int kStageBytesPerWarp = 32 * kRec;
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
+// TMEM columns: D_c [0,64), D_s [64,128), S_c [128,192), S_s [192,256) (the epilogue's FP32 block sums),
+// A stage s at 256 + 64 s: c_hi [0,16) | c_lo [16,32) | s_hi [32,48) | s_lo [48,64)
+constexpr uint32_t kColS = 128, kColA = 256;
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
 constexpr uint32_t kIdesc =
     (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-constexpr uint32_t kLastBit = 1u << 23, kFlipBit = 1u << 31;
 
 struct Layout {
-    uint32_t bring, table, zero, stage, xchg, tabs, bars, total;
+    uint32_t bring, table, stage, tabs, bars, total;
 };
 
 __host__ __device__ inline Layout layout(int T, int M) {
+    (void)M;
     Layout L;
     L.bring = 0;
     L.table = kBS * kBChunk;
-    const uint32_t tab_bytes = (uint32_t)(T / 4 + 1) * 8u * (uint32_t)(M > 0 ? M : 1);
-    L.zero = (L.table + tab_bytes + 15u) & ~15u;
-    L.stage = L.zero + 16;
-    L.xchg = L.stage + kProd * kStageBytesPerWarp;
-    L.tabs = (L.xchg + kClips * 32 * kXS * 4 + 15u) & ~15u;
+    const uint32_t tab_bytes = (uint32_t)(T / 4 + 1) * 256u;   // 32 lanes x (cos, sin) per row
+    L.stage = (L.table + tab_bytes + 15u) & ~15u;
+    L.tabs = L.stage + kProd * kStageBytesPerWarp;
     // rowoff int32[kMaxRows + 1], nmax int32[kMaxRows], then doubles f_rows, f_invn, f_axm [kMaxRows each]
-    L.bars = L.tabs + 4 * (2 * kMaxRows + 2) + 8 * 3 * kMaxRows;
-    L.bars = (L.bars + 7u) & ~7u;
+    L.bars = (L.tabs + 4 * (2 * kMaxRows + 2) + 8 * 3 * kMaxRows + 7u) & ~7u;
     L.total = L.bars + 8 * (2 * kAS + 2 * kBS + 4) + 16;
     return L;
 }
@@ -102,6 +103,27 @@ __device__ __forceinline__ void tmem_st_zero32(uint32_t taddr) {
         "r"(z)
         : "memory");
 }
+__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+                 "r"(z)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t (&r)[1]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // TS-form MMA: D[tmem] (+)= A[tmem] * B[smem desc]^T
@@ -113,17 +135,19 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
         : "memory");
 }
 
-// split for the tensor core: hi = the top 10 mantissa bits (exact tf32), lo = tf32(v - hi) (rna)
+// split for the tensor core: hi = the top 10 mantissa bits (exact tf32), lo = v - hi (exact in fp32; the
+// MMA reads its top 19 bits: |lo - tf32(lo)| < 2^-10 |lo| < 2^-20 |v|)
 __device__ __forceinline__ void split_hl(float v, uint32_t &hi, uint32_t &lo) {
     hi = __float_as_uint(v) & 0xFFFFE000u;
-    lo = tf32_rna(v - __uint_as_float(hi));
+    lo = __float_as_uint(v - __uint_as_float(hi));
 }
 
 __device__ __forceinline__ uint32_t bf16_bits(float v) {   // exact for the small integer weights
     return __float_as_uint(v) >> 16;
 }
 
-// chunk block bookkeeping (identical in the MMA and epilogue warps)
+// accumulation blocks (identical in the MMA and epilogue warps): D_c blocks start at A chunks j % 16 == 0,
+// D_s blocks at j % 16 == 8 (and j == 0), so the two flushes never coincide inside an item
 __host__ __device__ inline int blocks_c(int nch) { return (nch + kFlush - 1) / kFlush; }
 __host__ __device__ inline int blocks_s(int nch) { return nch <= kFlush / 2 ? 1 : 1 + (nch - kFlush / 2 + kFlush - 1) / kFlush; }
 __device__ __forceinline__ bool c_start(int j) { return j % kFlush == 0; }
@@ -135,9 +159,9 @@ struct Args {
     const int64_t *corner_ptr;
     int64_t B;
     const int32_t *x, *y, *w;
-    const int32_t *cptr;        // [B][nch + 1] chunk starts (relative to the clip's first corner)
-    const uint8_t *btab;        // [nch][hi 8 KB | lo 8 KB]
-    int32_t T, M, N, nch;
+    const int32_t *cptr;        // [B][nch + 1] A-chunk starts (relative to the clip's first corner)
+    const uint8_t *btab;        // [nchb][hi 8 KB | lo 8 KB]
+    int32_t T, M, N, nch, nchb;
     int64_t items;
     EpiArgs ea;
     void *F;
@@ -147,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = su32(smem);
-    const int T = A.T, M = A.M, nch = A.nch;
+    const int T = A.T, M = A.M, nch = A.nch, nchb = A.nchb;
     const Layout L = layout(T, M);
     uint64_t *bars = (uint64_t *)(smem + L.bars);
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kAS + 2 * kBS + 4);
@@ -159,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     auto DFULL = [&](int d) { return bar0 + 8u * (2 * kAS + 2 * kBS + d); };
     auto DEMPTY = [&](int d) { return bar0 + 8u * (2 * kAS + 2 * kBS + 2 + d); };
     int32_t *rowoff = (int32_t *)(smem + L.tabs);          // [2M + 2]
-    int32_t *nmaxr = rowoff + (kMaxRows + 1);               // [2M + 1] entries per output row (half count)
+    int32_t *nmaxr = rowoff + (kMaxRows + 1);               // [2M + 1] half-width of each output row
     double *f_rows = (double *)(smem + L.tabs + 4 * (2 * kMaxRows + 2));
     double *f_invn = f_rows + kMaxRows;
     double *f_axm = f_invn + kMaxRows;
@@ -168,15 +192,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 
     // ---- setup: quarter-wave table, output tables, barriers, TMEM
     {
+        // row u: lane l < M holds (cos, sin)(2 pi (l+1) u / T); lane M holds (T/2, u) (the x-weighted axis
+        // row: x = c_q T/2 + s_q u, see the decode); other lanes 0
         const int rows = T / 4 + 1;
         float2 *tab = (float2 *)(smem + L.table);
-        for (int i = tid; i < rows * M; i += kThreads) {
-            const int u = i / M, m = i % M + 1;
-            double sn, cs;
-            sincospi(2.0 * (double)(((int64_t)m * u) % T) / (double)T, &sn, &cs);
+        for (int i = tid; i < rows * 32; i += kThreads) {
+            const int u = i >> 5, l = i & 31;
+            double sn = 0.0, cs = 0.0;
+            if (l < M) sincospi(2.0 * (double)(((int64_t)(l + 1) * u) % T) / (double)T, &sn, &cs);
+            else if (l == M) { cs = 0.5 * (double)T; sn = (double)u; }
             tab[i] = make_float2((float)cs, (float)sn);
         }
-        if (tid < 4) ((uint32_t *)(smem + L.zero))[tid] = 0u;
         const double pi = 3.141592653589793238462643383279502884;
         for (int a = tid; a < kMaxRows; a += kThreads) {
             f_rows[a] = a ? -1.0 / (4.0 * pi * pi * (double)a) : 0.0;
@@ -192,9 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 off += c < 0 ? 0 : 2 * c + 1;
             }
             rowoff[2 * ea.M + 1] = off;
-            for (int s = 0; s < kAS; ++s) { mbar_init(AFULL(s), 4); mbar_init(AEMPTY(s), 1); }
-            for (int s = 0; s < kBS; ++s) { mbar_init(BFULL(s), 1); mbar_init(BEMPTY(s), 1); }
-            for (int d = 0; d < 2; ++d) { mbar_init(DFULL(d), 1); mbar_init(DEMPTY(d), 4); }
+            for (int st = 0; st < kAS; ++st) { mbar_init(AFULL(st), 4); mbar_init(AEMPTY(st), 1); }
+            for (int st = 0; st < kBS; ++st) { mbar_init(BFULL(st), 1); mbar_init(BEMPTY(st), 1); }
+            for (int d = 0; d < 2; ++d) { mbar_init(DFULL(d), 1); mbar_init(DEMPTY(d), kEpi); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         fence_proxy_async();
@@ -211,93 +237,130 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 
     if (warp < kProd) {
         // ================================ producers ================================
-        const int q = warp & 3, par = warp >> 2;
+        // Warp (q, p) gathers clip q of every item for the A chunks j = p (mod 4) into TMEM stage p.
+        // Per batch of <= 32 corners a lane-parallel decode writes one 24-byte record per corner: three
+        // lane-halves {row address, bf16 weight pair}, for even lanes (odd m: the (-1)^m quarter-wave flip
+        // folded into the weights), odd lanes, and the axis lane (weights (w c_q, w s_q) against the table's
+        // (T/2, u): x = c_q T/2 + s_q u).  The gather walks the corners with uniform control: one LDS.64 of
+        // the lane's record half, one LDS.64 of (cos, sin) from the table row, two FFMAs; at a row end (bit
+        // mask) the two sums are split hi/lo into the row's TMEM columns (column from the chunk's occupancy).
+        const int q = warp & 3, p = warp >> 2;
         const uint32_t lrow = (uint32_t)(32 * q) << 16;                  // TMEM lane base of sub-partition q
-        const bool tl = lane < M;                                         // table lane: m = lane + 1
-        const bool axis = lane == M;                                      // x-weighted axis row (Eq. F0l)
-        const uint32_t lmask = tl ? 0x3FFFFu : 0u;
-        const uint32_t lbase = tl ? (uint32_t)(8 * lane) : sbase + L.zero;
-        const uint32_t oddm = (tl && !(lane & 1)) ? kFlipBit : 0u;       // (-1)^m flip for odd m
-        const uint32_t stg = sbase + L.stage + warp * kStageBytesPerWarp; // {a, wcs} x 32, then prefixes x 32
+        const bool axis = lane == M;
+        const uint32_t lane8 = 8u * (uint32_t)lane;
+        const uint32_t stg = sbase + L.stage + warp * kStageBytesPerWarp;
+        const uint32_t recl = stg + (axis ? 16u : ((lane & 1) ? 8u : 0u));   // this lane's half of each record
         const uint32_t tabaddr = sbase + L.table;
+        const uint32_t tcol = tmem + lrow + kColA + 64u * (uint32_t)p;     // stage p
         const int T2 = T / 2, T4 = T / 4, T34 = 3 * (T / 4);
-        uint32_t gc = 0;
+        uint32_t uses = 0;                                                  // uses of stage p so far
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             const int64_t clip = item * kClips + q;
             const bool real = clip < A.B;
             const int64_t k0 = real ? A.corner_ptr[clip] : 0;
+            // this warp's chunk bounds in registers: lane t holds the bounds of chunk p + 4t and p + 4(32 + t)
             const int32_t *cp = A.cptr + (real ? clip : 0) * (int64_t)(nch + 1);
-            for (int j = 0; j < nch; ++j, ++gc) {
-                if ((j & 1) != par) continue;
-                const int s = (int)(gc % kAS);
-                const uint32_t ph = (gc / kAS) & 1u;
-                mbar_wait(AEMPTY(s), ph ^ 1u);
+            int32_t cs0 = 0, ce0 = 0, cs1 = 0, ce1 = 0;
+            {
+                const int j0 = p + 4 * lane, j1 = p + 4 * (32 + lane);
+                if (real && j0 < nch) { cs0 = __ldg(cp + j0); ce0 = __ldg(cp + j0 + 1); }
+                if (real && j1 < nch) { cs1 = __ldg(cp + j1); ce1 = __ldg(cp + j1 + 1); }
+            }
+            const int nt = nch > p ? (nch - p + 3) / 4 : 0;               // chunks of this warp in the item
+            auto bound = [&](int t, bool end) -> uint32_t {   // uniform
+                const int32_t a0 = __shfl_sync(0xffffffffu, end ? ce0 : cs0, t & 31);
+                const int32_t a1 = __shfl_sync(0xffffffffu, end ? ce1 : cs1, t & 31);
+                return (uint32_t)(t < 32 ? a0 : a1);
+            };
+            // software prefetch of the next batch's corners (x, y, w of corner kb + lane) and of the y after it
+            int ptc = 0;                          // chunk index t of the prefetched batch (nt: none)
+            uint32_t pkb = 0, pce = 0;
+            int32_t px = 0, py = 0, pw = 0, pyn = -1;
+            auto advance = [&](int t, uint32_t kb_next) {
+                uint32_t ce = t < nt ? bound(t, true) : 0u;
+                while (t < nt && kb_next >= ce) {
+                    ++t;
+                    if (t >= nt) break;
+                    kb_next = bound(t, false);
+                    ce = bound(t, true);
+                }
+                ptc = t < nt ? t : nt;
+                pkb = kb_next;
+                pce = ce;
+                if (ptc < nt) {
+                    const bool ok = pkb + (uint32_t)lane < pce;
+                    const int64_t k = k0 + pkb + lane;
+                    px = ok ? __ldg(A.x + k) : 0;
+                    py = ok ? __ldg(A.y + k) : 0;
+                    pw = ok ? __ldg(A.w + k) : 0;
+                    pyn = (pkb + 32u < pce) ? __ldg(A.y + k0 + pkb + 32) : -1;
+                }
+            };
+            advance(0, nt > 0 ? bound(0, false) : 0u);
+            for (int t = 0; t < nt; ++t, ++uses) {
+                const int j = p + 4 * t;
+                const uint32_t ca = bound(t, false), cb = bound(t, true);
+                // stage p is free once the MMAs of its previous chunk have completed: park on the named barrier
+                // the MMA warp arrives at after issuing them (a hardware wait, no polling), then confirm the
+                // completion on the commit's mbarrier
+                if (uses > 0) named_bar(4 + p, 32 + 4 * 32);
+                mbar_wait_park(AEMPTY(p), (uses & 1u) ^ 1u);
                 tc_fence_after();
-                const uint32_t tcol = tmem + lrow + 128u + 128u * (uint32_t)s;
-                tmem_st_zero32(tcol);
-                tmem_st_zero32(tcol + 32);
-                tmem_st_zero32(tcol + 64);
-                tmem_st_zero32(tcol + 96);
+                tmem_st_zero16(tcol);
+                tmem_st_zero16(tcol + 16);
+                tmem_st_zero16(tcol + 32);
+                tmem_st_zero16(tcol + 48);
                 tmem_wait_st();
-                const int32_t ca = real ? __ldg(cp + j) : 0, cb = real ? __ldg(cp + j + 1) : 0;
                 const int32_t y0 = j * kYC;
                 float ac = 0.f, as = 0.f;
-                int32_t carry = 0, pbase = 0;
-                for (int32_t kb = ca; kb < cb; kb += 32) {
-                    const int n = cb - kb < 32 ? cb - kb : 32;
-                    // ---- decode (lane i = corner kb + i): record {a, wcs} + inclusive prefix of w x
+                for (uint32_t kb = ca; kb < cb; kb += 32) {
+                    const uint32_t n = cb - kb < 32u ? cb - kb : 32u;
+                    uint32_t lastmask, occ;
+                    // ---- decode (lane i = corner kb + i), from the prefetched registers
                     {
-                        const bool ok = lane < n;
-                        const int64_t k = k0 + kb + lane;
-                        const int32_t x = ok ? __ldg(A.x + k) : 0;
-                        const int32_t yy = ok ? __ldg(A.y + k) : 0;
-                        const int32_t w = ok ? __ldg(A.w + k) : 0;
+                        const bool ok = (uint32_t)lane < n;
+                        const int32_t x = px, yy = py, w = pw, yafter = pyn;
+                        advance(t, kb + 32);                      // next batch's loads in flight
                         int32_t ynext = __shfl_down_sync(0xffffffffu, yy, 1);
-                        if (lane == n - 1) ynext = (kb + n < cb) ? __ldg(A.y + k + 1) : -1;
-                        const bool last = ynext != yy;
+                        if ((uint32_t)lane == n - 1) ynext = yafter;   // -1 at the chunk's end
+                        const bool last = ok && ynext != yy;
+                        // quarter-wave row: x = c_q T/2 + s_q u; cos(m x) = f_q cos(m u), sin(m x) = f_q s_q sin(m u)
+                        // with f_q = (-1)^m for q = 1, 2
                         int32_t u;
-                        uint32_t flip = 0u;
-                        float ss = 1.f;
+                        float fs = 1.f, ss = 1.f, cq = 0.f;
                         if (x <= T4) { u = x; }
-                        else if (x <= T2) { u = T2 - x; flip = kFlipBit; ss = -1.f; }
-                        else if (x <= T34) { u = x - T2; flip = kFlipBit; }
-                        else { u = T - x; ss = -1.f; }
-                        const uint32_t a = (tabaddr + (uint32_t)u * 8u * (uint32_t)M) | ((uint32_t)(yy - y0) << 18) |
-                                           (last ? kLastBit : 0u) | flip;
+                        else if (x <= T2) { u = T2 - x; fs = -1.f; ss = -1.f; cq = 1.f; }
+                        else if (x <= T34) { u = x - T2; fs = -1.f; cq = 1.f; }
+                        else { u = T - x; ss = -1.f; cq = 2.f; }
+                        const uint32_t a = tabaddr + (uint32_t)u * 256u;
                         const float wf = (float)w;
-                        const uint32_t wcs = bf16_bits(wf) | (bf16_bits(wf * ss) << 16);
-                        int32_t p = w * x;
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const int32_t t = __shfl_up_sync(0xffffffffu, p, d);
-                            if (lane >= d) p += t;
-                        }
-                        p += carry;
-                        carry = __shfl_sync(0xffffffffu, p, 31);
-                        sts64u(stg + 8u * lane, ok ? a : 0u, ok ? wcs : 0u);
-                        sts32i(stg + 256u + 4u * lane, p);
+                        const uint32_t wodd = bf16_bits(wf) | (bf16_bits(wf * ss) << 16);            // even m
+                        const uint32_t wevn = bf16_bits(wf * fs) | (bf16_bits(wf * ss * fs) << 16);   // odd m
+                        const uint32_t wax = bf16_bits(wf * cq) | (bf16_bits(wf * ss) << 16);         // axis lane
+                        sts64u(stg + kRec * lane, a, wevn);          // lane l even <-> m = l + 1 odd
+                        sts64u(stg + kRec * lane + 8u, a, wodd);
+                        sts64u(stg + kRec * lane + 16u, a, wax);
+                        lastmask = __reduce_or_sync(0xffffffffu, last ? (1u << lane) : 0u);
+                        occ = __reduce_or_sync(0xffffffffu, ok ? (1u << (yy - y0)) : 0u);
                     }
                     __syncwarp();
-                    // ---- gather: corner by corner (uniform loop), one LDS.64 of (cos, sin) per lane
-                    for (int i = 0; i < n; ++i) {
-                        const uint2 r = lds64u(stg + 8u * i);
-                        const float2 v = lds64((r.x & lmask) + lbase);
-                        const float vc = __uint_as_float(__float_as_uint(v.x) ^ (r.x & oddm));
-                        const float vs = __uint_as_float(__float_as_uint(v.y) ^ (r.x & oddm));
-                        ac = fmaf(vc, __uint_as_float(r.y << 16), ac);
-                        as = fmaf(vs, __uint_as_float(r.y & 0xFFFF0000u), as);
-                        if (__any_sync(0xffffffffu, (r.x & kLastBit) != 0u)) {
-                            const uint32_t col = (r.x >> 18) & 31u;
-                            const int32_t p = lds32i(stg + 256u + 4u * i);
-                            if (axis) ac = (float)(p - pbase);
-                            pbase = p;
+                    // ---- gather (uniform control)
+                    for (uint32_t i = 0; i < n; ++i) {
+                        const uint2 r = lds64u(recl + kRec * i);
+                        const float2 v = lds64(r.x + lane8);
+                        ac = fmaf(v.x, __uint_as_float(r.y << 16), ac);
+                        as = fmaf(v.y, __uint_as_float(r.y & 0xFFFF0000u), as);
+                        if ((lastmask >> i) & 1u) {
+                            const uint32_t col = __ffs(occ) - 1u;
+                            occ &= occ - 1u;
+                            if (axis) { ac += as; as = 0.f; }     // x = c_q T/2 + s_q u, summed over the row
                             uint32_t h, l;
                             split_hl(ac, h, l);
                             tmem_st1(tcol + col, h);
-                            tmem_st1(tcol + 32u + col, l);
+                            tmem_st1(tcol + 16u + col, l);
                             split_hl(as, h, l);
-                            tmem_st1(tcol + 64u + col, h);
-                            tmem_st1(tcol + 96u + col, l);
+                            tmem_st1(tcol + 32u + col, h);
+                            tmem_st1(tcol + 48u + col, l);
                             ac = 0.f;
                             as = 0.f;
                         }
@@ -307,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 tmem_wait_st();
                 __syncwarp();
                 tc_fence_before();
-                if (lane == 0) mbar_arrive(AFULL(s));
+                named_arrive(8 + p, 32 + 4 * 32);    // stage full: the MMA warp waits on this named barrier
             }
         }
     } else if (warp == kMma) {
@@ -315,15 +378,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         const uint32_t bring = sbase + L.bring;
         int64_t my_items = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) ++my_items;
-        const uint32_t total = (uint32_t)(my_items * nch);
+        const uint32_t total = (uint32_t)(my_items * nchb);
         uint32_t lc = 0;   // B chunks loaded
         auto pump = [&](uint32_t upto) {
             while (lc < upto && lc < total) {
                 const int slot = (int)(lc % kBS);
-                mbar_wait(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
+                mbar_wait_park(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
                 if (elect_one()) {
                     mbar_expect_tx(BFULL(slot), kBChunk);
-                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)(lc % (uint32_t)nch) * kBChunk, kBChunk,
+                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)(lc % (uint32_t)nchb) * kBChunk, kBChunk,
                              BFULL(slot));
                 }
                 __syncwarp();
@@ -331,24 +394,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             }
         };
         pump(kBS - 1);
-        uint32_t gc = 0, tc_ = 0, ts_ = 0;   // chunk counter, D_c / D_s block counters
+        uint32_t gb = 0;                              // B chunks consumed
+        uint32_t us[kAS] = {0u, 0u, 0u, 0u};          // uses of each A stage
+        uint32_t tc_ = 0, ts_ = 0;                    // D_c / D_s blocks issued
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
-            for (int j = 0; j < nch; ++j, ++gc) {
-                const int s = (int)(gc % kAS);
-                const int b = (int)(gc % kBS);
-                mbar_wait(BFULL(b), (gc / kBS) & 1u);
-                mbar_wait(AFULL(s), (gc / kAS) & 1u);
+            const bool last_item = item + gridDim.x >= A.items;
+            for (int j = 0; j < nch; ++j) {
+                const int s = j & (kAS - 1);
+                const int b = (int)(gb % kBS);
+                const bool bfirst = (j & 1) == 0, blast = (j & 1) == 1 || j == nch - 1;
+                if (bfirst) mbar_wait_park(BFULL(b), (gb / kBS) & 1u);
+                named_bar(8 + s, 32 + 4 * 32);       // the 4 producer warps of stage s have filled it
                 tc_fence_after();
-                const uint32_t a0 = tmem + 128u + 128u * (uint32_t)s;
-                const uint64_t bh = umma_desc(bring + (uint32_t)b * kBChunk), bl = umma_desc(bring + (uint32_t)b * kBChunk + kBTile);
+                const uint32_t a0 = tmem + kColA + 64u * (uint32_t)s;
+                const uint32_t koff = (uint32_t)(j & 1) * 4u;   // 64 bytes into the 128-byte K row of the B chunk
+                const uint64_t bh = umma_desc(bring + (uint32_t)b * kBChunk) + koff,
+                               bl = umma_desc(bring + (uint32_t)b * kBChunk + kBTile) + koff;
                 const bool cs = c_start(j), ss = s_start(j);
                 auto issue = [&](int d) {
                     const uint32_t dt = tmem + 64u * (uint32_t)d;
-                    const uint32_t ah = a0 + 64u * (uint32_t)d, al = ah + 32u;
+                    const uint32_t ah = a0 + 32u * (uint32_t)d, al = ah + 16u;
                     const uint32_t fresh = d == 0 ? (cs ? 1u : 0u) : (ss ? 1u : 0u);
                     if (elect_one()) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < 2; ++u) {
                             umma_ts(dt, ah + 8u * u, bh + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
                             umma_ts(dt, al + 8u * u, bh + 2u * u, 1u);
                             umma_ts(dt, ah + 8u * u, bl + 2u * u, 1u);
@@ -357,114 +426,141 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                     __syncwarp();
                 };
                 auto wait_d = [&](int d) {
-                    uint32_t &t = d == 0 ? tc_ : ts_;
-                    mbar_wait(DEMPTY(d), (t & 1u) ^ 1u);
+                    const uint32_t t = d == 0 ? tc_ : ts_;
+                    mbar_wait_park(DEMPTY(d), (t & 1u) ^ 1u);
                     tc_fence_after();
                 };
-                // a D whose accumulation block starts here waits for the epilogue to have read its last
+                // a D whose accumulation block starts here waits for the epilogue to have taken its last
                 // block; the other D's MMAs are issued first so the tensor pipe stays busy meanwhile
                 if (cs && ss) { wait_d(0); wait_d(1); issue(0); issue(1); }
                 else if (cs) { issue(1); wait_d(0); issue(0); }
                 else if (ss) { issue(0); wait_d(1); issue(1); }
                 else { issue(0); issue(1); }
+                const bool ce = c_end(j, nch), se = s_end(j, nch);
                 if (elect_one()) {
                     umma_commit(AEMPTY(s));
-                    umma_commit(BEMPTY(b));
-                    if (c_end(j, nch)) umma_commit(DFULL(0));
-                    if (s_end(j, nch)) umma_commit(DFULL(1));
+                    if (blast) umma_commit(BEMPTY(b));
+                    if (ce) umma_commit(DFULL(0));
+                    if (se) umma_commit(DFULL(1));
                 }
                 __syncwarp();
-                if (c_end(j, nch)) ++tc_;
-                if (s_end(j, nch)) ++ts_;
-                pump(gc + kBS);
+                // wake the epilogue warps (parked on a named barrier) for a finished block
+                if (ce) { named_arrive(2, 32 + kEpi * 32); ++tc_; }
+                if (se) { named_arrive(3, 32 + kEpi * 32); ++ts_; }
+                // the producers of stage s's next use wait for these MMAs: wake them (no arrival for the
+                // stage's last use in the CTA, which nobody waits for)
+                if (!(last_item && j >= nch - kAS)) named_arrive(4 + s, 32 + 4 * 32);
+                ++us[s];
+                if (blast) { ++gb; pump(gb + kBS - 1); }
             }
         }
     } else {
         // ================================ epilogue ================================
-        const int e = warp - kProd, q = e & 3, kind = e >> 2;   // kind 0: D_c (cos rows), 1: D_s (sin rows)
-        const uint32_t dt = tmem + ((uint32_t)(32 * q) << 16) + 64u * (uint32_t)kind;
-        const int nb = kind == 0 ? blocks_c(nch) : blocks_s(nch);
-        float *xc = (float *)(smem + L.xchg) + (size_t)(q * 32 + lane) * kXS;
-        uint32_t t = 0;
+        // Warp q owns TMEM lanes 32q..32q+31 = clip q of each item.  Per finished accumulation block of D_c
+        // or D_s it adds the FP32 block into the running sums S_c / S_s (TMEM); per item it then writes the
+        // clip's window / pupil coefficients from S_c (cos rows) and S_s (sin rows) of its lanes.
+        const int q = warp - kMma + kEpi;   // warps 16..19
+        const uint32_t lrow = (uint32_t)(32 * q) << 16;
+        uint32_t t_[2] = {0u, 0u};
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
-            float S[64];
+            bool first[2] = {true, true};
+            for (int j = 0; j < nch; ++j) {
+                const bool ev[2] = {c_end(j, nch), s_end(j, nch)};
 #pragma unroll
-            for (int i = 0; i < 64; ++i) S[i] = 0.f;
-            for (int bi = 0; bi < nb; ++bi, ++t) {
-                mbar_wait_sleep(DFULL(kind), t & 1u);
-                tc_fence_after();
+                for (int d = 1; d >= 0; --d) {   // s blocks end before c blocks at a shared j (j == nch-1): order fixed
+                    if (!ev[d]) continue;
+                    named_bar(2 + d, 32 + kEpi * 32);
+                    mbar_wait(DFULL(d), t_[d] & 1u);
+                    tc_fence_after();
+                    const uint32_t dsrc = tmem + lrow + 64u * (uint32_t)d;
+                    const uint32_t sdst = tmem + lrow + kColS + 64u * (uint32_t)d;
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    uint32_t r0[16];
-                    TMEM_LD16(dt + 16u * h, r0);
-                    tmem_wait_ld();
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t rd[16], rs[16];
+                        TMEM_LD16(dsrc + 16u * h, rd);
+                        if (!first[d]) TMEM_LD16(sdst + 16u * h, rs);
+                        tmem_wait_ld();
+                        if (!first[d]) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) S[16 * h + i] += __uint_as_float(r0[i]);
+                            for (int i = 0; i < 16; ++i) rd[i] = __float_as_uint(__uint_as_float(rd[i]) + __uint_as_float(rs[i]));
+                        }
+                        tmem_st16(sdst + 16u * h, rd);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(DEMPTY(d));
+                    first[d] = false;
+                    ++t_[d];
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(DEMPTY(kind));
             }
-            // ---- a4 + a5: cos rows combine with the sin rows of the same lane (exchange in SMEM).  D columns:
-            // c < 31: n = c + 1 (cos), 31: the y-weighted axis column, 31 + b: n = b (sin) — fixed offsets so
-            // that S stays in registers (static indices below)
-            if (kind == 1) {
-#pragma unroll
-                for (int i = 0; i < 64; ++i) xc[i] = S[i];
-            }
-            named_bar(1, kEpi * 32);
+            // ---- a4 + a5.  S columns: c < 31: n = c + 1 (cos), 31: the y-weighted axis column, 31 + b: n = b (sin).
+            // The TMEM loads are warp-wide (tcgen05.ld is .sync.aligned); each lane then writes its own row.
             const int64_t clip = item * kClips + q;
-            if (kind == 0 && clip < A.B && lane <= M) {
+            if (clip < A.B) {
                 void *Fc = ea.out_f32 ? (void *)((float2 *)A.F + clip * ea.out_per_clip)
                                       : (void *)((double2 *)A.F + clip * ea.out_per_clip);
                 const bool dmask = ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0;
-                if (lane < M) {
-                    const int m = lane + 1;
-                    const int nm = nmaxr[ea.M + m];
-                    if (nm >= 0) {
-                        const int32_t op = rowoff[ea.M + m] + nm, on = rowoff[ea.M - m] + nm;
-                        const double mm = (double)m * (double)m;
-                        {   // n = 0: Eq. Fk0, F[m,0] = i (Pc_ax - i Ps_ax) / (2 pi m T)
-                            const bool mk = dmask && mm > ea.r2;
-                            const double re = mk ? 0.0 : (double)xc[31] * f_axm[m], im = mk ? 0.0 : (double)S[31] * f_axm[m];
-                            store_out(Fc, op, make_double2(re, im), ea.out_f32);
-                            store_out(Fc, on, make_double2(re, -im), ea.out_f32);
-                        }
+                const uint32_t sc_ = tmem + lrow + kColS, ss_ = sc_ + 64u;
+                const bool row = lane < M, ax = lane == M;
+                const int m = lane + 1;
+                const int nm = row ? nmaxr[ea.M + m] : (ax ? nmaxr[ea.M] : -1);
+                const int32_t op = row ? rowoff[ea.M + m] + nm : (ax ? rowoff[ea.M] + nm : 0);
+                const int32_t on = row ? rowoff[ea.M - m] + nm : 0;
+                const double mm = (double)m * (double)m;
+                {
+                    uint32_t a1[1], a2[1];
+                    tmem_ld1(sc_ + 31u, a1);
+                    tmem_ld1(ss_ + 31u, a2);
+                    tmem_wait_ld();
+                    if (row && nm >= 0) {   // n = 0: Eq. Fk0, F[m,0] = i (Pc_ax - i Ps_ax) / (2 pi m T)
+                        const bool mk = dmask && mm > ea.r2;
+                        const double re = mk ? 0.0 : (double)__uint_as_float(a2[0]) * f_axm[m];
+                        const double im = mk ? 0.0 : (double)__uint_as_float(a1[0]) * f_axm[m];
+                        store_out(Fc, op, make_double2(re, im), ea.out_f32);
+                        store_out(Fc, on, make_double2(re, -im), ea.out_f32);
+                    } else if (ax && nm >= 0) {   // DC (Eq. Fdc)
+                        const double dc = (double)ea.area_dev[clip] / ((double)T * (double)T);
+                        store_out(Fc, op, make_double2(dc, 0.0), ea.out_f32);
+                    }
+                }
 #pragma unroll
-                        for (int b = 1; b <= 31; ++b) {
-                            if (b > nm) break;
+                for (int g = 0; g < 4; ++g) {   // b = 8 g + 1 .. 8 g + 8
+                    if (8 * g + 1 > ea.N) break;   // uniform
+                    uint32_t pcc[8], pcs[8], psc[8], pss[8];
+                    tmem_ld8(sc_ + 8u * g, pcc);         // S_c[b - 1]
+                    tmem_ld8(sc_ + 32u + 8u * g, pcs);   // S_c[31 + b]
+                    tmem_ld8(ss_ + 8u * g, psc);
+                    tmem_ld8(ss_ + 32u + 8u * g, pss);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int b = 8 * g + i + 1;
+                        if (b > nm) break;
+                        if (row) {
                             // Eq. Fkl: S(m, +-b) from the quadrant products, F = -S / (4 pi^2 m n)
-                            const double pcc = S[b - 1], pcs = S[31 + b], psc = xc[b - 1], pss = xc[31 + b];
+                            const double c_c = __uint_as_float(pcc[i]), c_s = __uint_as_float(pcs[i]);
+                            const double s_c = __uint_as_float(psc[i]), s_s = __uint_as_float(pss[i]);
                             const bool mk = dmask && mm + (double)b * (double)b > ea.r2;
                             const double sc = f_rows[m] * f_invn[b];
-                            double re = mk ? 0.0 : (pcc - pss) * sc, im = mk ? 0.0 : -(psc + pcs) * sc;   // n = +b
+                            double re = mk ? 0.0 : (c_c - s_s) * sc, im = mk ? 0.0 : -(s_c + c_s) * sc;   // n = +b
                             store_out(Fc, op + b, make_double2(re, im), ea.out_f32);
                             store_out(Fc, on - b, make_double2(re, -im), ea.out_f32);
-                            re = mk ? 0.0 : -(pcc + pss) * sc;                                              // n = -b
-                            im = mk ? 0.0 : (psc - pcs) * sc;
+                            re = mk ? 0.0 : -(c_c + s_s) * sc;                                              // n = -b
+                            im = mk ? 0.0 : (s_c - c_s) * sc;
                             store_out(Fc, op - b, make_double2(re, im), ea.out_f32);
                             store_out(Fc, on + b, make_double2(re, -im), ea.out_f32);
-                        }
-                    }
-                } else {   // lane == M: row m = 0 (the x-weighted axis row, Eq. F0l) and the DC (Eq. Fdc)
-                    const int nm = nmaxr[ea.M];
-                    if (nm >= 0) {
-                        const int32_t o0 = rowoff[ea.M] + nm;
-                        const double dc = (double)ea.area_dev[clip] / ((double)T * (double)T);
-                        store_out(Fc, o0, make_double2(dc, 0.0), ea.out_f32);
-#pragma unroll
-                        for (int b = 1; b <= 31; ++b) {
-                            if (b > nm) break;
+                        } else {   // lane M: F[0,b] = i (P_ax,c - i P_ax,s) / (2 pi b T) (Eq. F0l)
                             const bool mk = dmask && (double)b * (double)b > ea.r2;
-                            // F[0,b] = i (P_ax,c - i P_ax,s) / (2 pi b T)
-                            const double re = mk ? 0.0 : (double)S[31 + b] * f_axm[b], im = mk ? 0.0 : (double)S[b - 1] * f_axm[b];
-                            store_out(Fc, o0 + b, make_double2(re, im), ea.out_f32);
-                            store_out(Fc, o0 - b, make_double2(re, -im), ea.out_f32);
+                            const double re = mk ? 0.0 : (double)__uint_as_float(pcs[i]) * f_axm[b];
+                            const double im = mk ? 0.0 : (double)__uint_as_float(pcc[i]) * f_axm[b];
+                            store_out(Fc, op + b, make_double2(re, im), ea.out_f32);
+                            store_out(Fc, op - b, make_double2(re, -im), ea.out_f32);
                         }
                     }
                 }
             }
-            named_bar(1, kEpi * 32);   // exchange buffer free for the next item
+            __syncwarp();
         }
     }
 
@@ -479,13 +575,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 // B operand of every chunk (64 rows, fixed offsets): row b - 1 = cos(2 pi b y / T) for b = 1..N, row 31 = y
 // (the coordinate weight of Eq. Fk0), row 31 + b = sin(2 pi b y / T); other rows and lattice rows y > T: 0.
 // hi = tf32(v), lo = tf32(v - hi), both in the SW128 K-major stage layout (row r, k = y - 32 c).
-__global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restrict__ btab) {
-    const int64_t total = (int64_t)nch * 64 * kYC;
+__global__ void k_lat_btab(int32_t T, int32_t N, int32_t nchb, uint8_t *__restrict__ btab) {
+    const int64_t total = (int64_t)nchb * 64 * kBY;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i / (64 * kYC));
-        const int r = (int)((i / kYC) % 64);
-        const int k = (int)(i % kYC);
-        const int64_t y = (int64_t)c * kYC + k;
+        const int c = (int)(i / (64 * kBY));
+        const int r = (int)((i / kBY) % 64);
+        const int k = (int)(i % kBY);
+        const int64_t y = (int64_t)c * kBY + k;
         double v = 0.0;
         if (y <= T) {
             if (r < 31 && r < N) v = cospi(2.0 * (double)(((int64_t)(r + 1) * y) % T) / (double)T);
@@ -503,61 +599,78 @@ __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restric
 }
 
 // chunk starts of every clip: cptr[b][j] = first corner (relative to the clip's start) with y >= 32 j,
-// j = 0 .. nch (cptr[b][nch] = the clip's corner count); flags an unsorted clip in *unsorted.
+// j = 0 .. nch (cptr[b][nch] = the clip's corner count): one thread per (clip, j), a binary search over the
+// clip's y-sorted corners (latency hidden by the thread count)
 __global__ void __launch_bounds__(256) k_lat_cptr(const int64_t *__restrict__ corner_ptr, int64_t B,
-                                                  const int32_t *__restrict__ y, int32_t nch, int32_t *__restrict__ cptr,
-                                                  int32_t *__restrict__ unsorted) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < B; b += nw) {
+                                                  const int32_t *__restrict__ y, int32_t nch, int32_t *__restrict__ cptr) {
+    const int64_t total = B * (int64_t)(nch + 1);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / (nch + 1);
+        const int32_t j = (int32_t)(t - b * (nch + 1));
         const int64_t k0 = corner_ptr[b];
-        const int32_t K = (int32_t)(corner_ptr[b + 1] - k0);
-        int32_t *out = cptr + b * (int64_t)(nch + 1);
-        int bad = 0;
-        for (int32_t i = lane; i < K; i += 32) {
-            const int32_t yy = __ldg(y + k0 + i);
-            const int32_t c = yy >> 5;
-            const int32_t cprev = i > 0 ? (__ldg(y + k0 + i - 1) >> 5) : -1;
-            if (i > 0 && __ldg(y + k0 + i - 1) > yy) bad = 1;
-            for (int32_t jj = cprev + 1; jj <= c && jj <= nch; ++jj) out[jj] = i;
+        int32_t lo = 0, hi = (int32_t)(corner_ptr[b + 1] - k0);
+        const int32_t yv = j * kYC;
+        while (lo < hi) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (__ldg(y + k0 + mid) < yv) lo = mid + 1;
+            else hi = mid;
         }
-        if (lane == 0) {
-            const int32_t clast = K > 0 ? (__ldg(y + k0 + K - 1) >> 5) : -1;
-            for (int32_t jj = clast + 1; jj <= nch; ++jj) out[jj] = K;
+        cptr[t] = lo;
+    }
+}
+
+// y-sortedness of every clip: a decrease y[k-1] > y[k] is allowed only where k starts a clip
+__global__ void __launch_bounds__(256) k_lat_sorted(const int64_t *__restrict__ corner_ptr, int64_t B,
+                                                    const int32_t *__restrict__ y, int64_t K, int32_t *__restrict__ unsorted) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+        if (__ldg(y + k - 1) <= __ldg(y + k)) continue;
+        int64_t lo = 0, hi = B;   // is k a clip start?  (rare: a decrease)
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (corner_ptr[mid] < k) lo = mid + 1;
+            else hi = mid;
         }
-        if (__any_sync(0xffffffffu, bad) && lane == 0) *unsorted = 1;
+        if (lo > B || corner_ptr[lo] != k) *unsorted = 1;
     }
 }
 
 }  // namespace lat
 
-int32_t lattice_chunks(int32_t T) { return (T + 1 + lat::kYC - 1) / lat::kYC; }
+int32_t lattice_chunks(int32_t T) { return (T + 1 + lat::kYC - 1) / lat::kYC; }     // A chunks (16 rows)
+int32_t lattice_bchunks(int32_t T) { return (T + 1 + lat::kBY - 1) / lat::kBY; }    // B chunks (32 rows)
 
 size_t lattice_smem_bytes(int32_t T, int32_t M) { return (size_t)lat::layout(T, M).total + 1024; }
 
 // the lattice-row form applies (T and window limits, SMEM budget); the caller adds the sortedness condition
 bool lattice_eligible(int32_t T, const EpiArgs &ea) {
-    if (T < 4 || (T % 4) != 0 || T > 4096) return false;
+    if (T < 4 || (T % 4) != 0 || T > 2496) return false;   // the quarter-wave table: (T/4 + 1) x 256 B of SMEM
     if (ea.M < 0 || ea.N < 0 || ea.M > 31 || ea.N > 31) return false;
     if (ea.m_lo != -ea.M || ea.m_hi != ea.M || !ea.out_f32) return false;
     return lattice_smem_bytes(T, ea.M) <= 227 * 1024;
 }
 
+static size_t btab_bytes(int32_t T) { return ((size_t)lattice_bchunks(T) * lat::kBChunk + 255) & ~(size_t)255; }
+
 size_t lattice_ws_bytes(int64_t B, int32_t T) {
-    const int32_t nch = lattice_chunks(T);
-    return (size_t)nch * lat::kBChunk + 256 + (size_t)B * (nch + 1) * 4 + 256 + 256;
+    return btab_bytes(T) + (size_t)B * (lattice_chunks(T) + 1) * 4 + 256;
 }
 
-fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int32_t T, int32_t N,
-                                   void *ws, int32_t *unsorted_dev, cudaStream_t s) {
+fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int64_t K, int32_t T,
+                                   int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s) {
     const int32_t nch = lattice_chunks(T);
     uint8_t *btab = (uint8_t *)ws;
-    int32_t *cptr = (int32_t *)(btab + (((size_t)nch * lat::kBChunk + 255) & ~(size_t)255));
-    lat::k_lat_btab<<<148, 256, 0, s>>>(T, N, nch, btab);
+    int32_t *cptr = (int32_t *)(btab + btab_bytes(T));
+    lat::k_lat_btab<<<148, 256, 0, s>>>(T, N, lattice_bchunks(T), btab);
     FCFS_CHECK_LAUNCH("k_lat_btab");
-    const int64_t blocks = (B + 7) / 8;
-    lat::k_lat_cptr<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(corner_ptr, B, y, nch, cptr, unsorted_dev);
+    const int64_t threads = B * (int64_t)(nch + 1);
+    const int64_t blocks = (threads + 255) / 256;
+    lat::k_lat_cptr<<<(unsigned)(blocks < 65536 ? blocks : 65536), 256, 0, s>>>(corner_ptr, B, y, nch, cptr);
     FCFS_CHECK_LAUNCH("k_lat_cptr");
+    if (check && K > 1) {
+        const int64_t kb = (K + 255) / 256;
+        lat::k_lat_sorted<<<(unsigned)(kb < 65536 ? kb : 65536), 256, 0, s>>>(corner_ptr, B, y, K, unsorted_dev);
+        FCFS_CHECK_LAUNCH("k_lat_sorted");
+    }
     return FCFS_OK;
 }
 
@@ -569,8 +682,8 @@ fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *
     a.B = B;
     a.x = x; a.y = y; a.w = w;
     a.btab = (const uint8_t *)ws;
-    a.cptr = (const int32_t *)((const uint8_t *)ws + (((size_t)nch * lat::kBChunk + 255) & ~(size_t)255));
-    a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch;
+    a.cptr = (const int32_t *)((const uint8_t *)ws + btab_bytes(T));
+    a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch; a.nchb = lattice_bchunks(T);
     a.items = (B + lat::kClips - 1) / lat::kClips;
     a.ea = ea;
     a.F = F;

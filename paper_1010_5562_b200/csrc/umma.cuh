@@ -55,10 +55,37 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         if (++n > (1u << 24)) __trap();
     }
 }
+// wait with a suspend-time hint: the warp is parked in hardware until the phase completes (or ~hint ns
+// pass) instead of spinning on try_wait, so waiting warps take no issue slots from the working ones
+__device__ __forceinline__ bool mbar_try_hint(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_park(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try_hint(bar, parity, 1000000u)) {
+        if (++n > (1u << 22)) __trap();
+    }
+}
+// poll with a fixed back-off of `ns` between polls: for waits that are long by construction (an epilogue
+// waiting for a whole accumulation block), where each poll would otherwise take issue slots
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns) {
+    uint32_t n = 0;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        if (++n > (1u << 24)) __trap();
+    }
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ uint32_t tf32_rna(float v) {
     uint32_t r;
