@@ -5,25 +5,28 @@
 //     S[m,n] = sum_k w_k E(m x_k) E(n y_k) = sum_{y=0..T} G[m,y] E(n y),
 //     G[m,y] = sum_{k: y_k = y} w_k E(m x_k)                     (the row DFT of row y)
 //
-// With T <= 2048 the second factor is a FIXED table over the T+1 lattice rows, the same for every clip, so
-// the contraction becomes a dense GEMM whose B operand (E(n y) split hi/lo, 16 KB per 32 rows) streams
-// from L2 by bulk copies and is shared by all clips, and whose A operand G is generated on the fly:
+// With T <= 2496 the second factor is a FIXED table over the T+1 lattice rows, the same for every clip, so
+// the contraction becomes a dense GEMM whose B operand (E(n y) split hi/lo) streams from L2 by bulk copies
+// and is shared by all clips, and whose A operand G is generated on the fly:
 //
 //   * A lives in TENSOR MEMORY (tcgen05.mma with A from TMEM, "TS" form): TMEM sub-partition q holds clip
 //     q of a 4-clip work item, lane l = frequency m = l+1 (lane M: the x-weighted axis row of Eq. F0l).
-//     The producer warp of sub-partition q gathers E(m x_k) for its 32 lanes from a quarter-wave SMEM table
-//     (one conflict-free LDS.64 of (cos, sin) per corner), accumulates the row sums in registers and
-//     writes each finished row's hi/lo split into the stage's TMEM columns (tcgen05.st).  G never exists
-//     in HBM or SMEM ("no full-length arrays").
-//   * The MMA warp issues per 32-row chunk and 4-clip item: D_c += A_c^hi B^hi + A_c^lo B^hi + A_c^hi B^lo
-//     and the same for D_s (sin rows): 24 MMAs of M=128, N=64, K=8 (tf32), A from TMEM, B from SMEM.
-//   * FP32 TMEM accumulation in blocks of 8 chunks (96 MMA roundings); the epilogue warps add
-//     every block into FP32 registers and, per item, write the window / pupil coefficients (a4 + a5).
+//     Two producer warps per sub-partition gather E(m x_k) for their 32 lanes from a quarter-wave SMEM
+//     table (one conflict-free LDS.64 of (cos, sin) per corner), accumulate the row sums in registers (one
+//     FFMA2 per corner) and store each finished row's hi/lo split into its TMEM stage (tcgen05.st).  G never
+//     exists in HBM or SMEM ("no full-length arrays").
+//   * A stage holds 16 lattice rows with hi and lo interleaved along K, (hi_0, lo_0, hi_1, lo_1, ...), so
+//     one MMA stream against B' = (B^hi_0, B^hi_0, B^hi_1, B^hi_1, ...) gives (A^hi + A^lo) B^hi and one
+//     against B'' = (B^lo_0, 0, B^lo_1, 0, ...) gives A^hi B^lo: the three products of the split, 16 MMAs
+//     of M=128, N=64, K=8 per chunk and 4 clips (cos and sin rows).
+//   * FP32 TMEM accumulation in blocks of 16 chunks (256 rows, 128 MMA roundings); the
+//     epilogue warps add every block into FP32 sums (also in TMEM) and, per item, write the window /
+//     pupil coefficients (a4 + a5).
 //
 // Phases are exact integers (lattice vertices): the table row is u = x, T/2 - x, x - T/2 or
-// T - x (quarter-wave symmetry), with the sign (-1)^m applied by a sign-bit flip on odd m and the sin sign
-// folded into the corner weight.  Requires: T % 4 == 0, (T/4 + 1) * 8 M bytes of table in SMEM, M <= 31,
-// N <= 31, the full signed window rows, and corners sorted by y within each clip (checked on the device).
+// T - x (quarter-wave symmetry), with the sign (-1)^m of odd m folded into per-lane-parity weights and the
+// sin sign into the sin weight.  Requires: T % 4 == 0, T <= 2496, M, N <= 31, the full signed window rows,
+// and corners sorted by y within each clip (checked on the device unless the caller guarantees it).
 #include "coeff.cuh"
 #include "umma.cuh"
 
@@ -31,24 +34,29 @@ namespace fcfs {
 namespace lat {
 using namespace fcfs::tc;
 
-constexpr int kYC = 16;                     // lattice rows per A chunk (the K of 2 MMAs per product)
-constexpr int kBY = 32;                     // lattice rows per B chunk (one SW128 row of K; serves 2 A chunks)
+constexpr int kYC = 16;                     // lattice rows per chunk
 constexpr int kClips = 4;                   // clips per work item: clip q on TMEM lanes 32q .. 32q+31
-constexpr int kAS = 4;                      // A stages in TMEM (64 columns each); A chunk j uses stage j % 4
+constexpr int kAS = 4;                      // A stages in TMEM (64 columns each); chunk j uses stage j % 4,
+                                            // so each producer warp ping-pongs between two stages
 constexpr int kBS = 4;                      // B chunk ring in SMEM
-constexpr int kProd = 16;                   // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod 4)
+constexpr int kPW = 4;                      // producer warps per sub-partition
+constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA + B-loader warp
-constexpr int kThreads = (kMma + 1) * 32;   // 672
-constexpr int kBTile = 64 * kBY * 4;        // 8 KB: 64 B rows x 32 lattice rows, tf32, SW128 K-major
-constexpr int kBChunk = 2 * kBTile;         // hi + lo
-constexpr int kFlush = 16;                  // A chunks per FP32 TMEM accumulation block (256 rows, 96 MMA roundings)
+constexpr int kThreads = (kMma + 1) * 32;
+constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (16 lattice rows, hi/lo interleaved)
+constexpr int kBChunk = 2 * kBTile;         // B' + B''
+constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation block (256 rows)
 constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
-constexpr int kStageBytesPerWarp = 32 * kRec;
+constexpr int kStageBytesPerWarp = 32 * kRec + 32 * 4;   // 32 records + 32 flush columns
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
+constexpr int kMaxChunks = 160;             // chunks per clip: (T + 1) / 16 rounded up, T <= 2496
 // TMEM columns: D_c [0,64), D_s [64,128), S_c [128,192), S_s [192,256) (the epilogue's FP32 block sums),
-// A stage s at 256 + 64 s: c_hi [0,16) | c_lo [16,32) | s_hi [32,48) | s_lo [48,64)
+// A stage s at 256 + 64 s: cos (hi, lo) x 16 rows | sin (hi, lo) x 16
 constexpr uint32_t kColS = 128, kColA = 256;
+// named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s free (MMA -> producers);
+// 10 + s: stage s full (producers -> MMA)
+constexpr int kBarD = 2, kBarFree = 4, kBarFull = 4 + kAS;
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
 constexpr uint32_t kIdesc =
     (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -58,11 +66,12 @@ struct Layout {
 };
 
 __host__ __device__ inline Layout layout(int T, int M) {
-    (void)M;
     Layout L;
     L.bring = 0;
     L.table = kBS * kBChunk;
-    const uint32_t tab_bytes = (uint32_t)(T / 4 + 1) * 256u;   // 32 lanes x (cos, sin) per row
+    // row u: lanes 0 .. M (M table lanes + the axis lane), stride 8 (M + 1) B; lanes above M read into the
+    // next row (finite values into A rows nobody reads); one zero row of padding at the end
+    const uint32_t tab_bytes = (uint32_t)(T / 4 + 2) * 8u * (uint32_t)(M + 1) + 256u;
     L.stage = (L.table + tab_bytes + 15u) & ~15u;
     L.tabs = L.stage + kProd * kStageBytesPerWarp;
     // rowoff int32[kMaxRows + 1], nmax int32[kMaxRows], then doubles f_rows, f_invn, f_axm [kMaxRows each]
@@ -81,19 +90,19 @@ __device__ __forceinline__ uint2 lds64u(uint32_t addr) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
 }
-__device__ __forceinline__ int32_t lds32i(uint32_t addr) {
-    int32_t v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
 }
 __device__ __forceinline__ void sts64u(uint32_t addr, uint32_t a, uint32_t b) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
-__device__ __forceinline__ void sts32i(uint32_t addr, int32_t a) {
-    asm volatile("st.shared.s32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
-}
-__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
 }
 __device__ __forceinline__ void tmem_st_zero32(uint32_t taddr) {
     const uint32_t z = 0;
@@ -102,12 +111,6 @@ __device__ __forceinline__ void tmem_st_zero32(uint32_t taddr) {
         "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
         "r"(z)
         : "memory");
-}
-__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
-    const uint32_t z = 0;
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
-                 "r"(z)
-                 : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
@@ -125,6 +128,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                  : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// packed FP32x2 FMA (SASS FFMA2): (ac, as) += (v.x, v.y) * (wc, ws)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%6, %7};\n"
+        " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
 
 // TS-form MMA: D[tmem] (+)= A[tmem] * B[smem desc]^T
 __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t accumulate) {
@@ -146,22 +159,21 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {   // exact for the smal
     return __float_as_uint(v) >> 16;
 }
 
-// accumulation blocks (identical in the MMA and epilogue warps): D_c blocks start at A chunks j % 16 == 0,
+// accumulation blocks (identical in the MMA and epilogue warps): D_c blocks start at chunks j % 16 == 0,
 // D_s blocks at j % 16 == 8 (and j == 0), so the two flushes never coincide inside an item
-__host__ __device__ inline int blocks_c(int nch) { return (nch + kFlush - 1) / kFlush; }
-__host__ __device__ inline int blocks_s(int nch) { return nch <= kFlush / 2 ? 1 : 1 + (nch - kFlush / 2 + kFlush - 1) / kFlush; }
-__device__ __forceinline__ bool c_start(int j) { return j % kFlush == 0; }
-__device__ __forceinline__ bool s_start(int j) { return j == 0 || j % kFlush == kFlush / 2; }
-__device__ __forceinline__ bool c_end(int j, int nch) { return j % kFlush == kFlush - 1 || j == nch - 1; }
-__device__ __forceinline__ bool s_end(int j, int nch) { return j % kFlush == kFlush / 2 - 1 || j == nch - 1; }
+__host__ __device__ inline bool c_start(int j) { return j % kFlush == 0; }
+__host__ __device__ inline bool s_start(int j) { return j == 0 || j % kFlush == kFlush / 2; }
+__host__ __device__ inline bool c_end(int j, int nch) { return j % kFlush == kFlush - 1 || j == nch - 1; }
+__host__ __device__ inline bool s_end(int j, int nch) { return j % kFlush == kFlush / 2 - 1 || j == nch - 1; }
+
 
 struct Args {
     const int64_t *corner_ptr;
     int64_t B;
     const int32_t *x, *y, *w;
-    const int32_t *cptr;        // [B][nch + 1] A-chunk starts (relative to the clip's first corner)
-    const uint8_t *btab;        // [nchb][hi 8 KB | lo 8 KB]
-    int32_t T, M, N, nch, nchb;
+    const int32_t *cptr;        // [B][nch + 1] chunk starts (relative to the clip's first corner)
+    const uint8_t *btab;        // [nch][B' 8 KB | B'' 8 KB]
+    int32_t T, M, N, nch;
     int64_t items;
     EpiArgs ea;
     void *F;
@@ -171,12 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = su32(smem);
-    const int T = A.T, M = A.M, nch = A.nch, nchb = A.nchb;
+    const int T = A.T, M = A.M, N = A.N, nch = A.nch;
     const Layout L = layout(T, M);
     uint64_t *bars = (uint64_t *)(smem + L.bars);
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * kAS + 2 * kBS + 4);
     const uint32_t bar0 = su32(bars);
-    auto AFULL = [&](int s) { return bar0 + 8u * s; };
     auto AEMPTY = [&](int s) { return bar0 + 8u * (kAS + s); };
     auto BFULL = [&](int s) { return bar0 + 8u * (2 * kAS + s); };
     auto BEMPTY = [&](int s) { return bar0 + 8u * (2 * kAS + kBS + s); };
@@ -192,15 +203,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 
     // ---- setup: quarter-wave table, output tables, barriers, TMEM
     {
-        // row u: lane l < M holds (cos, sin)(2 pi (l+1) u / T); lane M holds (T/2, u) (the x-weighted axis
-        // row: x = c_q T/2 + s_q u, see the decode); other lanes 0
-        const int rows = T / 4 + 1;
+        // row u, lane l < M: (cos, sin)(2 pi (l+1) u / T); lane M: (T/2, u) (the x-weighted axis row:
+        // x = c_q T/2 + s_q u, see the decode)
+        const int rows = T / 4 + 2, lanes = M + 1;
         float2 *tab = (float2 *)(smem + L.table);
-        for (int i = tid; i < rows * 32; i += kThreads) {
-            const int u = i >> 5, l = i & 31;
+        for (int i = tid; i < rows * lanes + 32; i += kThreads) {
+            const int u = i / lanes, l = i % lanes;
             double sn = 0.0, cs = 0.0;
-            if (l < M) sincospi(2.0 * (double)(((int64_t)(l + 1) * u) % T) / (double)T, &sn, &cs);
-            else if (l == M) { cs = 0.5 * (double)T; sn = (double)u; }
+            if (u <= T / 4) {
+                if (l < M) sincospi(2.0 * (double)(((int64_t)(l + 1) * u) % T) / (double)T, &sn, &cs);
+                else { cs = 0.5 * (double)T; sn = (double)u; }
+            }
             tab[i] = make_float2((float)cs, (float)sn);
         }
         const double pi = 3.141592653589793238462643383279502884;
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 off += c < 0 ? 0 : 2 * c + 1;
             }
             rowoff[2 * ea.M + 1] = off;
-            for (int st = 0; st < kAS; ++st) { mbar_init(AFULL(st), 4); mbar_init(AEMPTY(st), 1); }
+            for (int st = 0; st < kAS; ++st) mbar_init(AEMPTY(st), 1);
             for (int st = 0; st < kBS; ++st) { mbar_init(BFULL(st), 1); mbar_init(BEMPTY(st), 1); }
             for (int d = 0; d < 2; ++d) { mbar_init(DFULL(d), 1); mbar_init(DEMPTY(d), kEpi); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -234,46 +247,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         tc_fence_after();
     }
     const uint32_t tmem = *tmem_slot;
+    int64_t my_items = 0;
+    for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) ++my_items;
+    const int64_t total_chunks = my_items * nch;
 
     if (warp < kProd) {
         // ================================ producers ================================
-        // Warp (q, p) gathers clip q of every item for the A chunks j = p (mod 4) into TMEM stage p.
-        // Per batch of <= 32 corners a lane-parallel decode writes one 24-byte record per corner: three
-        // lane-halves {row address, bf16 weight pair}, for even lanes (odd m: the (-1)^m quarter-wave flip
-        // folded into the weights), odd lanes, and the axis lane (weights (w c_q, w s_q) against the table's
-        // (T/2, u): x = c_q T/2 + s_q u).  The gather walks the corners with uniform control: one LDS.64 of
-        // the lane's record half, one LDS.64 of (cos, sin) from the table row, two FFMAs; at a row end (bit
-        // mask) the two sums are split hi/lo into the row's TMEM columns (column from the chunk's occupancy).
+        // Warp (q, p) gathers clip q of every item for the chunks j = p (mod kPW) into TMEM stage j % 4 (one
+        // stage per warp for kPW = 4; two, alternately, for kPW = 2).  Per batch of <= 32 corners a lane-parallel decode writes one
+        // 24-byte record per corner: three lane-halves {row address, bf16 weight pair}, for even lanes (odd m:
+        // the (-1)^m quarter-wave flip folded into the weights), odd lanes, and the axis lane (weights (w c_q,
+        // w s_q) against the table's (T/2, u): x = c_q T/2 + s_q u).  The gather walks the corners with
+        // uniform control: one LDS.64 of the lane's record half, one LDS.64 of (cos, sin) from the table row,
+        // one FFMA2; at a row end (bit mask) the two sums are split hi/lo into the row's TMEM columns.
         const int q = warp & 3, p = warp >> 2;
         const uint32_t lrow = (uint32_t)(32 * q) << 16;                  // TMEM lane base of sub-partition q
         const bool axis = lane == M;
         const uint32_t lane8 = 8u * (uint32_t)lane;
+        const uint32_t rowb = 8u * (uint32_t)(M + 1);                     // table row stride
         const uint32_t stg = sbase + L.stage + warp * kStageBytesPerWarp;
         const uint32_t recl = stg + (axis ? 16u : ((lane & 1) ? 8u : 0u));   // this lane's half of each record
+        const uint32_t fcl = stg + 32u * kRec;                              // flush columns [32]
         const uint32_t tabaddr = sbase + L.table;
-        const uint32_t tcol = tmem + lrow + kColA + 64u * (uint32_t)p;     // stage p
         const int T2 = T / 2, T4 = T / 4, T34 = 3 * (T / 4);
-        uint32_t uses = 0;                                                  // uses of stage p so far
+        uint32_t uses0 = 0, uses1 = 0;                                      // uses of stages p, p + kPW so far
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             const int64_t clip = item * kClips + q;
             const bool real = clip < A.B;
             const int64_t k0 = real ? A.corner_ptr[clip] : 0;
-            // this warp's chunk bounds in registers: lane t holds the bounds of chunk p + 4t and p + 4(32 + t)
+            // this warp's chunk bounds in registers: lane l holds the bounds of chunks p + kPW (l + 32 h)
+            constexpr int kNB = (kMaxChunks / kPW + 31) / 32;
             const int32_t *cp = A.cptr + (real ? clip : 0) * (int64_t)(nch + 1);
-            int32_t cs0 = 0, ce0 = 0, cs1 = 0, ce1 = 0;
-            {
-                const int j0 = p + 4 * lane, j1 = p + 4 * (32 + lane);
-                if (real && j0 < nch) { cs0 = __ldg(cp + j0); ce0 = __ldg(cp + j0 + 1); }
-                if (real && j1 < nch) { cs1 = __ldg(cp + j1); ce1 = __ldg(cp + j1 + 1); }
+            int32_t cs[kNB], ce[kNB];
+#pragma unroll
+            for (int h = 0; h < kNB; ++h) {
+                const int jj = p + kPW * (32 * h + lane);
+                cs[h] = ce[h] = 0;
+                if (real && jj < nch) { cs[h] = __ldg(cp + jj); ce[h] = __ldg(cp + jj + 1); }
             }
-            const int nt = nch > p ? (nch - p + 3) / 4 : 0;               // chunks of this warp in the item
+            const int nt = nch > p ? (nch - p + kPW - 1) / kPW : 0;       // chunks of this warp in the item
             auto bound = [&](int t, bool end) -> uint32_t {   // uniform
-                const int32_t a0 = __shfl_sync(0xffffffffu, end ? ce0 : cs0, t & 31);
-                const int32_t a1 = __shfl_sync(0xffffffffu, end ? ce1 : cs1, t & 31);
-                return (uint32_t)(t < 32 ? a0 : a1);
+                int32_t v = 0;
+#pragma unroll
+                for (int h = 0; h < kNB; ++h) {
+                    const int32_t a = __shfl_sync(0xffffffffu, end ? ce[h] : cs[h], t & 31);
+                    if ((t >> 5) == h) v = a;
+                }
+                return (uint32_t)v;
             };
             // software prefetch of the next batch's corners (x, y, w of corner kb + lane) and of the y after it
-            int ptc = 0;                          // chunk index t of the prefetched batch (nt: none)
+            int ptc = 0;
             uint32_t pkb = 0, pce = 0;
             int32_t px = 0, py = 0, pw = 0, pyn = -1;
             auto advance = [&](int t, uint32_t kb_next) {
@@ -297,25 +320,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 }
             };
             advance(0, nt > 0 ? bound(0, false) : 0u);
-            for (int t = 0; t < nt; ++t, ++uses) {
-                const int j = p + 4 * t;
+            for (int t = 0; t < nt; ++t) {
+                const int j = p + kPW * t;
+                const int s = j & (kAS - 1);      // stages p (, p + kPW): every use of them is this warp group's
+                const bool second = s >= kPW;
+                const uint32_t us_ = second ? uses1 : uses0;
+                if (second) ++uses1; else ++uses0;
                 const uint32_t ca = bound(t, false), cb = bound(t, true);
-                // stage p is free once the MMAs of its previous chunk have completed: park on the named barrier
-                // the MMA warp arrives at after issuing them (a hardware wait, no polling), then confirm the
-                // completion on the commit's mbarrier
-                if (uses > 0) named_bar(4 + p, 32 + 4 * 32);
-                mbar_wait_park(AEMPTY(p), (uses & 1u) ^ 1u);
+                // stage s is free once the MMAs of its previous chunk have completed: park on the named barrier
+                // the MMA warp arrives at after issuing them (a hardware wait), then confirm the completion on
+                // the commit's mbarrier
+                if (us_ > 0) named_bar(kBarFree + s, 32 + 4 * 32);
+                mbar_wait_park(AEMPTY(s), (us_ & 1u) ^ 1u);
                 tc_fence_after();
-                tmem_st_zero16(tcol);
-                tmem_st_zero16(tcol + 16);
-                tmem_st_zero16(tcol + 32);
-                tmem_st_zero16(tcol + 48);
+                const uint32_t tcol = tmem + lrow + kColA + 64u * (uint32_t)s;
+                tmem_st_zero32(tcol);
+                tmem_st_zero32(tcol + 32);
                 tmem_wait_st();
                 const int32_t y0 = j * kYC;
-                float ac = 0.f, as = 0.f;
+                float2 acc = make_float2(0.f, 0.f);     // (cos, sin) sums of the current row
                 for (uint32_t kb = ca; kb < cb; kb += 32) {
                     const uint32_t n = cb - kb < 32u ? cb - kb : 32u;
-                    uint32_t lastmask, occ;
+                    uint32_t lastmask;
                     // ---- decode (lane i = corner kb + i), from the prefetched registers
                     {
                         const bool ok = (uint32_t)lane < n;
@@ -332,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                         else if (x <= T2) { u = T2 - x; fs = -1.f; ss = -1.f; cq = 1.f; }
                         else if (x <= T34) { u = x - T2; fs = -1.f; cq = 1.f; }
                         else { u = T - x; ss = -1.f; cq = 2.f; }
-                        const uint32_t a = tabaddr + (uint32_t)u * 256u;
+                        const uint32_t a = tabaddr + (uint32_t)u * rowb;
                         const float wf = (float)w;
                         const uint32_t wodd = bf16_bits(wf) | (bf16_bits(wf * ss) << 16);            // even m
                         const uint32_t wevn = bf16_bits(wf * fs) | (bf16_bits(wf * ss * fs) << 16);   // odd m
@@ -341,28 +367,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                         sts64u(stg + kRec * lane + 8u, a, wodd);
                         sts64u(stg + kRec * lane + 16u, a, wax);
                         lastmask = __reduce_or_sync(0xffffffffu, last ? (1u << lane) : 0u);
-                        occ = __reduce_or_sync(0xffffffffu, ok ? (1u << (yy - y0)) : 0u);
+                        sts32(fcl + 4u * lane, 2u * (uint32_t)(yy - y0));   // the row's (hi, lo) column pair
                     }
                     __syncwarp();
                     // ---- gather (uniform control)
                     for (uint32_t i = 0; i < n; ++i) {
                         const uint2 r = lds64u(recl + kRec * i);
                         const float2 v = lds64(r.x + lane8);
-                        ac = fmaf(v.x, __uint_as_float(r.y << 16), ac);
-                        as = fmaf(v.y, __uint_as_float(r.y & 0xFFFF0000u), as);
-                        if ((lastmask >> i) & 1u) {
-                            const uint32_t col = __ffs(occ) - 1u;
-                            occ &= occ - 1u;
-                            if (axis) { ac += as; as = 0.f; }     // x = c_q T/2 + s_q u, summed over the row
-                            uint32_t h, l;
-                            split_hl(ac, h, l);
-                            tmem_st1(tcol + col, h);
-                            tmem_st1(tcol + 16u + col, l);
-                            split_hl(as, h, l);
-                            tmem_st1(tcol + 32u + col, h);
-                            tmem_st1(tcol + 48u + col, l);
-                            ac = 0.f;
-                            as = 0.f;
+                        acc = ffma2(v, make_float2(__uint_as_float(r.y << 16), __uint_as_float(r.y & 0xFFFF0000u)), acc);
+                        if ((lastmask >> i) & 1u) {   // row end: its (hi, lo) pairs into the row's columns
+                            const uint32_t col = lds32(fcl + 4u * i);
+                            uint32_t h, l, h2, l2;
+                            split_hl(acc.x, h, l);
+                            split_hl(acc.y, h2, l2);
+                            tmem_st2(tcol + col, h, l);
+                            tmem_st2(tcol + 32u + col, h2, l2);
+                            acc = make_float2(0.f, 0.f);
                         }
                     }
                     __syncwarp();
@@ -370,15 +390,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 tmem_wait_st();
                 __syncwarp();
                 tc_fence_before();
-                named_arrive(8 + p, 32 + 4 * 32);    // stage full: the MMA warp waits on this named barrier
+                named_arrive(kBarFull + s, 32 + 4 * 32);    // stage full: the MMA warp waits on this
             }
         }
     } else if (warp == kMma) {
         // ============================ MMA issuer + B loader ============================
         const uint32_t bring = sbase + L.bring;
-        int64_t my_items = 0;
-        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) ++my_items;
-        const uint32_t total = (uint32_t)(my_items * nchb);
+        const uint32_t total = (uint32_t)total_chunks;
         uint32_t lc = 0;   // B chunks loaded
         auto pump = [&](uint32_t upto) {
             while (lc < upto && lc < total) {
@@ -386,42 +404,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 mbar_wait_park(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
                 if (elect_one()) {
                     mbar_expect_tx(BFULL(slot), kBChunk);
-                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)(lc % (uint32_t)nchb) * kBChunk, kBChunk,
+                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)(lc % (uint32_t)nch) * kBChunk, kBChunk,
                              BFULL(slot));
                 }
                 __syncwarp();
                 ++lc;
             }
         };
-        pump(kBS - 1);
-        uint32_t gb = 0;                              // B chunks consumed
-        uint32_t us[kAS] = {0u, 0u, 0u, 0u};          // uses of each A stage
-        uint32_t tc_ = 0, ts_ = 0;                    // D_c / D_s blocks issued
+        pump(kBS);
+        uint32_t tc_ = 0, ts_ = 0;   // D_c / D_s blocks issued
+        uint32_t gc = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             const bool last_item = item + gridDim.x >= A.items;
-            for (int j = 0; j < nch; ++j) {
+            for (int j = 0; j < nch; ++j, ++gc) {
                 const int s = j & (kAS - 1);
-                const int b = (int)(gb % kBS);
-                const bool bfirst = (j & 1) == 0, blast = (j & 1) == 1 || j == nch - 1;
-                if (bfirst) mbar_wait_park(BFULL(b), (gb / kBS) & 1u);
-                named_bar(8 + s, 32 + 4 * 32);       // the 4 producer warps of stage s have filled it
+                const int b = (int)(gc % kBS);
+                mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
+                named_bar(kBarFull + s, 32 + 4 * 32);       // the 4 producer warps of the chunk have filled it
                 tc_fence_after();
                 const uint32_t a0 = tmem + kColA + 64u * (uint32_t)s;
-                const uint32_t koff = (uint32_t)(j & 1) * 4u;   // 64 bytes into the 128-byte K row of the B chunk
-                const uint64_t bh = umma_desc(bring + (uint32_t)b * kBChunk) + koff,
-                               bl = umma_desc(bring + (uint32_t)b * kBChunk + kBTile) + koff;
+                const uint64_t b1 = umma_desc(bring + (uint32_t)b * kBChunk), b2 = umma_desc(bring + (uint32_t)b * kBChunk + kBTile);
                 const bool cs = c_start(j), ss = s_start(j);
                 auto issue = [&](int d) {
                     const uint32_t dt = tmem + 64u * (uint32_t)d;
-                    const uint32_t ah = a0 + 32u * (uint32_t)d, al = ah + 16u;
+                    const uint32_t ad = a0 + 32u * (uint32_t)d;
                     const uint32_t fresh = d == 0 ? (cs ? 1u : 0u) : (ss ? 1u : 0u);
                     if (elect_one()) {
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            umma_ts(dt, ah + 8u * u, bh + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
-                            umma_ts(dt, al + 8u * u, bh + 2u * u, 1u);
-                            umma_ts(dt, ah + 8u * u, bl + 2u * u, 1u);
-                        }
+                        for (int u = 0; u < 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
+                            umma_ts(dt, ad + 8u * u, b1 + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)   // A^hi B^lo
+                            umma_ts(dt, ad + 8u * u, b2 + 2u * u, 1u);
                     }
                     __syncwarp();
                 };
@@ -439,19 +453,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 const bool ce = c_end(j, nch), se = s_end(j, nch);
                 if (elect_one()) {
                     umma_commit(AEMPTY(s));
-                    if (blast) umma_commit(BEMPTY(b));
+                    umma_commit(BEMPTY(b));
                     if (ce) umma_commit(DFULL(0));
                     if (se) umma_commit(DFULL(1));
                 }
                 __syncwarp();
-                // wake the epilogue warps (parked on a named barrier) for a finished block
-                if (ce) { named_arrive(2, 32 + kEpi * 32); ++tc_; }
-                if (se) { named_arrive(3, 32 + kEpi * 32); ++ts_; }
-                // the producers of stage s's next use wait for these MMAs: wake them (no arrival for the
-                // stage's last use in the CTA, which nobody waits for)
-                if (!(last_item && j >= nch - kAS)) named_arrive(4 + s, 32 + 4 * 32);
-                ++us[s];
-                if (blast) { ++gb; pump(gb + kBS - 1); }
+                if (ce) { named_arrive(kBarD + 0, 32 + kEpi * 32); ++tc_; }
+                if (se) { named_arrive(kBarD + 1, 32 + kEpi * 32); ++ts_; }
+                // the producers of stage s's next use wait for these MMAs (no arrival for the stage's last use
+                // in the CTA, which nobody waits for)
+                if (!(last_item && j >= nch - kAS)) named_arrive(kBarFree + s, 32 + 4 * 32);
+                pump(gc + kBS);   // chunk gc + 3 into the slot of chunk gc - 1 (completed by now)
             }
         }
     } else {
@@ -467,9 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             for (int j = 0; j < nch; ++j) {
                 const bool ev[2] = {c_end(j, nch), s_end(j, nch)};
 #pragma unroll
-                for (int d = 1; d >= 0; --d) {   // s blocks end before c blocks at a shared j (j == nch-1): order fixed
+                for (int d = 0; d < 2; ++d) {   // at a shared j (j == nch-1) the MMA warp arrives for c first
                     if (!ev[d]) continue;
-                    named_bar(2 + d, 32 + kEpi * 32);
+                    named_bar(kBarD + d, 32 + kEpi * 32);
                     mbar_wait(DFULL(d), t_[d] & 1u);
                     tc_fence_after();
                     const uint32_t dsrc = tmem + lrow + 64u * (uint32_t)d;
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 }
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {   // b = 8 g + 1 .. 8 g + 8
-                    if (8 * g + 1 > ea.N) break;   // uniform
+                    if (8 * g + 1 > N) break;   // uniform
                     uint32_t pcc[8], pcs[8], psc[8], pss[8];
                     tmem_ld8(sc_ + 8u * g, pcc);         // S_c[b - 1]
                     tmem_ld8(sc_ + 32u + 8u * g, pcs);   // S_c[31 + b]
@@ -537,10 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                     for (int i = 0; i < 8; ++i) {
                         const int b = 8 * g + i + 1;
                         if (b > nm) break;
+                        const double c_c = __uint_as_float(pcc[i]), c_s = __uint_as_float(pcs[i]);
+                        const double s_c = __uint_as_float(psc[i]), s_s = __uint_as_float(pss[i]);
                         if (row) {
                             // Eq. Fkl: S(m, +-b) from the quadrant products, F = -S / (4 pi^2 m n)
-                            const double c_c = __uint_as_float(pcc[i]), c_s = __uint_as_float(pcs[i]);
-                            const double s_c = __uint_as_float(psc[i]), s_s = __uint_as_float(pss[i]);
                             const bool mk = dmask && mm + (double)b * (double)b > ea.r2;
                             const double sc = f_rows[m] * f_invn[b];
                             double re = mk ? 0.0 : (c_c - s_s) * sc, im = mk ? 0.0 : -(s_c + c_s) * sc;   // n = +b
@@ -550,10 +562,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                             im = mk ? 0.0 : (s_c - c_s) * sc;
                             store_out(Fc, op - b, make_double2(re, im), ea.out_f32);
                             store_out(Fc, on + b, make_double2(re, -im), ea.out_f32);
-                        } else {   // lane M: F[0,b] = i (P_ax,c - i P_ax,s) / (2 pi b T) (Eq. F0l)
+                        } else {   // lane M: F[0,b] = i (P_ax,c - i P_ax,s) / (2 pi b T), P_ax = D_c + D_s of lane M
                             const bool mk = dmask && (double)b * (double)b > ea.r2;
-                            const double re = mk ? 0.0 : (double)__uint_as_float(pcs[i]) * f_axm[b];
-                            const double im = mk ? 0.0 : (double)__uint_as_float(pcc[i]) * f_axm[b];
+                            const double re = mk ? 0.0 : (c_s + s_s) * f_axm[b];
+                            const double im = mk ? 0.0 : (c_c + s_c) * f_axm[b];
                             store_out(Fc, op + b, make_double2(re, im), ea.out_f32);
                             store_out(Fc, op - b, make_double2(re, -im), ea.out_f32);
                         }
@@ -572,16 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     }
 }
 
-// B operand of every chunk (64 rows, fixed offsets): row b - 1 = cos(2 pi b y / T) for b = 1..N, row 31 = y
-// (the coordinate weight of Eq. Fk0), row 31 + b = sin(2 pi b y / T); other rows and lattice rows y > T: 0.
-// hi = tf32(v), lo = tf32(v - hi), both in the SW128 K-major stage layout (row r, k = y - 32 c).
-__global__ void k_lat_btab(int32_t T, int32_t N, int32_t nchb, uint8_t *__restrict__ btab) {
-    const int64_t total = (int64_t)nchb * 64 * kBY;
+// B operand of chunk c (16 lattice rows y = 16 c + i), N-rows: b - 1 = cos(2 pi b y / T) for b = 1..N, 31 = y
+// (the coordinate weight of Eq. Fk0), 31 + b = sin(2 pi b y / T); other rows and y > T: 0.  Split v = hi + lo
+// (hi = tf32(v), lo = tf32(v - hi)); B' holds (hi, hi) at K = (2i, 2i+1), B'' holds (lo, 0); both in the
+// SW128 K-major stage layout (row r, k).
+__global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restrict__ btab) {
+    const int64_t total = (int64_t)nch * 64 * kYC;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i / (64 * kBY));
-        const int r = (int)((i / kBY) % 64);
-        const int k = (int)(i % kBY);
-        const int64_t y = (int64_t)c * kBY + k;
+        const int c = (int)(i / (64 * kYC));
+        const int r = (int)((i / kYC) % 64);
+        const int yi = (int)(i % kYC);
+        const int64_t y = (int64_t)c * kYC + yi;
         double v = 0.0;
         if (y <= T) {
             if (r < 31 && r < N) v = cospi(2.0 * (double)(((int64_t)(r + 1) * y) % T) / (double)T);
@@ -590,15 +603,18 @@ __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nchb, uint8_t *__restri
         }
         const float hi = __uint_as_float(tc::tf32_rna((float)v));
         const float lo = __uint_as_float(tc::tf32_rna((float)(v - (double)hi)));
-        const uint32_t off = (uint32_t)(r / 8) * 1024u + (uint32_t)(r % 8) * 128u + ((uint32_t)((k / 4) ^ (r % 8)) << 4) +
-                             (uint32_t)(k % 4) * 4u;
         uint8_t *ch = btab + (size_t)c * kBChunk;
-        *(float *)(ch + off) = hi;
-        *(float *)(ch + kBTile + off) = lo;
+        for (int h = 0; h < 2; ++h) {
+            const int k = 2 * yi + h;
+            const uint32_t off = (uint32_t)(r / 8) * 1024u + (uint32_t)(r % 8) * 128u + ((uint32_t)((k / 4) ^ (r % 8)) << 4) +
+                                 (uint32_t)(k % 4) * 4u;
+            *(float *)(ch + off) = hi;
+            *(float *)(ch + kBTile + off) = h == 0 ? lo : 0.f;
+        }
     }
 }
 
-// chunk starts of every clip: cptr[b][j] = first corner (relative to the clip's start) with y >= 32 j,
+// chunk starts of every clip: cptr[b][j] = first corner (relative to the clip's start) with y >= 16 j,
 // j = 0 .. nch (cptr[b][nch] = the clip's corner count): one thread per (clip, j), a binary search over the
 // clip's y-sorted corners (latency hidden by the thread count)
 __global__ void __launch_bounds__(256) k_lat_cptr(const int64_t *__restrict__ corner_ptr, int64_t B,
@@ -636,31 +652,36 @@ __global__ void __launch_bounds__(256) k_lat_sorted(const int64_t *__restrict__ 
 
 }  // namespace lat
 
-int32_t lattice_chunks(int32_t T) { return (T + 1 + lat::kYC - 1) / lat::kYC; }     // A chunks (16 rows)
-int32_t lattice_bchunks(int32_t T) { return (T + 1 + lat::kBY - 1) / lat::kBY; }    // B chunks (32 rows)
+int32_t lattice_chunks(int32_t T) { return (T + 1 + lat::kYC - 1) / lat::kYC; }
 
 size_t lattice_smem_bytes(int32_t T, int32_t M) { return (size_t)lat::layout(T, M).total + 1024; }
 
 // the lattice-row form applies (T and window limits, SMEM budget); the caller adds the sortedness condition
 bool lattice_eligible(int32_t T, const EpiArgs &ea) {
-    if (T < 4 || (T % 4) != 0 || T > 2496) return false;   // the quarter-wave table: (T/4 + 1) x 256 B of SMEM
+    if (T < 4 || (T % 4) != 0 || T > 2496) return false;   // quarter-wave table rows in SMEM; chunk registers
     if (ea.M < 0 || ea.N < 0 || ea.M > 31 || ea.N > 31) return false;
     if (ea.m_lo != -ea.M || ea.m_hi != ea.M || !ea.out_f32) return false;
+    if (lattice_chunks(T) > 4 * 64) return false;
     return lattice_smem_bytes(T, ea.M) <= 227 * 1024;
 }
 
-static size_t btab_bytes(int32_t T) { return ((size_t)lattice_bchunks(T) * lat::kBChunk + 255) & ~(size_t)255; }
+static size_t btab_bytes(int32_t T) { return ((size_t)lattice_chunks(T) * lat::kBChunk + 255) & ~(size_t)255; }
 
-size_t lattice_ws_bytes(int64_t B, int32_t T) {
-    return btab_bytes(T) + (size_t)B * (lattice_chunks(T) + 1) * 4 + 256;
+static int lattice_grid(int64_t B) {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = (B + lat::kClips - 1) / lat::kClips;
+    return (int)(items < sms ? items : sms);
 }
+
+size_t lattice_ws_bytes(int64_t B, int32_t T) { return btab_bytes(T) + (size_t)B * (lattice_chunks(T) + 1) * 4 + 256; }
 
 fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int64_t K, int32_t T,
                                    int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s) {
     const int32_t nch = lattice_chunks(T);
     uint8_t *btab = (uint8_t *)ws;
     int32_t *cptr = (int32_t *)(btab + btab_bytes(T));
-    lat::k_lat_btab<<<148, 256, 0, s>>>(T, N, lattice_bchunks(T), btab);
+    lat::k_lat_btab<<<148, 256, 0, s>>>(T, N, nch, btab);
     FCFS_CHECK_LAUNCH("k_lat_btab");
     const int64_t threads = B * (int64_t)(nch + 1);
     const int64_t blocks = (threads + 255) / 256;
@@ -683,15 +704,13 @@ fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *
     a.x = x; a.y = y; a.w = w;
     a.btab = (const uint8_t *)ws;
     a.cptr = (const int32_t *)((const uint8_t *)ws + btab_bytes(T));
-    a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch; a.nchb = lattice_bchunks(T);
+    a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch;
     a.items = (B + lat::kClips - 1) / lat::kClips;
     a.ea = ea;
     a.F = F;
     const size_t smem = lattice_smem_bytes(T, ea.M);
     FCFS_TRY(ensure_smem((const void *)lat::k_lattice, smem, true));
-    int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = a.items < sms ? a.items : sms;
+    const int grid = lattice_grid(B);
     lat::k_lattice<<<(unsigned)grid, lat::kThreads, smem, s>>>(a);
     FCFS_CHECK_LAUNCH("k_lattice");
     return FCFS_OK;
