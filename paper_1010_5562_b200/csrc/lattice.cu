@@ -42,8 +42,9 @@ constexpr int kBS = 4;                      // B chunk ring in SMEM
 constexpr int kPW = 4;                      // producer warps per sub-partition
 constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
-constexpr int kMma = kProd + kEpi;          // MMA + B-loader warp
-constexpr int kThreads = (kMma + 1) * 32;
+constexpr int kMma = kProd + kEpi;          // MMA issuer warp
+constexpr int kLoad = kMma + 1;             // B-loader warp (on another sub-partition than the MMA warp)
+constexpr int kThreads = (kLoad + 1) * 32;
 constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (16 lattice rows, hi/lo interleaved)
 constexpr int kBChunk = 2 * kBTile;         // B' + B''
 constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation block (256 rows)
@@ -249,7 +250,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     const uint32_t tmem = *tmem_slot;
     int64_t my_items = 0;
     for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) ++my_items;
-    const int64_t total_chunks = my_items * nch;
 
     if (warp < kProd) {
         // ================================ producers ================================
@@ -394,24 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             }
         }
     } else if (warp == kMma) {
-        // ============================ MMA issuer + B loader ============================
+        // ================================ MMA issuer ================================
         const uint32_t bring = sbase + L.bring;
-        const uint32_t total = (uint32_t)total_chunks;
-        uint32_t lc = 0;   // B chunks loaded
-        auto pump = [&](uint32_t upto) {
-            while (lc < upto && lc < total) {
-                const int slot = (int)(lc % kBS);
-                mbar_wait_park(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
-                if (elect_one()) {
-                    mbar_expect_tx(BFULL(slot), kBChunk);
-                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)(lc % (uint32_t)nch) * kBChunk, kBChunk,
-                             BFULL(slot));
-                }
-                __syncwarp();
-                ++lc;
-            }
-        };
-        pump(kBS);
         uint32_t tc_ = 0, ts_ = 0;   // D_c / D_s blocks issued
         uint32_t gc = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
@@ -463,7 +447,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 // the producers of stage s's next use wait for these MMAs (no arrival for the stage's last use
                 // in the CTA, which nobody waits for)
                 if (!(last_item && j >= nch - kAS)) named_arrive(kBarFree + s, 32 + 4 * 32);
-                pump(gc + kBS);   // chunk gc + 3 into the slot of chunk gc - 1 (completed by now)
+            }
+        }
+    } else if (warp == kLoad) {
+        // ================================ B loader ================================
+        // streams the B chunks (16 KB each, L2-resident: the table is shared by every clip) into the ring
+        const uint32_t bring = sbase + L.bring;
+        uint32_t lc = 0;
+        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
+            for (int j = 0; j < nch; ++j, ++lc) {
+                const int slot = (int)(lc % kBS);
+                mbar_wait_park(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
+                if (elect_one()) {
+                    mbar_expect_tx(BFULL(slot), kBChunk);
+                    bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)j * kBChunk, kBChunk, BFULL(slot));
+                }
+                __syncwarp();
             }
         }
     } else {
