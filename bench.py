@@ -60,7 +60,52 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
     ap.add_argument("--e2e-split", type=int, default=8, help="sub-batches of the pipelined end-to-end measurement")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the extra lines (c4 / c5 FP64, c4 split-TF32) of the default c3 run")
     return ap.parse_args()
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args):
+    """--gpus N without a torchrun environment: re-exec this command under torch.distributed.run with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+EXTRAS = (("c4", "fp64"), ("c5", "fp64"), ("c4", "tf32x3"))
+
+
+def run_extras(args):
+    """The default c3 run also measures the FP64 single-clip configs and c4 split-TF32 (each in a child
+    bench.py process: its own plans, clocks, roofline and sampled oracle baseline); their lines are
+    embedded under "extra"."""
+    out = {}
+    for cfg, prec in EXTRAS:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg, "--prec", prec, "--steps",
+               str(min(args.steps, 5)), "--warmup", "3", "--no-e2e", "--no-extra", "--cpu-seconds", "4"]
+        if prec != "fp64":
+            cmd.append("--no-cpu-baseline")         # the oracle does not depend on the precision: see c4_fp64
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                               env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+            lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+            d = json.loads(lines[-1]) if lines else {"error": (r.stderr or "no output")[-400:]}
+        except Exception as ex:   # a failed extra must not lose the main line
+            d = {"error": repr(ex)[:400]}
+        for k in ("e2e", "metric", "unit", "higher_is_better", "vs_baseline", "data", "n_gpus"):
+            d.pop(k, None)
+        out[f"{cfg}_{prec}"] = d
+    return out
 
 
 def load_peaks():
@@ -143,11 +188,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def cpu_baseline(wl, target_s, prec):
-    """The oracle as it stands (extraction + direct sums), timed on a bounded sample of clips."""
+def cpu_baseline(wl, target_s, prec, one_core=True):
+    """The oracle as it stands (extraction + direct sums), timed on a bounded sample of the workload.
+
+    Extraction and coefficients are timed separately, on all host cores (the oracle's
+    OpenMP coefficient loop; its extraction is serial) and, when one_core, again on one core (the
+    paper's single-threaded setup).  Batched clips: whole clips (all coefficients) until
+    ~target_s.  One clip: the full extraction plus a fixed random sample of coefficients, extrapolated
+    to the full window (t = t_extract + t_sample x W / sample)."""
     import oracle
     cores = oracle.max_threads()
     ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    W = len(ms)
     chop_s = 0.0
     if getattr(wl, "layout", None) is not None:
         lay = wl.layout
@@ -155,39 +207,75 @@ def cpu_baseline(wl, target_s, prec):
         ch = oracle.chop_rects(lay.rects, lay.T, lay.tiles_x, lay.tiles_y)
         chop_s = time.perf_counter() - t0
         wl = inputs.Workload("layout tiles", wl.T, wl.M, wl.N, wl.r2, ch["rects"], None, ch["tile_ptr"], ())
-    terms = 0
-    t0 = time.perf_counter()
-    b = 0
-    nclips = 0
-    while True:
+
+    def extract_clip(b):
         r0, r1 = wl.clip_rect_range(b % wl.B)
-        sub = wl.rects[r0:r1]
         gp = None
         if wl.group_ptr is not None:
             g0, g1 = (wl.clip_ptr[b], wl.clip_ptr[b + 1]) if wl.clip_ptr is not None else (0, len(wl.group_ptr) - 1)
             gp = wl.group_ptr[g0:g1 + 1] - wl.group_ptr[g0]
-        e = oracle.extract(sub, wl.T, gp)
-        if wl.B == 1 and wl.R > 20000:
-            # one huge clip: sample the output set instead of the clips
-            rng = np.random.default_rng(0)
-            pick = rng.choice(len(ms), size=min(len(ms), 64), replace=False)
-            oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms[pick], ns[pick])
-            terms += len(pick) * e["K"]
-            nclips += 1
-            sample = f"1 clip, extraction + {len(pick)} of {len(ms)} coefficients (K={e['K']})"
-            break
-        oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
-        terms += len(ms) * e["K"]
-        nclips += 1
-        b += 1
-        sample = f"{nclips} clips (extraction + all {len(ms)} coefficients each)"
-        if time.perf_counter() - t0 > target_s or nclips >= wl.B:
-            break
-    dt = time.perf_counter() - t0 + chop_s * nclips / max(wl.B, 1)
+        t0 = time.perf_counter()
+        e = oracle.extract(wl.rects[r0:r1], wl.T, gp)
+        return e, time.perf_counter() - t0
+
+    if wl.B == 1 and wl.R > 20000:
+        # one huge clip: the whole extraction + a sample of the output set, extrapolated to all W outputs
+        e, t_ex = extract_clip(0)
+        K = e["K"]
+        rng = np.random.default_rng(0)
+        pick = rng.choice(W, size=min(W, 64), replace=False)
+        t0 = time.perf_counter()
+        oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms[pick], ns[pick])
+        t_c = (time.perf_counter() - t0) / len(pick)               # per coefficient, all cores
+        terms = float(W) * K
+        full = t_ex + t_c * W
+        out = {"value": terms / full / 1e9, "unit": "Gterm/s", "cores": cores, "kind": "oracle",
+               "sample": (f"1 clip: full extraction (K={K}) + {len(pick)} of {W} coefficients (seeded random), "
+                          f"extrapolated to all {W}"),
+               "extract_s": round(t_ex, 4), "coeffs_s_per_coef": t_c, "extrapolated_full_s": round(full, 2),
+               "seconds": round(t_ex + t_c * len(pick), 3)}
+        if one_core:
+            p1 = pick[:16]
+            t0 = time.perf_counter()
+            oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms[p1], ns[p1], nthreads=1)
+            t_c1 = (time.perf_counter() - t0) / len(p1)
+            full1 = t_ex + t_c1 * W
+            out["one_core"] = {"value": terms / full1 / 1e9, "unit": "Gterm/s", "cores": 1,
+                               "sample": f"the same extraction + {len(p1)} coefficients on one core, extrapolated",
+                               "coeffs_s_per_coef": t_c1, "extrapolated_full_s": round(full1, 2)}
+        return out
+
+    def run(nthreads, budget):
+        terms = 0
+        t_ex = t_co = 0.0
+        n = 0
+        t0 = time.perf_counter()
+        while True:
+            e, te = extract_clip(n)
+            tc0 = time.perf_counter()
+            oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns, nthreads=nthreads)
+            t_co += time.perf_counter() - tc0
+            t_ex += te
+            terms += W * e["K"]
+            n += 1
+            if time.perf_counter() - t0 > budget or n >= wl.B:
+                break
+        return terms, n, t_ex, t_co
+
+    terms, n, t_ex, t_co = run(0, target_s)
+    dt = t_ex + t_co + chop_s * n / max(wl.B, 1)
+    sample = f"{n} clips (extraction + all {W} coefficients each)"
     if chop_s:
         sample += f"; + the host chop of the whole layout ({chop_s:.2f} s) charged pro rata"
-    return {"value": terms / dt / 1e9, "unit": "Gterm/s", "cores": cores, "kind": "oracle", "sample": sample,
-            "seconds": round(dt, 3)}
+    out = {"value": terms / dt / 1e9, "unit": "Gterm/s", "cores": cores, "kind": "oracle", "sample": sample,
+           "seconds": round(dt, 3), "extract_s_per_clip": t_ex / n, "coeffs_s_per_clip": t_co / n}
+    if one_core:
+        terms1, n1, t_ex1, t_co1 = run(1, max(1.0, target_s / 3))
+        dt1 = t_ex1 + t_co1 + chop_s * n1 / max(wl.B, 1)
+        out["one_core"] = {"value": terms1 / dt1 / 1e9, "unit": "Gterm/s", "cores": 1,
+                           "sample": f"{n1} clips on one core", "seconds": round(dt1, 3),
+                           "extract_s_per_clip": t_ex1 / n1, "coeffs_s_per_clip": t_co1 / n1}
+    return out
 
 
 def run_reference(args, rank, world):
@@ -222,11 +310,11 @@ def run_reference(args, rank, world):
     prec = args.prec or ("tf32x3" if args.config in ("c3", "layout") else "fp64")
     per_step = max(2.0, min(20.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_baseline(wl, per_step / 4, prec)
+        cpu_baseline(wl, per_step / 4, prec, one_core=False)
     vals = []
     last = None
     for _ in range(args.steps):
-        last = cpu_baseline(wl, per_step, prec)
+        last = cpu_baseline(wl, per_step, prec, one_core=False)
         vals.append(last["value"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": "fourier_coeff_vertex_terms_per_sec", "value": v, "unit": "Gterm/s",
@@ -369,9 +457,13 @@ def bench_haar(args, rank, world, dev):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)                          # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -426,13 +518,25 @@ def main():
 
         def extract():
             return vp.run(pvx, pvy, ppp, cp)
+    elif wl.B == 1 and world > 1:
+        # one clip on N GPUs: a1 sharded by lattice-row bands (fcfs_vertices_from_rects_band) and the
+        # band lists all_gathered into the canonical list on every rank (dist.gather_corners)
+        from paper_1010_5562_b200 import dist as fdist
+        vp = None
+        bandx = fdist.BandExtract(wl.R, wl.T, rank, world, G=G, max_group=mg, grouped=gp is not None, device=dev)
+        gathered = {}
+
+        def extract():
+            x, y, w, k, a = fdist.gather_corners(*bandx.run(rects, gp))
+            gathered.update(x=x, y=y, w=w, K=k, area=a)
+            return k
     else:
         vp = fcfs.VerticesPlan(wl.R, wl.T, G, wl.B, mg, grouped=gp is not None, device=dev)
 
         def extract():
             return vp.run(rects, gp, cp)
     K = extract()
-    cptr_h = vp.corner_ptr.cpu().numpy()
+    cptr_h = vp.corner_ptr.cpu().numpy() if vp is not None else np.array([0, K], np.int64)
     kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
     if wl.B > 1:
         plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, form=args.form,
@@ -442,20 +546,24 @@ def main():
             return plan.run(vp.corner_ptr, vp.x[:K], vp.y[:K], vp.w[:K], vp.area)
         out_bytes = plan.out.numel() * plan.out.element_size()
     elif world > 1:
-        # one clip on N GPUs: every rank extracts the clip (same canonical corner list), computes its
-        # shard and the collective assembles the full window (strong scaling)
-        from paper_1010_5562_b200 import dist as fdist
-        area_h = int(vp.area[0].item())
+        # ... then each rank computes its shard with its own pre-built plan and the collective assembles
+        # the full window (strong scaling): frequency rows + all_gather, or corner blocks (GEMM route) +
+        # reduce_scatter + all_gather
         full_n = (2 * wl.M + 1) * (2 * wl.N + 1)
 
         class _P:
             out = torch.empty(full_n, dtype=torch.complex128 if prec == "fp64" else torch.complex64, device=dev)
         plan = _P()
+        if args.shard == "rows":
+            sharded = fdist.RowsSharded(wl.T, wl.M, wl.N, prec, rank, world, device=dev, route=args.route)
+        else:
+            sharded = fdist.VertexSharded(wl.T, wl.M, wl.N, prec, rank, world, device=dev)
 
         def coeffs():
+            g_ = gathered
             if args.shard == "rows":
-                return fdist.coeffs_rows_sharded(vp.x[:K], vp.y[:K], vp.w[:K], area_h, wl.T, wl.M, wl.N, prec)
-            return fdist.coeffs_vertex_sharded(vp.x[:K], vp.y[:K], vp.w[:K], wl.T, wl.M, wl.N, prec)
+                return sharded.run(g_["x"], g_["y"], g_["w"], g_["K"], g_["area"])
+            return sharded.run(g_["x"], g_["y"], g_["w"], g_["K"])
         out_bytes = plan.out.numel() * plan.out.element_size()
     else:
         plan = fcfs.CoeffsPlan(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, route=args.route)
@@ -498,6 +606,11 @@ def main():
     launches = fcfs.kernel_launches() - launches0
     stages = fcfs.profile_read()
     fcfs.profile_enable(False)
+    per_rank = None
+    if world > 1:
+        allst = [None] * world
+        dist.all_gather_object(allst, {k: round(v[0] / args.steps, 4) for k, v in stages.items()})
+        per_rank = allst
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -548,7 +661,8 @@ def main():
         # inner dimension of the contraction: corners (batched tcgen05 kernels) or row buckets (FP64, and
         # split-TF32 on one clip: Step 4 row structure, fcfs_row_buckets with the cap fcfs_coeffs uses)
         if prec == "fp64" or wl.B == 1:
-            rb = fcfs.row_buckets(vp.y[:K], vp.corner_ptr if wl.B > 1 else None, 32)
+            ysrc = vp.y if vp is not None else gathered["y"]
+            rb = fcfs.row_buckets(ysrc[:K], vp.corner_ptr if wl.B > 1 else None, 32)
             Kc = np.diff(rb["clip_bptr"].cpu().numpy()).astype(np.float64)
             k_inner = "row buckets"
         elif getattr(plan, "form", 0) == fcfs.FORM_LATTICE:
@@ -693,8 +807,13 @@ def main():
                 "K_per_gpu": int(K), "terms_per_step_per_gpu": terms,
                 "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
                 "e2e": e2e}
+        if per_rank is not None:
+            line["per_rank_stage_ms_per_step"] = per_rank
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds, prec)
+        if (world == 1 and args.config == "c3" and not args.no_extra and args.prec in (None, "tf32x3")
+                and args.input == "rects"):
+            line["extra"] = run_extras(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -155,6 +155,20 @@ fcfs_status fcfs_vertices_from_rects_edges(const int32_t *rects, int64_t R, cons
                                            int32_t *ye, int32_t *c, int32_t *ecnt, void *ws,
                                            size_t ws_bytes, void *stream);
 
+/* One clip's canonical corners restricted to the lattice rows y_lo <= y < y_hi — the y-band
+ * shard of a1 for multi-GPU single-clip runs (Prop. 2 linearity).  A
+ * canonical corner is the sum of the raw corners of one (x, y) key (Prop. 1), so the
+ * band's list is exactly the unbanded list's rows in [y_lo, y_hi): rank r of P extracting the band
+ * [y_r, y_{r+1}) and the bands concatenated in order give the canonical list bit for bit.
+ * Arguments as fcfs_vertices_from_rects with clip_ptr = NULL, B = 1 (same workspace query with
+ * B = 1); corner_ptr int64 [2]; area = sum over the band's corners of w x y (the bands' areas sum
+ * to the clip's).  0 <= y_lo <= y_hi (y_hi > T: no upper cut), else FCFS_E_INVALID.  One sync. */
+fcfs_status fcfs_vertices_from_rects_band(const int32_t *rects, int64_t R, const int64_t *group_ptr,
+                                          int64_t G, int32_t T, int64_t max_group, int32_t y_lo,
+                                          int32_t y_hi, int32_t *x, int32_t *y, int32_t *w, int64_t cap,
+                                          int64_t *corner_ptr, int64_t *area, int64_t *K_host, void *ws,
+                                          size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------------------------------
  * a1 from polygon vertex lists (the paper's own input: Alg. 2 REQUIRE "clockwise vertex lists",
  * P:930-935; lines 9-10 "+1 at the end, -1 at the start of each horizontal edge").

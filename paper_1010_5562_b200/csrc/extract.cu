@@ -287,6 +287,19 @@ __global__ void k_fill_sentinel(unsigned long long *keys, int32_t *wts, int64_t 
     }
 }
 
+// y-band of one clip (fcfs_vertices_from_rects_band): raw corners with y outside [y_lo, y_hi) become
+// sentinels of weight 0 before the sort.  A canonical corner is a sum over raw corners of one (x, y)
+// key, so the band's canonical corners are exactly the unbanded ones with y in the band.
+__global__ void k_band_filter(unsigned long long *keys, int32_t *wts, int64_t n, int cb, int32_t y_lo, int32_t y_hi) {
+    const unsigned long long mask = (1ull << cb) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        if (k == kSentinel) continue;
+        const int32_t yy = (int32_t)((k >> cb) & mask);
+        if (yy < y_lo || yy >= y_hi) { keys[i] = kSentinel; wts[i] = 0; }
+    }
+}
+
 __global__ void k_flags(const int32_t *wts, const int64_t *num_runs, int64_t n, int32_t *flags) {
     int64_t nr = *num_runs;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -980,9 +993,10 @@ size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_grou
 fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
-                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {
+                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo, int32_t y_hi) {
     const bool singleton = (group_ptr == nullptr);
-    if (singleton && T <= 65534 && (clip_ptr != nullptr || R <= kClipRects)) {
+    const bool band = y_lo > 0 || y_hi <= T;
+    if (!band && singleton && T <= 65534 && (clip_ptr != nullptr || R <= kClipRects)) {
         fcfs_status st = extract_clips(rects, R, clip_ptr, B, T, x, y, w, cap, corner_ptr, area, K_host, ws,
                                        ws_bytes, s);
         if (st != FCFS_E_UNSUPPORTED) return st;   // else: a clip is too large for the per-clip path
@@ -1039,6 +1053,12 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         }
         k_fill_sentinel<<<148 * 4, 256, 0, s>>>(W.keys_a, W.w_a, cap_raw, raw_count);
         FCFS_CHECK_LAUNCH("k_fill_sentinel");
+    }
+    if (band) {
+        int64_t blocks = (cap_raw + threads - 1) / threads;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        k_band_filter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, cap_raw, cb, y_lo, y_hi);
+        FCFS_CHECK_LAUNCH("k_band_filter");
     }
     int64_t Kh = 0;
     int32_t errh = 0;

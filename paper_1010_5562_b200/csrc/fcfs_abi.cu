@@ -77,7 +77,8 @@ size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_grou
 fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
-                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s);
+                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo = 0,
+                    int32_t y_hi = 0x7fffffff);
 size_t extract_polygons_workspace_bytes(int64_t V, int64_t B);
 fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, const int64_t *poly_ptr, int64_t P,
                              const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
@@ -414,7 +415,8 @@ size_t fcfs_vertices_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t ma
 static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
                                  const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                                  int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
-                                 int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream, const EdgeWs *eo) {
+                                 int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream, const EdgeWs *eo,
+                                 int32_t y_lo = 0, int32_t y_hi = 0x7fffffff) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && !rects) || !corner_ptr || !area || !K_total_host) {
         set_error("fcfs_vertices_from_rects: invalid sizes or null pointers");
@@ -428,7 +430,7 @@ static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t 
     if (st != FCFS_OK) return st;
     StageScope scope(kStageExtract, (cudaStream_t)stream);
     st = extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area, K_total_host,
-                 ws, ws_bytes, (cudaStream_t)stream);
+                 ws, ws_bytes, (cudaStream_t)stream, y_lo, y_hi);
     if (st != FCFS_OK || !eo) return st;
     if (*K_total_host > 0) return run_edges(x, y, w, corner_ptr, B, *eo, (cudaStream_t)stream);
     FCFS_TRY_CUDA(cudaMemsetAsync(eo->cnt, 0, sizeof(int32_t) * (size_t)B, (cudaStream_t)stream));
@@ -460,6 +462,18 @@ fcfs_status fcfs_vertices_from_rects_edges(const int32_t *rects, int64_t R, cons
     e.xa = xa; e.xb = xb; e.y = ye; e.c = c; e.cnt = ecnt;
     return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
                          K_total_host, ws, ws_bytes, stream, &e);
+}
+
+fcfs_status fcfs_vertices_from_rects_band(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                          int32_t T, int64_t max_group, int32_t y_lo, int32_t y_hi, int32_t *x,
+                                          int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                          int64_t *K_host, void *ws, size_t ws_bytes, void *stream) {
+    if (y_lo < 0 || y_hi < y_lo) {
+        set_error("fcfs_vertices_from_rects_band: band [%d, %d) invalid", y_lo, y_hi);
+        return FCFS_E_INVALID;
+    }
+    return vertices_impl(rects, R, group_ptr, G, nullptr, 1, T, max_group, x, y, w, cap, corner_ptr, area, K_host, ws,
+                         ws_bytes, stream, nullptr, y_lo, y_hi);
 }
 
 size_t fcfs_haar_workspace_bytes(int64_t B, int32_t T) { return haar_workspace_bytes(B, T); }

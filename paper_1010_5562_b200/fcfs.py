@@ -83,6 +83,9 @@ _lib.fcfs_vertices_from_rects.restype = _i32
 _lib.fcfs_vertices_from_rects_edges.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P,
                                                 ctypes.POINTER(_i64), _P, _P, _P, _P, _P, _P, _sz, _P]
 _lib.fcfs_vertices_from_rects_edges.restype = _i32
+_lib.fcfs_vertices_from_rects_band.argtypes = [_P, _i64, _P, _i64, _i32, _i64, _i32, _i32, _P, _P, _P, _i64, _P,
+                                               _P, ctypes.POINTER(_i64), _P, _sz, _P]
+_lib.fcfs_vertices_from_rects_band.restype = _i32
 _lib.fcfs_polygons_workspace_bytes.argtypes = [_i64, _i64, _i64]
 _lib.fcfs_polygons_workspace_bytes.restype = _sz
 _lib.fcfs_vertices_from_polygons.argtypes = [_P, _P, _i64, _P, _i64, _P, _i64, _i32, _P, _P, _P, _i64, _P, _P,
@@ -131,7 +134,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
-            "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form"]
+            "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -389,6 +392,20 @@ class VerticesPlan:
                 _ptr(e["xa"]), _ptr(e["xb"]), _ptr(e["y"]), _ptr(e["c"]), _ptr(e["ecnt"]), _ptr(self.ws),
                 self.ws.numel(), _stream(stream))
         _check(st, "fcfs_vertices_from_rects")
+        self.K = K.value
+        return self.K
+
+    def run_band(self, rects, y_lo, y_hi, group_ptr=None, stream=None):
+        """One clip's corners with y_lo <= y < y_hi (fcfs_vertices_from_rects_band); self.area[0] is the
+        band's share of the area.  Needs B == 1."""
+        if self.B != 1:
+            raise FcfsError(E_INVALID, "run_band needs a single-clip plan")
+        K = ctypes.c_int64(0)
+        st = _lib.fcfs_vertices_from_rects_band(_ptr(rects), self.R, _ptr(group_ptr), self.G, self.T, self.mg,
+                                                int(y_lo), int(y_hi), _ptr(self.x), _ptr(self.y), _ptr(self.w),
+                                                self.cap, _ptr(self.corner_ptr), _ptr(self.area), ctypes.byref(K),
+                                                _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_vertices_from_rects_band")
         self.K = K.value
         return self.K
 

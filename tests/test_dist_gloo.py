@@ -57,6 +57,71 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _oracle_band(rects, group_ptr, T, y_lo, y_hi):
+    """This rank's band on CPU: the oracle's canonical list restricted to rows y_lo <= y < y_hi (what
+    fcfs_vertices_from_rects_band returns on the GPU; that kernel is checked against this rule in
+    test_gpu_parity.py)."""
+    e = oracle.extract(rects.numpy(), T, None if group_ptr is None else group_ptr.numpy())
+    sel = (e["y"] >= y_lo) & (e["y"] < y_hi)
+    x, y, w = (torch.from_numpy(np.ascontiguousarray(e[k][sel])) for k in ("x", "y", "w"))
+    area = torch.tensor([int((e["w"][sel].astype(np.int64) * e["x"][sel] * e["y"][sel]).sum())], dtype=torch.int64)
+    return x, y, w, int(sel.sum()), area
+
+
+def _worker_bands(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = inputs.c4(seed=3, n_poly=3000, T=4096, M=8)
+        rects = torch.from_numpy(wl.rects)
+        ex = fdist.BandExtract(rects.shape[0], wl.T, rank, world, extract=_oracle_band)
+        x, y, w, K, area = fdist.extract_band_sharded(rects, wl.T, extractor=ex)
+        M = N = 6
+        rs = fdist.RowsSharded(wl.T, M, N, "fp64", rank, world, device="cpu", compute=_oracle_rows)
+        rows = rs.run(x, y, w, K, area)
+        rows2 = rs.run(x, y, w, K, area)          # the plan / buffers are reused across steps
+        vs = fdist.VertexSharded(wl.T, M, N, "fp64", rank, world, device="cpu", compute=_oracle_vblock)
+        vb = vs.run(x, y, w, K)
+        q.put((rank, x.numpy(), y.numpy(), w.numpy(), K, area, rows.numpy(), rows2.numpy(), vb.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target, world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res, key=lambda t: t[0])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_band_sharded_extraction_gathers_the_canonical_list(world):
+    """y-band shards of a1 + all_gather == the single-process canonical list, bit for bit; the band
+    areas sum to the clip's; rows / vertex-block shards of the gathered list reassemble the window."""
+    res = _spawn(_worker_bands, world)
+    wl = inputs.c4(seed=3, n_poly=3000, T=4096, M=8)
+    e = oracle.extract(wl.rects, wl.T)
+    ms, ns = oracle.window(6, 6)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
+    for rank, x, y, w, K, area, rows, rows2, vb in res:
+        assert K == e["K"] and area == int(e["area"][0])
+        assert np.array_equal(x, e["x"]) and np.array_equal(y, e["y"]) and np.array_equal(w, e["w"])
+        assert np.array_equal(rows, Fr) and np.array_equal(rows2, Fr)
+        assert np.all(np.abs(vb - Fr) <= 1e-12 * B + (B == 0) * 1e-15)
+    # the bands tile the lattice rows 0..T exactly
+    for P in (1, 2, 3, 4, 8):
+        b = [fdist.band_range(wl.T, r, P) for r in range(P)]
+        assert b[0][0] == 0 and b[-1][1] == wl.T + 1 and all(b[i][1] == b[i + 1][0] for i in range(P - 1))
+
+
 def test_partition_helpers_cover_exactly():
     for world in (1, 2, 3, 4, 8):
         B = 4096

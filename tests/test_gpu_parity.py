@@ -1161,3 +1161,82 @@ def test_chop_random_sweep(fcfs, seed):
     assert g["n"] == e["n"]
     assert np.array_equal(g["rects"].cpu().numpy().reshape(-1, 4), np.asarray(e["rects"]).reshape(-1, 4))
     assert np.array_equal(g["tile_ptr"].cpu().numpy(), e["tile_ptr"])
+
+
+# ---------------------------------------------------------------------------------------------
+# multi-GPU single-clip path, emulated rank by rank on one GPU: y-band sharded extraction
+# (fcfs_vertices_from_rects_band) and per-rank rows plans (dist.RowsSharded)
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["c4small", "c2small", "maxT"])
+def test_band_extraction_concatenates_to_the_canonical_list(fcfs, case):
+    from paper_1010_5562_b200 import dist as fdist
+    if case == "c4small":
+        wl = inputs.c4(seed=7, n_poly=20000, T=65536, M=8)
+    elif case == "c2small":
+        wl = inputs.c2(seed=7, n_poly=300, T=4096)
+    else:   # the largest T: rects touching y = 0 and y = T (the last band holds row T)
+        rng = np.random.default_rng(11)
+        T = 1 << 20
+        x0 = rng.integers(0, T - 10, 3000); y0 = rng.integers(0, T - 10, 3000)
+        r = np.stack([x0, y0, np.minimum(x0 + rng.integers(1, 5000, 3000), T),
+                      np.minimum(y0 + rng.integers(1, 5000, 3000), T)], 1).astype(np.int32)
+        r[:3] = [[0, 0, 7, T], [5, T - 3, T, T], [T - 9, 0, T, 1]]
+        wl = inputs.Workload("maxT", T, 4, 4, -1.0, r, None, None, ("fp64",))
+    e = oracle.extract(wl.rects, wl.T, wl.group_ptr)
+    rects = torch.from_numpy(wl.rects).cuda()
+    gp = None if wl.group_ptr is None else torch.from_numpy(wl.group_ptr).cuda()
+    G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
+    mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
+    for P in (1, 2, 3, 5, 8):
+        xs, ys, ws, area = [], [], [], 0
+        for rank in range(P):
+            ex = fdist.BandExtract(wl.R, wl.T, rank, P, G=G, max_group=mg, grouped=gp is not None)
+            x, y, w, K, a = ex.run(rects, gp)
+            yy = y[:K].cpu().numpy()
+            lo, hi = ex.band
+            assert K == 0 or (yy.min() >= lo and yy.max() < hi)
+            xs.append(x[:K].cpu().numpy()); ys.append(yy); ws.append(w[:K].cpu().numpy())
+            area += int(a[0].item())
+        assert np.array_equal(np.concatenate(xs), e["x"]), P
+        assert np.array_equal(np.concatenate(ys), e["y"]), P
+        assert np.array_equal(np.concatenate(ws), e["w"]), P
+        assert area == int(e["area"][0]), P
+
+
+def test_band_rejects_bad_band(fcfs):
+    vp = fcfs.VerticesPlan(4, 64, device="cuda")
+    rects = torch.tensor([[0, 0, 8, 8]] * 4, dtype=torch.int32, device="cuda")
+    with pytest.raises(fcfs.FcfsError):
+        vp.run_band(rects, 10, 5)
+    with pytest.raises(fcfs.FcfsError):
+        vp.run_band(rects, -1, 5)
+    assert vp.run_band(rects, 3, 3) == 0          # an empty band is valid: no corners
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_rows_sharded_plans_reassemble_the_window(fcfs, prec):
+    """Each emulated rank's RowsSharded plan (fcfs_shard ROWS, built once, run twice) gives its rows of
+    the oracle window; the rank-ordered concatenation is the full window."""
+    from paper_1010_5562_b200 import dist as fdist
+    wl = inputs.c4(seed=2, n_poly=4000, T=65536, M=8)
+    g = _gpu_extract(fcfs, wl)
+    K = g["K"]
+    M = N = 12
+    ms, ns = oracle.window(M, N)
+    e = oracle.extract(wl.rects, wl.T)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
+    tol = 1e-12 if prec == "fp64" else 1e-5
+    P = 3
+    parts = []
+    for rank in range(P):
+        rs = fdist.RowsSharded(wl.T, M, N, prec, rank, P, device="cuda")
+        loc = rs._local(g["x"], g["y"], g["w"], K, int(g["area"][0]))
+        loc2 = rs._local(g["x"], g["y"], g["w"], K, int(g["area"][0]))
+        torch.cuda.synchronize()
+        assert len(rs.plans) == 1
+        parts.append(loc2.cpu().numpy().copy())
+        assert np.array_equal(loc.cpu().numpy(), parts[-1])
+    F = np.concatenate(parts)
+    err = np.abs(F.astype(np.complex128) - Fr)
+    assert np.all(err <= tol * B + (B == 0) * 1e-7)
