@@ -9,6 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfcfs.so")
+CHECKED_LIB = os.path.join(HERE, "libfcfs_checked.so")
 SOURCES = ["fcfs_abi.cu", "extract.cu", "buckets.cu", "contract_fp64.cu", "contract_tf32.cu", "epilogue.cu", "fft_route.cu", "chop.cu", "haar.cu", "edges.cu", "lattice.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -24,8 +25,13 @@ def _stale(obj, src):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, extra=()) -> str:
-    objdir = os.path.join(HERE, "build_obj")
+def build(verbose: bool = False, extra=(), checked: bool = False) -> str:
+    """libfcfs.so; checked=True builds libfcfs_checked.so instead: the same sources with -DFCFS_CHECKED
+    (device-side FCFS_DCHECK invariants, common.cuh), for tests only."""
+    lib = CHECKED_LIB if checked else LIB
+    if checked:
+        extra = (*extra, "-DFCFS_CHECKED")
+    objdir = os.path.join(HERE, "build_obj_checked" if checked else "build_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -45,13 +51,13 @@ def build(verbose: bool = False, extra=()) -> str:
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    if procs or not os.path.exists(LIB):
-        tmp = LIB + f".tmp{os.getpid()}"
+    if procs or not os.path.exists(lib):
+        tmp = lib + f".tmp{os.getpid()}"
         subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
                                "-cudart", "static"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    print(build(verbose=True, checked="--checked" in sys.argv))

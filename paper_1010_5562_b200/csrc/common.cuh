@@ -1,6 +1,7 @@
 // common.cuh — internal helpers of libfcfs.so (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "../../include/fcfs.h"
@@ -42,6 +43,23 @@ struct StageScope {
         cudaError_t _e = cudaGetLastError();                     \
         if (_e != cudaSuccess) return fcfs::cuda_status(_e, name); \
     } while (0)
+
+// ---- device-side invariant checks of the checked build (libfcfs_checked.so, -DFCFS_CHECKED):
+// index / address / protocol invariants of the hand-written kernels; a violation prints the site and
+// traps (the launch then fails with cudaErrorLaunchFailure -> FCFS_E_CUDA).  Compiled out of
+// libfcfs.so.  compute-sanitizer is closed on this GPU pool; this build is the bounds check instead.
+#ifdef FCFS_CHECKED
+#define FCFS_DCHECK(cond)                                                                              \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("FCFS_DCHECK failed: %s at %s:%d block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define FCFS_DCHECK(cond) ((void)0)
+#endif
 
 // ---- workspace carving (256-byte aligned bump allocator) ---------------------------------
 struct Carver {

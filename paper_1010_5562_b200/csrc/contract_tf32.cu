@@ -638,6 +638,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                 fetch(kr0);
                 for (int64_t ks = c0; ks < c1; ks += kBKp, ++sc) {
                     const int my_slot = slot;
+                    FCFS_DCHECK(my_slot >= 0 && my_slot < kS && n >= 1 && n <= kChunk);
                     const uint32_t my_ph = ph;
                     if (++slot == kS) { slot = 0; ph ^= 1; }
                     if ((int)(sc & 3) != gq) continue;
@@ -739,6 +740,7 @@ k_gemm_tf32(CornerSrc src, GemmPlan plan, TabGeom g, double *__restrict__ P_ws, 
                         const int two = (kPer == 2 && st + 1 < nst) ? 1 : 0;
                         const int s1 = (stage + 1 == kS) ? 0 : stage + 1;
                         const uint32_t p1 = (stage + 1 == kS) ? phase_bit ^ 1 : phase_bit;
+                        FCFS_DCHECK(stage >= 0 && stage < kS && s1 >= 0 && s1 < kS && nst >= 1);
                         mbar_wait(FULL(stage), phase_bit, ABL(64));
                         if (two) mbar_wait(FULL(s1), p1, ABL(64));
                         if (lane == 0) trace(tr, 50, msc);

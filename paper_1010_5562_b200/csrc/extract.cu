@@ -665,9 +665,11 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             if (!rok[j]) continue;
             const int4 q = rq[j];
             int p = atomicAdd(&hist[q.y], 2);
+            FCFS_DCHECK(p >= 0 && p + 1 < kCap);
             bxw[p] = ((uint32_t)q.x << 16) | 0x0001u;       by[p] = (int16_t)q.y;
             bxw[p + 1] = ((uint32_t)q.z << 16) | 0xFFFFu;   by[p + 1] = (int16_t)q.y;
             p = atomicAdd(&hist[q.w], 2);
+            FCFS_DCHECK(p >= 0 && p + 1 < kCap);
             bxw[p] = ((uint32_t)q.x << 16) | 0xFFFFu;       by[p] = (int16_t)q.w;
             bxw[p + 1] = ((uint32_t)q.z << 16) | 0x0001u;   by[p + 1] = (int16_t)q.w;
         }

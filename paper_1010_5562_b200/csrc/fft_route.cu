@@ -243,6 +243,7 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
                 }
             }
         };
+        FCFS_DCHECK(yv >= 0 && yv < g.T && yptr[yv] <= yptr[yv + 1]);
         run(yptr[yv], yptr[yv + 1]);   // the y = T run (phase of row 0) is added by k_fr_rowsT
 #pragma unroll
         for (int j = 0; j < kRowsPerThread; ++j) {
@@ -434,6 +435,7 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
     }
     __syncthreads();
     const uint32_t bytes = (uint32_t)(g.T2 * sizeof(V)), pbytes = (uint32_t)g.T2 * 2u;
+    FCFS_DCHECK(((su32(buf) | su32(pv)) & 15u) == 0 && (bytes & 15u) == 0 && (pbytes & 15u) == 0);
     double2 ax = make_double2(0.0, 0.0);
     const uint32_t maskT = (uint32_t)g.T - 1u;
     const int lead = g.t2bits & 3;
@@ -466,6 +468,7 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
         // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
         for (int o = threadIdx.x; o < nn; o += kThreads) {
             const int n = o - N;
+            FCFS_DCHECK(pad(n >= 0 ? n : n + g.T2) < LP && (n >= 0 ? n : n + g.T2) < g.T2);
             const V z = buf[pad(n >= 0 ? n : n + g.T2)];
             const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
             X[o] = cadd(X[o], to_d(cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z)));

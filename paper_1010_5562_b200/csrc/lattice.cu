@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 const uint32_t us_ = second ? uses1 : uses0;
                 if (second) ++uses1; else ++uses0;
                 const uint32_t ca = bound(t, false), cb = bound(t, true);
+                FCFS_DCHECK(ca <= cb && (!real || (int64_t)cb <= A.corner_ptr[clip + 1] - k0));
                 // stage s is free once the MMAs of its previous chunk have completed: park on the named barrier
                 // the MMA warp arrives at after issuing them (a hardware wait), then confirm the completion on
                 // the commit's mbarrier
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                         else if (x <= T34) { u = x - T2; fs = -1.f; cq = 1.f; }
                         else { u = T - x; ss = -1.f; cq = 2.f; }
                         const uint32_t a = tabaddr + (uint32_t)u * rowb;
+                        FCFS_DCHECK(!ok || (u >= 0 && u <= T4 && yy >= y0 && yy < y0 + kYC));
                         const float wf = (float)w;
                         const uint32_t wodd = bf16_bits(wf) | (bf16_bits(wf * ss) << 16);            // even m
                         const uint32_t wevn = bf16_bits(wf * fs) | (bf16_bits(wf * ss * fs) << 16);   // odd m
@@ -367,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                         sts64u(stg + kRec * lane + 8u, a, wodd);
                         sts64u(stg + kRec * lane + 16u, a, wax);
                         lastmask = __reduce_or_sync(0xffffffffu, last ? (1u << lane) : 0u);
+                        FCFS_DCHECK(n >= 1 && n <= 32);
                         sts32(fcl + 4u * lane, 2u * (uint32_t)(yy - y0));   // the row's (hi, lo) column pair
                     }
                     __syncwarp();
@@ -375,8 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                         const uint2 r = lds64u(recl + kRec * i);
                         const float2 v = lds64(r.x + lane8);
                         acc = ffma2(v, make_float2(__uint_as_float(r.y << 16), __uint_as_float(r.y & 0xFFFF0000u)), acc);
+                        FCFS_DCHECK(r.x >= tabaddr && r.x + lane8 + 8u <= sbase + L.stage);
                         if ((lastmask >> i) & 1u) {   // row end: its (hi, lo) pairs into the row's columns
                             const uint32_t col = lds32(fcl + 4u * i);
+                            FCFS_DCHECK(col < 2u * kYC);
                             uint32_t h, l, h2, l2;
                             split_hl(acc.x, h, l);
                             split_hl(acc.y, h2, l2);
@@ -403,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             for (int j = 0; j < nch; ++j, ++gc) {
                 const int s = j & (kAS - 1);
                 const int b = (int)(gc % kBS);
+                FCFS_DCHECK(s >= 0 && s < kAS && b >= 0 && b < kBS);
                 mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
                 named_bar(kBarFull + s, 32 + 4 * 32);       // the 4 producer warps of the chunk have filled it
                 tc_fence_after();
@@ -519,6 +525,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 const int32_t op = row ? rowoff[ea.M + m] + nm : (ax ? rowoff[ea.M] + nm : 0);
                 const int32_t on = row ? rowoff[ea.M - m] + nm : 0;
                 const double mm = (double)m * (double)m;
+                FCFS_DCHECK(nm < 0 || (op - nm >= 0 && op + nm < ea.out_per_clip &&
+                                       (!row || (on - nm >= 0 && on + nm < ea.out_per_clip))));
                 {
                     uint32_t a1[1], a2[1];
                     tmem_ld1(sc_ + 31u, a1);

@@ -16,10 +16,12 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfcfs.so")
+# FCFS_LIBRARY (tests only) selects another build of the same ABI, e.g. libfcfs_checked.so (the
+# device-side invariant checks of tools/checked_run.sh); the default is the in-tree libfcfs.so.
+LIB_PATH = os.environ.get("FCFS_LIBRARY") or os.path.join(_HERE, "libfcfs.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libfcfs.so not found at {LIB_PATH}: build it with "
+    raise ImportError(f"{os.path.basename(LIB_PATH)} not found at {LIB_PATH}: build it with "
                       "`python -m paper_1010_5562_b200.build` (no CPU fallback exists)")
 
 _lib = ctypes.CDLL(LIB_PATH)
