@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
     ap.add_argument("--e2e-split", type=int, default=8, help="sub-batches of the pipelined end-to-end measurement")
+    ap.add_argument("--no-small", action="store_true",
+                    help="small single clips (c1): the general extraction + coefficient path instead of the "
+                         "one-launch fcfs_small_clip latency path replayed as a CUDA graph")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the extra lines (c4 / c5 FP64, c4 split-TF32) of the default c3 run")
     return ap.parse_args()
@@ -498,7 +501,24 @@ def main():
     cp = None if wl.clip_ptr is None else torch.from_numpy(wl.clip_ptr).to(dev)
     mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
     G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
-    if args.config == "layout":
+    small = None
+    if (wl.B == 1 and world == 1 and args.input == "rects" and args.config != "layout" and not args.no_small
+            and fcfs.SmallClipPlan.supported(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, G, mg)):
+        # latency path: a1-a5 in one kernel launch with no host sync (fcfs_small_clip), the step
+        # captured once in a CUDA graph and replayed
+        small = fcfs.SmallClipPlan(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, prec, G=G, max_group=mg, device=dev)
+        small.run(rects, gp)
+        torch.cuda.synchronize()
+        K_small = small.check()
+        g_stream = torch.cuda.Stream(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=g_stream):
+            small.run(rects, gp, stream=g_stream)
+        vp = None
+
+        def extract():
+            return K_small
+    elif args.config == "layout":
         # layout -> tiles on the GPU, then the tiles' corners as one batch
         lay = wl.layout
         chop = fcfs.ChopPlan(wl.R, wl.T, lay.tiles_x, lay.tiles_y, device=dev)
@@ -538,7 +558,14 @@ def main():
     K = extract()
     cptr_h = vp.corner_ptr.cpu().numpy() if vp is not None else np.array([0, K], np.int64)
     kmax = int(np.diff(cptr_h).max()) if wl.B > 0 else 0
-    if wl.B > 1:
+    if small is not None:
+        plan = small
+
+        def coeffs():
+            graph.replay()
+            return small.out
+        out_bytes = small.out.numel() * small.out.element_size()
+    elif wl.B > 1:
         plan = fcfs.BatchedPlan(wl.B, K, kmax, wl.T, wl.M, wl.N, wl.r2, layout, prec, device=dev, form=args.form,
                                 sorted_y=True)   # corners from fcfs_vertices_from_* are y-sorted per clip
 
@@ -624,9 +651,27 @@ def main():
     peaks, src = load_peaks()
     c_ms, c_n = stages["contract"]
     c_ms_launch = c_ms / max(c_n, 1)
-    fft_route = (wl.B == 1 and world == 1 and
+    fft_route = (small is None and wl.B == 1 and world == 1 and
                  fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, route=args.route) == 1)
-    if fft_route:
+    if small is not None:
+        # one kernel per step (a graph of one launch): its time is the step's; algorithmic work = the
+        # direct sums over the half window, one complex MAC (8 flop) per (output, corner)
+        c_ms_launch = ms_per_step
+        alg_flops = 8.0 * (W / 2.0) * K
+        achieved = alg_flops / (c_ms_launch / 1e3) / 1e12
+        clocks = clk.summary()
+        try:
+            peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dfma_tflops"]
+            peak_note = "FP64 CUDA-core DFMA measured by tools/fp64_peak.cu (profiles/fp64_peak.json)"
+        except Exception:
+            mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = 148 * 64 * 2 * mhz * 1e6 / 1e12
+            peak_note = f"FP64 DFMA derived: 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz"
+        peak_note += "; latency-bound (one launch per step, the whole clip in every CTA's shared memory)"
+        bound = "alu"
+        k_inner = "canonical corners (direct sums, fcfs_small_clip)"
+        Kc = np.array([float(K)])
+    elif fft_route:
         # lattice-FFT route (NEXT-2, FP64 or FP32 CUDA cores): algorithmic work of the contract stage =
         # G rows (one complex rotation + real-weighted complex MAC per corner and row: 10 flop) +
         # the T1 length-T2 FFTs per row (5 T2 log2 T2) + the outer twiddled sum (8 flop per n and y1)
@@ -701,7 +746,8 @@ def main():
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else
                                    ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else "")),
-            "kernel": (f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
+            "kernel": ("k_small_clip (a1-a5 in one launch, CUDA graph replay)" if small is not None else
+                       f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
                        if fft_route else ("contract stage (lattice-row form: k_lat_btab + k_lat_cptr + k_lattice)"
                                           if getattr(plan, "form", 0) == fcfs.FORM_LATTICE else "k_gemm_" + prec)),
             "k_inner": f"{k_inner}: {int(Kc.sum())}",
@@ -798,7 +844,7 @@ def main():
         line = {"metric": "fourier_coeff_vertex_terms_per_sec", "value": round(value, 3), "unit": "Gterm/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
                 "higher_is_better": True, "scaling": "strong" if single_sharded else "weak", "vs_baseline": None,
-                "dtype": ("f64" if prec == "fp64" else
+                "dtype": ("f64" if (prec == "fp64" or small is not None) else
                           "f32 (lattice-FFT route on FP32 CUDA cores, FP64 outer sums; the split-precision contract)"
                           if fft_route else
                           "tf32x3 (split-TF32, FP32-accurate; FP64 flush)" if prec == "tf32x3" else

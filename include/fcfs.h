@@ -303,6 +303,28 @@ fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int6
                                       size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Latency path for ONE SMALL CLIP: a1-a5 in a single kernel launch with NO host synchronisation
+ * (capturable in a CUDA graph) — the paper's "only a few CFS coefficients" regime, evaluated term
+ * by term (Goertzel-like) with the exact integer phase.  Every CTA extracts
+ * the clip's canonical corners in shared memory (as fcfs_vertices_from_rects: unions within groups,
+ * groups summed) and computes its rows of the half window (Eqs. Fkl / Fk0 / F0l / Fdc),
+ * mirrored by conjugation.  Arithmetic is FP64 for every `prec` (the split precisions only select
+ * complex64 output), so the result meets the FP64 contract (1e-12 B).
+ *
+ * rects, R, group_ptr, G, T, max_group: as fcfs_vertices_from_rects with clip_ptr = NULL (B = 1).
+ * win        window / pupil, output layout as fcfs_coeffs (F: complex128 for FCFS_FP64, else complex64).
+ * K_dev      int64 [1] device out (canonical corner count) or NULL.
+ * status_dev int32 [1] device out: FCFS_OK, FCFS_E_RANGE (a bad rect) or FCFS_E_UNSUPPORTED (a group
+ *            above max_group / more than 2048 raw corners), written by the kernel — the call itself
+ *            does not synchronise, so read it after the stream's work completes.
+ * Limits (host-checked, FCFS_E_UNSUPPORTED): T <= 8192, M <= 63, N <= 4096, max_group <= 100, 4 R <= 2048 for
+ * singleton groups.  fcfs_small_clip_supported() answers the same question (1 / 0). */
+int32_t fcfs_small_clip_supported(int64_t R, int64_t G, int32_t T, int64_t max_group, const fcfs_window *win);
+fcfs_status fcfs_small_clip(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                            int32_t T, int64_t max_group, const fcfs_window *win, fcfs_precision prec,
+                            void *F, int64_t *K_dev, int32_t *status_dev, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * Row buckets of a corner list — the row structure of Step 4: corners on one row
  * y share E_y[n, y], so sum_k w_k E_x[m,k] E_y[n,k] = sum_b E_y[n, y_b] sum_{k in b} w_k E_x[m,k]
  * and the FP64 contraction runs over buckets instead of corners.  fcfs_coeffs[_batched] compute

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfcfs.so")
 CHECKED_LIB = os.path.join(HERE, "libfcfs_checked.so")
-SOURCES = ["fcfs_abi.cu", "extract.cu", "buckets.cu", "contract_fp64.cu", "contract_tf32.cu", "epilogue.cu", "fft_route.cu", "chop.cu", "haar.cu", "edges.cu", "lattice.cu"]
+SOURCES = ["fcfs_abi.cu", "extract.cu", "buckets.cu", "contract_fp64.cu", "contract_tf32.cu", "epilogue.cu", "fft_route.cu", "chop.cu", "haar.cu", "edges.cu", "lattice.cu", "small.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]

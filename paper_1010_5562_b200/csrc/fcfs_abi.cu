@@ -79,6 +79,11 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                     int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo = 0,
                     int32_t y_hi = 0x7fffffff);
+size_t small_clip_smem_bytes(int32_t T, int64_t max_group);
+bool small_clip_eligible(int64_t R, int64_t G, int32_t T, int64_t max_group, int32_t M, int32_t N, bool grouped);
+fcfs_status launch_small_clip(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G, int32_t T,
+                              int64_t max_group, const fcfs_window &win, int32_t out_f32, void *F, int64_t *K_dev,
+                              int32_t *status_dev, cudaStream_t s);
 size_t extract_polygons_workspace_bytes(int64_t V, int64_t B);
 fcfs_status extract_polygons(const int32_t *vx, const int32_t *vy, int64_t V, const int64_t *poly_ptr, int64_t P,
                              const int64_t *clip_ptr, int64_t B, int32_t T, int32_t *x, int32_t *y, int32_t *w,
@@ -570,6 +575,35 @@ int32_t fcfs_coeffs_route(int64_t K, int32_t T, const fcfs_window *win, fcfs_pre
     if (shard && shard->kind == FCFS_SHARD_VERTEX_BLOCK) k = shard->k_hi - shard->k_lo;
     FftPlan fp;
     return fft_route_plan(T, win->M, win->N, m_lo, m_hi, k, prec != FCFS_FP64, fp, opt->route) ? 1 : 0;
+}
+
+int32_t fcfs_small_clip_supported(int64_t R, int64_t G, int32_t T, int64_t max_group, const fcfs_window *win) {
+    if (!valid_T(T) || R < 0 || !win || check_window(win) != FCFS_OK) return 0;
+    return small_clip_eligible(R, G, T, max_group, win->M, win->N, G != R || max_group > 1) ? 1 : 0;
+}
+
+fcfs_status fcfs_small_clip(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G, int32_t T,
+                            int64_t max_group, const fcfs_window *win, fcfs_precision prec, void *F, int64_t *K_dev,
+                            int32_t *status_dev, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    fcfs_status st = check_window(win);
+    if (st != FCFS_OK) return st;
+    if (R < 0 || (R > 0 && !rects) || !F || !status_dev || (group_ptr == nullptr && G != R) || G < 0) {
+        set_error("fcfs_small_clip: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    const int64_t mg = group_ptr == nullptr ? 1 : max_group;
+    if (!small_clip_eligible(R, G, T, mg, win->M, win->N, group_ptr != nullptr)) {
+        set_error("fcfs_small_clip: outside the small-clip limits (T <= 8192, M <= 63, N <= 4096, groups <= 100 rects, "
+                  "<= 2048 raw corners)");
+        return FCFS_E_UNSUPPORTED;
+    }
+    st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageContract, (cudaStream_t)stream);
+    return launch_small_clip(rects, R, group_ptr, G, T, mg, *win, prec != FCFS_FP64, F, K_dev, status_dev,
+                             (cudaStream_t)stream);
 }
 
 fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,

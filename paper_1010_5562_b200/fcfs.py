@@ -122,6 +122,11 @@ _lib.fcfs_row_buckets_workspace_bytes.restype = _sz
 _lib.fcfs_row_buckets.argtypes = [_P, _P, _i64, _i64, _i32, _P, _P, _P, ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_row_buckets.restype = _i32
 
+_lib.fcfs_small_clip_supported.argtypes = [_i64, _i64, _i32, _i64, _WP]
+_lib.fcfs_small_clip_supported.restype = _i32
+_lib.fcfs_small_clip.argtypes = [_P, _i64, _P, _i64, _i32, _i64, _WP, _i32, _P, _P, _P, _P]
+_lib.fcfs_small_clip.restype = _i32
+
 _lib.fcfs_profile_enable.argtypes = [_i32]
 _lib.fcfs_profile_enable.restype = _i32
 _lib.fcfs_profile_read.argtypes = [_P, _P, _i32]
@@ -136,7 +141,8 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_row_buckets", "fcfs_polygons_workspace_bytes", "fcfs_vertices_from_polygons",
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
-            "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band"]
+            "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band",
+            "fcfs_small_clip_supported", "fcfs_small_clip"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -459,6 +465,40 @@ def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=N
     """a2-a5 for one clip.  Returns complex128 (fp64) or complex64 (tf32x3) cuda tensor."""
     plan = CoeffsPlan(x.shape[0], T, M, N, r2, layout, prec, shard, device=x.device, route=route)
     return plan.run(x, y, w, area, stream=stream)
+
+
+class SmallClipPlan:
+    """fcfs_small_clip: a1-a5 of one small clip in one kernel launch, no host synchronisation (the step
+    can be captured in a CUDA graph).  ``status`` / ``K`` are device tensors written by the kernel."""
+
+    def __init__(self, R, T, M, N, r2=-1.0, layout="dense", prec="fp64", G=None, max_group=1, device="cuda"):
+        self.R, self.T, self.prec = int(R), int(T), _PREC[prec]
+        self.G = self.R if G is None else int(G)
+        self.mg = max(int(max_group), 1)
+        self.win = make_window(M, N, r2, layout)
+        self.out = torch.empty(window_size(M, N, r2, layout), dtype=_out_dtype(prec), device=device)
+        self.K = torch.zeros(1, dtype=torch.int64, device=device)
+        self.status = torch.full((1,), -1, dtype=torch.int32, device=device)
+
+    @staticmethod
+    def supported(R, T, M, N, r2=-1.0, layout="dense", G=None, max_group=1):
+        win = make_window(M, N, r2, layout)
+        return bool(_lib.fcfs_small_clip_supported(int(R), int(R if G is None else G), int(T), int(max_group),
+                                                   ctypes.byref(win)))
+
+    def run(self, rects, group_ptr=None, stream=None):
+        st = _lib.fcfs_small_clip(_ptr(rects), self.R, _ptr(group_ptr), self.G, self.T, self.mg,
+                                  ctypes.byref(self.win), self.prec, _ptr(self.out), _ptr(self.K),
+                                  _ptr(self.status), _stream(stream))
+        _check(st, "fcfs_small_clip")
+        return self.out
+
+    def check(self):
+        """After the stream's work completed: raise if the kernel reported an error."""
+        st = int(self.status.item())
+        if st != FCFS_OK:
+            raise FcfsError(st, "fcfs_small_clip (device status)")
+        return int(self.K.item())
 
 
 class BatchedPlan:

@@ -1240,3 +1240,93 @@ def test_rows_sharded_plans_reassemble_the_window(fcfs, prec):
     F = np.concatenate(parts)
     err = np.abs(F.astype(np.complex128) - Fr)
     assert np.all(err <= tol * B + (B == 0) * 1e-7)
+
+
+# ---------------------------------------------------------------------------------------------
+# latency path: fcfs_small_clip (a1-a5 in one launch, no host sync, CUDA-graph capturable)
+# ---------------------------------------------------------------------------------------------
+
+def _small_case(name):
+    if name == "c1":
+        return inputs.c1(seed=0)
+    if name == "c1s3":
+        return inputs.c1(seed=3, T=3000, n_rects=90, M=20)         # T not a power of two
+    if name == "singleton":
+        rng = np.random.default_rng(4)
+        r = inputs.random_rects(rng, 300, 8192, 4, 900)
+        return inputs.Workload("singleton", 8192, 63, 40, -1.0, r, None, None, ("fp64",))
+    if name == "pupil":
+        w3 = inputs.c3(seed=1, clips=1, n_lines=120)
+        return inputs.Workload("pupil", w3.T, w3.M, w3.N, w3.r2, w3.rects, None, None, ("tf32x3",))
+    if name == "tiny":
+        r = np.array([[0, 0, 1, 1], [3, 4, 7, 9]], np.int32)
+        return inputs.Workload("tiny", 16, 5, 3, -1.0, r, np.array([0, 1, 2], np.int64), None, ("fp64",))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["c1", "c1s3", "singleton", "pupil", "tiny"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_small_clip_matches_oracle(fcfs, name, prec):
+    wl = _small_case(name)
+    layout = "pupil" if wl.r2 >= 0 else "dense"
+    gp = wl.group_ptr
+    G = wl.R if gp is None else len(gp) - 1
+    mg = 1 if gp is None else int(np.diff(gp).max())
+    assert fcfs.SmallClipPlan.supported(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, G, mg)
+    plan = fcfs.SmallClipPlan(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, prec, G=G, max_group=mg)
+    F = plan.run(torch.from_numpy(wl.rects).cuda(), None if gp is None else torch.from_numpy(gp).cuda())
+    torch.cuda.synchronize()
+    e = oracle.extract(wl.rects, wl.T, gp)
+    assert plan.check() == e["K"]
+    ms, ns = oracle.window(wl.M, wl.N, wl.r2)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
+    Fg = F.cpu().numpy().astype(np.complex128)
+    tol = 1e-12 if prec == "fp64" else 1e-5
+    err = np.abs(Fg - Fr)
+    # B == 0 only at the DC, which is exact in FP64 and rounded once to complex64 otherwise
+    zero_tol = 1e-15 if prec == "fp64" else 1e-7 * np.abs(Fr)
+    assert np.all(err <= tol * B + (B == 0) * zero_tol), np.max(err / np.maximum(B, 1e-300))
+    # the conjugate mirror is exact: F[-m, -n] == conj F[m, n]
+    idx = {(int(m), int(n)): i for i, (m, n) in enumerate(zip(ms, ns))}
+    Fc = F.cpu().numpy()
+    for i, (m, n) in enumerate(zip(ms, ns)):
+        j = idx[(-int(m), -int(n))]
+        assert Fc[j] == np.conj(Fc[i])
+    if prec == "fp64":
+        assert Fc[idx[(0, 0)]].real == float(e["area"][0]) / (wl.T * wl.T)
+
+
+def test_small_clip_graph_replay_and_status(fcfs):
+    """The step is one launch with no host sync: capture it in a CUDA graph and replay it on new rects
+    written into the same input buffer; device status reports a bad rect; host limits are enforced."""
+    wl = inputs.c1(seed=0)
+    w2 = inputs.c1(seed=9)
+    assert wl.R == w2.R and len(wl.group_ptr) == len(w2.group_ptr)
+    rects = torch.from_numpy(wl.rects).cuda()
+    gp = torch.from_numpy(wl.group_ptr).cuda()
+    plan = fcfs.SmallClipPlan(wl.R, wl.T, wl.M, wl.N, prec="fp64", G=1, max_group=wl.R)
+    plan.run(rects, gp)                       # warm up (smem attribute, module load) outside the capture
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(rects, gp, stream=s)
+    for src in (w2, wl):
+        rects.copy_(torch.from_numpy(src.rects))
+        g.replay()
+        torch.cuda.synchronize()
+        e = oracle.extract(src.rects, src.T, src.group_ptr)
+        assert plan.check() == e["K"]
+        ms, ns = oracle.window(src.M, src.N)
+        Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], src.T, ms, ns)
+        assert np.all(np.abs(plan.out.cpu().numpy() - Fr) <= 1e-12 * B + (B == 0) * 1e-15)
+    bad = torch.from_numpy(wl.rects).cuda()
+    bad[3] = torch.tensor([5, 5, 5, 9])      # empty rect
+    plan.run(bad, gp)
+    torch.cuda.synchronize()
+    with pytest.raises(fcfs.FcfsError):
+        plan.check()
+    assert not fcfs.SmallClipPlan.supported(10, 9000, 8, 8)                 # T > 8192
+    assert not fcfs.SmallClipPlan.supported(600, 1024, 8, 8)                # 2400 raw corners
+    with pytest.raises(fcfs.FcfsError):
+        fcfs.SmallClipPlan(600, 1024, 8, 8).run(torch.zeros((600, 4), dtype=torch.int32, device="cuda"))
