@@ -18,6 +18,7 @@
 // Batched clips of singleton groups take the per-clip paths below (one CTA per clip, SMEM sort,
 // look-back offsets, direct output) instead.
 #include <cub/cub.cuh>
+#include <utility>
 
 #include "common.cuh"
 
@@ -287,16 +288,37 @@ __global__ void k_fill_sentinel(unsigned long long *keys, int32_t *wts, int64_t 
     }
 }
 
-// y-band of one clip (fcfs_vertices_from_rects_band): raw corners with y outside [y_lo, y_hi) become
-// sentinels of weight 0 before the sort.  A canonical corner is a sum over raw corners of one (x, y)
-// key, so the band's canonical corners are exactly the unbanded ones with y in the band.
-__global__ void k_band_filter(unsigned long long *keys, int32_t *wts, int64_t n, int cb, int32_t y_lo, int32_t y_hi) {
+// y-band of one clip (fcfs_vertices_from_rects_band): the raw corners with y in [y_lo, y_hi) are
+// compacted (warp-aggregated append, any order: the sort follows) so that the sort and merge run over
+// the band's share only.  A canonical corner is a sum over the raw corners of one (x, y) key, so the
+// band's canonical corners are exactly the unbanded ones with y in the band.
+__global__ void k_band_compact(const unsigned long long *__restrict__ keys, const int32_t *__restrict__ wts, int64_t n,
+                               int cb, int32_t y_lo, int32_t y_hi, unsigned long long *okeys, int32_t *owts,
+                               unsigned long long *count) {
     const unsigned long long mask = (1ull << cb) - 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
-        if (k == kSentinel) continue;
-        const int32_t yy = (int32_t)((k >> cb) & mask);
-        if (yy < y_lo || yy >= y_hi) { keys[i] = kSentinel; wts[i] = 0; }
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const int64_t i = i0 + lane;
+        bool keep = false;
+        unsigned long long k = kSentinel;
+        int32_t wv = 0;
+        if (i < n) {
+            k = keys[i];
+            wv = wts[i];
+            const int32_t yy = (int32_t)((k >> cb) & mask);
+            keep = k != kSentinel && wv != 0 && yy >= y_lo && yy < y_hi;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (m == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+            const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+            okeys[slot] = k;
+            owts[slot] = wv;
+        }
     }
 }
 
@@ -1057,10 +1079,27 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
         FCFS_CHECK_LAUNCH("k_fill_sentinel");
     }
     if (band) {
+        // compact the band's raw corners into keys_b / w_b, then sort only those (one extra host read of
+        // the count: the sort sizes are host-side)
+        unsigned long long *cnt = (unsigned long long *)W.K;
+        FCFS_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
         int64_t blocks = (cap_raw + threads - 1) / threads;
         if (blocks > 148 * 16) blocks = 148 * 16;
-        k_band_filter<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, cap_raw, cb, y_lo, y_hi);
-        FCFS_CHECK_LAUNCH("k_band_filter");
+        k_band_compact<<<(unsigned)blocks, threads, 0, s>>>(W.keys_a, W.w_a, cap_raw, cb, y_lo, y_hi, W.keys_b,
+                                                            W.w_b, cnt);
+        FCFS_CHECK_LAUNCH("k_band_compact");
+        unsigned long long nb = 0;
+        FCFS_TRY_CUDA(cudaMemcpyAsync(&nb, cnt, sizeof(nb), cudaMemcpyDeviceToHost, s));
+        FCFS_TRY_CUDA(cudaStreamSynchronize(s));
+        if (nb == 0) {   // an empty band: one sentinel so the tail runs on a non-empty list
+            k_fill_sentinel<<<1, 32, 0, s>>>(W.keys_b, W.w_b, 1, nullptr);
+            FCFS_CHECK_LAUNCH("k_fill_sentinel");
+            nb = 1;
+        }
+        std::swap(W.keys_a, W.keys_b);
+        std::swap(W.w_a, W.w_b);
+        cap_raw = (int64_t)nb;
+        FCFS_TRY_CUDA(cudaMemsetAsync(W.num_runs, 0, 2 * sizeof(int64_t), s));
     }
     int64_t Kh = 0;
     int32_t errh = 0;
