@@ -36,10 +36,10 @@ using namespace fcfs::tc;
 
 constexpr int kYC = 16;                     // lattice rows per chunk
 constexpr int kClips = 4;                   // clips per work item: clip q on TMEM lanes 32q .. 32q+31
-constexpr int kAS = 4;                      // A stages in TMEM (64 columns each); chunk j uses stage j % 4,
+constexpr int kAS = 6;                      // A stages in TMEM (64 columns each); chunk j uses stage j % 6,
                                             // so each producer warp ping-pongs between two stages
-constexpr int kBS = 4;                      // B chunk ring in SMEM
-constexpr int kPW = 4;                      // producer warps per sub-partition
+constexpr int kBS = 4;                      // B chunk ring in SMEM (16 KB slots)
+constexpr int kPW = 3;                      // producer warps per sub-partition (each owns stages p, p + 3)
 constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA issuer warp
@@ -52,12 +52,15 @@ constexpr int kRec = 24;                    // decoded corner record: 3 lane-hal
 constexpr int kStageBytesPerWarp = 32 * kRec + 32 * 4;   // 32 records + 32 flush columns
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
 constexpr int kMaxChunks = 160;             // chunks per clip: (T + 1) / 16 rounded up, T <= 2496
-// TMEM columns: D_c [0,64), D_s [64,128), S_c [128,192), S_s [192,256) (the epilogue's FP32 block sums),
-// A stage s at 256 + 64 s: cos (hi, lo) x 16 rows | sin (hi, lo) x 16
-constexpr uint32_t kColS = 128, kColA = 256;
+// TMEM columns: D_c [0,64), D_s [64,128), A stage s at 128 + 64 s: cos (hi, lo) x 16 rows | sin (hi, lo) x 16.
+// The epilogue's FP32 block sums S live in an L2-resident global scratch ([CTA][clip q][col / 4][lane]
+// float4: 64 KB per CTA), which frees TMEM for six A stages (two per producer warp).
+constexpr uint32_t kColA = 128;
 // named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s free (MMA -> producers);
 // 10 + s: stage s full (producers -> MMA)
 constexpr int kBarD = 2, kBarFree = 4, kBarFull = 4 + kAS;
+static_assert(kBarFull + kAS <= 16, "named barriers");
+static_assert(kAS == 2 * kPW, "each producer warp owns two stages");
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
 constexpr uint32_t kIdesc =
     (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -178,6 +181,7 @@ struct Args {
     int64_t items;
     EpiArgs ea;
     void *F;
+    float4 *S;                  // [gridDim][kClips][32 col quads][32 lanes] FP32 block sums
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
@@ -253,8 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 
     if (warp < kProd) {
         // ================================ producers ================================
-        // Warp (q, p) gathers clip q of every item for the chunks j = p (mod kPW) into TMEM stage j % 4 (one
-        // stage per warp for kPW = 4; two, alternately, for kPW = 2).  Per batch of <= 32 corners a lane-parallel decode writes one
+        // Warp (q, p) gathers clip q of every item for the chunks j = p (mod kPW) into TMEM stage j % kAS,
+        // i.e. stages p and p + kPW alternately (it fills one while the MMAs of the other complete).  Per batch of <= 32 corners a lane-parallel decode writes one
         // 24-byte record per corner: three lane-halves {row address, bf16 weight pair}, for even lanes (odd m:
         // the (-1)^m quarter-wave flip folded into the weights), odd lanes, and the axis lane (weights (w c_q,
         // w s_q) against the table's (T/2, u): x = c_q T/2 + s_q u).  The gather walks the corners with
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             advance(0, nt > 0 ? bound(0, false) : 0u);
             for (int t = 0; t < nt; ++t) {
                 const int j = p + kPW * t;
-                const int s = j & (kAS - 1);      // stages p (, p + kPW): every use of them is this warp group's
+                const int s = j % kAS;            // stages p, p + kPW: every use of them is this warp group's
                 const bool second = s >= kPW;
                 const uint32_t us_ = second ? uses1 : uses0;
                 if (second) ++uses1; else ++uses0;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             const bool last_item = item + gridDim.x >= A.items;
             for (int j = 0; j < nch; ++j, ++gc) {
-                const int s = j & (kAS - 1);
+                const int s = j % kAS;
                 const int b = (int)(gc % kBS);
                 FCFS_DCHECK(s >= 0 && s < kAS && b >= 0 && b < kBS);
                 mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
@@ -463,7 +467,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             for (int j = 0; j < nch; ++j, ++lc) {
                 const int slot = (int)(lc % kBS);
-                mbar_wait_park(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u);
+                // a sleeping poll: the loader runs kBS chunks ahead, and a spinning wait would take issue
+                // slots from the producers of its sub-partition
+                mbar_wait_backoff(BEMPTY(slot), ((lc / kBS) & 1u) ^ 1u, 256);
                 if (elect_one()) {
                     mbar_expect_tx(BFULL(slot), kBChunk);
                     bulk_g2s(bring + (uint32_t)slot * kBChunk, A.btab + (size_t)j * kBChunk, kBChunk, BFULL(slot));
@@ -474,10 +480,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     } else {
         // ================================ epilogue ================================
         // Warp q owns TMEM lanes 32q..32q+31 = clip q of each item.  Per finished accumulation block of D_c
-        // or D_s it adds the FP32 block into the running sums S_c / S_s (TMEM); per item it then writes the
-        // clip's window / pupil coefficients from S_c (cos rows) and S_s (sin rows) of its lanes.
-        const int q = warp - kMma + kEpi;   // warps 16..19
+        // or D_s it copies the block to registers, releases D at once, then adds it into the FP32 sums S
+        // in the CTA's global scratch (its own lane's row: float4 loads / stores coalesced over the warp);
+        // per item it then writes the clip's window / pupil coefficients from S.
+        const int q = warp - kProd;   // warps kProd .. kProd + 3: warp % 4 == q (TMEM lane quadrant)
         const uint32_t lrow = (uint32_t)(32 * q) << 16;
+        float4 *Sq = A.S + ((size_t)blockIdx.x * kClips + q) * 32 * 32;   // [col quad][lane]
         uint32_t t_[2] = {0u, 0u};
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             bool first[2] = {true, true};
@@ -490,23 +498,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                     mbar_wait(DFULL(d), t_[d] & 1u);
                     tc_fence_after();
                     const uint32_t dsrc = tmem + lrow + 64u * (uint32_t)d;
-                    const uint32_t sdst = tmem + lrow + kColS + 64u * (uint32_t)d;
+                    uint32_t rd[64];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
-                        uint32_t rd[16], rs[16];
-                        TMEM_LD16(dsrc + 16u * h, rd);
-                        if (!first[d]) TMEM_LD16(sdst + 16u * h, rs);
+                        uint32_t r16[16];
+                        TMEM_LD16(dsrc + 16u * h, r16);
                         tmem_wait_ld();
-                        if (!first[d]) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) rd[i] = __float_as_uint(__uint_as_float(rd[i]) + __uint_as_float(rs[i]));
-                        }
-                        tmem_st16(sdst + 16u * h, rd);
+                        for (int i = 0; i < 16; ++i) rd[16 * h + i] = r16[i];
                     }
-                    tmem_wait_st();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(DEMPTY(d));
+                    if (lane == 0) mbar_arrive(DEMPTY(d));   // D is free for the next block's MMAs
+                    float4 *Sd = Sq + (size_t)(16 * d) * 32 + lane;
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; ++c4) {
+                        float4 v = make_float4(__uint_as_float(rd[4 * c4]), __uint_as_float(rd[4 * c4 + 1]),
+                                               __uint_as_float(rd[4 * c4 + 2]), __uint_as_float(rd[4 * c4 + 3]));
+                        if (!first[d]) {
+                            const float4 o = Sd[c4 * 32];
+                            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                        }
+                        Sd[c4 * 32] = v;
+                    }
                     first[d] = false;
                     ++t_[d];
                 }
@@ -518,7 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 void *Fc = ea.out_f32 ? (void *)((float2 *)A.F + clip * ea.out_per_clip)
                                       : (void *)((double2 *)A.F + clip * ea.out_per_clip);
                 const bool dmask = ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0;
-                const uint32_t sc_ = tmem + lrow + kColS, ss_ = sc_ + 64u;
+                auto Sv = [&](int c) -> float {   // S column c of this lane (c < 64: D_c, c >= 64: D_s)
+                    const float4 v = Sq[(size_t)(c >> 2) * 32 + lane];
+                    return (c & 3) == 0 ? v.x : ((c & 3) == 1 ? v.y : ((c & 3) == 2 ? v.z : v.w));
+                };
                 const bool row = lane < M, ax = lane == M;
                 const int m = lane + 1;
                 const int nm = row ? nmaxr[ea.M + m] : (ax ? nmaxr[ea.M] : -1);
@@ -528,14 +545,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 FCFS_DCHECK(nm < 0 || (op - nm >= 0 && op + nm < ea.out_per_clip &&
                                        (!row || (on - nm >= 0 && on + nm < ea.out_per_clip))));
                 {
-                    uint32_t a1[1], a2[1];
-                    tmem_ld1(sc_ + 31u, a1);
-                    tmem_ld1(ss_ + 31u, a2);
-                    tmem_wait_ld();
+                    const float a1 = Sv(31), a2 = Sv(64 + 31);
                     if (row && nm >= 0) {   // n = 0: Eq. Fk0, F[m,0] = i (Pc_ax - i Ps_ax) / (2 pi m T)
                         const bool mk = dmask && mm > ea.r2;
-                        const double re = mk ? 0.0 : (double)__uint_as_float(a2[0]) * f_axm[m];
-                        const double im = mk ? 0.0 : (double)__uint_as_float(a1[0]) * f_axm[m];
+                        const double re = mk ? 0.0 : (double)a2 * f_axm[m];
+                        const double im = mk ? 0.0 : (double)a1 * f_axm[m];
                         store_out(Fc, op, make_double2(re, im), ea.out_f32);
                         store_out(Fc, on, make_double2(re, -im), ea.out_f32);
                     } else if (ax && nm >= 0) {   // DC (Eq. Fdc)
@@ -546,18 +560,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {   // b = 8 g + 1 .. 8 g + 8
                     if (8 * g + 1 > N) break;   // uniform
-                    uint32_t pcc[8], pcs[8], psc[8], pss[8];
-                    tmem_ld8(sc_ + 8u * g, pcc);         // S_c[b - 1]
-                    tmem_ld8(sc_ + 32u + 8u * g, pcs);   // S_c[31 + b]
-                    tmem_ld8(ss_ + 8u * g, psc);
-                    tmem_ld8(ss_ + 32u + 8u * g, pss);
-                    tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int b = 8 * g + i + 1;
                         if (b > nm) break;
-                        const double c_c = __uint_as_float(pcc[i]), c_s = __uint_as_float(pcs[i]);
-                        const double s_c = __uint_as_float(psc[i]), s_s = __uint_as_float(pss[i]);
+                        // S_c[b - 1], S_c[31 + b], S_s[b - 1], S_s[31 + b]
+                        const double c_c = Sv(b - 1), c_s = Sv(31 + b);
+                        const double s_c = Sv(64 + b - 1), s_s = Sv(64 + 31 + b);
                         if (row) {
                             // Eq. Fkl: S(m, +-b) from the quadrant products, F = -S / (4 pi^2 m n)
                             const bool mk = dmask && mm + (double)b * (double)b > ea.r2;
@@ -681,7 +690,12 @@ static int lattice_grid(int64_t B) {
     return (int)(items < sms ? items : sms);
 }
 
-size_t lattice_ws_bytes(int64_t B, int32_t T) { return btab_bytes(T) + (size_t)B * (lattice_chunks(T) + 1) * 4 + 256; }
+static size_t cptr_bytes(int64_t B, int32_t T) { return ((size_t)B * (lattice_chunks(T) + 1) * 4 + 255) & ~(size_t)255; }
+static constexpr size_t kSBytesPerCta = (size_t)lat::kClips * 32 * 32 * sizeof(float4);   // 64 KB
+
+size_t lattice_ws_bytes(int64_t B, int32_t T) {
+    return btab_bytes(T) + cptr_bytes(B, T) + (size_t)lattice_grid(B) * kSBytesPerCta + 256;
+}
 
 fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int64_t K, int32_t T,
                                    int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s) {
@@ -711,6 +725,7 @@ fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *
     a.x = x; a.y = y; a.w = w;
     a.btab = (const uint8_t *)ws;
     a.cptr = (const int32_t *)((const uint8_t *)ws + btab_bytes(T));
+    a.S = (float4 *)((uint8_t *)ws + btab_bytes(T) + cptr_bytes(B, T));
     a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch;
     a.items = (B + lat::kClips - 1) / lat::kClips;
     a.ea = ea;
