@@ -745,7 +745,8 @@ def main():
             bound = "tensor"
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else
-                                   ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else "")),
+                                   ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else
+                                    "edges" if (prec == "tf32x3" and wl.B > 1 and k_inner.startswith("edges")) else "")),
             "kernel": ("k_small_clip (a1-a5 in one launch, CUDA graph replay)" if small is not None else
                        f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
                        if fft_route else ("contract stage (lattice-row form: k_lat_btab + k_lat_cptr + k_lattice)"

@@ -4,9 +4,11 @@
 set -u
 T=${1:-r01}
 O=gpurun_out
-NB="--no-cpu-baseline --no-e2e"
+NB="--no-cpu-baseline --no-e2e --no-extra"
 # ---- bench lines (each command exits before any profiler run of the same command)
-timeout 300 python bench.py --steps 10 --warmup 3 > $O/${T}_bench_c3.json 2> $O/${T}_bench_c3.err
+timeout 900 python bench.py --steps 10 --warmup 3 > $O/${T}_bench_c3.json 2> $O/${T}_bench_c3.err
+timeout 300 python bench.py --form edge --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_edges.json 2>/dev/null
+timeout 300 python bench.py --config c1 --no-small --steps 10 --warmup 3 --no-cpu-baseline > $O/${T}_bench_c1_general.json 2>/dev/null
 timeout 300 python bench.py --prec f16x3 --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_f16x3.json 2>/dev/null
 timeout 300 python bench.py --form corner --steps 10 --warmup 3 $NB > $O/${T}_bench_c3_corners.json 2>/dev/null
 for c in c1 c2 c4 c5; do
@@ -29,9 +31,12 @@ $B4 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control non
 $B5 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/${T}_launches_c5_fp64.csv $B5 > $O/ncu_l5.log 2>&1
 # ---- ncu --set full of the dominant kernels
 F="ncu --set full --clock-control none --import-source on"
-$B3 > /dev/null 2>&1 && $F -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf32 $B3 > $O/ncu_f1.log 2>&1
+$B3 > /dev/null 2>&1 && $F -k regex:k_lattice -s 1 -c 1 -o $O/${T}_prof_c3_lattice $B3 > $O/ncu_f1.log 2>&1
+$B3 --form edge > /dev/null 2>&1 && $F -k regex:k_gemm_tf32 -s 1 -c 1 -o $O/${T}_prof_c3_tf32 $B3 --form edge > $O/ncu_f1e.log 2>&1
+B1="python bench.py --config c1 --steps 2 --warmup 1 $NB"
+$B1 > /dev/null 2>&1 && $F -k regex:k_small_clip -s 1 -c 1 -o $O/${T}_prof_c1_small $B1 > $O/ncu_f1s.log 2>&1
 $B3 > /dev/null 2>&1 && $F -k regex:k_clip_corners -s 1 -c 1 -o $O/${T}_prof_c3_extract $B3 > $O/ncu_f2.log 2>&1
-$B3 > /dev/null 2>&1 && $F -k regex:k_edges -s 1 -c 1 -o $O/${T}_prof_c3_edges $B3 > $O/ncu_f2e.log 2>&1
+$B3 --form edge > /dev/null 2>&1 && $F -k regex:k_edges -s 1 -c 1 -o $O/${T}_prof_c3_edges $B3 --form edge > $O/ncu_f2e.log 2>&1
 $B4 > /dev/null 2>&1 && $F -k regex:"k_fr_rows|k_fr_fft2|k_fr_row0" -s 0 -c 4 -o $O/${T}_prof_c4_fp64_fft $B4 > $O/ncu_f3.log 2>&1
 $B4 --route gemm > /dev/null 2>&1 && $F -k regex:"k_gemm_fp64|k_gsum_fp64|k_hsum_fp64" -s 0 -c 3 -o $O/${T}_prof_c4_fp64_gemm $B4 --route gemm > $O/ncu_f4.log 2>&1
 B4t="python bench.py --config c4 --prec tf32x3 --steps 1 --warmup 1 $NB"
