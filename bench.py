@@ -85,19 +85,22 @@ def spawn_ranks(args):
     os.execv(sys.executable, cmd)
 
 
-EXTRAS = (("c4", "fp64"), ("c5", "fp64"), ("c4", "tf32x3"))
+EXTRAS = (("c4", "fp64", None), ("c5", "fp64", None), ("c4", "tf32x3", None), ("c4", "fp64", "gemm"))
 
 
 def run_extras(args):
-    """The default c3 run also measures the FP64 single-clip configs and c4 split-TF32 (each in a child
-    bench.py process: its own plans, clocks, roofline and sampled oracle baseline); their lines are
+    """The default c3 run also measures the FP64 single-clip configs (lattice-FFT route, the default),
+    c4 split-TF32 and c4 FP64 on the row-bucket DMMA GEMM route (the FP64 tensor-core roofline), each in a
+    child bench.py process (its own plans, clocks, roofline and sampled oracle baseline); their lines are
     embedded under "extra"."""
     out = {}
-    for cfg, prec in EXTRAS:
+    for cfg, prec, route in EXTRAS:
         cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg, "--prec", prec, "--steps",
                str(min(args.steps, 5)), "--warmup", "3", "--no-e2e", "--no-extra", "--cpu-seconds", "4"]
-        if prec != "fp64":
-            cmd.append("--no-cpu-baseline")         # the oracle does not depend on the precision: see c4_fp64
+        if route:
+            cmd += ["--route", route]
+        if prec != "fp64" or route:
+            cmd.append("--no-cpu-baseline")         # the oracle does not depend on the precision / route
         try:
             r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
                                env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
@@ -107,7 +110,7 @@ def run_extras(args):
             d = {"error": repr(ex)[:400]}
         for k in ("e2e", "metric", "unit", "higher_is_better", "vs_baseline", "data", "n_gpus"):
             d.pop(k, None)
-        out[f"{cfg}_{prec}"] = d
+        out[f"{cfg}_{prec}" + (f"_{route}" if route else "")] = d
     return out
 
 
