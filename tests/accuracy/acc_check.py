@@ -18,4 +18,4 @@ Fr, B = oracle.coeffs(x, y, w, int(g["area"][0].item()), wl.T, ms, ns)
 r = np.abs(F[idx] - Fr) / np.maximum(B, 1e-300)
 r[(ms == 0) & (ns == 0)] = 0
 i = int(np.argmax(r))
-print(f"{cfg} {prec} dbg={os.environ.get('FCFS_DEBUG','0')}: max err/B {r.max():.3e} at (m,n)=({ms[i]},{ns[i]}); median {np.median(r):.3e}; axis max {r[:40].max():.3e}")
+print(f"{cfg} {prec} max err/B {r.max():.3e} at (m,n)=({ms[i]},{ns[i]}); median {np.median(r):.3e}; axis max {r[:40].max():.3e}")
