@@ -34,12 +34,12 @@ namespace fcfs {
 namespace lat {
 using namespace fcfs::tc;
 
-constexpr int kYC = 16;                     // lattice rows per chunk
+constexpr int kYC = 12;                     // lattice rows per chunk (K = 24 of the 32-wide B tiles)
 constexpr int kClips = 4;                   // clips per work item: clip q on TMEM lanes 32q .. 32q+31
-constexpr int kAS = 6;                      // A stages in TMEM (64 columns each); chunk j uses stage j % 6,
+constexpr int kAS = 8;                      // A stages in TMEM (48 columns each); chunk j uses stage j % 8,
                                             // so each producer warp ping-pongs between two stages
 constexpr int kBS = 4;                      // B chunk ring in SMEM (16 KB slots)
-constexpr int kPW = 3;                      // producer warps per sub-partition (each owns stages p, p + 3)
+constexpr int kPW = 4;                      // producer warps per sub-partition (each owns stages p, p + 4)
 constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA issuer warp
@@ -51,14 +51,18 @@ constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation
 constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
 constexpr int kStageBytesPerWarp = 32 * kRec + 32 * 4;   // 32 records + 32 flush columns
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
-constexpr int kMaxChunks = 160;             // chunks per clip: (T + 1) / 16 rounded up, T <= 2496
-// TMEM columns: D_c [0,64), D_s [64,128), A stage s at 128 + 64 s: cos (hi, lo) x 16 rows | sin (hi, lo) x 16.
+constexpr int kMaxChunks = 209;             // chunks per clip: (T + 1) / 12 rounded up, T <= 2496
+constexpr int kStageCols = 4 * kYC;         // TMEM columns per A stage: cos (hi, lo) x 12 rows | sin (hi, lo) x 12
+// TMEM columns: D_c [0,64), D_s [64,128), A stage s at 128 + 48 s: cos (hi, lo) x 12 rows | sin (hi, lo) x 12.
 // The epilogue's FP32 block sums S live in an L2-resident global scratch ([CTA][clip q][col / 4][lane]
 // float4: 64 KB per CTA), which frees TMEM for six A stages (two per producer warp).
 constexpr uint32_t kColA = 128;
 // named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s free (MMA -> producers);
 // 10 + s: stage s full (producers -> MMA)
-constexpr int kBarD = 2, kBarFree = 4, kBarFull = 4 + kAS;
+// named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s full (producers -> MMA).
+// Stage s free (MMA completion -> producers) is the commit's mbarrier alone: with two stages per warp the
+// producers rarely wait for it.
+constexpr int kBarD = 2, kBarFull = 4;
 static_assert(kBarFull + kAS <= 16, "named barriers");
 static_assert(kAS == 2 * kPW, "each producer warp owns two stages");
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
@@ -113,6 +117,13 @@ __device__ __forceinline__ void tmem_st_zero32(uint32_t taddr) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
         "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
         "r"(z)
         : "memory");
 }
@@ -332,15 +343,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 if (second) ++uses1; else ++uses0;
                 const uint32_t ca = bound(t, false), cb = bound(t, true);
                 FCFS_DCHECK(ca <= cb && (!real || (int64_t)cb <= A.corner_ptr[clip + 1] - k0));
-                // stage s is free once the MMAs of its previous chunk have completed: park on the named barrier
-                // the MMA warp arrives at after issuing them (a hardware wait), then confirm the completion on
-                // the commit's mbarrier
-                if (us_ > 0) named_bar(kBarFree + s, 32 + 4 * 32);
-                mbar_wait_park(AEMPTY(s), (us_ & 1u) ^ 1u);
+                // stage s is free once the MMAs of its previous chunk (two chunks of this warp ago) completed
+                // (a sleeping poll: try_wait's own suspend wakes on every barrier event of the CTA, so a parked
+                // warp would keep taking issue slots from the working producers of its sub-partition)
+                mbar_wait_backoff(AEMPTY(s), (us_ & 1u) ^ 1u, 32);
                 tc_fence_after();
-                const uint32_t tcol = tmem + lrow + kColA + 64u * (uint32_t)s;
+                const uint32_t tcol = tmem + lrow + kColA + (uint32_t)kStageCols * (uint32_t)s;
                 tmem_st_zero32(tcol);
-                tmem_st_zero32(tcol + 32);
+                tmem_st_zero16(tcol + 32);
                 tmem_wait_st();
                 const int32_t y0 = j * kYC;
                 float2 acc = make_float2(0.f, 0.f);     // (cos, sin) sums of the current row
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                             split_hl(acc.x, h, l);
                             split_hl(acc.y, h2, l2);
                             tmem_st2(tcol + col, h, l);
-                            tmem_st2(tcol + 32u + col, h2, l2);
+                            tmem_st2(tcol + 2u * kYC + col, h2, l2);
                             acc = make_float2(0.f, 0.f);
                         }
                     }
@@ -416,19 +426,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
                 named_bar(kBarFull + s, 32 + 4 * 32);       // the 4 producer warps of the chunk have filled it
                 tc_fence_after();
-                const uint32_t a0 = tmem + kColA + 64u * (uint32_t)s;
+                const uint32_t a0 = tmem + kColA + (uint32_t)kStageCols * (uint32_t)s;
                 const uint64_t b1 = umma_desc(bring + (uint32_t)b * kBChunk), b2 = umma_desc(bring + (uint32_t)b * kBChunk + kBTile);
                 const bool cs = c_start(j), ss = s_start(j);
                 auto issue = [&](int d) {
                     const uint32_t dt = tmem + 64u * (uint32_t)d;
-                    const uint32_t ad = a0 + 32u * (uint32_t)d;
+                    const uint32_t ad = a0 + 2u * kYC * (uint32_t)d;
                     const uint32_t fresh = d == 0 ? (cs ? 1u : 0u) : (ss ? 1u : 0u);
                     if (elect_one()) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
+                        for (int u = 0; u < kYC / 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
                             umma_ts(dt, ad + 8u * u, b1 + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)   // A^hi B^lo
+                        for (int u = 0; u < kYC / 4; ++u)   // A^hi B^lo
                             umma_ts(dt, ad + 8u * u, b2 + 2u * u, 1u);
                     }
                     __syncwarp();
@@ -456,7 +466,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 if (se) { named_arrive(kBarD + 1, 32 + kEpi * 32); ++ts_; }
                 // the producers of stage s's next use wait for these MMAs (no arrival for the stage's last use
                 // in the CTA, which nobody waits for)
-                if (!(last_item && j >= nch - kAS)) named_arrive(kBarFree + s, 32 + 4 * 32);
             }
         }
     } else if (warp == kLoad) {
@@ -605,14 +614,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 // (hi = tf32(v), lo = tf32(v - hi)); B' holds (hi, hi) at K = (2i, 2i+1), B'' holds (lo, 0); both in the
 // SW128 K-major stage layout (row r, k).
 __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restrict__ btab) {
-    const int64_t total = (int64_t)nch * 64 * kYC;
+    constexpr int kKP = 16;   // K pairs of a 32-wide tile: pairs >= kYC are padding (zeros)
+    const int64_t total = (int64_t)nch * 64 * kKP;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i / (64 * kYC));
-        const int r = (int)((i / kYC) % 64);
-        const int yi = (int)(i % kYC);
+        const int c = (int)(i / (64 * kKP));
+        const int r = (int)((i / kKP) % 64);
+        const int yi = (int)(i % kKP);
         const int64_t y = (int64_t)c * kYC + yi;
         double v = 0.0;
-        if (y <= T) {
+        if (yi < kYC && y <= T) {
             if (r < 31 && r < N) v = cospi(2.0 * (double)(((int64_t)(r + 1) * y) % T) / (double)T);
             else if (r == 31) v = (double)y;
             else if (r > 31 && r - 31 <= N) v = sinpi(2.0 * (double)(((int64_t)(r - 31) * y) % T) / (double)T);
