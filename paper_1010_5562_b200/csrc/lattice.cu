@@ -687,7 +687,7 @@ bool lattice_eligible(int32_t T, const EpiArgs &ea) {
     if (T < 4 || (T % 4) != 0 || T > 2496) return false;   // quarter-wave table rows in SMEM; chunk registers
     if (ea.M < 0 || ea.N < 0 || ea.M > 31 || ea.N > 31) return false;
     if (ea.m_lo != -ea.M || ea.m_hi != ea.M || !ea.out_f32) return false;
-    if (lattice_chunks(T) > 4 * 64) return false;
+    if (lattice_chunks(T) > lat::kMaxChunks) return false;   // the producers' register-cached chunk bounds
     return lattice_smem_bytes(T, ea.M) <= 227 * 1024;
 }
 
