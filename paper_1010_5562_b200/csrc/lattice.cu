@@ -43,7 +43,7 @@ constexpr int kPW = 4;                      // producer warps per sub-partition 
 constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA issuer warp
-constexpr int kLoad = kMma + 1;             // B-loader warp (on another sub-partition than the MMA warp)
+constexpr int kLoad = kMma + 2;             // B-loader warp; kMma and kMma + 1 issue the D_c and D_s MMAs
 constexpr int kThreads = (kLoad + 1) * 32;
 constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (16 lattice rows, hi/lo interleaved)
 constexpr int kBChunk = 2 * kBTile;         // B' + B''
@@ -64,6 +64,7 @@ constexpr uint32_t kColA = 128;
 // producers rarely wait for it.
 constexpr int kBarD = 2, kBarFull = 4;
 static_assert(kBarFull + kAS <= 16, "named barriers");
+constexpr int kFullCount = 32 * kClips + 64;   // stage full: one producer warp per clip + both MMA warps
 static_assert(kAS == 2 * kPW, "each producer warp owns two stages");
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
 constexpr uint32_t kIdesc =
@@ -247,8 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 off += c < 0 ? 0 : 2 * c + 1;
             }
             rowoff[2 * ea.M + 1] = off;
-            for (int st = 0; st < kAS; ++st) mbar_init(AEMPTY(st), 1);
-            for (int st = 0; st < kBS; ++st) { mbar_init(BFULL(st), 1); mbar_init(BEMPTY(st), 1); }
+            for (int st = 0; st < kAS; ++st) mbar_init(AEMPTY(st), 2);   // one commit per MMA warp
+            for (int st = 0; st < kBS; ++st) { mbar_init(BFULL(st), 1); mbar_init(BEMPTY(st), 2); }
             for (int d = 0; d < 2; ++d) { mbar_init(DFULL(d), 1); mbar_init(DEMPTY(d), kEpi); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
@@ -409,63 +410,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 tmem_wait_st();
                 __syncwarp();
                 tc_fence_before();
-                named_arrive(kBarFull + s, 32 + 4 * 32);    // stage full: the MMA warp waits on this
+                named_arrive(kBarFull + s, kFullCount);     // stage full: the MMA warps wait on this
             }
         }
-    } else if (warp == kMma) {
-        // ================================ MMA issuer ================================
+    } else if (warp == kMma || warp == kMma + 1) {
+        // ============================ MMA issuers: D_c (kMma), D_s (kMma + 1) ============================
+        // Two warps, one per accumulator: each waits for the chunk, issues its 6 MMAs and commits (the
+        // stage and B slot barriers expect both commits), so neither loop is on the other's critical path.
+        const int d = warp - kMma;
         const uint32_t bring = sbase + L.bring;
-        uint32_t tc_ = 0, ts_ = 0;   // D_c / D_s blocks issued
+        const uint64_t bdesc0 = umma_desc(bring);
+        const uint32_t dt = tmem + 64u * (uint32_t)d;
+        uint32_t td = 0;   // D blocks issued
         uint32_t gc = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
-            const bool last_item = item + gridDim.x >= A.items;
             for (int j = 0; j < nch; ++j, ++gc) {
                 const int s = j % kAS;
-                const int b = (int)(gc % kBS);
-                FCFS_DCHECK(s >= 0 && s < kAS && b >= 0 && b < kBS);
+                const uint32_t b = gc % kBS;
+                FCFS_DCHECK(s >= 0 && s < kAS && b < kBS);
                 mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
-                named_bar(kBarFull + s, 32 + 4 * 32);       // the 4 producer warps of the chunk have filled it
+                named_bar(kBarFull + s, kFullCount);        // the 4 producer warps of the chunk have filled it
+                const bool fresh = d == 0 ? c_start(j) : s_start(j);
+                if (fresh) mbar_wait_park(DEMPTY(d), (td & 1u) ^ 1u);   // the epilogue took the last block
                 tc_fence_after();
-                const uint32_t a0 = tmem + kColA + (uint32_t)kStageCols * (uint32_t)s;
-                const uint64_t b1 = umma_desc(bring + (uint32_t)b * kBChunk), b2 = umma_desc(bring + (uint32_t)b * kBChunk + kBTile);
-                const bool cs = c_start(j), ss = s_start(j);
-                auto issue = [&](int d) {
-                    const uint32_t dt = tmem + 64u * (uint32_t)d;
-                    const uint32_t ad = a0 + 2u * kYC * (uint32_t)d;
-                    const uint32_t fresh = d == 0 ? (cs ? 1u : 0u) : (ss ? 1u : 0u);
-                    if (elect_one()) {
-#pragma unroll
-                        for (int u = 0; u < kYC / 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
-                            umma_ts(dt, ad + 8u * u, b1 + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
-#pragma unroll
-                        for (int u = 0; u < kYC / 4; ++u)   // A^hi B^lo
-                            umma_ts(dt, ad + 8u * u, b2 + 2u * u, 1u);
-                    }
-                    __syncwarp();
-                };
-                auto wait_d = [&](int d) {
-                    const uint32_t t = d == 0 ? tc_ : ts_;
-                    mbar_wait_park(DEMPTY(d), (t & 1u) ^ 1u);
-                    tc_fence_after();
-                };
-                // a D whose accumulation block starts here waits for the epilogue to have taken its last
-                // block; the other D's MMAs are issued first so the tensor pipe stays busy meanwhile
-                if (cs && ss) { wait_d(0); wait_d(1); issue(0); issue(1); }
-                else if (cs) { issue(1); wait_d(0); issue(0); }
-                else if (ss) { issue(0); wait_d(1); issue(1); }
-                else { issue(0); issue(1); }
-                const bool ce = c_end(j, nch), se = s_end(j, nch);
+                const uint32_t ad = tmem + kColA + (uint32_t)kStageCols * (uint32_t)s + 2u * kYC * (uint32_t)d;
+                const uint64_t b1 = bdesc0 + (uint64_t)(b * (uint32_t)(kBChunk >> 4));
+                const uint64_t b2 = b1 + (uint64_t)(kBTile >> 4);
+                const bool end = d == 0 ? c_end(j, nch) : s_end(j, nch);
                 if (elect_one()) {
+#pragma unroll
+                    for (int u = 0; u < kYC / 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
+                        umma_ts(dt, ad + 8u * u, b1 + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
+#pragma unroll
+                    for (int u = 0; u < kYC / 4; ++u)   // A^hi B^lo
+                        umma_ts(dt, ad + 8u * u, b2 + 2u * u, 1u);
                     umma_commit(AEMPTY(s));
                     umma_commit(BEMPTY(b));
-                    if (ce) umma_commit(DFULL(0));
-                    if (se) umma_commit(DFULL(1));
+                    if (end) umma_commit(DFULL(d));
                 }
                 __syncwarp();
-                if (ce) { named_arrive(kBarD + 0, 32 + kEpi * 32); ++tc_; }
-                if (se) { named_arrive(kBarD + 1, 32 + kEpi * 32); ++ts_; }
-                // the producers of stage s's next use wait for these MMAs (no arrival for the stage's last use
-                // in the CTA, which nobody waits for)
+                if (end) { named_arrive(kBarD + d, 32 + kEpi * 32); ++td; }
             }
         }
     } else if (warp == kLoad) {
