@@ -11,17 +11,19 @@
 //
 //   * A lives in TENSOR MEMORY (tcgen05.mma with A from TMEM, "TS" form): TMEM sub-partition q holds clip
 //     q of a 4-clip work item, lane l = frequency m = l+1 (lane M: the x-weighted axis row of Eq. F0l).
-//     Two producer warps per sub-partition gather E(m x_k) for their 32 lanes from a quarter-wave SMEM
+//     Four producer warps per sub-partition gather E(m x_k) for their 32 lanes from a quarter-wave SMEM
 //     table (one conflict-free LDS.64 of (cos, sin) per corner), accumulate the row sums in registers (one
 //     FFMA2 per corner) and store each finished row's hi/lo split into its TMEM stage (tcgen05.st).  G never
 //     exists in HBM or SMEM ("no full-length arrays").
-//   * A stage holds 16 lattice rows with hi and lo interleaved along K, (hi_0, lo_0, hi_1, lo_1, ...), so
+//   * A stage holds 12 lattice rows with hi and lo interleaved along K, (hi_0, lo_0, hi_1, lo_1, ...), so
 //     one MMA stream against B' = (B^hi_0, B^hi_0, B^hi_1, B^hi_1, ...) gives (A^hi + A^lo) B^hi and one
-//     against B'' = (B^lo_0, 0, B^lo_1, 0, ...) gives A^hi B^lo: the three products of the split, 16 MMAs
-//     of M=128, N=64, K=8 per chunk and 4 clips (cos and sin rows).
-//   * FP32 TMEM accumulation in blocks of 16 chunks (256 rows, 128 MMA roundings); the
-//     epilogue warps add every block into FP32 sums (also in TMEM) and, per item, write the window /
-//     pupil coefficients (a4 + a5).
+//     against B'' = (B^lo_0, 0, B^lo_1, 0, ...) gives A^hi B^lo: the three products of the split, 12 MMAs
+//     of M=128, N=64, K=8 per chunk and 4 clips (cos and sin rows).  Eight 48-column stages (two per
+//     producer warp: it fills one while the MMAs of the other run); one MMA-issuer warp per accumulator
+//     (D_c, D_s) and a B-loader warp streaming the 16 KB chunks of the shared table from L2.
+//   * FP32 TMEM accumulation in blocks of 16 chunks (192 rows, 96 MMA roundings); the
+//     epilogue warps copy every block out of TMEM (releasing D at once), add it into FP32 sums in an
+//     L2-resident global scratch and, per item, write the window / pupil coefficients (a4 + a5).
 //
 // Phases are exact integers (lattice vertices): the table row is u = x, T/2 - x, x - T/2 or
 // T - x (quarter-wave symmetry), with the sign (-1)^m of odd m folded into per-lane-parity weights and the
@@ -45,9 +47,9 @@ constexpr int kEpi = 4;                     // epilogue warps: sub-partition q =
 constexpr int kMma = kProd + kEpi;          // MMA issuer warp
 constexpr int kLoad = kMma + 2;             // B-loader warp; kMma and kMma + 1 issue the D_c and D_s MMAs
 constexpr int kThreads = (kLoad + 1) * 32;
-constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (16 lattice rows, hi/lo interleaved)
+constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (12 lattice rows hi/lo interleaved + 8 K of zeros)
 constexpr int kBChunk = 2 * kBTile;         // B' + B''
-constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation block (256 rows)
+constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation block (192 rows)
 constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
 constexpr int kStageBytesPerWarp = 32 * kRec + 32 * 4;   // 32 records + 32 flush columns
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     }
 }
 
-// B operand of chunk c (16 lattice rows y = 16 c + i), N-rows: b - 1 = cos(2 pi b y / T) for b = 1..N, 31 = y
+// B operand of chunk c (kYC lattice rows y = kYC c + i), N-rows: b - 1 = cos(2 pi b y / T) for b = 1..N, 31 = y
 // (the coordinate weight of Eq. Fk0), 31 + b = sin(2 pi b y / T); other rows and y > T: 0.  Split v = hi + lo
 // (hi = tf32(v), lo = tf32(v - hi)); B' holds (hi, hi) at K = (2i, 2i+1), B'' holds (lo, 0); both in the
 // SW128 K-major stage layout (row r, k).
