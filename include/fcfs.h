@@ -124,7 +124,8 @@ typedef struct {
 /* ------------------------------------------------------------------------------------------
  * a1 — vertex extraction (Alg. 2 lines 1-14; Prop. 1; Step 1 P:866-868).
  *
- * rects      int32 [R][4] (x0, y0, x1, y1), device.
+ * rects      int32 [R][4] (x0, y0, x1, y1), device, 16-byte aligned (one int4 load per rect; else
+ *            FCFS_E_INVALID).  Corner arrays (x, y, w) of every entry point need only 4-byte alignment.
  * group_ptr  int64 [G+1] CSR over rects, device; NULL => every rect is its own group (G == R).
  *            Within a group the rects are UNIONED; groups are SUMMED (reading A5).
  * clip_ptr   int64 [B+1] CSR over groups, device; NULL => one clip (B == 1).

@@ -46,7 +46,8 @@ __device__ __forceinline__ uint32_t bucket_flags(const BucketSegInfo &a, int64_t
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int j0 = t * bk::kItems;
     const int64_t k0 = ks + j0;
-    if (j0 + bk::kItems <= n && (k0 & 3) == 0) {
+    // vector loads only where the address itself is 16-byte aligned (the caller's y may start anywhere)
+    if (j0 + bk::kItems <= n && (((uintptr_t)(a.y + k0)) & 15u) == 0) {
         const int4 *p = (const int4 *)(a.y + k0);
 #pragma unroll
         for (int v = 0; v < bk::kItems / 4; ++v) {

@@ -423,7 +423,7 @@ static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t 
                                  int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream, const EdgeWs *eo,
                                  int32_t y_lo = 0, int32_t y_hi = 0x7fffffff) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
-    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && !rects) || !corner_ptr || !area || !K_total_host) {
+    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) || !corner_ptr || !area || !K_total_host) {
         set_error("fcfs_vertices_from_rects: invalid sizes or null pointers");
         return FCFS_E_INVALID;
     }
@@ -508,7 +508,7 @@ fcfs_status fcfs_chop_rects(const int32_t *rects, int64_t R, int32_t T, int32_t 
                             int32_t *out_rects, int64_t cap, int64_t *tile_ptr, int64_t *n_host, void *ws,
                             size_t ws_bytes, void *stream) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
-    if (R < 0 || (R > 0 && !rects) || tiles_x < 1 || tiles_y < 1 || !tile_ptr || !n_host || cap < 0 ||
+    if (R < 0 || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) || tiles_x < 1 || tiles_y < 1 || !tile_ptr || !n_host || cap < 0 ||
         (cap > 0 && !out_rects) || (int64_t)tiles_x * tiles_y >= (int64_t(1) << 31) ||
         (int64_t)tiles_x * T >= (int64_t(1) << 31) || (int64_t)tiles_y * T >= (int64_t(1) << 31) ||
         cap >= (int64_t(1) << 31)) {
@@ -588,7 +588,7 @@ fcfs_status fcfs_small_clip(const int32_t *rects, int64_t R, const int64_t *grou
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     fcfs_status st = check_window(win);
     if (st != FCFS_OK) return st;
-    if (R < 0 || (R > 0 && !rects) || !F || !status_dev || (group_ptr == nullptr && G != R) || G < 0) {
+    if (R < 0 || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) || !F || !status_dev || (group_ptr == nullptr && G != R) || G < 0) {
         set_error("fcfs_small_clip: invalid sizes or null pointers");
         return FCFS_E_INVALID;
     }

@@ -310,6 +310,27 @@ def test_nccl_sharded_paths_world1(fcfs):
             assert torch.equal(rows, full)
             ms, ns, Fr, B = _oracle_window(g, wl.T, 20, 20)
             _assert_parity(vb.cpu().numpy(), Fr, B, prec, f"vblock/{prec}", ms, ns)
+        # the bench's single-clip pipeline through the real NCCL collectives: y-band a1 + all_gather of the
+        # corner lists, then per-rank plans (rows, vertex blocks) reused across two steps
+        w4 = inputs.c4(seed=4, n_poly=5000, T=65536, M=8)
+        rects = torch.from_numpy(w4.rects).cuda()
+        e = oracle.extract(w4.rects, w4.T)
+        bx = fdist.BandExtract(w4.R, w4.T, 0, 1)
+        rs = fdist.RowsSharded(w4.T, 16, 16, "fp64", 0, 1)
+        vs = fdist.VertexSharded(w4.T, 16, 16, "fp64", 0, 1)
+        for _ in range(2):
+            x, y, w, K, area = fdist.extract_band_sharded(rects, w4.T, extractor=bx)
+            assert K == e["K"] and area == int(e["area"][0])
+            assert np.array_equal(x.cpu().numpy(), e["x"]) and np.array_equal(y.cpu().numpy(), e["y"])
+            assert np.array_equal(w.cpu().numpy(), e["w"])
+            Frow = rs.run(x, y, w, K, area)
+            Fvb = vs.run(x, y, w, K)
+            torch.cuda.synchronize()
+            ms, ns = oracle.window(16, 16)
+            Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], w4.T, ms, ns)
+            _assert_parity(Frow.cpu().numpy(), Fr, B, "fp64", "nccl rows", ms, ns)
+            _assert_parity(Fvb.cpu().numpy(), Fr, B, "fp64", "nccl vblock", ms, ns)
+        assert len(rs.plans) == 1 and len(vs.plans) == 1
     finally:
         dist.destroy_process_group()
 
@@ -1330,3 +1351,33 @@ def test_small_clip_graph_replay_and_status(fcfs):
     assert not fcfs.SmallClipPlan.supported(600, 1024, 8, 8)                # 2400 raw corners
     with pytest.raises(fcfs.FcfsError):
         fcfs.SmallClipPlan(600, 1024, 8, 8).run(torch.zeros((600, 4), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("route", ["gemm", "fft"])
+@pytest.mark.parametrize("off", [1, 2, 3])
+def test_corner_arrays_at_any_4_byte_offset(fcfs, route, off):
+    """x, y, w views that start 4, 8 or 12 bytes into an allocation (e.g. rows of a gathered [3, K]
+    tensor): every kernel must use vector loads only where the address itself is aligned."""
+    wl = inputs.c4(seed=6, n_poly=3000, T=65536, M=8)
+    g = _gpu_extract(fcfs, wl)
+    K = g["K"]
+    views = []
+    for k in ("x", "y", "w"):
+        buf = torch.zeros(K + 8, dtype=torch.int32, device="cuda")
+        buf[off:off + K] = g[k][:K]
+        views.append(buf[off:off + K])
+    area = int(g["area"][0])
+    F = fcfs.coeffs(*views, area, wl.T, 12, 12, prec="fp64", route=route)
+    torch.cuda.synchronize()
+    ms, ns, Fr, B = _oracle_window(g, wl.T, 12, 12)
+    _assert_parity(F.cpu().numpy(), Fr, B, "fp64", f"offset {off} {route}", ms, ns)
+
+
+def test_misaligned_rects_rejected(fcfs):
+    wl = inputs.c1(seed=0)
+    buf = torch.zeros(wl.R * 4 + 4, dtype=torch.int32, device="cuda")
+    buf[1:1 + wl.R * 4] = torch.from_numpy(wl.rects).cuda().reshape(-1)
+    bad = buf[1:1 + wl.R * 4].view(wl.R, 4)            # 4 bytes past a 16-byte boundary
+    with pytest.raises(fcfs.FcfsError) as ex:
+        fcfs.vertices_from_rects(bad, wl.T, torch.from_numpy(wl.group_ptr).cuda())
+    assert ex.value.status == fcfs.E_INVALID
