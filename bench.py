@@ -63,6 +63,10 @@ def parse():
     ap.add_argument("--no-small", action="store_true",
                     help="small single clips (c1): the general extraction + coefficient path instead of the "
                          "one-launch fcfs_small_clip latency path replayed as a CUDA graph")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="single clips on the lattice-FFT route: time the host-synchronising API calls instead of "
+                         "the sync-free pipeline (fcfs_vertices_from_rects_async + fcfs_coeffs_async) replayed as "
+                         "a CUDA graph")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the extra lines (c4 / c5 FP64, c4 split-TF32) of the default c3 run")
     return ap.parse_args()
@@ -602,6 +606,28 @@ def main():
         def coeffs():
             return plan.run(vp.x[:K], vp.y[:K], vp.w[:K], area_h)
         out_bytes = plan.out.numel() * plan.out.element_size()
+    graph_plan = None
+    if (small is None and wl.B == 1 and world == 1 and args.input == "rects" and args.config != "layout"
+            and not args.no_graph and args.route != "gemm"
+            and fcfs.coeffs_route(K, wl.T, wl.M, wl.N, wl.r2, layout, prec, route=args.route) == 1):
+        # one clip on the lattice-FFT route: the whole step (a1-a5) without a host sync, captured once in a
+        # CUDA graph and replayed; the host-synchronising CoeffsPlan above stays for the stage timing
+        graph_plan = fcfs.AsyncClipPlan(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, prec, G=G, max_group=mg, device=dev)
+        graph_plan.run(rects, gp)
+        torch.cuda.synchronize()
+        assert graph_plan.check() == K
+        g_stream = torch.cuda.Stream(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=g_stream):
+            graph_plan.run(rects, gp, stream=g_stream)
+        sync_coeffs, extract_sync = coeffs, extract
+
+        def extract():
+            return K
+
+        def coeffs():
+            graph.replay()
+            return graph_plan.out
     terms = float(W) * float(K)                     # per rank per step
     single_sharded = wl.B == 1 and world > 1
     if single_sharded:
@@ -652,6 +678,16 @@ def main():
 
     # ---------------- roofline of the dominant kernel (the a3 contraction)
     peaks, src = load_peaks()
+    if graph_plan is not None:
+        # stage times of the same work through the host-synchronising calls (outside the timed region)
+        fcfs.profile_enable(True)
+        fcfs.profile_read()
+        for _ in range(args.steps):
+            extract_sync()
+            sync_coeffs()
+        torch.cuda.synchronize()
+        stages = fcfs.profile_read()
+        fcfs.profile_enable(False)
     c_ms, c_n = stages["contract"]
     c_ms_launch = c_ms / max(c_n, 1)
     fft_route = (small is None and wl.B == 1 and world == 1 and
@@ -750,6 +786,8 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config, prec, "fft" if fft_route else
                                    ("corners" if (prec == "tf32x3" and wl.B > 1 and k_inner == "corners") else
                                     "edges" if (prec == "tf32x3" and wl.B > 1 and k_inner.startswith("edges")) else "")),
+            "step": ("sync-free a1-a5 (fcfs_vertices_from_rects_async + fcfs_coeffs_async) replayed as a CUDA graph; "
+                     "stage times from the host-synchronising calls" if graph_plan is not None else None),
             "kernel": ("k_small_clip (a1-a5 in one launch, CUDA graph replay)" if small is not None else
                        f"contract stage (lattice-FFT route, {'FP64' if prec == 'fp64' else 'FP32'}: k_fr_rows + k_fr_fft2)"
                        if fft_route else ("contract stage (lattice-row form: k_lat_btab + k_lat_cptr + k_lattice)"

@@ -304,6 +304,32 @@ fcfs_status fcfs_coeffs_batched_edges(const int64_t *corner_ptr, int64_t B, int6
                                       size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Sync-free single-clip pipeline (capturable in a CUDA graph; SURVEY §8(b) "device-side K"):
+ *
+ * fcfs_vertices_from_rects_async — a1 exactly as fcfs_vertices_from_rects (same workspace query, same
+ *   bit-exact canonical output) but with no host synchronisation: the corner count goes to K_dev
+ *   (int64 [1], device) and the outcome to status_dev (int32 [1], device: FCFS_OK, FCFS_E_RANGE,
+ *   FCFS_E_UNSUPPORTED, FCFS_E_WORKSPACE or FCFS_E_CAPACITY when K > cap), to be read after the stream's
+ *   work completes.  Always the general (sort) path; no edge output.
+ * fcfs_coeffs_async — a2-a5 of one clip on the lattice-FFT route for a corner
+ *   list whose count K is in device memory (K_dev, K <= K_cap) and whose area is area_dev (int64 [1]);
+ *   corners must be y-sorted (fcfs_vertices_from_rects_async output is).  Workspace:
+ *   fcfs_coeffs_workspace_bytes(K_cap, T, win, prec, NULL, &opt) with opt.route = FCFS_ROUTE_FFT.
+ *   status_dev (device) becomes FCFS_E_INVALID if the corners are not y-sorted, FCFS_E_CAPACITY if
+ *   K > K_cap; it is only written when it holds FCFS_OK, so the extraction's status carries through
+ *   when both calls share one word.  FCFS_E_UNSUPPORTED (host) when the FFT route does not apply. */
+fcfs_status fcfs_vertices_from_rects_async(const int32_t *rects, int64_t R, const int64_t *group_ptr,
+                                           int64_t G, const int64_t *clip_ptr, int64_t B, int32_t T,
+                                           int64_t max_group, int32_t *x, int32_t *y, int32_t *w,
+                                           int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                           int64_t *K_dev, int32_t *status_dev, void *ws,
+                                           size_t ws_bytes, void *stream);
+fcfs_status fcfs_coeffs_async(const int32_t *x, const int32_t *y, const int32_t *w,
+                              const int64_t *K_dev, int64_t K_cap, const int64_t *area_dev, int32_t T,
+                              const fcfs_window *win, fcfs_precision prec, void *F, int32_t *status_dev,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * Latency path for ONE SMALL CLIP: a1-a5 in a single kernel launch with NO host synchronisation
  * (capturable in a CUDA graph) — the paper's "only a few CFS coefficients" regime, evaluated term
  * by term (Goertzel-like) with the exact integer phase.  Every CTA extracts

@@ -230,6 +230,8 @@ struct FftPlan {
 bool fft_route_plan(int32_t T, int32_t M, int32_t N, int32_t m_lo, int32_t m_hi, int64_t K, bool f32, FftPlan &p,
                     int32_t route = FCFS_ROUTE_AUTO);
 size_t fft_route_ws_bytes(const FftPlan &p);
+fcfs_status fft_route_prepare_dev(const int32_t *y, const int64_t *K_dev, int64_t K_cap, const FftPlan &p, void *ws,
+                                  size_t ws_bytes, int32_t *status_dev, cudaStream_t s);
 fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const FftPlan &p, void *ws, size_t ws_bytes,
                               bool &sorted, cudaStream_t s);
 fcfs_status fft_route_run(const int32_t *x, const int32_t *w, int64_t k_lo, const FftPlan &p, void *ws,

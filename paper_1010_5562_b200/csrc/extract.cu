@@ -933,9 +933,19 @@ fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_p
 
 // steps 2-5 of the general path on the raw (key, weight) list in W.keys_a / W.w_a: sort, merge
 // equal keys (sum), drop zeros, scatter + area, corner_ptr; one stream sync for K and the error bits
+// the sync-free path's ending: K and the error bits become a device status word (fcfs_status codes)
+__global__ void k_extract_status(const int64_t *K, const int32_t *err, int64_t cap, int64_t *K_dev, int32_t *status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t k = *K;
+    const int32_t e = *err;
+    *K_dev = k;
+    *status = (e & 1) ? FCFS_E_RANGE : (e & 2) ? FCFS_E_UNSUPPORTED : (e & 4) ? FCFS_E_WORKSPACE
+                                                                  : (k > cap ? FCFS_E_CAPACITY : FCFS_OK);
+}
+
 static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int cb, int end_bit, int64_t B, int64_t cap, int32_t *x,
                                   int32_t *y, int32_t *w, int64_t *corner_ptr, int64_t *area, int64_t &Kh,
-                                  int32_t &errh, cudaStream_t s) {
+                                  int32_t &errh, cudaStream_t s, int64_t *K_dev = nullptr, int32_t *status_dev = nullptr) {
     const int threads = 256;
     size_t tb = W.cub_bytes;
     FCFS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, W.keys_a, W.keys_b, W.w_a, W.w_b, (int)cap_raw,
@@ -958,6 +968,11 @@ static fcfs_status finish_corners(ExtractWs &W, int64_t cap_raw, int cb, int end
     int64_t pb = (B + 1 + threads - 1) / threads;
     k_corner_ptr<<<(unsigned)(pb < 1024 ? pb : 1024), threads, 0, s>>>(W.keys_b, W.K, B, corner_ptr, cb);
     FCFS_CHECK_LAUNCH("k_corner_ptr");
+    if (K_dev) {   // sync-free: K and the status stay on the device
+        k_extract_status<<<1, 32, 0, s>>>(W.K, W.err, cap, K_dev, status_dev);
+        FCFS_CHECK_LAUNCH("k_extract_status");
+        return FCFS_OK;
+    }
     FCFS_TRY_CUDA(cudaMemcpyAsync(&Kh, W.K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaMemcpyAsync(&errh, W.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaStreamSynchronize(s));
@@ -1017,10 +1032,16 @@ size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_grou
 fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
-                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo, int32_t y_hi) {
+                    int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo, int32_t y_hi,
+                    int64_t *K_dev, int32_t *status_dev) {
     const bool singleton = (group_ptr == nullptr);
     const bool band = y_lo > 0 || y_hi <= T;
-    if (!band && singleton && T <= 65534 && (clip_ptr != nullptr || R <= kClipRects)) {
+    const bool async = K_dev != nullptr;   // sync-free: the general path, K and the status on the device
+    if (async && band) {
+        set_error("fcfs_vertices_from_rects: a band extraction is not available sync-free");
+        return FCFS_E_INVALID;
+    }
+    if (!async && !band && singleton && T <= 65534 && (clip_ptr != nullptr || R <= kClipRects)) {
         fcfs_status st = extract_clips(rects, R, clip_ptr, B, T, x, y, w, cap, corner_ptr, area, K_host, ws,
                                        ws_bytes, s);
         if (st != FCFS_E_UNSUPPORTED) return st;   // else: a clip is too large for the per-clip path
@@ -1103,8 +1124,9 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
     }
     int64_t Kh = 0;
     int32_t errh = 0;
-    fcfs_status st = finish_corners(W, cap_raw, cb, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s);
-    if (st != FCFS_OK) return st;
+    fcfs_status st = finish_corners(W, cap_raw, cb, end_bit, B, cap, x, y, w, corner_ptr, area, Kh, errh, s, K_dev,
+                                    status_dev);
+    if (st != FCFS_OK || async) return st;
     if (K_host) *K_host = Kh;
     if (errh & 1) {
         set_error("fcfs_vertices_from_rects: a rect lies outside [0,T]^2 or is empty");

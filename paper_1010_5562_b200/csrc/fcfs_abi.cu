@@ -78,7 +78,7 @@ fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, i
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                     int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s, int32_t y_lo = 0,
-                    int32_t y_hi = 0x7fffffff);
+                    int32_t y_hi = 0x7fffffff, int64_t *K_dev = nullptr, int32_t *status_dev = nullptr);
 size_t small_clip_smem_bytes(int32_t T, int64_t max_group);
 bool small_clip_eligible(int64_t R, int64_t G, int32_t T, int64_t max_group, int32_t M, int32_t N, bool grouped);
 fcfs_status launch_small_clip(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G, int32_t T,
@@ -421,9 +421,11 @@ static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t 
                                  const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                                  int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                                  int64_t *K_total_host, void *ws, size_t ws_bytes, void *stream, const EdgeWs *eo,
-                                 int32_t y_lo = 0, int32_t y_hi = 0x7fffffff) {
+                                 int32_t y_lo = 0, int32_t y_hi = 0x7fffffff, int64_t *K_dev = nullptr,
+                                 int32_t *status_dev = nullptr) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
-    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) || !corner_ptr || !area || !K_total_host) {
+    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) || !corner_ptr || !area ||
+        (!K_total_host && !(K_dev && status_dev))) {
         set_error("fcfs_vertices_from_rects: invalid sizes or null pointers");
         return FCFS_E_INVALID;
     }
@@ -435,7 +437,8 @@ static fcfs_status vertices_impl(const int32_t *rects, int64_t R, const int64_t 
     if (st != FCFS_OK) return st;
     StageScope scope(kStageExtract, (cudaStream_t)stream);
     st = extract(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area, K_total_host,
-                 ws, ws_bytes, (cudaStream_t)stream, y_lo, y_hi);
+                 ws, ws_bytes, (cudaStream_t)stream, y_lo, y_hi, K_dev, status_dev);
+    if (K_dev) return st;   // sync-free: no host K, no edge pass
     if (st != FCFS_OK || !eo) return st;
     if (*K_total_host > 0) return run_edges(x, y, w, corner_ptr, B, *eo, (cudaStream_t)stream);
     FCFS_TRY_CUDA(cudaMemsetAsync(eo->cnt, 0, sizeof(int32_t) * (size_t)B, (cudaStream_t)stream));
@@ -467,6 +470,15 @@ fcfs_status fcfs_vertices_from_rects_edges(const int32_t *rects, int64_t R, cons
     e.xa = xa; e.xb = xb; e.y = ye; e.c = c; e.cnt = ecnt;
     return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area,
                          K_total_host, ws, ws_bytes, stream, &e);
+}
+
+fcfs_status fcfs_vertices_from_rects_async(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
+                                           const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
+                                           int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
+                                           int64_t *K_dev, int32_t *status_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!K_dev || !status_dev) { set_error("fcfs_vertices_from_rects_async: K_dev / status_dev NULL"); return FCFS_E_INVALID; }
+    return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area, nullptr, ws,
+                         ws_bytes, stream, nullptr, 0, 0x7fffffff, K_dev, status_dev);
 }
 
 fcfs_status fcfs_vertices_from_rects_band(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
@@ -689,6 +701,42 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
     return launch_epilogue(plan, W.P, ea, F, s);
+}
+
+fcfs_status fcfs_coeffs_async(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *K_dev, int64_t K_cap,
+                              const int64_t *area_dev, int32_t T, const fcfs_window *win, fcfs_precision prec, void *F,
+                              int32_t *status_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    fcfs_status st = check_window(win);
+    if (st != FCFS_OK) return st;
+    if (K_cap < 1 || !x || !y || !w || !K_dev || !area_dev || !F || !status_dev) {
+        set_error("fcfs_coeffs_async: null pointer or K_cap < 1");
+        return FCFS_E_INVALID;
+    }
+    if (prec != FCFS_FP64 && prec != FCFS_TF32X3 && prec != FCFS_F16X3) { set_error("bad precision %d", prec); return FCFS_E_INVALID; }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    st = device_ok();
+    if (st != FCFS_OK) return st;
+    GemmPlan plan = make_plan(win->M, win->N, -win->M, win->M, 1, K_cap, false);
+    plan.phys = prec == FCFS_FP64 ? 0 : 1;
+    FftPlan fp;
+    if (!fft_route_plan(T, win->M, win->N, -win->M, win->M, K_cap, prec != FCFS_FP64, fp, FCFS_ROUTE_FFT)) {
+        set_error("fcfs_coeffs_async: the lattice-FFT route does not apply to T=%d, N=%d", T, win->N);
+        return FCFS_E_UNSUPPORTED;
+    }
+    Carver cv(ws, ws_bytes);
+    CoeffWs W;
+    carve_coeff(cv, plan, W, !fusable(plan, prec, win->M, -win->M, win->M, true), K_cap, 1, prec, true, &fp);
+    if (!cv.fits()) { set_error("fcfs_coeffs_async: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    EpiArgs ea;
+    ea.M = win->M; ea.N = win->N; ea.layout = win->layout; ea.r2 = win->pupil_r2;
+    ea.m_lo = -win->M; ea.m_hi = win->M; ea.T = T; ea.area_dev = area_dev; ea.area_host = 0;
+    ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
+    ea.out_per_clip = 0;
+    StageScope scope(kStageContract, s);
+    FCFS_TRY(fft_route_prepare_dev(y, K_dev, K_cap, fp, W.fft, W.fft_bytes, status_dev, s));
+    return fft_route_run(x, w, 0, fp, W.fft, W.fft_bytes, ea, F, s);
 }
 
 size_t fcfs_batched_workspace_bytes(int64_t B, int64_t K_total, int64_t K_max, int32_t T, const fcfs_window *win,

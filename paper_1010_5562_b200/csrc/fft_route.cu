@@ -99,9 +99,11 @@ __global__ void k_fr_table(V *tab, Geo g) {
         tab[i] = tw_entry<V>(i, g.T, g.lbits, g.nhi);
 }
 
-// yptr[v] = #corners in [k_lo, k_hi) with y < v, v in [0, T+1]; flag = 1 if y decreases somewhere
+// yptr[v] = #corners in [k_lo, k_hi) with y < v, v in [0, T+1]; flag = 1 if y decreases somewhere.
+// K_dev != NULL: the corner count comes from device memory (the sync-free path; K <= the planned cap)
 __global__ void k_fr_yptr(const int32_t *__restrict__ y, int64_t k_lo, int64_t K, int32_t T, int32_t *yptr,
-                          int32_t *flag) {
+                          int32_t *flag, const int64_t *K_dev) {
+    if (K_dev) K = *K_dev;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= (int64_t)T + 1; v += stride) {
         int64_t lo = 0, hi = K;
@@ -684,12 +686,36 @@ fcfs_status fft_route_prepare(const int32_t *y, int64_t k_lo, int64_t K, const F
     int64_t n = (int64_t)p.T + 2 > K ? (int64_t)p.T + 2 : K;
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    fr::k_fr_yptr<<<(unsigned)blocks, 256, 0, s>>>(y, k_lo, K, p.T, W.yptr, W.flag);
+    fr::k_fr_yptr<<<(unsigned)blocks, 256, 0, s>>>(y, k_lo, K, p.T, W.yptr, W.flag, nullptr);
     FCFS_CHECK_LAUNCH("k_fr_yptr");
     int32_t f = 0;
     FCFS_TRY_CUDA(cudaMemcpyAsync(&f, W.flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     FCFS_TRY_CUDA(cudaStreamSynchronize(s));
     sorted = f == 0;
+    return FCFS_OK;
+}
+
+// the sync-free variant: K from device memory (<= K_cap, the planned size), the sortedness flag turned
+// into a device status instead of a host read (the corners of fcfs_vertices_from_rects_async are sorted)
+__global__ void k_fr_status(const int32_t *flag, const int64_t *K_dev, int64_t K_cap, int32_t *status) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && *status == FCFS_OK)
+        *status = *flag ? FCFS_E_INVALID : (*K_dev > K_cap ? FCFS_E_CAPACITY : FCFS_OK);
+}
+
+fcfs_status fft_route_prepare_dev(const int32_t *y, const int64_t *K_dev, int64_t K_cap, const FftPlan &p, void *ws,
+                                  size_t ws_bytes, int32_t *status_dev, cudaStream_t s) {
+    Carver cv(ws, ws_bytes);
+    FftWs W;
+    carve_fft(cv, p, W);
+    if (!cv.fits()) { set_error("fft route: workspace %zu < %zu", ws_bytes, cv.used()); return FCFS_E_WORKSPACE; }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.flag, 0, sizeof(int32_t), s));
+    int64_t n = (int64_t)p.T + 2 > K_cap ? (int64_t)p.T + 2 : K_cap;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    fr::k_fr_yptr<<<(unsigned)blocks, 256, 0, s>>>(y, 0, K_cap, p.T, W.yptr, W.flag, K_dev);
+    FCFS_CHECK_LAUNCH("k_fr_yptr");
+    k_fr_status<<<1, 32, 0, s>>>(W.flag, K_dev, K_cap, status_dev);
+    FCFS_CHECK_LAUNCH("k_fr_status");
     return FCFS_OK;
 }
 

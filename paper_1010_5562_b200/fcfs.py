@@ -122,6 +122,11 @@ _lib.fcfs_row_buckets_workspace_bytes.restype = _sz
 _lib.fcfs_row_buckets.argtypes = [_P, _P, _i64, _i64, _i32, _P, _P, _P, ctypes.POINTER(_i64), _P, _sz, _P]
 _lib.fcfs_row_buckets.restype = _i32
 
+_lib.fcfs_vertices_from_rects_async.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P, _P,
+                                                _P, _P, _sz, _P]
+_lib.fcfs_vertices_from_rects_async.restype = _i32
+_lib.fcfs_coeffs_async.argtypes = [_P, _P, _P, _P, _i64, _P, _i32, _WP, _i32, _P, _P, _P, _sz, _P]
+_lib.fcfs_coeffs_async.restype = _i32
 _lib.fcfs_small_clip_supported.argtypes = [_i64, _i64, _i32, _i64, _WP]
 _lib.fcfs_small_clip_supported.restype = _i32
 _lib.fcfs_small_clip.argtypes = [_P, _i64, _P, _i64, _i32, _i64, _WP, _i32, _P, _P, _P, _P]
@@ -142,7 +147,8 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_coeffs_route", "fcfs_chop_workspace_bytes", "fcfs_chop_rects",
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
             "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band",
-            "fcfs_small_clip_supported", "fcfs_small_clip"]
+            "fcfs_small_clip_supported", "fcfs_small_clip", "fcfs_vertices_from_rects_async",
+            "fcfs_coeffs_async"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -465,6 +471,48 @@ def coeffs(x, y, w, area, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=N
     """a2-a5 for one clip.  Returns complex128 (fp64) or complex64 (tf32x3) cuda tensor."""
     plan = CoeffsPlan(x.shape[0], T, M, N, r2, layout, prec, shard, device=x.device, route=route)
     return plan.run(x, y, w, area, stream=stream)
+
+
+class AsyncClipPlan:
+    """One clip's a1-a5 with no host synchronisation (fcfs_vertices_from_rects_async + fcfs_coeffs_async
+    on the lattice-FFT route): K, the area and the outcome stay on the device, so the whole step can be
+    captured in a CUDA graph.  ``check()`` (after the stream's work) raises on a device-reported error and
+    returns K."""
+
+    def __init__(self, R, T, M, N, r2=-1.0, layout="dense", prec="fp64", G=None, max_group=1, device="cuda"):
+        self.vp = VerticesPlan(R, T, G, 1, max_group, grouped=max_group > 1 or (G is not None and G != R),
+                               device=device)
+        self.T, self.prec = int(T), _PREC[prec]
+        self.win = make_window(M, N, r2, layout)
+        self.K_cap = max(self.vp.cap, 1)
+        self.opt = make_options(route="fft")
+        nbytes = _lib.fcfs_coeffs_workspace_bytes(self.K_cap, self.T, ctypes.byref(self.win), self.prec, None,
+                                                  ctypes.byref(self.opt))
+        if nbytes == 0:
+            raise FcfsError(E_INVALID, "fcfs_coeffs_workspace_bytes")
+        self.ws = _ws(nbytes, device)
+        self.out = torch.empty(window_size(M, N, r2, layout), dtype=_out_dtype(prec), device=device)
+        self.K = torch.zeros(1, dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def run(self, rects, group_ptr=None, stream=None):
+        vp = self.vp
+        st = _lib.fcfs_vertices_from_rects_async(_ptr(rects), vp.R, _ptr(group_ptr), vp.G, None, 1, vp.T, vp.mg,
+                                                 _ptr(vp.x), _ptr(vp.y), _ptr(vp.w), vp.cap, _ptr(vp.corner_ptr),
+                                                 _ptr(vp.area), _ptr(self.K), _ptr(self.status), _ptr(vp.ws),
+                                                 vp.ws.numel(), _stream(stream))
+        _check(st, "fcfs_vertices_from_rects_async")
+        st = _lib.fcfs_coeffs_async(_ptr(vp.x), _ptr(vp.y), _ptr(vp.w), _ptr(self.K), self.K_cap, _ptr(vp.area),
+                                    self.T, ctypes.byref(self.win), self.prec, _ptr(self.out), _ptr(self.status),
+                                    _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_coeffs_async")
+        return self.out
+
+    def check(self):
+        st = int(self.status.item())
+        if st != FCFS_OK:
+            raise FcfsError(st, "AsyncClipPlan (device status)")
+        return int(self.K.item())
 
 
 class SmallClipPlan:

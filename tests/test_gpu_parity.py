@@ -1381,3 +1381,61 @@ def test_misaligned_rects_rejected(fcfs):
     with pytest.raises(fcfs.FcfsError) as ex:
         fcfs.vertices_from_rects(bad, wl.T, torch.from_numpy(wl.group_ptr).cuda())
     assert ex.value.status == fcfs.E_INVALID
+
+
+# ---------------------------------------------------------------------------------------------
+# sync-free single-clip pipeline (fcfs_vertices_from_rects_async + fcfs_coeffs_async), graph replay
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg,prec", [("c2", "fp64"), ("c2", "tf32x3"), ("c4", "fp64")])
+def test_async_clip_pipeline_matches_oracle_and_replays(fcfs, cfg, prec):
+    if cfg == "c2":
+        wl = inputs.c2(seed=3, n_poly=400)
+    else:
+        wl = inputs.c4(seed=3, n_poly=20000, T=65536, M=48)
+    gp = None if wl.group_ptr is None else torch.from_numpy(wl.group_ptr).cuda()
+    G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
+    mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
+    rects = torch.from_numpy(wl.rects).cuda()
+    plan = fcfs.AsyncClipPlan(wl.R, wl.T, wl.M, wl.N, prec=prec, G=G, max_group=mg)
+    plan.run(rects, gp)
+    torch.cuda.synchronize()
+    e = oracle.extract(wl.rects, wl.T, wl.group_ptr)
+    assert plan.check() == e["K"]
+    K = e["K"]
+    assert np.array_equal(plan.vp.x[:K].cpu().numpy(), e["x"]) and np.array_equal(plan.vp.w[:K].cpu().numpy(), e["w"])
+    rng = np.random.default_rng(1)
+    ms_all, ns_all = oracle.window(wl.M, wl.N)
+    pick = rng.choice(len(ms_all), size=min(len(ms_all), 700), replace=False)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms_all[pick], ns_all[pick])
+    _assert_parity(plan.out.cpu().numpy()[pick], Fr, B, prec, f"async {cfg}", ms_all[pick], ns_all[pick])
+    # capture the step and replay it on other rects written into the same buffer
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(rects, gp, stream=s)
+    rects2 = wl.rects.copy()
+    rects2[:, [0, 2]] = np.minimum(rects2[:, [0, 2]] + 3, wl.T)       # shifted in x (still valid)
+    rects2 = rects2[rects2[:, 0] < rects2[:, 2]]
+    if len(rects2) == wl.R:
+        rects.copy_(torch.from_numpy(rects2))
+        g.replay()
+        torch.cuda.synchronize()
+        e2 = oracle.extract(rects2, wl.T, wl.group_ptr)
+        assert plan.check() == e2["K"]
+        Fr2, B2 = oracle.coeffs(e2["x"], e2["y"], e2["w"], e2["area"][0], wl.T, ms_all[pick], ns_all[pick])
+        _assert_parity(plan.out.cpu().numpy()[pick], Fr2, B2, prec, f"async replay {cfg}", ms_all[pick], ns_all[pick])
+
+
+def test_async_clip_reports_errors_on_the_device(fcfs):
+    wl = inputs.c2(seed=3, n_poly=50)
+    gp = torch.from_numpy(wl.group_ptr).cuda()
+    G = len(wl.group_ptr) - 1
+    plan = fcfs.AsyncClipPlan(wl.R, wl.T, wl.M, wl.N, G=G, max_group=int(np.diff(wl.group_ptr).max()))
+    bad = torch.from_numpy(wl.rects).cuda()
+    bad[0] = torch.tensor([9, 9, 9, 20])          # empty rect
+    plan.run(bad, gp)
+    torch.cuda.synchronize()
+    with pytest.raises(fcfs.FcfsError) as ex:
+        plan.check()
+    assert ex.value.status == fcfs.E_RANGE
