@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 // stage s is free once the MMAs of its previous chunk (two chunks of this warp ago) completed
                 // (a sleeping poll: try_wait's own suspend wakes on every barrier event of the CTA, so a parked
                 // warp would keep taking issue slots from the working producers of its sub-partition)
-                mbar_wait_backoff(AEMPTY(s), (us_ & 1u) ^ 1u, 32);
+                mbar_wait_backoff(AEMPTY(s), (us_ & 1u) ^ 1u, 128);
                 tc_fence_after();
                 const uint32_t tcol = tmem + lrow + kColA + (uint32_t)kStageCols * (uint32_t)s;
                 tmem_st_zero32(tcol);
