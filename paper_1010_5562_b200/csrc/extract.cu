@@ -316,6 +316,7 @@ __global__ void k_band_compact(const unsigned long long *__restrict__ keys, cons
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) {
             const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+            FCFS_DCHECK((int64_t)slot < n);
             okeys[slot] = k;
             owts[slot] = wv;
         }

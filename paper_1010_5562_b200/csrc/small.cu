@@ -134,6 +134,7 @@ __device__ void group_union(Shared &S, uint8_t *dyn, const int4 *rects, int n, i
     compress_s(vx, 2 * n, tmp, ux, &S.nxy[0], S.cub.scan);
     compress_s(vy, 2 * n, tmp, uy, &S.nxy[1], S.cub.scan);
     const int nx = S.nxy[0], ny = S.nxy[1];
+    FCFS_DCHECK(nx >= 1 && ny >= 1 && nx <= 2 * n && ny <= 2 * n);
     for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) grid[t] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_clip(Args A) {
             const int c = A.layout == FCFS_LAYOUT_PUPIL ? pupil_nmax(i - A.M, A.r2, A.N) : A.N;
             off += c < 0 ? 0 : 2 * c + 1;
         }
+        S.rowoff[2 * A.M + 1] = off;   // the window size (bounds checks)
     }
     __syncthreads();
     const float rT = 1.0f / (float)T;
@@ -342,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_clip(Args A) {
         if (m == 0) {
             Ak[k] = make_double2((double)S.cw[k] * (double)S.cx[k], 0.0);
         } else {
+            FCFS_DCHECK(mod_t(m * S.cx[k], T, rT) >= 0 && mod_t(m * S.cx[k], T, rT) < T);
             const double2 e = tab[mod_t(m * S.cx[k], T, rT)];
             Ak[k] = make_double2((double)S.cw[k] * e.x, -(double)S.cw[k] * e.y);   // w e^{-i theta}
         }
@@ -369,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_clip(Args A) {
             const int32_t an = n < 0 ? -n : n;
             const double sg = n < 0 ? -1.0 : 1.0;   // E(-v) = conj E(v)
             for (int k = lane; k < K; k += 32) {
+                FCFS_DCHECK(mod_t(an * S.cy[k], T, rT) >= 0 && mod_t(an * S.cy[k], T, rT) < T);
                 double2 e = tab[mod_t(an * S.cy[k], T, rT)];
                 e.y *= sg;
                 s = make_double2(fma(Ak[k].x, e.x, fma(Ak[k].y, e.y, s.x)),   // A * (c - i s)
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_clip(Args A) {
             f = make_double2(s.x / d, s.y / d);
         }
         if (dmask && (double)m * m + (double)n * n > A.r2) f = make_double2(0.0, 0.0);
+        FCFS_DCHECK(op + n >= 0 && on - n >= 0 && op + n < S.rowoff[2 * A.M + 1] && on - n < S.rowoff[2 * A.M + 1]);
         put(A, op + n, f);
         put(A, on - n, make_double2(f.x, -f.y));   // F[-m, -n] = conj F[m, n]
     }

@@ -81,7 +81,23 @@ def case_haar():
     fcfs.haar(g["x"], g["y"], g["w"], g["area"], lay.T, g["corner_ptr"])
 
 
-CASES = {"extract": case_extract, "c1": case_c1, "c3": case_c3, "c4": case_c4, "haar": case_haar}
+def case_latency():
+    wl = inputs.c1(seed=0)
+    rects = dev(wl.rects, torch.int32)
+    gp = dev(wl.group_ptr, torch.int64)
+    sp = fcfs.SmallClipPlan(wl.R, wl.T, wl.M, wl.N, G=1, max_group=wl.R)
+    sp.run(rects, gp)
+    torch.cuda.synchronize()
+    sp.check()
+    w2 = inputs.c2(seed=2, n_poly=200)
+    ap = fcfs.AsyncClipPlan(w2.R, w2.T, w2.M, w2.N, G=len(w2.group_ptr) - 1, max_group=int(np.diff(w2.group_ptr).max()))
+    ap.run(dev(w2.rects, torch.int32), dev(w2.group_ptr, torch.int64))
+    torch.cuda.synchronize()
+    ap.check()
+
+
+CASES = {"extract": case_extract, "c1": case_c1, "c3": case_c3, "c4": case_c4, "haar": case_haar,
+         "latency": case_latency}
 
 if __name__ == "__main__":
     fcfs.device_check()
