@@ -21,7 +21,7 @@
 //     of M=128, N=64, K=8 per chunk and 4 clips (cos and sin rows).  Eight 48-column stages (two per
 //     producer warp: it fills one while the MMAs of the other run); one MMA-issuer warp per accumulator
 //     (D_c, D_s) and a B-loader warp streaming the 16 KB chunks of the shared table from L2.
-//   * FP32 TMEM accumulation in blocks of 16 chunks (192 rows, 96 MMA roundings); the
+//   * FP32 TMEM accumulation in blocks of 21 chunks (252 rows, 126 MMA roundings); the
 //     epilogue warps copy every block out of TMEM (releasing D at once), add it into FP32 sums in an
 //     L2-resident global scratch and, per item, write the window / pupil coefficients (a4 + a5).
 //
@@ -49,7 +49,7 @@ constexpr int kLoad = kMma + 2;             // B-loader warp; kMma and kMma + 1 
 constexpr int kThreads = (kLoad + 1) * 32;
 constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (12 lattice rows hi/lo interleaved + 8 K of zeros)
 constexpr int kBChunk = 2 * kBTile;         // B' + B''
-constexpr int kFlush = 16;                  // chunks per FP32 TMEM accumulation block (192 rows)
+constexpr int kFlush = 21;                  // chunks per FP32 TMEM accumulation block (252 rows, 126 MMA roundings)
 constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
 constexpr int kStageBytesPerWarp = 32 * kRec + 32 * 4;   // 32 records + 32 flush columns
 constexpr int kMaxRows = 64;                // output rows |m| <= 31 -> 63 rows (+1)
