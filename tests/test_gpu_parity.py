@@ -1439,3 +1439,67 @@ def test_async_clip_reports_errors_on_the_device(fcfs):
     with pytest.raises(fcfs.FcfsError) as ex:
         plan.check()
     assert ex.value.status == fcfs.E_RANGE
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_lattice_form_random_sweep(fcfs, seed):
+    """Seeded random configurations of the lattice-row form (T % 4 == 0 up to 2496, M, N in [0, 31], dense /
+    pupil / masked, 1..13 clips of 0..60 rects; clip counts around the 4-clip item and chunk counts around
+    the 12-row chunk and 21-chunk accumulation block) against the oracle on every clip."""
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.choice([12, 48, 256, 1000, 1200, 2048, 2496, 4 * int(rng.integers(3, 600))]))
+    M, N = int(rng.integers(0, 32)), int(rng.integers(0, 32))
+    layout = ["dense", "pupil", "masked"][seed % 3]
+    B = int(rng.integers(1, 14))
+    rects, cp = _lattice_clips(rng, T, B, sizes=[int(v) for v in rng.integers(0, 61, B)])
+    g = _extract_checked(fcfs, rects, T, None, cp)
+    r2 = -1.0 if layout == "dense" else float(rng.uniform(0.2, 1.0) * (M * M + N * N) + 0.5)
+    lay = "pupil" if layout == "pupil" else "dense"
+    kmax = max(1, int(np.diff(g["corner_ptr"].cpu().numpy()).max()))
+    plan = fcfs.BatchedPlan(B, g["K"], kmax, T, M, N, r2, lay, "tf32x3", form="lattice", sorted_y=True)
+    assert plan.form == fcfs.FORM_LATTICE, (T, M, N)
+    F = plan.run(g["corner_ptr"], g["x"], g["y"], g["w"], g["area"]).cpu().numpy()
+    ms, ns = oracle.window(M, N, r2 if lay == "pupil" else -1.0)
+    cpn = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    area = g["area"].cpu().numpy()
+    for b in range(B):
+        sl = slice(cpn[b], cpn[b + 1])
+        Fr, Bd = oracle.coeffs(x[sl], y[sl], w[sl], area[b], T, ms, ns)
+        if layout == "masked":
+            out = (ms.astype(np.float64) ** 2 + ns.astype(np.float64) ** 2) > r2
+            Fr[out] = 0
+            Bd[out] = 0
+        _assert_parity(F[b], Fr, Bd, "tf32x3", f"lattice sweep seed {seed} T={T} M={M} N={N} clip {b}", ms, ns)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_small_clip_random_sweep(fcfs, seed):
+    """Seeded random small clips through fcfs_small_clip (one group of up to 100 rects, or up to 500
+    singleton rects; T up to 8192 incl. non-powers of two; dense or pupil windows) against the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    T = int(rng.choice([16, 100, 1024, 3000, 4096, 8192]))
+    M, N = int(rng.integers(0, min(64, T // 2 + 1))), int(rng.integers(0, min(200, T // 2 + 1)))
+    grouped = seed % 2 == 0
+    n = int(rng.integers(1, 101 if grouped else 501))
+    r = inputs.random_rects(rng, n, T, 1, max(2, T // 6))
+    gp = np.array([0, len(r)], np.int64) if grouped else None
+    G = 1 if grouped else len(r)
+    mg = len(r) if grouped else 1
+    r2 = -1.0 if seed % 3 else float(rng.uniform(0.3, 1.0) * (M * M + N * N) + 0.5)
+    layout = "pupil" if r2 >= 0 else "dense"
+    if not fcfs.SmallClipPlan.supported(len(r), T, M, N, r2, layout, G, mg):
+        pytest.skip("outside the small-clip limits")
+    plan = fcfs.SmallClipPlan(len(r), T, M, N, r2, layout, "fp64", G=G, max_group=mg)
+    plan.run(torch.from_numpy(r).cuda(), None if gp is None else torch.from_numpy(gp).cuda())
+    torch.cuda.synchronize()
+    try:
+        K = plan.check()
+    except fcfs.FcfsError as ex:          # a union with more than 2048 raw corners: reported, not wrong
+        assert ex.status == fcfs.E_UNSUPPORTED
+        return
+    e = oracle.extract(r, T, gp)
+    assert K == e["K"]
+    ms, ns = oracle.window(M, N, r2)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
+    _assert_parity(plan.out.cpu().numpy(), Fr, B, "fp64", f"small sweep seed {seed}", ms, ns)
