@@ -298,6 +298,10 @@ __global__ void k_band_compact(const unsigned long long *__restrict__ keys, cons
     const unsigned long long mask = (1ull << cb) - 1;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // lane 0 carries the warp's running area of one clip across iterations (one atomic per warp and clip
+    // run instead of per iteration: a single large clip otherwise serialises ~K/32 atomics on area[0])
+    int64_t acc_b = -1;
+    long long acc_a = 0;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const int64_t i = i0 + lane;
         bool keep = false;
@@ -337,6 +341,10 @@ __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, c
     // clip, so a warp nearly always holds one clip: one atomic per warp instead of one per corner)
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // lane 0 carries the warp's running area of one clip across iterations (one atomic per warp and clip
+    // run instead of per iteration: a single large clip otherwise serialises ~K/32 atomics on area[0])
+    int64_t acc_b = -1;
+    long long acc_a = 0;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const int64_t i = i0 + lane;
         const bool valid = i < n;
@@ -358,11 +366,19 @@ __global__ void k_scatter(const unsigned long long *ukeys, const int32_t *agg, c
         const int64_t b0 = __shfl_sync(0xffffffffu, b, 0);
         if (__all_sync(0xffffffffu, !valid || b == b0)) {
             for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            if (lane == 0 && a != 0) atomicAdd((unsigned long long *)&area[b0], (unsigned long long)a);
+            if (lane == 0 && a != 0) {
+                if (b0 != acc_b) {
+                    if (acc_a != 0) atomicAdd((unsigned long long *)&area[acc_b], (unsigned long long)acc_a);
+                    acc_b = b0;
+                    acc_a = 0;
+                }
+                acc_a += a;
+            }
         } else if (valid && a != 0) {
             atomicAdd((unsigned long long *)&area[b], (unsigned long long)a);
         }
     }
+    if (lane == 0 && acc_a != 0) atomicAdd((unsigned long long *)&area[acc_b], (unsigned long long)acc_a);
 }
 
 __global__ void k_corner_ptr(const unsigned long long *ckeys, const int64_t *K, int64_t B, int64_t *corner_ptr,
