@@ -449,6 +449,55 @@ __device__ int64_t clip_lookback(unsigned long long *status, int64_t b, int64_t 
     return prefix;
 }
 
+// The same look-back walked by a whole warp (all 32 lanes call it; every lane returns the prefix): each
+// step reads 32 predecessors' status words at once (lane l: clip j - l) instead of one, so a clip whose
+// recent predecessors have only published their counts waits for one L2 round trip per 32 clips
+// rather than per clip.  Same status protocol (mixes with clip_lookback).
+// agg_published: the caller already stored this clip's aggregate (clip_publish_count), earlier in its
+// work, so that its successors' walks do not wait for the rest of it.
+__device__ __forceinline__ void clip_publish_count(unsigned long long *status, int64_t b, int64_t count) {
+    if (b > 0) {
+        volatile unsigned long long *st = status;
+        st[b] = kLbAgg | (unsigned long long)count;
+        __threadfence();
+    }
+}
+__device__ int64_t clip_lookback_warp(unsigned long long *status, int64_t b, int64_t B, int64_t count,
+                                      int64_t *corner_ptr, bool agg_published = false) {
+    volatile unsigned long long *st = status;
+    const int lane = threadIdx.x & 31;
+    int64_t prefix = 0;
+    if (b > 0) {
+        if (lane == 0 && !agg_published) {
+            st[b] = kLbAgg | (unsigned long long)count;
+            __threadfence();
+        }
+        __syncwarp();
+        for (int64_t j = b - 1;; j -= 32) {
+            const int64_t idx = j - lane;
+            unsigned long long v = kLbInc;                  // before clip 0: an inclusive prefix of 0
+            if (idx >= 0) {
+                do { v = st[idx]; } while ((v >> 62) == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+            // lanes up to (and including) the nearest inclusive predecessor contribute
+            const int stop = inc ? __ffs(inc) - 1 : 31;
+            long long c = lane <= stop ? (long long)(v & kLbMask) : 0;
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            prefix += c;
+            if (inc) break;
+        }
+    }
+    if (lane == 0) {
+        st[b] = kLbInc | (unsigned long long)(prefix + count);
+        __threadfence();
+        corner_ptr[b] = prefix;
+        if (b == B - 1) corner_ptr[B] = prefix + count;
+    }
+    __syncwarp();
+    return prefix;
+}
+
 __global__ void __launch_bounds__(kClipThreads, 1)
 k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_ptr, int64_t B, int64_t R,
                int32_t T, int32_t *xs, int32_t *ys, int32_t *ws, int64_t cap, int64_t *corner_ptr,
@@ -522,7 +571,10 @@ k_clip_corners(const int4 *__restrict__ rects, const int64_t *__restrict__ clip_
         int total = 0;
         IntScan(tmp.scan).ExclusiveSum(keep, pos, total);
         __syncthreads();
-        if (threadIdx.x == 0) s_off = clip_lookback(status, b, B, total, corner_ptr);
+        if (threadIdx.x < 32) {
+            const int64_t pre = clip_lookback_warp(status, b, B, total, corner_ptr);
+            if (threadIdx.x == 0) s_off = pre;
+        }
         __syncthreads();
         const int64_t base = s_off;
 #pragma unroll
@@ -623,15 +675,21 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     __syncthreads();
     int outp = incl - cnt;
     for (int i = 0; i < wid; ++i) outp += wsum[i];
+    int total = 0;
+    if (wid == 0) {   // the clip's count is known: publish it before the compaction (successors' walks)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) total += wsum[i];
+        if (lane == 0) clip_publish_count(status, b, total);
+    }
     for (int i = lo; i < hi; ++i) {
         const int16_t wv = sw[i];
         if (wv != 0) { bxw[outp] = syx[i]; by[outp] = wv; ++outp; }
     }
-    if (threadIdx.x == (int)blockDim.x - 1) *tot_s = outp;     // the last thread ends at the clip total
+    if (wid == 0) {   // the look-back walk of warp 0 overlaps the other warps' compaction
+        const int64_t pre = clip_lookback_warp(status, b, B, total, corner_ptr, true);
+        if (lane == 0) { *s_off = pre; *tot_s = total; }
+    }
     __syncthreads();
-    const int total = *tot_s;
-    if (threadIdx.x == 0) *s_off = clip_lookback(status, b, B, total, corner_ptr);
-    __syncthreads();
+    total = *tot_s;
     const int64_t base = *s_off;
     for (int i = threadIdx.x; i < total; i += (int)blockDim.x) {   // coalesced stores, final positions
         if (base + i >= cap) break;

@@ -34,20 +34,24 @@
 
 namespace fcfs {
 namespace lat {
+#ifndef KBS_
+#define KBS_ 6
+#endif
 using namespace fcfs::tc;
 
 constexpr int kYC = 12;                     // lattice rows per chunk (K = 24 of the 32-wide B tiles)
 constexpr int kClips = 4;                   // clips per work item: clip q on TMEM lanes 32q .. 32q+31
-constexpr int kAS = 8;                      // A stages in TMEM (48 columns each); chunk j uses stage j % 8,
-                                            // so each producer warp ping-pongs between two stages
-constexpr int kBS = 4;                      // B chunk ring in SMEM (16 KB slots)
-constexpr int kPW = 4;                      // producer warps per sub-partition (each owns stages p, p + 4)
+constexpr int kAS = 8;                      // A stages in TMEM (48 columns each): the CTA's g-th chunk (counted
+                                            // over its items) uses stage g % 8
+constexpr int kBS = KBS_;                   // B chunk ring in SMEM (12 KB slots)
+constexpr int kPW = 4;                      // producer warps per sub-partition (chunk j of an item: warp j % kPW;
+                                            // 5 measured 3% slower: spills and shared-memory pipe contention)
 constexpr int kProd = 4 * kPW;              // producer warps: sub-partition q = w & 3, chunks j = w >> 2 (mod kPW)
 constexpr int kEpi = 4;                     // epilogue warps: sub-partition q = e
 constexpr int kMma = kProd + kEpi;          // MMA issuer warp
 constexpr int kLoad = kMma + 2;             // B-loader warp; kMma and kMma + 1 issue the D_c and D_s MMAs
 constexpr int kThreads = (kLoad + 1) * 32;
-constexpr int kBTile = 64 * 32 * 4;         // 8 KB: 64 B rows x 32 K (12 lattice rows hi/lo interleaved + 8 K of zeros)
+constexpr int kBTile = 64 * 2 * kYC * 4;    // 6 KB: 64 B rows x 24 K (12 lattice rows hi/lo interleaved), no swizzle
 constexpr int kBChunk = 2 * kBTile;         // B' + B''
 constexpr int kFlush = 21;                  // chunks per FP32 TMEM accumulation block (252 rows, 126 MMA roundings)
 constexpr int kRec = 24;                    // decoded corner record: 3 lane-halves {row address, weights}
@@ -67,7 +71,7 @@ constexpr uint32_t kColA = 128;
 constexpr int kBarD = 2, kBarFull = 4;
 static_assert(kBarFull + kAS <= 16, "named barriers");
 constexpr int kFullCount = 32 * kClips + 64;   // stage full: one producer warp per clip + both MMA warps
-static_assert(kAS == 2 * kPW, "each producer warp owns two stages");
+static_assert(kPW <= kAS, "a producer's previous chunk proves the stage's older use complete");
 // instruction descriptor: D = F32, A = B = TF32, K-major, N = 64, M = 128
 constexpr uint32_t kIdesc =
     (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -198,6 +202,16 @@ struct Args {
     float4 *S;                  // [gridDim][kClips][32 col quads][32 lanes] FP32 block sums
 };
 
+#ifdef LAT_TRACE
+// diagnostic build only (tools/lat_trace.py): clock64 stamps of CTA 0's chunks
+constexpr int kTrMax = 8192;
+__device__ long long g_tr[kTrMax][12];   // per chunk g: [q] wait start, [4+q] fill start, [8+q] full
+__device__ long long g_trm[kTrMax][4];   // per chunk g: MMA warp d after FULL [d], before BFULL [2 + d]
+#define TR(stmt) do { if (blockIdx.x == 0) { stmt; } } while (0)
+#else
+#define TR(stmt) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -271,8 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 
     if (warp < kProd) {
         // ================================ producers ================================
-        // Warp (q, p) gathers clip q of every item for the chunks j = p (mod kPW) into TMEM stage j % kAS,
-        // i.e. stages p and p + kPW alternately (it fills one while the MMAs of the other complete).  Per batch of <= 32 corners a lane-parallel decode writes one
+        // Warp (q, p) gathers clip q of every item for the chunks j = p (mod kPW) into TMEM stage g % kAS (g:
+        // the CTA's chunk counter over its items).  Per batch of <= 32 corners a lane-parallel decode writes one
         // 24-byte record per corner: three lane-halves {row address, bf16 weight pair}, for even lanes (odd m:
         // the (-1)^m quarter-wave flip folded into the weights), odd lanes, and the axis lane (weights (w c_q,
         // w s_q) against the table's (T/2, u): x = c_q T/2 + s_q u).  The gather walks the corners with
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         const uint32_t fcl = stg + 32u * kRec;                              // flush columns [32]
         const uint32_t tabaddr = sbase + L.table;
         const int T2 = T / 2, T4 = T / 4, T34 = 3 * (T / 4);
-        uint32_t uses0 = 0, uses1 = 0;                                      // uses of stages p, p + kPW so far
+        uint32_t gbase = 0;                                                 // the CTA's chunks before this item
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             const int64_t clip = item * kClips + q;
             const bool real = clip < A.B;
@@ -340,16 +354,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
             advance(0, nt > 0 ? bound(0, false) : 0u);
             for (int t = 0; t < nt; ++t) {
                 const int j = p + kPW * t;
-                const int s = j % kAS;            // stages p, p + kPW: every use of them is this warp group's
-                const bool second = s >= kPW;
-                const uint32_t us_ = second ? uses1 : uses0;
-                if (second) ++uses1; else ++uses0;
+                const uint32_t g = gbase + (uint32_t)j;
+                const int s = (int)(g % kAS);     // the stage's (g / kAS)-th use
                 const uint32_t ca = bound(t, false), cb = bound(t, true);
                 FCFS_DCHECK(ca <= cb && (!real || (int64_t)cb <= A.corner_ptr[clip + 1] - k0));
-                // stage s is free once the MMAs of its previous chunk (two chunks of this warp ago) completed
+                // stage s is free once the MMAs of its previous use (chunk g - kAS) completed; an older use
+                // cannot be pending: this warp's previous chunk g - kPW >= g - kAS waited for chunk g - kPW - kAS
                 // (a sleeping poll: try_wait's own suspend wakes on every barrier event of the CTA, so a parked
                 // warp would keep taking issue slots from the working producers of its sub-partition)
-                mbar_wait_backoff(AEMPTY(s), (us_ & 1u) ^ 1u, 128);
+                TR(if (lane == 0 && g < kTrMax) g_tr[g][q] = clock64());
+                mbar_wait_backoff(AEMPTY(s), ((g / kAS) & 1u) ^ 1u, 128);
+                TR(if (lane == 0 && g < kTrMax) g_tr[g][4 + q] = clock64());
                 tc_fence_after();
                 const uint32_t tcol = tmem + lrow + kColA + (uint32_t)kStageCols * (uint32_t)s;
                 tmem_st_zero32(tcol);
@@ -412,8 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 tmem_wait_st();
                 __syncwarp();
                 tc_fence_before();
+                TR(if (lane == 0 && g < kTrMax) g_tr[g][8 + q] = clock64());
                 named_arrive(kBarFull + s, kFullCount);     // stage full: the MMA warps wait on this
             }
+            gbase += (uint32_t)nch;
         }
     } else if (warp == kMma || warp == kMma + 1) {
         // ============================ MMA issuers: D_c (kMma), D_s (kMma + 1) ============================
@@ -421,17 +438,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         // stage and B slot barriers expect both commits), so neither loop is on the other's critical path.
         const int d = warp - kMma;
         const uint32_t bring = sbase + L.bring;
-        const uint64_t bdesc0 = umma_desc(bring);
+        const uint64_t bdesc0 = umma_desc_kmajor_noswz(bring, 64 * 16, 128);   // K core columns 1 KB apart
         const uint32_t dt = tmem + 64u * (uint32_t)d;
         uint32_t td = 0;   // D blocks issued
         uint32_t gc = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
             for (int j = 0; j < nch; ++j, ++gc) {
-                const int s = j % kAS;
+                const int s = (int)(gc % kAS);
                 const uint32_t b = gc % kBS;
                 FCFS_DCHECK(s >= 0 && s < kAS && b < kBS);
+                TR(if (lane == 0 && gc < kTrMax) g_trm[gc][2 + d] = clock64());
                 mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
                 named_bar(kBarFull + s, kFullCount);        // the 4 producer warps of the chunk have filled it
+                TR(if (lane == 0 && gc < kTrMax) g_trm[gc][d] = clock64());
                 const bool fresh = d == 0 ? c_start(j) : s_start(j);
                 if (fresh) mbar_wait_park(DEMPTY(d), (td & 1u) ^ 1u);   // the epilogue took the last block
                 tc_fence_after();
@@ -442,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
                 if (elect_one()) {
 #pragma unroll
                     for (int u = 0; u < kYC / 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
-                        umma_ts(dt, ad + 8u * u, b1 + 2u * u, (u > 0 || !fresh) ? 1u : 0u);
+                        umma_ts(dt, ad + 8u * u, b1 + 128u * u, (u > 0 || !fresh) ? 1u : 0u);
 #pragma unroll
                     for (int u = 0; u < kYC / 4; ++u)   // A^hi B^lo
-                        umma_ts(dt, ad + 8u * u, b2 + 2u * u, 1u);
+                        umma_ts(dt, ad + 8u * u, b2 + 128u * u, 1u);
                     umma_commit(AEMPTY(s));
                     umma_commit(BEMPTY(b));
                     if (end) umma_commit(DFULL(d));
@@ -598,9 +617,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 // B operand of chunk c (kYC lattice rows y = kYC c + i), N-rows: b - 1 = cos(2 pi b y / T) for b = 1..N, 31 = y
 // (the coordinate weight of Eq. Fk0), 31 + b = sin(2 pi b y / T); other rows and y > T: 0.  Split v = hi + lo
 // (hi = tf32(v), lo = tf32(v - hi)); B' holds (hi, hi) at K = (2i, 2i+1), B'' holds (lo, 0); both in the
-// SW128 K-major stage layout (row r, k).
+// K-major no-swizzle layout (row r, k).
 __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restrict__ btab) {
-    constexpr int kKP = 16;   // K pairs of a 32-wide tile: pairs >= kYC are padding (zeros)
+    constexpr int kKP = kYC;   // K pairs (hi, hi) / (lo, 0): one per lattice row
     const int64_t total = (int64_t)nch * 64 * kKP;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int c = (int)(i / (64 * kKP));
@@ -618,7 +637,8 @@ __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restric
         uint8_t *ch = btab + (size_t)c * kBChunk;
         for (int h = 0; h < 2; ++h) {
             const int k = 2 * yi + h;
-            const uint32_t off = (uint32_t)(r / 8) * 1024u + (uint32_t)(r % 8) * 128u + ((uint32_t)((k / 4) ^ (r % 8)) << 4) +
+            // K-major, no swizzle: 8-row x 16-byte core matrices, 128 B apart along N, 1 KB apart along K
+            const uint32_t off = (uint32_t)(k / 4) * 1024u + (uint32_t)(r / 8) * 128u + (uint32_t)(r % 8) * 16u +
                                  (uint32_t)(k % 4) * 4u;
             *(float *)(ch + off) = hi;
             *(float *)(ch + kBTile + off) = h == 0 ? lo : 0.f;
@@ -735,3 +755,11 @@ fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *
 }
 
 }  // namespace fcfs
+
+#ifdef LAT_TRACE
+extern "C" int fcfs_lat_trace_read(void *tr, void *trm) {
+    if (cudaMemcpyFromSymbol(tr, fcfs::lat::g_tr, sizeof(fcfs::lat::g_tr)) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(trm, fcfs::lat::g_trm, sizeof(fcfs::lat::g_trm)) != cudaSuccess) return -1;
+    return 0;
+}
+#endif
