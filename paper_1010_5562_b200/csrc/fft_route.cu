@@ -199,6 +199,11 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
           const int32_t *__restrict__ yptr, const int16_t *__restrict__ perm, const V *__restrict__ tab, Geo g,
           int32_t m_first, int32_t m_last, int32_t row_off, V *Gd) {
     using S = typename Cx<V>::S;
+    // the two-level table in shared memory (<= 32 KB): its lookups are the kernel's latency chain
+    extern __shared__ __align__(16) unsigned char fr_rows_smem[];
+    V *stab = (V *)fr_rows_smem;
+    for (int i = threadIdx.x; i < g.nhi + (1 << g.lbits); i += blockDim.x) stab[i] = tab[i];
+    __syncthreads();
     const int32_t m0 = m_first + kRowsPerThread * (int32_t)blockIdx.y;
     const uint32_t mask = (uint32_t)g.T - 1u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g.T; t += (int64_t)gridDim.x * blockDim.x) {
@@ -222,13 +227,13 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
                     nxa = (uint32_t)__ldg(x + k_lo + k + 2); nxb = (uint32_t)__ldg(x + k_lo + k + 3);
                     nwa = __ldg(w + k_lo + k + 2); nwb = __ldg(w + k_lo + k + 3);
                 }
-                V ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
-                V eb = tw_ldg(tab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
+                V ea = tw_smem(stab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                V eb = tw_smem(stab, ((uint32_t)m0 * xb) & mask, g.lbits, g.nhi);
                 if constexpr (sizeof(S) == 8) {
                     // FP64: the second-order recurrence E_{m+1} = 2 cos(theta) E_m - E_{m-1} (2 FMA per step
                     // instead of a complex multiply's 4); its error grows as ~m^2/2 ulp: < 130 ulp over 16 rows
-                    V pa = tw_ldg(tab, ((uint32_t)(m0 + 1) * xa) & mask, g.lbits, g.nhi);
-                    V pb = tw_ldg(tab, ((uint32_t)(m0 + 1) * xb) & mask, g.lbits, g.nhi);
+                    V pa = tw_smem(stab, ((uint32_t)(m0 + 1) * xa) & mask, g.lbits, g.nhi);
+                    V pb = tw_smem(stab, ((uint32_t)(m0 + 1) * xb) & mask, g.lbits, g.nhi);
                     const S ta = 2 * fma(pa.x, ea.x, pa.y * ea.y), tb = 2 * fma(pb.x, eb.x, pb.y * eb.y);   // 2 Re(E_{m+1} conj E_m)
                     acc[0].x = fma(wa, ea.x, fma(wb, eb.x, acc[0].x));
                     acc[0].y = fma(wa, ea.y, fma(wb, eb.y, acc[0].y));
@@ -243,7 +248,7 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
                         acc[j].y = fma(wa, pa.y, fma(wb, pb.y, acc[j].y));
                     }
                 } else {
-                    const V sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi), sb = tw_ldg(tab, xb & mask, g.lbits, g.nhi);
+                    const V sa = tw_smem(stab, xa & mask, g.lbits, g.nhi), sb = tw_smem(stab, xb & mask, g.lbits, g.nhi);
 #pragma unroll
                     for (int j = 0; j < kRowsPerThread; ++j) {
                         if (j) { ea = cmul(ea, sa); eb = cmul(eb, sb); }
@@ -255,8 +260,8 @@ k_fr_rows(const int32_t *__restrict__ x, const int32_t *__restrict__ w, int64_t 
             if (k < k1) {
                 const uint32_t xa = (uint32_t)__ldg(x + k_lo + k);
                 const S wa = (S)__ldg(w + k_lo + k);
-                V ea = tw_ldg(tab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
-                const V sa = tw_ldg(tab, xa & mask, g.lbits, g.nhi);
+                V ea = tw_smem(stab, ((uint32_t)m0 * xa) & mask, g.lbits, g.nhi);
+                const V sa = tw_smem(stab, xa & mask, g.lbits, g.nhi);
 #pragma unroll
                 for (int j = 0; j < kRowsPerThread; ++j) {
                     if (j) ea = cmul(ea, sa);
@@ -749,7 +754,8 @@ static fcfs_status run_route(const int32_t *x, const int32_t *w, int64_t k_lo, c
             const int32_t m_first = p.mA + (int32_t)(ra - p.row0), m_last = p.mA + (int32_t)(c1 - 1 - p.row0);
             const int64_t rb = (m_last - m_first + fr::kRowsPerThread) / fr::kRowsPerThread;
             dim3 grid((unsigned)tblocks, (unsigned)rb);
-            fr::k_fr_rows<V><<<grid, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.perm, tab, g, m_first, m_last,
+            const size_t rsmem = sizeof(V) * (size_t)(g.nhi + (1 << g.lbits));
+            fr::k_fr_rows<V><<<grid, fr::kThreads, rsmem, s>>>(x, w, k_lo, W.yptr, W.perm, tab, g, m_first, m_last,
                                                            (int32_t)(ra - c0), Gd);
             FCFS_CHECK_LAUNCH("k_fr_rows");
             fr::k_fr_rowsT<V><<<(unsigned)rb, fr::kThreads, 0, s>>>(x, w, k_lo, W.yptr, W.pinv, tab, g, m_first,
