@@ -509,6 +509,7 @@ def main():
     mg = 1 if wl.group_ptr is None else int(np.diff(wl.group_ptr).max())
     G = wl.R if wl.group_ptr is None else len(wl.group_ptr) - 1
     small = None
+    graph_launches = 0   # kernels per replay of a captured step (replays bypass the launch counter)
     if (wl.B == 1 and world == 1 and args.input == "rects" and args.config != "layout" and not args.no_small
             and fcfs.SmallClipPlan.supported(wl.R, wl.T, wl.M, wl.N, wl.r2, layout, G, mg)):
         # latency path: a1-a5 in one kernel launch with no host sync (fcfs_small_clip), the step
@@ -519,8 +520,10 @@ def main():
         K_small = small.check()
         g_stream = torch.cuda.Stream(dev)
         graph = torch.cuda.CUDAGraph()
+        lc0 = fcfs.kernel_launches()
         with torch.cuda.graph(graph, stream=g_stream):
             small.run(rects, gp, stream=g_stream)
+        graph_launches = fcfs.kernel_launches() - lc0   # this library's kernels in one replay
         vp = None
 
         def extract():
@@ -618,8 +621,10 @@ def main():
         assert graph_plan.check() == K
         g_stream = torch.cuda.Stream(dev)
         graph = torch.cuda.CUDAGraph()
+        lc0 = fcfs.kernel_launches()
         with torch.cuda.graph(graph, stream=g_stream):
             graph_plan.run(rects, gp, stream=g_stream)
+        graph_launches = fcfs.kernel_launches() - lc0   # this library's kernels in one replay
         sync_coeffs, extract_sync = coeffs, extract
 
         def extract():
@@ -659,7 +664,7 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = fcfs.kernel_launches() - launches0
+    launches = fcfs.kernel_launches() - launches0 + graph_launches * args.steps
     stages = fcfs.profile_read()
     fcfs.profile_enable(False)
     per_rank = None
