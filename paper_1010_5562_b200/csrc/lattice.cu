@@ -442,22 +442,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         const uint32_t dt = tmem + 64u * (uint32_t)d;
         uint32_t td = 0;   // D blocks issued
         uint32_t gc = 0;
+        // incremental stage / slot / phase / block counters (no division in the issue loop)
+        uint32_t s = 0, b = 0, bph = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
+            // (j - first block start) mod kFlush: D_c blocks start at j % kFlush == 0, D_s at kFlush / 2
+            int jf = d == 0 ? 0 : kFlush - kFlush / 2;
             for (int j = 0; j < nch; ++j, ++gc) {
-                const int s = (int)(gc % kAS);
-                const uint32_t b = gc % kBS;
-                FCFS_DCHECK(s >= 0 && s < kAS && b < kBS);
+                FCFS_DCHECK(s == gc % kAS && b == gc % kBS && bph == ((gc / kBS) & 1u));
                 TR(if (lane == 0 && gc < kTrMax) g_trm[gc][2 + d] = clock64());
-                mbar_wait_park(BFULL(b), (gc / kBS) & 1u);
-                named_bar(kBarFull + s, kFullCount);        // the 4 producer warps of the chunk have filled it
+                mbar_wait_park(BFULL(b), bph);
+                named_bar(kBarFull + (int)s, kFullCount);   // the 4 producer warps of the chunk have filled it
                 TR(if (lane == 0 && gc < kTrMax) g_trm[gc][d] = clock64());
-                const bool fresh = d == 0 ? c_start(j) : s_start(j);
+                const bool fresh = j == 0 || jf == 0;
+                FCFS_DCHECK(fresh == (d == 0 ? c_start(j) : s_start(j)));
                 if (fresh) mbar_wait_park(DEMPTY(d), (td & 1u) ^ 1u);   // the epilogue took the last block
                 tc_fence_after();
-                const uint32_t ad = tmem + kColA + (uint32_t)kStageCols * (uint32_t)s + 2u * kYC * (uint32_t)d;
+                const uint32_t ad = tmem + kColA + (uint32_t)kStageCols * s + 2u * kYC * (uint32_t)d;
                 const uint64_t b1 = bdesc0 + (uint64_t)(b * (uint32_t)(kBChunk >> 4));
                 const uint64_t b2 = b1 + (uint64_t)(kBTile >> 4);
-                const bool end = d == 0 ? c_end(j, nch) : s_end(j, nch);
+                const bool end = jf == kFlush - 1 || j == nch - 1;
+                FCFS_DCHECK(end == (d == 0 ? c_end(j, nch) : s_end(j, nch)));
+                const uint32_t sc = s, bc = b;
+                static_assert((kAS & (kAS - 1)) == 0, "stage counter wraps by mask");
+                s = (s + 1u) & (kAS - 1u);
+                if (++b == (uint32_t)kBS) { b = 0; bph ^= 1u; }
+                if (++jf == kFlush) jf = 0;
                 if (elect_one()) {
 #pragma unroll
                     for (int u = 0; u < kYC / 4; ++u)   // (A^hi + A^lo) B^hi over the interleaved K
@@ -465,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
 #pragma unroll
                     for (int u = 0; u < kYC / 4; ++u)   // A^hi B^lo
                         umma_ts(dt, ad + 8u * u, b2 + 128u * u, 1u);
-                    umma_commit(AEMPTY(s));
-                    umma_commit(BEMPTY(b));
+                    umma_commit(AEMPTY(sc));
+                    umma_commit(BEMPTY(bc));
                     if (end) umma_commit(DFULL(d));
                 }
                 __syncwarp();
