@@ -605,9 +605,10 @@ static constexpr int kSmallRects = 448 * 3;        // the small per-clip bucket 
 
 // exclusive scan of the nb bucket sizes in hist (thread t owns buckets [t*per, (t+1)*per)); ends
 // with a __syncthreads
+template <int kNT>
 __device__ __forceinline__ void bucket_scan(int32_t *hist, int nb, int32_t *wsum) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int per = (nb + kNT - 1) / kNT;
     const int lo = threadIdx.x * per, hi = min(lo + per, nb);
     int sown = 0;
     for (int i = lo; i < hi; ++i) sown += hist[i];
@@ -627,6 +628,7 @@ __device__ __forceinline__ void bucket_scan(int32_t *hist, int nb, int32_t *wsum
 // (groups / polygons are summed), a block scan over the sorted positions drops zero weights, and the
 // clip is written in canonical (y, x) order straight to its CSR position (look-back offset,
 // coalesced), with its exact int64 area.  Ends with a __syncthreads.
+template <bool kPaired, int kNT>
 __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32_t *bxw, uint32_t *syx, int16_t *by,
                                             int16_t *sw, int32_t *hist, int32_t *wsum, long long *asum,
                                             int *tot_s, int64_t *s_off, int32_t *xs, int32_t *ys, int32_t *ws,
@@ -634,8 +636,42 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
                                             int64_t *area) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nv = hist[nb - 1];                    // valid corners (invalid rects skipped)
+    if constexpr (kPaired) {
+        // rects: every bucket holds whole edges, (x0, w) (x1, -w) at an even position, so a thread takes
+        // one edge and ranks both of its corners in one pass over the bucket's edges (8-byte loads; four
+        // compares per load instead of one)
+        for (int t = threadIdx.x; 2 * t < nv; t += kNT) {
+            const int i0 = 2 * t, i1 = i0 + 1;
+            const int y = by[i0];
+            const int st = y ? hist[y - 1] : 0, en = hist[y];
+            FCFS_DCHECK((st & 1) == 0 && (en & 1) == 0 && st <= i0 && i1 < en);
+            const uint2 me = *(const uint2 *)(bxw + i0);
+            const uint32_t xa = me.x >> 16, xb = me.y >> 16;
+            int ra = 0, rb = 0, wa = 0, wb = 0;
+            bool fa = true, fb = true;
+            for (int j = st; j < en; j += 2) {
+                const uint2 v = *(const uint2 *)(bxw + j);
+                const uint32_t x0 = v.x >> 16, x1 = v.y >> 16;
+                const int w0 = (int)(int16_t)(v.x & 0xFFFFu), w1 = (int)(int16_t)(v.y & 0xFFFFu);
+                const bool a0 = x0 == xa, a1 = x1 == xa, b0 = x0 == xb, b1 = x1 == xb;
+                // entry j is before i0 iff j < i0 (then j + 1 < i0 too); entry j + 1 is before i1 iff j < i0
+                // or j == i0; i0 itself is before i1
+                const bool pa = j < i0, pb = j <= i0;
+                ra += (int)((x0 < xa) | (a0 & pa)) + (int)((x1 < xa) | (a1 & pa));
+                rb += (int)((x0 < xb) | (b0 & pb)) + (int)((x1 < xb) | (b1 & pa));
+                wa += (a0 ? w0 : 0) + (a1 ? w1 : 0);
+                wb += (b0 ? w0 : 0) + (b1 ? w1 : 0);
+                fa &= !(a0 & pa) & !(a1 & pa);
+                fb &= !(b0 & pb) & !(b1 & pa);
+            }
+            syx[st + ra] = ((uint32_t)y << 16) | xa;
+            sw[st + ra] = fa ? (int16_t)wa : (int16_t)0;
+            syx[st + rb] = ((uint32_t)y << 16) | xb;
+            sw[st + rb] = fb ? (int16_t)wb : (int16_t)0;
+        }
+    } else
     // rank inside the bucket by x (ties by index); the first of equal x carries the run sum
-    for (int i = threadIdx.x; i < nv; i += (int)blockDim.x) {
+    for (int i = threadIdx.x; i < nv; i += kNT) {
         const int y = by[i];
         const int st = y ? hist[y - 1] : 0, en = hist[y];
         const uint32_t xi = bxw[i] >> 16;
@@ -655,7 +691,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     }
     __syncthreads();
     // compact the non-zero sorted entries: thread t owns sorted positions [t*pp, (t+1)*pp)
-    const int pp = (nv + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int pp = (nv + kNT - 1) / kNT;
     const int lo = threadIdx.x * pp, hi = min(lo + pp, nv);
     int cnt = 0;
     long long a = 0;
@@ -677,7 +713,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     for (int i = 0; i < wid; ++i) outp += wsum[i];
     int total = 0;
     if (wid == 0) {   // the clip's count is known: publish it before the compaction (successors' walks)
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) total += wsum[i];
+        for (int i = 0; i < (kNT >> 5); ++i) total += wsum[i];
         if (lane == 0) clip_publish_count(status, b, total);
     }
     for (int i = lo; i < hi; ++i) {
@@ -691,7 +727,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     __syncthreads();
     total = *tot_s;
     const int64_t base = *s_off;
-    for (int i = threadIdx.x; i < total; i += (int)blockDim.x) {   // coalesced stores, final positions
+    for (int i = threadIdx.x; i < total; i += kNT) {   // coalesced stores, final positions
         if (base + i >= cap) break;
         const uint32_t yx = bxw[i];
         xs[base + i] = (int32_t)(yx & 0xFFFFu);
@@ -700,7 +736,7 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
     }
     if (threadIdx.x == 0) {
         long long t = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += asum[i];
+        for (int i = 0; i < (kNT >> 5); ++i) t += asum[i];
         area[b] = t;
     }
     __syncthreads();
@@ -755,7 +791,7 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             atomicAdd(&hist[rq[j].w], 2);
         }
         __syncthreads();
-        bucket_scan(hist, nb, wsum);
+        bucket_scan<kThr>(hist, nb, wsum);
         // scatter into buckets: afterwards hist[y] = end of bucket y (= start of bucket y + 1)
 #pragma unroll
         for (int j = 0; j < kRPT; ++j) {
@@ -771,7 +807,7 @@ k_clip_corners_bucket(const int4 *__restrict__ rects, const int64_t *__restrict_
             bxw[p + 1] = ((uint32_t)q.z << 16) | 0x0001u;   by[p + 1] = (int16_t)q.w;
         }
         __syncthreads();
-        bucket_emit(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
+        bucket_emit<true, kThr>(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
                     status, area);
     }
 }
@@ -889,7 +925,7 @@ k_clip_polygons_bucket(const int32_t *__restrict__ vx, const int32_t *__restrict
         for (int i = threadIdx.x; i < nvr; i += kBucketThreads)
             if (sw[i] != 0) atomicAdd(&hist[syx[i] >> 16], 1);
         __syncthreads();
-        bucket_scan(hist, nb, wsum);
+        bucket_scan<kBucketThreads>(hist, nb, wsum);
         for (int i = threadIdx.x; i < nvr; i += kBucketThreads) {
             const int16_t wv = sw[i];
             if (wv == 0) continue;
@@ -899,7 +935,7 @@ k_clip_polygons_bucket(const int32_t *__restrict__ vx, const int32_t *__restrict
             by[p] = (int16_t)(yx >> 16);
         }
         __syncthreads();
-        bucket_emit(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
+        bucket_emit<false, kBucketThreads>(b, B, nb, bxw, syx, by, sw, hist, wsum, asum, &tot_s, &s_off, xs, ys, ws, cap, corner_ptr,
                     status, area);
     }
 }
