@@ -108,6 +108,28 @@ def test_extraction_edge_cases(fcfs):
     assert ei.value.status == fcfs.E_RANGE
 
 
+@pytest.mark.parametrize("per_clip", [1, 7, 300, 1344, 2000, 2600])
+def test_extraction_heavy_ties_per_clip_paths(fcfs, per_clip):
+    """Batched singleton-group clips on a 4-value coordinate grid: identical rects, shared and abutting
+    edges, equal x inside every bucket (the paired rank loop of the per-clip bucket kernel ranks both
+    corners of an edge against the bucket's edges), merged weights +-2 and cancelled corners.  1344 and
+    2000 rects run the two per-clip variants, 2600 the general path; bit-exact vs oracle.extract."""
+    rng = np.random.default_rng(per_clip)
+    clips, T = 12, 8
+    n = clips * per_clip
+    xs = rng.choice([0, 2, 4, 6], size=(n, 2))
+    ys = rng.choice([0, 3, 5, 7], size=(n, 2))
+    x0, x1 = xs.min(1), xs.max(1)
+    y0, y1 = ys.min(1), ys.max(1)
+    x1 = np.where(x1 == x0, x0 + 2, x1)
+    y1 = np.where(y1 == y0, y0 + 1, y1)
+    rects = np.stack([x0, y0, x1, y1], 1).astype(np.int32)
+    cp = np.arange(clips + 1, dtype=np.int64) * per_clip
+    e = oracle.extract(rects, T, None, cp)
+    g = fcfs.vertices_from_rects(_dev(rects, torch.int32), T, None, _dev(cp, torch.int64))
+    _assert_extract_equal(g, e)
+
+
 # ------------------------------------------------------------------ a2-a5: one clip, full window
 
 def _clip_coeffs(fcfs, wl, prec, M=None, N=None, r2=None, layout="dense", shard=None):
