@@ -416,11 +416,27 @@ __device__ __forceinline__ void pass_inplace(V *buf, int L, int Ns, const V *tw2
             }
         } else {
             const V w1 = tw_smem(tw2, (uint32_t)(k * (L / (Ns * R))), g.b2, g.nhi2);
-            V wr = w1;
+            if constexpr (R == 16) {
+                // powers by a tree of depth 4 (w2 = w1^2, w4 = w2^2, w8 = w4^2; w_r = w_{r & 8} w_{r & 4} ...)
+                // instead of a chain of 14 dependent products
+                const V w2 = cmul(w1, w1);
+                const V w3 = cmul(w2, w1);
+                const V w4 = cmul(w2, w2);
+                const V w8 = cmul(w4, w4);
+                v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3); v[4] = cmul(v[4], w4);
+                v[8] = cmul(v[8], w8);
+                v[5] = cmul(v[5], cmul(w4, w1)); v[6] = cmul(v[6], cmul(w4, w2)); v[7] = cmul(v[7], cmul(w4, w3));
+                const V w12 = cmul(w8, w4);
+                v[9] = cmul(v[9], cmul(w8, w1)); v[10] = cmul(v[10], cmul(w8, w2)); v[11] = cmul(v[11], cmul(w8, w3));
+                v[12] = cmul(v[12], w12);
+                v[13] = cmul(v[13], cmul(w12, w1)); v[14] = cmul(v[14], cmul(w12, w2)); v[15] = cmul(v[15], cmul(w12, w3));
+            } else {
+                V wr = w1;
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                v[r] = cmul(v[r], wr);
-                if (r + 1 < R) wr = cmul(wr, w1);
+                for (int r = 1; r < R; ++r) {
+                    v[r] = cmul(v[r], wr);
+                    if (r + 1 < R) wr = cmul(wr, w1);
+                }
             }
         }
         dft<R>(v);
