@@ -105,7 +105,6 @@ fcfs_status launch_gemm_tf32(const CornerSrc &src, const GemmPlan &plan, int32_t
                              const EpiArgs *ea, void *F, bool f16, cudaStream_t s);
 bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 
-// sm_100 check, cached per device (atomics: several host threads call this concurrently)
 // lattice.cu
 bool lattice_eligible(int32_t T, const EpiArgs &ea);
 size_t lattice_ws_bytes(int64_t B, int32_t T);
@@ -114,6 +113,7 @@ fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const i
 fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *x, const int32_t *y, const int32_t *w,
                            int32_t T, const EpiArgs &ea, void *F, void *ws, cudaStream_t s);
 
+// sm_100 check, cached per device (atomics: several host threads call this concurrently)
 static fcfs_status device_ok() {
     static std::atomic<int> cached[64];   // 0 = unknown, 1 = sm_100, 2 = other
     int dev = 0;

@@ -22,9 +22,10 @@
 // Kernels: k_fr_yptr (CSR of the y-sorted corner list over y, sortedness flag), k_fr_table (the
 // two-level e^{-2 pi i p / T} table), k_fr_row0 / k_fr_rows (G, thread = one y and 16 consecutive m:
 // two exact-phase lookups per corner and the angle-addition recurrence over 16 m; written in the
-// [row][y1][y2] order the FFT reads), k_fr_fft (CTA per row: the T1 sub-rows streamed by TMA bulk
-// copies into a double-buffered staging area, Stockham radix-16 FFT in shared memory, outer
-// twiddled accumulation in registers) and k_fr_epilogue (window / pupil / rows, axes, DC, mirror).
+// [row][y1][y2] order the FFT reads), k_fr_fft2 (CTA per (row, range of sub-rows), 2 CTAs / SM: each
+// sub-row arrives by a TMA bulk copy into one padded shared buffer, is transformed in place by Stockham
+// passes (radix 2/4/8 lead, then radix 16), and the outer twiddled sum accumulates X[n] in shared memory)
+// and k_fr_epilogue (window / pupil / rows, axes, DC, mirror).
 // Error (FP64): the FFT's is ~log2(T2) u ||G||_2 per output and ||G|| <= sum |w| (the L1 bound B up
 // to the 1/(4 pi^2 m n) factor), far inside 1e-12 B.
 #include <cstdlib>
@@ -509,6 +510,24 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
         else if (lead == 3) { pass_inplace<8>(buf, g.T2, Ns, tw2, g, y1, ax, pv); Ns = 8; }
         for (; Ns < g.T2; Ns <<= 4) pass_inplace<16>(buf, g.T2, Ns, tw2, g, y1, ax, pv);
         // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
+#ifndef FR_OUTER_TABLE
+        if constexpr (sizeof(typename Cx<V>::S) == 8) {
+            // FP64: a thread's outputs are kThreads apart: its first twiddle from the table (exact integer
+            // phase), the rest by the step e^{-2 pi i kThreads y1 / T} (<= 16 products: error ~16 u)
+            const int o0 = threadIdx.x;
+            V e = tw_ldg(tabT, ((uint32_t)(o0 - N + g.T) * (uint32_t)y1) & maskT, g.lbits, g.nhi);
+            const V step = tw_ldg(tabT, ((uint32_t)kThreads * (uint32_t)y1) & maskT, g.lbits, g.nhi);
+            for (int o = o0; o < nn; o += kThreads) {
+                const int n = o - N;
+                FCFS_DCHECK(pad(n >= 0 ? n : n + g.T2) < LP && (n >= 0 ? n : n + g.T2) < g.T2);
+                const V z = buf[pad(n >= 0 ? n : n + g.T2)];
+                X[o] = cadd(X[o], to_d(cmul(e, z)));
+                e = cmul(e, step);
+            }
+        } else
+#endif
+        // FP32 route: every twiddle from the table (a recurrence in FP32 would spend the split contract's
+        // error budget)
         for (int o = threadIdx.x; o < nn; o += kThreads) {
             const int n = o - N;
             FCFS_DCHECK(pad(n >= 0 ? n : n + g.T2) < LP && (n >= 0 ? n : n + g.T2) < g.T2);
@@ -516,6 +535,7 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
             const uint32_t ph = ((uint32_t)(n + g.T) * (uint32_t)y1) & maskT;
             X[o] = cadd(X[o], to_d(cmul(tw_ldg(tabT, ph, g.lbits, g.nhi), z)));
         }
+
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
     }
