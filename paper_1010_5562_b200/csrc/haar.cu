@@ -24,6 +24,12 @@ namespace fcfs {
 namespace haar {
 
 constexpr int kThreads = 256;
+#ifndef HAAR_UC
+#define HAAR_UC 8
+#endif
+#ifndef HAAR_UR
+#define HAAR_UR 4
+#endif
 
 // scratch per clip: for each level j (n = 2^j cells per side) five int64 n x n arrays at
 // level_off(j) = 5 (4^j - 1) / 3: [0] hh, [1] hg partial, [2] hg column totals, [3] gh partial,
@@ -100,13 +106,28 @@ __global__ void k_haar_cols(const int64_t *scratch, const int64_t *__restrict__ 
         if (j == 0) o[0] = (double)area[b] / (double)T;   // X_{0,0,0}
         int64_t *Lw = const_cast<int64_t *>(L);
         int64_t run = 0;
-        for (int64_t ky = 0; ky < n; ++ky) {
-            const int64_t c = ky * n + kx;
-            const int64_t part = L[1 * n * n + c], tot = L[2 * n * n + c];
-            o[ky * T + n + kx] = (double)(part + s * run) * scale;
-            run += tot;
-            if (part) Lw[1 * n * n + c] = 0;   // leave the scratch zero for the next call (sparse clears)
-            if (tot) Lw[2 * n * n + c] = 0;
+        // kU rows per step, all loads first: the loads of a step are independent, and issuing them
+        // together hides the latency that a load -> store -> next load walk would expose per row
+        constexpr int kU = HAAR_UC;
+        for (int64_t k0 = 0; k0 < n; k0 += kU) {
+            int64_t part[kU], tot[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t c = (k0 + u) * n + kx;
+                const bool ok = k0 + u < n;
+                part[u] = ok ? L[1 * n * n + c] : 0;
+                tot[u] = ok ? L[2 * n * n + c] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t ky = k0 + u;
+                if (ky >= n) break;
+                const int64_t c = ky * n + kx;
+                o[ky * T + n + kx] = (double)(part[u] + s * run) * scale;
+                run += tot[u];
+                if (part[u]) Lw[1 * n * n + c] = 0;   // leave the scratch zero for the next call (sparse clears)
+                if (tot[u]) Lw[2 * n * n + c] = 0;
+            }
         }
     }
 }
@@ -125,26 +146,40 @@ __global__ void k_haar_rows(const int64_t *scratch, int64_t B, int32_t T, int J,
         const int64_t *L = scratch + b * clip_scratch(J) + level_off(j);
         double *o = out + b * (int64_t)T * T + (n + ky) * T;
         int64_t carry = 0;
-        for (int64_t k0 = 0; k0 < n; k0 += 32) {
-            const int64_t kx = k0 + lane;
-            const bool ok = kx < n;
-            const int64_t c = ky * n + kx;
-            const int64_t tot = ok ? L[4 * n * n + c] : 0;
-            const int64_t part = ok ? L[3 * n * n + c] : 0, hh = ok ? L[0 * n * n + c] : 0;
-            int64_t inc = tot;
-            for (int d = 1; d < 32; d <<= 1) {
-                const int64_t v = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += v;
+        constexpr int kU = HAAR_UR;   // 32-column chunks per step, all loads first (independent: latency overlapped)
+        for (int64_t k00 = 0; k00 < n; k00 += 32 * kU) {
+            int64_t tot[kU], part[kU], hh[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t kx = k00 + 32 * u + lane;
+                const bool ok = kx < n;
+                const int64_t c = ky * n + kx;
+                tot[u] = ok ? L[4 * n * n + c] : 0;
+                part[u] = ok ? L[3 * n * n + c] : 0;
+                hh[u] = ok ? L[0 * n * n + c] : 0;
             }
-            if (ok) {
-                o[kx] = (double)(part + s * (carry + inc - tot)) * scale;
-                o[n + kx] = (double)hh * scale;
-                int64_t *Lw = const_cast<int64_t *>(L);
-                if (tot) Lw[4 * n * n + c] = 0;
-                if (part) Lw[3 * n * n + c] = 0;
-                if (hh) Lw[0 * n * n + c] = 0;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t k0 = k00 + 32 * u;
+                if (k0 >= n) break;   // uniform
+                const int64_t kx = k0 + lane;
+                const bool ok = kx < n;
+                const int64_t c = ky * n + kx;
+                int64_t inc = tot[u];
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int64_t v = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += v;
+                }
+                if (ok) {
+                    o[kx] = (double)(part[u] + s * (carry + inc - tot[u])) * scale;
+                    o[n + kx] = (double)hh[u] * scale;
+                    int64_t *Lw = const_cast<int64_t *>(L);
+                    if (tot[u]) Lw[4 * n * n + c] = 0;
+                    if (part[u]) Lw[3 * n * n + c] = 0;
+                    if (hh[u]) Lw[0 * n * n + c] = 0;
+                }
+                carry += __shfl_sync(0xffffffffu, inc, 31);
             }
-            carry += __shfl_sync(0xffffffffu, inc, 31);
         }
     }
 }
