@@ -205,9 +205,13 @@ fcfs_status fcfs_vertices_from_polygons(const int32_t *vx, const int32_t *vy, in
  *            as produced by fcfs_vertices_from_* (any order);  area  int64 [B] (device).
  * out        double [B][T][T] (device): out[b][r][c], r = y index: (0,0) = X_{0,0,0} = area/T; level j:
  *            hg at (ky, 2^j + kx), gh at (2^j + ky, kx), hh at (2^j + ky, 2^j + kx).  Every value is
- *            exact (an integer times 2^j / T).  Workspace: 5 (T^2 - 1) / 3 int64 per clip; it must be
- *            zero-initialised before its first use, and every successful call leaves it zero (the
- *            kernels clear the entries they used instead of an O(T^2) memset per call).
+ *            exact (an integer times 2^j / T).  Clips whose corners are sorted by y (the order
+ *            fcfs_vertices_from_* emit) take a band sweep that reads only the corners; any other order
+ *            takes a scatter of the corners into a per-clip scratch (a device flag picks the path: no
+ *            host sync).  Workspace (fcfs_haar_workspace_bytes): the scatter scratch, 5 (T^2 - 1) / 3
+ *            int64 per clip, which must be zero-initialised before its first use and which every
+ *            successful call leaves zero (the kernels clear the entries they used instead of an O(T^2)
+ *            memset per call), then B (T + 1) + 1 int32 of per-call scratch (row pointers, the flag).
  * ------------------------------------------------------------------------------------------ */
 size_t fcfs_haar_workspace_bytes(int64_t B, int32_t T);
 fcfs_status fcfs_haar(const int64_t *corner_ptr, int64_t B, int64_t K, const int32_t *x, const int32_t *y,

@@ -289,7 +289,8 @@ class HaarPlan:
         if nb == 0:
             raise FcfsError(E_INVALID, "fcfs_haar_workspace_bytes")
         self.ws = _ws(nb, device)
-        self.ws.zero_()                      # fcfs_haar: zero before first use, left zero by every call
+        self.ws.zero_()                      # fcfs_haar: the scatter scratch is zeroed once, left zero by every call
+        self.scratch_bytes = self.B * 5 * (self.T * self.T - 1) // 3 * 8
         self.out = torch.empty((self.B, self.T, self.T), dtype=torch.float64, device=device)
 
     def run(self, x, y, w, area, corner_ptr=None, stream=None):

@@ -951,7 +951,30 @@ def test_haar_plan_reuse_leaves_workspace_zero(fcfs):
         for b in range(3):
             sl = slice(cp[b], cp[b + 1])
             assert np.array_equal(H[b], oracle.haar(x[sl], y[sl], w[sl], 64))
-    assert torch.count_nonzero(plan.ws).item() == 0
+    assert torch.count_nonzero(plan.ws[:plan.scratch_bytes]).item() == 0
+
+
+@pytest.mark.parametrize("T", [64, 256])
+def test_haar_any_corner_order_scatter_path(fcfs, T):
+    """Corner lists NOT sorted by y (fcfs_haar accepts any order): the device flag sends them through the
+    scatter + scan path; bitwise equal to the oracle and to the band sweep on the sorted list, and the
+    scatter scratch is left zero."""
+    ps = inputs.polygon_clips(11, clips=3, T=T, n_poly=14, max_cols=6, size=max(4, T // 16))
+    g = _gpu_polys(fcfs, ps)
+    cp = g["corner_ptr"].cpu().numpy()
+    x, y, w = (g[k].cpu().numpy() for k in ("x", "y", "w"))
+    plan = fcfs.HaarPlan(3, T)
+    Hs = plan.run(g["x"], g["y"], g["w"], g["area"], g["corner_ptr"]).cpu().numpy().copy()   # sorted: band sweep
+    rng = np.random.default_rng(T)
+    perm = np.concatenate([cp[b] + rng.permutation(cp[b + 1] - cp[b]) for b in range(3)]).astype(np.int64)
+    xp, yp, wp = (torch.from_numpy(np.ascontiguousarray(a[perm])).cuda() for a in (x, y, w))
+    Hu = plan.run(xp, yp, wp, g["area"], g["corner_ptr"]).cpu().numpy()
+    for b in range(3):
+        sl = slice(cp[b], cp[b + 1])
+        ref = oracle.haar(x[sl], y[sl], w[sl], T)
+        assert np.array_equal(Hs[b], ref), f"band sweep clip {b}"
+        assert np.array_equal(Hu[b], ref), f"scatter path clip {b}"
+    assert torch.count_nonzero(plan.ws[:plan.scratch_bytes]).item() == 0
 
 
 # ------------------------------------------------------------------ maximum sizes and degenerate cases
