@@ -438,7 +438,7 @@ def bench_haar(args, rank, world, dev):
     peaks, src = load_peaks()
     ach = coefs * 8.0 / (h_ms / 1e3) / 1e9        # algorithmic bytes: the 8-byte coefficient written once
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "kernel": "fcfs_haar (scatter + col/row scans)",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "kernel": "fcfs_haar (band sweep: k_haar_yptr + k_haar_band)",
             "alg_bytes_per_launch": coefs * 8.0, "kernel_ms_per_launch": round(h_ms, 4),
             "stage_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in stages.items()},
             "peak_source": f"{src} HBM copy bandwidth"}
