@@ -287,13 +287,19 @@ __global__ void __launch_bounds__(kBT) k_haar_band(const int32_t *__restrict__ x
         if (v) atomicAdd((unsigned long long *)&colp[kx], (unsigned long long)v);
     }
     const int per = (n + kBT - 1) / kBT;   // scan: thread tid owns cells [tid per, (tid + 1) per)
+    // this thread's first corner of the current row, loaded one row ahead (the loads overlap the previous
+    // row's scan and outputs instead of stalling every row at the barrier after the scatter)
+    int32_t px = T, py = 0, pw = 0;
+    if (ky0 < ky1 && k0 + rb[0] + tid < k0 + rb[1]) {
+        const int64_t k = k0 + rb[0] + tid;
+        px = __ldg(x + k); py = __ldg(y + k); pw = __ldg(w + k);
+    }
     for (int ky = ky0; ky < ky1; ++ky) {
         // the corners of cell row ky: one contiguous range of the y-sorted list
         const int64_t pa = k0 + rb[ky - ky0], pe = k0 + rb[ky - ky0 + 1];
-        for (int64_t k = pa + tid; k < pe; k += kBT) {
-            const int32_t xk = __ldg(x + k), yk = __ldg(y + k);
-            if (xk >= T) continue;
-            const long long wk = __ldg(w + k);
+        auto add = [&](int32_t xk, int32_t yk, int32_t wi) {
+            if (xk >= T) return;
+            const long long wk = wi;
             const int32_t kx = xk >> sh, dx = xk - (kx << sh), dy = yk - (ky << sh);
             const long long ihx = -(long long)(dx <= hs ? dx : s - dx), ihy = -(long long)(dy <= hs ? dy : s - dy);
             const long long igx = s - dx, igy = s - dy;
@@ -302,6 +308,12 @@ __global__ void __launch_bounds__(kBT) k_haar_band(const int32_t *__restrict__ x
             atomicAdd((unsigned long long *)&pgh[kx], (unsigned long long)(wk * igx * ihy));
             atomicAdd((unsigned long long *)&tgh[kx], (unsigned long long)(wk * ihy));
             atomicAdd((unsigned long long *)&hhv[kx], (unsigned long long)(wk * ihx * ihy));
+        };
+        if (pa + tid < pe) add(px, py, pw);
+        for (int64_t k = pa + tid + kBT; k < pe; k += kBT) add(__ldg(x + k), __ldg(y + k), __ldg(w + k));
+        if (ky + 1 < ky1) {
+            const int64_t qe = k0 + rb[ky - ky0 + 2];
+            if (pe + tid < qe) { px = __ldg(x + pe + tid); py = __ldg(y + pe + tid); pw = __ldg(w + pe + tid); }
         }
         __syncthreads();
         // exclusive prefix of the gh row totals over kx, in place
