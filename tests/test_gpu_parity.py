@@ -954,7 +954,7 @@ def test_haar_plan_reuse_leaves_workspace_zero(fcfs):
     assert torch.count_nonzero(plan.ws[:plan.scratch_bytes]).item() == 0
 
 
-@pytest.mark.parametrize("T", [64, 256])
+@pytest.mark.parametrize("T", [64, 256, 2048])
 def test_haar_any_corner_order_scatter_path(fcfs, T):
     """Corner lists NOT sorted by y (fcfs_haar accepts any order): the device flag sends them through the
     scatter + scan path; bitwise equal to the oracle and to the band sweep on the sorted list, and the
