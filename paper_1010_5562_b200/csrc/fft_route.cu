@@ -510,7 +510,6 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
         else if (lead == 3) { pass_inplace<8>(buf, g.T2, Ns, tw2, g, y1, ax, pv); Ns = 8; }
         for (; Ns < g.T2; Ns <<= 4) pass_inplace<16>(buf, g.T2, Ns, tw2, g, y1, ax, pv);
         // outer step: X[n] += e^{-2 pi i n y1 / T} Z[n mod T2]
-#ifndef FR_OUTER_TABLE
         if constexpr (sizeof(typename Cx<V>::S) == 8) {
             // FP64: a thread's outputs are kThreads apart: its first twiddle from the table (exact integer
             // phase), the rest by the step e^{-2 pi i kThreads y1 / T} (<= 16 products: error ~16 u)
@@ -525,7 +524,6 @@ k_fr_fft2(const V *__restrict__ Gd, const double2 *__restrict__ GT, const V *__r
                 e = cmul(e, step);
             }
         } else
-#endif
         // FP32 route: every twiddle from the table (a recurrence in FP32 would spend the split contract's
         // error budget)
         for (int o = threadIdx.x; o < nn; o += kThreads) {
