@@ -298,10 +298,6 @@ __global__ void k_band_compact(const unsigned long long *__restrict__ keys, cons
     const unsigned long long mask = (1ull << cb) - 1;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // lane 0 carries the warp's running area of one clip across iterations (one atomic per warp and clip
-    // run instead of per iteration: a single large clip otherwise serialises ~K/32 atomics on area[0])
-    int64_t acc_b = -1;
-    long long acc_a = 0;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const int64_t i = i0 + lane;
         bool keep = false;
@@ -641,10 +637,10 @@ __device__ __forceinline__ void bucket_emit(int64_t b, int64_t B, int nb, uint32
         // one edge and ranks both of its corners in one pass over the bucket's edges (8-byte loads; four
         // compares per load instead of one)
         for (int t = threadIdx.x; 2 * t < nv; t += kNT) {
-            const int i0 = 2 * t, i1 = i0 + 1;
+            const int i0 = 2 * t;
             const int y = by[i0];
             const int st = y ? hist[y - 1] : 0, en = hist[y];
-            FCFS_DCHECK((st & 1) == 0 && (en & 1) == 0 && st <= i0 && i1 < en);
+            FCFS_DCHECK((st & 1) == 0 && (en & 1) == 0 && st <= i0 && i0 + 1 < en);
             const uint2 me = *(const uint2 *)(bxw + i0);
             const uint32_t xa = me.x >> 16, xb = me.y >> 16;
             int ra = 0, rb = 0, wa = 0, wb = 0;
