@@ -26,7 +26,7 @@
 namespace fcfs {
 namespace sm {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;              // 1024 measured slower (64-register cap, idle warps in the output phase)
 constexpr int kItems = 4;
 constexpr int kMaxRaw = kThreads * kItems;   // 2048 raw corners per clip
 constexpr int kMaxGroup = 100;
@@ -135,17 +135,19 @@ __device__ void group_union(Shared &S, uint8_t *dyn, const int4 *rects, int n, i
     compress_s(vy, 2 * n, tmp, uy, &S.nxy[1], S.cub.scan);
     const int nx = S.nxy[0], ny = S.nxy[1];
     FCFS_DCHECK(nx >= 1 && ny >= 1 && nx <= 2 * n && ny <= 2 * n);
-    for (int t = threadIdx.x; t < nx * ny; t += blockDim.x) grid[t] = 0;
+    // row stride ny + 1 (odd): the column pass (lanes along i) hits 32 distinct banks, not one
+    const int ld = ny + 1;
+    for (int t = threadIdx.x; t < nx * ld; t += blockDim.x) grid[t] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int4 q = sr[i];
         if (q.x == q.z) continue;
         const int i0 = find_s(ux, nx, q.x), i1 = find_s(ux, nx, q.z);
         const int j0 = find_s(uy, ny, q.y), j1 = find_s(uy, ny, q.w);
-        atomicAdd(&grid[i0 * ny + j0], 1);
-        atomicAdd(&grid[i1 * ny + j0], -1);
-        atomicAdd(&grid[i0 * ny + j1], -1);
-        atomicAdd(&grid[i1 * ny + j1], 1);
+        atomicAdd(&grid[i0 * ld + j0], 1);
+        atomicAdd(&grid[i1 * ld + j0], -1);
+        atomicAdd(&grid[i0 * ld + j1], -1);
+        atomicAdd(&grid[i1 * ld + j1], 1);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -153,12 +155,12 @@ __device__ void group_union(Shared &S, uint8_t *dyn, const int4 *rects, int n, i
         int carry = 0;
         for (int j0 = 0; j0 < ny; j0 += 32) {
             const int j = j0 + lane;
-            int v = j < ny ? grid[i * ny + j] : 0;
+            int v = j < ny ? grid[i * ld + j] : 0;
             for (int d = 1; d < 32; d <<= 1) {
                 const int u = __shfl_up_sync(0xffffffffu, v, d);
                 if (lane >= d) v += u;
             }
-            if (j < ny) grid[i * ny + j] = carry + v;
+            if (j < ny) grid[i * ld + j] = carry + v;
             carry += __shfl_sync(0xffffffffu, v, 31);
         }
     }
@@ -167,23 +169,23 @@ __device__ void group_union(Shared &S, uint8_t *dyn, const int4 *rects, int n, i
         int carry = 0;
         for (int i0 = 0; i0 < nx; i0 += 32) {
             const int i = i0 + lane;
-            int v = i < nx ? grid[i * ny + j] : 0;
+            int v = i < nx ? grid[i * ld + j] : 0;
             for (int d = 1; d < 32; d <<= 1) {
                 const int u = __shfl_up_sync(0xffffffffu, v, d);
                 if (lane >= d) v += u;
             }
-            if (i < nx) grid[i * ny + j] = carry + v > 0 ? 1 : 0;   // union indicator
+            if (i < nx) grid[i * ld + j] = carry + v > 0 ? 1 : 0;   // union indicator
             carry += __shfl_sync(0xffffffffu, v, 31);
         }
     }
     __syncthreads();
     for (int i = warp; i < nx; i += nw)                           // mixed difference
         for (int j = lane; j < ny; j += 32) {
-        const int t = i * ny + j;
+        const int t = i * ld + j;
         const int c00 = grid[t];
-        const int cm0 = i > 0 ? grid[t - ny] : 0;
+        const int cm0 = i > 0 ? grid[t - ld] : 0;
         const int c0m = j > 0 ? grid[t - 1] : 0;
-        const int cmm = (i > 0 && j > 0) ? grid[t - ny - 1] : 0;
+        const int cmm = (i > 0 && j > 0) ? grid[t - ld - 1] : 0;
         const int wv = c00 - cm0 - c0m + cmm;
         if (wv != 0) push_raw(S, ux[i], uy[j], wv);
         }
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_small_clip(Args A) {
 size_t small_clip_smem_bytes(int32_t T, int64_t max_group) {
     const int64_t mg = max_group < 1 ? 1 : max_group;
     const size_t scratch = sizeof(int4) * sm::kMaxGroup + sizeof(int32_t) * 10 * sm::kMaxGroup +
-                           sizeof(int32_t) * (size_t)(2 * mg) * (size_t)(2 * mg);
+                           sizeof(int32_t) * (size_t)(2 * mg) * (size_t)(2 * mg + 1);
     const size_t table = sizeof(double2) * ((size_t)T + sm::kMaxRaw);
     return sm::kSharedBytes + (scratch > table ? scratch : table);
 }
