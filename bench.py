@@ -45,9 +45,10 @@ def parse():
     ap.add_argument("--haar-tiles", type=int, default=16, help="haar: tiles per side (T=1024 tiles)")
     ap.add_argument("--prec", default=None, choices=["fp64", "tf32x3", "f16x3"])
     ap.add_argument("--clips", type=int, default=4096, help="c3 clips per GPU")
-    ap.add_argument("--shard", default="rows", choices=["rows", "vblock"],
+    ap.add_argument("--shard", default="rows", choices=["rows", "peers", "vblock"],
                     help="single-clip configs (c1, c2, c4, c5) on N > 1 GPUs: frequency rows + all_gather, "
-                         "or vertex blocks + reduce_scatter")
+                         "frequency rows stored by the epilogue into every rank's window over NVLink "
+                         "(fcfs_coeffs_rows_to_peers), or vertex blocks + reduce_scatter")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--route", default=None, choices=["auto", "gemm", "fft"],
                     help="single-clip configs: fcfs_options.route (default: the library's cost model)")
@@ -593,12 +594,14 @@ def main():
         plan = _P()
         if args.shard == "rows":
             sharded = fdist.RowsSharded(wl.T, wl.M, wl.N, prec, rank, world, device=dev, route=args.route)
+        elif args.shard == "peers":
+            sharded = fdist.RowsPeers(wl.T, wl.M, wl.N, prec, rank, world, device=dev, route=args.route)
         else:
             sharded = fdist.VertexSharded(wl.T, wl.M, wl.N, prec, rank, world, device=dev)
 
         def coeffs():
             g_ = gathered
-            if args.shard == "rows":
+            if args.shard in ("rows", "peers"):
                 return sharded.run(g_["x"], g_["y"], g_["w"], g_["K"], g_["area"])
             return sharded.run(g_["x"], g_["y"], g_["w"], g_["K"])
         out_bytes = plan.out.numel() * plan.out.element_size()

@@ -271,6 +271,19 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
                         int64_t area, int32_t T, const fcfs_window *win, fcfs_precision prec,
                         const fcfs_shard *shard, const fcfs_options *opt, void *F, void *ws,
                         size_t ws_bytes, void *stream);
+/* The ROWS shard of one clip with its all_gather fused into the epilogue (multi-GPU single clips,
+ * BASELINE.json north_star (6); linearity Prop. 2): as fcfs_coeffs with a FCFS_SHARD_ROWS
+ * shard and the DENSE layout, but instead of writing the shard's rows to F, the epilogue stores every
+ * output (m, n) of rows [m_lo, m_hi] at its FULL-window position (m + M)(2N + 1) + (n + N) into each of
+ * peers[0 .. n_peers) — full-window buffers of all ranks (this rank's own and the peers' mapped into
+ * this process, e.g. by CUDA IPC over NVLink).  1 <= n_peers <= 8.  The kernel ends with a system-scope
+ * fence; the caller orders the ranks (a barrier or any collective after this call on every rank)
+ * before reading a buffer.  Workspace: fcfs_coeffs_workspace_bytes with the same shard. */
+fcfs_status fcfs_coeffs_rows_to_peers(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K,
+                                      int64_t area, int32_t T, const fcfs_window *win,
+                                      fcfs_precision prec, const fcfs_shard *shard,
+                                      const fcfs_options *opt, void *const *peers, int32_t n_peers,
+                                      void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * a3-a5 batched — B independent clips (the paper's tiles) in one launch sequence.

@@ -62,4 +62,16 @@ __device__ __forceinline__ void store_out(void *F, int64_t o, double2 v, int out
     else ((double2 *)F)[o] = v;
 }
 
+// an output (m, n) of a single-clip ROWS epilogue: to F at the shard-relative index o_rel, or — the peer
+// mode — to every peer buffer at the full DENSE-window index (the all_gather of the rows done by the
+// epilogue's own stores over NVLink; the caller orders the peers' reads after this kernel)
+__device__ __forceinline__ void store_row_out(const EpiArgs &ea, void *F, int64_t o_rel, int m, int n, double2 v) {
+    if (ea.peer_n == 0) {
+        store_out(F, o_rel, v, ea.out_f32);
+        return;
+    }
+    const int64_t o = (int64_t)(m + ea.M) * (2 * ea.N + 1) + (n + ea.N);
+    for (int p = 0; p < ea.peer_n; ++p) store_out(ea.peer[p], o, v, ea.out_f32);
+}
+
 }  // namespace fcfs

@@ -155,7 +155,12 @@ struct EpiArgs {
     const int64_t *area_dev;     // per-clip area (device) or nullptr
     int64_t area_host;
     int32_t out_f32;             // 1: complex64, 0: complex128
+    // ROWS shard written straight into full-window buffers (fcfs_coeffs_rows_to_peers): every output of
+    // this rank's rows goes to peer[0 .. peer_n) at its full DENSE-window position; 0 = write F as usual
+    int32_t peer_n = 0;
+    void *peer[8] = {};
 };
+constexpr int kMaxPeers = 8;
 
 __host__ __device__ inline int32_t ilog2_ceil(int64_t v) {
     int32_t b = 0;

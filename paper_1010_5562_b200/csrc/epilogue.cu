@@ -62,10 +62,10 @@ __global__ void k_epilogue(const double *__restrict__ P_ws, GemmPlan pl, EpiArgs
             if (ea.layout == FCFS_LAYOUT_DENSE && ea.r2 >= 0.0)
                 keep = (double)m * (double)m + (double)n * (double)n <= ea.r2;
             v = keep ? coeff(P_ws, pl, ea, clip, m, n, dc) : make_double2(0.0, 0.0);
-            const int64_t o = off + (n - nlo);
-            store_out(F, o, v, ea.out_f32);
+            store_row_out(ea, F, off + (n - nlo), m, n, v);
         }
     }
+    if (ea.peer_n) __threadfence_system();   // peer stores performed before the kernel's completion is seen
 }
 
 fcfs_status launch_epilogue(const GemmPlan &plan, const double *P_ws, const EpiArgs &ea, void *F, cudaStream_t s) {

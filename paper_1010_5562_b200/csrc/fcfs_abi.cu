@@ -618,9 +618,10 @@ fcfs_status fcfs_small_clip(const int32_t *rects, int64_t R, const int64_t *grou
                              (cudaStream_t)stream);
 }
 
-fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
-                        const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard,
-                        const fcfs_options *opt, void *F, void *ws, size_t ws_bytes, void *stream) {
+static fcfs_status coeffs_one(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
+                              const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard,
+                              const fcfs_options *opt, void *F, void *ws, size_t ws_bytes, void *stream,
+                              void *const *peers, int32_t n_peers) {
     if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
     fcfs_status st = check_window(win);
     if (st == FCFS_OK) st = check_options(opt);
@@ -662,6 +663,8 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     ea.m_lo = m_lo; ea.m_hi = m_hi; ea.T = T; ea.area_dev = nullptr; ea.area_host = area;
     ea.out_f32 = prec == FCFS_FP64 ? 0 : 1;
     ea.out_per_clip = 0;
+    ea.peer_n = n_peers;
+    for (int32_t i = 0; i < n_peers; ++i) ea.peer[i] = peers[i];
     if (vblock) {
         st = launch_block_area(src, W.area, s);
         if (st != FCFS_OK) return st;
@@ -701,6 +704,33 @@ fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, in
     if (st != FCFS_OK || fused) return st;
     StageScope scope(kStageEpilogue, s);
     return launch_epilogue(plan, W.P, ea, F, s);
+}
+
+fcfs_status fcfs_coeffs(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area, int32_t T,
+                        const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard,
+                        const fcfs_options *opt, void *F, void *ws, size_t ws_bytes, void *stream) {
+    return coeffs_one(x, y, w, K, area, T, win, prec, shard, opt, F, ws, ws_bytes, stream, nullptr, 0);
+}
+
+fcfs_status fcfs_coeffs_rows_to_peers(const int32_t *x, const int32_t *y, const int32_t *w, int64_t K, int64_t area,
+                                      int32_t T, const fcfs_window *win, fcfs_precision prec, const fcfs_shard *shard,
+                                      const fcfs_options *opt, void *const *peers, int32_t n_peers, void *ws,
+                                      size_t ws_bytes, void *stream) {
+    if (!shard || shard->kind != FCFS_SHARD_ROWS) {
+        set_error("fcfs_coeffs_rows_to_peers: needs a ROWS shard");
+        return FCFS_E_INVALID;
+    }
+    if (!win || win->layout != FCFS_LAYOUT_DENSE) {
+        set_error("fcfs_coeffs_rows_to_peers: ROWS shards use the DENSE layout");
+        return FCFS_E_INVALID;
+    }
+    if (!peers || n_peers < 1 || n_peers > kMaxPeers) {
+        set_error("fcfs_coeffs_rows_to_peers: n_peers=%d outside [1, %d]", n_peers, kMaxPeers);
+        return FCFS_E_INVALID;
+    }
+    for (int32_t i = 0; i < n_peers; ++i)
+        if (!peers[i]) { set_error("fcfs_coeffs_rows_to_peers: peer %d is NULL", i); return FCFS_E_INVALID; }
+    return coeffs_one(x, y, w, K, area, T, win, prec, shard, opt, peers[0], ws, ws_bytes, stream, peers, n_peers);
 }
 
 fcfs_status fcfs_coeffs_async(const int32_t *x, const int32_t *y, const int32_t *w, const int64_t *K_dev, int64_t K_cap,

@@ -615,8 +615,9 @@ __global__ void k_fr_epilogue(const double2 *__restrict__ Xs, const double2 *__r
                 v = make_double2(re, neg ? -im : im);
             }
         }
-        store_out(F, off + (n - nlo), v, ea.out_f32);
+        store_row_out(ea, F, off + (n - nlo), m, n, v);
     }
+    if (ea.peer_n) __threadfence_system();   // peer stores performed before the kernel's completion is seen
 }
 
 }  // namespace fr

@@ -9,6 +9,9 @@ By linearity (Prop. 2) and separability (Lemma 1)
             rank order, ARE the canonical (y, x)-sorted list, and the band areas sum to the clip's.
 * rows    — one clip, disjoint signed frequency-row ranges m in [m_lo, m_hi] (fcfs_shard ROWS);
             ranks all_gather their rows into the full window.
+* peers   — the rows shard with its all_gather fused into the epilogue: every rank's kernel stores its
+            rows straight into every rank's full-window buffer (fcfs_coeffs_rows_to_peers; peer buffers
+            mapped by CUDA IPC over NVLink), then one collective orders the ranks before the window is read.
 * vblock  — one clip, contiguous blocks of the canonical corner list (fcfs_shard VERTEX_BLOCK, on the
             row-bucket GEMM route: the lattice-FFT route would repeat its per-row FFTs on every rank);
             every rank computes the whole window from its block, the partial windows are summed with a
@@ -171,6 +174,66 @@ class RowsSharded:
             if b >= a:
                 parts.append(self.gathered[r * self.per:r * self.per + (b - a + 1)])
         return torch.cat(parts).reshape(-1)
+
+
+def peer_buffers(full, group=None):
+    """Device pointers of every rank's `full` buffer in this process (rank order): this rank's own pointer
+    and the other ranks' buffers opened from their CUDA IPC handles (torch's storage sharing; same node,
+    P2P over NVLink).  Returns (pointers, keep-alive storages)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world == 1:
+        return [full.data_ptr()], []
+    handle = full.untyped_storage()._share_cuda_()
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    ptrs, keep = [], []
+    for r in range(world):
+        if r == rank:
+            ptrs.append(full.data_ptr())
+            continue
+        st = torch.UntypedStorage._new_shared_cuda(*handles[r])
+        keep.append(st)
+        ptrs.append(st.data_ptr())
+    return ptrs, keep
+
+
+class RowsPeers:
+    """Full dense window of one clip with the rows' all_gather fused into the epilogue: this rank computes
+    its signed rows (fcfs_shard ROWS) and its epilogue stores every output at its full-window position into
+    every rank's buffer (fcfs_coeffs_rows_to_peers over NVLink), then one small all_reduce orders the ranks
+    (each rank's stores precede its collective; the collective completes after all ranks joined).  No
+    all_gather of the rows, no per-rank slice buffers.  ``run_local`` (tests) replaces the CUDA call."""
+
+    def __init__(self, T, M, N, prec, rank, world, device="cuda", route=None, group=None, run_local=None):
+        self.T, self.M, self.N, self.prec, self.route = int(T), int(M), int(N), prec, route
+        self.world, self.device, self.run_local = world, device, run_local
+        self.m_lo, self.m_hi = row_range(M, rank, world)
+        self.dtype = torch.complex128 if prec == "fp64" else torch.complex64
+        self.full = torch.zeros((2 * M + 1) * (2 * N + 1), dtype=self.dtype, device=device)
+        self.ptrs, self._keep = peer_buffers(self.full, group) if run_local is None else ([], [])
+        self.flag = torch.zeros(1, dtype=torch.float32, device=device)
+        self.plans = {}
+
+    def run(self, x, y, w, K, area, group=None):
+        if self.m_hi >= self.m_lo:
+            if self.run_local is not None:
+                self.run_local(self, x[:K], y[:K], w[:K], area)
+            else:
+                plan = self.plans.get(K)
+                if plan is None:
+                    from . import fcfs
+                    sh = fcfs.Shard(fcfs.SHARD_ROWS, self.m_lo, self.m_hi, 0, 0)
+                    plan = fcfs.CoeffsPlan(K, self.T, self.M, self.N, prec=self.prec, shard=sh, device=self.device,
+                                           route=self.route)
+                    self.plans = {K: plan}
+                plan.run_to_peers(x[:K], y[:K], w[:K], area, self.ptrs)
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(self.flag, group=group)   # stream-ordered: every rank's peer stores precede it
+        else:                                         # gloo (tests): host barrier after the device work
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+        return self.full
 
 
 class VertexSharded:

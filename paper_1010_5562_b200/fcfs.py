@@ -107,6 +107,9 @@ _lib.fcfs_coeffs_route.argtypes = [_i64, _i32, _WP, _i32, _SP, _OP]
 _lib.fcfs_coeffs_route.restype = _i32
 _lib.fcfs_coeffs.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _OP, _P, _P, _sz, _P]
 _lib.fcfs_coeffs.restype = _i32
+_lib.fcfs_coeffs_rows_to_peers.argtypes = [_P, _P, _P, _i64, _i64, _i32, _WP, _i32, _SP, _OP,
+                                           ctypes.POINTER(ctypes.c_void_p), _i32, _P, _sz, _P]
+_lib.fcfs_coeffs_rows_to_peers.restype = _i32
 _lib.fcfs_batched_workspace_bytes.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32, _OP]
 _lib.fcfs_batched_workspace_bytes.restype = _sz
 _lib.fcfs_coeffs_batched_form.argtypes = [_i64, _i64, _i64, _i32, _WP, _i32, _OP]
@@ -148,7 +151,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
             "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band",
             "fcfs_small_clip_supported", "fcfs_small_clip", "fcfs_vertices_from_rects_async",
-            "fcfs_coeffs_async"]
+            "fcfs_coeffs_async", "fcfs_coeffs_rows_to_peers"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -458,6 +461,18 @@ class CoeffsPlan:
                               _stream(stream))
         _check(st, "fcfs_coeffs")
         return out
+
+    def run_to_peers(self, x, y, w, area, peers, stream=None):
+        """ROWS shard with its all_gather fused into the epilogue (fcfs_coeffs_rows_to_peers): this rank's rows
+        are stored at their full-window positions into every buffer of ``peers`` (device pointers or tensors
+        of the full DENSE window: this rank's own and the other ranks' mapped into this process)."""
+        ptrs = [p if isinstance(p, int) else p.data_ptr() for p in peers]
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        st = _lib.fcfs_coeffs_rows_to_peers(_ptr(x), _ptr(y), _ptr(w), self.K, int(area), self.T,
+                                            ctypes.byref(self.win), self.prec, ctypes.byref(self.shard),
+                                            ctypes.byref(self.opt), arr, len(ptrs), _ptr(self.ws), self.ws.numel(),
+                                            _stream(stream))
+        _check(st, "fcfs_coeffs_rows_to_peers")
 
 
 def coeffs_route(K, T, M, N, r2=-1.0, layout="dense", prec="fp64", shard=None, route=None):

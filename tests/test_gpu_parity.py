@@ -5,6 +5,8 @@ seeded inputs.  Tolerances (BASELINE.json north_star):
   FP64:   |F_gpu - F_ref| <= 1e-12 * B[m,n]
   TF32X3: |F_gpu - F_ref| <= 1e-5  * B[m,n]
 where B[m,n] = sum_k |term_k| is the oracle's per-coefficient L1 bound."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -213,6 +215,66 @@ def test_row_shards_concatenate_to_full(fcfs, prec):
     _assert_parity(full, Fr, B, prec, "full", ms, ns)
 
 
+@pytest.mark.parametrize("route", ["fft", "gemm"])
+@pytest.mark.parametrize("prec", ["fp64", "tf32x3"])
+def test_rows_to_peers_emulated_ranks(fcfs, route, prec):
+    """fcfs_coeffs_rows_to_peers: P = 3 ranks emulated on one GPU, each rank's epilogue storing its rows into
+    all three full-window buffers (the fused all_gather); every buffer equals the unsharded window bit for
+    bit (and the oracle), including an empty rank and a rank that owns the m = 0 row."""
+    wl = inputs.c2(seed=5, n_poly=300)
+    g = _gpu_extract(fcfs, wl)
+    area = int(g["area"][0].item())
+    M = N = 24
+    full = fcfs.coeffs(g["x"], g["y"], g["w"], area, wl.T, M, N, prec=prec, route=route)
+    bufs = [torch.full_like(full, complex(7.0, 7.0)) for _ in range(3)]
+    for lo, hi in [(-24, -1), (0, 24), (5, 4)]:             # the last rank owns no rows
+        sh = fcfs.Shard(fcfs.SHARD_ROWS, lo, hi, 0, 0)
+        if hi < lo:
+            continue
+        plan = fcfs.CoeffsPlan(g["K"], wl.T, M, N, prec=prec, shard=sh, route=route)
+        plan.run_to_peers(g["x"], g["y"], g["w"], area, bufs)
+    torch.cuda.synchronize()
+    ms, ns, Fr, B = _oracle_window(g, wl.T, M, N)
+    for i, b in enumerate(bufs):
+        assert torch.equal(b, full), f"peer buffer {i} != unsharded window"
+    _assert_parity(bufs[2].cpu().numpy(), Fr, B, prec, "peers", ms, ns)
+
+
+def test_rows_to_peers_two_processes(fcfs):
+    """Two processes on one GPU (gloo plumbing): each maps the other's full window by CUDA IPC
+    (dist.peer_buffers) and its epilogue stores its rows into both (RowsPeers); both windows equal the
+    unsharded window bit for bit.  (No kernel waits on another: the ordering is a host barrier.)"""
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_peers_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), "2", str(port)]) for r in range(2)]
+    codes = [p.wait(timeout=300) for p in procs]
+    assert codes == [0, 0]
+
+
+def test_rows_to_peers_rejects_bad_arguments(fcfs):
+    import ctypes
+    wl = inputs.c1(seed=2)
+    g = _gpu_extract(fcfs, wl)
+    area = int(g["area"][0].item())
+    buf = torch.zeros(fcfs.window_size(8, 8), dtype=torch.complex128, device="cuda")
+    sh = fcfs.Shard(fcfs.SHARD_ROWS, -8, 8, 0, 0)
+    plan = fcfs.CoeffsPlan(g["K"], wl.T, 8, 8, shard=sh)
+    for peers in ([], [buf] * 9, [0]):
+        with pytest.raises(fcfs.FcfsError) as ei:
+            plan.run_to_peers(g["x"], g["y"], g["w"], area, peers)
+        assert ei.value.status == fcfs.E_INVALID
+    vb = fcfs.CoeffsPlan(g["K"], wl.T, 8, 8, shard=fcfs.Shard(fcfs.SHARD_VERTEX_BLOCK, 0, 0, 0, 4))
+    with pytest.raises(fcfs.FcfsError) as ei:
+        vb.run_to_peers(g["x"], g["y"], g["w"], area, [buf])
+    assert ei.value.status == fcfs.E_INVALID
+
+
 @pytest.mark.parametrize("prec", ["fp64", "tf32x3", "f16x3"])
 def test_vertex_blocks_sum_to_full(fcfs, prec):
     wl = inputs.c2(seed=4, n_poly=600)
@@ -340,6 +402,7 @@ def test_nccl_sharded_paths_world1(fcfs):
         bx = fdist.BandExtract(w4.R, w4.T, 0, 1)
         rs = fdist.RowsSharded(w4.T, 16, 16, "fp64", 0, 1)
         vs = fdist.VertexSharded(w4.T, 16, 16, "fp64", 0, 1)
+        rp = fdist.RowsPeers(w4.T, 16, 16, "fp64", 0, 1)
         for _ in range(2):
             x, y, w, K, area = fdist.extract_band_sharded(rects, w4.T, extractor=bx)
             assert K == e["K"] and area == int(e["area"][0])
@@ -352,7 +415,10 @@ def test_nccl_sharded_paths_world1(fcfs):
             Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], w4.T, ms, ns)
             _assert_parity(Frow.cpu().numpy(), Fr, B, "fp64", "nccl rows", ms, ns)
             _assert_parity(Fvb.cpu().numpy(), Fr, B, "fp64", "nccl vblock", ms, ns)
-        assert len(rs.plans) == 1 and len(vs.plans) == 1
+            Fp = rp.run(x, y, w, K, area)                   # rows stored by the epilogue (peer = itself)
+            torch.cuda.synchronize()
+            assert torch.equal(Fp, Frow)
+        assert len(rs.plans) == 1 and len(vs.plans) == 1 and len(rp.plans) == 1
     finally:
         dist.destroy_process_group()
 
