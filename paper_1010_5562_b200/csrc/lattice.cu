@@ -61,13 +61,10 @@ constexpr int kMaxChunks = 209;             // chunks per clip: (T + 1) / 12 rou
 constexpr int kStageCols = 4 * kYC;         // TMEM columns per A stage: cos (hi, lo) x 12 rows | sin (hi, lo) x 12
 // TMEM columns: D_c [0,64), D_s [64,128), A stage s at 128 + 48 s: cos (hi, lo) x 12 rows | sin (hi, lo) x 12.
 // The epilogue's FP32 block sums S live in an L2-resident global scratch ([CTA][clip q][col / 4][lane]
-// float4: 64 KB per CTA), which frees TMEM for six A stages (two per producer warp).
+// float4: 64 KB per CTA), which frees TMEM for the eight A stages (two per producer warp).
 constexpr uint32_t kColA = 128;
-// named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s free (MMA -> producers);
-// 10 + s: stage s full (producers -> MMA)
 // named barriers: 2 + d: D block d finished (MMA -> epilogue); 4 + s: stage s full (producers -> MMA).
-// Stage s free (MMA completion -> producers) is the commit's mbarrier alone: with two stages per warp the
-// producers rarely wait for it.
+// Stage s free (MMA completion -> producers) is the commit's mbarrier alone (a sleeping poll).
 constexpr int kBarD = 2, kBarFull = 4;
 static_assert(kBarFull + kAS <= 16, "named barriers");
 constexpr int kFullCount = 32 * kClips + 64;   // stage full: one producer warp per clip + both MMA warps
@@ -181,8 +178,8 @@ __device__ __forceinline__ uint32_t bf16_bits(float v) {   // exact for the smal
     return __float_as_uint(v) >> 16;
 }
 
-// accumulation blocks (identical in the MMA and epilogue warps): D_c blocks start at chunks j % 16 == 0,
-// D_s blocks at j % 16 == 8 (and j == 0), so the two flushes never coincide inside an item
+// accumulation blocks (identical in the MMA and epilogue warps): D_c blocks start at chunks j % kFlush == 0,
+// D_s blocks at j % kFlush == kFlush / 2 (and j == 0), so the two flushes never coincide inside an item
 __host__ __device__ inline bool c_start(int j) { return j % kFlush == 0; }
 __host__ __device__ inline bool s_start(int j) { return j == 0 || j % kFlush == kFlush / 2; }
 __host__ __device__ inline bool c_end(int j, int nch) { return j % kFlush == kFlush - 1 || j == nch - 1; }
