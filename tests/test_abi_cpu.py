@@ -115,3 +115,24 @@ def test_options_are_validated_and_route_forcing_is_explicit(fcfs):
     c = fcfs.make_options(form="corner")
     assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 1, ctypes.byref(c)) == fcfs.FORM_CORNER
     assert form(4096, 1 << 24, 5000, 2048, ctypes.byref(wp), 2, None) == fcfs.FORM_CORNER
+
+
+def _build_c_demo(fcfs, out):
+    """gcc, plain C: include/fcfs.h is a C header and libfcfs.so is usable without Python."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    lib_dir = os.path.dirname(fcfs.LIB_PATH)
+    cuda = "/usr/local/cuda"
+    subprocess.check_call([gcc, "-O2", "-Wall", "-Werror", "-std=c11", os.path.join(ROOT, "examples", "fcfs_c_demo.c"),
+                           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+                           "-L", lib_dir, "-lfcfs", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+                           f"-Wl,-rpath,{lib_dir}:{os.path.join(cuda, 'lib64')}", "-o", out])
+    return out
+
+
+def test_c_demo_compiles_and_links(fcfs, tmp_path):
+    exe = _build_c_demo(fcfs, str(tmp_path / "fcfs_c_demo"))
+    assert os.path.exists(exe)

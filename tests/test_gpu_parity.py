@@ -1614,3 +1614,28 @@ def test_small_clip_random_sweep(fcfs, seed):
     ms, ns = oracle.window(M, N, r2)
     Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], T, ms, ns)
     _assert_parity(plan.out.cpu().numpy(), Fr, B, "fp64", f"small sweep seed {seed}", ms, ns)
+
+
+def test_c_demo_program_matches_oracle(fcfs, tmp_path):
+    """The C-ABI driven from a plain C program (examples/fcfs_c_demo.c: cudaMalloc, fcfs_vertices_from_rects,
+    fcfs_coeffs, no Python in the process): its FP64 window of a c1 clip equals the oracle within 1e-12 B
+    and its K / area bit for bit."""
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_abi_cpu import _build_c_demo
+    exe = _build_c_demo(fcfs, str(tmp_path / "fcfs_c_demo"))
+    wl = inputs.c1(seed=11)
+    M = 16
+    rects_bin, out_bin = tmp_path / "rects.bin", tmp_path / "out.bin"
+    wl.rects.astype(np.int32).tofile(rects_bin)
+    subprocess.check_call([exe, str(rects_bin), str(wl.R), str(wl.T), str(M), str(out_bin)], timeout=120)
+    raw = np.fromfile(out_bin, dtype=np.uint8)
+    nout = (2 * M + 1) ** 2
+    F = raw[:nout * 16].view(np.complex128)
+    K, area = raw[nout * 16:].view(np.int64)
+    e = oracle.extract(wl.rects, wl.T, wl.group_ptr)
+    assert K == e["K"] and area == int(e["area"][0])
+    ms, ns = oracle.window(M, M)
+    Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
+    _assert_parity(F, Fr, B, "fp64", "C demo", ms, ns)
