@@ -341,6 +341,18 @@ fcfs_status fcfs_vertices_from_rects_async(const int32_t *rects, int64_t R, cons
                                            int64_t cap, int64_t *corner_ptr, int64_t *area,
                                            int64_t *K_dev, int32_t *status_dev, void *ws,
                                            size_t ws_bytes, void *stream);
+/* fcfs_vertices_from_clips_async — a1 of B clips of singleton groups (group_ptr NULL: every rect its own
+ *   group, clip_ptr required) with no host synchronisation, on the per-clip shared-memory bucket path of
+ *   fcfs_vertices_from_rects (bit-exact, the same canonical output): the caller bounds the rects per clip,
+ *   max_clip_rects <= 2048 (T <= 65534), which selects the kernel variant up front instead of a read-back.
+ *   K_dev / status_dev as fcfs_vertices_from_rects_async (FCFS_E_UNSUPPORTED in status_dev if a clip holds
+ *   more than the launched variant's capacity).  Workspace: fcfs_vertices_workspace_bytes(R, R, B, 1).
+ *   With fcfs_coeffs_batched on the lattice-row form (opt.sorted_y = 1: no host sync either; K_total and
+ *   K_max then serve only planning, so upper bounds are valid) a whole batched step is capturable. */
+fcfs_status fcfs_vertices_from_clips_async(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B,
+                                           int32_t T, int64_t max_clip_rects, int32_t *x, int32_t *y, int32_t *w,
+                                           int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_dev,
+                                           int32_t *status_dev, void *ws, size_t ws_bytes, void *stream);
 fcfs_status fcfs_coeffs_async(const int32_t *x, const int32_t *y, const int32_t *w,
                               const int64_t *K_dev, int64_t K_cap, const int64_t *area_dev, int32_t T,
                               const fcfs_window *win, fcfs_precision prec, void *F, int32_t *status_dev,

@@ -954,6 +954,17 @@ size_t extract_clip_workspace_bytes(int64_t R, int64_t B) {
     return cv.used();
 }
 
+// outcome of the sync-free per-clip path: K = corner_ptr[B]; the err bits of the per-clip kernels
+// (1 a bad rect, 8 a clip above the launched variant's capacity) become an fcfs_status word
+__global__ void k_clips_status(const int64_t *corner_ptr, int64_t B, const int32_t *err, int64_t cap, int64_t *K_dev,
+                               int32_t *status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t k = corner_ptr[B];
+    const int32_t e = *err;
+    *K_dev = k;
+    *status = (e & 8) ? FCFS_E_UNSUPPORTED : (e & 1) ? FCFS_E_RANGE : (k > cap ? FCFS_E_CAPACITY : FCFS_OK);
+}
+
 static fcfs_status clips_result(int64_t Kh, int32_t errh, int64_t cap, int64_t *K_host) {
     if (errh & 8) {
         set_error("a clip has more than %d rects", kClipRects);
@@ -972,6 +983,55 @@ static fcfs_status clips_result(int64_t Kh, int32_t errh, int64_t cap, int64_t *
 }
 
 // returns FCFS_E_UNSUPPORTED (after a sync) if a clip exceeds kClipRects: the caller falls back
+// The per-clip bucket path with no host synchronisation (batched clips of singleton groups): the caller
+// bounds the rects per clip (max_clip_rects <= kClipRects), which picks the variant up front instead of
+// a read-back of the overflow bit; K and the outcome stay on the device (K_dev, status_dev).
+fcfs_status extract_clips_async(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B, int32_t T,
+                                int64_t max_clip_rects, int32_t *x, int32_t *y, int32_t *w, int64_t cap,
+                                int64_t *corner_ptr, int64_t *area, int64_t *K_dev, int32_t *status_dev, void *ws,
+                                size_t ws_bytes, cudaStream_t s) {
+    if (max_clip_rects < 0 || max_clip_rects > kClipRects || T > 65534) {
+        set_error("fcfs_vertices_from_clips_async: max_clip_rects=%lld (<= %d) or T=%d (<= 65534) unsupported",
+                  (long long)max_clip_rects, kClipRects, T);
+        return FCFS_E_UNSUPPORTED;
+    }
+    Carver cv(ws, ws_bytes);
+    ClipWs W;
+    carve_clip(cv, R, B, W);
+    if (!cv.fits()) {
+        set_error("fcfs_vertices_from_clips_async: workspace %zu < %zu bytes", ws_bytes, cv.used());
+        return FCFS_E_WORKSPACE;
+    }
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.err, 0, 4 * sizeof(int32_t), s));
+    FCFS_TRY_CUDA(cudaMemsetAsync(W.status, 0, B * sizeof(unsigned long long), s));
+    const int64_t grid = B;
+    if (T <= kBucketMaxT) {
+        if (max_clip_rects <= kSmallRects) {
+            FCFS_TRY(ensure_smem((const void *)k_clip_corners_bucket<448, 3>,
+                                 4 * kSmallRects * 12 + (kBucketMaxT + 2) * 4, true));
+            const size_t bsmem = 4 * kSmallRects * 12 + (size_t)(T + 2) * 4;
+            k_clip_corners_bucket<448, 3><<<(unsigned)grid, 448, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T, x,
+                                                                            y, w, cap, corner_ptr, W.status, area,
+                                                                            W.err);
+        } else {
+            FCFS_TRY(ensure_smem((const void *)k_clip_corners_bucket<512, 4>, kBucketCap * 12 + (kBucketMaxT + 2) * 4,
+                                 true));
+            const size_t bsmem = kBucketCap * 12 + (size_t)(T + 2) * 4;
+            k_clip_corners_bucket<512, 4><<<(unsigned)grid, 512, bsmem, s>>>((const int4 *)rects, clip_ptr, B, R, T, x,
+                                                                            y, w, cap, corner_ptr, W.status, area,
+                                                                            W.err);
+        }
+        FCFS_CHECK_LAUNCH("k_clip_corners_bucket");
+    } else {
+        k_clip_corners<<<(unsigned)grid, kClipThreads, 0, s>>>((const int4 *)rects, clip_ptr, B, R, T, x, y, w, cap,
+                                                               corner_ptr, W.status, area, W.err);
+        FCFS_CHECK_LAUNCH("k_clip_corners");
+    }
+    k_clips_status<<<1, 32, 0, s>>>(corner_ptr, B, W.err, cap, K_dev, status_dev);
+    FCFS_CHECK_LAUNCH("k_clips_status");
+    return FCFS_OK;
+}
+
 fcfs_status extract_clips(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B, int32_t T,
                           int32_t *x, int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
                           int64_t *K_host, void *ws, size_t ws_bytes, cudaStream_t s) {

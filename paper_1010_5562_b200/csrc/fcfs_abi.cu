@@ -74,6 +74,10 @@ void profile_mark(int stage, int begin, cudaStream_t s) {
 
 // extract.cu
 size_t extract_workspace_bytes(int64_t R, int64_t G, int64_t B, int64_t max_group, bool singleton);
+fcfs_status extract_clips_async(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B, int32_t T,
+                                int64_t max_clip_rects, int32_t *x, int32_t *y, int32_t *w, int64_t cap,
+                                int64_t *corner_ptr, int64_t *area, int64_t *K_dev, int32_t *status_dev, void *ws,
+                                size_t ws_bytes, cudaStream_t s);
 fcfs_status extract(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,
                     const int64_t *clip_ptr, int64_t B, int32_t T, int64_t max_group, int32_t *x,
                     int32_t *y, int32_t *w, int64_t cap, int64_t *corner_ptr, int64_t *area,
@@ -479,6 +483,24 @@ fcfs_status fcfs_vertices_from_rects_async(const int32_t *rects, int64_t R, cons
     if (!K_dev || !status_dev) { set_error("fcfs_vertices_from_rects_async: K_dev / status_dev NULL"); return FCFS_E_INVALID; }
     return vertices_impl(rects, R, group_ptr, G, clip_ptr, B, T, max_group, x, y, w, cap, corner_ptr, area, nullptr, ws,
                          ws_bytes, stream, nullptr, 0, 0x7fffffff, K_dev, status_dev);
+}
+
+fcfs_status fcfs_vertices_from_clips_async(const int32_t *rects, int64_t R, const int64_t *clip_ptr, int64_t B,
+                                           int32_t T, int64_t max_clip_rects, int32_t *x, int32_t *y, int32_t *w,
+                                           int64_t cap, int64_t *corner_ptr, int64_t *area, int64_t *K_dev,
+                                           int32_t *status_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!valid_T(T)) { set_error("T=%d outside [1, 2^20]", T); return FCFS_E_INVALID; }
+    if (R < 0 || B < 1 || B >= (int64_t(1) << 22) || !clip_ptr || (R > 0 && (!rects || ((uintptr_t)rects & 15u))) ||
+        !corner_ptr || !area || !K_dev || !status_dev || (cap > 0 && (!x || !y || !w))) {
+        set_error("fcfs_vertices_from_clips_async: invalid sizes or null pointers");
+        return FCFS_E_INVALID;
+    }
+    if (ws == nullptr || ((uintptr_t)ws & 255)) { set_error("ws NULL or not 256-byte aligned"); return FCFS_E_WORKSPACE; }
+    fcfs_status st = device_ok();
+    if (st != FCFS_OK) return st;
+    StageScope scope(kStageExtract, (cudaStream_t)stream);
+    return extract_clips_async(rects, R, clip_ptr, B, T, max_clip_rects, x, y, w, cap, corner_ptr, area, K_dev,
+                               status_dev, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 fcfs_status fcfs_vertices_from_rects_band(const int32_t *rects, int64_t R, const int64_t *group_ptr, int64_t G,

@@ -129,6 +129,9 @@ _lib.fcfs_vertices_from_rects_async.argtypes = [_P, _i64, _P, _i64, _P, _i64, _i
                                                 _P, _P, _sz, _P]
 _lib.fcfs_vertices_from_rects_async.restype = _i32
 _lib.fcfs_coeffs_async.argtypes = [_P, _P, _P, _P, _i64, _P, _i32, _WP, _i32, _P, _P, _P, _sz, _P]
+_lib.fcfs_vertices_from_clips_async.argtypes = [_P, _i64, _P, _i64, _i32, _i64, _P, _P, _P, _i64, _P, _P, _P, _P, _P,
+                                                _sz, _P]
+_lib.fcfs_vertices_from_clips_async.restype = _i32
 _lib.fcfs_coeffs_async.restype = _i32
 _lib.fcfs_small_clip_supported.argtypes = [_i64, _i64, _i32, _i64, _WP]
 _lib.fcfs_small_clip_supported.restype = _i32
@@ -151,7 +154,7 @@ EXPORTED = ["fcfs_vertices_workspace_bytes", "fcfs_vertices_from_rects", "fcfs_c
             "fcfs_haar_workspace_bytes", "fcfs_haar", "fcfs_edges", "fcfs_vertices_from_rects_edges",
             "fcfs_coeffs_batched_edges", "fcfs_coeffs_batched_form", "fcfs_vertices_from_rects_band",
             "fcfs_small_clip_supported", "fcfs_small_clip", "fcfs_vertices_from_rects_async",
-            "fcfs_coeffs_async", "fcfs_coeffs_rows_to_peers"]
+            "fcfs_coeffs_async", "fcfs_coeffs_rows_to_peers", "fcfs_vertices_from_clips_async"]
 STAGES = ("extract", "contract", "epilogue", "pairing")
 
 
@@ -411,6 +414,27 @@ class VerticesPlan:
                 self.ws.numel(), _stream(stream))
         _check(st, "fcfs_vertices_from_rects")
         self.K = K.value
+        return self.K
+
+    def run_clips_async(self, rects, clip_ptr, max_clip_rects, stream=None):
+        """B clips of singleton groups with no host synchronisation (fcfs_vertices_from_clips_async): K and the
+        outcome stay on the device (self.K_dev, self.status; ``check_async()`` reads them after the stream's
+        work), so the call can be captured in a CUDA graph."""
+        if not hasattr(self, "K_dev"):
+            self.K_dev = torch.zeros(1, dtype=torch.int64, device=self.x.device)
+            self.status = torch.zeros(1, dtype=torch.int32, device=self.x.device)
+        st = _lib.fcfs_vertices_from_clips_async(_ptr(rects), self.R, _ptr(clip_ptr), self.B, self.T,
+                                                 int(max_clip_rects), _ptr(self.x), _ptr(self.y), _ptr(self.w),
+                                                 self.cap, _ptr(self.corner_ptr), _ptr(self.area), _ptr(self.K_dev),
+                                                 _ptr(self.status), _ptr(self.ws), self.ws.numel(), _stream(stream))
+        _check(st, "fcfs_vertices_from_clips_async")
+
+    def check_async(self):
+        """The device-side outcome of run_clips_async (raises on an error status); returns K."""
+        st = int(self.status.item())
+        if st != FCFS_OK:
+            raise FcfsError(st, "fcfs_vertices_from_clips_async (device status)")
+        self.K = int(self.K_dev.item())
         return self.K
 
     def run_band(self, rects, y_lo, y_hi, group_ptr=None, stream=None):

@@ -1639,3 +1639,64 @@ def test_c_demo_program_matches_oracle(fcfs, tmp_path):
     ms, ns = oracle.window(M, M)
     Fr, B = oracle.coeffs(e["x"], e["y"], e["w"], e["area"][0], wl.T, ms, ns)
     _assert_parity(F, Fr, B, "fp64", "C demo", ms, ns)
+
+
+def test_clips_async_extraction_and_graph_replay(fcfs):
+    """fcfs_vertices_from_clips_async: bit-exact with the synchronising per-clip path; captured with the
+    lattice-form batched coefficients in a CUDA graph and replayed on NEW rects (the graph reads the rects
+    buffer); device status for a clip above max_clip_rects and for a bad rect."""
+    wl = inputs.c3(seed=21, clips=24)
+    rects = _dev(wl.rects, torch.int32)
+    cp = _dev(wl.clip_ptr, torch.int64)
+    vp = fcfs.VerticesPlan(wl.R, wl.T, None, wl.B, 1, grouped=False)
+    vp.run_clips_async(rects, cp, 1200)
+    torch.cuda.synchronize()
+    K = vp.check_async()
+    e = oracle.extract(wl.rects, wl.T, None, wl.clip_ptr)
+    g = {"K": K, "x": vp.x[:K], "y": vp.y[:K], "w": vp.w[:K], "corner_ptr": vp.corner_ptr, "area": vp.area}
+    _assert_extract_equal(g, e)
+    kmax = int(np.diff(e["corner_ptr"]).max())
+    plan = fcfs.BatchedPlan(wl.B, 4 * wl.R, 4 * 1200, wl.T, wl.M, wl.N, wl.r2, "pupil", "tf32x3", form="lattice",
+                            sorted_y=True)   # upper bounds for K_total / K_max: planning only on this form
+    assert plan.form == 3 and kmax <= 4 * 1200
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        vp.run_clips_async(rects, cp, 1200, stream=s)
+        plan.run(vp.corner_ptr, vp.x, vp.y, vp.w, vp.area, stream=s)
+    w2 = inputs.c3(seed=22, clips=24)
+    for wk in (wl, w2):
+        rects.copy_(_dev(wk.rects, torch.int32))   # same shapes (1200 rects per clip), new coordinates
+        graph.replay()
+        torch.cuda.synchronize()
+        K2 = vp.check_async()
+        ek = oracle.extract(wk.rects, wk.T, None, wk.clip_ptr)
+        assert K2 == ek["K"]
+        F = plan.out.view(wk.B, -1).cpu().numpy()
+        ms, ns = oracle.window(wk.M, wk.N, wk.r2)
+        for b in (0, 13, 23):
+            sl = slice(ek["corner_ptr"][b], ek["corner_ptr"][b + 1])
+            Fr, B = oracle.coeffs(ek["x"][sl], ek["y"][sl], ek["w"][sl], ek["area"][b], wk.T, ms, ns)
+            _assert_parity(F[b], Fr, B, "tf32x3", f"graph clip {b}", ms, ns)
+    # clips above the capacity the bound selects (1400 rects, bound 1200 -> the 1344-rect variant): device
+    # status E_UNSUPPORTED; a bad rect: E_RANGE
+    wb = inputs.c3(seed=23, clips=4, n_lines=1400)
+    vb = fcfs.VerticesPlan(wb.R, wb.T, None, wb.B, 1, grouped=False)
+    vb.run_clips_async(_dev(wb.rects, torch.int32), _dev(wb.clip_ptr, torch.int64), 1200)
+    torch.cuda.synchronize()
+    with pytest.raises(fcfs.FcfsError) as ei:
+        vb.check_async()
+    assert ei.value.status == fcfs.E_UNSUPPORTED
+    vb.run_clips_async(_dev(wb.rects, torch.int32), _dev(wb.clip_ptr, torch.int64), 1400)   # the 2048 variant
+    torch.cuda.synchronize()
+    Kb = vb.check_async()
+    eb = oracle.extract(wb.rects, wb.T, None, wb.clip_ptr)
+    _assert_extract_equal({"K": Kb, "x": vb.x[:Kb], "y": vb.y[:Kb], "w": vb.w[:Kb], "corner_ptr": vb.corner_ptr,
+                           "area": vb.area}, eb)
+    bad = wl.rects.copy()
+    bad[5] = [10, 10, 10, 20]
+    vp.run_clips_async(_dev(bad, torch.int32), cp, 1200)
+    torch.cuda.synchronize()
+    with pytest.raises(fcfs.FcfsError) as ei:
+        vp.check_async()
+    assert ei.value.status == fcfs.E_RANGE
