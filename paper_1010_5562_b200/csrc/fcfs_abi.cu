@@ -113,7 +113,7 @@ bool tf32_can_fuse(const GemmPlan &plan, const EpiArgs &ea);
 bool lattice_eligible(int32_t T, const EpiArgs &ea);
 size_t lattice_ws_bytes(int64_t B, int32_t T);
 fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int64_t K, int32_t T,
-                                   int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s);
+                                   int32_t M, int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s);
 fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *x, const int32_t *y, const int32_t *w,
                            int32_t T, const EpiArgs &ea, void *F, void *ws, cudaStream_t s);
 
@@ -857,7 +857,7 @@ static fcfs_status batched_impl(const int64_t *corner_ptr, int64_t B, int64_t K_
         // stream sync) and an unsorted batch takes the edge form instead
         StageScope scope(kStageContract, s);
         FCFS_TRY_CUDA(cudaMemsetAsync(W.flag, 0, sizeof(int32_t), s));
-        st = launch_lattice_prepare(corner_ptr, B, y, K_total, T, win->N, W.lat, W.flag, !opt->sorted_y, s);
+        st = launch_lattice_prepare(corner_ptr, B, y, K_total, T, win->M, win->N, W.lat, W.flag, !opt->sorted_y, s);
         if (st != FCFS_OK) return st;
         int32_t unsorted = 0;
         if (!opt->sorted_y) {

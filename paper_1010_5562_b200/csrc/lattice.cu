@@ -192,6 +192,7 @@ struct Args {
     const int32_t *x, *y, *w;
     const int32_t *cptr;        // [B][nch + 1] chunk starts (relative to the clip's first corner)
     const uint8_t *btab;        // [nch][B' 8 KB | B'' 8 KB]
+    const float2 *qtab;         // the quarter-wave table, built once per call (k_lat_qtab)
     int32_t T, M, N, nch;
     int64_t items;
     EpiArgs ea;
@@ -237,15 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lattice(Args A) {
         // x = c_q T/2 + s_q u, see the decode)
         const int rows = T / 4 + 2, lanes = M + 1;
         float2 *tab = (float2 *)(smem + L.table);
-        for (int i = tid; i < rows * lanes + 32; i += kThreads) {
-            const int u = i / lanes, l = i % lanes;
-            double sn = 0.0, cs = 0.0;
-            if (u <= T / 4) {
-                if (l < M) sincospi(2.0 * (double)(((int64_t)(l + 1) * u) % T) / (double)T, &sn, &cs);
-                else { cs = 0.5 * (double)T; sn = (double)u; }
-            }
-            tab[i] = make_float2((float)cs, (float)sn);
-        }
+        for (int i = tid; i < rows * lanes + 32; i += kThreads) tab[i] = __ldg(A.qtab + i);   // from L2
         const double pi = 3.141592653589793238462643383279502884;
         for (int a = tid; a < kMaxRows; a += kThreads) {
             f_rows[a] = a ? -1.0 / (4.0 * pi * pi * (double)a) : 0.0;
@@ -652,6 +645,22 @@ __global__ void k_lat_btab(int32_t T, int32_t N, int32_t nch, uint8_t *__restric
     }
 }
 
+// the quarter-wave table of k_lattice, once per call (every CTA copies it from L2 instead of evaluating
+// (T/4 + 2)(M + 1) FP64 sincospi): row u, lane l < M: (cos, sin)(2 pi (l+1) u / T); lane M: (T/2, u) (the
+// x-weighted axis row); rows past T/4: 0
+__global__ void k_lat_qtab(int32_t T, int32_t M, float2 *__restrict__ qtab) {
+    const int rows = T / 4 + 2, lanes = M + 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * lanes + 32; i += gridDim.x * blockDim.x) {
+        const int u = i / lanes, l = i % lanes;
+        double sn = 0.0, cs = 0.0;
+        if (u <= T / 4) {
+            if (l < M) sincospi(2.0 * (double)(((int64_t)(l + 1) * u) % T) / (double)T, &sn, &cs);
+            else { cs = 0.5 * (double)T; sn = (double)u; }
+        }
+        qtab[i] = make_float2((float)cs, (float)sn);
+    }
+}
+
 // chunk starts of every clip: cptr[b][j] = first corner (relative to the clip's start) with y >= 16 j,
 // j = 0 .. nch (cptr[b][nch] = the clip's corner count): one thread per (clip, j), a binary search over the
 // clip's y-sorted corners (latency hidden by the thread count)
@@ -715,17 +724,22 @@ static int lattice_grid(int64_t B) {
 static size_t cptr_bytes(int64_t B, int32_t T) { return ((size_t)B * (lattice_chunks(T) + 1) * 4 + 255) & ~(size_t)255; }
 static constexpr size_t kSBytesPerCta = (size_t)lat::kClips * 32 * 32 * sizeof(float4);   // 64 KB
 
+static size_t qtab_bytes(int32_t T) { return ((size_t)(T / 4 + 2) * (lat::kMaxRows / 2) * 8 + 32 * 8 + 255) & ~(size_t)255; }
+
 size_t lattice_ws_bytes(int64_t B, int32_t T) {
-    return btab_bytes(T) + cptr_bytes(B, T) + (size_t)lattice_grid(B) * kSBytesPerCta + 256;
+    return btab_bytes(T) + cptr_bytes(B, T) + (size_t)lattice_grid(B) * kSBytesPerCta + qtab_bytes(T) + 256;
 }
 
 fcfs_status launch_lattice_prepare(const int64_t *corner_ptr, int64_t B, const int32_t *y, int64_t K, int32_t T,
-                                   int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s) {
+                                   int32_t M, int32_t N, void *ws, int32_t *unsorted_dev, bool check, cudaStream_t s) {
     const int32_t nch = lattice_chunks(T);
     uint8_t *btab = (uint8_t *)ws;
     int32_t *cptr = (int32_t *)(btab + btab_bytes(T));
     lat::k_lat_btab<<<148, 256, 0, s>>>(T, N, nch, btab);
     FCFS_CHECK_LAUNCH("k_lat_btab");
+    float2 *qtab = (float2 *)(btab + btab_bytes(T) + cptr_bytes(B, T) + (size_t)lattice_grid(B) * kSBytesPerCta);
+    lat::k_lat_qtab<<<148, 256, 0, s>>>(T, M, qtab);
+    FCFS_CHECK_LAUNCH("k_lat_qtab");
     const int64_t threads = B * (int64_t)(nch + 1);
     const int64_t blocks = (threads + 255) / 256;
     lat::k_lat_cptr<<<(unsigned)(blocks < 65536 ? blocks : 65536), 256, 0, s>>>(corner_ptr, B, y, nch, cptr);
@@ -748,6 +762,8 @@ fcfs_status launch_lattice(const int64_t *corner_ptr, int64_t B, const int32_t *
     a.btab = (const uint8_t *)ws;
     a.cptr = (const int32_t *)((const uint8_t *)ws + btab_bytes(T));
     a.S = (float4 *)((uint8_t *)ws + btab_bytes(T) + cptr_bytes(B, T));
+    a.qtab = (const float2 *)((const uint8_t *)ws + btab_bytes(T) + cptr_bytes(B, T) +
+                              (size_t)lattice_grid(B) * kSBytesPerCta);
     a.T = T; a.M = ea.M; a.N = ea.N; a.nch = nch;
     a.items = (B + lat::kClips - 1) / lat::kClips;
     a.ea = ea;
